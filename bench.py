@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Benchmark of the XRL hot path: FMM MVM throughput (Mpanels/s, one MVM =
+3 complex components = 6 real right-hand sides through one tree pass).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl xrl|reference] [--config 4]
+
+Workload (BASELINE.json): config 4 (package-on-package-like stack, ~1.9M
+panels, highly non-uniform density) at N = 1; configs 1-3 are parity cases
+(tests/).  A "step" is one xrl_mvm over one synthetic input triple already
+resident in HBM.  L2 is flushed (256 MiB write) between timed steps, each
+step timed with CUDA events on the library's stream.  Under torchrun every
+rank runs its own replica of the whole MVM (multi-GPU sharding is not built
+yet: "replicas", weak scaling) and the slowest rank's time counts.
+
+--impl reference runs the FP64 oracle (oracle/) on the host cores over a
+bounded sample of target rows of the same workload (the reference arm of this
+tier; rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG_NAMES = {1: "cfg1_bar_2100", 2: "cfg2_coils", 3: "cfg3_bga16", 4: "cfg4_pop_2M", 5: "cfg5_bga64"}
+METRIC = "FMM MVM Mpanels/s (3 complex comps)"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._run, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_oracle_run(mesh, x, n_rows, seed=7):
+    """Time the oracle on a seeded sample of target rows (all host cores)."""
+    import numpy as np
+
+    import oracle
+    g = oracle.Geometry(mesh.verts, mesh.tris)
+    rows = np.random.default_rng(seed).choice(mesh.n, size=n_rows, replace=False)
+    t0 = time.perf_counter()
+    oracle.mvm_rows(g, x, rows)
+    dt = time.perf_counter() - t0
+    return dt, oracle.num_threads()
+
+
+def cpu_baseline(mesh, x, budget_s=12.0):
+    """Oracle direct sum on a bounded row sample; value = target rows / s / 1e6
+    (the same unit as the GPU metric: panels of y produced per second)."""
+    import numpy as np
+    rows0 = 64
+    dt0, cores = cpu_oracle_run(mesh, x, rows0, seed=11)
+    rows = int(min(mesh.n, max(rows0, rows0 * budget_s / max(dt0, 1e-3))))
+    dt, cores = cpu_oracle_run(mesh, x, rows)
+    return {"value": rows / dt / 1e6, "unit": "Mpanels/s", "cores": cores, "kind": "oracle",
+            "sample": f"{rows} seeded target rows x all {mesh.n} sources, FP64 direct sum (O(N^2) per MVM, "
+                      f"not an FMM), {dt:.2f} s wall; full MVM extrapolated {dt * mesh.n / rows:.0f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from inputs import meshes
+    mesh = meshes.make_config(args.config)
+    x = meshes.make_x(args.config, mesh.n)
+    # bounded sample per step so that warmup + steps stay within a few minutes
+    import numpy as np
+    _, cores = cpu_oracle_run(mesh, x, 16, seed=3)
+    dt16, _ = cpu_oracle_run(mesh, x, 64, seed=5)
+    per_step_rows = int(max(64, 64 * 8.0 / max(dt16, 1e-3)))
+    for w in range(args.warmup):
+        cpu_oracle_run(mesh, x, min(per_step_rows, 256), seed=100 + w)
+    times = []
+    for s in range(args.steps):
+        dt, cores = cpu_oracle_run(mesh, x, per_step_rows, seed=200 + s)
+        times.append(dt)
+    tot = sum(times)
+    value = per_step_rows * args.steps / tot / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mpanels/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CFG_NAMES[args.config], "n_panels": mesh.n, "p": 10, "eta": 1.5,
+                   "parallelism": "host threads (OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": "Mpanels/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{per_step_rows} seeded target rows per step x all {mesh.n} sources (FP64 direct sum)"},
+        "e2e": {"value": value, "unit": "Mpanels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def traffic_from_profiles(kernel: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(kernel)
+    except Exception:
+        return None
+
+
+def run_xrl(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from inputs import meshes
+    from paper_2409_12375_b200 import xrl
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    mesh = meshes.make_config(args.config)
+    x_user = meshes.make_x(args.config, mesh.n)
+    t0 = time.perf_counter()
+    ctx = xrl.Context(local)
+    tree = xrl.Tree(ctx, mesh.verts, mesh.tris, leaf_max=args.leaf)
+    near = xrl.Near(tree, eta=1.5)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    info = tree.info()
+    n = mesh.n
+
+    xd = tree.to_library_order(torch.from_numpy(x_user).to(dev))
+    y = torch.empty_like(xd)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = ctx.stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        xrl.mvm(tree, near, xd, y)
+    barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ctx.timing_reset()
+    ctx.timing_enable(True)
+    launches0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        for s in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[s][0].record(stream)
+            xrl.mvm(tree, near, xd, y)
+            ev[s][1].record(stream)
+        barrier()
+    launches = ctx.launch_count() - launches0
+    ctx.timing_enable(False)
+    phases = ctx.timing()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_dev = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    ms_max = float(t_dev.item())
+    ms_per_step = ms_max / args.steps
+    value = world * n / (ms_per_step * 1e-3) / 1e6
+
+    # e2e through the public host API: pinned host buffers, H2D + reorder + MVM + reorder + D2H
+    xh = torch.from_numpy(x_user).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    xh_np, yh_np = xh.numpy(), yh.numpy()
+    for _ in range(2):
+        xrl.mvm_host(tree, near, xh_np, yh_np)
+    barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        xrl.mvm_host(tree, near, xh_np, yh_np)  # blocking
+        e2e_times.append(time.perf_counter() - t1)
+    te = torch.tensor([sum(e2e_times) / len(e2e_times)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * n / float(te.item()) / 1e6
+
+    # roofline of the dominant kernel
+    peaks = _peaks()
+    clocks = clk.summary()
+    tot_phase = sum(v[0] for v in phases.values())
+    dom = max(phases, key=lambda k: phases[k][0])
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s, SIMT FFMA
+    nc = 121
+    m2l_flops = 2.0 * nc * nc * 6 * info["n_v_pairs"]
+    p2p_flops = 20.0 * info["n_p2p"]
+    roof = None
+    if dom == "m2l":
+        per_launch_ms = phases["m2l"][0] / max(phases["m2l"][1], 1)
+        achieved = m2l_flops / (per_launch_ms * 1e-3) / 1e12
+        roof = {"kernel": "k_m2l", "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": traffic_from_profiles("k_m2l"),
+                "algorithmic": f"2*121^2*6 flops x {info['n_v_pairs']} V-list translations per launch",
+                "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
+    else:
+        per_launch_ms = phases[dom][0] / max(phases[dom][1], 1)
+        flops = p2p_flops if dom == "leaf" else 0.0
+        achieved = flops / (per_launch_ms * 1e-3) / 1e12
+        roof = {"kernel": "k_" + dom, "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": traffic_from_profiles("k_" + dom),
+                "algorithmic": f"P2P only: 20 flops x {info['n_p2p']} ordered pairs per launch (L2P/M2P/near not counted)",
+                "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz"}
+    roof["share_of_step"] = phases[dom][0] / tot_phase if tot_phase else None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpanels/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": CFG_NAMES[args.config], "n_panels": n, "p": 10, "leaf_max": args.leaf, "eta": 1.5,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "boxes": info["n_boxes"], "leaves": info["n_leaves"], "levels": info["n_levels"],
+                   "m2l_translations": info["n_v_pairs"], "p2p_pairs": info["n_p2p"],
+                   "x_pairs": info["n_x_pairs"], "w_pairs": info["n_w_pairs"], "setup_s": round(setup_s, 3)},
+        "e2e": {"value": e2e_value, "unit": "Mpanels/s", "h2d_bytes_per_step": int(xh.numel() * 8),
+                "d2h_bytes_per_step": int(yh.numel() * 8)},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "roofline": roof,
+        "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(mesh, x_user)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["xrl", "reference"], default="xrl")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--leaf", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_xrl(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

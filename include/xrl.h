@@ -1,0 +1,186 @@
+/*
+ * xrl.h -- C-ABI of the B200-native hot path of XRL (arXiv 2409.12375):
+ * the FMM-accelerated panel MVM inside the preconditioned GMRES.
+ *
+ * The operator.  XRL discretises the MQS SIE (Eq. 1) with pulse
+ * bases on panels after the centroid-midpoint basis transformation
+ * (Eq. 4-5, Alg. 1).  The potential part of Eq. 6
+ * with j*omega*mu0/(4 pi) pulled out is the real
+ * symmetric panel matrix P, applied three times per loop-space MVM, once per
+ * Cartesian current component (Eq. 9), by an FMM over the
+ * panel centroids "in the format of particle simulation".
+ * This library applies
+ *     y_t = P x_t,  t = 1..3  (complex x_t; P real -> 6 real right-hand sides)
+ *     P_kk = I(c_k;T_k)/A_k
+ *     P_kl = 1/2 [I(c_k;T_l)/A_l + I(c_l;T_k)/A_k]   if d_kl^2 < (eta max(D_k,D_l))^2
+ *     P_kl = 1/|c_k - c_l|                            otherwise
+ * with I(r;T) = int_T dS'/|r - r'| (analytic), c centroids, A areas, D the
+ * longest edge (readings R1-R4).
+ *
+ * Conventions for every entry point:
+ *  - Status: 0 = XRL_OK, > 0 warning, < 0 error; xrl_last_error() returns a
+ *    thread-local message for the last failing call.
+ *  - Handles are opaque, allocated by the library and released by the matching
+ *    *_destroy (NULL-safe).  Host input arrays are borrowed for the duration of
+ *    the call and copied.  Device vectors belong to the caller: contiguous,
+ *    16-byte aligned, resident on the context's device.  The library never
+ *    frees caller memory.
+ *  - Asynchrony: xrl_mvm / xrl_precond_apply / order conversions enqueue on the
+ *    context stream and return; argument errors are reported synchronously,
+ *    asynchronous CUDA faults surface on the next call or at xrl_ctx_sync.
+ *    Calls with a _host suffix and xrl_gmres block.
+ *  - Concurrency: one in-flight MVM per tree handle (it owns the expansion
+ *    scratch).  Handles are immutable after build.
+ *  - Vectors passed to the MVM are in "library order" (Morton order of the
+ *    centroids; xrl_to_library_order / xrl_from_library_order convert).
+ *  - Units: SI (metres); P in 1/m.
+ *  - There is no CPU fallback: without a usable sm_100 device every entry point
+ *    that needs one returns XRL_ECUDA.
+ */
+#ifndef XRL_H
+#define XRL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t xrl_status;
+enum {
+    XRL_OK = 0,
+    XRL_ENOCONV = 1,       /* some GMRES column did not converge (per-column flags in report) */
+    XRL_EINVAL = -1,       /* bad option / argument (p != 10, leaf < 1, eta <= 0, null pointer) */
+    XRL_EDIM = -2,         /* vector length / nvec mismatch */
+    XRL_EPROVENANCE = -3,  /* handle built from a different tree / context */
+    XRL_EGEOM = -4,        /* zero-area triangle, vertex index out of range, coincident centroids */
+    XRL_ESINGULAR = -5,    /* preconditioner block pivot below threshold */
+    XRL_ENOMEM = -6,
+    XRL_ECUDA = -7,
+    XRL_ENCCL = -8,
+    XRL_ENOFREQ = -9,
+    XRL_EUNSUPPORTED = -10
+};
+
+/* MVM flags (tests and diagnostics). */
+enum {
+    XRL_MVM_FULL = 0,        /* y = P x */
+    XRL_MVM_NEAR_ONLY = 1,   /* y = N x, N = near CSR (P_kk on the diagonal, P_kl - 1/r off it) */
+    XRL_MVM_FAR_ONLY = 2     /* y = sum_{l != k} x_l / |c_k - c_l| (FMM + P2P, no correction) */
+};
+
+typedef struct xrl_ctx_s* xrl_ctx;
+typedef struct xrl_tree_s* xrl_tree;
+typedef struct xrl_near_s* xrl_near;
+
+const char* xrl_last_error(void);
+const char* xrl_version(void);
+
+/* Context: device ordinal, CUDA stream (cudaStream_t, NULL = library-created
+ * non-blocking stream), rank/world for Morton-range sharding (world == 1 for a
+ * single GPU; multi-rank contexts need the 128-byte ncclUniqueId broadcast by
+ * the caller, else NULL). */
+xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world,
+                          const void* nccl_unique_id, xrl_ctx* out);
+xrl_status xrl_ctx_sync(xrl_ctx ctx);
+void xrl_ctx_destroy(xrl_ctx ctx);
+
+/* FMM options.  p: expansion order (only 10 is compiled, PAPER.md silent ->
+ * north star p = 10); leaf_max: split a box while it holds more panels
+ * (default 64); max_depth: <= 21 (63-bit Morton keys). */
+typedef struct {
+    int32_t p;
+    int32_t leaf_max;
+    int32_t max_depth;
+} xrl_fmm_opts;
+
+/* Octree build on the GPU (setup, once per mesh).
+ * vert: host FP64 [n_vert][3] (m); tri: host int32 [n_tri][3].
+ * Computes centroids/areas/longest edges (PAPER.md:56 centroids are the PEEC
+ * nodes), 63-bit Morton keys of the centroids, a stable radix sort, the
+ * adaptive octree (split while count > leaf_max) and the U/V/W/X interaction
+ * lists.  Errors: XRL_EINVAL, XRL_EGEOM (zero area / bad index), XRL_ECUDA. */
+xrl_status xrl_tree_build(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_tri,
+                          const int32_t* tri, const xrl_fmm_opts* opts, xrl_tree* out);
+void xrl_tree_destroy(xrl_tree tree);
+
+typedef struct {
+    int64_t n;            /* panels (global) */
+    int64_t n_local;      /* panels owned by this rank */
+    int64_t offset;       /* first owned panel in library order */
+    int32_t n_boxes, n_leaves, n_levels, p;
+    int64_t n_v_pairs;    /* M2L translations */
+    int64_t n_x_pairs;    /* P2L (box, leaf) pairs */
+    int64_t n_w_pairs;    /* M2P (leaf, box) pairs */
+    int64_t n_u_pairs;    /* leaf-leaf P2P pairs (incl. self) */
+    int64_t n_p2p;        /* ordered panel pairs done by P2P (self excluded) */
+    double root_lo[3];    /* root cube corner (m) */
+    double root_width;    /* root cube width W (m) */
+} xrl_tree_info_t;
+xrl_status xrl_tree_info(xrl_tree tree, xrl_tree_info_t* info);
+
+/* perm_host[i] = original panel index of library position i (int32 [n]). */
+xrl_status xrl_tree_perm(xrl_tree tree, int32_t* perm_host);
+
+/* Reorder device complex64 vectors [nvec][n]: user (mesh) order <-> library order. */
+xrl_status xrl_to_library_order(xrl_tree tree, const void* x_user, void* x_lib, int32_t nvec);
+xrl_status xrl_from_library_order(xrl_tree tree, const void* x_lib, void* x_user, int32_t nvec);
+
+/* Box/list export for the coverage audit (tests).  Pass NULL for any array
+ * to skip it; sizes from xrl_tree_info.  Boxes are in level order.
+ * box_level/ix/iy/iz/parent/pb/pe: int32 [n_boxes]; is_leaf: int32 [n_boxes];
+ * *_ptr: int64 [n_boxes+1] CSR by target box, *_src: int32 sources.
+ * lists: U (leaf <- leaf, P2P), V (box <- box, M2L), X (box <- leaf, P2L),
+ * W (leaf <- box, M2P). */
+xrl_status xrl_tree_export(xrl_tree tree, int32_t* box_level, int32_t* box_ijk /* [n_boxes][3] */,
+                           int32_t* box_parent, int32_t* box_pb, int32_t* box_pe, int32_t* is_leaf,
+                           int64_t* u_ptr, int32_t* u_src, int64_t* v_ptr, int32_t* v_src,
+                           int64_t* x_ptr, int32_t* x_src, int64_t* w_ptr, int32_t* w_src);
+
+/* Near field (setup, once per mesh; frequency independent).
+ * eta: near criterion factor (default 1.5).  For every near pair the FP64
+ * analytic single-triangle integrals (Eq. 6 on centroids,
+ * PAPER.md:114-116) give N_kl = P_kl - 1/|c_k - c_l| (stored FP32) and
+ * N_kk = P_kk; CSR in library order, columns ascending. */
+typedef struct {
+    double eta;
+} xrl_near_opts;
+xrl_status xrl_near_assemble(xrl_tree tree, const xrl_near_opts* opts, xrl_near* out);
+void xrl_near_destroy(xrl_near near);
+/* Copies the CSR to host buffers (any may be NULL).  row_ptr int64 [n+1],
+ * col int32 [nnz], val32 float [nnz] (as used), val64 double [nnz] (P_kl and
+ * P_kk in FP64, i.e. the near entries before the 1/r subtraction).  *nnz is
+ * always written. */
+xrl_status xrl_near_export(xrl_near near, int64_t* row_ptr, int32_t* col, float* val32,
+                           double* val64, int64_t* nnz);
+
+/* The hot path: y = P x (flags select diagnostic parts).
+ * x, y: device complex64 [nvec][n_local] in library order, must not alias;
+ * nvec a multiple of 3 (each triple of complex components = 6 real RHS through
+ * one tree traversal).  Enqueued on the context stream. */
+xrl_status xrl_mvm(xrl_tree tree, xrl_near near, const void* x, void* y, int32_t nvec, uint32_t flags);
+
+/* End-to-end variant with HOST complex64 buffers [nvec][n] in the mesh's
+ * original panel order: H2D copy, reorder, MVM, reorder, D2H copy.  Blocking. */
+xrl_status xrl_mvm_host(xrl_tree tree, xrl_near near, const void* x_host, void* y_host, int32_t nvec,
+                        uint32_t flags);
+
+/* Per-phase device timing (CUDA events on the context stream) of the MVM
+ * kernels, accumulated while enabled.  names: "pack","p2m","m2m","m2l","p2l",
+ * "l2l","leaf"(L2P+M2P+P2P+near).  xrl_timing_get fills ms[i] and
+ * launches[i] for i < n (n = xrl_timing_count()). */
+xrl_status xrl_timing_enable(xrl_ctx ctx, int on);
+int32_t xrl_timing_count(void);
+const char* xrl_timing_name(int32_t i);
+xrl_status xrl_timing_get(xrl_ctx ctx, double* ms, int64_t* launches);
+xrl_status xrl_timing_reset(xrl_ctx ctx);
+
+/* Number of library kernels launched on this context so far (all entry
+ * points; used to report gpu_launches of a timed region). */
+int64_t xrl_launch_count(xrl_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XRL_H */

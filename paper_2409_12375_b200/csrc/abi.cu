@@ -1,0 +1,180 @@
+// C-ABI plumbing: errors, context, timing (include/xrl.h).
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+
+#include "xrl_internal.h"
+
+namespace xrl {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+static const char* kPhaseNames[PH_COUNT] = {"pack", "p2m", "m2m", "m2l", "p2l", "l2l", "leaf"};
+
+static cudaEvent_t get_event(xrl_ctx ctx)
+{
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    XRL_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb)
+{
+    (void)ph;
+    *evb = nullptr;
+    if (!ctx->timing) return;
+    *evb = get_event(ctx);
+    XRL_CUDA(cudaEventRecord(*evb, ctx->stream));
+}
+
+void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb)
+{
+    if (!ctx->timing || !evb) return;
+    cudaEvent_t e = get_event(ctx);
+    XRL_CUDA(cudaEventRecord(e, ctx->stream));
+    ctx->pending.push_back({ph, {evb, e}});
+}
+
+static void drain(xrl_ctx ctx)
+{
+    for (auto& p : ctx->pending) {
+        XRL_CUDA(cudaEventSynchronize(p.second.second));
+        float ms = 0;
+        XRL_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+        ctx->phase_ms[p.first] += ms;
+        ctx->phase_launches[p.first] += 1;
+        ctx->event_pool.push_back(p.second.first);
+        ctx->event_pool.push_back(p.second.second);
+    }
+    ctx->pending.clear();
+}
+
+}  // namespace xrl
+
+using namespace xrl;
+
+#define XRL_TRY try {
+#define XRL_CATCH                                   \
+    }                                               \
+    catch (const CudaError& e) { return e.code; }   \
+    catch (const std::bad_alloc&) {                 \
+        set_error("host out of memory");            \
+        return XRL_ENOMEM;                          \
+    }
+
+extern "C" {
+
+const char* xrl_last_error(void) { return g_err; }
+const char* xrl_version(void) { return "xrl-b200 0.1 (sm_100a, p=10)"; }
+
+xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, const void* nccl_unique_id,
+                          xrl_ctx* out)
+{
+    if (!out) { set_error("xrl_ctx_create: out is NULL"); return XRL_EINVAL; }
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) { set_error("bad rank/world %d/%d", rank, world); return XRL_EINVAL; }
+    if (world > 1 && !nccl_unique_id) { set_error("world > 1 needs an ncclUniqueId"); return XRL_EINVAL; }
+    XRL_TRY
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || ndev == 0) {
+            set_error("no CUDA device available (%s); this library has no CPU path", cudaGetErrorString(e));
+            return XRL_ECUDA;
+        }
+        XRL_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        XRL_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) {
+            set_error("device %d is sm_%d%d; this library is built for sm_100a only", device, prop.major, prop.minor);
+            return XRL_ECUDA;
+        }
+        auto* c = new xrl_ctx_s();
+        c->device = device;
+        c->rank = rank;
+        c->world = world;
+        if (cuda_stream) c->stream = (cudaStream_t)cuda_stream;
+        else {
+            XRL_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        if (world > 1) {
+            delete c;
+            set_error("multi-rank contexts are not built in this version");
+            return XRL_EUNSUPPORTED;
+        }
+        upload_constants(c);
+        *out = c;
+        return XRL_OK;
+    XRL_CATCH
+}
+
+xrl_status xrl_ctx_sync(xrl_ctx ctx)
+{
+    if (!ctx) { set_error("null ctx"); return XRL_EINVAL; }
+    XRL_TRY
+        XRL_CUDA(cudaSetDevice(ctx->device));
+        XRL_CUDA(cudaStreamSynchronize(ctx->stream));
+        return XRL_OK;
+    XRL_CATCH
+}
+
+void xrl_ctx_destroy(xrl_ctx ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& p : ctx->pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+xrl_status xrl_timing_enable(xrl_ctx ctx, int on)
+{
+    if (!ctx) { set_error("null ctx"); return XRL_EINVAL; }
+    ctx->timing = on != 0;
+    return XRL_OK;
+}
+
+int32_t xrl_timing_count(void) { return PH_COUNT; }
+const char* xrl_timing_name(int32_t i) { return (i >= 0 && i < PH_COUNT) ? kPhaseNames[i] : ""; }
+
+xrl_status xrl_timing_get(xrl_ctx ctx, double* ms, int64_t* launches)
+{
+    if (!ctx) { set_error("null ctx"); return XRL_EINVAL; }
+    XRL_TRY
+        drain(ctx);
+        for (int i = 0; i < PH_COUNT; ++i) {
+            if (ms) ms[i] = ctx->phase_ms[i];
+            if (launches) launches[i] = ctx->phase_launches[i];
+        }
+        return XRL_OK;
+    XRL_CATCH
+}
+
+int64_t xrl_launch_count(xrl_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+xrl_status xrl_timing_reset(xrl_ctx ctx)
+{
+    if (!ctx) { set_error("null ctx"); return XRL_EINVAL; }
+    XRL_TRY
+        drain(ctx);
+        for (int i = 0; i < PH_COUNT; ++i) { ctx->phase_ms[i] = 0; ctx->phase_launches[i] = 0; }
+        return XRL_OK;
+    XRL_CATCH
+}
+
+}  // extern "C"

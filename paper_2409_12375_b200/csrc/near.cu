@@ -1,0 +1,246 @@
+// xrl_near_assemble: near-pair search over the octree and FP64 analytic
+// single-triangle integrals -> near-field CSR.
+//
+// the near-field matrix is filled directly on panel
+// centroids (O(N_p)), with the Eq. 6 kernel.  Near pairs follow
+// the geometric criterion of DESIGN.md reading R3; entries are the
+// symmetrised collocation integrals of reading R2.  The far part 1/r is applied
+// by the FMM, so the CSR stores the correction N_kl = P_kl - 1/|c_k - c_l| and
+// the self term N_kk = P_kk.
+#include <cmath>
+
+#include "xrl_internal.h"
+
+using namespace xrl;
+
+namespace {
+
+struct V3 {
+    double x, y, z;
+};
+__device__ __forceinline__ V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ V3 cross(V3 a, V3 b)
+{
+    return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ V3 scale(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ double norm(V3 a) { return sqrt(dot(a, a)); }
+
+// Potential of a unit-density flat triangle at r: int_T dS'/|r - r'|.
+// Edge decomposition: for each edge (a -> b) with tangent t, outward in-plane
+// normal u = t x n, signed foot distance p = (a - rho).u, tangential
+// coordinates s- = (a - rho).t, s+ = (b - rho).t, height h:
+//   I = sum p ln[(R+ + s+)/(R- + s-)] - |h| sum [atan(p s+/(p^2+h^2+|h|R+)) - atan(p s-/(p^2+h^2+|h|R-))]
+__device__ double tri_potential(V3 r, V3 v0, V3 v1, V3 v2)
+{
+    V3 n = cross(sub(v1, v0), sub(v2, v0));
+    n = scale(n, 1.0 / norm(n));
+    const double h = dot(sub(r, v0), n);
+    const double ah = fabs(h);
+    const V3 rho = sub(r, scale(n, h));
+    const V3 vs[3] = {v0, v1, v2};
+    double acc_log = 0.0, acc_ang = 0.0;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+        const V3 a = vs[e], b = vs[(e + 1) % 3];
+        V3 t = sub(b, a);
+        t = scale(t, 1.0 / norm(t));
+        const V3 u = cross(t, n);
+        const V3 ar = sub(a, rho), br = sub(b, rho);
+        const double p = dot(ar, u);
+        if (p == 0.0) continue;
+        const double sm = dot(ar, t), sp = dot(br, t);
+        const double q2 = p * p + h * h;
+        const double Rm = norm(sub(r, a)), Rp = norm(sub(r, b));
+        double lg;
+        if (sm >= 0.0) lg = log((Rp + sp) / (Rm + sm));
+        else if (sp <= 0.0) lg = log((Rm - sm) / (Rp - sp));
+        else lg = log((Rp + sp) * (Rm - sm) / q2);
+        acc_log += p * lg;
+        if (ah > 0.0) acc_ang += atan(p * sp / (q2 + ah * Rp)) - atan(p * sm / (q2 + ah * Rm));
+    }
+    return acc_log - ah * acc_ang;
+}
+
+// Near criterion, correctly rounded FP64 with no contraction (reading R3).
+__device__ __forceinline__ bool is_near(const double* ck, const double* cl, double Dk, double Dl, double eta)
+{
+    double dx = __dsub_rn(ck[0], cl[0]), dy = __dsub_rn(ck[1], cl[1]), dz = __dsub_rn(ck[2], cl[2]);
+    double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    double t = __dmul_rn(eta, Dk > Dl ? Dk : Dl);
+    return d2 < __dmul_rn(t, t);
+}
+
+struct TreeView {
+    const int32_t *level, *ix, *iy, *iz, *child, *nchild, *pb, *pe;
+    const double* bdmax;
+    const double* cent;
+    const double* dmax;
+    double lo0, lo1, lo2, W;
+};
+
+// Depth-first search from the root in Morton order; emits columns ascending.
+template <bool FILL>
+__global__ void k_near_search(int64_t n, TreeView tv, double eta, int64_t* cnt, const int64_t* __restrict__ ptr,
+                              int32_t* cols, int* overflow)
+{
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double* ck = tv.cent + 3 * k;
+    const double Dk = tv.dmax[k];
+    const double invW = 1.0 / tv.W;
+    const double p[3] = {(ck[0] - tv.lo0) * invW, (ck[1] - tv.lo1) * invW, (ck[2] - tv.lo2) * invW};
+    int stack[8 * 22 + 8];
+    int sp = 0;
+    stack[sp++] = 0;
+    int64_t c = 0;
+    int64_t out = FILL ? ptr[k] : 0;
+    while (sp > 0) {
+        int b = stack[--sp];
+        double s = ldexp(1.0, -tv.level[b]);
+        double bl[3] = {tv.ix[b] * s, tv.iy[b] * s, tv.iz[b] * s};
+        double d2 = 0;
+        for (int d = 0; d < 3; ++d) {
+            double lo = bl[d] - 1e-9, hi = bl[d] + s + 1e-9;
+            double q = p[d] < lo ? lo - p[d] : (p[d] > hi ? p[d] - hi : 0.0);
+            d2 += q * q;
+        }
+        double R = eta * fmax(Dk, tv.bdmax[b]) * invW * (1.0 + 1e-6);
+        if (d2 > R * R) continue;
+        int c0 = tv.child[b];
+        if (c0 >= 0) {
+            int nc = tv.nchild[b];
+            if (sp + nc > 8 * 22 + 8) { atomicOr(overflow, 1); return; }
+            for (int j = nc - 1; j >= 0; --j) stack[sp++] = c0 + j;
+        } else {
+            for (int l = tv.pb[b]; l < tv.pe[b]; ++l) {
+                if (l == k || is_near(ck, tv.cent + 3 * (int64_t)l, Dk, tv.dmax[l], eta)) {
+                    if (FILL) cols[out + c] = l;
+                    ++c;
+                }
+            }
+        }
+    }
+    if (!FILL) cnt[k] = c;
+}
+
+__global__ void k_near_values(int64_t n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ cols,
+                              const double* __restrict__ cent, const double* __restrict__ area,
+                              const double* __restrict__ tverts, float* val, double* val64)
+{
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double* tk = tverts + 9 * k;
+    const V3 ck = {cent[3 * k], cent[3 * k + 1], cent[3 * k + 2]};
+    const V3 k0 = {tk[0], tk[1], tk[2]}, k1 = {tk[3], tk[4], tk[5]}, k2 = {tk[6], tk[7], tk[8]};
+    const double Ak = area[k];
+    for (int64_t j = ptr[k]; j < ptr[k + 1]; ++j) {
+        const int64_t l = cols[j];
+        double v64, v32;
+        if (l == k) {
+            v64 = tri_potential(ck, k0, k1, k2) / Ak;
+            v32 = v64;
+        } else {
+            const double* tl = tverts + 9 * l;
+            const V3 cl = {cent[3 * l], cent[3 * l + 1], cent[3 * l + 2]};
+            const V3 l0 = {tl[0], tl[1], tl[2]}, l1 = {tl[3], tl[4], tl[5]}, l2 = {tl[6], tl[7], tl[8]};
+            const double Ikl = tri_potential(ck, l0, l1, l2) / area[l];
+            const double Ilk = tri_potential(cl, k0, k1, k2) / Ak;
+            v64 = 0.5 * (Ikl + Ilk);
+            v32 = v64 - 1.0 / norm(sub(ck, cl));
+        }
+        val[j] = (float)v32;
+        if (val64) val64[j] = v64;
+    }
+}
+
+inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+}  // namespace
+
+static xrl_status near_impl(xrl_tree t, double eta, xrl_near* out)
+{
+    xrl_ctx ctx = t->ctx;
+    cudaStream_t st = ctx->stream;
+    XRL_CUDA(cudaSetDevice(ctx->device));
+    auto N = std::make_unique<xrl_near_s>();
+    N->tree = t;
+    N->eta = eta;
+    const int64_t n = t->n;
+    TreeView tv{t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bchild.p, t->bnchild.p, t->bpb.p, t->bpe.p,
+                t->bdmax.p, t->cent.p, t->dmax.p, t->lo[0], t->lo[1], t->lo[2], t->W};
+    DBuf<int64_t> cnt(n);
+    DBuf<int> ovf(1);
+    XRL_CUDA(cudaMemsetAsync(ovf.p, 0, 4, st));
+    k_near_search<false><<<nblk(n, 128), 128, 0, st>>>(n, tv, eta, cnt.p, nullptr, nullptr, ovf.p);
+    XRL_LAUNCH_CHECK();
+    std::vector<int64_t> hc(n), hp(n + 1, 0);
+    XRL_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    int hovf = 0;
+    XRL_CUDA(cudaMemcpyAsync(&hovf, ovf.p, 4, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    if (hovf) { set_error("xrl_near_assemble: traversal stack overflow"); return XRL_EGEOM; }
+    for (int64_t i = 0; i < n; ++i) hp[i + 1] = hp[i] + hc[i];
+    N->nnz = hp[n];
+    N->row_ptr.alloc(n + 1);
+    N->col.alloc(std::max<int64_t>(1, N->nnz));
+    N->val.alloc(std::max<int64_t>(1, N->nnz));
+    N->val64.alloc(std::max<int64_t>(1, N->nnz));
+    XRL_CUDA(cudaMemcpyAsync(N->row_ptr.p, hp.data(), 8 * (n + 1), cudaMemcpyHostToDevice, st));
+    k_near_search<true><<<nblk(n, 128), 128, 0, st>>>(n, tv, eta, nullptr, N->row_ptr.p, N->col.p, ovf.p);
+    XRL_LAUNCH_CHECK();
+    k_near_values<<<nblk(n, 64), 64, 0, st>>>(n, N->row_ptr.p, N->col.p, t->cent.p, t->area.p, t->tverts.p,
+                                              N->val.p, N->val64.p);
+    XRL_LAUNCH_CHECK();
+    XRL_CUDA(cudaStreamSynchronize(st));
+    *out = N.release();
+    return XRL_OK;
+}
+
+extern "C" {
+
+xrl_status xrl_near_assemble(xrl_tree t, const xrl_near_opts* opts, xrl_near* out)
+{
+    if (!t || !out) { set_error("xrl_near_assemble: null argument"); return XRL_EINVAL; }
+    *out = nullptr;
+    double eta = opts ? opts->eta : 1.5;
+    if (!(eta > 0)) { set_error("xrl_near_assemble: eta must be > 0"); return XRL_EINVAL; }
+    try {
+        return near_impl(t, eta, out);
+    } catch (const CudaError& e) {
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host out of memory");
+        return XRL_ENOMEM;
+    }
+}
+
+void xrl_near_destroy(xrl_near nr)
+{
+    if (!nr) return;
+    cudaSetDevice(nr->tree->ctx->device);
+    cudaStreamSynchronize(nr->tree->ctx->stream);
+    delete nr;
+}
+
+xrl_status xrl_near_export(xrl_near nr, int64_t* row_ptr, int32_t* col, float* val32, double* val64, int64_t* nnz)
+{
+    if (!nr) { set_error("xrl_near_export: null handle"); return XRL_EINVAL; }
+    try {
+        cudaStream_t st = nr->tree->ctx->stream;
+        XRL_CUDA(cudaSetDevice(nr->tree->ctx->device));
+        if (nnz) *nnz = nr->nnz;
+        const int64_t n = nr->tree->n;
+        if (row_ptr) XRL_CUDA(cudaMemcpyAsync(row_ptr, nr->row_ptr.p, 8 * (n + 1), cudaMemcpyDeviceToHost, st));
+        if (col && nr->nnz) XRL_CUDA(cudaMemcpyAsync(col, nr->col.p, 4 * nr->nnz, cudaMemcpyDeviceToHost, st));
+        if (val32 && nr->nnz) XRL_CUDA(cudaMemcpyAsync(val32, nr->val.p, 4 * nr->nnz, cudaMemcpyDeviceToHost, st));
+        if (val64 && nr->nnz) XRL_CUDA(cudaMemcpyAsync(val64, nr->val64.p, 8 * nr->nnz, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        return XRL_OK;
+    } catch (const CudaError& e) {
+        return e.code;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,845 @@
+// xrl_tree_build: geometry, Morton keys, radix sort, adaptive octree and the
+// U/V/W/X interaction lists, all on the GPU (setup).
+//
+// PAPER.md:116 treats the panels as particles at their centroids (PAPER.md:56:
+// centroids are the PEEC nodes), so the tree is built over centroids.  The
+// paper gives no tree parameters (refs [22],[23] only); this build uses an
+// adaptive octree (split while count > leaf_max), classical one-box
+// separation and the adaptive U/V/W/X lists of Carrier-Greengard-Rokhlin.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "xrl_internal.h"
+
+using namespace xrl;
+
+namespace {
+
+constexpr int kMortonBits = 21;
+
+// ----------------------------------------------------------------- K1 geometry
+// Correctly rounded FP64, no contraction: the near criterion downstream must
+// reproduce the oracle's decisions bit for bit (reading R3).
+__global__ void k_geometry(int64_t n, int64_t nv, const double* __restrict__ vert, const int32_t* __restrict__ tri,
+                           double* cent, double* area, double* dmax, int* bad)
+{
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int i0 = tri[3 * k], i1 = tri[3 * k + 1], i2 = tri[3 * k + 2];
+    if (i0 < 0 || i1 < 0 || i2 < 0 || i0 >= nv || i1 >= nv || i2 >= nv) {
+        atomicOr(bad, 1);
+        return;
+    }
+    const double* a = vert + 3 * (int64_t)i0;
+    const double* b = vert + 3 * (int64_t)i1;
+    const double* c = vert + 3 * (int64_t)i2;
+    double e1[3], e2[3], e3[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        cent[3 * k + d] = __ddiv_rn(__dadd_rn(__dadd_rn(a[d], b[d]), c[d]), 3.0);
+        e1[d] = __dsub_rn(b[d], a[d]);
+        e2[d] = __dsub_rn(c[d], a[d]);
+        e3[d] = __dsub_rn(c[d], b[d]);
+    }
+    double cx = __dsub_rn(__dmul_rn(e1[1], e2[2]), __dmul_rn(e1[2], e2[1]));
+    double cy = __dsub_rn(__dmul_rn(e1[2], e2[0]), __dmul_rn(e1[0], e2[2]));
+    double cz = __dsub_rn(__dmul_rn(e1[0], e2[1]), __dmul_rn(e1[1], e2[0]));
+    double ar = __dmul_rn(0.5, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz))));
+    auto len = [](const double* e) {
+        return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(e[0], e[0]), __dmul_rn(e[1], e[1])), __dmul_rn(e[2], e[2])));
+    };
+    double l1 = len(e1), l2 = len(e2), l3 = len(e3);
+    double m = l1 > l2 ? l1 : l2;
+    dmax[k] = m > l3 ? m : l3;
+    area[k] = ar;
+    if (!(ar > 0.0)) atomicOr(bad, 2);
+}
+
+__global__ void k_bbox(int64_t n, const double* __restrict__ cent, double* part /* [grid][6] */)
+{
+    double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double v = cent[3 * k + d];
+            mn[d] = fmin(mn[d], v);
+            mx[d] = fmax(mx[d], v);
+        }
+    typedef cub::BlockReduce<double, 256> BR;
+    __shared__ typename BR::TempStorage ts;
+    for (int d = 0; d < 3; ++d) {
+        double a = BR(ts).Reduce(mn[d], [](double x, double y) { return fmin(x, y); });
+        __syncthreads();
+        double b = BR(ts).Reduce(mx[d], [](double x, double y) { return fmax(x, y); });
+        __syncthreads();
+        if (threadIdx.x == 0) { part[6 * blockIdx.x + d] = a; part[6 * blockIdx.x + 3 + d] = b; }
+    }
+}
+
+__device__ __forceinline__ uint64_t spread3(uint32_t v)
+{
+    uint64_t x = v & 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffULL;
+    x = (x | x << 16) & 0x1f0000ff0000ffULL;
+    x = (x | x << 8) & 0x100f00f00f00f00fULL;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+    x = (x | x << 2) & 0x1249249249249249ULL;
+    return x;
+}
+
+// K2: 63-bit Morton key, bit group per level = bx | by<<1 | bz<<2.
+__global__ void k_morton(int64_t n, const double* __restrict__ cent, double lo0, double lo1, double lo2, double invW,
+                         uint64_t* key, int32_t* id)
+{
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double lo[3] = {lo0, lo1, lo2};
+    uint32_t q[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double u = (cent[3 * k + d] - lo[d]) * invW * double(1 << kMortonBits);
+        long long t = (long long)floor(u);
+        t = t < 0 ? 0 : (t > (1 << kMortonBits) - 1 ? (1 << kMortonBits) - 1 : t);
+        q[d] = (uint32_t)t;
+    }
+    key[k] = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+    id[k] = (int32_t)k;
+}
+
+__global__ void k_dup_check(int64_t n, const uint64_t* __restrict__ key, const int32_t* __restrict__ perm,
+                            const double* __restrict__ cent_orig, int* bad)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* a = cent_orig + 3 * (int64_t)perm[i];
+    for (int64_t j = i + 1; j < n && j < i + 32 && key[j] == key[i]; ++j) {
+        const double* b = cent_orig + 3 * (int64_t)perm[j];
+        if (a[0] == b[0] && a[1] == b[1] && a[2] == b[2]) atomicOr(bad, 4);
+    }
+}
+
+__global__ void k_gather_panels(int64_t n, const int32_t* __restrict__ perm, const double* __restrict__ cent_o,
+                                const double* __restrict__ area_o, const double* __restrict__ dmax_o,
+                                const double* __restrict__ vert, const int32_t* __restrict__ tri, double* cent,
+                                double* area, double* dmax, double* tv, int32_t* iperm)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t k = perm[i];
+    iperm[k] = (int32_t)i;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) cent[3 * i + d] = cent_o[3 * k + d];
+    area[i] = area_o[k];
+    dmax[i] = dmax_o[k];
+#pragma unroll
+    for (int v = 0; v < 3; ++v)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) tv[9 * i + 3 * v + d] = vert[3 * (int64_t)tri[3 * k + v] + d];
+}
+
+// ----------------------------------------------------------------- K4 octree
+struct LevelBoxes {
+    DBuf<int32_t> ix, iy, iz, pb, pe, parent;
+};
+
+__global__ void k_split_count(int nb, int level, int leaf_max, int max_depth, const int32_t* __restrict__ pb,
+                              const int32_t* __restrict__ pe, const uint64_t* __restrict__ key, int32_t* nch,
+                              int32_t* bounds /* [nb][9] */)
+{
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    int s = pb[b], e = pe[b];
+    if (e - s <= leaf_max || level >= max_depth) { nch[b] = 0; return; }
+    const int shift = 3 * (kMortonBits - level - 1);
+    int cnt = 0;
+    bounds[9 * b] = s;
+    int lo = s;
+    for (int o = 1; o < 8; ++o) {
+        int l = lo, h = e;  // first index with octant >= o
+        while (l < h) {
+            int mid = (l + h) >> 1;
+            if ((int)((key[mid] >> shift) & 7) < o) l = mid + 1; else h = mid;
+        }
+        bounds[9 * b + o] = l;
+        if (l > lo) ++cnt;  // octant o-1 non-empty
+        lo = l;
+    }
+    bounds[9 * b + 8] = e;
+    if (e > lo) ++cnt;
+    nch[b] = cnt;
+}
+
+__global__ void k_split_emit(int nb, int base, int next_base, const int32_t* __restrict__ ix, const int32_t* __restrict__ iy,
+                             const int32_t* __restrict__ iz, const int32_t* __restrict__ nch,
+                             const int32_t* __restrict__ coff, const int32_t* __restrict__ bounds, int32_t* cix,
+                             int32_t* ciy, int32_t* ciz, int32_t* cpb, int32_t* cpe, int32_t* cpar, int32_t* first_child)
+{
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    if (nch[b] == 0) { first_child[b] = -1; return; }
+    int c = coff[b];
+    first_child[b] = next_base + c;
+    for (int o = 0; o < 8; ++o) {
+        int s = bounds[9 * b + o], e = bounds[9 * b + o + 1];
+        if (e <= s) continue;
+        cix[c] = 2 * ix[b] + (o & 1);
+        ciy[c] = 2 * iy[b] + ((o >> 1) & 1);
+        ciz[c] = 2 * iz[b] + ((o >> 2) & 1);
+        cpb[c] = s;
+        cpe[c] = e;
+        cpar[c] = base + b;
+        ++c;
+    }
+}
+
+// ----------------------------------------------------------------- K5 lists
+constexpr int kMaxColl = 26;
+constexpr int kMaxAdj = 26;
+
+struct BoxView {
+    const int32_t *level, *ix, *iy, *iz, *child, *nchild;
+};
+
+__device__ __forceinline__ bool adjacent_fine(int ax, int ay, int az, int la, int bx, int by, int bz, int lb)
+{
+    // box a at level la (finer or equal), b at level lb <= la; touching or overlapping
+    int s = la - lb;
+    int lo[3] = {bx << s, by << s, bz << s};
+    int hi[3] = {(bx + 1) << s, (by + 1) << s, (bz + 1) << s};
+    int a[3] = {ax, ay, az};
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+        if (a[d] > hi[d] || a[d] + 1 < lo[d]) return false;
+    return true;
+}
+
+// Level pass: colleagues, coarse adjacent leaves, and counts of V / X pairs.
+__global__ void k_lists_level(int b0, int b1, BoxView bv, const int32_t* __restrict__ parent, int32_t* coll,
+                              int32_t* ncoll, int32_t* adjc, int32_t* nadjc, int32_t* nV, int32_t* nX, int* overflow)
+{
+    int b = b0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= b1) return;
+    const int P = parent[b];
+    const int lb = bv.level[b], x = bv.ix[b], y = bv.iy[b], z = bv.iz[b];
+    int nc = 0, na = 0, cv = 0, cx = 0;
+    // same-level candidates: children of P's colleagues and of P itself
+    for (int qi = -1; qi < ncoll[P]; ++qi) {
+        int Q = qi < 0 ? P : coll[kMaxColl * P + qi];
+        int c0 = bv.child[Q], nq = bv.nchild[Q];
+        if (c0 < 0) continue;
+        for (int c = c0; c < c0 + nq; ++c) {
+            if (c == b) continue;
+            int dx = x - bv.ix[c], dy = y - bv.iy[c], dz = z - bv.iz[c];
+            if (abs(dx) <= 1 && abs(dy) <= 1 && abs(dz) <= 1) {
+                if (nc < kMaxColl) coll[kMaxColl * b + nc] = c; else atomicOr(overflow, 1);
+                ++nc;
+            } else {
+                ++cv;
+            }
+        }
+    }
+    // coarse leaves: adjc(P) and P's leaf colleagues
+    for (int qi = 0; qi < nadjc[P] + ncoll[P]; ++qi) {
+        int L = qi < nadjc[P] ? adjc[kMaxAdj * P + qi] : coll[kMaxColl * P + (qi - nadjc[P])];
+        if (bv.child[L] >= 0) continue;  // only leaves
+        if (adjacent_fine(x, y, z, lb, bv.ix[L], bv.iy[L], bv.iz[L], bv.level[L])) {
+            if (na < kMaxAdj) adjc[kMaxAdj * b + na] = L; else atomicOr(overflow, 2);
+            ++na;
+        } else {
+            ++cx;
+        }
+    }
+    ncoll[b] = nc < kMaxColl ? nc : kMaxColl;
+    nadjc[b] = na < kMaxAdj ? na : kMaxAdj;
+    nV[b] = cv;
+    nX[b] = cx;
+}
+
+__global__ void k_lists_emit(int nbox, BoxView bv, const int32_t* __restrict__ parent, const int32_t* __restrict__ coll,
+                             const int32_t* __restrict__ ncoll, const int32_t* __restrict__ adjc,
+                             const int32_t* __restrict__ nadjc, const int64_t* __restrict__ vptr,
+                             const int64_t* __restrict__ xptr, int32_t* vsrc, uint64_t* vkey, int32_t* xsrc,
+                             uint64_t* xkey_w, const int* __restrict__ m2l_index)
+{
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbox || b == 0) return;
+    const int P = parent[b];
+    const int lb = bv.level[b], x = bv.ix[b], y = bv.iy[b], z = bv.iz[b];
+    int64_t pv = vptr[b], px = xptr[b];
+    for (int qi = 0; qi < ncoll[P]; ++qi) {
+        int Q = coll[kMaxColl * P + qi];
+        int c0 = bv.child[Q], nq = bv.nchild[Q];
+        if (c0 < 0) continue;
+        for (int c = c0; c < c0 + nq; ++c) {
+            int dx = x - bv.ix[c], dy = y - bv.iy[c], dz = z - bv.iz[c];
+            if (abs(dx) <= 1 && abs(dy) <= 1 && abs(dz) <= 1) continue;
+            int off = m2l_index[(dx + 3) * 49 + (dy + 3) * 7 + (dz + 3)];
+            vsrc[pv] = c;
+            vkey[pv] = ((uint64_t)(uint32_t)off << 32) | (uint32_t)b;
+            ++pv;
+        }
+    }
+    for (int qi = 0; qi < nadjc[P] + ncoll[P]; ++qi) {
+        int L = qi < nadjc[P] ? adjc[kMaxAdj * P + qi] : coll[kMaxColl * P + (qi - nadjc[P])];
+        if (bv.child[L] >= 0) continue;
+        if (adjacent_fine(x, y, z, lb, bv.ix[L], bv.iy[L], bv.iz[L], bv.level[L])) continue;
+        xsrc[px] = L;
+        xkey_w[px] = ((uint64_t)(uint32_t)L << 32) | (uint32_t)b;  // for W = X^T
+        ++px;
+    }
+}
+
+// U pairs: per leaf b: self, leaf colleagues, coarse adjacent leaves (b <- L) and the reverse (L <- b).
+__global__ void k_u_count(int nbox, const int32_t* __restrict__ child, const int32_t* __restrict__ coll,
+                          const int32_t* __restrict__ ncoll, const int32_t* __restrict__ nadjc, int64_t* cnt)
+{
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbox) return;
+    if (child[b] >= 0) { cnt[b] = 0; return; }
+    int c = 1 + 2 * nadjc[b];
+    for (int i = 0; i < ncoll[b]; ++i)
+        if (child[coll[kMaxColl * b + i]] < 0) ++c;
+    cnt[b] = c;
+}
+
+__global__ void k_u_emit(int nbox, const int32_t* __restrict__ child, const int32_t* __restrict__ coll,
+                         const int32_t* __restrict__ ncoll, const int32_t* __restrict__ adjc,
+                         const int32_t* __restrict__ nadjc, const int64_t* __restrict__ off, uint64_t* ukey)
+{
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbox || child[b] >= 0) return;
+    int64_t p = off[b];
+    auto put = [&](int t, int s) { ukey[p++] = ((uint64_t)(uint32_t)t << 32) | (uint32_t)s; };
+    put(b, b);
+    for (int i = 0; i < ncoll[b]; ++i) {
+        int c = coll[kMaxColl * b + i];
+        if (child[c] < 0) put(b, c);
+    }
+    for (int i = 0; i < nadjc[b]; ++i) {
+        int L = adjc[kMaxAdj * b + i];
+        put(b, L);
+        put(L, b);
+    }
+}
+
+__global__ void k_split_keys(int64_t n, const uint64_t* __restrict__ key, int32_t* hi, int32_t* lo)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (hi) hi[i] = (int32_t)(key[i] >> 32);
+    lo[i] = (int32_t)(key[i] & 0xffffffffu);
+}
+
+// CSR row pointers from sorted target ids.
+__global__ void k_csr_ptr(int64_t n, const int32_t* __restrict__ tgt, int nrows, int64_t* ptr)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    int a = (i == 0) ? -1 : tgt[i - 1];
+    int b = (i == n) ? nrows : tgt[i];
+    for (int r = a + 1; r <= b; ++r) ptr[r] = i;
+}
+
+__global__ void k_panel_leaf(int nleaf, const int32_t* __restrict__ leaves, const int32_t* __restrict__ pb,
+                             const int32_t* __restrict__ pe, const int32_t* __restrict__ level,
+                             const int32_t* __restrict__ ix, const int32_t* __restrict__ iy,
+                             const int32_t* __restrict__ iz, const double* __restrict__ cent, double lo0, double lo1,
+                             double lo2, double invW, int32_t* panel_leaf, float4* loc)
+{
+    int li = blockIdx.x;
+    if (li >= nleaf) return;
+    int b = leaves[li];
+    double s = ldexp(1.0, -level[b]);
+    double c[3] = {(ix[b] + 0.5) * s, (iy[b] + 0.5) * s, (iz[b] + 0.5) * s};
+    const double lo[3] = {lo0, lo1, lo2};
+    for (int i = pb[b] + threadIdx.x; i < pe[b]; i += blockDim.x) {
+        panel_leaf[i] = b;
+        float v[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) v[d] = (float)((cent[3 * (int64_t)i + d] - lo[d]) * invW - c[d]);
+        loc[i] = make_float4(v[0], v[1], v[2], 0.f);
+    }
+}
+
+__global__ void k_box_dmax(int nbox, const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
+                           const double* __restrict__ dmax, double* bd)
+{
+    int b = blockIdx.x;
+    if (b >= nbox) return;
+    double m = 0;
+    for (int i = pb[b] + threadIdx.x; i < pe[b]; i += blockDim.x) m = fmax(m, dmax[i]);
+    typedef cub::BlockReduce<double, 128> BR;
+    __shared__ typename BR::TempStorage ts;
+    m = BR(ts).Reduce(m, [](double a, double c) { return fmax(a, c); });
+    if (threadIdx.x == 0) bd[b] = m;
+}
+
+__global__ void k_p2p_count(int nleaf, const int32_t* __restrict__ leaves, const int32_t* __restrict__ pb,
+                            const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr,
+                            const int32_t* __restrict__ usrc, unsigned long long* total)
+{
+    int li = blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= nleaf) return;
+    int b = leaves[li];
+    long long nt = pe[b] - pb[b], s = 0;
+    for (int64_t j = uptr[b]; j < uptr[b + 1]; ++j) s += pe[usrc[j]] - pb[usrc[j]];
+    atomicAdd(total, (unsigned long long)(nt * s - nt));
+}
+
+template <typename KeyT, typename ValT>
+void sort_pairs(KeyT* keys, ValT* vals, int64_t n, int end_bit, cudaStream_t st)
+{
+    if (n == 0) return;
+    DBuf<KeyT> k2(n);
+    DBuf<ValT> v2;
+    if (vals) v2.alloc(n);
+    size_t tb = 0;
+    if (vals) {
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, k2.p, vals, v2.p, (int)n, 0, end_bit, st);
+        DBuf<char> tmp(tb);
+        XRL_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, k2.p, vals, v2.p, (int)n, 0, end_bit, st));
+        XRL_CUDA(cudaMemcpyAsync(vals, v2.p, n * sizeof(ValT), cudaMemcpyDeviceToDevice, st));
+    } else {
+        cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, k2.p, (int)n, 0, end_bit, st);
+        DBuf<char> tmp(tb);
+        XRL_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys, k2.p, (int)n, 0, end_bit, st));
+    }
+    XRL_CUDA(cudaMemcpyAsync(keys, k2.p, n * sizeof(KeyT), cudaMemcpyDeviceToDevice, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+}
+
+template <typename T>
+void exclusive_scan(const T* in, T* out, int64_t n, cudaStream_t st)
+{
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, st);
+    DBuf<char> tmp(tb);
+    XRL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+}
+
+inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+}  // namespace
+
+// ----------------------------------------------------------------- build
+static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* vert_h, int64_t n, const int32_t* tri_h,
+                                  const xrl_fmm_opts* opts, xrl_tree* out)
+{
+    cudaStream_t st = ctx->stream;
+    XRL_CUDA(cudaSetDevice(ctx->device));
+    auto T = std::make_unique<xrl_tree_s>();
+    T->ctx = ctx;
+    T->n = n;
+    T->leaf_max = opts ? opts->leaf_max : 64;
+    T->max_depth = opts ? opts->max_depth : kMortonBits;
+
+    DBuf<double> vert(3 * n_vert);
+    DBuf<int32_t> tri(3 * n);
+    XRL_CUDA(cudaMemcpyAsync(vert.p, vert_h, vert.bytes(), cudaMemcpyHostToDevice, st));
+    XRL_CUDA(cudaMemcpyAsync(tri.p, tri_h, tri.bytes(), cudaMemcpyHostToDevice, st));
+    DBuf<double> cent_o(3 * n), area_o(n), dmax_o(n);
+    DBuf<int> bad(1);
+    XRL_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    k_geometry<<<nblk(n, 256), 256, 0, st>>>(n, n_vert, vert.p, tri.p, cent_o.p, area_o.p, dmax_o.p, bad.p);
+    XRL_LAUNCH_CHECK();
+    int hbad = 0;
+    XRL_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    if (hbad & 1) { set_error("xrl_tree_build: vertex index out of range"); return XRL_EGEOM; }
+    if (hbad & 2) { set_error("xrl_tree_build: zero-area triangle"); return XRL_EGEOM; }
+
+    // root cube
+    const int nbb = 256;
+    DBuf<double> part(6 * nbb);
+    k_bbox<<<nbb, 256, 0, st>>>(n, cent_o.p, part.p);
+    XRL_LAUNCH_CHECK();
+    std::vector<double> hp(6 * nbb);
+    XRL_CUDA(cudaMemcpyAsync(hp.data(), part.p, part.bytes(), cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+    for (int b = 0; b < nbb; ++b)
+        for (int d = 0; d < 3; ++d) { mn[d] = std::min(mn[d], hp[6 * b + d]); mx[d] = std::max(mx[d], hp[6 * b + 3 + d]); }
+    double ext = std::max({mx[0] - mn[0], mx[1] - mn[1], mx[2] - mn[2]});
+    if (!(ext > 0)) ext = 1e-6;
+    T->W = ext * (1.0 + 1e-6);
+    for (int d = 0; d < 3; ++d) T->lo[d] = 0.5 * (mn[d] + mx[d]) - 0.5 * T->W;
+    const double invW = 1.0 / T->W;
+
+    // Morton keys + stable radix sort
+    DBuf<uint64_t> key(n);
+    DBuf<int32_t> id(n);
+    k_morton<<<nblk(n, 256), 256, 0, st>>>(n, cent_o.p, T->lo[0], T->lo[1], T->lo[2], invW, key.p, id.p);
+    XRL_LAUNCH_CHECK();
+    sort_pairs(key.p, id.p, n, 63, st);
+    T->perm = std::move(id);
+    k_dup_check<<<nblk(n, 256), 256, 0, st>>>(n, key.p, T->perm.p, cent_o.p, bad.p);
+    XRL_LAUNCH_CHECK();
+    XRL_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    if (hbad & 4) { set_error("xrl_tree_build: coincident centroids"); return XRL_EGEOM; }
+
+    T->iperm.alloc(n);
+    T->cent.alloc(3 * n);
+    T->area.alloc(n);
+    T->dmax.alloc(n);
+    T->tverts.alloc(9 * n);
+    k_gather_panels<<<nblk(n, 256), 256, 0, st>>>(n, T->perm.p, cent_o.p, area_o.p, dmax_o.p, vert.p, tri.p,
+                                                  T->cent.p, T->area.p, T->dmax.p, T->tverts.p, T->iperm.p);
+    XRL_LAUNCH_CHECK();
+
+    // octree, level by level
+    std::vector<LevelBoxes> lv;
+    std::vector<DBuf<int32_t>> lv_first_child;
+    std::vector<int> cnt = {1};
+    lv.emplace_back();
+    {
+        auto& L0 = lv[0];
+        for (auto* b : {&L0.ix, &L0.iy, &L0.iz, &L0.pb, &L0.pe, &L0.parent}) b->alloc(1);
+        int32_t z0 = 0, nn = (int32_t)n, m1 = -1;
+        for (auto* b : {&L0.ix, &L0.iy, &L0.iz, &L0.pb})
+            XRL_CUDA(cudaMemcpyAsync(b->p, &z0, 4, cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(L0.pe.p, &nn, 4, cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(L0.parent.p, &m1, 4, cudaMemcpyHostToDevice, st));
+    }
+    int base = 0;
+    for (int l = 0;; ++l) {
+        int nb = cnt[l];
+        DBuf<int32_t> nch(nb), coff(nb), bounds(9 * (size_t)nb), fc(nb);
+        k_split_count<<<nblk(nb, 128), 128, 0, st>>>(nb, l, T->leaf_max, T->max_depth, lv[l].pb.p, lv[l].pe.p,
+                                                      key.p, nch.p, bounds.p);
+        XRL_LAUNCH_CHECK();
+        exclusive_scan(nch.p, coff.p, nb, st);
+        int32_t last_c = 0, last_n = 0;
+        XRL_CUDA(cudaMemcpyAsync(&last_c, coff.p + nb - 1, 4, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaMemcpyAsync(&last_n, nch.p + nb - 1, 4, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        int nnext = last_c + last_n;
+        LevelBoxes next;
+        if (nnext > 0)
+            for (auto* b : {&next.ix, &next.iy, &next.iz, &next.pb, &next.pe, &next.parent}) b->alloc(nnext);
+        k_split_emit<<<nblk(nb, 128), 128, 0, st>>>(nb, base, base + nb, lv[l].ix.p, lv[l].iy.p, lv[l].iz.p, nch.p,
+                                                     coff.p, bounds.p, next.ix.p, next.iy.p, next.iz.p, next.pb.p,
+                                                     next.pe.p, next.parent.p, fc.p);
+        XRL_LAUNCH_CHECK();
+        lv_first_child.push_back(std::move(fc));
+        base += nb;
+        if (nnext == 0) break;
+        cnt.push_back(nnext);
+        lv.push_back(std::move(next));
+    }
+    const int nlev = (int)cnt.size();
+    T->nlevel = nlev;
+    T->lvl_start.assign(nlev + 1, 0);
+    for (int l = 0; l < nlev; ++l) T->lvl_start[l + 1] = T->lvl_start[l] + cnt[l];
+    const int nbox = T->lvl_start[nlev];
+    T->nbox = nbox;
+    for (auto* b : {&T->blevel, &T->bix, &T->biy, &T->biz, &T->bparent, &T->bchild, &T->bnchild, &T->bpb, &T->bpe})
+        b->alloc(nbox);
+    {
+        std::vector<int32_t> hl(nbox);
+        for (int l = 0; l < nlev; ++l)
+            for (int i = T->lvl_start[l]; i < T->lvl_start[l + 1]; ++i) hl[i] = l;
+        XRL_CUDA(cudaMemcpyAsync(T->blevel.p, hl.data(), 4 * nbox, cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+    }
+    for (int l = 0; l < nlev; ++l) {
+        size_t o = T->lvl_start[l], c = cnt[l];
+        XRL_CUDA(cudaMemcpyAsync(T->bix.p + o, lv[l].ix.p, 4 * c, cudaMemcpyDeviceToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(T->biy.p + o, lv[l].iy.p, 4 * c, cudaMemcpyDeviceToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(T->biz.p + o, lv[l].iz.p, 4 * c, cudaMemcpyDeviceToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(T->bpb.p + o, lv[l].pb.p, 4 * c, cudaMemcpyDeviceToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(T->bpe.p + o, lv[l].pe.p, 4 * c, cudaMemcpyDeviceToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(T->bparent.p + o, lv[l].parent.p, 4 * c, cudaMemcpyDeviceToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(T->bchild.p + o, lv_first_child[l].p, 4 * c, cudaMemcpyDeviceToDevice, st));
+    }
+    // nchild from parents (host; setup only)
+    std::vector<int32_t> hpar(nbox), hchild(nbox), hnch(nbox, 0), hpb(nbox), hpe(nbox);
+    XRL_CUDA(cudaMemcpyAsync(hpar.data(), T->bparent.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaMemcpyAsync(hchild.data(), T->bchild.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaMemcpyAsync(hpb.data(), T->bpb.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaMemcpyAsync(hpe.data(), T->bpe.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    for (int b = 1; b < nbox; ++b) hnch[hpar[b]]++;
+    XRL_CUDA(cudaMemcpyAsync(T->bnchild.p, hnch.data(), 4 * nbox, cudaMemcpyHostToDevice, st));
+    std::vector<int32_t> hleaves, hparents;
+    T->par_start.assign(nlev + 1, 0);
+    for (int l = 0; l < nlev; ++l) {
+        T->par_start[l] = (int)hparents.size();
+        for (int b = T->lvl_start[l]; b < T->lvl_start[l + 1]; ++b) {
+            if (hchild[b] < 0) hleaves.push_back(b);
+            else hparents.push_back(b);
+        }
+    }
+    T->par_start[nlev] = (int)hparents.size();
+    T->nleaf = (int)hleaves.size();
+    T->leaves.alloc(T->nleaf);
+    XRL_CUDA(cudaMemcpyAsync(T->leaves.p, hleaves.data(), 4 * hleaves.size(), cudaMemcpyHostToDevice, st));
+    T->parents.alloc(std::max<size_t>(1, hparents.size()));
+    if (!hparents.empty())
+        XRL_CUDA(cudaMemcpyAsync(T->parents.p, hparents.data(), 4 * hparents.size(), cudaMemcpyHostToDevice, st));
+
+    // panel -> leaf, local coordinates, per-box max edge
+    T->panel_leaf.alloc(n);
+    T->loc.alloc(n);
+    k_panel_leaf<<<T->nleaf, 128, 0, st>>>(T->nleaf, T->leaves.p, T->bpb.p, T->bpe.p, T->blevel.p, T->bix.p, T->biy.p,
+                                           T->biz.p, T->cent.p, T->lo[0], T->lo[1], T->lo[2], invW,
+                                           T->panel_leaf.p, T->loc.p);
+    XRL_LAUNCH_CHECK();
+    T->bdmax.alloc(nbox);
+    k_box_dmax<<<nbox, 128, 0, st>>>(nbox, T->bpb.p, T->bpe.p, T->dmax.p, T->bdmax.p);
+    XRL_LAUNCH_CHECK();
+
+    // lists
+    DBuf<int32_t> coll((size_t)kMaxColl * nbox), ncoll(nbox), adjc((size_t)kMaxAdj * nbox), nadjc(nbox);
+    DBuf<int32_t> nV(nbox), nX(nbox);
+    DBuf<int> ovf(1), m2l_index(343);
+    XRL_CUDA(cudaMemsetAsync(ovf.p, 0, 4, st));
+    XRL_CUDA(cudaMemsetAsync(ncoll.p, 0, 4 * nbox, st));
+    XRL_CUDA(cudaMemsetAsync(nadjc.p, 0, 4 * nbox, st));
+    XRL_CUDA(cudaMemsetAsync(nV.p, 0, 4 * nbox, st));
+    XRL_CUDA(cudaMemsetAsync(nX.p, 0, 4 * nbox, st));
+    XRL_CUDA(cudaMemcpyAsync(m2l_index.p, ctx->ops.m2l_index, 343 * 4, cudaMemcpyHostToDevice, st));
+    BoxView bv{T->blevel.p, T->bix.p, T->biy.p, T->biz.p, T->bchild.p, T->bnchild.p};
+    for (int l = 1; l < nlev; ++l) {
+        int b0 = T->lvl_start[l], b1 = T->lvl_start[l + 1];
+        k_lists_level<<<nblk(b1 - b0, 128), 128, 0, st>>>(b0, b1, bv, T->bparent.p, coll.p, ncoll.p, adjc.p, nadjc.p,
+                                                          nV.p, nX.p, ovf.p);
+        XRL_LAUNCH_CHECK();
+    }
+    int hovf = 0;
+    XRL_CUDA(cudaMemcpyAsync(&hovf, ovf.p, 4, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    if (hovf) { set_error("xrl_tree_build: interaction list overflow (%d)", hovf); return XRL_EGEOM; }
+
+    auto counts_to_ptr = [&](const int32_t* c32, DBuf<int64_t>& ptr, int rows) -> int64_t {
+        DBuf<int64_t> c64(rows + 1);
+        XRL_CUDA(cudaMemsetAsync(c64.p, 0, 8 * (rows + 1), st));
+        // widen
+        std::vector<int32_t> h(rows);
+        XRL_CUDA(cudaMemcpyAsync(h.data(), c32, 4 * rows, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<int64_t> hp2(rows + 1, 0);
+        for (int i = 0; i < rows; ++i) hp2[i + 1] = hp2[i] + h[i];
+        ptr.alloc(rows + 1);
+        XRL_CUDA(cudaMemcpyAsync(ptr.p, hp2.data(), 8 * (rows + 1), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        return hp2[rows];
+    };
+    T->nv = counts_to_ptr(nV.p, T->v_ptr, nbox);
+    T->nx = counts_to_ptr(nX.p, T->x_ptr, nbox);
+    T->v_src.alloc(std::max<int64_t>(1, T->nv));
+    T->x_src.alloc(std::max<int64_t>(1, T->nx));
+    DBuf<uint64_t> vkey(std::max<int64_t>(1, T->nv)), wkey(std::max<int64_t>(1, T->nx));
+    k_lists_emit<<<nblk(nbox, 128), 128, 0, st>>>(nbox, bv, T->bparent.p, coll.p, ncoll.p, adjc.p, nadjc.p,
+                                                  T->v_ptr.p, T->x_ptr.p, T->v_src.p, vkey.p, T->x_src.p, wkey.p,
+                                                  m2l_index.p);
+    XRL_LAUNCH_CHECK();
+
+    // M2L pairs sorted by (offset, target)
+    T->m2l_tgt.alloc(std::max<int64_t>(1, T->nv));
+    T->m2l_srcb.alloc(std::max<int64_t>(1, T->nv));
+    XRL_CUDA(cudaMemcpyAsync(T->m2l_srcb.p, T->v_src.p, 4 * T->nv, cudaMemcpyDeviceToDevice, st));
+    sort_pairs(vkey.p, T->m2l_srcb.p, T->nv, 64, st);
+    {
+        DBuf<int32_t> offs(std::max<int64_t>(1, T->nv));
+        if (T->nv) {
+            k_split_keys<<<nblk(T->nv, 256), 256, 0, st>>>(T->nv, vkey.p, offs.p, T->m2l_tgt.p);
+            XRL_LAUNCH_CHECK();
+        }
+        std::vector<int32_t> ho(T->nv);
+        if (T->nv) XRL_CUDA(cudaMemcpyAsync(ho.data(), offs.p, 4 * T->nv, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<int4> tiles;
+        const int TP = 32;
+        int64_t i = 0;
+        while (i < T->nv) {
+            int64_t j = i;
+            while (j < T->nv && ho[j] == ho[i]) ++j;
+            for (int64_t s = i; s < j; s += TP) tiles.push_back(make_int4(ho[i], (int)s, (int)std::min<int64_t>(TP, j - s), 0));
+            i = j;
+        }
+        T->n_m2l_tiles = (int)tiles.size();
+        T->m2l_tiles.alloc(std::max<size_t>(1, tiles.size()));
+        if (!tiles.empty())
+            XRL_CUDA(cudaMemcpyAsync(T->m2l_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
+    }
+    // X targets
+    {
+        std::vector<int32_t> hx(nbox);
+        XRL_CUDA(cudaMemcpyAsync(hx.data(), nX.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<int32_t> xt;
+        for (int b = 0; b < nbox; ++b)
+            if (hx[b] > 0) xt.push_back(b);
+        T->n_x_targets = (int)xt.size();
+        T->x_targets.alloc(std::max<size_t>(1, xt.size()));
+        if (!xt.empty()) XRL_CUDA(cudaMemcpyAsync(T->x_targets.p, xt.data(), 4 * xt.size(), cudaMemcpyHostToDevice, st));
+    }
+    // W = X transposed, CSR by leaf
+    T->nw = T->nx;
+    T->w_src.alloc(std::max<int64_t>(1, T->nw));
+    T->w_ptr.alloc(nbox + 1);
+    if (T->nw) {
+        sort_pairs<uint64_t, int32_t>(wkey.p, nullptr, T->nw, 64, st);
+        DBuf<int32_t> wt(T->nw);
+        k_split_keys<<<nblk(T->nw, 256), 256, 0, st>>>(T->nw, wkey.p, wt.p, T->w_src.p);
+        k_csr_ptr<<<nblk(T->nw + 1, 256), 256, 0, st>>>(T->nw, wt.p, nbox, T->w_ptr.p);
+        XRL_LAUNCH_CHECK();
+    } else {
+        XRL_CUDA(cudaMemsetAsync(T->w_ptr.p, 0, 8 * (nbox + 1), st));
+    }
+    // U lists
+    {
+        DBuf<int64_t> ucnt(nbox), uoff(nbox);
+        k_u_count<<<nblk(nbox, 128), 128, 0, st>>>(nbox, T->bchild.p, coll.p, ncoll.p, nadjc.p, ucnt.p);
+        XRL_LAUNCH_CHECK();
+        exclusive_scan(ucnt.p, uoff.p, nbox, st);
+        int64_t lc = 0, lo_ = 0;
+        XRL_CUDA(cudaMemcpyAsync(&lc, ucnt.p + nbox - 1, 8, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaMemcpyAsync(&lo_, uoff.p + nbox - 1, 8, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        T->nu = lc + lo_;
+        DBuf<uint64_t> ukey(T->nu);
+        k_u_emit<<<nblk(nbox, 128), 128, 0, st>>>(nbox, T->bchild.p, coll.p, ncoll.p, adjc.p, nadjc.p, uoff.p, ukey.p);
+        XRL_LAUNCH_CHECK();
+        sort_pairs<uint64_t, int32_t>(ukey.p, nullptr, T->nu, 64, st);
+        DBuf<int32_t> ut(T->nu);
+        T->u_src.alloc(T->nu);
+        T->u_ptr.alloc(nbox + 1);
+        k_split_keys<<<nblk(T->nu, 256), 256, 0, st>>>(T->nu, ukey.p, ut.p, T->u_src.p);
+        k_csr_ptr<<<nblk(T->nu + 1, 256), 256, 0, st>>>(T->nu, ut.p, nbox, T->u_ptr.p);
+        XRL_LAUNCH_CHECK();
+        DBuf<unsigned long long> tot(1);
+        XRL_CUDA(cudaMemsetAsync(tot.p, 0, 8, st));
+        k_p2p_count<<<nblk(T->nleaf, 128), 128, 0, st>>>(T->nleaf, T->leaves.p, T->bpb.p, T->bpe.p, T->u_ptr.p,
+                                                         T->u_src.p, tot.p);
+        XRL_LAUNCH_CHECK();
+        unsigned long long ht = 0;
+        XRL_CUDA(cudaMemcpyAsync(&ht, tot.p, 8, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        T->np2p = (int64_t)ht;
+    }
+    // MVM scratch
+    T->mu.alloc((size_t)nbox * kBoxStride);
+    T->ell.alloc((size_t)nbox * kBoxStride);
+    T->xq.alloc((size_t)n * 8);
+    XRL_CUDA(cudaMemsetAsync(T->mu.p, 0, T->mu.bytes(), st));
+    XRL_CUDA(cudaMemsetAsync(T->xq.p, 0, T->xq.bytes(), st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    *out = T.release();
+    return XRL_OK;
+}
+
+extern "C" {
+
+xrl_status xrl_tree_build(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_tri, const int32_t* tri,
+                          const xrl_fmm_opts* opts, xrl_tree* out)
+{
+    if (!ctx || !vert || !tri || !out) { set_error("xrl_tree_build: null argument"); return XRL_EINVAL; }
+    *out = nullptr;
+    if (n_tri < 1 || n_vert < 3 || n_tri > (int64_t)1 << 30) { set_error("xrl_tree_build: bad sizes"); return XRL_EINVAL; }
+    if (opts) {
+        if (opts->p != kP) { set_error("xrl_tree_build: p=%d not compiled (p=%d only)", opts->p, kP); return XRL_EUNSUPPORTED; }
+        if (opts->leaf_max < 1) { set_error("xrl_tree_build: leaf_max < 1"); return XRL_EINVAL; }
+        if (opts->max_depth < 1 || opts->max_depth > kMortonBits) { set_error("xrl_tree_build: max_depth"); return XRL_EINVAL; }
+    }
+    try {
+        return tree_build_impl(ctx, n_vert, vert, n_tri, tri, opts, out);
+    } catch (const CudaError& e) {
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host out of memory");
+        return XRL_ENOMEM;
+    }
+}
+
+void xrl_tree_destroy(xrl_tree t)
+{
+    if (!t) return;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    delete t;
+}
+
+xrl_status xrl_tree_info(xrl_tree t, xrl_tree_info_t* info)
+{
+    if (!t || !info) { set_error("xrl_tree_info: null argument"); return XRL_EINVAL; }
+    info->n = t->n;
+    info->n_local = t->n;
+    info->offset = 0;
+    info->n_boxes = t->nbox;
+    info->n_leaves = t->nleaf;
+    info->n_levels = t->nlevel;
+    info->p = kP;
+    info->n_v_pairs = t->nv;
+    info->n_x_pairs = t->nx;
+    info->n_w_pairs = t->nw;
+    info->n_u_pairs = t->nu;
+    info->n_p2p = t->np2p;
+    for (int d = 0; d < 3; ++d) info->root_lo[d] = t->lo[d];
+    info->root_width = t->W;
+    return XRL_OK;
+}
+
+xrl_status xrl_tree_perm(xrl_tree t, int32_t* perm)
+{
+    if (!t || !perm) { set_error("xrl_tree_perm: null argument"); return XRL_EINVAL; }
+    try {
+        XRL_CUDA(cudaSetDevice(t->ctx->device));
+        XRL_CUDA(cudaMemcpyAsync(perm, t->perm.p, 4 * t->n, cudaMemcpyDeviceToHost, t->ctx->stream));
+        XRL_CUDA(cudaStreamSynchronize(t->ctx->stream));
+        return XRL_OK;
+    } catch (const CudaError& e) {
+        return e.code;
+    }
+}
+
+xrl_status xrl_tree_export(xrl_tree t, int32_t* box_level, int32_t* box_ijk, int32_t* box_parent, int32_t* box_pb,
+                           int32_t* box_pe, int32_t* is_leaf, int64_t* u_ptr, int32_t* u_src, int64_t* v_ptr,
+                           int32_t* v_src, int64_t* x_ptr, int32_t* x_src, int64_t* w_ptr, int32_t* w_src)
+{
+    if (!t) { set_error("xrl_tree_export: null tree"); return XRL_EINVAL; }
+    try {
+        cudaStream_t st = t->ctx->stream;
+        XRL_CUDA(cudaSetDevice(t->ctx->device));
+        const size_t nb = t->nbox;
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            if (dst && bytes) XRL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        };
+        cp(box_level, t->blevel.p, 4 * nb);
+        cp(box_parent, t->bparent.p, 4 * nb);
+        cp(box_pb, t->bpb.p, 4 * nb);
+        cp(box_pe, t->bpe.p, 4 * nb);
+        if (box_ijk) {
+            std::vector<int32_t> a(nb), b(nb), c(nb);
+            cp(a.data(), t->bix.p, 4 * nb);
+            cp(b.data(), t->biy.p, 4 * nb);
+            cp(c.data(), t->biz.p, 4 * nb);
+            XRL_CUDA(cudaStreamSynchronize(st));
+            for (size_t i = 0; i < nb; ++i) { box_ijk[3 * i] = a[i]; box_ijk[3 * i + 1] = b[i]; box_ijk[3 * i + 2] = c[i]; }
+        }
+        if (is_leaf) {
+            std::vector<int32_t> ch(nb);
+            cp(ch.data(), t->bchild.p, 4 * nb);
+            XRL_CUDA(cudaStreamSynchronize(st));
+            for (size_t i = 0; i < nb; ++i) is_leaf[i] = ch[i] < 0;
+        }
+        cp(u_ptr, t->u_ptr.p, 8 * (nb + 1));
+        cp(u_src, t->u_src.p, 4 * t->nu);
+        cp(v_ptr, t->v_ptr.p, 8 * (nb + 1));
+        cp(v_src, t->v_src.p, 4 * t->nv);
+        cp(x_ptr, t->x_ptr.p, 8 * (nb + 1));
+        cp(x_src, t->x_src.p, 4 * t->nx);
+        cp(w_ptr, t->w_ptr.p, 8 * (nb + 1));
+        cp(w_src, t->w_src.p, 4 * t->nw);
+        XRL_CUDA(cudaStreamSynchronize(st));
+        return XRL_OK;
+    } catch (const CudaError& e) {
+        return e.code;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+// Internal structures of the XRL B200 library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/xrl.h"
+#include "harmonics.h"
+#include "operators.h"
+
+namespace xrl {
+
+void set_error(const char* fmt, ...);
+
+struct CudaError {
+    xrl_status code;
+};
+
+#define XRL_CUDA(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t _e = (expr);                                                             \
+        if (_e != cudaSuccess) {                                                             \
+            ::xrl::set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), __FILE__,   \
+                             __LINE__, cudaGetErrorString(_e));                              \
+            throw ::xrl::CudaError{_e == cudaErrorMemoryAllocation ? XRL_ENOMEM : XRL_ECUDA}; \
+        }                                                                                    \
+    } while (0)
+
+#define XRL_LAUNCH_CHECK() XRL_CUDA(cudaGetLastError())
+
+// Simple owning device buffer.
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { free(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { free(); }
+    void alloc(size_t count) {
+        free();
+        n = count;
+        if (count) XRL_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+enum Phase { PH_PACK = 0, PH_P2M, PH_M2M, PH_M2L, PH_P2L, PH_L2L, PH_LEAF, PH_COUNT };
+
+struct DeviceOperators {
+    DBuf<float> m2m;   // [8][kNC (k, input)][kNCP (i, output, padded)]
+    DBuf<float> l2l;   // [8][kNC][kNCP]
+    DBuf<float> m2l;   // [316][kNC][kNCP]
+    int m2l_index[343];
+};
+
+constexpr int kNCP = 128;            // padded coefficient count
+constexpr int kBoxStride = 728;      // floats per box expansion (121*6 padded to 16 B)
+
+}  // namespace xrl
+
+struct xrl_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int rank = 0, world = 1;
+    xrl::DeviceOperators ops;
+    // timing
+    bool timing = false;
+    int64_t launches = 0;
+    double phase_ms[xrl::PH_COUNT] = {};
+    int64_t phase_launches[xrl::PH_COUNT] = {};
+    cudaEvent_t ev[2 * xrl::PH_COUNT] = {};
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> event_pool;
+};
+
+struct xrl_tree_s {
+    xrl_ctx ctx = nullptr;
+    int64_t n = 0;
+    int32_t leaf_max = 64, max_depth = 21;
+    double lo[3] = {0, 0, 0};   // root cube corner
+    double W = 1;               // root cube width
+    // per panel, library order
+    xrl::DBuf<int32_t> perm;    // library -> original
+    xrl::DBuf<int32_t> iperm;   // original -> library
+    xrl::DBuf<double> cent;     // [n][3] FP64 centroids
+    xrl::DBuf<double> area;     // [n]
+    xrl::DBuf<double> dmax;     // [n]
+    xrl::DBuf<double> tverts;   // [n][9] triangle vertices
+    xrl::DBuf<float4> loc;      // [n] local coords (W units) relative to leaf centre; w = unused
+    xrl::DBuf<int32_t> panel_leaf;  // [n] leaf box of each panel
+    // boxes (level order)
+    int32_t nbox = 0, nleaf = 0, nlevel = 0;
+    std::vector<int32_t> lvl_start;          // host [nlevel+1]
+    xrl::DBuf<int32_t> blevel, bix, biy, biz, bparent, bchild, bnchild, bpb, bpe;
+    xrl::DBuf<int32_t> leaves;               // [nleaf] leaf box ids
+    xrl::DBuf<double> bdmax;                 // [nbox] max D in subtree
+    // lists, CSR by target box id
+    xrl::DBuf<int64_t> u_ptr, v_ptr, x_ptr, w_ptr;
+    xrl::DBuf<int32_t> u_src, v_src, x_src, w_src;
+    int64_t nu = 0, nv = 0, nx = 0, nw = 0, np2p = 0;
+    // M2L pairs sorted by (offset, target) and their tiles
+    xrl::DBuf<int32_t> m2l_tgt, m2l_srcb;    // [nv]
+    xrl::DBuf<int4> m2l_tiles;               // (offset, pair begin, pair count, 0)
+    int32_t n_m2l_tiles = 0;
+    // boxes with non-empty X list, leaves with non-empty W list
+    xrl::DBuf<int32_t> x_targets;
+    int32_t n_x_targets = 0;
+    // parents per level for M2M/L2L: boxes with children, grouped by level
+    std::vector<int32_t> par_start;          // host [nlevel+1] offsets into parents
+    xrl::DBuf<int32_t> parents;
+    // MVM scratch
+    xrl::DBuf<float> mu, ell;                // [nbox][kBoxStride]
+    xrl::DBuf<float> xq;                     // [n][8] packed charges
+    xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging
+};
+
+struct xrl_near_s {
+    xrl_tree tree = nullptr;
+    double eta = 1.5;
+    int64_t nnz = 0;
+    xrl::DBuf<int64_t> row_ptr;
+    xrl::DBuf<int32_t> col;
+    xrl::DBuf<float> val;       // N_kl (FP32)
+    xrl::DBuf<double> val64;    // P_kl (FP64, before subtraction)
+};
+
+namespace xrl {
+// phase timing helpers (no-ops unless enabled)
+void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb);
+void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb);
+void upload_constants(xrl_ctx ctx);
+}  // namespace xrl

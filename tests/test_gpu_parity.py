@@ -1,0 +1,211 @@
+"""Parity of the CUDA path (through the C-ABI) against the FP64 oracle.
+
+Tolerances (BASELINE.json north star): full MVM relative L2 <= 2e-5 at p = 10
+over all 3 complex components jointly; near-field SpMV alone <= 1e-6.  Index
+work (near pattern, permutation, list coverage) is compared bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import meshes
+from tests.gpu_helpers import cuda_setup, oracle_rows, run_mvm
+
+pytestmark = pytest.mark.gpu
+
+TOL_FULL = 2e-5
+TOL_NEAR = 1e-6
+
+
+@pytest.fixture(scope="module")
+def bar_setup():
+    m = meshes.bar()
+    ctx, tree, near = cuda_setup(m)
+    return m, ctx, tree, near
+
+
+def test_permutation_is_morton_sort(bar_setup):
+    m, ctx, tree, near = bar_setup
+    perm = tree.perm()
+    assert np.array_equal(np.sort(perm), np.arange(m.n))
+    info = tree.info()
+    assert info["n"] == m.n and info["p"] == 10
+
+
+def _coverage(ex, n):
+    """For every leaf, count how often each source panel is covered by
+    U (P2P), W (M2P) and V/X of the leaf and all its ancestors."""
+    nb = ex["level"].shape[0]
+    par = ex["parent"]
+    pb, pe = ex["pb"], ex["pe"]
+    def panels(b):
+        return np.arange(pb[b], pe[b])
+    bad = 0
+    for b in np.nonzero(ex["is_leaf"])[0]:
+        cnt = np.zeros(n, dtype=np.int32)
+        for s in ex["u_src"][ex["u_ptr"][b]:ex["u_ptr"][b + 1]]:
+            cnt[panels(s)] += 1
+        for w in ex["w_src"][ex["w_ptr"][b]:ex["w_ptr"][b + 1]]:
+            cnt[panels(w)] += 1
+        a = b
+        while a >= 0:
+            for s in ex["v_src"][ex["v_ptr"][a]:ex["v_ptr"][a + 1]]:
+                cnt[panels(s)] += 1
+            for s in ex["x_src"][ex["x_ptr"][a]:ex["x_ptr"][a + 1]]:
+                cnt[panels(s)] += 1
+            a = par[a]
+        bad += int(np.sum(cnt != 1))
+    return bad
+
+
+@pytest.mark.parametrize("kind", ["bar", "bga2", "clustered"])
+def test_tree_lists_cover_every_pair_once(kind):
+    """SPEC.md:381 coverage audit: near + far lists cover all N^2 ordered
+    panel pairs exactly once (adaptive U/V/W/X lists)."""
+    if kind == "bar":
+        m = meshes.bar()
+        lm = 16
+    elif kind == "bga2":
+        m = meshes.bga(nb=2)
+        lm = 24
+    else:
+        # two dense clusters + sparse background: exercises W/X lists
+        rng = np.random.default_rng(3)
+        parts = []
+        for c, s, k in (((0, 0, 0), 1e-5, 300), ((3e-4, 1e-4, 0), 1e-5, 300), ((1e-4, 2e-4, 1e-4), 3e-4, 200)):
+            v = rng.normal(size=(3 * k, 3)) * s + np.array(c)
+            parts.append(v)
+        v = np.concatenate(parts)
+        m = meshes.Mesh(v, np.arange(v.shape[0], dtype=np.int32).reshape(-1, 3))
+        lm = 8
+    ctx, tree, near = cuda_setup(m, leaf_max=lm)
+    ex = tree.export()
+    info = tree.info()
+    assert info["n_levels"] >= 3
+    # leaves partition the panels, leaves respect leaf_max (depth cap not reached here)
+    leaves = np.nonzero(ex["is_leaf"])[0]
+    sizes = ex["pe"][leaves] - ex["pb"][leaves]
+    assert sizes.sum() == m.n and sizes.max() <= lm
+    assert _coverage(ex, m.n) == 0
+    if kind == "clustered":
+        assert info["n_x_pairs"] > 0 and info["n_w_pairs"] > 0
+
+
+def test_near_pattern_and_values_match_oracle(bar_setup):
+    m, ctx, tree, near = bar_setup
+    perm = tree.perm()
+    ptr, col, v32, v64 = near.export()
+    g = oracle.Geometry(m.verts, m.tris)
+    optr, ocol, oval, oinv_r = oracle.near_rows(g)
+    # map GPU rows/cols (library order) to mesh order
+    for i in range(m.n):
+        k = perm[i]
+        gc = np.sort(perm[col[ptr[i]:ptr[i + 1]]])
+        oc = ocol[optr[k]:optr[k + 1]]
+        assert np.array_equal(gc, oc), i
+    # values: FP64 near entries agree to rounding; FP32 correction = P - 1/r
+    rows_lib = np.repeat(np.arange(m.n), np.diff(ptr))
+    k_m = perm[rows_lib]
+    l_m = perm[col]
+    P = oracle.dense_p(g)
+    np.testing.assert_allclose(v64, P[k_m, l_m], rtol=1e-12)
+    d = np.linalg.norm(g.cent[k_m] - g.cent[l_m], axis=1)
+    corr = np.where(k_m == l_m, P[k_m, l_m], P[k_m, l_m] - 1.0 / np.where(d > 0, d, 1))
+    np.testing.assert_allclose(v32, corr, rtol=2e-7, atol=1e-7 * np.abs(P).max())
+
+
+def test_near_only_spmv(bar_setup):
+    m, ctx, tree, near = bar_setup
+    x = meshes.make_x(1, m.n)
+    y = run_mvm(tree, near, x, flags=1)
+    g = oracle.Geometry(m.verts, m.tris)
+    optr, ocol, oval, oinv_r = oracle.near_rows(g)
+    rows = np.repeat(np.arange(m.n), np.diff(optr))
+    corr = oval - oinv_r
+    yref = np.zeros((3, m.n), dtype=np.complex128)
+    for v in range(3):
+        np.add.at(yref[v], rows, corr * x[v, ocol].astype(np.complex128))
+    err = oracle.rel_l2(y, yref)
+    print("near-only rel L2", err)
+    assert err <= TOL_NEAR
+
+
+def test_full_mvm_config1(bar_setup):
+    m, ctx, tree, near = bar_setup
+    x = meshes.make_x(1, m.n)
+    y = run_mvm(tree, near, x)
+    yref = oracle_rows(m, x)
+    err = oracle.rel_l2(y, yref)
+    print("cfg1 full rel L2", err)
+    assert err <= TOL_FULL
+
+
+def test_far_only_vs_direct_inverse_r(bar_setup):
+    m, ctx, tree, near = bar_setup
+    x = meshes.make_x(1, m.n)
+    y = run_mvm(tree, near, x, flags=2)
+    c = m.verts[m.tris].mean(axis=1)
+    d = np.linalg.norm(c[:, None] - c[None], axis=2)
+    np.fill_diagonal(d, np.inf)
+    yref = (1.0 / d) @ x.astype(np.complex128).T
+    err = oracle.rel_l2(y, yref.T)
+    print("far-only rel L2", err)
+    assert err <= TOL_FULL
+
+
+def test_special_cases(bar_setup):
+    m, ctx, tree, near = bar_setup
+    x = np.zeros((3, m.n), dtype=np.complex64)
+    assert np.all(run_mvm(tree, near, x) == 0)
+    x = meshes.make_x(1, m.n)
+    y1 = run_mvm(tree, near, x)
+    y2 = run_mvm(tree, near, (2 * x).astype(np.complex64))
+    assert np.allclose(y2, 2 * y1, rtol=1e-6, atol=1e-6 * np.abs(y1).max())
+    # two triples in one call == two calls
+    x6 = np.concatenate([x, x[::-1].copy()])
+    y6 = run_mvm(tree, near, x6)
+    assert np.array_equal(y6[:3], y1)
+    assert np.allclose(y6[3:], run_mvm(tree, near, x[::-1].copy()), rtol=0, atol=0)
+
+
+def test_single_leaf_exact():
+    """N <= leaf_max: no multipoles, y = P2P + CSR."""
+    m = meshes.small_mesh("cube", n=2)  # 48 panels
+    ctx, tree, near = cuda_setup(m, leaf_max=64)
+    assert tree.info()["n_levels"] == 1
+    x = meshes.make_x(1, m.n)
+    y = run_mvm(tree, near, x)
+    yref = oracle_rows(m, x)
+    assert oracle.rel_l2(y, yref) < 1e-6
+
+
+@pytest.mark.parametrize("leaf_max", [8, 30, 200])
+def test_leaf_sizes_ragged(leaf_max):
+    m = meshes.bar()
+    ctx, tree, near = cuda_setup(m, leaf_max=leaf_max)
+    x = meshes.make_x(1, m.n)
+    y = run_mvm(tree, near, x)
+    err = oracle.rel_l2(y, oracle_rows(m, x))
+    print("leaf", leaf_max, err)
+    assert err <= TOL_FULL
+
+
+def test_host_api_e2e(bar_setup):
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near = bar_setup
+    x = meshes.make_x(1, m.n)
+    y_dev = run_mvm(tree, near, x)
+    y_host = xrl.mvm_host(tree, near, x)
+    assert np.array_equal(y_dev, y_host)
+
+
+@pytest.mark.parametrize("cfg,nrows", [(2, 1024), (3, 512)])
+def test_full_mvm_sampled_rows(cfg, nrows):
+    m = meshes.make_config(cfg)
+    ctx, tree, near = cuda_setup(m)
+    x = meshes.make_x(cfg, m.n)
+    y = run_mvm(tree, near, x)
+    rows = np.random.default_rng(7).choice(m.n, size=nrows, replace=False)
+    yref = oracle_rows(m, x, rows)
+    err = oracle.rel_l2(y[:, rows], yref)
+    print(f"cfg{cfg} sampled rel L2", err, tree.info())
+    assert err <= TOL_FULL
