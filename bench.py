@@ -158,10 +158,12 @@ def run_reference(args):
     return 0
 
 
-def traffic_from_profiles(kernel: str):
+def traffic_from_profiles(kernel: str, key: str):
+    """DRAM read+write bytes per launch of `kernel` from a committed ncu
+    capture of the same workload/leaf (profiles/traffic.json), else None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p)).get(kernel)
+        return json.load(open(p)).get(key, {}).get(kernel)
     except Exception:
         return None
 
@@ -247,34 +249,46 @@ def run_xrl(args):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * n / float(te.item()) / 1e6
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel (+ the other hot kernels for reference)
     peaks = _peaks()
     clocks = clk.summary()
     tot_phase = sum(v[0] for v in phases.values())
-    dom = max(phases, key=lambda k: phases[k][0])
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s, SIMT FFMA
+    fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s, SIMT FFMA (derivation: DESIGN.md)
+    hbm_peak = float(peaks.get("hbm_gbs", 6551.4))
     nc = 121
-    m2l_flops = 2.0 * nc * nc * 6 * info["n_v_pairs"]
-    p2p_flops = 20.0 * info["n_p2p"]
-    roof = None
-    if dom == "m2l":
-        per_launch_ms = phases["m2l"][0] / max(phases["m2l"][1], 1)
-        achieved = m2l_flops / (per_launch_ms * 1e-3) / 1e12
-        roof = {"kernel": "k_m2l", "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": traffic_from_profiles("k_m2l"),
-                "algorithmic": f"2*121^2*6 flops x {info['n_v_pairs']} V-list translations per launch",
-                "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
-    else:
-        per_launch_ms = phases[dom][0] / max(phases[dom][1], 1)
-        flops = p2p_flops if dom == "leaf" else 0.0
-        achieved = flops / (per_launch_ms * 1e-3) / 1e12
-        roof = {"kernel": "k_" + dom, "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": traffic_from_profiles("k_" + dom),
-                "algorithmic": f"P2P only: 20 flops x {info['n_p2p']} ordered pairs per launch (L2P/M2P/near not counted)",
-                "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz"}
+    nnz = near.nnz()
+    tkey = f"{CFG_NAMES[args.config]}_leaf{args.leaf}"
+
+    def per_launch_ms(ph):
+        ms_, cnt = phases[ph]
+        return ms_ / max(cnt, 1)
+
+    roofs = {}
+    if phases["m2l"][1]:
+        a = 2.0 * nc * nc * 6 * info["n_v_pairs"] / (per_launch_ms("m2l") * 1e-3) / 1e12
+        roofs["m2l"] = {"kernel": "k_m2l", "bound": "alu", "achieved": a, "peak": fp32_peak, "unit": "TFLOP/s",
+                        "frac": a / fp32_peak, "traffic": traffic_from_profiles("k_m2l", tkey),
+                        "algorithmic": f"2*121^2*6 = 175692 flops x {info['n_v_pairs']} V-list translations per launch",
+                        "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 flops x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
+    if phases["p2p"][1]:
+        a = 20.0 * info["n_p2p"] / (per_launch_ms("p2p") * 1e-3) / 1e12
+        roofs["p2p"] = {"kernel": "k_p2p", "bound": "alu", "achieved": a, "peak": fp32_peak, "unit": "TFLOP/s",
+                        "frac": a / fp32_peak, "traffic": traffic_from_profiles("k_p2p", tkey),
+                        "algorithmic": f"20 flops x {info['n_p2p']} ordered panel pairs per launch",
+                        "peak_source": "as k_m2l"}
+    if phases["near"][1]:
+        byts = 8.0 * nnz + 56.0 * n
+        a = byts / (per_launch_ms("near") * 1e-3) / 1e9
+        roofs["near"] = {"kernel": "k_near_spmv", "bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": a / hbm_peak, "traffic": traffic_from_profiles("k_near_spmv", tkey),
+                         "algorithmic": f"8 B x {nnz} nnz + 56 B x {n} rows (row_ptr, x, y) per launch",
+                         "peak_source": "hbm_gbs, MEASURED_PEAKS.json"}
+    dom = max(phases, key=lambda k: phases[k][0])
+    roof = dict(roofs.get(dom) or {"kernel": "k_" + dom})
     roof["share_of_step"] = phases[dom][0] / tot_phase if tot_phase else None
+    roof["others"] = {k: {kk: v[kk] for kk in ("achieved", "peak", "unit", "frac")} for k, v in roofs.items() if k != dom}
 
     line = {
         "metric": METRIC, "value": value, "unit": "Mpanels/s", "n_gpus": world, "steps": args.steps,
@@ -285,7 +299,8 @@ def run_xrl(args):
                    "l2": "flushed (256 MiB write) between timed steps",
                    "boxes": info["n_boxes"], "leaves": info["n_leaves"], "levels": info["n_levels"],
                    "m2l_translations": info["n_v_pairs"], "p2p_pairs": info["n_p2p"],
-                   "x_pairs": info["n_x_pairs"], "w_pairs": info["n_w_pairs"], "setup_s": round(setup_s, 3)},
+                   "x_pairs": info["n_x_pairs"], "w_pairs": info["n_w_pairs"], "near_nnz": nnz,
+                   "setup_s": round(setup_s, 3)},
         "e2e": {"value": e2e_value, "unit": "Mpanels/s", "h2d_bytes_per_step": int(xh.numel() * 8),
                 "d2h_bytes_per_step": int(yh.numel() * 8)},
         "gpu_launches": launches,
@@ -310,7 +325,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["xrl", "reference"], default="xrl")
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--leaf", type=int, default=64)
+    ap.add_argument("--leaf", type=int, default=512)  # tuned for config 4
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -76,13 +76,15 @@ typedef struct xrl_near_s* xrl_near;
 const char* xrl_last_error(void);
 const char* xrl_version(void);
 
-/* Context: device ordinal, CUDA stream (cudaStream_t, NULL = library-created
- * non-blocking stream), rank/world for Morton-range sharding (world == 1 for a
+/* Context: device ordinal, CUDA stream the library enqueues on (cudaStream_t;
+ * NULL = the legacy default stream, as everywhere in CUDA), rank/world for Morton-range sharding (world == 1 for a
  * single GPU; multi-rank contexts need the 128-byte ncclUniqueId broadcast by
  * the caller, else NULL). */
 xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world,
                           const void* nccl_unique_id, xrl_ctx* out);
 xrl_status xrl_ctx_sync(xrl_ctx ctx);
+/* Destroying a context that still has trees defers the release until the
+ * last tree built on it is destroyed (likewise a tree with near handles). */
 void xrl_ctx_destroy(xrl_ctx ctx);
 
 /* FMM options.  p: expansion order (only 10 is compiled, PAPER.md silent ->
@@ -130,8 +132,11 @@ xrl_status xrl_from_library_order(xrl_tree tree, const void* x_lib, void* x_user
  * to skip it; sizes from xrl_tree_info.  Boxes are in level order.
  * box_level/ix/iy/iz/parent/pb/pe: int32 [n_boxes]; is_leaf: int32 [n_boxes];
  * *_ptr: int64 [n_boxes+1] CSR by target box, *_src: int32 sources.
- * lists: U (leaf <- leaf, P2P), V (box <- box, M2L), X (box <- leaf, P2L),
- * W (leaf <- box, M2P). */
+ * lists: U (leaf <- box, direct P2P: adjacent leaves, plus adaptive X/W
+ * pairs between small boxes evaluated directly), V (box <- box, M2L),
+ * X (non-leaf box <- leaf, P2L), W (leaf <- box with > 96 panels, M2P).
+ * Every ordered panel pair is covered exactly once by U, W, and the V/X
+ * lists of the target's leaf and its ancestors. */
 xrl_status xrl_tree_export(xrl_tree tree, int32_t* box_level, int32_t* box_ijk /* [n_boxes][3] */,
                            int32_t* box_parent, int32_t* box_pb, int32_t* box_pe, int32_t* is_leaf,
                            int64_t* u_ptr, int32_t* u_src, int64_t* v_ptr, int32_t* v_src,

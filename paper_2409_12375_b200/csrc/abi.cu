@@ -17,7 +17,7 @@ void set_error(const char* fmt, ...)
     va_end(ap);
 }
 
-static const char* kPhaseNames[PH_COUNT] = {"pack", "p2m", "m2m", "m2l", "p2l", "l2l", "leaf"};
+static const char* kPhaseNames[PH_COUNT] = {"pack", "p2m", "m2m", "m2l", "p2l", "l2l", "l2p_m2p", "p2p", "near"};
 
 static cudaEvent_t get_event(xrl_ctx ctx)
 {
@@ -31,20 +31,20 @@ static cudaEvent_t get_event(xrl_ctx ctx)
     return e;
 }
 
-void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb)
+void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb, cudaStream_t st)
 {
     (void)ph;
     *evb = nullptr;
     if (!ctx->timing) return;
     *evb = get_event(ctx);
-    XRL_CUDA(cudaEventRecord(*evb, ctx->stream));
+    XRL_CUDA(cudaEventRecord(*evb, st));
 }
 
-void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb)
+void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb, cudaStream_t st)
 {
     if (!ctx->timing || !evb) return;
     cudaEvent_t e = get_event(ctx);
-    XRL_CUDA(cudaEventRecord(e, ctx->stream));
+    XRL_CUDA(cudaEventRecord(e, st));
     ctx->pending.push_back({ph, {evb, e}});
 }
 
@@ -105,11 +105,10 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         c->device = device;
         c->rank = rank;
         c->world = world;
-        if (cuda_stream) c->stream = (cudaStream_t)cuda_stream;
-        else {
-            XRL_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-            c->own_stream = true;
-        }
+        c->stream = (cudaStream_t)cuda_stream;  // NULL = legacy default stream
+        XRL_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         if (world > 1) {
             delete c;
             set_error("multi-rank contexts are not built in this version");
@@ -134,13 +133,27 @@ xrl_status xrl_ctx_sync(xrl_ctx ctx)
 void xrl_ctx_destroy(xrl_ctx ctx)
 {
     if (!ctx) return;
+    ctx->dead = true;
+    ctx_release(ctx);
+}
+
+}  // extern "C"
+
+void xrl::ctx_release(xrl_ctx ctx)
+{
+    if (!ctx->dead || ctx->refs > 0) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (auto& p : ctx->pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->side) { cudaStreamSynchronize(ctx->side); cudaStreamDestroy(ctx->side); }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
+
+extern "C" {
 
 xrl_status xrl_timing_enable(xrl_ctx ctx, int on)
 {

@@ -30,8 +30,8 @@ __constant__ RecTables<float> c_tab;
 
 namespace {
 
-constexpr int kTP = 32;          // pairs per M2L tile
-constexpr int kBCols = kTP * 6;  // 192 columns of the M2L B tile
+constexpr int kTP = 16;          // pairs per M2L tile
+constexpr int kBCols = kTP * 6 + 4;  // 96 columns of the M2L B tile (+4 pad: spreads the gather over banks)
 
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d)
 {
@@ -175,76 +175,106 @@ __global__ void __launch_bounds__(128) k_l2l(int b0, const int32_t* __restrict__
 }
 
 // ------------------------------------------------------------------ M2L
-// Tile = (offset o, pairs [begin, begin+count)), count <= 32.
-// C[128 x 192] = T_o[128 x 121] * B[121 x 192], B[k][p*6+r] = mu_src(p)[k][r].
-// 256 threads: rg = tid % 16 owns rows rg*8..+7, pg = tid / 16 owns pairs 2pg, 2pg+1.
+// Tile = (offset o, pairs [begin, begin+count)), count <= kTP = 16.  Tiles are
+// ordered target-chunk-major (4096 target boxes per chunk), then by offset, so
+// the mu gathers and the ell reductions of the tiles in flight stay in L2.
+// C[128 x 96] = T_o[128 x 121] * B[121 x 96], B[k][p*6+r] = mu_src(p)[k][r].
+// 256 threads: rg = tid % 16 owns rows rg*4..+3 and 64+rg*4..+3 (float4 rows
+// contiguous across the 16 lanes: no bank conflicts), cg = tid / 16 owns pair cg.
+// 108 KB shared memory -> 2 CTAs per SM so one CTA's loads overlap the other's FMAs.
 constexpr int kM2LSmem = (kNC * kNCP + kNC * kBCols) * 4;
 
-__global__ void __launch_bounds__(256, 1) k_m2l(const int4* __restrict__ tiles, const int32_t* __restrict__ tgt,
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__global__ void __launch_bounds__(256, 2) k_m2l(const int4* __restrict__ tiles, const int32_t* __restrict__ tgt,
                                                 const int32_t* __restrict__ srcb, const float* __restrict__ ops,
                                                 const float* __restrict__ mu, float* __restrict__ ell)
 {
     extern __shared__ __align__(16) float sm[];
     float* Ts = sm;                    // [121][128]
-    float* Bs = sm + kNC * kNCP;       // [121][192]
+    float* Bs = sm + kNC * kNCP;       // [121][96]
     const int4 tile = tiles[blockIdx.x];
     const int off = tile.x, begin = tile.y, count = tile.z;
     const int tid = threadIdx.x;
     {
         const float4* g = reinterpret_cast<const float4*>(ops + (size_t)off * kNC * kNCP);
         float4* s = reinterpret_cast<float4*>(Ts);
-        for (int j = tid; j < kNC * kNCP / 4; j += 256) s[j] = g[j];
+        for (int j = tid; j < kNC * kNCP / 4; j += 256) cp_async16(s + j, g + j);
     }
     for (int j = tid; j < kTP * 363; j += 256) {
         const int p = j / 363, q = j % 363;
-        float2 v = make_float2(0.f, 0.f);
-        if (p < count) v = reinterpret_cast<const float2*>(mu + (size_t)srcb[begin + p] * kBoxStride)[q];
         const int k = q / 3, r2 = q % 3;
-        *reinterpret_cast<float2*>(&Bs[k * kBCols + p * 6 + 2 * r2]) = v;
+        float* dst = &Bs[k * kBCols + p * 6 + 2 * r2];
+        if (p < count) cp_async8(dst, reinterpret_cast<const float2*>(mu + (size_t)srcb[begin + p] * kBoxStride) + q);
+        else *reinterpret_cast<float2*>(dst) = make_float2(0.f, 0.f);
     }
+    cp_async_wait_all();
     __syncthreads();
-    const int rg = tid & 15, pg = tid >> 4;
-    float acc[8][12];
+    const int rg = tid & 15, cg = tid >> 4;
+    float acc[8][6];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
 #pragma unroll
-        for (int c = 0; c < 12; ++c) acc[a][c] = 0.f;
-    const float* tp = Ts + rg * 8;
-    const float* bp = Bs + pg * 12;
-#pragma unroll 2
+        for (int c = 0; c < 6; ++c) acc[a][c] = 0.f;
+    const float* tp = Ts + rg * 4;
+    const float* bp = Bs + cg * 6;
+#pragma unroll 4
     for (int k = 0; k < kNC; ++k) {
         const float4 t0 = *reinterpret_cast<const float4*>(tp + k * kNCP);
-        const float4 t1 = *reinterpret_cast<const float4*>(tp + k * kNCP + 4);
-        const float4 b0 = *reinterpret_cast<const float4*>(bp + k * kBCols);
-        const float4 b1 = *reinterpret_cast<const float4*>(bp + k * kBCols + 4);
-        const float4 b2 = *reinterpret_cast<const float4*>(bp + k * kBCols + 8);
+        const float4 t1 = *reinterpret_cast<const float4*>(tp + k * kNCP + 64);
+        const float2 b0 = *reinterpret_cast<const float2*>(bp + k * kBCols);
+        const float2 b1 = *reinterpret_cast<const float2*>(bp + k * kBCols + 2);
+        const float2 b2 = *reinterpret_cast<const float2*>(bp + k * kBCols + 4);
         const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-        const float bv[12] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+        const float bv[6] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y};
 #pragma unroll
         for (int a = 0; a < 8; ++a)
 #pragma unroll
-            for (int c = 0; c < 12; ++c) acc[a][c] = fmaf(tv[a], bv[c], acc[a][c]);
+            for (int c = 0; c < 6; ++c) acc[a][c] = fmaf(tv[a], bv[c], acc[a][c]);
     }
+    if (cg >= count) return;
+    float* base = ell + (size_t)tgt[begin + cg] * kBoxStride;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int p = 2 * pg + q;
-        if (p >= count) continue;
-        float* base = ell + (size_t)tgt[begin + p] * kBoxStride;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int i = rg * 8 + 2 * j;
-            if (i >= kNC) continue;
-            float* o = base + 6 * i;
-            const float* a0 = acc[2 * j] + 6 * q;
-            const float* a1 = acc[2 * j + 1] + 6 * q;
-            red_add_v4(o, a0[0], a0[1], a0[2], a0[3]);
-            red_add_v4(o + 4, a0[4], a0[5], a1[0], a1[1]);
-            if (i + 1 < kNC) red_add_v4(o + 8, a1[2], a1[3], a1[4], a1[5]);
-        }
+    for (int j = 0; j < 4; ++j) {
+        const int i = (j >> 1) * 64 + rg * 4 + 2 * (j & 1);
+        if (i >= kNC) continue;
+        float* o = base + 6 * i;
+        const float* a0 = acc[2 * j];
+        const float* a1 = acc[2 * j + 1];
+        red_add_v4(o, a0[0], a0[1], a0[2], a0[3]);
+        red_add_v4(o + 4, a0[4], a0[5], a1[0], a1[1]);
+        if (i + 1 < kNC) red_add_v4(o + 8, a1[2], a1[3], a1[4], a1[5]);
     }
 }
 
 // ------------------------------------------------------------------ P2L (X list)
+// One CTA per target box b; the panels of all leaves in X(b) are flattened and
+// processed 128 at a time (one panel per thread computes It and its charges
+// into shared memory, then 128 threads reduce the 726 outputs).
+constexpr int kXWin = 64;                 // X leaves per window
+constexpr int kP2LChunk = 128;
+constexpr int kP2LSmem = kP2LChunk * (kNC + 6) * 4;
+
+__device__ __forceinline__ int find_seg(const int* off, int n, int j)
+{
+    int lo = 0, hi = n - 1;  // largest i with off[i] <= j
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= j) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
 __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, const int64_t* __restrict__ xptr,
                                              const int32_t* __restrict__ xsrc, const int32_t* __restrict__ level,
                                              const int32_t* __restrict__ ix, const int32_t* __restrict__ iy,
@@ -252,28 +282,47 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
                                              const int32_t* __restrict__ pe, const float4* __restrict__ loc,
                                              const float* __restrict__ xq, float* __restrict__ ell)
 {
-    __shared__ float H[kChunk][kNC];
-    __shared__ float Q[kChunk][6];
+    extern __shared__ __align__(16) float psm[];
+    float* H = psm;                        // [128][121]
+    float* Q = psm + kP2LChunk * kNC;      // [128][6]
+    __shared__ int Xoff[kXWin + 1], Xid[kXWin];
+    __shared__ float3 Xd[kXWin];
     const int b = xt[blockIdx.x];
     const int lb = level[b];
     const float3 cb = box_center(lb, ix[b], iy[b], iz[b]);
     const float inv_s = ldexpf(1.f, lb);
     float acc[6] = {0, 0, 0, 0, 0, 0};
-    for (int64_t j = xptr[b]; j < xptr[b + 1]; ++j) {
-        const int L = xsrc[j];
-        const float3 cL = box_center(level[L], ix[L], iy[L], iz[L]);
-        const float dx = cL.x - cb.x, dy = cL.y - cb.y, dz = cL.z - cb.z;
-        for (int c0 = pb[L]; c0 < pe[L]; c0 += kChunk) {
-            const int cn = min(kChunk, pe[L] - c0);
+    for (int64_t x0 = xptr[b]; x0 < xptr[b + 1]; x0 += kXWin) {
+        const int nx = (int)min((int64_t)kXWin, xptr[b + 1] - x0);
+        __syncthreads();
+        if (threadIdx.x < nx) {
+            const int L = xsrc[x0 + threadIdx.x];
+            Xid[threadIdx.x] = L;
+            const float3 cL = box_center(level[L], ix[L], iy[L], iz[L]);
+            Xd[threadIdx.x] = make_float3(cL.x - cb.x, cL.y - cb.y, cL.z - cb.z);
+        }
+        if (threadIdx.x == 0) {
+            int o = 0;
+            for (int i = 0; i < nx; ++i) { Xoff[i] = o; const int L = xsrc[x0 + i]; o += pe[L] - pb[L]; }
+            Xoff[nx] = o;
+        }
+        __syncthreads();
+        const int total = Xoff[nx];
+        for (int c0 = 0; c0 < total; c0 += kP2LChunk) {
+            const int cn = min(kP2LChunk, total - c0);
             if (threadIdx.x < cn) {
-                const int i = c0 + threadIdx.x;
+                const int j = c0 + threadIdx.x;
+                const int li = find_seg(Xoff, nx, j);
+                const int i = pb[Xid[li]] + (j - Xoff[li]);
+                const float3 d = Xd[li];
                 const float4 p = loc[i];
                 float h[kNC];
-                irregular_harmonics<kP>((p.x + dx) * inv_s, (p.y + dy) * inv_s, (p.z + dz) * inv_s, c_tab, h);
+                irregular_harmonics<kP>((p.x + d.x) * inv_s, (p.y + d.y) * inv_s, (p.z + d.z) * inv_s, c_tab, h);
+                float* Hr = H + threadIdx.x * kNC;
 #pragma unroll
-                for (int k = 0; k < kNC; ++k) H[threadIdx.x][k] = (k == 0 || degree_of(k) * degree_of(k) == k) ? h[k] : 2.f * h[k];
+                for (int k = 0; k < kNC; ++k) Hr[k] = (degree_of(k) * degree_of(k) == k) ? h[k] : 2.f * h[k];
 #pragma unroll
-                for (int r = 0; r < 6; ++r) Q[threadIdx.x][r] = xq[8 * (int64_t)i + r];
+                for (int r = 0; r < 6; ++r) Q[threadIdx.x * 6 + r] = xq[8 * (int64_t)i + r];
             }
             __syncthreads();
 #pragma unroll
@@ -282,7 +331,7 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
                 if (o < kNC * 6) {
                     const int k = o / 6, r = o % 6;
                     float a = acc[jj];
-                    for (int p = 0; p < cn; ++p) a += H[p][k] * Q[p][r];
+                    for (int p = 0; p < cn; ++p) a = fmaf(H[p * kNC + k], Q[p * 6 + r], a);
                     acc[jj] = a;
                 }
             }
@@ -297,135 +346,197 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
     }
 }
 
-// ------------------------------------------------------------------ leaf evaluation
-// Per target leaf: L2P + M2P(W) + P2P(U) + near CSR; 128 threads = 2 halves x 64 targets.
-__global__ void __launch_bounds__(128) k_leaf(
+// ------------------------------------------------------------------ near-field SpMV
+// y = N x for the 6 real RHS (N: FP32 CSR of the near correction and the self
+// terms).  HBM-bound: 8 B per nonzero (col + val) + the gathered charges
+// (L2-resident) + 24 B of y per row.  8 lanes per row, 4 rows per warp,
+// shuffle reduction over the 8 lanes.
+__global__ void __launch_bounds__(256) k_near_spmv(int64_t n, const int64_t* __restrict__ ptr,
+                                                   const int32_t* __restrict__ col, const float* __restrict__ val,
+                                                   const float* __restrict__ xq, float2* __restrict__ y)
+{
+    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+    const int lane = threadIdx.x & 7;
+    float a[6] = {0, 0, 0, 0, 0, 0};
+    if (row < n) {
+        const int64_t e = ptr[row + 1];
+#pragma unroll 2
+        for (int64_t j = ptr[row] + lane; j < e; j += 8) {
+            const float v = __ldcs(val + j);
+            const int64_t c = __ldcs(col + j);
+            const float4 q0 = __ldg(reinterpret_cast<const float4*>(xq + 8 * c));
+            const float2 q1 = __ldg(reinterpret_cast<const float2*>(xq + 8 * c) + 2);
+            a[0] = fmaf(v, q0.x, a[0]); a[1] = fmaf(v, q0.y, a[1]); a[2] = fmaf(v, q0.z, a[2]);
+            a[3] = fmaf(v, q0.w, a[3]); a[4] = fmaf(v, q1.x, a[4]); a[5] = fmaf(v, q1.y, a[5]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+        a[r] += __shfl_xor_sync(0xffffffffu, a[r], 1);
+        a[r] += __shfl_xor_sync(0xffffffffu, a[r], 2);
+        a[r] += __shfl_xor_sync(0xffffffffu, a[r], 4);
+    }
+    if (row < n && lane < 3) y[lane * n + row] = make_float2(a[2 * lane], a[2 * lane + 1]);
+}
+
+// ------------------------------------------------------------------ P2P
+// One CTA (128 threads) per target leaf; targets in chunks of nt <= 64.  The
+// CTA is split into G = 128 / nt groups of nt threads (thread = (target,
+// group)); the U-list source panels are flattened, staged 512 at a time in
+// shared memory (coordinates re-based to the target leaf centre, W units)
+// and split over the groups.  y += (1/W) sum_{l != k} x_l / r_kl.
+constexpr int kUWin = 64;
+constexpr int kSrcChunk = 512;
+
+__global__ void __launch_bounds__(128) k_p2p(
     const int32_t* __restrict__ leaves, const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
     const int32_t* __restrict__ iy, const int32_t* __restrict__ iz, const int32_t* __restrict__ pb,
     const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
-    const int64_t* __restrict__ wptr, const int32_t* __restrict__ wsrc, const float4* __restrict__ loc,
-    const float* __restrict__ xq, const float* __restrict__ mu, const float* __restrict__ ell,
-    const int64_t* __restrict__ nptr, const int32_t* __restrict__ ncol, const float* __restrict__ nval, float invW,
-    int do_far, int do_near, int64_t n, float2* __restrict__ y)
+    const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate, int64_t n,
+    float2* __restrict__ y)
 {
-    __shared__ float Ls[kBoxStride];
-    __shared__ float Ms[2][kBoxStride];
-    __shared__ float4 Sp[128];
-    __shared__ float Sq[128][6];
-    __shared__ float Red[64][12];
+    __shared__ float4 Sp[kSrcChunk];
+    __shared__ float4 Sq[kSrcChunk][2];
+    __shared__ float Red[128][6];
+    __shared__ int Uoff[kUWin + 1], Uid[kUWin];
+    __shared__ float3 Ud[kUWin];
     const int b = leaves[blockIdx.x];
-    const int lb = level[b];
-    const float3 cb = box_center(lb, ix[b], iy[b], iz[b]);
-    const float inv_sb = ldexpf(1.f, lb);
-    const int half = threadIdx.x >> 6, lane = threadIdx.x & 63;
-    if (do_far)
-        for (int j = threadIdx.x; j < kBoxStride / 4; j += 128)
-            reinterpret_cast<float4*>(Ls)[j] = reinterpret_cast<const float4*>(ell + (size_t)b * kBoxStride)[j];
+    const float3 cb = box_center(level[b], ix[b], iy[b], iz[b]);
+    const int tid = threadIdx.x;
     for (int t0 = pb[b]; t0 < pe[b]; t0 += 64) {
-        const int ti = t0 + lane;
-        const bool act = ti < pe[b];
+        const int nt = min(64, pe[b] - t0);
+        const int G = 128 / nt;
+        const int t = tid % nt, g = tid / nt;
+        const bool act = g < G;
+        const int ti = t0 + t;
         float4 tp = make_float4(0.f, 0.f, 0.f, 0.f);
         if (act) tp = loc[ti];
-        float far[6] = {0, 0, 0, 0, 0, 0}, nr[6] = {0, 0, 0, 0, 0, 0};
-        __syncthreads();
-        if (do_far) {
-            // L2P
-            if (half == 0 && act) {
-                float h[kNC];
-                regular_harmonics<kP>(tp.x * inv_sb, tp.y * inv_sb, tp.z * inv_sb, c_tab, h);
-#pragma unroll
-                for (int k = 0; k < kNC; ++k)
-#pragma unroll
-                    for (int r = 0; r < 6; ++r) far[r] += Ls[6 * k + r] * h[k];
-#pragma unroll
-                for (int r = 0; r < 6; ++r) far[r] *= inv_sb;
-            }
-            // M2P over the W list, two boxes per step (one per half)
-            const int64_t w0 = wptr[b], w1 = wptr[b + 1];
-            for (int64_t wj = w0; wj < w1; wj += 2) {
-                __syncthreads();
-                for (int j = threadIdx.x; j < 2 * (kBoxStride / 4); j += 128) {
-                    const int hh = j / (kBoxStride / 4), q = j % (kBoxStride / 4);
-                    if (wj + hh < w1)
-                        reinterpret_cast<float4*>(Ms[hh])[q] =
-                            reinterpret_cast<const float4*>(mu + (size_t)wsrc[wj + hh] * kBoxStride)[q];
-                }
-                __syncthreads();
-                if (act && wj + half < w1) {
-                    const int w = wsrc[wj + half];
-                    const int lw = level[w];
-                    const float3 cw = box_center(lw, ix[w], iy[w], iz[w]);
-                    const float inv_sw = ldexpf(1.f, lw);
-                    float h[kNC];
-                    irregular_harmonics<kP>((tp.x + cb.x - cw.x) * inv_sw, (tp.y + cb.y - cw.y) * inv_sw,
-                                            (tp.z + cb.z - cw.z) * inv_sw, c_tab, h);
-                    float a[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-                    for (int k = 0; k < kNC; ++k) {
-                        const float hk = (k == 0 || degree_of(k) * degree_of(k) == k) ? h[k] : 2.f * h[k];
-#pragma unroll
-                        for (int r = 0; r < 6; ++r) a[r] += Ms[half][6 * k + r] * hk;
-                    }
-#pragma unroll
-                    for (int r = 0; r < 6; ++r) far[r] += a[r] * inv_sw;
-                }
-            }
-            // P2P over the U list (W units)
-            for (int64_t uj = uptr[b]; uj < uptr[b + 1]; ++uj) {
-                const int s = usrc[uj];
+        float far[6] = {0, 0, 0, 0, 0, 0};
+        for (int64_t u0 = uptr[b]; u0 < uptr[b + 1]; u0 += kUWin) {
+            const int nu = (int)min((int64_t)kUWin, uptr[b + 1] - u0);
+            __syncthreads();
+            if (tid < nu) {
+                const int s = usrc[u0 + tid];
+                Uid[tid] = s;
                 const float3 cs = box_center(level[s], ix[s], iy[s], iz[s]);
-                const float dx = cs.x - cb.x, dy = cs.y - cb.y, dz = cs.z - cb.z;
-                for (int s0 = pb[s]; s0 < pe[s]; s0 += 128) {
-                    const int sn = min(128, pe[s] - s0);
-                    __syncthreads();
-                    if (threadIdx.x < sn) {
-                        const int i = s0 + threadIdx.x;
-                        const float4 p = loc[i];
-                        Sp[threadIdx.x] = make_float4(p.x + dx, p.y + dy, p.z + dz, 0.f);
-                        const float4 q0 = reinterpret_cast<const float4*>(xq + 8 * (int64_t)i)[0];
-                        const float2 q1 = reinterpret_cast<const float2*>(xq + 8 * (int64_t)i)[2];
-                        Sq[threadIdx.x][0] = q0.x; Sq[threadIdx.x][1] = q0.y; Sq[threadIdx.x][2] = q0.z;
-                        Sq[threadIdx.x][3] = q0.w; Sq[threadIdx.x][4] = q1.x; Sq[threadIdx.x][5] = q1.y;
-                    }
-                    __syncthreads();
-                    if (act) {
-                        for (int j = half; j < sn; j += 2) {
-                            const float4 sp = Sp[j];
-                            const float ddx = tp.x - sp.x, ddy = tp.y - sp.y, ddz = tp.z - sp.z;
-                            const float r2 = ddx * ddx + ddy * ddy + ddz * ddz;
-                            const float ri = r2 > 0.f ? rsqrtf(r2) : 0.f;
-#pragma unroll
-                            for (int r = 0; r < 6; ++r) far[r] += Sq[j][r] * ri;
-                        }
+                Ud[tid] = make_float3(cs.x - cb.x, cs.y - cb.y, cs.z - cb.z);
+            }
+            if (tid == 0) {
+                int o = 0;
+                for (int i = 0; i < nu; ++i) { Uoff[i] = o; const int s = usrc[u0 + i]; o += pe[s] - pb[s]; }
+                Uoff[nu] = o;
+            }
+            __syncthreads();
+            const int total = Uoff[nu];
+            for (int s0 = 0; s0 < total; s0 += kSrcChunk) {
+                const int sn = min(kSrcChunk, total - s0);
+                if (s0 > 0) __syncthreads();
+                for (int j = tid; j < sn; j += 128) {
+                    const int f = s0 + j;
+                    const int li = find_seg(Uoff, nu, f);
+                    const int i = pb[Uid[li]] + (f - Uoff[li]);
+                    const float3 d = Ud[li];
+                    const float4 p = loc[i];
+                    Sp[j] = make_float4(p.x + d.x, p.y + d.y, p.z + d.z, 0.f);
+                    const float4* q = reinterpret_cast<const float4*>(xq + 8 * (int64_t)i);
+                    Sq[j][0] = q[0];
+                    Sq[j][1] = q[1];
+                }
+                __syncthreads();
+                if (act) {
+#pragma unroll 4
+                    for (int j = g; j < sn; j += G) {
+                        const float4 sp = Sp[j];
+                        const float dx = tp.x - sp.x, dy = tp.y - sp.y, dz = tp.z - sp.z;
+                        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                        const float ri = r2 > 0.f ? rsqrtf(r2) : 0.f;
+                        const float4 q0 = Sq[j][0], q1 = Sq[j][1];
+                        far[0] = fmaf(q0.x, ri, far[0]); far[1] = fmaf(q0.y, ri, far[1]);
+                        far[2] = fmaf(q0.z, ri, far[2]); far[3] = fmaf(q0.w, ri, far[3]);
+                        far[4] = fmaf(q1.x, ri, far[4]); far[5] = fmaf(q1.y, ri, far[5]);
                     }
                 }
             }
         }
-        if (do_near && act) {
-            for (int64_t j = nptr[ti] + half; j < nptr[ti + 1]; j += 2) {
-                const float v = nval[j];
-                const int64_t c = ncol[j];
-                const float4 q0 = reinterpret_cast<const float4*>(xq + 8 * c)[0];
-                const float2 q1 = reinterpret_cast<const float2*>(xq + 8 * c)[2];
-                nr[0] += v * q0.x; nr[1] += v * q0.y; nr[2] += v * q0.z;
-                nr[3] += v * q0.w; nr[4] += v * q1.x; nr[5] += v * q1.y;
-            }
-        }
         __syncthreads();
-        if (half == 1) {
 #pragma unroll
-            for (int r = 0; r < 6; ++r) { Red[lane][r] = far[r]; Red[lane][6 + r] = nr[r]; }
-        }
+        for (int r = 0; r < 6; ++r) Red[tid][r] = far[r];
         __syncthreads();
-        if (half == 0 && act) {
+        if (tid < nt) {
             float tot[6];
 #pragma unroll
-            for (int r = 0; r < 6; ++r) tot[r] = (far[r] + Red[lane][r]) * invW + (nr[r] + Red[lane][6 + r]);
+            for (int r = 0; r < 6; ++r) {
+                float f = 0.f;
+                for (int gg = 0; gg < G; ++gg) f += Red[tid + gg * nt][r];
+                tot[r] = f * invW;
+            }
+            if (accumulate) {
+                const float2 a = y[ti], c = y[n + ti], d = y[2 * n + ti];
+                tot[0] += a.x; tot[1] += a.y; tot[2] += c.x; tot[3] += c.y; tot[4] += d.x; tot[5] += d.y;
+            }
             y[ti] = make_float2(tot[0], tot[1]);
             y[n + ti] = make_float2(tot[2], tot[3]);
             y[2 * n + ti] = make_float2(tot[4], tot[5]);
         }
     }
+}
+
+// ------------------------------------------------------------------ L2P + M2P
+// One thread per target panel: y += (1/W) [ (1/s_b) sum ell_b Rt(u) + sum_{w in W(b)} (1/s_w) sum c mu_w It(u_w) ].
+__global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, const int32_t* __restrict__ panel_leaf,
+                                                 const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
+                                                 const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
+                                                 const int64_t* __restrict__ wptr, const int32_t* __restrict__ wsrc,
+                                                 const float4* __restrict__ loc, const float* __restrict__ mu,
+                                                 const float* __restrict__ ell, float invW, float2* __restrict__ y)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int b = panel_leaf[i];
+    const int lb = level[b];
+    const float3 cb = box_center(lb, ix[b], iy[b], iz[b]);
+    const float inv_sb = ldexpf(1.f, lb);
+    const float4 tp = loc[i];
+    float far[6] = {0, 0, 0, 0, 0, 0};
+    {
+        float h[kNC];
+        regular_harmonics<kP>(tp.x * inv_sb, tp.y * inv_sb, tp.z * inv_sb, c_tab, h);
+        const float2* L = reinterpret_cast<const float2*>(ell + (size_t)b * kBoxStride);
+#pragma unroll
+        for (int k = 0; k < kNC; ++k) {
+            const float2 l0 = __ldg(L + 3 * k), l1 = __ldg(L + 3 * k + 1), l2 = __ldg(L + 3 * k + 2);
+            far[0] = fmaf(l0.x, h[k], far[0]); far[1] = fmaf(l0.y, h[k], far[1]);
+            far[2] = fmaf(l1.x, h[k], far[2]); far[3] = fmaf(l1.y, h[k], far[3]);
+            far[4] = fmaf(l2.x, h[k], far[4]); far[5] = fmaf(l2.y, h[k], far[5]);
+        }
+#pragma unroll
+        for (int r = 0; r < 6; ++r) far[r] *= inv_sb;
+    }
+    for (int64_t wj = wptr[b]; wj < wptr[b + 1]; ++wj) {
+        const int w = wsrc[wj];
+        const int lw = level[w];
+        const float3 cw = box_center(lw, ix[w], iy[w], iz[w]);
+        const float inv_sw = ldexpf(1.f, lw);
+        float h[kNC];
+        irregular_harmonics<kP>((tp.x + cb.x - cw.x) * inv_sw, (tp.y + cb.y - cw.y) * inv_sw,
+                                (tp.z + cb.z - cw.z) * inv_sw, c_tab, h);
+        const float2* M = reinterpret_cast<const float2*>(mu + (size_t)w * kBoxStride);
+        float a[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < kNC; ++k) {
+            const float hk = (degree_of(k) * degree_of(k) == k) ? h[k] : 2.f * h[k];
+            const float2 m0 = __ldg(M + 3 * k), m1 = __ldg(M + 3 * k + 1), m2 = __ldg(M + 3 * k + 2);
+            a[0] = fmaf(m0.x, hk, a[0]); a[1] = fmaf(m0.y, hk, a[1]);
+            a[2] = fmaf(m1.x, hk, a[2]); a[3] = fmaf(m1.y, hk, a[3]);
+            a[4] = fmaf(m2.x, hk, a[4]); a[5] = fmaf(m2.y, hk, a[5]);
+        }
+#pragma unroll
+        for (int r = 0; r < 6; ++r) far[r] = fmaf(a[r], inv_sw, far[r]);
+    }
+    float2 a = y[i], c = y[n + i], d = y[2 * n + i];
+    y[i] = make_float2(fmaf(far[0], invW, a.x), fmaf(far[1], invW, a.y));
+    y[n + i] = make_float2(fmaf(far[2], invW, c.x), fmaf(far[3], invW, c.y));
+    y[2 * n + i] = make_float2(fmaf(far[4], invW, d.x), fmaf(far[5], invW, d.y));
 }
 
 __global__ void k_permute(int64_t n, int nvec, const int32_t* __restrict__ idx, const float2* __restrict__ in,
@@ -474,6 +585,7 @@ void upload_constants(xrl_ctx ctx)
     upload_padded(ctx->ops.m2l, ops.m2l, kNM2L);
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kM2LSmem));
+    XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
 }
 
 }  // namespace xrl
@@ -481,26 +593,48 @@ void upload_constants(xrl_ctx ctx)
 static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags)
 {
     xrl_ctx ctx = t->ctx;
-    cudaStream_t st = ctx->stream;
+    cudaStream_t st = ctx->stream, side = ctx->side;
     const int64_t n = t->n;
     const bool do_far = flags != XRL_MVM_NEAR_ONLY;
     const bool do_near = flags != XRL_MVM_FAR_ONLY;
+    const float invW = (float)(1.0 / t->W);
     cudaEvent_t ev;
 
-    phase_begin(ctx, PH_PACK, &ev);
+    phase_begin(ctx, PH_PACK, &ev, st);
     k_pack<<<nblk(n, 256), 256, 0, st>>>(n, x, t->xq.p);
     XRL_LAUNCH_CHECK();
     ctx->launches += 1;
-    phase_end(ctx, PH_PACK, ev);
+    phase_end(ctx, PH_PACK, ev, st);
+
+    // fork: near SpMV and P2P depend only on the packed charges -> side stream,
+    // overlapping the upward pass and the M2L on the main stream.
+    XRL_CUDA(cudaEventRecord(ctx->ev_fork, st));
+    XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+    if (do_near) {
+        phase_begin(ctx, PH_NEAR, &ev, side);
+        k_near_spmv<<<nblk(8 * n, 256), 256, 0, side>>>(n, nr->row_ptr.p, nr->col.p, nr->val.p, t->xq.p, y);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+        phase_end(ctx, PH_NEAR, ev, side);
+    }
+    if (do_far) {
+        phase_begin(ctx, PH_P2P, &ev, side);
+        k_p2p<<<t->nleaf, 128, 0, side>>>(t->leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p, t->bpe.p,
+                                          t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW, do_near ? 1 : 0, n, y);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+        phase_end(ctx, PH_P2P, ev, side);
+    }
+    XRL_CUDA(cudaEventRecord(ctx->ev_join, side));
 
     if (do_far && t->nlevel > 1) {
-        phase_begin(ctx, PH_P2M, &ev);
+        phase_begin(ctx, PH_P2M, &ev, st);
         k_p2m<<<t->nleaf, 128, 0, st>>>(t->leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p, t->xq.p, t->mu.p);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
-        phase_end(ctx, PH_P2M, ev);
+        phase_end(ctx, PH_P2M, ev, st);
 
-        phase_begin(ctx, PH_M2M, &ev);
+        phase_begin(ctx, PH_M2M, &ev, st);
         for (int l = t->nlevel - 2; l >= 2; --l) {
             const int np = t->par_start[l + 1] - t->par_start[l];
             if (np == 0) continue;
@@ -509,9 +643,9 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
-        phase_end(ctx, PH_M2M, ev);
+        phase_end(ctx, PH_M2M, ev, st);
 
-        phase_begin(ctx, PH_M2L, &ev);
+        phase_begin(ctx, PH_M2L, &ev, st);
         XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), st));
         if (t->n_m2l_tiles > 0) {
             k_m2l<<<t->n_m2l_tiles, 256, kM2LSmem, st>>>(t->m2l_tiles.p, t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l.p,
@@ -519,37 +653,37 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
-        phase_end(ctx, PH_M2L, ev);
+        phase_end(ctx, PH_M2L, ev, st);
 
-        phase_begin(ctx, PH_P2L, &ev);
+        phase_begin(ctx, PH_P2L, &ev, st);
         if (t->n_x_targets > 0) {
-            k_p2l<<<t->n_x_targets, 128, 0, st>>>(t->x_targets.p, t->x_ptr.p, t->x_src.p, t->blevel.p, t->bix.p,
-                                                  t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->loc.p, t->xq.p, t->ell.p);
+            k_p2l<<<t->n_x_targets, 128, kP2LSmem, st>>>(t->x_targets.p, t->x_ptr.p, t->x_src.p, t->blevel.p, t->bix.p,
+                                                         t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->loc.p, t->xq.p,
+                                                         t->ell.p);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
-        phase_end(ctx, PH_P2L, ev);
+        phase_end(ctx, PH_P2L, ev, st);
 
-        phase_begin(ctx, PH_L2L, &ev);
+        phase_begin(ctx, PH_L2L, &ev, st);
         for (int l = 3; l < t->nlevel; ++l) {
             const int b0 = t->lvl_start[l], nb = t->lvl_start[l + 1] - b0;
             k_l2l<<<nb, 128, 0, st>>>(b0, t->bparent.p, t->bix.p, t->biy.p, t->biz.p, ctx->ops.l2l.p, t->ell.p);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
-        phase_end(ctx, PH_L2L, ev);
-    } else if (do_far) {
-        XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), st));
+        phase_end(ctx, PH_L2L, ev, st);
     }
-
-    phase_begin(ctx, PH_LEAF, &ev);
-    k_leaf<<<t->nleaf, 128, 0, st>>>(t->leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p, t->bpe.p,
-                                     t->u_ptr.p, t->u_src.p, t->w_ptr.p, t->w_src.p, t->loc.p, t->xq.p, t->mu.p,
-                                     t->ell.p, nr->row_ptr.p, nr->col.p, nr->val.p, (float)(1.0 / t->W),
-                                     do_far ? 1 : 0, do_near ? 1 : 0, n, y);
-    XRL_LAUNCH_CHECK();
-    ctx->launches += 1;
-    phase_end(ctx, PH_LEAF, ev);
+    // join, then the local-expansion / W-list evaluation completes y
+    XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    if (do_far && t->nlevel > 1) {
+        phase_begin(ctx, PH_L2P, &ev, st);
+        k_l2p_m2p<<<nblk(n, 128), 128, 0, st>>>(n, t->panel_leaf.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
+                                                t->w_ptr.p, t->w_src.p, t->loc.p, t->mu.p, t->ell.p, invW, y);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+        phase_end(ctx, PH_L2P, ev, st);
+    }
 }
 
 extern "C" {

@@ -84,7 +84,8 @@ XRL_HD void regular_harmonics(T x, T y, T z, const Tab& tab, T* h)
         if (m == 0) h[0] = cr;
         else { h[hidx(m, m)] = cr; h[hidx(m, m) + 1] = ci; }
 #pragma unroll
-        for (int n = m + 1; n <= P; ++n) {
+        for (int n = 1; n <= P; ++n) {
+            if (n <= m) continue;
             const T a = tab.A[n * (P + 1) + m] * z;
             const T b = tab.B[n * (P + 1) + m] * r2;
             const T nr = a * pr - b * qr;
@@ -116,7 +117,8 @@ XRL_HD void irregular_harmonics(T x, T y, T z, const Tab& tab, T* h)
         if (m == 0) h[0] = cr;
         else { h[hidx(m, m)] = cr; h[hidx(m, m) + 1] = ci; }
 #pragma unroll
-        for (int n = m + 1; n <= P; ++n) {
+        for (int n = 1; n <= P; ++n) {
+            if (n <= m) continue;
             const T a = tab.A[n * (P + 1) + m] * z;
             const T b = tab.B[n * (P + 1) + m];
             const T nr = (a * pr - b * qr) * ir2;

@@ -194,6 +194,7 @@ static xrl_status near_impl(xrl_tree t, double eta, xrl_near* out)
                                               N->val.p, N->val64.p);
     XRL_LAUNCH_CHECK();
     XRL_CUDA(cudaStreamSynchronize(st));
+    ++t->refs;
     *out = N.release();
     return XRL_OK;
 }
@@ -219,9 +220,12 @@ xrl_status xrl_near_assemble(xrl_tree t, const xrl_near_opts* opts, xrl_near* ou
 void xrl_near_destroy(xrl_near nr)
 {
     if (!nr) return;
-    cudaSetDevice(nr->tree->ctx->device);
-    cudaStreamSynchronize(nr->tree->ctx->stream);
+    xrl_tree t = nr->tree;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
     delete nr;
+    --t->refs;
+    tree_release(t);
 }
 
 xrl_status xrl_near_export(xrl_near nr, int64_t* row_ptr, int32_t* col, float* val32, double* val64, int64_t* nnz)

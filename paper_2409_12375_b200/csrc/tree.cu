@@ -197,6 +197,7 @@ __global__ void k_split_emit(int nb, int base, int next_base, const int32_t* __r
 // ----------------------------------------------------------------- K5 lists
 constexpr int kMaxColl = 26;
 constexpr int kMaxAdj = 26;
+constexpr int kM2LChunk = 4096;   // target boxes per M2L tile chunk (L2 locality)
 
 struct BoxView {
     const int32_t *level, *ix, *iy, *iz, *child, *nchild;
@@ -257,11 +258,22 @@ __global__ void k_lists_level(int b0, int b1, BoxView bv, const int32_t* __restr
     nX[b] = cx;
 }
 
+// Emits V pairs (keyed for the M2L tile order) and classifies every X pair
+// (b <- L, L a coarser leaf not adjacent to b, parent(b) adjacent to L) and
+// its W dual (L <- b):
+//   X kept as P2L only if b is not a leaf, else direct P2P (b <- L);
+//   W kept as M2P only if b holds more than kWDirect panels, else P2P (L <- b).
+// Direct evaluation is exact and cheaper than the expansion for small boxes.
+// Unused slots hold kSent and sort to the end.
+constexpr uint64_t kSent = ~0ull;
+constexpr int kWDirect = 96;
+
 __global__ void k_lists_emit(int nbox, BoxView bv, const int32_t* __restrict__ parent, const int32_t* __restrict__ coll,
                              const int32_t* __restrict__ ncoll, const int32_t* __restrict__ adjc,
                              const int32_t* __restrict__ nadjc, const int64_t* __restrict__ vptr,
-                             const int64_t* __restrict__ xptr, int32_t* vsrc, uint64_t* vkey, int32_t* xsrc,
-                             uint64_t* xkey_w, const int* __restrict__ m2l_index)
+                             const int64_t* __restrict__ xptr, const int32_t* __restrict__ pb,
+                             const int32_t* __restrict__ pe, int32_t* vsrc, uint64_t* vkey, uint64_t* xkey,
+                             uint64_t* wkey, uint64_t* ukx, uint64_t* ukw, const int* __restrict__ m2l_index)
 {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nbox || b == 0) return;
@@ -277,18 +289,35 @@ __global__ void k_lists_emit(int nbox, BoxView bv, const int32_t* __restrict__ p
             if (abs(dx) <= 1 && abs(dy) <= 1 && abs(dz) <= 1) continue;
             int off = m2l_index[(dx + 3) * 49 + (dy + 3) * 7 + (dz + 3)];
             vsrc[pv] = c;
-            vkey[pv] = ((uint64_t)(uint32_t)off << 32) | (uint32_t)b;
+            vkey[pv] = ((uint64_t)(b / kM2LChunk) << 41) | ((uint64_t)(uint32_t)off << 32) | (uint32_t)b;
             ++pv;
         }
     }
+    const bool b_leaf = bv.child[b] < 0;
+    const bool b_big = pe[b] - pb[b] > kWDirect;
     for (int qi = 0; qi < nadjc[P] + ncoll[P]; ++qi) {
         int L = qi < nadjc[P] ? adjc[kMaxAdj * P + qi] : coll[kMaxColl * P + (qi - nadjc[P])];
         if (bv.child[L] >= 0) continue;
         if (adjacent_fine(x, y, z, lb, bv.ix[L], bv.iy[L], bv.iz[L], bv.level[L])) continue;
-        xsrc[px] = L;
-        xkey_w[px] = ((uint64_t)(uint32_t)L << 32) | (uint32_t)b;  // for W = X^T
+        const uint64_t bl = ((uint64_t)(uint32_t)b << 32) | (uint32_t)L;
+        const uint64_t lbk = ((uint64_t)(uint32_t)L << 32) | (uint32_t)b;
+        xkey[px] = b_leaf ? kSent : bl;
+        ukx[px] = b_leaf ? bl : kSent;
+        wkey[px] = b_big ? lbk : kSent;
+        ukw[px] = b_big ? kSent : lbk;
         ++px;
     }
+}
+
+__global__ void k_count_valid(int64_t n, const uint64_t* __restrict__ key, int64_t* out)
+{
+    // keys sorted ascending, sentinels last: out = first index holding kSent
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (key[mid] == kSent) hi = mid; else lo = mid + 1;
+    }
+    *out = lo;
 }
 
 // U pairs: per leaf b: self, leaf colleagues, coarse adjacent leaves (b <- L) and the reverse (L <- b).
@@ -432,6 +461,12 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     XRL_CUDA(cudaSetDevice(ctx->device));
     auto T = std::make_unique<xrl_tree_s>();
     T->ctx = ctx;
+    struct CtxRef {
+        xrl_ctx c;
+        bool keep = false;
+        ~CtxRef() { if (!keep) --c->refs; }
+    } cref{ctx};
+    ++ctx->refs;
     T->n = n;
     T->leaf_max = opts ? opts->leaf_max : 64;
     T->max_depth = opts ? opts->max_depth : kMortonBits;
@@ -629,14 +664,41 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         return hp2[rows];
     };
     T->nv = counts_to_ptr(nV.p, T->v_ptr, nbox);
-    T->nx = counts_to_ptr(nX.p, T->x_ptr, nbox);
+    DBuf<int64_t> xcand_ptr;
+    const int64_t nxc = counts_to_ptr(nX.p, xcand_ptr, nbox);  // X candidates (before classification)
     T->v_src.alloc(std::max<int64_t>(1, T->nv));
-    T->x_src.alloc(std::max<int64_t>(1, T->nx));
-    DBuf<uint64_t> vkey(std::max<int64_t>(1, T->nv)), wkey(std::max<int64_t>(1, T->nx));
+    DBuf<uint64_t> vkey(std::max<int64_t>(1, T->nv)), xkey(std::max<int64_t>(1, nxc)), wkey(std::max<int64_t>(1, nxc));
+    DBuf<uint64_t> ukx(std::max<int64_t>(1, nxc)), ukw(std::max<int64_t>(1, nxc));
     k_lists_emit<<<nblk(nbox, 128), 128, 0, st>>>(nbox, bv, T->bparent.p, coll.p, ncoll.p, adjc.p, nadjc.p,
-                                                  T->v_ptr.p, T->x_ptr.p, T->v_src.p, vkey.p, T->x_src.p, wkey.p,
-                                                  m2l_index.p);
+                                                  T->v_ptr.p, xcand_ptr.p, T->bpb.p, T->bpe.p, T->v_src.p, vkey.p,
+                                                  xkey.p, wkey.p, ukx.p, ukw.p, m2l_index.p);
     XRL_LAUNCH_CHECK();
+    DBuf<int64_t> dcount(1);
+    auto sort_valid = [&](DBuf<uint64_t>& k, int64_t cnt) -> int64_t {
+        if (cnt == 0) return 0;
+        sort_pairs<uint64_t, int32_t>(k.p, nullptr, cnt, 64, st);
+        k_count_valid<<<1, 1, 0, st>>>(cnt, k.p, dcount.p);
+        XRL_LAUNCH_CHECK();
+        int64_t h = 0;
+        XRL_CUDA(cudaMemcpyAsync(&h, dcount.p, 8, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        return h;
+    };
+    auto keys_to_csr = [&](const uint64_t* k, int64_t cnt, DBuf<int64_t>& ptr, DBuf<int32_t>& src) {
+        ptr.alloc(nbox + 1);
+        src.alloc(std::max<int64_t>(1, cnt));
+        if (cnt == 0) { XRL_CUDA(cudaMemsetAsync(ptr.p, 0, 8 * (nbox + 1), st)); return; }
+        DBuf<int32_t> tg(cnt);
+        k_split_keys<<<nblk(cnt, 256), 256, 0, st>>>(cnt, k, tg.p, src.p);
+        k_csr_ptr<<<nblk(cnt + 1, 256), 256, 0, st>>>(cnt, tg.p, nbox, ptr.p);
+        XRL_LAUNCH_CHECK();
+        XRL_CUDA(cudaStreamSynchronize(st));
+    };
+    T->nx = sort_valid(xkey, nxc);
+    keys_to_csr(xkey.p, T->nx, T->x_ptr, T->x_src);
+    T->nw = sort_valid(wkey, nxc);
+    keys_to_csr(wkey.p, T->nw, T->w_ptr, T->w_src);
+    const int64_t nukx = sort_valid(ukx, nxc), nukw = sort_valid(ukw, nxc);
 
     // M2L pairs sorted by (offset, target)
     T->m2l_tgt.alloc(std::max<int64_t>(1, T->nv));
@@ -653,12 +715,13 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         if (T->nv) XRL_CUDA(cudaMemcpyAsync(ho.data(), offs.p, 4 * T->nv, cudaMemcpyDeviceToHost, st));
         XRL_CUDA(cudaStreamSynchronize(st));
         std::vector<int4> tiles;
-        const int TP = 32;
+        const int TP = 16;
         int64_t i = 0;
         while (i < T->nv) {
             int64_t j = i;
-            while (j < T->nv && ho[j] == ho[i]) ++j;
-            for (int64_t s = i; s < j; s += TP) tiles.push_back(make_int4(ho[i], (int)s, (int)std::min<int64_t>(TP, j - s), 0));
+            while (j < T->nv && ho[j] == ho[i]) ++j;  // same (chunk, offset)
+            for (int64_t s = i; s < j; s += TP)
+                tiles.push_back(make_int4(ho[i] & 511, (int)s, (int)std::min<int64_t>(TP, j - s), ho[i] >> 9));
             i = j;
         }
         T->n_m2l_tiles = (int)tiles.size();
@@ -666,30 +729,17 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         if (!tiles.empty())
             XRL_CUDA(cudaMemcpyAsync(T->m2l_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
     }
-    // X targets
+    // X targets (boxes with kept P2L pairs)
     {
-        std::vector<int32_t> hx(nbox);
-        XRL_CUDA(cudaMemcpyAsync(hx.data(), nX.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+        std::vector<int64_t> hx(nbox + 1);
+        XRL_CUDA(cudaMemcpyAsync(hx.data(), T->x_ptr.p, 8 * (nbox + 1), cudaMemcpyDeviceToHost, st));
         XRL_CUDA(cudaStreamSynchronize(st));
         std::vector<int32_t> xt;
         for (int b = 0; b < nbox; ++b)
-            if (hx[b] > 0) xt.push_back(b);
+            if (hx[b + 1] > hx[b]) xt.push_back(b);
         T->n_x_targets = (int)xt.size();
         T->x_targets.alloc(std::max<size_t>(1, xt.size()));
         if (!xt.empty()) XRL_CUDA(cudaMemcpyAsync(T->x_targets.p, xt.data(), 4 * xt.size(), cudaMemcpyHostToDevice, st));
-    }
-    // W = X transposed, CSR by leaf
-    T->nw = T->nx;
-    T->w_src.alloc(std::max<int64_t>(1, T->nw));
-    T->w_ptr.alloc(nbox + 1);
-    if (T->nw) {
-        sort_pairs<uint64_t, int32_t>(wkey.p, nullptr, T->nw, 64, st);
-        DBuf<int32_t> wt(T->nw);
-        k_split_keys<<<nblk(T->nw, 256), 256, 0, st>>>(T->nw, wkey.p, wt.p, T->w_src.p);
-        k_csr_ptr<<<nblk(T->nw + 1, 256), 256, 0, st>>>(T->nw, wt.p, nbox, T->w_ptr.p);
-        XRL_LAUNCH_CHECK();
-    } else {
-        XRL_CUDA(cudaMemsetAsync(T->w_ptr.p, 0, 8 * (nbox + 1), st));
     }
     // U lists
     {
@@ -701,10 +751,13 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         XRL_CUDA(cudaMemcpyAsync(&lc, ucnt.p + nbox - 1, 8, cudaMemcpyDeviceToHost, st));
         XRL_CUDA(cudaMemcpyAsync(&lo_, uoff.p + nbox - 1, 8, cudaMemcpyDeviceToHost, st));
         XRL_CUDA(cudaStreamSynchronize(st));
-        T->nu = lc + lo_;
+        const int64_t nadj = lc + lo_;
+        T->nu = nadj + nukx + nukw;
         DBuf<uint64_t> ukey(T->nu);
         k_u_emit<<<nblk(nbox, 128), 128, 0, st>>>(nbox, T->bchild.p, coll.p, ncoll.p, adjc.p, nadjc.p, uoff.p, ukey.p);
         XRL_LAUNCH_CHECK();
+        if (nukx) XRL_CUDA(cudaMemcpyAsync(ukey.p + nadj, ukx.p, 8 * nukx, cudaMemcpyDeviceToDevice, st));
+        if (nukw) XRL_CUDA(cudaMemcpyAsync(ukey.p + nadj + nukx, ukw.p, 8 * nukw, cudaMemcpyDeviceToDevice, st));
         sort_pairs<uint64_t, int32_t>(ukey.p, nullptr, T->nu, 64, st);
         DBuf<int32_t> ut(T->nu);
         T->u_src.alloc(T->nu);
@@ -729,8 +782,20 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     XRL_CUDA(cudaMemsetAsync(T->mu.p, 0, T->mu.bytes(), st));
     XRL_CUDA(cudaMemsetAsync(T->xq.p, 0, T->xq.bytes(), st));
     XRL_CUDA(cudaStreamSynchronize(st));
+    cref.keep = true;
     *out = T.release();
     return XRL_OK;
+}
+
+void xrl::tree_release(xrl_tree t)
+{
+    if (!t->dead || t->refs > 0) return;
+    xrl_ctx ctx = t->ctx;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    delete t;
+    --ctx->refs;
+    ctx_release(ctx);
 }
 
 extern "C" {
@@ -759,9 +824,8 @@ xrl_status xrl_tree_build(xrl_ctx ctx, int64_t n_vert, const double* vert, int64
 void xrl_tree_destroy(xrl_tree t)
 {
     if (!t) return;
-    cudaSetDevice(t->ctx->device);
-    cudaStreamSynchronize(t->ctx->stream);
-    delete t;
+    t->dead = true;
+    tree_release(t);
 }
 
 xrl_status xrl_tree_info(xrl_tree t, xrl_tree_info_t* info)

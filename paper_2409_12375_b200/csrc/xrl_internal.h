@@ -61,7 +61,7 @@ struct DBuf {
     size_t bytes() const { return n * sizeof(T); }
 };
 
-enum Phase { PH_PACK = 0, PH_P2M, PH_M2M, PH_M2L, PH_P2L, PH_L2L, PH_LEAF, PH_COUNT };
+enum Phase { PH_PACK = 0, PH_P2M, PH_M2M, PH_M2L, PH_P2L, PH_L2L, PH_L2P, PH_P2P, PH_NEAR, PH_COUNT };
 
 struct DeviceOperators {
     DBuf<float> m2m;   // [8][kNC (k, input)][kNCP (i, output, padded)]
@@ -78,12 +78,16 @@ constexpr int kBoxStride = 728;      // floats per box expansion (121*6 padded t
 struct xrl_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;      // library-owned side stream (near SpMV, P2P)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool own_stream = false;
     int rank = 0, world = 1;
     xrl::DeviceOperators ops;
     // timing
     bool timing = false;
     int64_t launches = 0;
+    int refs = 0;         // live trees
+    bool dead = false;    // destroy requested
     double phase_ms[xrl::PH_COUNT] = {};
     int64_t phase_launches[xrl::PH_COUNT] = {};
     cudaEvent_t ev[2 * xrl::PH_COUNT] = {};
@@ -93,6 +97,8 @@ struct xrl_ctx_s {
 
 struct xrl_tree_s {
     xrl_ctx ctx = nullptr;
+    int refs = 0;         // live near handles
+    bool dead = false;
     int64_t n = 0;
     int32_t leaf_max = 64, max_depth = 21;
     double lo[3] = {0, 0, 0};   // root cube corner
@@ -144,7 +150,9 @@ struct xrl_near_s {
 
 namespace xrl {
 // phase timing helpers (no-ops unless enabled)
-void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb);
-void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb);
+void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb, cudaStream_t st);
+void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb, cudaStream_t st);
 void upload_constants(xrl_ctx ctx);
+void ctx_release(xrl_ctx ctx);     // delete if dead and unreferenced
+void tree_release(xrl_tree t);
 }  // namespace xrl

@@ -246,6 +246,11 @@ class Near:
         check(lib().xrl_near_assemble(tree.h, ctypes.byref(NearOpts(eta)), ctypes.byref(h)))
         self.h = h
 
+    def nnz(self) -> int:
+        nnz = ctypes.c_int64()
+        check(lib().xrl_near_export(self.h, None, None, None, None, ctypes.byref(nnz)))
+        return int(nnz.value)
+
     def export(self):
         nnz = ctypes.c_int64()
         check(lib().xrl_near_export(self.h, None, None, None, None, ctypes.byref(nnz)))

@@ -62,4 +62,4 @@ def test_argument_errors_are_synchronous(libxrl):
     assert libxrl.xrl_mvm(None, None, None, None, 3, 0) == -1
     assert libxrl.xrl_tree_info(None, None) == -1
     assert libxrl.xrl_near_assemble(None, None, None) == -1
-    assert libxrl.xrl_timing_count() == 7
+    assert libxrl.xrl_timing_count() == 9

@@ -1,0 +1,29 @@
+"""Summarise an ncu report: python tools/ncu_summary.py rep.ncu-rep [out.json]"""
+import csv, io, json, subprocess, sys
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h = rows[0]
+want = ["Kernel Name", "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__registers_per_thread", "launch__grid_size",
+        "smsp__average_warp_latency_per_inst_issued.ratio", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__sass_thread_inst_executed_op_ffma_pred_on.sum", "sm__sass_thread_inst_executed_op_fadd_pred_on.sum",
+        "sm__sass_thread_inst_executed_op_fmul_pred_on.sum", "lts__t_sectors_srcunit_tex_op_red.sum"]
+stall = [k for k in h if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio")]
+out = []
+for r in rows[2:]:
+    d = {}
+    for w in want + stall:
+        if w in h:
+            d[w] = r[h.index(w)]
+    st = sorted(((float(d[k]) if d[k] else 0.0, k) for k in stall), reverse=True)[:5]
+    d = {k: v for k, v in d.items() if k not in stall}
+    d["top_stalls"] = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""): v for v, k in st}
+    out.append(d)
+for d in out:
+    print(json.dumps(d, indent=1))
+if len(sys.argv) > 2:
+    json.dump(out, open(sys.argv[2], "w"), indent=1)
