@@ -184,6 +184,107 @@ xrl_status xrl_timing_reset(xrl_ctx ctx);
  * points; used to report gpu_launches of a timed region). */
 int64_t xrl_launch_count(xrl_ctx ctx);
 
+
+/* ------------------------------------------------------------------------
+ * Loop-space operator, diagonal-of-P preconditioner and GMRES
+ * ------------------------------------------------------------------------ */
+typedef struct xrl_topo_s* xrl_topo;
+typedef struct xrl_op_s* xrl_op;
+typedef struct xrl_precond_s* xrl_precond;
+
+/* A port: two terminal panel sets (panel ids in the mesh's original order).
+ * Each terminal is a super-node tied to its panels by zero-impedance
+ * branches; the port branch carries the source (SPEC.md:52-55 convention;
+ * PAPER.md:90 V_edge = phi_i - phi_j on the excited branch). */
+typedef struct {
+    int32_t n_plus, n_minus;
+    const int32_t* plus;
+    const int32_t* minus;
+} xrl_port;
+
+typedef struct {
+    int64_t n_panels, n_edges, n_branches, n_loops;
+    int32_t n_ports, n_components;
+    int64_t n_vertex_loops, n_fundamental_loops, n_terminal_loops;
+    int64_t nnz_m, nnz_c;
+} xrl_topo_info_t;
+
+/* PEEC graph and loop basis (host, setup).  Edges: panels sharing an edge,
+ * reference direction from the lower to the higher library index.  CM maps
+ * A_t (Alg. 1): A_t(e,i) = (m_e - c_i)_t, A_t(e,j) = (c_j - m_e)_t.
+ * Loop matrix M (Eq. 7) from local vertex loops (fundamental
+ * cycles if those do not span the cycle space), terminal loops and one port
+ * loop per port.  Errors: XRL_EGEOM (non-manifold edge, disconnected
+ * terminals), XRL_EINVAL. */
+xrl_status xrl_topology_build(xrl_tree tree, int32_t n_ports, const xrl_port* ports, xrl_topo* out);
+xrl_status xrl_topology_info(xrl_topo topo, xrl_topo_info_t* info);
+/* Host export for tests (any pointer may be NULL).  branch_nodes int32
+ * [n_branches][2] (panel ids in mesh order, or -1-s for super-node s);
+ * branch_kind int8 (0 edge, 1 terminal, 2 port); edge_mid double [n_edges][3];
+ * M as CSR over loops: m_ptr int64 [n_loops+1], m_branch int32, m_sign int8;
+ * port_loop int32 [n_ports]; loop_kind int8 (0 vertex, 1 fundamental,
+ * 2 terminal, 3 port); C = M A (loop rows): c_ptr int64 [n_loops+1],
+ * c_panel int32 (mesh order), c_val double [nnz][3]. */
+xrl_status xrl_topology_export(xrl_topo topo, int32_t* branch_nodes, int8_t* branch_kind, double* edge_mid,
+                               int64_t* m_ptr, int32_t* m_branch, int8_t* m_sign, int32_t* port_loop,
+                               int8_t* loop_kind, int64_t* c_ptr, int32_t* c_panel, double* c_val);
+void xrl_topology_destroy(xrl_topo topo);
+
+/* Equivalent surface impedance, Sonnet double-plane model (Eq. 3)
+ * read as Z_s = (1+j) R_RF sqrt(f) / (1 - exp(-(1+j) R_RF sqrt(f)/R_DC)),
+ * R_DC = 2/(sigma zeta), R_RF = sqrt(pi mu0 / sigma) (reading R12);
+ * f = 0 gives the limit R_DC.  Host function. */
+xrl_status xrl_esi(double sigma, double zeta, double freq_hz, double* zs_re, double* zs_im);
+
+/* Loop-space operator at one frequency (Eq. 8-9):
+ *   A v = M sum_t A_t [ diag(Z_s/A) + alpha P ] A_t^T M^T v,  alpha = j omega mu0/(4 pi)
+ * applied as u_t = C_t^T v (C_t = M A_t), P u_t by xrl_mvm, w = sum_t C_t y_t.
+ * zs: per-panel complex Z_s (double [n][2], mesh order) or NULL to use
+ * xrl_esi(sigma, zeta, freq) for every panel.  Handles are borrowed. */
+xrl_status xrl_operator_create(xrl_tree tree, xrl_near near, xrl_topo topo, const double* zs, double sigma,
+                               double zeta, double freq_hz, xrl_op* out);
+/* w = A v; v, w device complex64 [nrhs][n_loops], must not alias. */
+xrl_status xrl_operator_apply(xrl_op op, const void* v, void* w, int32_t nrhs);
+void xrl_operator_destroy(xrl_op op);
+
+/* Diagonal-of-P preconditioner (Eq. 10-11) in block-Jacobi
+ * form (reading R13): Q = sum_t C_t diag(Z_s/A + alpha P_kk) C_t^T,
+ * loops cut into consecutive (Morton-ordered) blocks of <= block_size
+ * (<= 64), each diagonal block LU-inverted in FP64 and stored complex64.
+ * XRL_ESINGULAR if a pivot falls below 1e-13 of the block's largest entry. */
+xrl_status xrl_precond_build(xrl_op op, int32_t block_size, xrl_precond* out);
+/* z = blockdiag(Q)^-1 v; device complex64 [nrhs][n_loops]. */
+xrl_status xrl_precond_apply(xrl_precond pc, const void* v, void* z, int32_t nrhs);
+/* Host export of the block partition and the inverse blocks (tests):
+ * block_ptr int32 [n_blocks+1] (loop ranges), inv complex64 [n_blocks][bs][bs]
+ * (row-major, rows/cols beyond the block's size are 0). */
+xrl_status xrl_precond_export(xrl_precond pc, int32_t* n_blocks, int32_t* block_size, int32_t* block_ptr, void* inv);
+void xrl_precond_destroy(xrl_precond pc);
+
+/* Restarted GMRES (restart 50; relative residual 1e-4 above
+ * 1 MHz, 1e-6 at or below, reading C-A8), left-preconditioned (Eq. 11), one
+ * Krylov space per right-hand side, all columns stepping together so every
+ * operator call is batched.  CGS2 orthogonalisation; Hessenberg/Givens in FP64.
+ * tol <= 0 selects the paper's frequency rule.  b, x: device complex64
+ * [nrhs][n_loops] (x holds x0 on entry).  Per-column outputs (host, may be
+ * NULL): iters int32, rre double (preconditioned, as converged on),
+ * true_rre double (||b - A x|| / ||b||), converged int32.  Blocking; returns
+ * XRL_ENOCONV if any column did not converge. */
+typedef struct {
+    int32_t restart;
+    int32_t max_iters;
+    double tol;
+} xrl_gmres_opts;
+xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b, void* x, int32_t nrhs, const xrl_gmres_opts* opts,
+                     int32_t* iters, double* rre, double* true_rre, int32_t* converged);
+
+/* Port excitation V_l = M V_branch with `volts` on port `port`'s branch
+ * (device complex64 [n_loops], overwritten), and port currents read back from
+ * loop currents (I_port = current of the port branch = I_l of its loop):
+ * x device complex64 [nrhs][n_loops] -> i_ports host double [nrhs][n_ports][2]. */
+xrl_status xrl_port_rhs(xrl_topo topo, int32_t port, double volts, void* b);
+xrl_status xrl_port_currents(xrl_topo topo, const void* x, int32_t nrhs, double* i_ports);
+
 #ifdef __cplusplus
 }
 #endif

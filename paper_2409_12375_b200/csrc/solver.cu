@@ -1,0 +1,718 @@
+// Loop-space operator, diagonal-of-P block preconditioner, GMRES and port
+// excitation (Eq. 8-11).
+#include <cmath>
+#include <complex>
+
+#include "xrl_internal.h"
+
+using namespace xrl;
+
+namespace {
+
+constexpr double kMu0 = 4e-7 * M_PI;
+
+inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+
+// u[(3r+t)][k] = sum_{l} C_t(l,k) v[r][l]   (u_t = A_t^T M^T v, panel rows)
+__global__ void k_loops_to_panels(int64_t n, int64_t nl, int nrhs, const int64_t* __restrict__ ptr,
+                                  const int32_t* __restrict__ col, const float* __restrict__ val,
+                                  const float2* __restrict__ v, float2* __restrict__ u)
+{
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    for (int r = 0; r < nrhs; ++r) {
+        float2 a0 = {0, 0}, a1 = {0, 0}, a2 = {0, 0};
+        for (int64_t q = ptr[k]; q < ptr[k + 1]; ++q) {
+            const float2 x = v[(int64_t)r * nl + col[q]];
+            const float c0 = val[3 * q], c1 = val[3 * q + 1], c2 = val[3 * q + 2];
+            a0.x += c0 * x.x; a0.y += c0 * x.y;
+            a1.x += c1 * x.x; a1.y += c1 * x.y;
+            a2.x += c2 * x.x; a2.y += c2 * x.y;
+        }
+        u[(int64_t)(3 * r + 0) * n + k] = a0;
+        u[(int64_t)(3 * r + 1) * n + k] = a1;
+        u[(int64_t)(3 * r + 2) * n + k] = a2;
+    }
+}
+
+// w[r][l] = sum_t sum_k C_t(l,k) ( zsa_k u_t[k] + j alpha_im pu_t[k] )
+__global__ void k_panels_to_loops(int64_t n, int64_t nl, int nrhs, const int64_t* __restrict__ ptr,
+                                  const int32_t* __restrict__ col, const float* __restrict__ val,
+                                  const float2* __restrict__ zsa, float alpha_im, const float2* __restrict__ u,
+                                  const float2* __restrict__ pu, float2* __restrict__ w)
+{
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= nl) return;
+    for (int r = 0; r < nrhs; ++r) {
+        float2 acc = {0, 0};
+        for (int64_t q = ptr[l]; q < ptr[l + 1]; ++q) {
+            const int k = col[q];
+            const float2 z = zsa[k];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const float2 uu = u[(int64_t)(3 * r + t) * n + k];
+                const float2 pp = pu[(int64_t)(3 * r + t) * n + k];
+                const float2 y = make_float2(z.x * uu.x - z.y * uu.y - alpha_im * pp.y,
+                                             z.x * uu.y + z.y * uu.x + alpha_im * pp.x);
+                const float c = val[3 * q + t];
+                acc.x += c * y.x;
+                acc.y += c * y.y;
+            }
+        }
+        w[(int64_t)r * nl + l] = acc;
+    }
+}
+
+// ---------------------------------------------------------------- preconditioner
+// d_k = Z_s/A_k + j alpha P_kk (P_kk = diagonal of the near CSR, FP64).
+__global__ void k_diag_p(int64_t n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                         const double* __restrict__ val64, double* pkk)
+{
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double d = 0;
+    for (int64_t q = ptr[k]; q < ptr[k + 1]; ++q)
+        if (col[q] == k) d = val64[q];
+    pkk[k] = d;
+}
+
+constexpr int kBS = 64;
+
+// One CTA per block: assemble Q_BB = sum_k d_k c_a(k).c_b(k) (FP64 complex),
+// invert in place by Gauss-Jordan with partial pivoting, store transposed.
+__global__ void __launch_bounds__(256) k_block_inverse(const int32_t* __restrict__ bptr, const int64_t* __restrict__ clp,
+                                                       const int32_t* __restrict__ clc, const double* __restrict__ clv,
+                                                       const int64_t* __restrict__ cpp, const int32_t* __restrict__ cpc,
+                                                       const double2* __restrict__ dk, float2* __restrict__ inv,
+                                                       int* singular)
+{
+    extern __shared__ double2 Qsm[];
+    double2 (*Q)[kBS + 1] = reinterpret_cast<double2 (*)[kBS + 1]>(Qsm);
+    __shared__ int piv[kBS];
+    __shared__ double colmax[kBS];
+    __shared__ int pivrow;
+    __shared__ double qmax;
+    const int blk = blockIdx.x;
+    const int l0 = bptr[blk], m = bptr[blk + 1] - l0;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kBS * (kBS + 1); i += blockDim.x) (&Q[0][0])[i] = make_double2(0, 0);
+    __syncthreads();
+    // assembly: thread per row a
+    for (int a = tid; a < m; a += blockDim.x) {
+        const int la = l0 + a;
+        for (int64_t q = clp[la]; q < clp[la + 1]; ++q) {
+            const int k = clc[q];
+            const double ca0 = clv[3 * q], ca1 = clv[3 * q + 1], ca2 = clv[3 * q + 2];
+            const double2 d = dk[k];
+            for (int64_t q2 = cpp[k]; q2 < cpp[k + 1]; ++q2) {
+                const int lb = cpc[q2];
+                if (lb < l0 || lb >= l0 + m) continue;
+                // C value of (lb, k): find in lb's row (short rows)
+                double cb0 = 0, cb1 = 0, cb2 = 0;
+                for (int64_t q3 = clp[lb]; q3 < clp[lb + 1]; ++q3)
+                    if (clc[q3] == k) { cb0 = clv[3 * q3]; cb1 = clv[3 * q3 + 1]; cb2 = clv[3 * q3 + 2]; break; }
+                const double s = ca0 * cb0 + ca1 * cb1 + ca2 * cb2;
+                Q[a][lb - l0].x += d.x * s;
+                Q[a][lb - l0].y += d.y * s;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double mx = 0;
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < m; ++j) mx = fmax(mx, hypot(Q[i][j].x, Q[i][j].y));
+        qmax = mx;
+    }
+    __syncthreads();
+    // Gauss-Jordan in place
+    for (int k = 0; k < m; ++k) {
+        if (tid < m) colmax[tid] = (tid >= k) ? hypot(Q[tid][k].x, Q[tid][k].y) : -1.0;
+        __syncthreads();
+        if (tid == 0) {
+            int p = k;
+            for (int i = k + 1; i < m; ++i)
+                if (colmax[i] > colmax[p]) p = i;
+            pivrow = p;
+            piv[k] = p;
+            if (!(colmax[p] > 1e-13 * qmax)) atomicMax(singular, blk + 1);
+        }
+        __syncthreads();
+        const int p = pivrow;
+        if (p != k)
+            for (int j = tid; j < m; j += blockDim.x) { double2 t = Q[k][j]; Q[k][j] = Q[p][j]; Q[p][j] = t; }
+        __syncthreads();
+        const double2 pv = Q[k][k];
+        const double den = pv.x * pv.x + pv.y * pv.y;
+        const double2 ip = make_double2(pv.x / den, -pv.y / den);
+        __syncthreads();
+        // scale row k (with Q[k][k] := 1 before scaling -> becomes 1/pivot)
+        for (int j = tid; j < m; j += blockDim.x) {
+            const double2 v = (j == k) ? make_double2(1, 0) : Q[k][j];
+            Q[k][j] = make_double2(v.x * ip.x - v.y * ip.y, v.x * ip.y + v.y * ip.x);
+        }
+        __syncthreads();
+        // eliminate column k from the other rows
+        for (int idx = tid; idx < m * m; idx += blockDim.x) {
+            const int i = idx / m, j = idx % m;
+            if (i == k) continue;
+            const double2 f = Q[i][k];
+            if (j == k) continue;
+            const double2 r = Q[k][j];
+            Q[i][j].x -= f.x * r.x - f.y * r.y;
+            Q[i][j].y -= f.x * r.y + f.y * r.x;
+        }
+        __syncthreads();
+        for (int i = tid; i < m; i += blockDim.x) {
+            if (i == k) continue;
+            const double2 f = Q[i][k];
+            Q[i][k] = make_double2(-(f.x * ip.x - f.y * ip.y), -(f.x * ip.y + f.y * ip.x));
+        }
+        __syncthreads();
+    }
+    // undo the row interchanges as column interchanges, in reverse order
+    for (int k = m - 1; k >= 0; --k) {
+        const int p = piv[k];
+        if (p != k)
+            for (int i = tid; i < m; i += blockDim.x) { double2 t = Q[i][k]; Q[i][k] = Q[i][p]; Q[i][p] = t; }
+        __syncthreads();
+    }
+    // store transposed: inv[blk][b][a] = Q^-1[a][b]
+    float2* out = inv + (size_t)blk * kBS * kBS;
+    for (int idx = tid; idx < kBS * kBS; idx += blockDim.x) {
+        const int b = idx / kBS, a = idx % kBS;
+        out[idx] = (a < m && b < m) ? make_float2((float)Q[a][b].x, (float)Q[a][b].y) : make_float2(0.f, 0.f);
+    }
+}
+
+// z_B = inv_B v_B, thread per row, inverse stored column-major.
+__global__ void k_block_apply(int nl, int nrhs, const int32_t* __restrict__ bptr, const float2* __restrict__ inv,
+                              const float2* __restrict__ v, float2* __restrict__ z)
+{
+    __shared__ float2 vs[kBS];
+    const int blk = blockIdx.x;
+    const int l0 = bptr[blk], m = bptr[blk + 1] - l0;
+    const int a = threadIdx.x;
+    const float2* B = inv + (size_t)blk * kBS * kBS;
+    for (int r = 0; r < nrhs; ++r) {
+        __syncthreads();
+        if (a < m) vs[a] = v[(int64_t)r * nl + l0 + a];
+        __syncthreads();
+        if (a < m) {
+            float2 acc = {0, 0};
+            for (int b = 0; b < m; ++b) {
+                const float2 q = B[b * kBS + a];
+                acc.x += q.x * vs[b].x - q.y * vs[b].y;
+                acc.y += q.x * vs[b].y + q.y * vs[b].x;
+            }
+            z[(int64_t)r * nl + l0 + a] = acc;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- GMRES BLAS
+// h[r][i] = sum_x conj(V[r][i][x]) w[r][x], i < ni   (grid (ni, nrhs), FP64 accumulation)
+__global__ void k_gdots(int64_t nl, int ldv, const float2* __restrict__ V, const float2* __restrict__ w,
+                        double2* __restrict__ h, int ni)
+{
+    const int i = blockIdx.x, r = blockIdx.y;
+    const float2* vi = V + ((int64_t)r * ldv + i) * nl;
+    const float2* wr = w + (int64_t)r * nl;
+    double sx = 0, sy = 0;
+    for (int64_t x = threadIdx.x; x < nl; x += blockDim.x) {
+        const float2 a = vi[x], b = wr[x];
+        sx += (double)a.x * b.x + (double)a.y * b.y;
+        sy += (double)a.x * b.y - (double)a.y * b.x;
+    }
+    __shared__ double rx[256], ry[256];
+    rx[threadIdx.x] = sx;
+    ry[threadIdx.x] = sy;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) { rx[threadIdx.x] += rx[threadIdx.x + s]; ry[threadIdx.x] += ry[threadIdx.x + s]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) h[(int64_t)r * ni + i] = make_double2(rx[0], ry[0]);
+}
+
+// w[r][x] += sgn * sum_{i<ni} V[r][i][x] h[r][i]
+__global__ void k_gupdate(int64_t nl, int ldv, int nrhs, const float2* __restrict__ V, const double2* __restrict__ h,
+                          int ni, float sgn, float2* __restrict__ w)
+{
+    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (x >= nl) return;
+    for (int r = 0; r < nrhs; ++r) {
+        float ax = 0, ay = 0;
+        for (int i = 0; i < ni; ++i) {
+            const float2 v = V[((int64_t)r * ldv + i) * nl + x];
+            const double2 c = h[(int64_t)r * ni + i];
+            ax += v.x * (float)c.x - v.y * (float)c.y;
+            ay += v.x * (float)c.y + v.y * (float)c.x;
+        }
+        float2 o = w[(int64_t)r * nl + x];
+        o.x += sgn * ax;
+        o.y += sgn * ay;
+        w[(int64_t)r * nl + x] = o;
+    }
+}
+
+// out[r][x] = a[r][x] * s[r] (complex-real scale), s in FP64
+__global__ void k_gscale(int64_t nl, int nrhs, const float2* __restrict__ a, int64_t a_stride,
+                         const double* __restrict__ s, float2* __restrict__ out, int64_t o_stride)
+{
+    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (x >= nl) return;
+    for (int r = 0; r < nrhs; ++r) {
+        const float2 v = a[r * a_stride + x];
+        out[r * o_stride + x] = make_float2((float)(v.x * s[r]), (float)(v.y * s[r]));
+    }
+}
+
+// out = a - b
+__global__ void k_gsub(int64_t cnt, const float2* __restrict__ a, const float2* __restrict__ b, float2* __restrict__ out)
+{
+    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (x >= cnt) return;
+    out[x] = make_float2(a[x].x - b[x].x, a[x].y - b[x].y);
+}
+
+}  // namespace
+
+// ====================================================================== host
+using cd = std::complex<double>;
+
+static void esi_eval(double sigma, double zeta, double f, double& re, double& im)
+{
+    const double rdc = 2.0 / (sigma * zeta);
+    if (f <= 0) { re = rdc; im = 0; return; }
+    const double rrf = std::sqrt(M_PI * kMu0 / sigma);
+    const cd a = cd(1, 1) * rrf * std::sqrt(f);
+    const cd x = a / rdc;
+    cd z;
+    if (std::abs(x) < 1e-4) z = rdc / (1.0 - x / 2.0 + x * x / 6.0 - x * x * x / 24.0);  // a/(1-e^-x) = rdc*x/(1-e^-x)
+    else z = a / (1.0 - std::exp(-x));
+    re = z.real();
+    im = z.imag();
+}
+
+static void op_reserve(xrl_op op, int nrhs)
+{
+    if (op->cap_rhs >= nrhs) return;
+    op->u.alloc((size_t)3 * nrhs * op->tree->n);
+    op->pu.alloc((size_t)3 * nrhs * op->tree->n);
+    op->cap_rhs = nrhs;
+}
+
+static xrl_status op_apply(xrl_op op, const float2* v, float2* w, int nrhs)
+{
+    xrl_tree t = op->tree;
+    xrl_topo T = op->topo;
+    cudaStream_t st = t->ctx->stream;
+    const int64_t n = t->n, nl = T->n_loops;
+    op_reserve(op, nrhs);
+    k_loops_to_panels<<<nblk(n, 256), 256, 0, st>>>(n, nl, nrhs, T->cp_ptr.p, T->cp_col.p, T->cp_val.p, v, op->u.p);
+    XRL_LAUNCH_CHECK();
+    t->ctx->launches += 1;
+    xrl_status s = xrl_mvm(t, op->near, op->u.p, op->pu.p, 3 * nrhs, XRL_MVM_FULL);
+    if (s) return s;
+    k_panels_to_loops<<<nblk(nl, 256), 256, 0, st>>>(n, nl, nrhs, T->cl_ptr.p, T->cl_col.p, T->cl_val.p, op->zsa.p,
+                                                     (float)op->alpha_im, op->u.p, op->pu.p, w);
+    XRL_LAUNCH_CHECK();
+    t->ctx->launches += 1;
+    return XRL_OK;
+}
+
+static void pc_apply(xrl_precond pc, const float2* v, float2* z, int nrhs)
+{
+    xrl_tree t = pc->op->tree;
+    const int nl = (int)pc->op->topo->n_loops;
+    k_block_apply<<<pc->nblocks, kBS, 0, t->ctx->stream>>>(nl, nrhs, pc->bptr.p, pc->inv.p, v, z);
+    XRL_LAUNCH_CHECK();
+    t->ctx->launches += 1;
+}
+
+#define API_TRY try {
+#define API_CATCH                                   \
+    }                                               \
+    catch (const CudaError& e) { return e.code; }   \
+    catch (const std::bad_alloc&) {                 \
+        set_error("host out of memory");            \
+        return XRL_ENOMEM;                          \
+    }
+
+extern "C" {
+
+xrl_status xrl_esi(double sigma, double zeta, double f, double* re, double* im)
+{
+    if (!(sigma > 0) || !(zeta > 0) || f < 0 || !re || !im) { set_error("xrl_esi: sigma, zeta > 0 and f >= 0 required"); return XRL_EINVAL; }
+    esi_eval(sigma, zeta, f, *re, *im);
+    return XRL_OK;
+}
+
+xrl_status xrl_operator_create(xrl_tree t, xrl_near nr, xrl_topo T, const double* zs, double sigma, double zeta,
+                               double freq, xrl_op* out)
+{
+    if (!t || !nr || !T || !out) { set_error("xrl_operator_create: null argument"); return XRL_EINVAL; }
+    *out = nullptr;
+    if (nr->tree != t || T->tree != t) { set_error("xrl_operator_create: handles from different trees"); return XRL_EPROVENANCE; }
+    if (freq < 0) { set_error("xrl_operator_create: negative frequency"); return XRL_EINVAL; }
+    if (!zs && (!(sigma > 0) || !(zeta > 0))) { set_error("xrl_operator_create: need zs or sigma, zeta > 0"); return XRL_EINVAL; }
+    API_TRY
+        XRL_CUDA(cudaSetDevice(t->ctx->device));
+        auto op = std::make_unique<xrl_op_s>();
+        op->tree = t;
+        op->near = nr;
+        op->topo = T;
+        op->freq = freq;
+        op->omega = 2 * M_PI * freq;
+        op->alpha_im = op->omega * kMu0 / (4 * M_PI);
+        const int64_t n = t->n;
+        std::vector<double> area(n);
+        XRL_CUDA(cudaMemcpy(area.data(), t->area.p, 8 * n, cudaMemcpyDeviceToHost));
+        op->zsa_h.resize(2 * n);
+        std::vector<float2> zf(n);
+        double zr = 0, zi = 0;
+        if (!zs) esi_eval(sigma, zeta, freq, zr, zi);
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t k = T->perm[i];
+            const double a = zs ? zs[2 * k] : zr, b = zs ? zs[2 * k + 1] : zi;
+            op->zsa_h[2 * i] = a / area[i];
+            op->zsa_h[2 * i + 1] = b / area[i];
+            zf[i] = make_float2((float)(a / area[i]), (float)(b / area[i]));
+        }
+        op->zsa.alloc(n);
+        XRL_CUDA(cudaMemcpy(op->zsa.p, zf.data(), 8 * n, cudaMemcpyHostToDevice));
+        ++T->refs;
+        ++t->refs;
+        *out = op.release();
+        return XRL_OK;
+    API_CATCH
+}
+
+void xrl_operator_destroy(xrl_op op)
+{
+    if (!op) return;
+    xrl_tree t = op->tree;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    --op->topo->refs;
+    delete op;
+    --t->refs;
+    tree_release(t);
+}
+
+xrl_status xrl_operator_apply(xrl_op op, const void* v, void* w, int32_t nrhs)
+{
+    if (!op || !v || !w || nrhs < 1) { set_error("xrl_operator_apply: bad argument"); return XRL_EINVAL; }
+    if (v == w) { set_error("xrl_operator_apply: v and w alias"); return XRL_EINVAL; }
+    API_TRY
+        XRL_CUDA(cudaSetDevice(op->tree->ctx->device));
+        return op_apply(op, (const float2*)v, (float2*)w, nrhs);
+    API_CATCH
+}
+
+xrl_status xrl_precond_build(xrl_op op, int32_t block_size, xrl_precond* out)
+{
+    if (!op || !out) { set_error("xrl_precond_build: null argument"); return XRL_EINVAL; }
+    *out = nullptr;
+    if (block_size < 1 || block_size > kBS) { set_error("xrl_precond_build: block_size must be 1..%d", kBS); return XRL_EINVAL; }
+    API_TRY
+        xrl_tree t = op->tree;
+        xrl_topo T = op->topo;
+        cudaStream_t st = t->ctx->stream;
+        XRL_CUDA(cudaSetDevice(t->ctx->device));
+        const int64_t n = t->n, nl = T->n_loops;
+        auto pc = std::make_unique<xrl_precond_s>();
+        pc->op = op;
+        pc->bs = block_size;
+        for (int64_t l = 0; l < nl; l += block_size) pc->bptr_h.push_back((int32_t)l);
+        pc->bptr_h.push_back((int32_t)nl);
+        pc->nblocks = (int32_t)pc->bptr_h.size() - 1;
+        pc->bptr.alloc(pc->bptr_h.size());
+        XRL_CUDA(cudaMemcpyAsync(pc->bptr.p, pc->bptr_h.data(), 4 * pc->bptr_h.size(), cudaMemcpyHostToDevice, st));
+        // d_k = Z_s/A + j alpha P_kk
+        DBuf<double> pkk(n);
+        k_diag_p<<<nblk(n, 256), 256, 0, st>>>(n, op->near->row_ptr.p, op->near->col.p, op->near->val64.p, pkk.p);
+        XRL_LAUNCH_CHECK();
+        std::vector<double> hp(n);
+        XRL_CUDA(cudaMemcpyAsync(hp.data(), pkk.p, 8 * n, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<double2> hd(n);
+        for (int64_t i = 0; i < n; ++i) hd[i] = make_double2(op->zsa_h[2 * i], op->zsa_h[2 * i + 1] + op->alpha_im * hp[i]);
+        DBuf<double2> dk(n);
+        XRL_CUDA(cudaMemcpyAsync(dk.p, hd.data(), 16 * n, cudaMemcpyHostToDevice, st));
+        pc->inv.alloc((size_t)pc->nblocks * kBS * kBS);
+        DBuf<int> sing(1);
+        XRL_CUDA(cudaMemsetAsync(sing.p, 0, 4, st));
+        if (pc->nblocks > 0) {
+            const int smem = kBS * (kBS + 1) * (int)sizeof(double2);
+            XRL_CUDA(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            k_block_inverse<<<pc->nblocks, 256, smem, st>>>(pc->bptr.p, T->cl_ptr.p, T->cl_col.p, T->cl_val64.p, T->cp_ptr.p,
+                                                         T->cp_col.p, dk.p, pc->inv.p, sing.p);
+            XRL_LAUNCH_CHECK();
+        }
+        int hs = 0;
+        XRL_CUDA(cudaMemcpyAsync(&hs, sing.p, 4, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        if (hs) { set_error("xrl_precond_build: singular block %d (pivot below 1e-13 of the block max)", hs - 1); return XRL_ESINGULAR; }
+        ++T->refs;
+        *out = pc.release();
+        return XRL_OK;
+    API_CATCH
+}
+
+void xrl_precond_destroy(xrl_precond pc)
+{
+    if (!pc) return;
+    --pc->op->topo->refs;
+    delete pc;
+}
+
+xrl_status xrl_precond_apply(xrl_precond pc, const void* v, void* z, int32_t nrhs)
+{
+    if (!pc || !v || !z || nrhs < 1) { set_error("xrl_precond_apply: bad argument"); return XRL_EINVAL; }
+    API_TRY
+        XRL_CUDA(cudaSetDevice(pc->op->tree->ctx->device));
+        pc_apply(pc, (const float2*)v, (float2*)z, nrhs);
+        return XRL_OK;
+    API_CATCH
+}
+
+xrl_status xrl_precond_export(xrl_precond pc, int32_t* n_blocks, int32_t* block_size, int32_t* block_ptr, void* inv)
+{
+    if (!pc) { set_error("xrl_precond_export: null handle"); return XRL_EINVAL; }
+    API_TRY
+        if (n_blocks) *n_blocks = pc->nblocks;
+        if (block_size) *block_size = kBS;
+        if (block_ptr) std::copy(pc->bptr_h.begin(), pc->bptr_h.end(), block_ptr);
+        if (inv) {
+            // device stores column-major per block; export row-major
+            std::vector<float2> h((size_t)pc->nblocks * kBS * kBS);
+            XRL_CUDA(cudaMemcpy(h.data(), pc->inv.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+            float2* o = (float2*)inv;
+            for (int b = 0; b < pc->nblocks; ++b)
+                for (int i = 0; i < kBS; ++i)
+                    for (int j = 0; j < kBS; ++j) o[((size_t)b * kBS + i) * kBS + j] = h[((size_t)b * kBS + j) * kBS + i];
+        }
+        return XRL_OK;
+    API_CATCH
+}
+
+xrl_status xrl_port_rhs(xrl_topo T, int32_t port, double volts, void* b)
+{
+    if (!T || !b || port < 0 || port >= T->n_ports) { set_error("xrl_port_rhs: bad argument"); return XRL_EINVAL; }
+    API_TRY
+        xrl_ctx ctx = T->tree->ctx;
+        XRL_CUDA(cudaSetDevice(ctx->device));
+        std::vector<float2> h(T->n_loops, make_float2(0.f, 0.f));
+        // V_l = sum_b M(l,b) V_b, V_b = volts on the port branch only
+        int port_branch = -1, seen = -1;
+        for (int64_t b2 = 0; b2 < T->n_branches; ++b2)
+            if (T->br_kind[b2] == 2 && ++seen == port) { port_branch = (int)b2; break; }
+        for (int64_t l = 0; l < T->n_loops; ++l)
+            for (int64_t q = T->m_ptr[l]; q < T->m_ptr[l + 1]; ++q)
+                if (T->m_idx[q] == port_branch) h[l].x += (float)(T->m_val[q] * volts);
+        XRL_CUDA(cudaMemcpyAsync(b, h.data(), 8 * h.size(), cudaMemcpyHostToDevice, ctx->stream));
+        XRL_CUDA(cudaStreamSynchronize(ctx->stream));
+        return XRL_OK;
+    API_CATCH
+}
+
+xrl_status xrl_port_currents(xrl_topo T, const void* x, int32_t nrhs, double* ip)
+{
+    if (!T || !x || !ip || nrhs < 1) { set_error("xrl_port_currents: bad argument"); return XRL_EINVAL; }
+    API_TRY
+        xrl_ctx ctx = T->tree->ctx;
+        XRL_CUDA(cudaSetDevice(ctx->device));
+        const int64_t nl = T->n_loops;
+        for (int r = 0; r < nrhs; ++r)
+            for (int p = 0; p < T->n_ports; ++p) {
+                // I_branch = (M^T I_l)[port branch] = sign * I_l(port loop)
+                const int l = T->port_loop[p];
+                int sign = 0;
+                for (int64_t q = T->m_ptr[l]; q < T->m_ptr[l + 1]; ++q)
+                    if (T->br_kind[T->m_idx[q]] == 2) sign = T->m_val[q];
+                float2 v;
+                XRL_CUDA(cudaMemcpyAsync(&v, (const float2*)x + (size_t)r * nl + l, 8, cudaMemcpyDeviceToHost, ctx->stream));
+                XRL_CUDA(cudaStreamSynchronize(ctx->stream));
+                ip[2 * ((size_t)r * T->n_ports + p)] = sign * (double)v.x;
+                ip[2 * ((size_t)r * T->n_ports + p) + 1] = sign * (double)v.y;
+            }
+        return XRL_OK;
+    API_CATCH
+}
+
+xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_t nrhs, const xrl_gmres_opts* opts,
+                     int32_t* iters_out, double* rre_out, double* true_rre_out, int32_t* conv_out)
+{
+    if (!op || !b_ || !x_ || nrhs < 1) { set_error("xrl_gmres: bad argument"); return XRL_EINVAL; }
+    const int m = opts && opts->restart > 0 ? opts->restart : 50;
+    const int maxit = opts && opts->max_iters > 0 ? opts->max_iters : 2000;
+    double tol = opts ? opts->tol : 0;
+    if (!(tol > 0)) tol = op->freq > 1e6 ? 1e-4 : 1e-6;  // PAPER.md:152, reading C-A8
+    if (tol >= 1) { set_error("xrl_gmres: tol must be < 1"); return XRL_EINVAL; }
+    API_TRY
+        xrl_tree t = op->tree;
+        cudaStream_t st = t->ctx->stream;
+        XRL_CUDA(cudaSetDevice(t->ctx->device));
+        const int64_t nl = op->topo->n_loops;
+        const float2* b = (const float2*)b_;
+        float2* x = (float2*)x_;
+        DBuf<float2> V((size_t)nrhs * (m + 1) * nl), w((size_t)nrhs * nl), tmp((size_t)nrhs * nl);
+        DBuf<double2> dh((size_t)nrhs * (m + 1));
+        DBuf<double> ds(nrhs), ones(nrhs);
+        {
+            std::vector<double> one(nrhs, 1.0);
+            XRL_CUDA(cudaMemcpyAsync(ones.p, one.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
+        }
+        std::vector<double2> hh((size_t)nrhs * (m + 1));
+        auto Mx = [&](const float2* in, float2* o) {  // o = M^-1 in (or copy)
+            if (pc) pc_apply(pc, in, o, nrhs);
+            else XRL_CUDA(cudaMemcpyAsync(o, in, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
+        };
+        auto norms = [&](const float2* a, std::vector<double>& out) {  // ||a_r||
+            k_gdots<<<dim3(1, nrhs), 256, 0, st>>>(nl, 1, a, a, dh.p, 1);
+            XRL_LAUNCH_CHECK();
+            std::vector<double2> h(nrhs);
+            XRL_CUDA(cudaMemcpyAsync(h.data(), dh.p, 16 * nrhs, cudaMemcpyDeviceToHost, st));
+            XRL_CUDA(cudaStreamSynchronize(st));
+            out.resize(nrhs);
+            for (int r = 0; r < nrhs; ++r) out[r] = std::sqrt(std::max(h[r].x, 0.0));
+        };
+        // reference: ||M^-1 b|| (preconditioned RRE) and ||b||
+        std::vector<double> bnorm, pbnorm;
+        norms(b, bnorm);
+        Mx(b, tmp.p);
+        norms(tmp.p, pbnorm);
+        std::vector<int> iters(nrhs, 0), conv(nrhs, 0);
+        std::vector<double> rre(nrhs, 1.0);
+        for (int r = 0; r < nrhs; ++r)
+            if (bnorm[r] == 0) { conv[r] = 1; rre[r] = 0; }
+        int total = 0;
+        while (total < maxit) {
+            bool all = true;
+            for (int r = 0; r < nrhs; ++r) all = all && conv[r];
+            if (all) break;
+            // r0 = M^-1 (b - A x)
+            xrl_status s = op_apply(op, x, w.p, nrhs);
+            if (s) return s;
+            k_gsub<<<nblk(nrhs * nl, 256), 256, 0, st>>>(nrhs * nl, b, w.p, tmp.p);
+            XRL_LAUNCH_CHECK();
+            Mx(tmp.p, w.p);
+            std::vector<double> beta;
+            norms(w.p, beta);
+            std::vector<double> sc(nrhs);
+            for (int r = 0; r < nrhs; ++r) sc[r] = beta[r] > 0 ? 1.0 / beta[r] : 0.0;
+            XRL_CUDA(cudaMemcpyAsync(ds.p, sc.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
+            k_gscale<<<nblk(nl, 256), 256, 0, st>>>(nl, nrhs, w.p, nl, ds.p, V.p, (int64_t)(m + 1) * nl);
+            XRL_LAUNCH_CHECK();
+            // per-column Hessenberg, Givens and residual vector (FP64 host)
+            std::vector<std::vector<cd>> H(nrhs, std::vector<cd>((m + 1) * m, 0.0));
+            std::vector<std::vector<cd>> g(nrhs, std::vector<cd>(m + 1, 0.0)), cs(nrhs, std::vector<cd>(m)), sn(nrhs, std::vector<cd>(m));
+            for (int r = 0; r < nrhs; ++r) g[r][0] = beta[r];
+            std::vector<int> jlen(nrhs, 0);
+            std::vector<int> active(nrhs);
+            for (int r = 0; r < nrhs; ++r) active[r] = !conv[r] && beta[r] > 0;
+            int j = 0;
+            for (; j < m && total < maxit; ++j, ++total) {
+                bool any = false;
+                for (int r = 0; r < nrhs; ++r) any = any || active[r];
+                if (!any) break;
+                // w = M^-1 A v_j  (batched over the columns)
+                k_gscale<<<nblk(nl, 256), 256, 0, st>>>(nl, nrhs, V.p + (int64_t)j * nl, (int64_t)(m + 1) * nl,
+                                                        ones.p, tmp.p, nl);
+                XRL_LAUNCH_CHECK();
+                s = op_apply(op, tmp.p, w.p, nrhs);
+                if (s) return s;
+                Mx(w.p, tmp.p);
+                XRL_CUDA(cudaMemcpyAsync(w.p, tmp.p, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
+                // CGS2
+                std::vector<std::vector<cd>> hcol(nrhs, std::vector<cd>(j + 2, 0.0));
+                for (int pass = 0; pass < 2; ++pass) {
+                    k_gdots<<<dim3(j + 1, nrhs), 256, 0, st>>>(nl, m + 1, V.p, w.p, dh.p, j + 1);
+                    XRL_LAUNCH_CHECK();
+                    XRL_CUDA(cudaMemcpyAsync(hh.data(), dh.p, 16 * nrhs * (j + 1), cudaMemcpyDeviceToHost, st));
+                    XRL_CUDA(cudaStreamSynchronize(st));
+                    for (int r = 0; r < nrhs; ++r)
+                        for (int i = 0; i <= j; ++i) hcol[r][i] += cd(hh[(size_t)r * (j + 1) + i].x, hh[(size_t)r * (j + 1) + i].y);
+                    k_gupdate<<<nblk(nl, 256), 256, 0, st>>>(nl, m + 1, nrhs, V.p, dh.p, j + 1, -1.f, w.p);
+                    XRL_LAUNCH_CHECK();
+                }
+                std::vector<double> hn;
+                norms(w.p, hn);
+                for (int r = 0; r < nrhs; ++r) {
+                    hcol[r][j + 1] = hn[r];
+                    sc[r] = hn[r] > 1e-300 ? 1.0 / hn[r] : 0.0;
+                }
+                XRL_CUDA(cudaMemcpyAsync(ds.p, sc.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
+                k_gscale<<<nblk(nl, 256), 256, 0, st>>>(nl, nrhs, w.p, nl, ds.p, V.p + (int64_t)(j + 1) * nl, (int64_t)(m + 1) * nl);
+                XRL_LAUNCH_CHECK();
+                for (int r = 0; r < nrhs; ++r) {
+                    if (!active[r]) continue;
+                    auto& hc = hcol[r];
+                    for (int i = 0; i < j; ++i) {  // apply previous rotations
+                        const cd a = hc[i], bb = hc[i + 1];
+                        hc[i] = std::conj(cs[r][i]) * a + std::conj(sn[r][i]) * bb;
+                        hc[i + 1] = -sn[r][i] * a + cs[r][i] * bb;
+                    }
+                    const double den = std::sqrt(std::norm(hc[j]) + std::norm(hc[j + 1]));
+                    cs[r][j] = den > 0 ? hc[j] / den : 1.0;
+                    sn[r][j] = den > 0 ? hc[j + 1] / den : 0.0;
+                    hc[j] = den;
+                    hc[j + 1] = 0;
+                    g[r][j + 1] = -sn[r][j] * g[r][j];
+                    g[r][j] = std::conj(cs[r][j]) * g[r][j];
+                    for (int i = 0; i <= j; ++i) H[r][(size_t)i * m + j] = hc[i];
+                    jlen[r] = j + 1;
+                    iters[r]++;
+                    rre[r] = std::abs(g[r][j + 1]) / (pbnorm[r] > 0 ? pbnorm[r] : 1.0);
+                    if (rre[r] < tol || hn[r] <= 1e-300) { conv[r] = 1; active[r] = 0; }
+                }
+            }
+            // x += V y,  H y = g (upper triangular, per column)
+            std::vector<double2> hy((size_t)nrhs * m, make_double2(0, 0));
+            int jmax = 0;
+            for (int r = 0; r < nrhs; ++r) {
+                const int jl = jlen[r];
+                jmax = std::max(jmax, jl);
+                std::vector<cd> y(jl);
+                for (int i = jl - 1; i >= 0; --i) {
+                    cd acc = g[r][i];
+                    for (int k = i + 1; k < jl; ++k) acc -= H[r][(size_t)i * m + k] * y[k];
+                    y[i] = acc / H[r][(size_t)i * m + i];
+                }
+                for (int i = 0; i < jl; ++i) hy[(size_t)r * m + i] = make_double2(y[i].real(), y[i].imag());
+            }
+            if (jmax > 0) {
+                DBuf<double2> dy((size_t)nrhs * jmax);
+                std::vector<double2> hy2((size_t)nrhs * jmax);
+                for (int r = 0; r < nrhs; ++r)
+                    for (int i = 0; i < jmax; ++i) hy2[(size_t)r * jmax + i] = hy[(size_t)r * m + i];
+                XRL_CUDA(cudaMemcpyAsync(dy.p, hy2.data(), 16 * hy2.size(), cudaMemcpyHostToDevice, st));
+                k_gupdate<<<nblk(nl, 256), 256, 0, st>>>(nl, m + 1, nrhs, V.p, dy.p, jmax, 1.f, x);
+                XRL_LAUNCH_CHECK();
+                XRL_CUDA(cudaStreamSynchronize(st));
+            }
+            if (j == 0) break;
+        }
+        // true relative residual ||b - A x|| / ||b||
+        xrl_status s = op_apply(op, x, w.p, nrhs);
+        if (s) return s;
+        k_gsub<<<nblk(nrhs * nl, 256), 256, 0, st>>>(nrhs * nl, b, w.p, tmp.p);
+        XRL_LAUNCH_CHECK();
+        std::vector<double> rn;
+        norms(tmp.p, rn);
+        bool all = true;
+        for (int r = 0; r < nrhs; ++r) {
+            if (iters_out) iters_out[r] = iters[r];
+            if (rre_out) rre_out[r] = rre[r];
+            if (true_rre_out) true_rre_out[r] = bnorm[r] > 0 ? rn[r] / bnorm[r] : 0.0;
+            if (conv_out) conv_out[r] = conv[r];
+            all = all && conv[r];
+        }
+        return all ? XRL_OK : XRL_ENOCONV;
+    API_CATCH
+}
+
+}  // extern "C"

@@ -469,6 +469,8 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     ++ctx->refs;
     T->n = n;
     T->leaf_max = opts ? opts->leaf_max : 64;
+    T->h_vert.assign(vert_h, vert_h + 3 * n_vert);
+    T->h_tri.assign(tri_h, tri_h + 3 * n);
     T->max_depth = opts ? opts->max_depth : kMortonBits;
 
     DBuf<double> vert(3 * n_vert);

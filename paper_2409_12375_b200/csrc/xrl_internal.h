@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
 #include <cstdio>
 #include <memory>
@@ -132,6 +133,9 @@ struct xrl_tree_s {
     // parents per level for M2M/L2L: boxes with children, grouped by level
     std::vector<int32_t> par_start;          // host [nlevel+1] offsets into parents
     xrl::DBuf<int32_t> parents;
+    // host copies of the mesh (original order) for the topology build
+    std::vector<double> h_vert;              // [nv][3]
+    std::vector<int32_t> h_tri;              // [n][3]
     // MVM scratch
     xrl::DBuf<float> mu, ell;                // [nbox][kBoxStride]
     xrl::DBuf<float> xq;                     // [n][8] packed charges
@@ -146,6 +150,51 @@ struct xrl_near_s {
     xrl::DBuf<int32_t> col;
     xrl::DBuf<float> val;       // N_kl (FP32)
     xrl::DBuf<double> val64;    // P_kl (FP64, before subtraction)
+};
+
+struct xrl_topo_s {
+    xrl_tree tree = nullptr;
+    int refs = 0;
+    int64_t n_edges = 0, n_branches = 0, n_loops = 0, nnz_c = 0;
+    int32_t n_ports = 0, n_components = 0;
+    int64_t n_vertex_loops = 0, n_fund_loops = 0, n_terminal_loops = 0;
+    std::vector<int32_t> perm;                   // library -> mesh order
+    std::vector<int32_t> edge_i, edge_j;         // library panel indices, i < j
+    std::vector<double> edge_mid;                // [n_edges][3]
+    std::vector<int32_t> br_a, br_b;             // branch endpoints (panel or n + super node)
+    std::vector<int8_t> br_kind;                 // 0 edge, 1 terminal, 2 port
+    std::vector<int64_t> m_ptr;                  // M CSR over loops
+    std::vector<int32_t> m_idx;
+    std::vector<int8_t> m_val;
+    std::vector<int32_t> port_loop;
+    std::vector<int8_t> loop_kind;
+    std::vector<int64_t> c_ptr_h;                // C = M A_t (host copy, FP64)
+    std::vector<int32_t> c_col_h;
+    std::vector<double> c_val_h;
+    xrl::DBuf<int64_t> cl_ptr, cp_ptr;           // C by loop rows / by panel rows
+    xrl::DBuf<int32_t> cl_col, cp_col;
+    xrl::DBuf<float> cl_val, cp_val;             // 3 floats per nonzero
+    xrl::DBuf<double> cl_val64;                  // FP64 copy for the preconditioner assembly
+};
+
+struct xrl_op_s {
+    xrl_tree tree = nullptr;
+    xrl_near near = nullptr;
+    xrl_topo topo = nullptr;
+    double freq = 0, omega = 0;
+    double alpha_im = 0;                         // alpha = j * alpha_im = j omega mu0 / 4 pi
+    std::vector<double> zsa_h;                   // Z_s/A per panel (library order), [n][2]
+    xrl::DBuf<float2> zsa;                       // device copy
+    xrl::DBuf<float2> u, pu;                     // scratch [3*nrhs][n]
+    int32_t cap_rhs = 0;
+};
+
+struct xrl_precond_s {
+    xrl_op op = nullptr;
+    int32_t bs = 64, nblocks = 0;
+    std::vector<int32_t> bptr_h;
+    xrl::DBuf<int32_t> bptr;
+    xrl::DBuf<float2> inv;                       // [nblocks][bs][bs]
 };
 
 namespace xrl {

@@ -26,6 +26,10 @@ EXPORTS = [
     "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble", "xrl_near_destroy",
     "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_timing_enable", "xrl_timing_count",
     "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count",
+    "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
+    "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
+    "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
+    "xrl_port_currents",
 ]
 
 
@@ -54,6 +58,25 @@ class TreeInfo(ctypes.Structure):
         d = {k: getattr(self, k) for k, _ in self._fields_}
         d["root_lo"] = list(self.root_lo)
         return d
+
+
+class Port(ctypes.Structure):
+    _fields_ = [("n_plus", ctypes.c_int32), ("n_minus", ctypes.c_int32),
+                ("plus", ctypes.c_void_p), ("minus", ctypes.c_void_p)]
+
+
+class TopoInfo(ctypes.Structure):
+    _fields_ = [("n_panels", ctypes.c_int64), ("n_edges", ctypes.c_int64), ("n_branches", ctypes.c_int64),
+                ("n_loops", ctypes.c_int64), ("n_ports", ctypes.c_int32), ("n_components", ctypes.c_int32),
+                ("n_vertex_loops", ctypes.c_int64), ("n_fundamental_loops", ctypes.c_int64),
+                ("n_terminal_loops", ctypes.c_int64), ("nnz_m", ctypes.c_int64), ("nnz_c", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class GmresOpts(ctypes.Structure):
+    _fields_ = [("restart", ctypes.c_int32), ("max_iters", ctypes.c_int32), ("tol", ctypes.c_double)]
 
 
 _lib = None
@@ -97,6 +120,29 @@ def lib():
         L.xrl_timing_reset.argtypes = [P]
         L.xrl_launch_count.argtypes = [P]
         L.xrl_launch_count.restype = i64
+        L.xrl_topology_build.argtypes = [P, i32, P, pp]
+        L.xrl_topology_info.argtypes = [P, ctypes.POINTER(TopoInfo)]
+        L.xrl_topology_export.argtypes = [P] * 12
+        L.xrl_topology_destroy.argtypes = [P]
+        L.xrl_topology_destroy.restype = None
+        f64 = ctypes.c_double
+        L.xrl_esi.argtypes = [f64, f64, f64, P, P]
+        L.xrl_operator_create.argtypes = [P, P, P, P, f64, f64, f64, pp]
+        L.xrl_operator_apply.argtypes = [P, P, P, i32]
+        L.xrl_operator_destroy.argtypes = [P]
+        L.xrl_operator_destroy.restype = None
+        L.xrl_precond_build.argtypes = [P, i32, pp]
+        L.xrl_precond_apply.argtypes = [P, P, P, i32]
+        L.xrl_precond_export.argtypes = [P, P, P, P, P]
+        L.xrl_precond_destroy.argtypes = [P]
+        L.xrl_precond_destroy.restype = None
+        L.xrl_gmres.argtypes = [P, P, P, P, i32, ctypes.POINTER(GmresOpts), P, P, P, P]
+        L.xrl_port_rhs.argtypes = [P, i32, f64, P]
+        L.xrl_port_currents.argtypes = [P, P, i32, P]
+        for name in ("xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_esi",
+                     "xrl_operator_create", "xrl_operator_apply", "xrl_precond_build", "xrl_precond_apply",
+                     "xrl_precond_export", "xrl_gmres", "xrl_port_rhs", "xrl_port_currents"):
+            getattr(L, name).restype = ctypes.c_int32
         for name in ("xrl_ctx_create", "xrl_ctx_sync", "xrl_tree_build", "xrl_tree_info", "xrl_tree_perm",
                      "xrl_to_library_order", "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble",
                      "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_timing_enable", "xrl_timing_get",
@@ -291,3 +337,163 @@ def mvm_host(tree: Tree, near: Near, x_host: np.ndarray, y_host: np.ndarray | No
         y_host = np.empty_like(x_host)
     check(lib().xrl_mvm_host(tree.h, near.h, _ptr(x_host), _ptr(y_host), x_host.shape[0], flags))
     return y_host
+
+
+def esi(sigma: float, zeta: float, freq: float) -> complex:
+    """Z_s of Eq. 3, reading R12."""
+    re, im = ctypes.c_double(), ctypes.c_double()
+    check(lib().xrl_esi(sigma, zeta, freq, ctypes.byref(re), ctypes.byref(im)))
+    return complex(re.value, im.value)
+
+
+class Topology:
+    """xrl_topology_build: edges, CM maps (Alg. 1), loop matrix with ports."""
+
+    def __init__(self, tree: Tree, ports=()):
+        self.tree = tree
+        self._keep = []
+        arr = (Port * max(1, len(ports)))()
+        for i, (plus, minus) in enumerate(ports):
+            p = np.ascontiguousarray(plus, dtype=np.int32)
+            m = np.ascontiguousarray(minus, dtype=np.int32)
+            self._keep += [p, m]
+            arr[i] = Port(p.size, m.size, p.ctypes.data, m.ctypes.data)
+        h = ctypes.c_void_p()
+        check(lib().xrl_topology_build(tree.h, len(ports), ctypes.cast(arr, ctypes.c_void_p) if ports else None,
+                                       ctypes.byref(h)))
+        self.h = h
+        self.n_ports = len(ports)
+
+    def info(self) -> dict:
+        ti = TopoInfo()
+        check(lib().xrl_topology_info(self.h, ctypes.byref(ti)))
+        return ti.as_dict()
+
+    @property
+    def n_loops(self) -> int:
+        return int(self.info()["n_loops"])
+
+    def export(self) -> dict:
+        i = self.info()
+        nb, ne, nl = i["n_branches"], i["n_edges"], i["n_loops"]
+        d = {"branch_nodes": np.empty((nb, 2), np.int32), "branch_kind": np.empty(nb, np.int8),
+             "edge_mid": np.empty((ne, 3)), "m_ptr": np.empty(nl + 1, np.int64),
+             "m_branch": np.empty(max(1, i["nnz_m"]), np.int32), "m_sign": np.empty(max(1, i["nnz_m"]), np.int8),
+             "port_loop": np.empty(max(1, i["n_ports"]), np.int32), "loop_kind": np.empty(nl, np.int8),
+             "c_ptr": np.empty(nl + 1, np.int64), "c_panel": np.empty(max(1, i["nnz_c"]), np.int32),
+             "c_val": np.empty((max(1, i["nnz_c"]), 3))}
+        check(lib().xrl_topology_export(self.h, *[_ptr(d[k]) for k in (
+            "branch_nodes", "branch_kind", "edge_mid", "m_ptr", "m_branch", "m_sign", "port_loop", "loop_kind",
+            "c_ptr", "c_panel", "c_val")]))
+        d["m_branch"] = d["m_branch"][:i["nnz_m"]]
+        d["m_sign"] = d["m_sign"][:i["nnz_m"]]
+        d["c_panel"] = d["c_panel"][:i["nnz_c"]]
+        d["c_val"] = d["c_val"][:i["nnz_c"]]
+        d["port_loop"] = d["port_loop"][:i["n_ports"]]
+        return d
+
+    def port_rhs(self, port: int, volts: float = 1.0, out=None):
+        import torch
+        out = torch.empty((1, self.n_loops), dtype=torch.complex64, device="cuda") if out is None else out
+        check(lib().xrl_port_rhs(self.h, port, volts, _ptr(out)))
+        return out
+
+    def port_currents(self, x) -> np.ndarray:
+        nrhs = x.shape[0]
+        out = np.empty((nrhs, self.n_ports, 2))
+        check(lib().xrl_port_currents(self.h, _ptr(x), nrhs, _ptr(out)))
+        return out[..., 0] + 1j * out[..., 1]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xrl_topology_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Operator:
+    """xrl_operator_create: loop-space operator of Eq. 8-9 at one frequency."""
+
+    def __init__(self, tree: Tree, near: Near, topo: Topology, freq: float, zs=None, sigma=5.8e7, zeta=1e-4):
+        self.tree, self.near, self.topo = tree, near, topo
+        z = None
+        if zs is not None:
+            zs = np.broadcast_to(np.asarray(zs, dtype=np.complex128), (tree.n,))
+            z = np.ascontiguousarray(np.stack([zs.real, zs.imag], axis=1))
+        h = ctypes.c_void_p()
+        check(lib().xrl_operator_create(tree.h, near.h, topo.h, _ptr(z), sigma, zeta, freq, ctypes.byref(h)))
+        self.h = h
+        self.freq = freq
+
+    def apply(self, v, w=None):
+        import torch
+        w = torch.empty_like(v) if w is None else w
+        check(lib().xrl_operator_apply(self.h, _ptr(v), _ptr(w), v.shape[0]))
+        return w
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xrl_operator_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Precond:
+    """xrl_precond_build: block-Jacobi diagonal-of-P preconditioner (Eq. 10)."""
+
+    def __init__(self, op: Operator, block_size: int = 64):
+        self.op = op
+        h = ctypes.c_void_p()
+        check(lib().xrl_precond_build(op.h, block_size, ctypes.byref(h)))
+        self.h = h
+
+    def apply(self, v, z=None):
+        import torch
+        z = torch.empty_like(v) if z is None else z
+        check(lib().xrl_precond_apply(self.h, _ptr(v), _ptr(z), v.shape[0]))
+        return z
+
+    def export(self):
+        nb, bs = ctypes.c_int32(), ctypes.c_int32()
+        check(lib().xrl_precond_export(self.h, ctypes.byref(nb), ctypes.byref(bs), None, None))
+        ptr = np.empty(nb.value + 1, np.int32)
+        inv = np.empty((nb.value, bs.value, bs.value), np.complex64)
+        check(lib().xrl_precond_export(self.h, None, None, _ptr(ptr), _ptr(inv)))
+        return ptr, inv
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xrl_precond_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gmres(op: Operator, pc, b, x=None, restart=50, max_iters=2000, tol=0.0):
+    """xrl_gmres: returns (x, report dict).  tol <= 0 uses PAPER.md:152's rule."""
+    import torch
+    x = torch.zeros_like(b) if x is None else x
+    nrhs = b.shape[0]
+    iters = np.zeros(nrhs, np.int32)
+    rre = np.zeros(nrhs)
+    trre = np.zeros(nrhs)
+    conv = np.zeros(nrhs, np.int32)
+    st = lib().xrl_gmres(op.h, pc.h if pc is not None else None, _ptr(b), _ptr(x), nrhs,
+                         ctypes.byref(GmresOpts(restart, max_iters, tol)), _ptr(iters), _ptr(rre), _ptr(trre),
+                         _ptr(conv))
+    check(st)
+    return x, {"iters": iters, "rre": rre, "true_rre": trre, "converged": conv.astype(bool), "status": st}

@@ -1,0 +1,167 @@
+"""Loop-space operator, diag-of-P block preconditioner and GMRES (SURVEY §8
+a14-a17) through the C-ABI, against the FP64 oracle (oracle/loop_oracle.py)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+from inputs import meshes
+from oracle import loop_oracle as lo
+from tests.gpu_helpers import cuda_setup
+
+pytestmark = pytest.mark.gpu
+
+SIGMA, ZETA = 5.8e7, 100e-6
+
+
+@pytest.fixture(scope="module")
+def bar_all():
+    from paper_2409_12375_b200 import xrl
+    m = meshes.bar()
+    ctx, tree, near = cuda_setup(m)
+    _, plus, minus = m.ports[0]
+    topo = xrl.Topology(tree, [(plus, minus)])
+    g = oracle.Geometry(m.verts, m.tris)
+    P = oracle.dense_p(g)
+    return m, ctx, tree, near, topo, g, P
+
+
+def _oracle_C(m, g, ex):
+    """C_t = M A_t with the library's loop matrix and branch orientation as
+    input data and the oracle's own Algorithm-1 maps."""
+    br = [tuple(b) for b in ex["branch_nodes"]]
+    A = lo.cm_maps(m.verts, m.tris, g.cent, br)
+    nl = len(ex["m_ptr"]) - 1
+    rows = np.repeat(np.arange(nl), np.diff(ex["m_ptr"]))
+    M = sp.csr_matrix((ex["m_sign"].astype(float), (rows, ex["m_branch"])), shape=(nl, len(br)))
+    phys = sp.diags((ex["branch_kind"] == 0).astype(float))
+    return M, [M @ phys @ A[t] for t in range(3)]
+
+
+def test_topology_loop_basis(bar_all):
+    m, ctx, tree, near, topo, g, P = bar_all
+    info = topo.info()
+    ex = topo.export()
+    nb = info["n_branches"]
+    # cycle rank: N_b - N_nodes + components (2100 panels + 2 super-nodes)
+    assert info["n_loops"] == nb - (m.n + 2) + 1 == 1150
+    assert info["n_vertex_loops"] > 1000 and info["n_fundamental_loops"] == 0
+    M, C = _oracle_C(m, g, ex)
+    # KCL: B M^T = 0 (integer, exact)
+    node = {}
+    ends = [(node.setdefault(int(a), len(node)), node.setdefault(int(b), len(node))) for a, b in ex["branch_nodes"]]
+    r = [x for e in ends for x in e]
+    c = [i for i in range(nb) for _ in (0, 1)]
+    v = [s for _ in range(nb) for s in (1, -1)]
+    B = sp.csr_matrix((v, (r, c)), shape=(len(node), nb))
+    assert abs(B @ M.T).max() == 0
+    assert np.linalg.matrix_rank(M.toarray()) == info["n_loops"]
+    # the port branch is in exactly one loop, the exported port loop
+    pb = np.nonzero(ex["branch_kind"] == 2)[0][0]
+    assert M[:, pb].nnz == 1 and M[ex["port_loop"][0], pb] != 0
+    # C = M A_t: library values equal the oracle's Algorithm-1 product
+    nl = info["n_loops"]
+    rows = np.repeat(np.arange(nl), np.diff(ex["c_ptr"]))
+    for t in range(3):
+        Clt = sp.csr_matrix((ex["c_val"][:, t], (rows, ex["c_panel"])), shape=(nl, m.n))
+        d = (Clt - C[t]).toarray()
+        assert np.abs(d).max() <= 1e-12 * np.abs(C[t].toarray()).max()
+
+
+@pytest.mark.parametrize("freq", [1e3, 1e8])
+def test_operator_apply_vs_oracle(bar_all, freq):
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo, g, P = bar_all
+    op = xrl.Operator(tree, near, topo, freq, sigma=SIGMA, zeta=ZETA)
+    ex = topo.export()
+    M, C = _oracle_C(m, g, ex)
+    nl = M.shape[0]
+    rng = np.random.default_rng(21)
+    v = (rng.random((2, nl)) * 2 - 1 + 1j * (rng.random((2, nl)) * 2 - 1)).astype(np.complex64)
+    w = op.apply(torch.from_numpy(v).cuda()).cpu().numpy()
+    zs = lo.esi(SIGMA, ZETA, freq)
+    alpha = 1j * 2 * np.pi * freq * lo.MU0 / (4 * np.pi)
+    Z = lo.loop_system(C, P, zs / g.area, alpha)
+    wref = (Z @ v.astype(np.complex128).T).T
+    err = oracle.rel_l2(w, wref)
+    print("operator rel L2", freq, err)
+    assert err <= 2e-5
+
+
+def test_precond_apply_vs_oracle(bar_all):
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo, g, P = bar_all
+    freq = 1e8
+    op = xrl.Operator(tree, near, topo, freq, sigma=SIGMA, zeta=ZETA)
+    pc = xrl.Precond(op, 64)
+    bptr, inv = pc.export()
+    ex = topo.export()
+    M, C = _oracle_C(m, g, ex)
+    nl = M.shape[0]
+    assert bptr[0] == 0 and bptr[-1] == nl and np.all(np.diff(bptr) <= 64)
+    rng = np.random.default_rng(5)
+    v = (rng.random((1, nl)) - 0.5 + 1j * (rng.random((1, nl)) - 0.5)).astype(np.complex64)
+    z = pc.apply(torch.from_numpy(v).cuda()).cpu().numpy()
+    zs = lo.esi(SIGMA, ZETA, freq)
+    alpha = 1j * 2 * np.pi * freq * lo.MU0 / (4 * np.pi)
+    zref = lo.precond_apply(C, zs / g.area, alpha, np.diag(P), bptr, v.astype(np.complex128))
+    err = oracle.rel_l2(z, zref)
+    print("precond rel L2", err)
+    assert err <= 1e-5
+
+
+def test_gmres_dc_bar_inductance(bar_all):
+    """Full DC solve of config 1 (north star): Z_port from the GPU GMRES equals
+    the oracle's dense FP64 solve (its own loop basis) and L matches the
+    closed-form thin-walled-tube partial inductance."""
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo, g, P = bar_all
+    f = 1e3
+    rdc = 2 / (SIGMA * ZETA)
+    op = xrl.Operator(tree, near, topo, f, zs=rdc)
+    pc = xrl.Precond(op, 64)
+    b = topo.port_rhs(0, 1.0)
+    x, rep = xrl.gmres(op, pc, b)            # tol rule: f <= 1 MHz -> 1e-6
+    assert rep["converged"].all(), rep
+    I = topo.port_currents(x)[0, 0]
+    Zg = 1.0 / I
+    Zo, _ = lo.port_impedance(m.verts, m.tris, g.cent, g.area, P, [(m.ports[0][1], m.ports[0][2])], rdc, f)
+    print("Z gpu", Zg, "oracle", Zo[0, 0], rep)
+    assert abs(Zg - Zo[0, 0]) / abs(Zo[0, 0]) < 1e-4
+    L = Zg.imag / (2 * np.pi * f)
+    Lt = lo.bar_partial_inductance_tube(1e-3, 1e-4)
+    assert abs(L - Lt) / Lt < 0.02
+    assert rep["true_rre"][0] < 1e-5
+    # preconditioned GMRES needs fewer iterations than unpreconditioned
+    _, rep0 = xrl.gmres(op, None, b, max_iters=3000)
+    print("iterations with / without preconditioner", rep["iters"], rep0["iters"])
+    assert rep["iters"][0] < rep0["iters"][0]
+
+
+def test_gmres_coils_two_ports():
+    """Config 2 (two coils, 2 ports) at one frequency: converges, a-posteriori
+    true residual <= 10 tol, reciprocal, passive, positive inductance."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m = meshes.coils()
+    ctx, tree, near = cuda_setup(m)
+    topo = xrl.Topology(tree, [(p, q) for _, p, q in m.ports])
+    f = 1e8
+    op = xrl.Operator(tree, near, topo, f, sigma=SIGMA, zeta=5e-6)
+    pc = xrl.Precond(op, 64)
+    nl = topo.n_loops
+    b = torch.zeros((2, nl), dtype=torch.complex64, device="cuda")
+    for p in range(2):
+        topo.port_rhs(p, 1.0, out=b[p:p + 1])
+    x, rep = xrl.gmres(op, pc, b)            # f > 1 MHz -> tol 1e-4
+    print("coils", topo.info(), rep)
+    assert rep["converged"].all()
+    assert np.all(rep["true_rre"] < 1e-3)
+    Y = topo.port_currents(x).T               # Y[:, q] = currents for excitation q
+    Z = np.linalg.inv(Y)
+    assert abs(Z[0, 1] - Z[1, 0]) / abs(Z[0, 1]) < 1e-2
+    assert Z[0, 0].real > 0 and Z[1, 1].real > 0
+    L = Z.imag / (2 * np.pi * f)
+    assert L[0, 0] > 0 and L[1, 1] > 0 and abs(L[0, 1]) < np.sqrt(L[0, 0] * L[1, 1])
