@@ -20,8 +20,11 @@
 //   k_leaf     per target leaf: L2P + M2P (W list) + P2P (U list) + near CSR,
 //              writes y once
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
+#include "tcgen05.h"
 #include "xrl_internal.h"
 
 using namespace xrl;
@@ -255,6 +258,127 @@ __global__ void __launch_bounds__(256, 2) k_m2l(const int4* __restrict__ tiles, 
         red_add_v4(o + 4, a0[4], a0[5], a1[0], a1[1]);
         if (i + 1 < kNC) red_add_v4(o + 8, a1[2], a1[3], a1[4], a1[5]);
     }
+}
+
+// ------------------------------------------------------------------ M2L on tcgen05
+// Tensor-core M2L: per 16-pair tile, D[128 x 96] (TMEM, FP32) = T_o[128 x 128]
+// x B[128 x 96] with 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi, 48
+// tcgen05.mma kind::tf32 M128 N96 K8), accuracy ~1e-6 relative.  T_o hi/lo
+// images are pre-laid-out in the canonical K-major core-matrix layout and
+// copied with cp.async when the tile's offset changes; the gathered source
+// multipoles are split hi/lo on the fly.  One CTA (4 warps) per SM walks
+// blocks of kTcR consecutive tiles (same offset -> operator reuse), blocks
+// dealt round-robin so all CTAs stay inside one L2-resident target chunk.
+// Epilogue: tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = coefficients),
+// red.global.add.{v4,v2}.f32 into ell.
+constexpr int kTcN = kTP * 6;                       // 96
+constexpr int kTcABytes = 128 * 128 * 4;            // one operator image
+constexpr int kTcBBytes = kTcN * 128 * 4;
+constexpr int kTcSmem = 2 * kTcABytes + 2 * kTcBBytes;
+constexpr int kTcR = 8;
+
+__device__ __forceinline__ void red_add_v2(float* p, float a, float b)
+{
+    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+
+__global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4* __restrict__ tiles, int ntiles,
+                                                   const int32_t* __restrict__ tgt, const int32_t* __restrict__ srcb,
+                                                   const float* __restrict__ img, const float* __restrict__ mu,
+                                                   float* __restrict__ ell)
+{
+    extern __shared__ __align__(1024) uint8_t tsm[];
+    float* Ah = reinterpret_cast<float*>(tsm);
+    float* Al = reinterpret_cast<float*>(tsm + kTcABytes);
+    float* Bh = reinterpret_cast<float*>(tsm + 2 * kTcABytes);
+    float* Bl = reinterpret_cast<float*>(tsm + 2 * kTcABytes + kTcBBytes);
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // zero B once: rows k >= 121 stay zero (A is zero-padded there too)
+    for (int i = tid; i < 2 * kTcBBytes / 16; i += 128) reinterpret_cast<float4*>(Bh)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid == 0) tc::mbar_init(&bar, 1);
+    if (warp == 0) tc::tmem_alloc<128>(&tbase);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t dtm = tbase;
+    const uint32_t idesc = tc::idesc_tf32(128, kTcN);
+    const uint32_t lboA = 16 * 128, lboB = (kTcN / 8) * 128;
+    int cur_off = -1;
+    uint32_t phase = 0;
+    for (int blk = blockIdx.x; blk * kTcR < ntiles; blk += gridDim.x) {
+        const int t1 = min(ntiles, (blk + 1) * kTcR);
+        for (int t = blk * kTcR; t < t1; ++t) {
+            const int4 tile = tiles[t];
+            const int off = tile.x, begin = tile.y, count = tile.z;
+            if (off != cur_off) {
+                const float4* g = reinterpret_cast<const float4*>(img + (size_t)off * 2 * 128 * 128);
+                float4* s = reinterpret_cast<float4*>(Ah);
+                for (int j = tid; j < 2 * kTcABytes / 16; j += 128) cp_async16(s + j, g + j);
+                cur_off = off;
+            }
+            // gather + split the 16 source multipoles: element (p, k, r) -> B row n = 6p + r, column k
+            for (int e = tid; e < kTP * kNC * 6; e += 128) {
+                const int p = e / (kNC * 6), q = e % (kNC * 6);
+                const int k = q / 6, r = q % 6;
+                const float x = (p < count) ? __ldg(mu + (size_t)srcb[begin + p] * kBoxStride + q) : 0.f;
+                const float h = tc::tf32_rna(x);
+                const uint32_t o = tc::core_offset(6 * p + r, k, kTcN) >> 2;
+                Bh[o] = h;
+                Bl[o] = x - h;
+            }
+            cp_async_wait_all();
+            tc::fence_proxy_async();
+            tc::fence_before();
+            __syncthreads();
+            tc::fence_after();
+            if (tid == 0) {
+                const uint32_t a0 = tc::smem_u32(Ah), al0 = tc::smem_u32(Al);
+                const uint32_t b0 = tc::smem_u32(Bh), bl0 = tc::smem_u32(Bl);
+#pragma unroll
+                for (int s2 = 0; s2 < 16; ++s2) {
+                    const uint64_t ah = tc::smem_desc(a0 + s2 * 2 * lboA, lboA, 128);
+                    const uint64_t al = tc::smem_desc(al0 + s2 * 2 * lboA, lboA, 128);
+                    const uint64_t bh = tc::smem_desc(b0 + s2 * 2 * lboB, lboB, 128);
+                    const uint64_t bl = tc::smem_desc(bl0 + s2 * 2 * lboB, lboB, 128);
+                    tc::mma_tf32(dtm, al, bh, idesc, s2 > 0);
+                    tc::mma_tf32(dtm, ah, bl, idesc, 1);
+                    tc::mma_tf32(dtm, ah, bh, idesc, 1);
+                }
+                tc::commit(&bar);
+            }
+            tc::mbar_wait(&bar, phase);
+            phase ^= 1;
+            tc::fence_after();
+            // epilogue: lane = coefficient i = 32*warp + lane; 96 columns = 16 pairs x 6 RHS
+            const int i = 32 * warp + lane;
+            float v[kTcN];
+            const uint32_t taddr = dtm + ((uint32_t)(32 * warp) << 16);
+            tc::tmem_ld32(taddr, v);
+            tc::tmem_ld32(taddr + 32, v + 32);
+            tc::tmem_ld32(taddr + 64, v + 64);
+            if (i < kNC) {
+#pragma unroll
+                for (int p = 0; p < kTP; ++p) {
+                    if (p >= count) break;
+                    float* o = ell + (size_t)tgt[begin + p] * kBoxStride + 6 * i;
+                    const float* x = v + 6 * p;
+                    if ((i & 1) == 0) {
+                        red_add_v4(o, x[0], x[1], x[2], x[3]);
+                        red_add_v2(o + 4, x[4], x[5]);
+                    } else {
+                        red_add_v2(o, x[0], x[1]);
+                        red_add_v4(o + 2, x[2], x[3], x[4], x[5]);
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<128>(tbase);
 }
 
 // ------------------------------------------------------------------ P2L (X list)
@@ -570,6 +694,35 @@ void upload_padded(DBuf<float>& dst, const std::vector<double>& src, int nmat)
     XRL_CUDA(cudaMemcpy(dst.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
 }
 
+float tf32_host(float x)
+{
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u = (u + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+// M2L operator images for k_m2l_tc: per offset, hi and lo tf32 parts of
+// T[i][k] (i, k < 121, zero padded to 128) in the core-matrix layout.
+void upload_tc_images(DBuf<float>& dst, const std::vector<double>& src)
+{
+    const size_t img = 128 * 128;
+    std::vector<float> h((size_t)kNM2L * 2 * img, 0.f);
+    for (int m = 0; m < kNM2L; ++m)
+        for (int i = 0; i < kNC; ++i)
+            for (int k = 0; k < kNC; ++k) {
+                const float a = (float)src[(size_t)m * kNC * kNC + (size_t)i * kNC + k];
+                const float hi = tf32_host(a);
+                const size_t o = tc::core_offset(i, k, 128) / 4;
+                h[(size_t)m * 2 * img + o] = hi;
+                h[(size_t)m * 2 * img + img + o] = a - hi;
+            }
+    dst.alloc(h.size());
+    XRL_CUDA(cudaMemcpy(dst.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+}
+
 }  // namespace
 
 namespace xrl {
@@ -583,6 +736,11 @@ void upload_constants(xrl_ctx ctx)
     upload_padded(ctx->ops.m2m, ops.m2m, 8);
     upload_padded(ctx->ops.l2l, ops.l2l, 8);
     upload_padded(ctx->ops.m2l, ops.m2l, kNM2L);
+    upload_tc_images(ctx->ops.m2l_tc, ops.m2l);
+    XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+    XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    const char* e = getenv("XRL_M2L_TC");   // tcgen05 3xTF32 M2L (opt-in)
+    ctx->m2l_simt = !(e && e[0] == '1');
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kM2LSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
@@ -647,9 +805,16 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
 
         phase_begin(ctx, PH_M2L, &ev, st);
         XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), st));
-        if (t->n_m2l_tiles > 0) {
+        if (t->n_m2l_tiles > 0 && ctx->m2l_simt) {
             k_m2l<<<t->n_m2l_tiles, 256, kM2LSmem, st>>>(t->m2l_tiles.p, t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l.p,
                                                          t->mu.p, t->ell.p);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+        } else if (t->n_m2l_tiles > 0) {
+            const int nblocks = (t->n_m2l_tiles + kTcR - 1) / kTcR;
+            const int grid = std::min(ctx->num_sms, nblocks);
+            k_m2l_tc<<<grid, 128, kTcSmem, st>>>(t->m2l_tiles.p, t->n_m2l_tiles, t->m2l_tgt.p, t->m2l_srcb.p,
+                                                 ctx->ops.m2l_tc.p, t->mu.p, t->ell.p);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }

@@ -700,7 +700,33 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     keys_to_csr(xkey.p, T->nx, T->x_ptr, T->x_src);
     T->nw = sort_valid(wkey, nxc);
     keys_to_csr(wkey.p, T->nw, T->w_ptr, T->w_src);
-    const int64_t nukx = sort_valid(ukx, nxc), nukw = sort_valid(ukw, nxc);
+    const int64_t nukx = sort_valid(ukx, nxc);
+    int64_t nukw = sort_valid(ukw, nxc);
+    // Direct W pairs (L <- w) whose source box w is not a leaf: P2P re-bases
+    // source panels relative to their own leaf, so expand w into its
+    // descendant leaves (contiguous panel ranges in Morton order).
+    DBuf<uint64_t> ukw_exp;
+    if (nukw) {
+        std::vector<uint64_t> hk(nukw);
+        XRL_CUDA(cudaMemcpyAsync(hk.data(), ukw.p, 8 * nukw, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<std::pair<int32_t, int32_t>> lf;  // (pb, leaf id) sorted by pb
+        for (int32_t b : hleaves) lf.push_back({hpb[b], b});
+        std::sort(lf.begin(), lf.end());
+        std::vector<uint64_t> ex;
+        ex.reserve(nukw);
+        for (uint64_t k : hk) {
+            const int32_t t = (int32_t)(k >> 32), w = (int32_t)(k & 0xffffffffu);
+            if (hchild[w] < 0) { ex.push_back(k); continue; }
+            auto it = std::lower_bound(lf.begin(), lf.end(), std::make_pair(hpb[w], INT32_MIN));
+            for (; it != lf.end() && it->first < hpe[w]; ++it)
+                ex.push_back(((uint64_t)(uint32_t)t << 32) | (uint32_t)it->second);
+        }
+        nukw = (int64_t)ex.size();
+        ukw_exp.alloc(nukw);
+        XRL_CUDA(cudaMemcpyAsync(ukw_exp.p, ex.data(), 8 * nukw, cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+    }
 
     // M2L pairs sorted by (offset, target)
     T->m2l_tgt.alloc(std::max<int64_t>(1, T->nv));
@@ -759,7 +785,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         k_u_emit<<<nblk(nbox, 128), 128, 0, st>>>(nbox, T->bchild.p, coll.p, ncoll.p, adjc.p, nadjc.p, uoff.p, ukey.p);
         XRL_LAUNCH_CHECK();
         if (nukx) XRL_CUDA(cudaMemcpyAsync(ukey.p + nadj, ukx.p, 8 * nukx, cudaMemcpyDeviceToDevice, st));
-        if (nukw) XRL_CUDA(cudaMemcpyAsync(ukey.p + nadj + nukx, ukw.p, 8 * nukw, cudaMemcpyDeviceToDevice, st));
+        if (nukw) XRL_CUDA(cudaMemcpyAsync(ukey.p + nadj + nukx, ukw_exp.p, 8 * nukw, cudaMemcpyDeviceToDevice, st));
         sort_pairs<uint64_t, int32_t>(ukey.p, nullptr, T->nu, 64, st);
         DBuf<int32_t> ut(T->nu);
         T->u_src.alloc(T->nu);

@@ -68,6 +68,7 @@ struct DeviceOperators {
     DBuf<float> m2m;   // [8][kNC (k, input)][kNCP (i, output, padded)]
     DBuf<float> l2l;   // [8][kNC][kNCP]
     DBuf<float> m2l;   // [316][kNC][kNCP]
+    DBuf<float> m2l_tc;  // [316][2 (hi, lo)][128 x 128 tf32, tcgen05 core-matrix layout]
     int m2l_index[343];
 };
 
@@ -86,6 +87,8 @@ struct xrl_ctx_s {
     xrl::DeviceOperators ops;
     // timing
     bool timing = false;
+    bool m2l_simt = true;             // false with XRL_M2L_TC=1: tcgen05 M2L
+    int num_sms = 148;
     int64_t launches = 0;
     int refs = 0;         // live trees
     bool dead = false;    // destroy requested

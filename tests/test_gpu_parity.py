@@ -89,6 +89,28 @@ def test_tree_lists_cover_every_pair_once(kind):
     print(kind, {k: info[k] for k in ("n_u_pairs", "n_v_pairs", "n_x_pairs", "n_w_pairs")})
 
 
+def _clustered_mesh():
+    rng = np.random.default_rng(3)
+    parts = []
+    for c, s, k in (((0, 0, 0), 1e-5, 300), ((3e-4, 1e-4, 0), 1e-5, 300), ((1e-4, 2e-4, 1e-4), 3e-4, 200)):
+        parts.append(rng.normal(size=(3 * k, 3)) * s + np.array(c))
+    v = np.concatenate(parts)
+    return meshes.Mesh(v, np.arange(v.shape[0], dtype=np.int32).reshape(-1, 3))
+
+
+@pytest.mark.parametrize("leaf_max", [4, 8, 16])
+def test_adaptive_lists_parity(leaf_max):
+    """Strongly non-uniform point set with small leaves: exercises kept
+    P2L/M2P pairs and X/W pairs converted to direct P2P (incl. non-leaf W
+    boxes expanded into their leaves)."""
+    m = _clustered_mesh()
+    ctx, tree, near = cuda_setup(m, leaf_max=leaf_max)
+    x = meshes.make_x(2, m.n)
+    err = oracle.rel_l2(run_mvm(tree, near, x), oracle_rows(m, x))
+    print("clustered leaf", leaf_max, err, tree.info())
+    assert err <= TOL_FULL
+
+
 def test_near_pattern_and_values_match_oracle(bar_setup):
     m, ctx, tree, near = bar_setup
     perm = tree.perm()
