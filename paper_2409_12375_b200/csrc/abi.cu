@@ -1,5 +1,6 @@
 // C-ABI plumbing: errors, context, timing (include/xrl.h).
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -8,6 +9,12 @@
 namespace xrl {
 
 static thread_local char g_err[1024] = "";
+
+bool sync_check_enabled()
+{
+    static const bool on = [] { const char* e = getenv("XRL_SYNC_CHECK"); return e && e[0] == '1'; }();
+    return on;
+}
 
 void set_error(const char* fmt, ...)
 {

@@ -473,8 +473,9 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
 // ------------------------------------------------------------------ near-field SpMV
 // y = N x for the 6 real RHS (N: FP32 CSR of the near correction and the self
 // terms).  HBM-bound: 8 B per nonzero (col + val) + the gathered charges
-// (L2-resident) + 24 B of y per row.  8 lanes per row, 4 rows per warp,
-// shuffle reduction over the 8 lanes.
+// (L2-resident) + 24 B of y per row.  8 lanes per row, 4 rows per warp; each
+// lane issues 4 independent (col, val) loads before their 4 gathers (memory-
+// level parallelism), shuffle reduction over the 8 lanes.
 __global__ void __launch_bounds__(256) k_near_spmv(int64_t n, const int64_t* __restrict__ ptr,
                                                    const int32_t* __restrict__ col, const float* __restrict__ val,
                                                    const float* __restrict__ xq, float2* __restrict__ y)
@@ -484,12 +485,12 @@ __global__ void __launch_bounds__(256) k_near_spmv(int64_t n, const int64_t* __r
     float a[6] = {0, 0, 0, 0, 0, 0};
     if (row < n) {
         const int64_t e = ptr[row + 1];
-#pragma unroll 2
+#pragma unroll 4
         for (int64_t j = ptr[row] + lane; j < e; j += 8) {
             const float v = __ldcs(val + j);
             const int64_t c = __ldcs(col + j);
-            const float4 q0 = __ldg(reinterpret_cast<const float4*>(xq + 8 * c));
-            const float2 q1 = __ldg(reinterpret_cast<const float2*>(xq + 8 * c) + 2);
+            const float4 q0 = reinterpret_cast<const float4*>(xq + 8 * c)[0];
+            const float2 q1 = reinterpret_cast<const float2*>(xq + 8 * c)[2];
             a[0] = fmaf(v, q0.x, a[0]); a[1] = fmaf(v, q0.y, a[1]); a[2] = fmaf(v, q0.z, a[2]);
             a[3] = fmaf(v, q0.w, a[3]); a[4] = fmaf(v, q1.x, a[4]); a[5] = fmaf(v, q1.y, a[5]);
         }
@@ -504,13 +505,46 @@ __global__ void __launch_bounds__(256) k_near_spmv(int64_t n, const int64_t* __r
 }
 
 // ------------------------------------------------------------------ P2P
-// One CTA (128 threads) per target leaf; targets in chunks of nt <= 64.  The
-// CTA is split into G = 128 / nt groups of nt threads (thread = (target,
-// group)); the U-list source panels are flattened, staged 512 at a time in
-// shared memory (coordinates re-based to the target leaf centre, W units)
-// and split over the groups.  y += (1/W) sum_{l != k} x_l / r_kl.
+// One CTA (128 threads) per target leaf; targets in passes of <= 128*kTPT.
+// Each thread owns kTPT consecutive targets (register blocking: one shared-
+// memory source load feeds kTPT pairs); with NG = ceil(T/kTPT) target groups
+// the CTA is split into S = 128/NG source groups.  U-list source leaves are
+// flattened (warp-parallel prefix sum), staged 512 panels at a time in shared
+// memory re-based to the target leaf centre (W units), and split over the
+// groups.  Only the target's own leaf needs the r = 0 (self) guard.
+// y += (1/W) sum_{l != k} x_l / r_kl.
 constexpr int kUWin = 64;
 constexpr int kSrcChunk = 512;
+constexpr int kTPT = 8;
+
+template <bool kSelf>
+__device__ __forceinline__ void p2p_range(int j0, int j1, int S, const float4* __restrict__ Sp,
+                                          const float4 (*__restrict__ Sq)[2], const float* tx, const float* ty,
+                                          const float* tz, float (*far)[6])
+{
+#pragma unroll 2
+    for (int j = j0; j < j1; j += S) {
+        const float4 sp = Sp[j];
+        const float4 q0 = Sq[j][0], q1 = Sq[j][1];
+#pragma unroll
+        for (int q = 0; q < kTPT; ++q) {
+            const float dx = tx[q] - sp.x, dy = ty[q] - sp.y, dz = tz[q] - sp.z;
+            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            float ri = rsqrtf(r2);
+            if (kSelf) ri = r2 > 0.f ? ri : 0.f;
+            far[q][0] = fmaf(q0.x, ri, far[q][0]); far[q][1] = fmaf(q0.y, ri, far[q][1]);
+            far[q][2] = fmaf(q0.z, ri, far[q][2]); far[q][3] = fmaf(q0.w, ri, far[q][3]);
+            far[q][4] = fmaf(q1.x, ri, far[q][4]); far[q][5] = fmaf(q1.y, ri, far[q][5]);
+        }
+    }
+}
+
+__device__ __forceinline__ int first_in_class(int lo, int sg, int S)
+{
+    // smallest j >= lo with j % S == sg
+    const int r = lo % S;
+    return lo + ((sg - r + S) % S);
+}
 
 __global__ void __launch_bounds__(128) k_p2p(
     const int32_t* __restrict__ leaves, const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
@@ -519,46 +553,74 @@ __global__ void __launch_bounds__(128) k_p2p(
     const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate, int64_t n,
     float2* __restrict__ y)
 {
-    __shared__ float4 Sp[kSrcChunk];
-    __shared__ float4 Sq[kSrcChunk][2];
-    __shared__ float Red[128][6];
-    __shared__ int Uoff[kUWin + 1], Uid[kUWin];
+    // the source staging buffers and the final reduction share one buffer
+    constexpr int kStageF = kSrcChunk * 12, kRedF = 128 * (kTPT * 6 + 1);
+    __shared__ __align__(16) float smraw[kStageF > kRedF ? kStageF : kRedF];
+    float4* Sp = reinterpret_cast<float4*>(smraw);
+    float4(*Sq)[2] = reinterpret_cast<float4(*)[2]>(smraw + 4 * kSrcChunk);
+    float(*Red)[kTPT * 6 + 1] = reinterpret_cast<float(*)[kTPT * 6 + 1]>(smraw);
+    __shared__ int Uoff[kUWin + 1], Uid[kUWin], Upb[kUWin];
     __shared__ float3 Ud[kUWin];
+    __shared__ int wsum[2];
     const int b = leaves[blockIdx.x];
     const float3 cb = box_center(level[b], ix[b], iy[b], iz[b]);
-    const int tid = threadIdx.x;
-    for (int t0 = pb[b]; t0 < pe[b]; t0 += 64) {
-        const int nt = min(64, pe[b] - t0);
-        const int G = 128 / nt;
-        const int t = tid % nt, g = tid / nt;
-        const bool act = g < G;
-        const int ti = t0 + t;
-        float4 tp = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (act) tp = loc[ti];
-        float far[6] = {0, 0, 0, 0, 0, 0};
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int t0 = pb[b]; t0 < pe[b]; t0 += 128 * kTPT) {
+        const int T = min(128 * kTPT, pe[b] - t0);
+        const int NG = (T + kTPT - 1) / kTPT;
+        const int S = max(1, 128 / NG);
+        const int tg = tid % NG, sg = tid / NG;
+        const bool act = sg < S;
+        float tx[kTPT], ty[kTPT], tz[kTPT];
+        float far[kTPT][6];
+#pragma unroll
+        for (int q = 0; q < kTPT; ++q) {
+            const int ti = tg * kTPT + q;
+            float4 p = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // padding target: far away, discarded
+            if (act && ti < T) p = loc[t0 + ti];
+            tx[q] = p.x; ty[q] = p.y; tz[q] = p.z;
+#pragma unroll
+            for (int r = 0; r < 6; ++r) far[q][r] = 0.f;
+        }
         for (int64_t u0 = uptr[b]; u0 < uptr[b + 1]; u0 += kUWin) {
             const int nu = (int)min((int64_t)kUWin, uptr[b + 1] - u0);
             __syncthreads();
-            if (tid < nu) {
-                const int s = usrc[u0 + tid];
-                Uid[tid] = s;
-                const float3 cs = box_center(level[s], ix[s], iy[s], iz[s]);
-                Ud[tid] = make_float3(cs.x - cb.x, cs.y - cb.y, cs.z - cb.z);
-            }
-            if (tid == 0) {
-                int o = 0;
-                for (int i = 0; i < nu; ++i) { Uoff[i] = o; const int s = usrc[u0 + i]; o += pe[s] - pb[s]; }
-                Uoff[nu] = o;
+            // window setup: ids, centre shifts and an exclusive prefix of the leaf sizes (2 warps)
+            int sz = 0;
+            if (tid < kUWin) {
+                if (tid < nu) {
+                    const int s = usrc[u0 + tid];
+                    Uid[tid] = s;
+                    Upb[tid] = pb[s];
+                    sz = pe[s] - pb[s];
+                    const float3 cs = box_center(level[s], ix[s], iy[s], iz[s]);
+                    Ud[tid] = make_float3(cs.x - cb.x, cs.y - cb.y, cs.z - cb.z);
+                }
+                int inc = sz;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                if (lane == 31) wsum[warp] = inc;
+                Uoff[tid + 1] = inc;  // provisional (warp-local)
             }
             __syncthreads();
+            if (tid >= 32 && tid < kUWin) Uoff[tid + 1] += wsum[0];
+            if (tid == 0) Uoff[0] = 0;
+            __syncthreads();
             const int total = Uoff[nu];
+            // the target leaf's own panels in the flattened window (needs the r = 0 guard)
+            int self_lo = 0, self_hi = 0;
+            for (int i = 0; i < nu; ++i)
+                if (Uid[i] == b) { self_lo = Uoff[i]; self_hi = Uoff[i + 1]; }
             for (int s0 = 0; s0 < total; s0 += kSrcChunk) {
                 const int sn = min(kSrcChunk, total - s0);
                 if (s0 > 0) __syncthreads();
                 for (int j = tid; j < sn; j += 128) {
                     const int f = s0 + j;
                     const int li = find_seg(Uoff, nu, f);
-                    const int i = pb[Uid[li]] + (f - Uoff[li]);
+                    const int i = Upb[li] + (f - Uoff[li]);
                     const float3 d = Ud[li];
                     const float4 p = loc[i];
                     Sp[j] = make_float4(p.x + d.x, p.y + d.y, p.z + d.z, 0.f);
@@ -568,40 +630,39 @@ __global__ void __launch_bounds__(128) k_p2p(
                 }
                 __syncthreads();
                 if (act) {
-#pragma unroll 4
-                    for (int j = g; j < sn; j += G) {
-                        const float4 sp = Sp[j];
-                        const float dx = tp.x - sp.x, dy = tp.y - sp.y, dz = tp.z - sp.z;
-                        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                        const float ri = r2 > 0.f ? rsqrtf(r2) : 0.f;
-                        const float4 q0 = Sq[j][0], q1 = Sq[j][1];
-                        far[0] = fmaf(q0.x, ri, far[0]); far[1] = fmaf(q0.y, ri, far[1]);
-                        far[2] = fmaf(q0.z, ri, far[2]); far[3] = fmaf(q0.w, ri, far[3]);
-                        far[4] = fmaf(q1.x, ri, far[4]); far[5] = fmaf(q1.y, ri, far[5]);
-                    }
+                    const int a0 = max(0, min(sn, self_lo - s0)), a1 = max(0, min(sn, self_hi - s0));
+                    p2p_range<false>(first_in_class(0, sg, S), a0, S, Sp, Sq, tx, ty, tz, far);
+                    p2p_range<true>(first_in_class(a0, sg, S), a1, S, Sp, Sq, tx, ty, tz, far);
+                    p2p_range<false>(first_in_class(a1, sg, S), sn, S, Sp, Sq, tx, ty, tz, far);
                 }
             }
         }
         __syncthreads();
 #pragma unroll
-        for (int r = 0; r < 6; ++r) Red[tid][r] = far[r];
+        for (int q = 0; q < kTPT; ++q)
+#pragma unroll
+            for (int r = 0; r < 6; ++r) Red[tid][q * 6 + r] = far[q][r];
         __syncthreads();
-        if (tid < nt) {
+        // reduce over the S source groups: thread handles target index ti = tid, tid + 128, ...
+        for (int ti = tid; ti < T; ti += 128) {
+            const int g0 = ti / kTPT, q = ti % kTPT;
             float tot[6];
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
                 float f = 0.f;
-                for (int gg = 0; gg < G; ++gg) f += Red[tid + gg * nt][r];
+                for (int gg = 0; gg < S; ++gg) f += Red[g0 + gg * NG][q * 6 + r];
                 tot[r] = f * invW;
             }
+            const int64_t k = t0 + ti;
             if (accumulate) {
-                const float2 a = y[ti], c = y[n + ti], d = y[2 * n + ti];
+                const float2 a = y[k], c = y[n + k], d = y[2 * n + k];
                 tot[0] += a.x; tot[1] += a.y; tot[2] += c.x; tot[3] += c.y; tot[4] += d.x; tot[5] += d.y;
             }
-            y[ti] = make_float2(tot[0], tot[1]);
-            y[n + ti] = make_float2(tot[2], tot[3]);
-            y[2 * n + ti] = make_float2(tot[4], tot[5]);
+            y[k] = make_float2(tot[0], tot[1]);
+            y[n + k] = make_float2(tot[2], tot[3]);
+            y[2 * n + k] = make_float2(tot[4], tot[5]);
         }
+        __syncthreads();
     }
 }
 

@@ -32,7 +32,12 @@ struct CudaError {
         }                                                                                    \
     } while (0)
 
-#define XRL_LAUNCH_CHECK() XRL_CUDA(cudaGetLastError())
+bool sync_check_enabled();  // XRL_SYNC_CHECK=1: synchronize after every launch (debugging)
+#define XRL_LAUNCH_CHECK()                                                                   \
+    do {                                                                                     \
+        XRL_CUDA(cudaGetLastError());                                                        \
+        if (::xrl::sync_check_enabled()) XRL_CUDA(cudaDeviceSynchronize());                  \
+    } while (0)
 
 // Simple owning device buffer.
 template <typename T>

@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/status.txt
+for L in 64 128 256 512 1024; do
+timeout 600 python bench.py --steps 5 --warmup 3 --leaf $L --no-cpu-baseline > gpurun_out/bench_leaf$L.log 2>&1; echo "bench leaf$L rc=$?" >> gpurun_out/status.txt
+done
+cat gpurun_out/status.txt
