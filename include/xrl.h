@@ -89,12 +89,28 @@ void xrl_ctx_destroy(xrl_ctx ctx);
 
 /* FMM options.  p: expansion order (only 10 is compiled, PAPER.md silent ->
  * north star p = 10); leaf_max: split a box while it holds more panels
- * (default 64); max_depth: <= 21 (63-bit Morton keys). */
+ * (default 64); max_depth: <= 21 (63-bit Morton keys).
+ * part_rank / part_world: Morton-range partition of the targets (SURVEY
+ * §8(e)).  On a multi-rank context they must equal its rank / world (or be
+ * 0 / 0).  On a single-rank context part_world > 1 builds rank part_rank's
+ * share only ("virtual partition", for testing the sharded path on one GPU
+ * through xrl_mvm_gathered).  0 / 0 = no partition. */
 typedef struct {
     int32_t p;
     int32_t leaf_max;
     int32_t max_depth;
+    int32_t part_rank;
+    int32_t part_world;
 } xrl_fmm_opts;
+
+/* Balanced contiguous cuts of n weighted items into `world` ranges:
+ * cuts[r] .. cuts[r+1] is range r (int64 [world+1]); the partition rule of
+ * the sharded MVM (leaf work estimates in Morton order).  Host function. */
+xrl_status xrl_partition_cuts(int64_t n, const double* weights, int32_t world, int64_t* cuts);
+
+/* 128-byte ncclUniqueId for xrl_ctx_create (rank 0 generates it, the caller
+ * broadcasts it to the other ranks, e.g. through torch.distributed). */
+xrl_status xrl_nccl_unique_id(void* out128);
 
 /* Octree build on the GPU (setup, once per mesh).
  * vert: host FP64 [n_vert][3] (m); tri: host int32 [n_tri][3].
@@ -160,13 +176,22 @@ xrl_status xrl_near_export(xrl_near near, int64_t* row_ptr, int32_t* col, float*
                            double* val64, int64_t* nnz);
 
 /* The hot path: y = P x (flags select diagnostic parts).
- * x, y: device complex64 [nvec][n_local] in library order, must not alias;
+ * x, y: device complex64 [nvec][n_local] in library order (this rank's slice
+ * [offset, offset + n_local) on a multi-rank context: the slices are
+ * gathered with NCCL inside the call), must not alias;
  * nvec a multiple of 3 (each triple of complex components = 6 real RHS through
  * one tree traversal).  Enqueued on the context stream. */
 xrl_status xrl_mvm(xrl_tree tree, xrl_near near, const void* x, void* y, int32_t nvec, uint32_t flags);
 
+/* As xrl_mvm, but x is already the full vector [nvec][n] (library order) and y
+ * this rank's slice [nvec][n_local]; no communication.  Used for the virtual
+ * partition on one GPU and by tests. */
+xrl_status xrl_mvm_gathered(xrl_tree tree, xrl_near near, const void* x_full, void* y, int32_t nvec, uint32_t flags);
+
 /* End-to-end variant with HOST complex64 buffers [nvec][n] in the mesh's
- * original panel order: H2D copy, reorder, MVM, reorder, D2H copy.  Blocking. */
+ * original panel order: H2D copy, reorder, MVM, reorder, D2H copy.  Blocking.
+ * On a multi-rank context the host buffers are the rank's slice
+ * [nvec][n_local] in library order (H2D, MVM with the NCCL gather, D2H). */
 xrl_status xrl_mvm_host(xrl_tree tree, xrl_near near, const void* x_host, void* y_host, int32_t nvec,
                         uint32_t flags);
 

@@ -19,7 +19,23 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
                   "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["abi.cu", "tree.cu", "near.cu", "fmm.cu", "solver.cu", "operators.cpp", "topology.cpp"]
+SOURCES = ["abi.cu", "tree.cu", "near.cu", "fmm.cu", "solver.cu", "comm.cu", "operators.cpp", "topology.cpp"]
+
+
+def _nccl_dirs():
+    """NCCL bundled with torch (the version torch.distributed loads), else the system one."""
+    try:
+        import nvidia.nccl as nn
+        base = nn.__path__[0]
+        if os.path.exists(os.path.join(base, "include", "nccl.h")):
+            return os.path.join(base, "include"), os.path.join(base, "lib")
+    except Exception:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+NCCL_INC, NCCL_LIB = _nccl_dirs()
+CUFLAGS = CUFLAGS + ["-I" + NCCL_INC]
 HEADERS = ["xrl_internal.h", "harmonics.h", "operators.h"]
 
 
@@ -55,7 +71,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if log:
                 print(f"--- {os.path.basename(o)}\n{log}")
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fopenmp", "-o", LIB + ".tmp"] + objs + ["-lcudart"]
+        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fopenmp", "-o", LIB + ".tmp"] + objs + [
+            "-lcudart", "-L" + NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + NCCL_LIB]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

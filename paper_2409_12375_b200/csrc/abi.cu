@@ -116,12 +116,11 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         XRL_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-        if (world > 1) {
-            delete c;
-            set_error("multi-rank contexts are not built in this version");
-            return XRL_EUNSUPPORTED;
-        }
         upload_constants(c);
+        if (world > 1) {
+            xrl_status st = comm_init(c, nccl_unique_id);
+            if (st) { delete c; return st; }
+        }
         *out = c;
         return XRL_OK;
     XRL_CATCH
@@ -153,6 +152,7 @@ void xrl::ctx_release(xrl_ctx ctx)
     cudaStreamSynchronize(ctx->stream);
     for (auto& p : ctx->pending) { cudaEventDestroy(p.second.first); cudaEventDestroy(p.second.second); }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    comm_destroy(ctx);
     if (ctx->side) { cudaStreamSynchronize(ctx->side); cudaStreamDestroy(ctx->side); }
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);

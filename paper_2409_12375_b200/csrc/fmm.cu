@@ -151,12 +151,13 @@ __global__ void __launch_bounds__(128) k_m2m(const int32_t* __restrict__ parents
     }
 }
 
-__global__ void __launch_bounds__(128) k_l2l(int b0, const int32_t* __restrict__ parent, const int32_t* __restrict__ ix,
-                                             const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
-                                             const float* __restrict__ op, float* __restrict__ ell)
+__global__ void __launch_bounds__(128) k_l2l(const int32_t* __restrict__ boxes, const int32_t* __restrict__ parent,
+                                             const int32_t* __restrict__ ix, const int32_t* __restrict__ iy,
+                                             const int32_t* __restrict__ iz, const float* __restrict__ op,
+                                             float* __restrict__ ell)
 {
     __shared__ float src[kBoxStride];
-    const int b = b0 + blockIdx.x;
+    const int b = boxes[blockIdx.x];
     const int P = parent[b];
     for (int j = threadIdx.x; j < kBoxStride / 4; j += blockDim.x)
         reinterpret_cast<float4*>(src)[j] = reinterpret_cast<const float4*>(ell + (size_t)P * kBoxStride)[j];
@@ -476,14 +477,16 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
 // (L2-resident) + 24 B of y per row.  8 lanes per row, 4 rows per warp; each
 // lane issues 4 independent (col, val) loads before their 4 gathers (memory-
 // level parallelism), shuffle reduction over the 8 lanes.
-__global__ void __launch_bounds__(256) k_near_spmv(int64_t n, const int64_t* __restrict__ ptr,
+__global__ void __launch_bounds__(256) k_near_spmv(int64_t n, int64_t r0, const int64_t* __restrict__ ptr,
                                                    const int32_t* __restrict__ col, const float* __restrict__ val,
                                                    const float* __restrict__ xq, float2* __restrict__ y)
 {
-    const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+    // rows r0 .. r0+n-1 (owned range); y local [3][n]
+    const int64_t lrow = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+    const int64_t row = r0 + lrow;
     const int lane = threadIdx.x & 7;
     float a[6] = {0, 0, 0, 0, 0, 0};
-    if (row < n) {
+    if (lrow < n) {
         const int64_t e = ptr[row + 1];
 #pragma unroll 4
         for (int64_t j = ptr[row] + lane; j < e; j += 8) {
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(256) k_near_spmv(int64_t n, const int64_t* __r
         a[r] += __shfl_xor_sync(0xffffffffu, a[r], 2);
         a[r] += __shfl_xor_sync(0xffffffffu, a[r], 4);
     }
-    if (row < n && lane < 3) y[lane * n + row] = make_float2(a[2 * lane], a[2 * lane + 1]);
+    if (lrow < n && lane < 3) y[lane * n + lrow] = make_float2(a[2 * lane], a[2 * lane + 1]);
 }
 
 // ------------------------------------------------------------------ P2P
@@ -551,8 +554,9 @@ __global__ void __launch_bounds__(128) k_p2p(
     const int32_t* __restrict__ iy, const int32_t* __restrict__ iz, const int32_t* __restrict__ pb,
     const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
     const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate, int64_t n,
-    float2* __restrict__ y)
+    int64_t p0, float2* __restrict__ y)
 {
+    // n, p0: owned panel range [p0, p0+n), y local [3][n]
     // the source staging buffers and the final reduction share one buffer
     constexpr int kStageF = kSrcChunk * 12, kRedF = 128 * (kTPT * 6 + 1);
     __shared__ __align__(16) float smraw[kStageF > kRedF ? kStageF : kRedF];
@@ -653,7 +657,7 @@ __global__ void __launch_bounds__(128) k_p2p(
                 for (int gg = 0; gg < S; ++gg) f += Red[g0 + gg * NG][q * 6 + r];
                 tot[r] = f * invW;
             }
-            const int64_t k = t0 + ti;
+            const int64_t k = t0 + ti - p0;
             if (accumulate) {
                 const float2 a = y[k], c = y[n + k], d = y[2 * n + k];
                 tot[0] += a.x; tot[1] += a.y; tot[2] += c.x; tot[3] += c.y; tot[4] += d.x; tot[5] += d.y;
@@ -668,15 +672,16 @@ __global__ void __launch_bounds__(128) k_p2p(
 
 // ------------------------------------------------------------------ L2P + M2P
 // One thread per target panel: y += (1/W) [ (1/s_b) sum ell_b Rt(u) + sum_{w in W(b)} (1/s_w) sum c mu_w It(u_w) ].
-__global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, const int32_t* __restrict__ panel_leaf,
+__global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, int64_t p0, const int32_t* __restrict__ panel_leaf,
                                                  const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
                                                  const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
                                                  const int64_t* __restrict__ wptr, const int32_t* __restrict__ wsrc,
                                                  const float4* __restrict__ loc, const float* __restrict__ mu,
                                                  const float* __restrict__ ell, float invW, float2* __restrict__ y)
 {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // local index, panel p0 + li
+    if (li >= n) return;
+    const int64_t i = p0 + li;
     const int b = panel_leaf[i];
     const int lb = level[b];
     const float3 cb = box_center(lb, ix[b], iy[b], iz[b]);
@@ -718,10 +723,10 @@ __global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, const int32_t* __res
 #pragma unroll
         for (int r = 0; r < 6; ++r) far[r] = fmaf(a[r], inv_sw, far[r]);
     }
-    float2 a = y[i], c = y[n + i], d = y[2 * n + i];
-    y[i] = make_float2(fmaf(far[0], invW, a.x), fmaf(far[1], invW, a.y));
-    y[n + i] = make_float2(fmaf(far[2], invW, c.x), fmaf(far[3], invW, c.y));
-    y[2 * n + i] = make_float2(fmaf(far[4], invW, d.x), fmaf(far[5], invW, d.y));
+    float2 a = y[li], c = y[n + li], d = y[2 * n + li];
+    y[li] = make_float2(fmaf(far[0], invW, a.x), fmaf(far[1], invW, a.y));
+    y[n + li] = make_float2(fmaf(far[2], invW, c.x), fmaf(far[3], invW, c.y));
+    y[2 * n + li] = make_float2(fmaf(far[4], invW, d.x), fmaf(far[5], invW, d.y));
 }
 
 __global__ void k_permute(int64_t n, int nvec, const int32_t* __restrict__ idx, const float2* __restrict__ in,
@@ -809,11 +814,13 @@ void upload_constants(xrl_ctx ctx)
 
 }  // namespace xrl
 
+// x: full (gathered) triple [3][n]; y: owned slice [3][n_local] of panels [p0, p1).
 static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags)
 {
     xrl_ctx ctx = t->ctx;
     cudaStream_t st = ctx->stream, side = ctx->side;
     const int64_t n = t->n;
+    const int64_t nl = t->p1 - t->p0, p0 = t->p0;
     const bool do_far = flags != XRL_MVM_NEAR_ONLY;
     const bool do_near = flags != XRL_MVM_FAR_ONLY;
     const float invW = (float)(1.0 / t->W);
@@ -831,15 +838,17 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
     XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
     if (do_near) {
         phase_begin(ctx, PH_NEAR, &ev, side);
-        k_near_spmv<<<nblk(8 * n, 256), 256, 0, side>>>(n, nr->row_ptr.p, nr->col.p, nr->val.p, t->xq.p, y);
+        if (nl > 0) k_near_spmv<<<nblk(8 * nl, 256), 256, 0, side>>>(nl, p0, nr->row_ptr.p, nr->col.p, nr->val.p, t->xq.p, y);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
         phase_end(ctx, PH_NEAR, ev, side);
     }
     if (do_far) {
         phase_begin(ctx, PH_P2P, &ev, side);
-        k_p2p<<<t->nleaf, 128, 0, side>>>(t->leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p, t->bpe.p,
-                                          t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW, do_near ? 1 : 0, n, y);
+        if (t->n_own_leaves > 0)
+            k_p2p<<<t->n_own_leaves, 128, 0, side>>>(t->own_leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
+                                                     t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
+                                                     invW, do_near ? 1 : 0, nl, p0, y);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
         phase_end(ctx, PH_P2P, ev, side);
@@ -893,8 +902,10 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
 
         phase_begin(ctx, PH_L2L, &ev, st);
         for (int l = 3; l < t->nlevel; ++l) {
-            const int b0 = t->lvl_start[l], nb = t->lvl_start[l + 1] - b0;
-            k_l2l<<<nb, 128, 0, st>>>(b0, t->bparent.p, t->bix.p, t->biy.p, t->biz.p, ctx->ops.l2l.p, t->ell.p);
+            const int b0 = t->l2l_start[l], nb = t->l2l_start[l + 1] - b0;
+            if (nb == 0) continue;
+            k_l2l<<<nb, 128, 0, st>>>(t->l2l_boxes.p + b0, t->bparent.p, t->bix.p, t->biy.p, t->biz.p, ctx->ops.l2l.p,
+                                      t->ell.p);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -902,9 +913,9 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
     }
     // join, then the local-expansion / W-list evaluation completes y
     XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-    if (do_far && t->nlevel > 1) {
+    if (do_far && t->nlevel > 1 && nl > 0) {
         phase_begin(ctx, PH_L2P, &ev, st);
-        k_l2p_m2p<<<nblk(n, 128), 128, 0, st>>>(n, t->panel_leaf.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
+        k_l2p_m2p<<<nblk(nl, 128), 128, 0, st>>>(nl, p0, t->panel_leaf.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
                                                 t->w_ptr.p, t->w_src.p, t->loc.p, t->mu.p, t->ell.p, invW, y);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
@@ -924,8 +935,41 @@ xrl_status xrl_mvm(xrl_tree t, xrl_near nr, const void* x, void* y, int32_t nvec
     if (((uintptr_t)x | (uintptr_t)y) & 15) { set_error("xrl_mvm: vectors must be 16-byte aligned"); return XRL_EINVAL; }
     try {
         XRL_CUDA(cudaSetDevice(t->ctx->device));
+        const int64_t nl = t->p1 - t->p0;
+        if (t->part_world == 1) {
+            for (int v = 0; v < nvec; v += 3)
+                mvm_triple(t, nr, (const float2*)x + (size_t)v * t->n, (float2*)y + (size_t)v * t->n, flags);
+            return XRL_OK;
+        }
+        if (t->ctx->world == 1) {
+            set_error("xrl_mvm: virtual partition (part_world > 1 on a single-rank context) needs xrl_mvm_gathered");
+            return XRL_EUNSUPPORTED;
+        }
+        if (t->xfull.n < (size_t)3 * t->n) t->xfull.alloc((size_t)3 * t->n);
+        for (int v = 0; v < nvec; v += 3) {
+            // gather the owned slices of the 3 components into the full vectors (NCCL over NVLink)
+            xrl_status s = gather_slices(t, (const float2*)x + (size_t)v * nl, t->xfull.p);
+            if (s) return s;
+            mvm_triple(t, nr, t->xfull.p, (float2*)y + (size_t)v * nl, flags);
+        }
+        return XRL_OK;
+    } catch (const CudaError& e) {
+        return e.code;
+    }
+}
+
+xrl_status xrl_mvm_gathered(xrl_tree t, xrl_near nr, const void* x_full, void* y, int32_t nvec, uint32_t flags)
+{
+    if (!t || !nr || !x_full || !y) { set_error("xrl_mvm_gathered: null argument"); return XRL_EINVAL; }
+    if (nr->tree != t) { set_error("xrl_mvm_gathered: near handle built from another tree"); return XRL_EPROVENANCE; }
+    if (nvec < 3 || nvec % 3) { set_error("xrl_mvm_gathered: nvec=%d must be a positive multiple of 3", nvec); return XRL_EDIM; }
+    if (x_full == y) { set_error("xrl_mvm_gathered: x and y alias"); return XRL_EINVAL; }
+    if (flags > XRL_MVM_FAR_ONLY) { set_error("xrl_mvm_gathered: bad flags"); return XRL_EINVAL; }
+    try {
+        XRL_CUDA(cudaSetDevice(t->ctx->device));
+        const int64_t nl = t->p1 - t->p0;
         for (int v = 0; v < nvec; v += 3)
-            mvm_triple(t, nr, (const float2*)x + (size_t)v * t->n, (float2*)y + (size_t)v * t->n, flags);
+            mvm_triple(t, nr, (const float2*)x_full + (size_t)v * t->n, (float2*)y + (size_t)v * nl, flags);
         return XRL_OK;
     } catch (const CudaError& e) {
         return e.code;
@@ -969,6 +1013,18 @@ xrl_status xrl_mvm_host(xrl_tree t, xrl_near nr, const void* x_host, void* y_hos
     try {
         cudaStream_t st = t->ctx->stream;
         XRL_CUDA(cudaSetDevice(t->ctx->device));
+        if (t->part_world > 1) {
+            // multi-rank: host buffers are this rank's slice [nvec][n_local] in library order
+            if (t->ctx->world == 1) { set_error("xrl_mvm_host: virtual partition not supported"); return XRL_EUNSUPPORTED; }
+            const size_t cl = (size_t)nvec * (t->p1 - t->p0);
+            if (t->xlib.n < cl) { t->xlib.alloc(cl); t->ylib.alloc(cl); }
+            XRL_CUDA(cudaMemcpyAsync(t->xlib.p, x_host, cl * 8, cudaMemcpyHostToDevice, st));
+            xrl_status s = xrl_mvm(t, nr, t->xlib.p, t->ylib.p, nvec, flags);
+            if (s) return s;
+            XRL_CUDA(cudaMemcpyAsync(y_host, t->ylib.p, cl * 8, cudaMemcpyDeviceToHost, st));
+            XRL_CUDA(cudaStreamSynchronize(st));
+            return XRL_OK;
+        }
         const size_t cnt = (size_t)nvec * t->n;
         if (t->xtmp.n < cnt) { t->xtmp.alloc(cnt); t->ytmp.alloc(cnt); t->xlib.alloc(cnt); t->ylib.alloc(cnt); }
         float2 *xl = t->xlib.p, *yl = t->ylib.p;

@@ -472,6 +472,8 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     T->h_vert.assign(vert_h, vert_h + 3 * n_vert);
     T->h_tri.assign(tri_h, tri_h + 3 * n);
     T->max_depth = opts ? opts->max_depth : kMortonBits;
+    T->part_rank = ctx->world > 1 ? ctx->rank : (opts ? opts->part_rank : 0);
+    T->part_world = ctx->world > 1 ? ctx->world : (opts && opts->part_world > 0 ? opts->part_world : 1);
 
     DBuf<double> vert(3 * n_vert);
     DBuf<int32_t> tri(3 * n);
@@ -728,47 +730,6 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         XRL_CUDA(cudaStreamSynchronize(st));
     }
 
-    // M2L pairs sorted by (offset, target)
-    T->m2l_tgt.alloc(std::max<int64_t>(1, T->nv));
-    T->m2l_srcb.alloc(std::max<int64_t>(1, T->nv));
-    XRL_CUDA(cudaMemcpyAsync(T->m2l_srcb.p, T->v_src.p, 4 * T->nv, cudaMemcpyDeviceToDevice, st));
-    sort_pairs(vkey.p, T->m2l_srcb.p, T->nv, 64, st);
-    {
-        DBuf<int32_t> offs(std::max<int64_t>(1, T->nv));
-        if (T->nv) {
-            k_split_keys<<<nblk(T->nv, 256), 256, 0, st>>>(T->nv, vkey.p, offs.p, T->m2l_tgt.p);
-            XRL_LAUNCH_CHECK();
-        }
-        std::vector<int32_t> ho(T->nv);
-        if (T->nv) XRL_CUDA(cudaMemcpyAsync(ho.data(), offs.p, 4 * T->nv, cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaStreamSynchronize(st));
-        std::vector<int4> tiles;
-        const int TP = 16;
-        int64_t i = 0;
-        while (i < T->nv) {
-            int64_t j = i;
-            while (j < T->nv && ho[j] == ho[i]) ++j;  // same (chunk, offset)
-            for (int64_t s = i; s < j; s += TP)
-                tiles.push_back(make_int4(ho[i] & 511, (int)s, (int)std::min<int64_t>(TP, j - s), ho[i] >> 9));
-            i = j;
-        }
-        T->n_m2l_tiles = (int)tiles.size();
-        T->m2l_tiles.alloc(std::max<size_t>(1, tiles.size()));
-        if (!tiles.empty())
-            XRL_CUDA(cudaMemcpyAsync(T->m2l_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
-    }
-    // X targets (boxes with kept P2L pairs)
-    {
-        std::vector<int64_t> hx(nbox + 1);
-        XRL_CUDA(cudaMemcpyAsync(hx.data(), T->x_ptr.p, 8 * (nbox + 1), cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaStreamSynchronize(st));
-        std::vector<int32_t> xt;
-        for (int b = 0; b < nbox; ++b)
-            if (hx[b + 1] > hx[b]) xt.push_back(b);
-        T->n_x_targets = (int)xt.size();
-        T->x_targets.alloc(std::max<size_t>(1, xt.size()));
-        if (!xt.empty()) XRL_CUDA(cudaMemcpyAsync(T->x_targets.p, xt.data(), 4 * xt.size(), cudaMemcpyHostToDevice, st));
-    }
     // U lists
     {
         DBuf<int64_t> ucnt(nbox), uoff(nbox);
@@ -803,6 +764,116 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         XRL_CUDA(cudaStreamSynchronize(st));
         T->np2p = (int64_t)ht;
     }
+    // ---- partition over ranks: contiguous Morton ranges of
+    // leaves balanced by estimated work; this rank owns panels [p0, p1).
+    {
+        std::vector<int64_t> hup(nbox + 1), hvp(nbox + 1);
+        std::vector<int32_t> hus(std::max<int64_t>(1, T->nu));
+        XRL_CUDA(cudaMemcpyAsync(hup.data(), T->u_ptr.p, 8 * (nbox + 1), cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaMemcpyAsync(hvp.data(), T->v_ptr.p, 8 * (nbox + 1), cudaMemcpyDeviceToHost, st));
+        if (T->nu) XRL_CUDA(cudaMemcpyAsync(hus.data(), T->u_src.p, 4 * T->nu, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<std::pair<int32_t, int32_t>> lf;
+        for (int32_t b : hleaves) lf.push_back({hpb[b], b});
+        std::sort(lf.begin(), lf.end());
+        std::vector<double> w(lf.size());
+        for (size_t i = 0; i < lf.size(); ++i) {
+            const int L = lf[i].second;
+            const double nL = hpe[L] - hpb[L];
+            double src = 0;
+            for (int64_t q = hup[L]; q < hup[L + 1]; ++q) src += hpe[hus[q]] - hpb[hus[q]];
+            double m2l = 0;
+            for (int a = L; a >= 0; a = hpar[a]) m2l += double(hvp[a + 1] - hvp[a]) * nL / double(hpe[a] - hpb[a]);
+            w[i] = 20.0 * nL * src + 175692.0 * m2l + 4000.0 * nL;
+        }
+        std::vector<int64_t> cuts(T->part_world + 1);
+        xrl_partition_cuts((int64_t)w.size(), w.data(), T->part_world, cuts.data());
+        const int64_t l0 = cuts[T->part_rank], l1 = cuts[T->part_rank + 1];
+        T->p0 = l0 < (int64_t)lf.size() ? hpb[lf[l0].second] : (int32_t)n;
+        T->p1 = l1 > l0 ? hpe[lf[l1 - 1].second] : T->p0;
+        if (l1 <= l0) T->p1 = T->p0;
+        T->part_cuts.resize(T->part_world + 1);
+        for (int r = 0; r <= T->part_world; ++r)
+            T->part_cuts[r] = cuts[r] < (int64_t)lf.size() ? hpb[lf[cuts[r]].second] : (int32_t)n;
+        std::vector<int32_t> own;
+        for (int64_t i = l0; i < l1; ++i) own.push_back(lf[i].second);
+        T->n_own_leaves = (int)own.size();
+        T->own_leaves.alloc(std::max<size_t>(1, own.size()));
+        if (!own.empty()) XRL_CUDA(cudaMemcpyAsync(T->own_leaves.p, own.data(), 4 * own.size(), cudaMemcpyHostToDevice, st));
+        // relevant boxes: panel range meets [p0, p1) (owned subtrees and their ancestors)
+        T->rel.assign(nbox, 0);
+        for (int b = 0; b < nbox; ++b) T->rel[b] = hpb[b] < T->p1 && hpe[b] > T->p0;
+        // L2L lists per level (levels >= 3)
+        std::vector<int32_t> l2l;
+        T->l2l_start.assign(nlev + 1, 0);
+        for (int l = 0; l < nlev; ++l) {
+            T->l2l_start[l] = (int)l2l.size();
+            if (l >= 3)
+                for (int b = T->lvl_start[l]; b < T->lvl_start[l + 1]; ++b)
+                    if (T->rel[b]) l2l.push_back(b);
+        }
+        T->l2l_start[nlev] = (int)l2l.size();
+        T->l2l_boxes.alloc(std::max<size_t>(1, l2l.size()));
+        if (!l2l.empty()) XRL_CUDA(cudaMemcpyAsync(T->l2l_boxes.p, l2l.data(), 4 * l2l.size(), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+    }
+    // M2L pairs sorted by (offset, target)
+    T->m2l_tgt.alloc(std::max<int64_t>(1, T->nv));
+    T->m2l_srcb.alloc(std::max<int64_t>(1, T->nv));
+    XRL_CUDA(cudaMemcpyAsync(T->m2l_srcb.p, T->v_src.p, 4 * T->nv, cudaMemcpyDeviceToDevice, st));
+    sort_pairs(vkey.p, T->m2l_srcb.p, T->nv, 64, st);
+    {
+        DBuf<int32_t> offs(std::max<int64_t>(1, T->nv));
+        if (T->nv) {
+            k_split_keys<<<nblk(T->nv, 256), 256, 0, st>>>(T->nv, vkey.p, offs.p, T->m2l_tgt.p);
+            XRL_LAUNCH_CHECK();
+        }
+        std::vector<int32_t> ho(T->nv), htg(T->nv), hsr(T->nv);
+        if (T->nv) {
+            XRL_CUDA(cudaMemcpyAsync(ho.data(), offs.p, 4 * T->nv, cudaMemcpyDeviceToHost, st));
+            XRL_CUDA(cudaMemcpyAsync(htg.data(), T->m2l_tgt.p, 4 * T->nv, cudaMemcpyDeviceToHost, st));
+            XRL_CUDA(cudaMemcpyAsync(hsr.data(), T->m2l_srcb.p, 4 * T->nv, cudaMemcpyDeviceToHost, st));
+        }
+        XRL_CUDA(cudaStreamSynchronize(st));
+        if (T->part_world > 1) {  // keep only the translations into relevant target boxes
+            int64_t k = 0;
+            for (int64_t q = 0; q < T->nv; ++q)
+                if (T->rel[htg[q]]) { ho[k] = ho[q]; htg[k] = htg[q]; hsr[k] = hsr[q]; ++k; }
+            ho.resize(k); htg.resize(k); hsr.resize(k);
+            if (k) {
+                XRL_CUDA(cudaMemcpyAsync(T->m2l_tgt.p, htg.data(), 4 * k, cudaMemcpyHostToDevice, st));
+                XRL_CUDA(cudaMemcpyAsync(T->m2l_srcb.p, hsr.data(), 4 * k, cudaMemcpyHostToDevice, st));
+                XRL_CUDA(cudaStreamSynchronize(st));
+            }
+        }
+        const int64_t nvk = (int64_t)ho.size();
+        std::vector<int4> tiles;
+        const int TP = 16;
+        int64_t i = 0;
+        while (i < nvk) {
+            int64_t j = i;
+            while (j < nvk && ho[j] == ho[i]) ++j;  // same (chunk, offset)
+            for (int64_t s = i; s < j; s += TP)
+                tiles.push_back(make_int4(ho[i] & 511, (int)s, (int)std::min<int64_t>(TP, j - s), ho[i] >> 9));
+            i = j;
+        }
+        T->n_m2l_tiles = (int)tiles.size();
+        T->m2l_tiles.alloc(std::max<size_t>(1, tiles.size()));
+        if (!tiles.empty())
+            XRL_CUDA(cudaMemcpyAsync(T->m2l_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
+    }
+    // X targets (boxes with kept P2L pairs)
+    {
+        std::vector<int64_t> hx(nbox + 1);
+        XRL_CUDA(cudaMemcpyAsync(hx.data(), T->x_ptr.p, 8 * (nbox + 1), cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<int32_t> xt;
+        for (int b = 0; b < nbox; ++b)
+            if (hx[b + 1] > hx[b] && T->rel[b]) xt.push_back(b);
+        T->n_x_targets = (int)xt.size();
+        T->x_targets.alloc(std::max<size_t>(1, xt.size()));
+        if (!xt.empty()) XRL_CUDA(cudaMemcpyAsync(T->x_targets.p, xt.data(), 4 * xt.size(), cudaMemcpyHostToDevice, st));
+    }
     // MVM scratch
     T->mu.alloc((size_t)nbox * kBoxStride);
     T->ell.alloc((size_t)nbox * kBoxStride);
@@ -828,6 +899,23 @@ void xrl::tree_release(xrl_tree t)
 
 extern "C" {
 
+xrl_status xrl_partition_cuts(int64_t n, const double* w, int32_t world, int64_t* cuts)
+{
+    if (n < 0 || world < 1 || !cuts || (n > 0 && !w)) { set_error("xrl_partition_cuts: bad argument"); return XRL_EINVAL; }
+    double tot = 0;
+    for (int64_t i = 0; i < n; ++i) tot += w[i] > 0 ? w[i] : 0;
+    cuts[0] = 0;
+    double acc = 0;
+    int64_t i = 0;
+    for (int r = 1; r < world; ++r) {
+        const double target = tot * r / world;
+        while (i < n && acc + 0.5 * (w[i] > 0 ? w[i] : 0) < target) { acc += w[i] > 0 ? w[i] : 0; ++i; }
+        cuts[r] = i;
+    }
+    cuts[world] = n;
+    return XRL_OK;
+}
+
 xrl_status xrl_tree_build(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_tri, const int32_t* tri,
                           const xrl_fmm_opts* opts, xrl_tree* out)
 {
@@ -838,6 +926,14 @@ xrl_status xrl_tree_build(xrl_ctx ctx, int64_t n_vert, const double* vert, int64
         if (opts->p != kP) { set_error("xrl_tree_build: p=%d not compiled (p=%d only)", opts->p, kP); return XRL_EUNSUPPORTED; }
         if (opts->leaf_max < 1) { set_error("xrl_tree_build: leaf_max < 1"); return XRL_EINVAL; }
         if (opts->max_depth < 1 || opts->max_depth > kMortonBits) { set_error("xrl_tree_build: max_depth"); return XRL_EINVAL; }
+        if (ctx->world > 1 && (opts->part_world != ctx->world || opts->part_rank != ctx->rank)) {
+            set_error("xrl_tree_build: part_rank/part_world must equal the context's rank/world");
+            return XRL_EINVAL;
+        }
+        if (opts->part_world < 0 || (opts->part_world > 0 && (opts->part_rank < 0 || opts->part_rank >= opts->part_world))) {
+            set_error("xrl_tree_build: bad part_rank/part_world");
+            return XRL_EINVAL;
+        }
     }
     try {
         return tree_build_impl(ctx, n_vert, vert, n_tri, tri, opts, out);
@@ -860,8 +956,8 @@ xrl_status xrl_tree_info(xrl_tree t, xrl_tree_info_t* info)
 {
     if (!t || !info) { set_error("xrl_tree_info: null argument"); return XRL_EINVAL; }
     info->n = t->n;
-    info->n_local = t->n;
-    info->offset = 0;
+    info->n_local = t->p1 - t->p0;
+    info->offset = t->p0;
     info->n_boxes = t->nbox;
     info->n_leaves = t->nleaf;
     info->n_levels = t->nlevel;

@@ -6,6 +6,7 @@
 #include <array>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
@@ -89,6 +90,7 @@ struct xrl_ctx_s {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool own_stream = false;
     int rank = 0, world = 1;
+    void* nccl_comm = nullptr;        // ncclComm_t when world > 1
     xrl::DeviceOperators ops;
     // timing
     bool timing = false;
@@ -141,6 +143,16 @@ struct xrl_tree_s {
     // parents per level for M2M/L2L: boxes with children, grouped by level
     std::vector<int32_t> par_start;          // host [nlevel+1] offsets into parents
     xrl::DBuf<int32_t> parents;
+    // partition: this rank owns panels [p0, p1)
+    int32_t part_rank = 0, part_world = 1;
+    int32_t p0 = 0, p1 = 0;
+    std::vector<int32_t> part_cuts;          // panel offsets of all ranks [world+1]
+    std::vector<uint8_t> rel;                // box relevant to this rank
+    xrl::DBuf<int32_t> own_leaves;           // owned leaves (Morton order)
+    int32_t n_own_leaves = 0;
+    std::vector<int32_t> l2l_start;          // per-level offsets into l2l_boxes
+    xrl::DBuf<int32_t> l2l_boxes;
+    xrl::DBuf<float2> xfull;                 // gathered x (multi-rank MVM)
     // host copies of the mesh (original order) for the topology build
     std::vector<double> h_vert;              // [nv][3]
     std::vector<int32_t> h_tri;              // [n][3]
@@ -211,5 +223,8 @@ void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb, cudaStream_t st);
 void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb, cudaStream_t st);
 void upload_constants(xrl_ctx ctx);
 void ctx_release(xrl_ctx ctx);     // delete if dead and unreferenced
+xrl_status comm_init(xrl_ctx ctx, const void* unique_id);
+void comm_destroy(xrl_ctx ctx);
+xrl_status gather_slices(xrl_tree t, const float2* x_local, float2* x_full);
 void tree_release(xrl_tree t);
 }  // namespace xrl

@@ -29,7 +29,7 @@ EXPORTS = [
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
     "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
-    "xrl_port_currents",
+    "xrl_port_currents", "xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_gathered",
 ]
 
 
@@ -40,7 +40,8 @@ class XrlError(RuntimeError):
 
 
 class FmmOpts(ctypes.Structure):
-    _fields_ = [("p", ctypes.c_int32), ("leaf_max", ctypes.c_int32), ("max_depth", ctypes.c_int32)]
+    _fields_ = [("p", ctypes.c_int32), ("leaf_max", ctypes.c_int32), ("max_depth", ctypes.c_int32),
+                ("part_rank", ctypes.c_int32), ("part_world", ctypes.c_int32)]
 
 
 class NearOpts(ctypes.Structure):
@@ -139,6 +140,11 @@ def lib():
         L.xrl_gmres.argtypes = [P, P, P, P, i32, ctypes.POINTER(GmresOpts), P, P, P, P]
         L.xrl_port_rhs.argtypes = [P, i32, f64, P]
         L.xrl_port_currents.argtypes = [P, P, i32, P]
+        L.xrl_partition_cuts.argtypes = [i64, P, i32, P]
+        L.xrl_nccl_unique_id.argtypes = [P]
+        L.xrl_mvm_gathered.argtypes = [P, P, P, P, i32, u32]
+        for name in ("xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_gathered"):
+            getattr(L, name).restype = ctypes.c_int32
         for name in ("xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_esi",
                      "xrl_operator_create", "xrl_operator_apply", "xrl_precond_build", "xrl_precond_apply",
                      "xrl_precond_export", "xrl_gmres", "xrl_port_rhs", "xrl_port_currents"):
@@ -175,17 +181,39 @@ def _dev_vec(t, n, name):
     return t
 
 
-class Context:
-    """xrl_ctx_create on `device`, running on torch's current stream (or `stream`)."""
+def partition_cuts(weights, world: int) -> np.ndarray:
+    """xrl_partition_cuts: balanced contiguous cuts (int64 [world+1])."""
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    cuts = np.empty(world + 1, dtype=np.int64)
+    check(lib().xrl_partition_cuts(w.size, _ptr(w), world, _ptr(cuts)))
+    return cuts
 
-    def __init__(self, device: int = 0, stream=None):
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    check(lib().xrl_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return bytes(buf)
+
+
+class Context:
+    """xrl_ctx_create on `device`, running on torch's current stream (or
+    `stream`).  rank/world > 1 needs the same 128-byte ncclUniqueId on every
+    rank (see distributed_context)."""
+
+    def __init__(self, device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         import torch
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.device = device
         self.stream = stream
+        self.rank, self.world = rank, world
+        idbuf = None
+        if world > 1:
+            idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
         h = ctypes.c_void_p()
-        check(lib().xrl_ctx_create(device, ctypes.c_void_p(stream.cuda_stream), 0, 1, None, ctypes.byref(h)))
+        check(lib().xrl_ctx_create(device, ctypes.c_void_p(stream.cuda_stream), rank, world,
+                                   ctypes.cast(idbuf, ctypes.c_void_p) if idbuf is not None else None,
+                                   ctypes.byref(h)))
         self.h = h
 
     def sync(self):
@@ -219,19 +247,43 @@ class Context:
             pass
 
 
+def distributed_context(device: int = 0, stream=None) -> Context:
+    """Context over the torch.distributed process group: rank 0 creates the
+    ncclUniqueId, torch.distributed broadcasts it (plumbing only)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if world == 1:
+        return Context(device, stream)
+    buf = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    if dist.get_backend() == "nccl":
+        b = buf.cuda(device)
+        dist.broadcast(b, 0)
+        buf = b.cpu()
+    else:
+        dist.broadcast(buf, 0)
+    return Context(device, stream, rank, world, bytes(buf.numpy().tobytes()))
+
+
 class Tree:
     """xrl_tree_build over a triangle mesh (host FP64 verts [nv,3], int32 tris [n,3])."""
 
-    def __init__(self, ctx: Context, verts, tris, p=10, leaf_max=64, max_depth=21):
+    def __init__(self, ctx: Context, verts, tris, p=10, leaf_max=64, max_depth=21, part_rank=None, part_world=None):
         self.ctx = ctx
         v = np.ascontiguousarray(verts, dtype=np.float64)
         t = np.ascontiguousarray(tris, dtype=np.int32)
-        opts = FmmOpts(p, leaf_max, max_depth)
+        if part_world is None:
+            part_rank, part_world = (ctx.rank, ctx.world) if ctx.world > 1 else (0, 0)
+        opts = FmmOpts(p, leaf_max, max_depth, part_rank or 0, part_world)
         h = ctypes.c_void_p()
         check(lib().xrl_tree_build(ctx.h, v.shape[0], _ptr(v), t.shape[0], _ptr(t), ctypes.byref(opts),
                                    ctypes.byref(h)))
         self.h = h
         self.n = t.shape[0]
+        i = self.info()
+        self.n_local, self.offset = int(i["n_local"]), int(i["offset"])
 
     def info(self) -> dict:
         ti = TreeInfo()
@@ -322,11 +374,22 @@ class Near:
 
 
 def mvm(tree: Tree, near: Near, x, y=None, flags=XRL_MVM_FULL):
-    """y = P x on the device (library order, complex64 [nvec][n])."""
+    """y = P x on the device (library order, complex64 [nvec][n_local]; the
+    rank's slice on a multi-rank context)."""
     import torch
-    _dev_vec(x, tree.n, "x")
-    y = torch.empty_like(x) if y is None else _dev_vec(y, tree.n, "y")
+    _dev_vec(x, tree.n_local, "x")
+    y = torch.empty_like(x) if y is None else _dev_vec(y, tree.n_local, "y")
     check(lib().xrl_mvm(tree.h, near.h, _ptr(x), _ptr(y), x.shape[0], flags))
+    return y
+
+
+def mvm_gathered(tree: Tree, near: Near, x_full, y=None, flags=XRL_MVM_FULL):
+    """xrl_mvm_gathered: full x [nvec][n] -> this rank's slice [nvec][n_local]."""
+    import torch
+    _dev_vec(x_full, tree.n, "x_full")
+    if y is None:
+        y = torch.empty((x_full.shape[0], tree.n_local), dtype=torch.complex64, device=x_full.device)
+    check(lib().xrl_mvm_gathered(tree.h, near.h, _ptr(x_full), _ptr(y), x_full.shape[0], flags))
     return y
 
 

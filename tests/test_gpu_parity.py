@@ -232,3 +232,28 @@ def test_full_mvm_sampled_rows(cfg, nrows, leaf):
     err = oracle.rel_l2(y[:, rows], yref)
     print(f"cfg{cfg} sampled rel L2", err, tree.info())
     assert err <= TOL_FULL
+
+
+@pytest.mark.parametrize("cfg,world,leaf", [(1, 2, 64), (1, 3, 16), (2, 4, 64)])
+def test_virtual_partition_concat_equals_full(cfg, world, leaf):
+    """Sharded MVM on one GPU: rank r's restricted passes from the
+    gathered x give exactly its slice of the full MVM; slices tile [0, n)."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m = meshes.make_config(cfg)
+    ctx, tree, near = cuda_setup(m, leaf_max=leaf)
+    x = meshes.make_x(cfg, m.n)
+    xl = tree.to_library_order(torch.from_numpy(x).cuda())
+    y_full = xrl.mvm(tree, near, xl).cpu().numpy()
+    parts, off = [], 0
+    for r in range(world):
+        tr = xrl.Tree(ctx, m.verts, m.tris, leaf_max=leaf, part_rank=r, part_world=world)
+        nr = xrl.Near(tr)
+        assert tr.offset == off and tr.n_local > 0
+        parts.append(xrl.mvm_gathered(tr, nr, xl).cpu().numpy())
+        off += tr.n_local
+    assert off == m.n
+    y_cat = np.concatenate(parts, axis=1)
+    err = oracle.rel_l2(y_cat, y_full)
+    print("virtual partition", cfg, world, err, [p.shape[1] for p in parts])
+    assert err < 1e-6
