@@ -170,6 +170,37 @@ def traffic_from_profiles(kernel: str, key: str):
         return None
 
 
+def gmres_iteration_time(xrl, tree, near, args, freq=1e9):
+    """BASELINE config 4 also asks for the GMRES iteration time: loop-space
+    operator at 1 GHz (sigma 5.8e7, zeta 10 um), block diag-of-P
+    preconditioner, one random complex RHS (seed 1404), a fixed number of
+    restarted-GMRES iterations timed with CUDA events (operator + preconditioner
+    + CGS2 orthogonalisation per iteration)."""
+    import numpy as np
+    import torch
+    t0 = time.perf_counter()
+    topo = xrl.Topology(tree, [])
+    op = xrl.Operator(tree, near, topo, freq, sigma=5.8e7, zeta=10e-6)
+    pc = xrl.Precond(op, 64)
+    setup = time.perf_counter() - t0
+    nl = topo.n_loops
+    rng = np.random.default_rng(1404)
+    b = torch.from_numpy((rng.random((1, nl)) - 0.5 + 1j * (rng.random((1, nl)) - 0.5)).astype(np.complex64)).cuda()
+    xrl.gmres(op, pc, b, max_iters=2, tol=1e-30)  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _, rep = xrl.gmres(op, pc, b, max_iters=args.gmres_iters, restart=50, tol=1e-30)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    info = topo.info()
+    return {"ms_per_iter": ms / max(int(rep["iters"][0]), 1), "iters": int(rep["iters"][0]), "freq_hz": freq,
+            "n_loops": nl, "vertex_loops": info["n_vertex_loops"], "fundamental_loops": info["n_fundamental_loops"],
+            "preconditioned_rre_after": float(rep["rre"][0]), "setup_s": round(setup, 2),
+            "note": "iteration = loop operator (sparse maps + FMM MVM) + block preconditioner + CGS2"}
+
+
 def run_xrl(args):
     import numpy as np
     import torch
@@ -316,6 +347,8 @@ def run_xrl(args):
         "roofline": roof,
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
     }
+    if world == 1 and args.gmres_iters > 0:
+        line["gmres"] = gmres_iteration_time(xrl, tree, near, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(mesh, x_user)
     if rank == 0:
@@ -335,6 +368,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--leaf", type=int, default=512)  # tuned for config 4
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gmres-iters", type=int, default=20, help="GMRES iteration-time probe (N=1); 0 = off")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

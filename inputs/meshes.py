@@ -319,6 +319,23 @@ def bga(nb=16, pitch=500 * UM, ball_r=150 * UM, hole_r=100 * UM, level=3,
     return Mesh(V, T, f"bga{nb}", C, [], {"nb": nb})
 
 
+def _fill_diagonal_contacts(occ: np.ndarray):
+    """Cells touching only along an edge (2x2 blocks [[1,0],[0,1]] or
+    [[0,1],[1,0]]) make a non-manifold surface; fill the lower-left free cell
+    of every such block (repeat until none remain)."""
+    while True:
+        a, b = occ[:-1, :-1], occ[1:, 1:]
+        c, d = occ[1:, :-1], occ[:-1, 1:]
+        p1 = a & b & ~c & ~d
+        p2 = c & d & ~a & ~b
+        if not (p1.any() or p2.any()):
+            return
+        i, j = np.nonzero(p1)
+        occ[i + 1, j] = True
+        i, j = np.nonzero(p2)
+        occ[i, j] = True
+
+
 def pop(seed=4242, via_seed=4243, n_traces=2000, n_vias=5000, domain=10e-3,
         len_lo=0.2e-3, len_hi=0.8e-3) -> Mesh:
     """Config 4: package-on-package-like stack.  Two solid ground planes
@@ -358,6 +375,7 @@ def pop(seed=4242, via_seed=4243, n_traces=2000, n_vias=5000, domain=10e-3,
                     occ[x, lo:hi + 1] = True
                     y = y1
                 axis ^= 1
+        _fill_diagonal_contacts(occ)
         parts.append(voxel_surface(occ[:, :, None], (0.0, 0.0, layer * 100 * UM), (tc, tc, 10 * UM)))
     # vias
     vr = np.random.default_rng(via_seed)
