@@ -37,6 +37,51 @@ __global__ void k_loops_to_panels(int64_t n, int64_t nl, int nrhs, const int64_t
 }
 
 // w[r][l] = sum_t sum_k C_t(l,k) ( zsa_k u_t[k] + j alpha_im pu_t[k] )
+constexpr int kLongRow = 64;  // loop rows longer than this (handle / fundamental loops) get a CTA each
+
+__device__ __forceinline__ float2 panel_y(const float2* __restrict__ zsa, float alpha_im, const float2* __restrict__ u,
+                                          const float2* __restrict__ pu, int64_t n, int r, int t, int k)
+{
+    const float2 z = zsa[k];
+    const float2 uu = u[(int64_t)(3 * r + t) * n + k];
+    const float2 pp = pu[(int64_t)(3 * r + t) * n + k];
+    return make_float2(z.x * uu.x - z.y * uu.y - alpha_im * pp.y, z.x * uu.y + z.y * uu.x + alpha_im * pp.x);
+}
+
+__global__ void __launch_bounds__(256) k_panels_to_loops_long(int64_t n, int64_t nl, int nrhs,
+                                                              const int32_t* __restrict__ rows,
+                                                              const int64_t* __restrict__ ptr,
+                                                              const int32_t* __restrict__ col,
+                                                              const float* __restrict__ val,
+                                                              const float2* __restrict__ zsa, float alpha_im,
+                                                              const float2* __restrict__ u,
+                                                              const float2* __restrict__ pu, float2* __restrict__ w)
+{
+    const int l = rows[blockIdx.x];
+    __shared__ float2 red[256];
+    for (int r = 0; r < nrhs; ++r) {
+        float2 acc = {0, 0};
+        for (int64_t q = ptr[l] + threadIdx.x; q < ptr[l + 1]; q += blockDim.x) {
+            const int k = col[q];
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const float2 y = panel_y(zsa, alpha_im, u, pu, n, r, t, k);
+                const float c = val[3 * q + t];
+                acc.x += c * y.x;
+                acc.y += c * y.y;
+            }
+        }
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        for (int st = 128; st > 0; st >>= 1) {
+            if (threadIdx.x < st) { red[threadIdx.x].x += red[threadIdx.x + st].x; red[threadIdx.x].y += red[threadIdx.x + st].y; }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) w[(int64_t)r * nl + l] = red[0];
+        __syncthreads();
+    }
+}
+
 __global__ void k_panels_to_loops(int64_t n, int64_t nl, int nrhs, const int64_t* __restrict__ ptr,
                                   const int32_t* __restrict__ col, const float* __restrict__ val,
                                   const float2* __restrict__ zsa, float alpha_im, const float2* __restrict__ u,
@@ -44,6 +89,7 @@ __global__ void k_panels_to_loops(int64_t n, int64_t nl, int nrhs, const int64_t
 {
     const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (l >= nl) return;
+    if (ptr[l + 1] - ptr[l] > kLongRow) return;  // done by k_panels_to_loops_long
     for (int r = 0; r < nrhs; ++r) {
         float2 acc = {0, 0};
         for (int64_t q = ptr[l]; q < ptr[l + 1]; ++q) {
@@ -212,7 +258,10 @@ __global__ void k_block_apply(int nl, int nrhs, const int32_t* __restrict__ bptr
 }
 
 // ---------------------------------------------------------------- GMRES BLAS
-// h[r][i] = sum_x conj(V[r][i][x]) w[r][x], i < ni   (grid (ni, nrhs), FP64 accumulation)
+// h[r][i] += sum_x conj(V[r][i][x]) w[r][x], i < ni   (grid (ni, nrhs, chunks), FP64
+// accumulation, h zeroed by the caller, one double atomic per block)
+constexpr int64_t kDotChunk = 16384;
+
 __global__ void k_gdots(int64_t nl, int ldv, const float2* __restrict__ V, const float2* __restrict__ w,
                         double2* __restrict__ h, int ni)
 {
@@ -220,7 +269,8 @@ __global__ void k_gdots(int64_t nl, int ldv, const float2* __restrict__ V, const
     const float2* vi = V + ((int64_t)r * ldv + i) * nl;
     const float2* wr = w + (int64_t)r * nl;
     double sx = 0, sy = 0;
-    for (int64_t x = threadIdx.x; x < nl; x += blockDim.x) {
+    const int64_t x0 = (int64_t)blockIdx.z * kDotChunk, x1 = min(nl, x0 + kDotChunk);
+    for (int64_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
         const float2 a = vi[x], b = wr[x];
         sx += (double)a.x * b.x + (double)a.y * b.y;
         sy += (double)a.x * b.y - (double)a.y * b.x;
@@ -233,7 +283,10 @@ __global__ void k_gdots(int64_t nl, int ldv, const float2* __restrict__ V, const
         if (threadIdx.x < s) { rx[threadIdx.x] += rx[threadIdx.x + s]; ry[threadIdx.x] += ry[threadIdx.x + s]; }
         __syncthreads();
     }
-    if (threadIdx.x == 0) h[(int64_t)r * ni + i] = make_double2(rx[0], ry[0]);
+    if (threadIdx.x == 0) {
+        atomicAdd(&h[(int64_t)r * ni + i].x, rx[0]);
+        atomicAdd(&h[(int64_t)r * ni + i].y, ry[0]);
+    }
 }
 
 // w[r][x] += sgn * sum_{i<ni} V[r][i][x] h[r][i]
@@ -320,6 +373,13 @@ static xrl_status op_apply(xrl_op op, const float2* v, float2* w, int nrhs)
                                                      (float)op->alpha_im, op->u.p, op->pu.p, w);
     XRL_LAUNCH_CHECK();
     t->ctx->launches += 1;
+    if (T->n_long > 0) {
+        k_panels_to_loops_long<<<T->n_long, 256, 0, st>>>(n, nl, nrhs, T->long_rows.p, T->cl_ptr.p, T->cl_col.p,
+                                                          T->cl_val.p, op->zsa.p, (float)op->alpha_im, op->u.p,
+                                                          op->pu.p, w);
+        XRL_LAUNCH_CHECK();
+        t->ctx->launches += 1;
+    }
     return XRL_OK;
 }
 
@@ -572,7 +632,8 @@ xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_
             else XRL_CUDA(cudaMemcpyAsync(o, in, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
         };
         auto norms = [&](const float2* a, std::vector<double>& out) {  // ||a_r||
-            k_gdots<<<dim3(1, nrhs), 256, 0, st>>>(nl, 1, a, a, dh.p, 1);
+            XRL_CUDA(cudaMemsetAsync(dh.p, 0, 16 * nrhs, st));
+            k_gdots<<<dim3(1, nrhs, (unsigned)((nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(nl, 1, a, a, dh.p, 1);
             XRL_LAUNCH_CHECK();
             std::vector<double2> h(nrhs);
             XRL_CUDA(cudaMemcpyAsync(h.data(), dh.p, 16 * nrhs, cudaMemcpyDeviceToHost, st));
@@ -630,7 +691,9 @@ xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_
                 // CGS2
                 std::vector<std::vector<cd>> hcol(nrhs, std::vector<cd>(j + 2, 0.0));
                 for (int pass = 0; pass < 2; ++pass) {
-                    k_gdots<<<dim3(j + 1, nrhs), 256, 0, st>>>(nl, m + 1, V.p, w.p, dh.p, j + 1);
+                    XRL_CUDA(cudaMemsetAsync(dh.p, 0, 16 * nrhs * (j + 1), st));
+                    k_gdots<<<dim3(j + 1, nrhs, (unsigned)((nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(
+                        nl, m + 1, V.p, w.p, dh.p, j + 1);
                     XRL_LAUNCH_CHECK();
                     XRL_CUDA(cudaMemcpyAsync(hh.data(), dh.p, 16 * nrhs * (j + 1), cudaMemcpyDeviceToHost, st));
                     XRL_CUDA(cudaStreamSynchronize(st));

@@ -186,17 +186,31 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
         vloop_comp.push_back(comp_of[T->edge_i[E[0]]]);
         vloops.push_back(std::move(L));
     }
+    // Per closed component of genus g: its vertex loops minus one (they sum
+    // to zero) plus 2g handle loops span the cycle space (edges - panels + 1).
+    // Handle loops by tree-cotree: BFS tree T* of the panel graph, a spanning
+    // forest T of the mesh vertices over edges not crossed by T*; each of the
+    // 2g remaining edges closes one fundamental cycle of T*.  Components with
+    // open boundaries (or failed fans) get fundamental cycles of T* for every
+    // chord instead.
+    std::vector<int64_t> ecount(ncomp, 0), pcount(ncomp, 0), vcount(ncomp, 0);
+    std::vector<uint8_t> comp_open(ncomp, 0);
+    for (int64_t e = 0; e < ne; ++e) ecount[comp_of[T->edge_i[e]]]++;
+    for (int64_t i = 0; i < n; ++i) pcount[comp_of[i]]++;
+    for (size_t i = 0; i < vloops.size(); ++i) vcount[vloop_comp[i]]++;
     {
-        // drop one vertex loop per component (the loops of a closed component sum to zero)
+        // a component is open if any of its panels has a vertex without a closed fan
+        for (int64_t i = 0; i < n; ++i) {
+            const int32_t* v = &t->h_tri[3 * (int64_t)perm[i]];
+            if (vbad[v[0]] || vbad[v[1]] || vbad[v[2]]) comp_open[comp_of[i]] = 1;
+        }
         std::vector<int> last(ncomp, -1);
         for (size_t i = 0; i < vloops.size(); ++i) last[vloop_comp[i]] = (int)i;
-        std::vector<uint8_t> drop(vloops.size(), 0);
-        for (int c = 0; c < ncomp; ++c)
-            if (last[c] >= 0) drop[last[c]] = 1;
-        for (size_t i = 0; i < vloops.size(); ++i)
-            if (!drop[i]) loops.push_back(std::move(vloops[i]));
+        for (size_t i = 0; i < vloops.size(); ++i) {
+            const int c = vloop_comp[i];
+            if (!comp_open[c] && (int)i != last[c]) loops.push_back(std::move(vloops[i]));
+        }
     }
-    const int64_t rank_panel = ne - n + ncomp;
     T->n_vertex_loops = (int64_t)loops.size();
     // adjacency of the panel graph (for BFS)
     std::vector<int64_t> pptr(n + 1, 0);
@@ -209,12 +223,18 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
     }
     auto other = [&](int e, int p) { return T->edge_i[e] == p ? T->edge_j[e] : T->edge_i[e]; };
     auto sign_from = [&](int e, int from) { return (int8_t)(T->edge_i[e] == from ? +1 : -1); };
-    if ((int64_t)loops.size() != rank_panel) {
-        // fallback: fundamental cycles of a BFS spanning forest
-        loops.clear();
+    std::vector<uint8_t> need(ncomp, 0);  // components needing extra (handle or fundamental) loops
+    bool any = false;
+    for (int c = 0; c < ncomp; ++c) {
+        const int64_t rank_c = ecount[c] - pcount[c] + 1;
+        need[c] = comp_open[c] || (vcount[c] - 1 != rank_c);
+        any = any || need[c];
+    }
+    if (any) {
+        // BFS tree T* of the panel graph in those components
         std::vector<int> par_e(n, -1), depth(n, -1);
         for (int64_t r = 0; r < n; ++r) {
-            if (depth[r] >= 0) continue;
+            if (depth[r] >= 0 || !need[comp_of[r]]) continue;
             std::queue<int> q;
             q.push((int)r);
             depth[r] = 0;
@@ -226,9 +246,25 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
                 }
             }
         }
+        std::vector<uint8_t> in_tstar(ne, 0);
+        for (int64_t i = 0; i < n; ++i)
+            if (par_e[i] >= 0) in_tstar[par_e[i]] = 1;
+        // closed components: spanning forest T of the vertices over edges not in T*
+        std::vector<uint8_t> in_t(ne, 0);
+        {
+            UF vuf((int)nv);
+            for (int64_t e = 0; e < ne; ++e) {
+                const int c = comp_of[T->edge_i[e]];
+                if (!need[c] || comp_open[c] || in_tstar[e]) continue;
+                const int va = (int)(ekey[e] >> 32), vb = (int)(ekey[e] & 0xffffffffu);
+                if (vuf.f(va) != vuf.f(vb)) { vuf.u(va, vb); in_t[e] = 1; }
+            }
+        }
         for (int64_t e = 0; e < ne; ++e) {
             int a = T->edge_i[e], b = T->edge_j[e];
-            if (par_e[b] == e || par_e[a] == e) continue;  // tree edge
+            const int c = comp_of[a];
+            if (!need[c] || in_tstar[e]) continue;
+            if (!comp_open[c] && in_t[e]) continue;  // closed: only the 2g leftover chords
             Loop L;
             L.kind = 1;
             L.key = morton(&T->edge_mid[3 * e]);
@@ -244,7 +280,6 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
             for (auto it = up_a.rbegin(); it != up_a.rend(); ++it) L.br.push_back(*it);
             loops.push_back(std::move(L));
         }
-        T->n_vertex_loops = 0;
     }
     T->n_fund_loops = (int64_t)loops.size() - T->n_vertex_loops;
     std::sort(loops.begin(), loops.end(), [](const Loop& a, const Loop& b) { return a.key < b.key; });
@@ -414,6 +449,14 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
         XRL_CUDA(cudaMemcpyAsync(T->cp_val.p, cpv.data(), 4 * cpv.size(), cudaMemcpyHostToDevice, st));
     }
     XRL_CUDA(cudaMemcpyAsync(T->cp_ptr.p, cpp.data(), 8 * cpp.size(), cudaMemcpyHostToDevice, st));
+    {
+        std::vector<int32_t> lr;
+        for (int64_t l = 0; l < T->n_loops; ++l)
+            if (clp[l + 1] - clp[l] > 64) lr.push_back((int32_t)l);
+        T->n_long = (int32_t)lr.size();
+        T->long_rows.alloc(std::max<size_t>(1, lr.size()));
+        if (!lr.empty()) XRL_CUDA(cudaMemcpyAsync(T->long_rows.p, lr.data(), 4 * lr.size(), cudaMemcpyHostToDevice, st));
+    }
     XRL_CUDA(cudaStreamSynchronize(st));
     T->perm = perm;
     ++t->refs;

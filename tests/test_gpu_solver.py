@@ -165,3 +165,38 @@ def test_gmres_coils_two_ports():
     assert Z[0, 0].real > 0 and Z[1, 1].real > 0
     L = Z.imag / (2 * np.pi * f)
     assert L[0, 0] > 0 and L[1, 1] > 0 and abs(L[0, 1]) < np.sqrt(L[0, 0] * L[1, 1])
+
+
+def test_mixed_loop_basis_with_handles():
+    """BGA patch: balls (genus 0) keep vertex loops, perforated plates (genus 4)
+    get fundamental cycles; the basis spans the cycle space and satisfies KCL,
+    and the operator still matches the oracle with that basis as input."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m = meshes.bga(nb=2)
+    ctx, tree, near = cuda_setup(m)
+    topo = xrl.Topology(tree, [])
+    info = topo.info()
+    ex = topo.export()
+    nb = info["n_branches"]
+    assert info["n_loops"] == nb - m.n + info["n_components"]
+    assert info["n_vertex_loops"] > 0 and info["n_fundamental_loops"] > 0
+    g = oracle.Geometry(m.verts, m.tris)
+    M, C = _oracle_C(m, g, ex)
+    node = {}
+    ends = [(node.setdefault(int(a), len(node)), node.setdefault(int(b), len(node))) for a, b in ex["branch_nodes"]]
+    B = sp.csr_matrix(([s for _ in range(nb) for s in (1, -1)],
+                       ([x for e in ends for x in e], [i for i in range(nb) for _ in (0, 1)])), shape=(len(node), nb))
+    assert abs(B @ M.T).max() == 0
+    freq = 1e9
+    op = xrl.Operator(tree, near, topo, freq, sigma=SIGMA, zeta=20e-6)
+    nl = info["n_loops"]
+    v = (np.random.default_rng(2).random((1, nl)) - 0.5).astype(np.complex64)
+    w = op.apply(torch.from_numpy(v).cuda()).cpu().numpy()
+    P = oracle.dense_p(g)
+    zs = lo.esi(SIGMA, 20e-6, freq)
+    alpha = 1j * 2 * np.pi * freq * lo.MU0 / (4 * np.pi)
+    wref = (lo.loop_system(C, P, zs / g.area, alpha) @ v.astype(np.complex128).T).T
+    err = oracle.rel_l2(w, wref)
+    print("bga2 mixed basis", info, err)
+    assert err <= 2e-5
