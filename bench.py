@@ -160,6 +160,11 @@ def run_reference(args):
     return 0
 
 
+def _tc_subtiles(tree) -> int:
+    """Number of 6-pair sub-tiles the tcgen05 M2L issues (from the library's tile list)."""
+    return int(tree.info()["n_m2l_subtiles"])
+
+
 def traffic_from_profiles(kernel: str, key: str):
     """DRAM read+write bytes per launch of `kernel` from a committed ncu
     capture of the same workload/leaf (profiles/traffic.json), else None."""
@@ -303,12 +308,27 @@ def run_xrl(args):
         return ms_ / max(cnt, 1)
 
     roofs = {}
-    if phases["m2l"][1]:
+    simt_m2l = os.environ.get("XRL_M2L_SIMT") == "1"
+    if phases["m2l"][1] and simt_m2l:
         a = 2.0 * nc * nc * 6 * info["n_v_pairs"] / (per_launch_ms("m2l") * 1e-3) / 1e12
         roofs["m2l"] = {"kernel": "k_m2l", "bound": "alu", "achieved": a, "peak": fp32_peak, "unit": "TFLOP/s",
                         "frac": a / fp32_peak, "traffic": traffic_from_profiles("k_m2l", tkey),
                         "algorithmic": f"2*121^2*6 = 175692 flops x {info['n_v_pairs']} V-list translations per launch",
                         "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 flops x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
+    elif phases["m2l"][1]:
+        # tcgen05 3xTF32: per 6-pair sub-tile 48 MMAs of M128 N48 K8 (2*128*48*8 flops each);
+        # 16-pair tiles -> sub-tiles of 6, 6, 4 pairs
+        n_sub = _tc_subtiles(tree)
+        issued = n_sub * 48 * 2.0 * 128 * 48 * 8
+        tf32_peak = float(peaks.get("bf16_tflops", 1656.1)) * 0.5  # nominal tf32/bf16 dense ratio 1.1/2.25
+        a = issued / (per_launch_ms("m2l") * 1e-3) / 1e12
+        alg = 2.0 * nc * nc * 6 * info["n_v_pairs"] / (per_launch_ms("m2l") * 1e-3) / 1e12
+        roofs["m2l"] = {"kernel": "k_m2l_tc", "bound": "tensor", "achieved": a, "peak": tf32_peak, "unit": "TFLOP/s",
+                        "frac": a / tf32_peak, "traffic": traffic_from_profiles("k_m2l_tc", tkey),
+                        "algorithmic": f"issued tcgen05 kind::tf32 MMA flops: {n_sub} sub-tiles x 48 x 2*128*48*8 per launch "
+                                       f"(3xTF32 split; FP32-equivalent algorithmic rate {alg:.1f} TFLOP/s = "
+                                       f"{alg / fp32_peak:.2f} of the FP32 SIMT peak)",
+                        "peak_source": "tf32 dense = bf16_tflops (MEASURED_PEAKS.json) x 0.5 (nominal 1.1/2.25 PF)"}
     if phases["p2p"][1]:
         a = 20.0 * info["n_p2p"] / (per_launch_ms("p2p") * 1e-3) / 1e12
         roofs["p2p"] = {"kernel": "k_p2p", "bound": "alu", "achieved": a, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -322,7 +342,7 @@ def run_xrl(args):
                          "frac": a / hbm_peak, "traffic": traffic_from_profiles("k_near_spmv", tkey),
                          "algorithmic": f"8 B x {nnz} nnz + 56 B x {n} rows (row_ptr, x, y) per launch",
                          "peak_source": "hbm_gbs, MEASURED_PEAKS.json"}
-    dom = max(phases, key=lambda k: phases[k][0])
+    dom = max(roofs, key=lambda k: phases[k][0]) if roofs else max(phases, key=lambda k: phases[k][0])
     roof = dict(roofs.get(dom) or {"kernel": "k_" + dom})
     roof["share_of_step"] = phases[dom][0] / tot_phase if tot_phase else None
     roof["others"] = {k: {kk: v[kk] for kk in ("achieved", "peak", "unit", "frac")} for k, v in roofs.items() if k != dom}

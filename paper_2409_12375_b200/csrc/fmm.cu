@@ -262,122 +262,196 @@ __global__ void __launch_bounds__(256, 2) k_m2l(const int4* __restrict__ tiles, 
 }
 
 // ------------------------------------------------------------------ M2L on tcgen05
-// Tensor-core M2L: per 16-pair tile, D[128 x 96] (TMEM, FP32) = T_o[128 x 128]
-// x B[128 x 96] with 3xTF32 (A_hi B_hi + A_hi B_lo + A_lo B_hi, 48
-// tcgen05.mma kind::tf32 M128 N96 K8), accuracy ~1e-6 relative.  T_o hi/lo
-// images are pre-laid-out in the canonical K-major core-matrix layout and
-// copied with cp.async when the tile's offset changes; the gathered source
-// multipoles are split hi/lo on the fly.  One CTA (4 warps) per SM walks
-// blocks of kTcR consecutive tiles (same offset -> operator reuse), blocks
-// dealt round-robin so all CTAs stay inside one L2-resident target chunk.
-// Epilogue: tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = coefficients),
-// red.global.add.{v4,v2}.f32 into ell.
-constexpr int kTcN = kTP * 6;                       // 96
-constexpr int kTcABytes = 128 * 128 * 4;            // one operator image
-constexpr int kTcBBytes = kTcN * 128 * 4;
-constexpr int kTcSmem = 2 * kTcABytes + 2 * kTcBBytes;
+// Tensor-core M2L.  After the upward pass every box's multipole is written once
+// as a TF32 hi/lo "image" in the tcgen05 canonical K-major core-matrix layout
+// with the 6 RHS padded to 8 rows, i.e. one 8-row core group per box:
+//   img[box][hi|lo][kc = k/4][r = 0..7][k % 4]   (32 x 128 B per part, 8 KB per box).
+// A sub-tile of 8 (target, source) pairs sharing one offset then needs as B
+// operand [kc][pair][128 B] (LBO = 768 B between K chunks, SBO = 128 B between
+// pairs): pure 16-byte cp.async copies.  D[128 x 48] (TMEM, FP32) = T_o x B
+// for 6 pairs with 3xTF32 (A_lo B_hi + A_hi B_lo + A_hi B_hi; 48 tcgen05.mma
+// kind::tf32 M128 N48 K8).  Pipeline (two B buffers, two TMEM accumulators): while MMA(t)
+// runs, the 8 warps drain the accumulator of t-1 (tcgen05.ld -> red.global.add
+// into ell) and issue the cp.async gather of t+1.  One persistent CTA per SM
+// walks blocks of kTcR tiles (same offset -> operator reuse), blocks dealt
+// round-robin so all CTAs stay inside one L2-resident target chunk.
+constexpr int kTcP = 6;                             // pairs per sub-tile
+constexpr int kTcN = kTcP * 8;                      // 48 MMA columns (6 RHS + 2 pad per pair)
+constexpr int kTcABytes = 128 * 128 * 4;            // one operator image (hi or lo): 64 KB
+constexpr int kTcBBytes = kTcN * 128 * 4;           // one B image (hi or lo): 24 KB
+constexpr int kTcSmem = 2 * kTcABytes + 4 * kTcBBytes;  // 224 KB: A hi/lo + 2 buffers x B hi/lo
 constexpr int kTcR = 8;
+constexpr int kTcThreads = 256;
+constexpr int kImgFloats = 2 * 32 * 32;             // per box: hi + lo, 32 K-chunks x 32 floats
 
 __device__ __forceinline__ void red_add_v2(float* p, float a, float b)
 {
     asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
-__global__ void __launch_bounds__(128, 1) k_m2l_tc(const int4* __restrict__ tiles, int ntiles,
-                                                   const int32_t* __restrict__ tgt, const int32_t* __restrict__ srcb,
-                                                   const float* __restrict__ img, const float* __restrict__ mu,
-                                                   float* __restrict__ ell)
+// img[b][part][kc][r][j] = split(mu[b][4 kc + j][r]) for r < 6, k < 121; else 0.
+__global__ void k_mu_img(int nbox, const float* __restrict__ mu, float* __restrict__ img)
+{
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one per (box, kc, r, j)
+    if (e >= (int64_t)nbox * 1024) return;
+    const int b = (int)(e >> 10), w = (int)(e & 1023);
+    const int kc = w >> 5, r = (w >> 2) & 7, j = w & 3;
+    const int k = 4 * kc + j;
+    const float x = (r < 6 && k < kNC) ? mu[(size_t)b * kBoxStride + 6 * k + r] : 0.f;
+    const float hi = tc::tf32_rna(x);
+    img[(size_t)b * kImgFloats + w] = hi;
+    img[(size_t)b * kImgFloats + 1024 + w] = x - hi;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict__ tiles, int ntiles,
+                                                          const int32_t* __restrict__ tgt,
+                                                          const int32_t* __restrict__ srcb,
+                                                          const float* __restrict__ aimg,
+                                                          const float* __restrict__ bimg, float* __restrict__ ell)
 {
     extern __shared__ __align__(1024) uint8_t tsm[];
     float* Ah = reinterpret_cast<float*>(tsm);
     float* Al = reinterpret_cast<float*>(tsm + kTcABytes);
-    float* Bh = reinterpret_cast<float*>(tsm + 2 * kTcABytes);
-    float* Bl = reinterpret_cast<float*>(tsm + 2 * kTcABytes + kTcBBytes);
-    __shared__ uint64_t bar;
+    float* Bbase = reinterpret_cast<float*>(tsm + 2 * kTcABytes);  // [buf][hi/lo][32 kc][8 pairs][32 floats]
+    __shared__ uint64_t bar[2];
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // zero B once: rows k >= 121 stay zero (A is zero-padded there too)
-    for (int i = tid; i < 2 * kTcBBytes / 16; i += 128) reinterpret_cast<float4*>(Bh)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (tid == 0) tc::mbar_init(&bar, 1);
+    if (tid == 0) { tc::mbar_init(&bar[0], 1); tc::mbar_init(&bar[1], 1); }
     if (warp == 0) tc::tmem_alloc<128>(&tbase);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t dtm = tbase;
     const uint32_t idesc = tc::idesc_tf32(128, kTcN);
-    const uint32_t lboA = 16 * 128, lboB = (kTcN / 8) * 128;
+    const uint32_t lboA = 16 * 128, lboB = kTcP * 128;
+    uint32_t ph[2] = {0, 0};
     int cur_off = -1;
-    uint32_t phase = 0;
-    for (int blk = blockIdx.x; blk * kTcR < ntiles; blk += gridDim.x) {
-        const int t1 = min(ntiles, (blk + 1) * kTcR);
-        for (int t = blk * kTcR; t < t1; ++t) {
-            const int4 tile = tiles[t];
-            const int off = tile.x, begin = tile.y, count = tile.z;
-            if (off != cur_off) {
-                const float4* g = reinterpret_cast<const float4*>(img + (size_t)off * 2 * 128 * 128);
-                float4* s = reinterpret_cast<float4*>(Ah);
-                for (int j = tid; j < 2 * kTcABytes / 16; j += 128) cp_async16(s + j, g + j);
-                cur_off = off;
+
+    // sub-tile sequence of this CTA: (tile index, half)
+    struct Sub { int off, begin, count; };
+    auto sub_at = [&](int blk, int ti, int half) -> Sub {
+        const int4 tile = tiles[ti];
+        return {tile.x, tile.y + half * kTcP, min(kTcP, tile.z - half * kTcP)};
+    };
+    // issue the cp.async copies of a sub-tile's B operand (hi and lo) into buffer buf
+    auto gather = [&](const Sub& sb, int buf) {
+        float* B = Bbase + (size_t)buf * 2 * (kTcBBytes / 4);
+        // 2 parts x 32 kc x 6 pairs x 8 pieces of 16 B = 3072 copies
+        for (int c = tid; c < 2 * 32 * kTcP * 8; c += kTcThreads) {
+            const int piece = c & 7, rest = c >> 3;
+            const int p = rest % kTcP, kc = (rest / kTcP) & 31, part = rest / (kTcP * 32);
+            float4* dst = reinterpret_cast<float4*>(B + part * (kTcBBytes / 4) + kc * (kTcP * 32) + p * 32) + piece;
+            if (p < sb.count) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    bimg + (size_t)srcb[sb.begin + p] * kImgFloats + part * 1024 + kc * 32) + piece;
+                cp_async16(dst, src);
+            } else {
+                *dst = make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            // gather + split the 16 source multipoles: element (p, k, r) -> B row n = 6p + r, column k
-            for (int e = tid; e < kTP * kNC * 6; e += 128) {
-                const int p = e / (kNC * 6), q = e % (kNC * 6);
-                const int k = q / 6, r = q % 6;
-                const float x = (p < count) ? __ldg(mu + (size_t)srcb[begin + p] * kBoxStride + q) : 0.f;
-                const float h = tc::tf32_rna(x);
-                const uint32_t o = tc::core_offset(6 * p + r, k, kTcN) >> 2;
-                Bh[o] = h;
-                Bl[o] = x - h;
-            }
-            cp_async_wait_all();
-            tc::fence_proxy_async();
-            tc::fence_before();
-            __syncthreads();
-            tc::fence_after();
-            if (tid == 0) {
-                const uint32_t a0 = tc::smem_u32(Ah), al0 = tc::smem_u32(Al);
-                const uint32_t b0 = tc::smem_u32(Bh), bl0 = tc::smem_u32(Bl);
-#pragma unroll
-                for (int s2 = 0; s2 < 16; ++s2) {
-                    const uint64_t ah = tc::smem_desc(a0 + s2 * 2 * lboA, lboA, 128);
-                    const uint64_t al = tc::smem_desc(al0 + s2 * 2 * lboA, lboA, 128);
-                    const uint64_t bh = tc::smem_desc(b0 + s2 * 2 * lboB, lboB, 128);
-                    const uint64_t bl = tc::smem_desc(bl0 + s2 * 2 * lboB, lboB, 128);
-                    tc::mma_tf32(dtm, al, bh, idesc, s2 > 0);
-                    tc::mma_tf32(dtm, ah, bl, idesc, 1);
-                    tc::mma_tf32(dtm, ah, bh, idesc, 1);
-                }
-                tc::commit(&bar);
-            }
-            tc::mbar_wait(&bar, phase);
-            phase ^= 1;
-            tc::fence_after();
-            // epilogue: lane = coefficient i = 32*warp + lane; 96 columns = 16 pairs x 6 RHS
-            const int i = 32 * warp + lane;
-            float v[kTcN];
-            const uint32_t taddr = dtm + ((uint32_t)(32 * warp) << 16);
-            tc::tmem_ld32(taddr, v);
-            tc::tmem_ld32(taddr + 32, v + 32);
-            tc::tmem_ld32(taddr + 64, v + 64);
-            if (i < kNC) {
-#pragma unroll
-                for (int p = 0; p < kTP; ++p) {
-                    if (p >= count) break;
-                    float* o = ell + (size_t)tgt[begin + p] * kBoxStride + 6 * i;
-                    const float* x = v + 6 * p;
-                    if ((i & 1) == 0) {
-                        red_add_v4(o, x[0], x[1], x[2], x[3]);
-                        red_add_v2(o + 4, x[4], x[5]);
-                    } else {
-                        red_add_v2(o, x[0], x[1]);
-                        red_add_v4(o + 2, x[2], x[3], x[4], x[5]);
-                    }
-                }
-            }
-            tc::fence_before();
-            __syncthreads();
         }
+    };
+    auto epilogue = [&](int buf, const Sub& sb) {
+        tc::mbar_wait(&bar[buf], ph[buf]);
+        ph[buf] ^= 1;
+        tc::fence_after();
+        const int qd = warp & 3, h = warp >> 2;       // TMEM lane quarter, column half (pairs 3h..3h+2)
+        const int i = 32 * qd + lane;                 // coefficient index = TMEM lane
+        float v[24];
+        const uint32_t ta = dtm + ((uint32_t)(32 * qd) << 16) + (uint32_t)(buf * 64 + 24 * h);
+        tc::tmem_ld8(ta, v);
+        tc::tmem_ld8(ta + 8, v + 8);
+        tc::tmem_ld8(ta + 16, v + 16);
+        if (i < kNC) {
+#pragma unroll
+            for (int pp = 0; pp < 3; ++pp) {
+                const int p = 3 * h + pp;
+                if (p >= sb.count) break;
+                float* o = ell + (size_t)tgt[sb.begin + p] * kBoxStride + 6 * i;
+                const float* x = v + 8 * pp;
+                if ((i & 1) == 0) {
+                    red_add_v4(o, x[0], x[1], x[2], x[3]);
+                    red_add_v2(o + 4, x[4], x[5]);
+                } else {
+                    red_add_v2(o, x[0], x[1]);
+                    red_add_v4(o + 2, x[2], x[3], x[4], x[5]);
+                }
+            }
+        }
+    };
+    auto load_a = [&](int off) {
+        const float4* g = reinterpret_cast<const float4*>(aimg + (size_t)off * 2 * 128 * 128);
+        float4* sa = reinterpret_cast<float4*>(Ah);
+        for (int j = tid; j < 2 * kTcABytes / 16; j += kTcThreads) cp_async16(sa + j, g + j);
+    };
+
+    // flatten this CTA's sub-tiles
+    int blk = blockIdx.x, ti = blk * kTcR, half = 0;
+    auto valid = [&]() { return blk * kTcR < ntiles && ti < min(ntiles, (blk + 1) * kTcR); };
+    auto advance = [&]() {
+        if ((half + 1) * kTcP < tiles[ti].z) { ++half; return; }
+        half = 0;
+        ++ti;
+        if (ti >= min(ntiles, (blk + 1) * kTcR)) { blk += gridDim.x; ti = blk * kTcR; }
+    };
+    if (!valid()) {
+        __syncthreads();
+        if (warp == 0) tc::tmem_dealloc<128>(tbase);
+        return;
     }
+    Sub cur = sub_at(blk, ti, half);
+    load_a(cur.off);
+    cur_off = cur.off;
+    gather(cur, 0);
+    int t = 0;
+    bool have_prev = false;
+    Sub prev{};
+    for (;;) {
+        const int buf = t & 1;
+        cp_async_wait_all();
+        tc::fence_proxy_async();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (tid == 0) {
+            const uint32_t a0 = tc::smem_u32(Ah), al0 = tc::smem_u32(Al);
+            float* Bh = Bbase + (size_t)buf * 2 * (kTcBBytes / 4);
+            const uint32_t b0 = tc::smem_u32(Bh), bl0 = tc::smem_u32(Bh + kTcBBytes / 4);
+            const uint32_t dst = dtm + (uint32_t)(buf * 64);
+#pragma unroll
+            for (int s2 = 0; s2 < 16; ++s2) {
+                const uint64_t ah = tc::smem_desc(a0 + s2 * 2 * lboA, lboA, 128);
+                const uint64_t al = tc::smem_desc(al0 + s2 * 2 * lboA, lboA, 128);
+                const uint64_t bh = tc::smem_desc(b0 + s2 * 2 * lboB, lboB, 128);
+                const uint64_t bl = tc::smem_desc(bl0 + s2 * 2 * lboB, lboB, 128);
+                tc::mma_tf32(dst, al, bh, idesc, s2 > 0);
+                tc::mma_tf32(dst, ah, bl, idesc, 1);
+                tc::mma_tf32(dst, ah, bh, idesc, 1);
+            }
+            tc::commit(&bar[buf]);
+        }
+        // drain t-1 (its MMA completed before MMA(t) was issued... or soon after)
+        if (have_prev) epilogue(buf ^ 1, prev);
+        prev = cur;
+        have_prev = true;
+        advance();
+        if (!valid()) break;
+        Sub nxt = sub_at(blk, ti, half);
+        if (nxt.off != cur_off) {
+            // the operator is about to change: wait for MMA(t) and drain it first
+            epilogue(buf, cur);
+            have_prev = false;
+            tc::fence_before();
+            __syncthreads();
+            load_a(nxt.off);
+            cur_off = nxt.off;
+        }
+        // buffer buf^1 was last read by MMA(t-1), drained above
+        gather(nxt, buf ^ 1);
+        cur = nxt;
+        ++t;
+    }
+    if (have_prev) epilogue(t & 1, prev);
+    tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<128>(tbase);
 }
@@ -805,8 +879,8 @@ void upload_constants(xrl_ctx ctx)
     upload_tc_images(ctx->ops.m2l_tc, ops.m2l);
     XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
     XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    const char* e = getenv("XRL_M2L_TC");   // tcgen05 3xTF32 M2L (opt-in)
-    ctx->m2l_simt = !(e && e[0] == '1');
+    const char* e = getenv("XRL_M2L_SIMT");  // SIMT FP32 M2L (ablation); default tcgen05 3xTF32
+    ctx->m2l_simt = e && e[0] == '1';
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kM2LSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
@@ -883,8 +957,12 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         } else if (t->n_m2l_tiles > 0) {
             const int nblocks = (t->n_m2l_tiles + kTcR - 1) / kTcR;
             const int grid = std::min(ctx->num_sms, nblocks);
-            k_m2l_tc<<<grid, 128, kTcSmem, st>>>(t->m2l_tiles.p, t->n_m2l_tiles, t->m2l_tgt.p, t->m2l_srcb.p,
-                                                 ctx->ops.m2l_tc.p, t->mu.p, t->ell.p);
+            if (t->mu_img.n < (size_t)t->nbox * kImgFloats) t->mu_img.alloc((size_t)t->nbox * kImgFloats);
+            k_mu_img<<<nblk((int64_t)t->nbox * 1024, 256), 256, 0, st>>>(t->nbox, t->mu.p, t->mu_img.p);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+            k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->m2l_tiles.p, t->n_m2l_tiles, t->m2l_tgt.p, t->m2l_srcb.p,
+                                                        ctx->ops.m2l_tc.p, t->mu_img.p, t->ell.p);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }

@@ -858,6 +858,8 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
             i = j;
         }
         T->n_m2l_tiles = (int)tiles.size();
+        T->n_m2l_subtiles = 0;
+        for (const int4& tl : tiles) T->n_m2l_subtiles += (tl.z + 5) / 6;
         T->m2l_tiles.alloc(std::max<size_t>(1, tiles.size()));
         if (!tiles.empty())
             XRL_CUDA(cudaMemcpyAsync(T->m2l_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
@@ -969,6 +971,8 @@ xrl_status xrl_tree_info(xrl_tree t, xrl_tree_info_t* info)
     info->n_p2p = t->np2p;
     for (int d = 0; d < 3; ++d) info->root_lo[d] = t->lo[d];
     info->root_width = t->W;
+    info->n_m2l_tiles = t->n_m2l_tiles;
+    info->n_m2l_subtiles = t->n_m2l_subtiles;
     return XRL_OK;
 }
 

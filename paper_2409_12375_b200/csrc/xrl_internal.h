@@ -94,7 +94,7 @@ struct xrl_ctx_s {
     xrl::DeviceOperators ops;
     // timing
     bool timing = false;
-    bool m2l_simt = true;             // false with XRL_M2L_TC=1: tcgen05 M2L
+    bool m2l_simt = false;            // XRL_M2L_SIMT=1: SIMT FP32 M2L instead of tcgen05
     int num_sms = 148;
     int64_t launches = 0;
     int refs = 0;         // live trees
@@ -137,6 +137,7 @@ struct xrl_tree_s {
     xrl::DBuf<int32_t> m2l_tgt, m2l_srcb;    // [nv]
     xrl::DBuf<int4> m2l_tiles;               // (offset, pair begin, pair count, 0)
     int32_t n_m2l_tiles = 0;
+    int64_t n_m2l_subtiles = 0;
     // boxes with non-empty X list, leaves with non-empty W list
     xrl::DBuf<int32_t> x_targets;
     int32_t n_x_targets = 0;
@@ -158,6 +159,7 @@ struct xrl_tree_s {
     std::vector<int32_t> h_tri;              // [n][3]
     // MVM scratch
     xrl::DBuf<float> mu, ell;                // [nbox][kBoxStride]
+    xrl::DBuf<float> mu_img;                 // tcgen05 M2L: per-box TF32 hi/lo images (8 KB)
     xrl::DBuf<float> xq;                     // [n][8] packed charges
     xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging
 };

@@ -53,7 +53,8 @@ class TreeInfo(ctypes.Structure):
                 ("n_boxes", ctypes.c_int32), ("n_leaves", ctypes.c_int32), ("n_levels", ctypes.c_int32),
                 ("p", ctypes.c_int32), ("n_v_pairs", ctypes.c_int64), ("n_x_pairs", ctypes.c_int64),
                 ("n_w_pairs", ctypes.c_int64), ("n_u_pairs", ctypes.c_int64), ("n_p2p", ctypes.c_int64),
-                ("root_lo", ctypes.c_double * 3), ("root_width", ctypes.c_double)]
+                ("root_lo", ctypes.c_double * 3), ("root_width", ctypes.c_double),
+                ("n_m2l_tiles", ctypes.c_int64), ("n_m2l_subtiles", ctypes.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
