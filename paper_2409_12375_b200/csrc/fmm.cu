@@ -267,22 +267,26 @@ __global__ void __launch_bounds__(256, 2) k_m2l(const int4* __restrict__ tiles, 
 // with the 6 RHS padded to 8 rows, i.e. one 8-row core group per box:
 //   img[box][hi|lo][kc = k/4][r = 0..7][k % 4]   (32 x 128 B per part, 8 KB per box).
 // A sub-tile of 8 (target, source) pairs sharing one offset then needs as B
-// operand [kc][pair][128 B] (LBO = 768 B between K chunks, SBO = 128 B between
-// pairs): pure 16-byte cp.async copies.  D[128 x 48] (TMEM, FP32) = T_o x B
-// for 6 pairs with 3xTF32 (A_lo B_hi + A_hi B_lo + A_hi B_hi; 48 tcgen05.mma
-// kind::tf32 M128 N48 K8).  Pipeline (two B buffers, two TMEM accumulators): while MMA(t)
-// runs, the 8 warps drain the accumulator of t-1 (tcgen05.ld -> red.global.add
-// into ell) and issue the cp.async gather of t+1.  One persistent CTA per SM
-// walks blocks of kTcR tiles (same offset -> operator reuse), blocks dealt
-// round-robin so all CTAs stay inside one L2-resident target chunk.
-constexpr int kTcP = 6;                             // pairs per sub-tile
-constexpr int kTcN = kTcP * 8;                      // 48 MMA columns (6 RHS + 2 pad per pair)
-constexpr int kTcABytes = 128 * 128 * 4;            // one operator image (hi or lo): 64 KB
-constexpr int kTcBBytes = kTcN * 128 * 4;           // one B image (hi or lo): 24 KB
-constexpr int kTcSmem = 2 * kTcABytes + 4 * kTcBBytes;  // 224 KB: A hi/lo + 2 buffers x B hi/lo
+// operand [kc][pair][128 B] (LBO = 1024 B between K chunks, SBO = 128 B between
+// pairs): pure 16-byte cp.async copies.  The operator T_o (hi and lo, 128 x 128
+// TF32) lives in TMEM (lane = output coefficient, column = input coefficient),
+// written with tcgen05.st when the offset changes, so the MMAs only read B from
+// shared memory.  D[128 x 64] (TMEM, FP32) = T_o x B with 3xTF32
+// (A_lo B_hi + A_hi B_lo + A_hi B_hi; 48 tcgen05.mma kind::tf32 M128 N64 K8).
+// Pipeline (two B buffers, two TMEM accumulators): while MMA(t) runs, the 8
+// warps issue the cp.async gather of t+1 and drain the accumulator of t-1
+// (tcgen05.ld -> red.global.add.{v4,v2}.f32 into ell).  One persistent CTA per
+// SM (TMEM 512 columns) walks blocks of kTcR tiles (same offset -> operator
+// reuse), blocks dealt round-robin so all CTAs stay inside one L2-resident
+// target chunk.  128 KB of shared memory leaves room for P2P CTAs on the SM.
+constexpr int kTcP = 8;                             // pairs per sub-tile
+constexpr int kTcN = kTcP * 8;                      // 64 MMA columns (6 RHS + 2 pad per pair)
+constexpr int kTcBBytes = kTcN * 128 * 4;           // one B image (hi or lo): 32 KB
+constexpr int kTcSmem = 4 * kTcBBytes;              // 2 buffers x (hi, lo)
 constexpr int kTcR = 8;
 constexpr int kTcThreads = 256;
 constexpr int kImgFloats = 2 * 32 * 32;             // per box: hi + lo, 32 K-chunks x 32 floats
+constexpr uint32_t kTcColD = 0, kTcColAh = 256, kTcColAl = 384;
 
 __device__ __forceinline__ void red_add_v2(float* p, float a, float b)
 {
@@ -310,36 +314,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                                                           const float* __restrict__ bimg, float* __restrict__ ell)
 {
     extern __shared__ __align__(1024) uint8_t tsm[];
-    float* Ah = reinterpret_cast<float*>(tsm);
-    float* Al = reinterpret_cast<float*>(tsm + kTcABytes);
-    float* Bbase = reinterpret_cast<float*>(tsm + 2 * kTcABytes);  // [buf][hi/lo][32 kc][8 pairs][32 floats]
+    float* Bbase = reinterpret_cast<float*>(tsm);  // [buf][hi/lo][32 kc][8 pairs][32 floats]
     __shared__ uint64_t bar[2];
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) { tc::mbar_init(&bar[0], 1); tc::mbar_init(&bar[1], 1); }
-    if (warp == 0) tc::tmem_alloc<128>(&tbase);
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t dtm = tbase;
     const uint32_t idesc = tc::idesc_tf32(128, kTcN);
-    const uint32_t lboA = 16 * 128, lboB = kTcP * 128;
+    const uint32_t lboB = kTcP * 128;
     uint32_t ph[2] = {0, 0};
     int cur_off = -1;
 
-    // sub-tile sequence of this CTA: (tile index, half)
     struct Sub { int off, begin, count; };
-    auto sub_at = [&](int blk, int ti, int half) -> Sub {
+    auto sub_at = [&](int ti, int half) -> Sub {
         const int4 tile = tiles[ti];
         return {tile.x, tile.y + half * kTcP, min(kTcP, tile.z - half * kTcP)};
     };
-    // issue the cp.async copies of a sub-tile's B operand (hi and lo) into buffer buf
+    // cp.async of a sub-tile's B operand (hi and lo) into buffer buf: 2 x 32 kc x 8 pairs x 8 x 16 B
     auto gather = [&](const Sub& sb, int buf) {
         float* B = Bbase + (size_t)buf * 2 * (kTcBBytes / 4);
-        // 2 parts x 32 kc x 6 pairs x 8 pieces of 16 B = 3072 copies
-        for (int c = tid; c < 2 * 32 * kTcP * 8; c += kTcThreads) {
-            const int piece = c & 7, rest = c >> 3;
-            const int p = rest % kTcP, kc = (rest / kTcP) & 31, part = rest / (kTcP * 32);
+        for (int c = tid; c < 4096; c += kTcThreads) {
+            const int part = c >> 11, kc = (c >> 6) & 31, p = (c >> 3) & 7, piece = c & 7;
             float4* dst = reinterpret_cast<float4*>(B + part * (kTcBBytes / 4) + kc * (kTcP * 32) + p * 32) + piece;
             if (p < sb.count) {
                 const float4* src = reinterpret_cast<const float4*>(
@@ -350,41 +349,59 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             }
         }
     };
-    auto epilogue = [&](int buf, const Sub& sb) {
+    auto wait_mma = [&](int buf) {
         tc::mbar_wait(&bar[buf], ph[buf]);
         ph[buf] ^= 1;
         tc::fence_after();
-        const int qd = warp & 3, h = warp >> 2;       // TMEM lane quarter, column half (pairs 3h..3h+2)
-        const int i = 32 * qd + lane;                 // coefficient index = TMEM lane
-        float v[24];
-        const uint32_t ta = dtm + ((uint32_t)(32 * qd) << 16) + (uint32_t)(buf * 64 + 24 * h);
-        tc::tmem_ld8(ta, v);
-        tc::tmem_ld8(ta + 8, v + 8);
-        tc::tmem_ld8(ta + 16, v + 16);
-        if (i < kNC) {
+    };
+    auto drain = [&](int buf, const Sub& sb) {
+        // lane quarter qd = warp % 4 (coefficients 32 qd + lane); pair group g = warp / 4 owns pairs g, g+2, ...
+        const int qd = warp & 3, g = warp >> 2;
+        const int i = 32 * qd + lane;
 #pragma unroll
-            for (int pp = 0; pp < 3; ++pp) {
-                const int p = 3 * h + pp;
-                if (p >= sb.count) break;
+        for (int pp = 0; pp < kTcP / 2; ++pp) {
+            const int p = g + 2 * pp;
+            float v[8];
+            tc::tmem_ld8(dtm + ((uint32_t)(32 * qd) << 16) + (uint32_t)(kTcColD + buf * 64 + 8 * p), v);
+            if (i < kNC && p < sb.count) {
                 float* o = ell + (size_t)tgt[sb.begin + p] * kBoxStride + 6 * i;
-                const float* x = v + 8 * pp;
                 if ((i & 1) == 0) {
-                    red_add_v4(o, x[0], x[1], x[2], x[3]);
-                    red_add_v2(o + 4, x[4], x[5]);
+                    red_add_v4(o, v[0], v[1], v[2], v[3]);
+                    red_add_v2(o + 4, v[4], v[5]);
                 } else {
-                    red_add_v2(o, x[0], x[1]);
-                    red_add_v4(o + 2, x[2], x[3], x[4], x[5]);
+                    red_add_v2(o, v[0], v[1]);
+                    red_add_v4(o + 2, v[2], v[3], v[4], v[5]);
                 }
             }
         }
     };
+    auto epilogue = [&](int buf, const Sub& sb) { wait_mma(buf); drain(buf, sb); };
+    // operator hi/lo rows into TMEM: warp w writes lanes of quarter w % 4, columns half (w / 4)
     auto load_a = [&](int off) {
-        const float4* g = reinterpret_cast<const float4*>(aimg + (size_t)off * 2 * 128 * 128);
-        float4* sa = reinterpret_cast<float4*>(Ah);
-        for (int j = tid; j < 2 * kTcABytes / 16; j += kTcThreads) cp_async16(sa + j, g + j);
+        const int qd = warp & 3, hf = warp >> 2;
+        const int i = 32 * qd + lane;
+        const float* rowh = aimg + ((size_t)off * 2 * 128 + i) * 128 + 64 * hf;
+        const float* rowl = rowh + 128 * 128;
+        const uint32_t ta = dtm + ((uint32_t)(32 * qd) << 16) + 64 * hf;
+        float v[32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(rowh + 32 * c) + j);
+                v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+            }
+            tc::tmem_st32(ta + kTcColAh + 32 * c, v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(rowl + 32 * c) + j);
+                v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+            }
+            tc::tmem_st32(ta + kTcColAl + 32 * c, v);
+        }
+        tc::tmem_st_wait();
     };
 
-    // flatten this CTA's sub-tiles
     int blk = blockIdx.x, ti = blk * kTcR, half = 0;
     auto valid = [&]() { return blk * kTcR < ntiles && ti < min(ntiles, (blk + 1) * kTcR); };
     auto advance = [&]() {
@@ -393,67 +410,72 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
         ++ti;
         if (ti >= min(ntiles, (blk + 1) * kTcR)) { blk += gridDim.x; ti = blk * kTcR; }
     };
-    if (!valid()) {
-        __syncthreads();
-        if (warp == 0) tc::tmem_dealloc<128>(tbase);
-        return;
-    }
-    Sub cur = sub_at(blk, ti, half);
-    load_a(cur.off);
-    cur_off = cur.off;
-    gather(cur, 0);
-    int t = 0;
-    bool have_prev = false;
-    Sub prev{};
-    for (;;) {
-        const int buf = t & 1;
-        cp_async_wait_all();
-        tc::fence_proxy_async();
-        tc::fence_before();
-        __syncthreads();
-        tc::fence_after();
-        if (tid == 0) {
-            const uint32_t a0 = tc::smem_u32(Ah), al0 = tc::smem_u32(Al);
-            float* Bh = Bbase + (size_t)buf * 2 * (kTcBBytes / 4);
-            const uint32_t b0 = tc::smem_u32(Bh), bl0 = tc::smem_u32(Bh + kTcBBytes / 4);
-            const uint32_t dst = dtm + (uint32_t)(buf * 64);
-#pragma unroll
-            for (int s2 = 0; s2 < 16; ++s2) {
-                const uint64_t ah = tc::smem_desc(a0 + s2 * 2 * lboA, lboA, 128);
-                const uint64_t al = tc::smem_desc(al0 + s2 * 2 * lboA, lboA, 128);
-                const uint64_t bh = tc::smem_desc(b0 + s2 * 2 * lboB, lboB, 128);
-                const uint64_t bl = tc::smem_desc(bl0 + s2 * 2 * lboB, lboB, 128);
-                tc::mma_tf32(dst, al, bh, idesc, s2 > 0);
-                tc::mma_tf32(dst, ah, bl, idesc, 1);
-                tc::mma_tf32(dst, ah, bh, idesc, 1);
-            }
-            tc::commit(&bar[buf]);
-        }
-        // drain t-1 (its MMA completed before MMA(t) was issued... or soon after)
-        if (have_prev) epilogue(buf ^ 1, prev);
-        prev = cur;
-        have_prev = true;
-        advance();
-        if (!valid()) break;
-        Sub nxt = sub_at(blk, ti, half);
-        if (nxt.off != cur_off) {
-            // the operator is about to change: wait for MMA(t) and drain it first
-            epilogue(buf, cur);
-            have_prev = false;
+    if (valid()) {
+        Sub cur = sub_at(ti, half);
+        load_a(cur.off);
+        cur_off = cur.off;
+        gather(cur, 0);
+        int t = 0;
+        bool have_prev = false;
+        Sub prev{};
+        for (;;) {
+            const int buf = t & 1;
+            cp_async_wait_all();
+            tc::fence_proxy_async();
             tc::fence_before();
             __syncthreads();
-            load_a(nxt.off);
-            cur_off = nxt.off;
+            tc::fence_after();
+            if (tid == 0) {
+                float* Bh = Bbase + (size_t)buf * 2 * (kTcBBytes / 4);
+                const uint32_t b0 = tc::smem_u32(Bh), bl0 = tc::smem_u32(Bh + kTcBBytes / 4);
+                const uint32_t dst = dtm + kTcColD + (uint32_t)(buf * 64);
+#pragma unroll
+                for (int s2 = 0; s2 < 16; ++s2) {
+                    const uint64_t bh = tc::smem_desc(b0 + s2 * 2 * lboB, lboB, 128);
+                    const uint64_t bl = tc::smem_desc(bl0 + s2 * 2 * lboB, lboB, 128);
+                    tc::mma_tf32_ts(dst, dtm + kTcColAl + 8 * s2, bh, idesc, s2 > 0);
+                    tc::mma_tf32_ts(dst, dtm + kTcColAh + 8 * s2, bl, idesc, 1);
+                    tc::mma_tf32_ts(dst, dtm + kTcColAh + 8 * s2, bh, idesc, 1);
+                }
+                tc::commit(&bar[buf]);
+            }
+            // MMA(t-1) done -> its B buffer (buf^1) is free: issue the gather of t+1 first,
+            // then drain the accumulator of t-1 while the copies and MMA(t) are in flight
+            const bool had_prev = have_prev;
+            const Sub pv = prev;
+            if (had_prev) wait_mma(buf ^ 1);
+            prev = cur;
+            have_prev = true;
+            advance();
+            const bool more = valid();
+            Sub nxt{};
+            bool switch_a = false;
+            if (more) {
+                nxt = sub_at(ti, half);
+                switch_a = nxt.off != cur_off;
+                if (!switch_a) gather(nxt, buf ^ 1);
+            }
+            if (had_prev) drain(buf ^ 1, pv);
+            if (!more) break;
+            if (switch_a) {
+                // the operator is about to change: wait for MMA(t) and drain it first
+                epilogue(buf, cur);
+                have_prev = false;
+                tc::fence_before();
+                __syncthreads();
+                tc::fence_after();
+                load_a(nxt.off);
+                cur_off = nxt.off;
+                gather(nxt, buf ^ 1);
+            }
+            cur = nxt;
+            ++t;
         }
-        // buffer buf^1 was last read by MMA(t-1), drained above
-        gather(nxt, buf ^ 1);
-        cur = nxt;
-        ++t;
+        if (have_prev) epilogue(t & 1, prev);
     }
-    if (have_prev) epilogue(t & 1, prev);
     tc::fence_before();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc<128>(tbase);
+    if (warp == 0) tc::tmem_dealloc<512>(tbase);
 }
 
 // ------------------------------------------------------------------ P2L (X list)
@@ -844,8 +866,9 @@ float tf32_host(float x)
     return r;
 }
 
-// M2L operator images for k_m2l_tc: per offset, hi and lo tf32 parts of
-// T[i][k] (i, k < 121, zero padded to 128) in the core-matrix layout.
+// M2L operator images for k_m2l_tc: per offset, the hi and lo TF32 parts of
+// T[i][k] (i, k < 121, zero padded to 128), row-major [part][i][k] (one TMEM
+// lane per row i).
 void upload_tc_images(DBuf<float>& dst, const std::vector<double>& src)
 {
     const size_t img = 128 * 128;
@@ -855,9 +878,8 @@ void upload_tc_images(DBuf<float>& dst, const std::vector<double>& src)
             for (int k = 0; k < kNC; ++k) {
                 const float a = (float)src[(size_t)m * kNC * kNC + (size_t)i * kNC + k];
                 const float hi = tf32_host(a);
-                const size_t o = tc::core_offset(i, k, 128) / 4;
-                h[(size_t)m * 2 * img + o] = hi;
-                h[(size_t)m * 2 * img + img + o] = a - hi;
+                h[(size_t)m * 2 * img + (size_t)i * 128 + k] = hi;
+                h[(size_t)m * 2 * img + img + (size_t)i * 128 + k] = a - hi;
             }
     dst.alloc(h.size());
     XRL_CUDA(cudaMemcpy(dst.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));

@@ -859,7 +859,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         }
         T->n_m2l_tiles = (int)tiles.size();
         T->n_m2l_subtiles = 0;
-        for (const int4& tl : tiles) T->n_m2l_subtiles += (tl.z + 5) / 6;
+        for (const int4& tl : tiles) T->n_m2l_subtiles += (tl.z + 7) / 8;
         T->m2l_tiles.alloc(std::max<size_t>(1, tiles.size()));
         if (!tiles.empty())
             XRL_CUDA(cudaMemcpyAsync(T->m2l_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
