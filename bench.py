@@ -161,7 +161,7 @@ def run_reference(args):
 
 
 def _tc_subtiles(tree) -> int:
-    """Number of 6-pair sub-tiles the tcgen05 M2L issues (from the library's tile list)."""
+    """Number of tcgen05 MMA groups (one per <= 16-pair tile) the M2L issues."""
     return int(tree.info()["n_m2l_subtiles"])
 
 
@@ -316,15 +316,15 @@ def run_xrl(args):
                         "algorithmic": f"2*121^2*6 = 175692 flops x {info['n_v_pairs']} V-list translations per launch",
                         "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 flops x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
     elif phases["m2l"][1]:
-        # tcgen05 3xTF32: per 8-pair sub-tile 48 MMAs of M128 N64 K8 (2*128*64*8 flops each)
+        # tcgen05 3xTF32: per 16-pair tile 48 MMAs of M128 N96 K8 (2*128*96*8 flops each)
         n_sub = _tc_subtiles(tree)
-        issued = n_sub * 48 * 2.0 * 128 * 64 * 8
+        issued = n_sub * 48 * 2.0 * 128 * 96 * 8
         tf32_peak = float(peaks.get("bf16_tflops", 1656.1)) * 0.5  # nominal tf32/bf16 dense ratio 1.1/2.25
         a = issued / (per_launch_ms("m2l") * 1e-3) / 1e12
         alg = 2.0 * nc * nc * 6 * info["n_v_pairs"] / (per_launch_ms("m2l") * 1e-3) / 1e12
         roofs["m2l"] = {"kernel": "k_m2l_tc", "bound": "tensor", "achieved": a, "peak": tf32_peak, "unit": "TFLOP/s",
                         "frac": a / tf32_peak, "traffic": traffic_from_profiles("k_m2l_tc", tkey),
-                        "algorithmic": f"issued tcgen05 kind::tf32 MMA flops: {n_sub} sub-tiles x 48 x 2*128*64*8 per launch "
+                        "algorithmic": f"issued tcgen05 kind::tf32 MMA flops: {n_sub} tiles x 48 x 2*128*96*8 per launch "
                                        f"(3xTF32 split; FP32-equivalent algorithmic rate {alg:.1f} TFLOP/s = "
                                        f"{alg / fp32_peak:.2f} of the FP32 SIMT peak)",
                         "peak_source": "tf32 dense = bf16_tflops (MEASURED_PEAKS.json) x 0.5 (nominal 1.1/2.25 PF)"}

@@ -135,7 +135,7 @@ typedef struct {
     double root_lo[3];    /* root cube corner (m) */
     double root_width;    /* root cube width W (m) */
     int64_t n_m2l_tiles;     /* 16-pair M2L tiles of this rank */
-    int64_t n_m2l_subtiles;  /* 8-pair tcgen05 sub-tiles of this rank */
+    int64_t n_m2l_subtiles;  /* tcgen05 MMA groups (one per <= 16-pair tile, N = 96) of this rank */
 } xrl_tree_info_t;
 xrl_status xrl_tree_info(xrl_tree tree, xrl_tree_info_t* info);
 

@@ -8,21 +8,21 @@
 // correction N = P - 1/r (near.cu).
 //
 // Kernels (one launch each unless noted):
-//   k_pack     complex64 [3][n] -> float [n][8] charges          (HBM, 48 B/panel)
-//   k_p2m      leaf multipoles mu = sum q Rt(u)                   (per leaf)
-//   k_m2m      child -> parent, per level (bottom-up)
-//   k_m2l      V-list translations, batched by offset: the 121x121 operator
-//              stays in shared memory while 32 (target, source) pairs x 6
-//              RHS stream through it (SGEMM-like register tiling, 8x12 per
-//              thread); results are accumulated with red.global.add.v4.f32
-//   k_p2l      X-list particle -> local
-//   k_l2l      parent -> child, per level (top-down)
-//   k_leaf     per target leaf: L2P + M2P (W list) + P2P (U list) + near CSR,
-//              writes y once
+//   k_pack       complex64 [3][n] -> float [n][8] charges          (HBM, 48 B/panel)
+//   k_near_spmv  near correction CSR x (side stream)               (HBM)
+//   k_p2p        U-list direct sum, packed f32x2 (side stream)     (FP32 pipe)
+//   k_p2m        leaf multipoles mu = sum q Rt(u)                   (per leaf)
+//   k_m2m        child -> parent, per level (bottom-up)
+//   k_mu_img     mu[k][r] -> FP32 r-major image for the tensor-core M2L
+//   k_m2l_tc     V-list translations on tcgen05 (3xTF32, warp-specialised)
+//   k_p2l        X-list particle -> local
+//   k_l2l        parent -> child, per level (top-down)
+//   k_l2p_m2p    per target panel: L2P + M2P (W list), completes y
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "tcgen05.h"
 #include "xrl_internal.h"
@@ -33,8 +33,6 @@ __constant__ RecTables<float> c_tab;
 
 namespace {
 
-constexpr int kTP = 16;          // pairs per M2L tile
-constexpr int kBCols = kTP * 6 + 4;  // 96 columns of the M2L B tile (+4 pad: spreads the gather over banks)
 
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d)
 {
@@ -156,11 +154,11 @@ __global__ void __launch_bounds__(128) k_l2l(const int32_t* __restrict__ boxes, 
                                              const int32_t* __restrict__ iz, const float* __restrict__ op,
                                              float* __restrict__ ell)
 {
-    __shared__ float src[kBoxStride];
+    __shared__ float src[kEllStride];  // parent ell[r][k]
     const int b = boxes[blockIdx.x];
     const int P = parent[b];
-    for (int j = threadIdx.x; j < kBoxStride / 4; j += blockDim.x)
-        reinterpret_cast<float4*>(src)[j] = reinterpret_cast<const float4*>(ell + (size_t)P * kBoxStride)[j];
+    for (int j = threadIdx.x; j < kEllStride / 4; j += blockDim.x)
+        reinterpret_cast<float4*>(src)[j] = reinterpret_cast<const float4*>(ell + (size_t)P * kEllStride)[j];
     __syncthreads();
     const int i = threadIdx.x;
     if (i >= kNC) return;
@@ -171,311 +169,322 @@ __global__ void __launch_bounds__(128) k_l2l(const int32_t* __restrict__ boxes, 
     for (int k = n * n; k < kNC; ++k) {
         const float t = T[k * kNCP + i];
 #pragma unroll
-        for (int r = 0; r < 6; ++r) acc[r] += t * src[6 * k + r];
+        for (int r = 0; r < 6; ++r) acc[r] += t * src[r * 128 + k];
     }
-    float* out = ell + (size_t)b * kBoxStride + 6 * i;
+    float* out = ell + (size_t)b * kEllStride + i;
 #pragma unroll
-    for (int r = 0; r < 6; ++r) out[r] += acc[r];
-}
-
-// ------------------------------------------------------------------ M2L
-// Tile = (offset o, pairs [begin, begin+count)), count <= kTP = 16.  Tiles are
-// ordered target-chunk-major (4096 target boxes per chunk), then by offset, so
-// the mu gathers and the ell reductions of the tiles in flight stay in L2.
-// C[128 x 96] = T_o[128 x 121] * B[121 x 96], B[k][p*6+r] = mu_src(p)[k][r].
-// 256 threads: rg = tid % 16 owns rows rg*4..+3 and 64+rg*4..+3 (float4 rows
-// contiguous across the 16 lanes: no bank conflicts), cg = tid / 16 owns pair cg.
-// 108 KB shared memory -> 2 CTAs per SM so one CTA's loads overlap the other's FMAs.
-constexpr int kM2LSmem = (kNC * kNCP + kNC * kBCols) * 4;
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
-{
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
-{
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-__global__ void __launch_bounds__(256, 2) k_m2l(const int4* __restrict__ tiles, const int32_t* __restrict__ tgt,
-                                                const int32_t* __restrict__ srcb, const float* __restrict__ ops,
-                                                const float* __restrict__ mu, float* __restrict__ ell)
-{
-    extern __shared__ __align__(16) float sm[];
-    float* Ts = sm;                    // [121][128]
-    float* Bs = sm + kNC * kNCP;       // [121][96]
-    const int4 tile = tiles[blockIdx.x];
-    const int off = tile.x, begin = tile.y, count = tile.z;
-    const int tid = threadIdx.x;
-    {
-        const float4* g = reinterpret_cast<const float4*>(ops + (size_t)off * kNC * kNCP);
-        float4* s = reinterpret_cast<float4*>(Ts);
-        for (int j = tid; j < kNC * kNCP / 4; j += 256) cp_async16(s + j, g + j);
-    }
-    for (int j = tid; j < kTP * 363; j += 256) {
-        const int p = j / 363, q = j % 363;
-        const int k = q / 3, r2 = q % 3;
-        float* dst = &Bs[k * kBCols + p * 6 + 2 * r2];
-        if (p < count) cp_async8(dst, reinterpret_cast<const float2*>(mu + (size_t)srcb[begin + p] * kBoxStride) + q);
-        else *reinterpret_cast<float2*>(dst) = make_float2(0.f, 0.f);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    const int rg = tid & 15, cg = tid >> 4;
-    float acc[8][6];
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int c = 0; c < 6; ++c) acc[a][c] = 0.f;
-    const float* tp = Ts + rg * 4;
-    const float* bp = Bs + cg * 6;
-#pragma unroll 4
-    for (int k = 0; k < kNC; ++k) {
-        const float4 t0 = *reinterpret_cast<const float4*>(tp + k * kNCP);
-        const float4 t1 = *reinterpret_cast<const float4*>(tp + k * kNCP + 64);
-        const float2 b0 = *reinterpret_cast<const float2*>(bp + k * kBCols);
-        const float2 b1 = *reinterpret_cast<const float2*>(bp + k * kBCols + 2);
-        const float2 b2 = *reinterpret_cast<const float2*>(bp + k * kBCols + 4);
-        const float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-        const float bv[6] = {b0.x, b0.y, b1.x, b1.y, b2.x, b2.y};
-#pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-            for (int c = 0; c < 6; ++c) acc[a][c] = fmaf(tv[a], bv[c], acc[a][c]);
-    }
-    if (cg >= count) return;
-    float* base = ell + (size_t)tgt[begin + cg] * kBoxStride;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int i = (j >> 1) * 64 + rg * 4 + 2 * (j & 1);
-        if (i >= kNC) continue;
-        float* o = base + 6 * i;
-        const float* a0 = acc[2 * j];
-        const float* a1 = acc[2 * j + 1];
-        red_add_v4(o, a0[0], a0[1], a0[2], a0[3]);
-        red_add_v4(o + 4, a0[4], a0[5], a1[0], a1[1]);
-        if (i + 1 < kNC) red_add_v4(o + 8, a1[2], a1[3], a1[4], a1[5]);
-    }
+    for (int r = 0; r < 6; ++r) out[r * 128] += acc[r];
 }
 
 // ------------------------------------------------------------------ M2L on tcgen05
-// Tensor-core M2L.  After the upward pass every box's multipole is written once
-// as a TF32 hi/lo "image" in the tcgen05 canonical K-major core-matrix layout
-// with the 6 RHS padded to 8 rows, i.e. one 8-row core group per box:
-//   img[box][hi|lo][kc = k/4][r = 0..7][k % 4]   (32 x 128 B per part, 8 KB per box).
-// A sub-tile of 8 (target, source) pairs sharing one offset then needs as B
-// operand [kc][pair][128 B] (LBO = 1024 B between K chunks, SBO = 128 B between
-// pairs): pure 16-byte cp.async copies.  The operator T_o (hi and lo, 128 x 128
-// TF32) lives in TMEM (lane = output coefficient, column = input coefficient),
-// written with tcgen05.st when the offset changes, so the MMAs only read B from
-// shared memory.  D[128 x 64] (TMEM, FP32) = T_o x B with 3xTF32
-// (A_lo B_hi + A_hi B_lo + A_hi B_hi; 48 tcgen05.mma kind::tf32 M128 N64 K8).
-// Pipeline (two B buffers, two TMEM accumulators): while MMA(t) runs, the 8
-// warps issue the cp.async gather of t+1 and drain the accumulator of t-1
-// (tcgen05.ld -> red.global.add.{v4,v2}.f32 into ell).  One persistent CTA per
-// SM (TMEM 512 columns) walks blocks of kTcR tiles (same offset -> operator
-// reuse), blocks dealt round-robin so all CTAs stay inside one L2-resident
-// target chunk.  128 KB of shared memory leaves room for P2P CTAs on the SM.
-constexpr int kTcP = 8;                             // pairs per sub-tile
-constexpr int kTcN = kTcP * 8;                      // 64 MMA columns (6 RHS + 2 pad per pair)
-constexpr int kTcBBytes = kTcN * 128 * 4;           // one B image (hi or lo): 32 KB
-constexpr int kTcSmem = 4 * kTcBBytes;              // 2 buffers x (hi, lo)
-constexpr int kTcR = 8;
-constexpr int kTcThreads = 256;
-constexpr int kImgFloats = 2 * 32 * 32;             // per box: hi + lo, 32 K-chunks x 32 floats
-constexpr uint32_t kTcColD = 0, kTcColAh = 256, kTcColAl = 384;
+// Tensor-core M2L (V list), 3xTF32 on tcgen05.mma kind::tf32.  Pairs (target t,
+// source s) sharing one offset o are cut into tiles of <= 21 pairs; a tile is one
+// 128 x 128 x 128 product
+//     D[(p, r)][i] = sum_k A[(p, r)][k] B[i][k],   A = mu_s(p)[r][k], B = T_o[i][k]
+// with row (p, r) = 6 p + r (126 rows used), i.e. the 6 RHS of 21 source
+// multipoles against one operator.  Roles (288 threads, warp-specialised):
+//   warps 0-3 (loaders, thread = TMEM lane (p, r)): LDG the FP32 multipole row
+//     (r-major image, 512 B), split it into TF32 hi/lo and tcgen05.st them into
+//     TMEM (A_hi, A_lo), one K-half (64 columns) at a time, one tile ahead;
+//   warp 8 (MMA issuer, one thread): per K-half 3 x 8 MMAs (A_lo B_hi, A_hi B_lo,
+//     A_hi B_hi, M128 N128 K8) into one of two TMEM accumulators; the operator
+//     hi/lo (128 KB, canonical K-major layout) stays in shared memory for a block
+//     of tiles with the same offset (cp.async.bulk);
+//   warps 4-7 (drain, thread = TMEM lane): tcgen05.ld the 121 coefficients of
+//     row (p, r) and red.global.add.v4 them into ell[t(p)][r][0..120] (r-major).
+// mbarriers: a_full/a_free per K-half (A), d_full/d_free per accumulator, op_full.
+// One persistent CTA per SM; blocks (runs of tiles with one (chunk, offset))
+// dealt round-robin, so all CTAs work inside one L2-resident target chunk.
+constexpr int kTcPairs = 21;                        // pairs per tile (126 of 128 TMEM lanes)
+constexpr int kTcThreads = 288;                     // 4 loader + 4 drain + 1 MMA warps
+constexpr int kTcOpBytes = 128 * 128 * 4;           // one operator part (hi or lo): 64 KB
+constexpr int kTcStageLd = 132;                     // drain stage row stride (floats; conflict-free STS.128)
+constexpr int kTcSmem = 2 * kTcOpBytes + 128 * kTcStageLd * 4 + 1024;  // operator hi + lo, drain stage (+ align)
+constexpr int kImgFloats = 6 * 128;                 // per box: r-major FP32 multipole image
+constexpr uint32_t kTcColAh = 0, kTcColAl = 128, kTcColD = 256;  // D buffers at 256 and 384
 
-__device__ __forceinline__ void red_add_v2(float* p, float a, float b)
-{
-    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
-}
-
-// img[b][part][kc][r][j] = split(mu[b][4 kc + j][r]) for r < 6, k < 121; else 0.
+// img[b][r][k] = mu[b][k][r] for k < 121, 0 for 121 <= k < 128.
 __global__ void k_mu_img(int nbox, const float* __restrict__ mu, float* __restrict__ img)
 {
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one per (box, kc, r, j)
-    if (e >= (int64_t)nbox * 1024) return;
-    const int b = (int)(e >> 10), w = (int)(e & 1023);
-    const int kc = w >> 5, r = (w >> 2) & 7, j = w & 3;
-    const int k = 4 * kc + j;
-    const float x = (r < 6 && k < kNC) ? mu[(size_t)b * kBoxStride + 6 * k + r] : 0.f;
-    const float hi = tc::tf32_rna(x);
-    img[(size_t)b * kImgFloats + w] = hi;
-    img[(size_t)b * kImgFloats + 1024 + w] = x - hi;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one per (box, r, k)
+    if (e >= (int64_t)nbox * kImgFloats) return;
+    const int b = (int)(e / kImgFloats), w = (int)(e % kImgFloats);
+    const int r = w >> 7, k = w & 127;
+    img[e] = k < kNC ? mu[(size_t)b * kBoxStride + 6 * k + r] : 0.f;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict__ tiles, int ntiles,
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     tc::smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+                 : "memory");
+}
+
+// 32-byte (whole sector) read-only load, no L1 allocation
+__device__ __forceinline__ void ldg256(const float* p, float* v)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.b32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+// whole-warp wait with a warp-uniform exit condition (keeps the warp converged)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t phase)
+{
+    while (!__all_sync(0xffffffffu, mbar_try(bar, phase))) {
+    }
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// This CTA's tile sequence: blocks blockIdx.x, blockIdx.x + gridDim.x, ...; all tiles of each block.
+struct TileSeq {
+    int bi, ti, tend;
+    bool ok;
+    __device__ TileSeq(const int4* __restrict__ blocks, int nblocks) : bi(blockIdx.x), ti(0), tend(0), ok(false)
+    {
+        for (; bi < nblocks; bi += gridDim.x) {
+            const int4 bk = __ldg(blocks + bi);
+            if (bk.y > 0) { ti = bk.x; tend = bk.x + bk.y; ok = true; return; }
+        }
+    }
+    __device__ void advance(const int4* __restrict__ blocks, int nblocks)
+    {
+        if (++ti < tend) return;
+        ok = false;
+        for (bi += gridDim.x; bi < nblocks; bi += gridDim.x) {
+            const int4 bk = __ldg(blocks + bi);
+            if (bk.y > 0) { ti = bk.x; tend = bk.x + bk.y; ok = true; return; }
+        }
+    }
+};
+
+// blocks[j] = {first tile, #tiles, offset, chunk}; tiles[t] = {offset, first pair, #pairs, chunk}
+__global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict__ blocks, int nblocks,
+                                                          const int4* __restrict__ tiles,
                                                           const int32_t* __restrict__ tgt,
                                                           const int32_t* __restrict__ srcb,
-                                                          const float* __restrict__ aimg,
-                                                          const float* __restrict__ bimg, float* __restrict__ ell)
+                                                          const float* __restrict__ opimg,
+                                                          const float* __restrict__ bimg, float* __restrict__ ell,
+                                                          int dbg)
 {
-    extern __shared__ __align__(1024) uint8_t tsm[];
-    float* Bbase = reinterpret_cast<float*>(tsm);  // [buf][hi/lo][32 kc][8 pairs][32 floats]
-    __shared__ uint64_t bar[2];
+    extern __shared__ uint8_t tsm_raw[];
+    uint8_t* opsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+    float* stage = reinterpret_cast<float*>(opsm + 2 * kTcOpBytes);  // [128 rows][kTcStageLd]
+    __shared__ uint64_t a_full[2], a_free[2], d_full[2], d_free[2], op_full;
     __shared__ uint32_t tbase;
+    __shared__ int rowdst[128];  // drain: target box of each accumulator row (-1: none)
+    __shared__ int4 mma_blk;     // MMA warp: current block descriptor (uniform)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) { tc::mbar_init(&bar[0], 1); tc::mbar_init(&bar[1], 1); }
-    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) {
+        for (int h = 0; h < 2; ++h) {
+            tc::mbar_init(&a_full[h], 4);
+            tc::mbar_init(&a_free[h], 1);
+            tc::mbar_init(&d_full[h], 1);
+            tc::mbar_init(&d_free[h], 4);
+        }
+        tc::mbar_init(&op_full, 1);
+    }
+    if (warp == 8) tc::tmem_alloc<512>(&tbase);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    const uint32_t dtm = tbase;
-    const uint32_t idesc = tc::idesc_tf32(128, kTcN);
-    const uint32_t lboB = kTcP * 128;
-    uint32_t ph[2] = {0, 0};
-    int cur_off = -1;
+    const uint32_t tm = tbase;
 
-    struct Sub { int off, begin, count; };
-    auto sub_at = [&](int ti, int half) -> Sub {
-        const int4 tile = tiles[ti];
-        return {tile.x, tile.y + half * kTcP, min(kTcP, tile.z - half * kTcP)};
-    };
-    // cp.async of a sub-tile's B operand (hi and lo) into buffer buf: 2 x 32 kc x 8 pairs x 8 x 16 B
-    auto gather = [&](const Sub& sb, int buf) {
-        float* B = Bbase + (size_t)buf * 2 * (kTcBBytes / 4);
-        for (int c = tid; c < 4096; c += kTcThreads) {
-            const int part = c >> 11, kc = (c >> 6) & 31, p = (c >> 3) & 7, piece = c & 7;
-            float4* dst = reinterpret_cast<float4*>(B + part * (kTcBBytes / 4) + kc * (kTcP * 32) + p * 32) + piece;
-            if (p < sb.count) {
-                const float4* src = reinterpret_cast<const float4*>(
-                    bimg + (size_t)srcb[sb.begin + p] * kImgFloats + part * 1024 + kc * 32) + piece;
-                cp_async16(dst, src);
-            } else {
-                *dst = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-    };
-    auto wait_mma = [&](int buf) {
-        tc::mbar_wait(&bar[buf], ph[buf]);
-        ph[buf] ^= 1;
-        tc::fence_after();
-    };
-    auto drain = [&](int buf, const Sub& sb) {
-        // lane quarter qd = warp % 4 (coefficients 32 qd + lane); pair group g = warp / 4 owns pairs g, g+2, ...
-        const int qd = warp & 3, g = warp >> 2;
-        const int i = 32 * qd + lane;
+    if (warp < 4) {
+        // ---------------- loaders: thread = TMEM lane L = (p, r).  A K-half of the multipole row
+        // (64 floats, 8 x 256-bit loads: whole 32-byte sectors per lane) is prefetched into
+        // registers half a tile ahead of its use; tile descriptors and source ids a tile ahead.
+        const int L = tid, p = L / 6, r = L % 6;
+        const bool lane_ok = L < 6 * kTcPairs;
+        const uint32_t ta = tm + ((uint32_t)(32 * warp) << 16);
+        auto row_of = [&](const int4& tl, bool ok) -> const float* {
+            if (!ok || !lane_ok || p >= tl.z || (dbg & 2)) return nullptr;
+            return bimg + (size_t)__ldg(srcb + tl.y + p) * kImgFloats + r * 128;
+        };
+        float x[64];
+        auto load_half = [&](const float* row, int h) {
 #pragma unroll
-        for (int pp = 0; pp < kTcP / 2; ++pp) {
-            const int p = g + 2 * pp;
-            float v[8];
-            tc::tmem_ld8(dtm + ((uint32_t)(32 * qd) << 16) + (uint32_t)(kTcColD + buf * 64 + 8 * p), v);
-            if (i < kNC && p < sb.count) {
-                float* o = ell + (size_t)tgt[sb.begin + p] * kBoxStride + 6 * i;
-                if ((i & 1) == 0) {
-                    red_add_v4(o, v[0], v[1], v[2], v[3]);
-                    red_add_v2(o + 4, v[4], v[5]);
+            for (int c = 0; c < 8; ++c) {
+                if (row) {
+                    ldg256(row + 64 * h + 8 * c, x + 8 * c);
                 } else {
-                    red_add_v2(o, v[0], v[1]);
-                    red_add_v4(o + 2, v[2], v[3], v[4], v[5]);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) x[8 * c + q] = 0.f;
                 }
             }
-        }
-    };
-    auto epilogue = [&](int buf, const Sub& sb) { wait_mma(buf); drain(buf, sb); };
-    // operator hi/lo rows into TMEM: warp w writes lanes of quarter w % 4, columns half (w / 4)
-    auto load_a = [&](int off) {
-        const int qd = warp & 3, hf = warp >> 2;
-        const int i = 32 * qd + lane;
-        const float* rowh = aimg + ((size_t)off * 2 * 128 + i) * 128 + 64 * hf;
-        const float* rowl = rowh + 128 * 128;
-        const uint32_t ta = dtm + ((uint32_t)(32 * qd) << 16) + 64 * hf;
-        float v[32];
+        };
+        TileSeq s0(blocks, nblocks);
+        const float* row0 = row_of(s0.ok ? __ldg(tiles + s0.ti) : make_int4(0, 0, 0, 0), s0.ok);
+        load_half(row0, 0);
+        TileSeq s1 = s0;
+        s1.advance(blocks, nblocks);
+        int4 tl1 = s1.ok ? __ldg(tiles + s1.ti) : make_int4(0, 0, 0, 0);
+        for (int j = 0; s0.ok; ++j) {
+            const float* row1 = nullptr;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float4 q = __ldg(reinterpret_cast<const float4*>(rowh + 32 * c) + j);
-                v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
-            }
-            tc::tmem_st32(ta + kTcColAh + 32 * c, v);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float4 q = __ldg(reinterpret_cast<const float4*>(rowl + 32 * c) + j);
-                v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
-            }
-            tc::tmem_st32(ta + kTcColAl + 32 * c, v);
-        }
-        tc::tmem_st_wait();
-    };
-
-    int blk = blockIdx.x, ti = blk * kTcR, half = 0;
-    auto valid = [&]() { return blk * kTcR < ntiles && ti < min(ntiles, (blk + 1) * kTcR); };
-    auto advance = [&]() {
-        if ((half + 1) * kTcP < tiles[ti].z) { ++half; return; }
-        half = 0;
-        ++ti;
-        if (ti >= min(ntiles, (blk + 1) * kTcR)) { blk += gridDim.x; ti = blk * kTcR; }
-    };
-    if (valid()) {
-        Sub cur = sub_at(ti, half);
-        load_a(cur.off);
-        cur_off = cur.off;
-        gather(cur, 0);
-        int t = 0;
-        bool have_prev = false;
-        Sub prev{};
-        for (;;) {
-            const int buf = t & 1;
-            cp_async_wait_all();
-            tc::fence_proxy_async();
-            tc::fence_before();
-            __syncthreads();
-            tc::fence_after();
-            if (tid == 0) {
-                float* Bh = Bbase + (size_t)buf * 2 * (kTcBBytes / 4);
-                const uint32_t b0 = tc::smem_u32(Bh), bl0 = tc::smem_u32(Bh + kTcBBytes / 4);
-                const uint32_t dst = dtm + kTcColD + (uint32_t)(buf * 64);
-#pragma unroll
-                for (int s2 = 0; s2 < 16; ++s2) {
-                    const uint64_t bh = tc::smem_desc(b0 + s2 * 2 * lboB, lboB, 128);
-                    const uint64_t bl = tc::smem_desc(bl0 + s2 * 2 * lboB, lboB, 128);
-                    tc::mma_tf32_ts(dst, dtm + kTcColAl + 8 * s2, bh, idesc, s2 > 0);
-                    tc::mma_tf32_ts(dst, dtm + kTcColAh + 8 * s2, bl, idesc, 1);
-                    tc::mma_tf32_ts(dst, dtm + kTcColAh + 8 * s2, bh, idesc, 1);
-                }
-                tc::commit(&bar[buf]);
-            }
-            // MMA(t-1) done -> its B buffer (buf^1) is free: issue the gather of t+1 first,
-            // then drain the accumulator of t-1 while the copies and MMA(t) are in flight
-            const bool had_prev = have_prev;
-            const Sub pv = prev;
-            if (had_prev) wait_mma(buf ^ 1);
-            prev = cur;
-            have_prev = true;
-            advance();
-            const bool more = valid();
-            Sub nxt{};
-            bool switch_a = false;
-            if (more) {
-                nxt = sub_at(ti, half);
-                switch_a = nxt.off != cur_off;
-                if (!switch_a) gather(nxt, buf ^ 1);
-            }
-            if (had_prev) drain(buf ^ 1, pv);
-            if (!more) break;
-            if (switch_a) {
-                // the operator is about to change: wait for MMA(t) and drain it first
-                epilogue(buf, cur);
-                have_prev = false;
-                tc::fence_before();
-                __syncthreads();
+            for (int h = 0; h < 2; ++h) {
+                // the MMAs of the previous tile must be done with this K-half of A
+                tc::mbar_wait(&a_free[h], (j & 1) ^ 1);
                 tc::fence_after();
-                load_a(nxt.off);
-                cur_off = nxt.off;
-                gather(nxt, buf ^ 1);
+#pragma unroll
+                for (int c2 = 0; c2 < 8; ++c2) {  // 8 columns at a time
+                    float hi[8], lo[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        hi[q] = tc::tf32_rna(x[8 * c2 + q]);
+                        lo[q] = x[8 * c2 + q] - hi[q];
+                    }
+                    tc::tmem_st8(ta + kTcColAh + 64 * h + 8 * c2, hi);
+                    tc::tmem_st8(ta + kTcColAl + 64 * h + 8 * c2, lo);
+                }
+                tc::tmem_st_wait();
+                tc::fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_full[h]);
+                if (h == 0) {
+                    load_half(row0, 1);
+                    row1 = row_of(tl1, s1.ok);
+                } else {
+                    load_half(row1, 0);
+                }
             }
-            cur = nxt;
-            ++t;
+            s0 = s1;
+            row0 = row1;
+            s1.advance(blocks, nblocks);
+            if (s1.ok) tl1 = __ldg(tiles + s1.ti);
         }
-        if (have_prev) epilogue(t & 1, prev);
+    } else if (warp < 8) {
+        // ---------------- drain: thread = TMEM lane L = (p, r) reads its accumulator row into a
+        // shared-memory stage; then each warp reduces whole rows into ell with one contiguous
+        // red.global.add.v4 per row (31 lanes x 16 B; ~2.3x the L2 reduction rate of row-per-lane)
+        const int L = tid - 128, p = L / 6, r = L % 6;
+        const bool lane_ok = L < 6 * kTcPairs;
+        const int qd = warp - 4;  // lane quarter (warp % 4)
+        TileSeq sq(blocks, nblocks);
+        int4 cur = sq.ok ? __ldg(tiles + sq.ti) : make_int4(0, 0, 0, 0);
+        int cur_t = (sq.ok && lane_ok && p < cur.z) ? __ldg(tgt + cur.y + p) : -1;
+        for (int j = 0; sq.ok; ++j) {
+            TileSeq nx = sq;
+            nx.advance(blocks, nblocks);
+            int nxt_t = -1;
+            int4 nxt = make_int4(0, 0, 0, 0);
+            if (nx.ok) {
+                nxt = __ldg(tiles + nx.ti);
+                if (lane_ok && p < nxt.z) nxt_t = __ldg(tgt + nxt.y + p);
+            }
+            const int d = j & 1;
+            tc::mbar_wait(&d_full[d], (j >> 1) & 1);
+            tc::fence_after();
+            const uint32_t ta = tm + ((uint32_t)(32 * qd) << 16) + kTcColD + 128 * d;
+            float* srow = stage + L * kTcStageLd;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float v[32];
+                if (dbg & 4) {
+                    for (int q = 0; q < 32; ++q) v[q] = 0.f;
+                } else {
+                    tc::tmem_ld32(ta + 32 * c, v);
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<float4*>(srow + 32 * c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&d_free[d]);  // accumulator d may be overwritten
+            rowdst[L] = cur_t;
+            named_bar_sync(1, 128);
+            for (int R = qd; R < 6 * kTcPairs; R += 4) {
+                const int t = rowdst[R];
+                if (t < 0 || (dbg & 1)) continue;
+                if (lane < 31) {
+                    const float4 v = *reinterpret_cast<const float4*>(stage + R * kTcStageLd + 4 * lane);
+                    red_add_v4(ell + (size_t)t * kEllStride + (R % 6) * 128 + 4 * lane, v.x, v.y, v.z, v.w);
+                }
+            }
+            named_bar_sync(1, 128);  // stage is reused by the next tile
+            sq = nx;
+            cur = nxt;
+            cur_t = nxt_t;
+        }
+    } else {
+        // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform control
+        // (block descriptors through shared memory, barrier waits voted with __all_sync) so the
+        // descriptors stay in uniform registers and lane 0 issues back-to-back UTCHMMAs
+        // (uniform bases recomputed here so they live in uniform registers)
+        const uint32_t tmu = tbase;
+        const uint32_t oph = (tc::smem_u32(tsm_raw) + 1023u) & ~1023u, opl = oph + kTcOpBytes;
+        const uint32_t idesc = tc::idesc_tf32(128, 128);
+        int j = 0, nb = 0;
+        for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x, ++nb) {
+            int4 bk = __ldg(blocks + bi);
+            bk.y = __shfl_sync(0xffffffffu, bk.y, 0);  // warp-uniform (keeps the MMA operands in uniform registers)
+            bk.z = __shfl_sync(0xffffffffu, bk.z, 0);
+            if (j > 0) {  // every MMA reading the previous operator must be complete
+                mbar_wait_warp(&d_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                tc::fence_after();
+            }
+            if (lane == 0) {
+                mbar_expect_tx(&op_full, 2 * kTcOpBytes);
+                const float* src = opimg + (size_t)bk.z * 2 * 128 * 128;
+                for (int c = 0; c < 4; ++c)
+                    bulk_g2s(opsm + c * (kTcOpBytes / 2), src + c * (kTcOpBytes / 8), kTcOpBytes / 2, &op_full);
+            }
+            mbar_wait_warp(&op_full, nb & 1);
+            for (int ti = 0; ti < bk.y; ++ti, ++j) {
+                const int d = j & 1;
+                mbar_wait_warp(&d_free[d], ((j >> 1) & 1) ^ 1);
+                tc::fence_after();
+                const uint32_t dst = tmu + kTcColD + 128 * d;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    mbar_wait_warp(&a_full[h], j & 1);
+                    tc::fence_after();
+                    if (tc::elect_one()) {
+#pragma unroll
+                        for (int s = 8 * h; s < 8 * h + 8; ++s) {
+                            // B (operator) element (i, k) at ((i/8)*32 + k/4)*128 + (i%8)*16 + (k%4)*4: LBO 128, SBO 4096
+                            const uint64_t bh = tc::smem_desc(oph + 256 * s, 128, 4096);
+                            const uint64_t bl = tc::smem_desc(opl + 256 * s, 128, 4096);
+                            tc::mma_tf32_ts(dst, tmu + kTcColAl + 8 * s, bh, idesc, s > 0);
+                            tc::mma_tf32_ts(dst, tmu + kTcColAh + 8 * s, bl, idesc, 1);
+                            tc::mma_tf32_ts(dst, tmu + kTcColAh + 8 * s, bh, idesc, 1);
+                        }
+                        tc::commit(&a_free[h]);
+                        if (h == 1) tc::commit(&d_full[d]);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 0) tc::tmem_dealloc<512>(tbase);
+    if (warp == 8) tc::tmem_dealloc<512>(tbase);
 }
 
 // ------------------------------------------------------------------ P2L (X list)
@@ -559,11 +568,11 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
             __syncthreads();
         }
     }
-    float* out = ell + (size_t)b * kBoxStride;
+    float* out = ell + (size_t)b * kEllStride;
 #pragma unroll
     for (int jj = 0; jj < 6; ++jj) {
         const int o = threadIdx.x + 128 * jj;
-        if (o < kNC * 6) out[o] += acc[jj];
+        if (o < kNC * 6) out[(o % 6) * 128 + o / 6] += acc[jj];
     }
 }
 
@@ -615,25 +624,88 @@ __global__ void __launch_bounds__(256) k_near_spmv(int64_t n, int64_t r0, const 
 constexpr int kUWin = 64;
 constexpr int kSrcChunk = 512;
 constexpr int kTPT = 8;
+constexpr int kTP2 = kTPT / 2;  // packed target pairs per thread
 
+// Packed FP32 pairs (sm_100 FFMA2/FADD2/FMUL2): two targets per instruction.
+// A scalar operand is broadcast to both halves by ptxas (".F32" operand form).
+using f2x = unsigned long long;
+__device__ __forceinline__ f2x pk2(float a, float b)
+{
+    f2x r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(f2x v)
+{
+    float2 r;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c)
+{
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ void fma2_acc(f2x& acc, f2x a, f2x b)
+{
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ f2x sub2(f2x a, f2x b)
+{
+    f2x d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b)
+{
+    f2x d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x ld_shared_u64(const void* p)
+{
+    f2x v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+__device__ __forceinline__ void st_shared_u64(void* p, f2x v)
+{
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "l"(v) : "memory");
+}
+// MUFU.RSQ without the denormal fix-up (FTZ, R8: r^2 is O(1e-12) or larger in W units)
+__device__ __forceinline__ float rsqrt_ftz(float x)
+{
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Per source: 3 FADD2 + FMUL2 + 2 FFMA2 + 2 MUFU + 6 FFMA2 per two targets (7 issue slots per pair).
 template <bool kSelf>
 __device__ __forceinline__ void p2p_range(int j0, int j1, int S, const float4* __restrict__ Sp,
-                                          const float4 (*__restrict__ Sq)[2], const float* tx, const float* ty,
-                                          const float* tz, float (*far)[6])
+                                          const float4 (*__restrict__ Sq)[2], const f2x* tx, const f2x* ty,
+                                          const f2x* tz, f2x (*acc)[6])
 {
 #pragma unroll 2
     for (int j = j0; j < j1; j += S) {
         const float4 sp = Sp[j];
         const float4 q0 = Sq[j][0], q1 = Sq[j][1];
+        const f2x sx = pk2(sp.x, sp.x), sy = pk2(sp.y, sp.y), sz = pk2(sp.z, sp.z);
+        const f2x c0 = pk2(q0.x, q0.x), c1 = pk2(q0.y, q0.y), c2 = pk2(q0.z, q0.z);
+        const f2x c3 = pk2(q0.w, q0.w), c4 = pk2(q1.x, q1.x), c5 = pk2(q1.y, q1.y);
 #pragma unroll
-        for (int q = 0; q < kTPT; ++q) {
-            const float dx = tx[q] - sp.x, dy = ty[q] - sp.y, dz = tz[q] - sp.z;
-            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            float ri = rsqrtf(r2);
-            if (kSelf) ri = r2 > 0.f ? ri : 0.f;
-            far[q][0] = fmaf(q0.x, ri, far[q][0]); far[q][1] = fmaf(q0.y, ri, far[q][1]);
-            far[q][2] = fmaf(q0.z, ri, far[q][2]); far[q][3] = fmaf(q0.w, ri, far[q][3]);
-            far[q][4] = fmaf(q1.x, ri, far[q][4]); far[q][5] = fmaf(q1.y, ri, far[q][5]);
+        for (int q = 0; q < kTP2; ++q) {
+            const f2x dx = sub2(tx[q], sx), dy = sub2(ty[q], sy), dz = sub2(tz[q], sz);
+            const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
+            float ra = rsqrt_ftz(r2.x), rb = rsqrt_ftz(r2.y);
+            if (kSelf) {
+                ra = r2.x > 0.f ? ra : 0.f;
+                rb = r2.y > 0.f ? rb : 0.f;
+            }
+            const f2x ri = pk2(ra, rb);
+            fma2_acc(acc[q][0], c0, ri); fma2_acc(acc[q][1], c1, ri); fma2_acc(acc[q][2], c2, ri);
+            fma2_acc(acc[q][3], c3, ri); fma2_acc(acc[q][4], c4, ri); fma2_acc(acc[q][5], c5, ri);
         }
     }
 }
@@ -654,11 +726,11 @@ __global__ void __launch_bounds__(128) k_p2p(
 {
     // n, p0: owned panel range [p0, p0+n), y local [3][n]
     // the source staging buffers and the final reduction share one buffer
-    constexpr int kStageF = kSrcChunk * 12, kRedF = 128 * (kTPT * 6 + 1);
+    constexpr int kStageF = kSrcChunk * 12, kRedF = 128 * (kTP2 * 6 + 1) * 2;
     __shared__ __align__(16) float smraw[kStageF > kRedF ? kStageF : kRedF];
     float4* Sp = reinterpret_cast<float4*>(smraw);
     float4(*Sq)[2] = reinterpret_cast<float4(*)[2]>(smraw + 4 * kSrcChunk);
-    float(*Red)[kTPT * 6 + 1] = reinterpret_cast<float(*)[kTPT * 6 + 1]>(smraw);
+    f2x(*Red)[kTP2 * 6 + 1] = reinterpret_cast<f2x(*)[kTP2 * 6 + 1]>(smraw);  // packed target pairs
     __shared__ int Uoff[kUWin + 1], Uid[kUWin], Upb[kUWin];
     __shared__ float3 Ud[kUWin];
     __shared__ int wsum[2];
@@ -671,16 +743,28 @@ __global__ void __launch_bounds__(128) k_p2p(
         const int S = max(1, 128 / NG);
         const int tg = tid % NG, sg = tid / NG;
         const bool act = sg < S;
-        float tx[kTPT], ty[kTPT], tz[kTPT];
-        float far[kTPT][6];
+        f2x tx[kTP2], ty[kTP2], tz[kTP2];
+        f2x acc[kTP2][6];  // acc[q][r] = (y of target 2q, y of target 2q+1), RHS r
 #pragma unroll
-        for (int q = 0; q < kTPT; ++q) {
-            const int ti = tg * kTPT + q;
-            float4 p = make_float4(1e30f, 1e30f, 1e30f, 0.f);  // padding target: far away, discarded
-            if (act && ti < T) p = loc[t0 + ti];
-            tx[q] = p.x; ty[q] = p.y; tz[q] = p.z;
+        for (int q = 0; q < kTP2; ++q) {
+            float4 p[2];
 #pragma unroll
-            for (int r = 0; r < 6; ++r) far[q][r] = 0.f;
+            for (int h = 0; h < 2; ++h) {
+                const int ti = tg * kTPT + 2 * q + h;
+                p[h] = make_float4(1e18f, 1e18f, 1e18f, 0.f);  // padding target: far away, discarded
+                if (act && ti < T) p[h] = loc[t0 + ti];
+            }
+            // round trip through shared memory so each packed pair is defined by one 64-bit load
+            // (ptxas otherwise keeps the halves in unrelated registers and re-pairs them per use)
+            float2* tp = reinterpret_cast<float2*>(smraw) + (tid * kTP2 + q) * 3;
+            tp[0] = make_float2(p[0].x, p[1].x);
+            tp[1] = make_float2(p[0].y, p[1].y);
+            tp[2] = make_float2(p[0].z, p[1].z);
+            tx[q] = ld_shared_u64(tp);
+            ty[q] = ld_shared_u64(tp + 1);
+            tz[q] = ld_shared_u64(tp + 2);
+#pragma unroll
+            for (int r = 0; r < 6; ++r) acc[q][r] = 0ull;
         }
         for (int64_t u0 = uptr[b]; u0 < uptr[b + 1]; u0 += kUWin) {
             const int nu = (int)min((int64_t)kUWin, uptr[b + 1] - u0);
@@ -731,26 +815,26 @@ __global__ void __launch_bounds__(128) k_p2p(
                 __syncthreads();
                 if (act) {
                     const int a0 = max(0, min(sn, self_lo - s0)), a1 = max(0, min(sn, self_hi - s0));
-                    p2p_range<false>(first_in_class(0, sg, S), a0, S, Sp, Sq, tx, ty, tz, far);
-                    p2p_range<true>(first_in_class(a0, sg, S), a1, S, Sp, Sq, tx, ty, tz, far);
-                    p2p_range<false>(first_in_class(a1, sg, S), sn, S, Sp, Sq, tx, ty, tz, far);
+                    p2p_range<false>(first_in_class(0, sg, S), a0, S, Sp, Sq, tx, ty, tz, acc);
+                    p2p_range<true>(first_in_class(a0, sg, S), a1, S, Sp, Sq, tx, ty, tz, acc);
+                    p2p_range<false>(first_in_class(a1, sg, S), sn, S, Sp, Sq, tx, ty, tz, acc);
                 }
             }
         }
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kTPT; ++q)
+        for (int q = 0; q < kTP2; ++q)
 #pragma unroll
-            for (int r = 0; r < 6; ++r) Red[tid][q * 6 + r] = far[q][r];
+            for (int r = 0; r < 6; ++r) st_shared_u64(&Red[tid][q * 6 + r], acc[q][r]);
         __syncthreads();
         // reduce over the S source groups: thread handles target index ti = tid, tid + 128, ...
         for (int ti = tid; ti < T; ti += 128) {
-            const int g0 = ti / kTPT, q = ti % kTPT;
+            const int g0 = ti / kTPT, q = (ti % kTPT) >> 1, h = ti & 1;
             float tot[6];
 #pragma unroll
             for (int r = 0; r < 6; ++r) {
                 float f = 0.f;
-                for (int gg = 0; gg < S; ++gg) f += Red[g0 + gg * NG][q * 6 + r];
+                for (int gg = 0; gg < S; ++gg) f += reinterpret_cast<const float*>(&Red[g0 + gg * NG][q * 6 + r])[h];
                 tot[r] = f * invW;
             }
             const int64_t k = t0 + ti - p0;
@@ -787,13 +871,11 @@ __global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, int64_t p0, const in
     {
         float h[kNC];
         regular_harmonics<kP>(tp.x * inv_sb, tp.y * inv_sb, tp.z * inv_sb, c_tab, h);
-        const float2* L = reinterpret_cast<const float2*>(ell + (size_t)b * kBoxStride);
+        const float* L = ell + (size_t)b * kEllStride;  // ell[r][k]
 #pragma unroll
         for (int k = 0; k < kNC; ++k) {
-            const float2 l0 = __ldg(L + 3 * k), l1 = __ldg(L + 3 * k + 1), l2 = __ldg(L + 3 * k + 2);
-            far[0] = fmaf(l0.x, h[k], far[0]); far[1] = fmaf(l0.y, h[k], far[1]);
-            far[2] = fmaf(l1.x, h[k], far[2]); far[3] = fmaf(l1.y, h[k], far[3]);
-            far[4] = fmaf(l2.x, h[k], far[4]); far[5] = fmaf(l2.y, h[k], far[5]);
+#pragma unroll
+            for (int r = 0; r < 6; ++r) far[r] = fmaf(__ldg(L + r * 128 + k), h[k], far[r]);
         }
 #pragma unroll
         for (int r = 0; r < 6; ++r) far[r] *= inv_sb;
@@ -867,8 +949,9 @@ float tf32_host(float x)
 }
 
 // M2L operator images for k_m2l_tc: per offset, the hi and lo TF32 parts of
-// T[i][k] (i, k < 121, zero padded to 128), row-major [part][i][k] (one TMEM
-// lane per row i).
+// T[i][k] (i, k < 121, zero padded to 128) in the tcgen05 canonical K-major
+// (no swizzle) layout of a 128 (N = i) x 128 (K = k) B operand: element (i, k)
+// at float ((i/8)*32 + k/4)*32 + (i%8)*4 + k%4 of its part; [offset][hi|lo][16384].
 void upload_tc_images(DBuf<float>& dst, const std::vector<double>& src)
 {
     const size_t img = 128 * 128;
@@ -878,8 +961,9 @@ void upload_tc_images(DBuf<float>& dst, const std::vector<double>& src)
             for (int k = 0; k < kNC; ++k) {
                 const float a = (float)src[(size_t)m * kNC * kNC + (size_t)i * kNC + k];
                 const float hi = tf32_host(a);
-                h[(size_t)m * 2 * img + (size_t)i * 128 + k] = hi;
-                h[(size_t)m * 2 * img + img + (size_t)i * 128 + k] = a - hi;
+                const size_t e = ((size_t)(i / 8) * 32 + k / 4) * 32 + (i % 8) * 4 + k % 4;
+                h[(size_t)m * 2 * img + e] = hi;
+                h[(size_t)m * 2 * img + img + e] = a - hi;
             }
     dst.alloc(h.size());
     XRL_CUDA(cudaMemcpy(dst.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
@@ -897,14 +981,10 @@ void upload_constants(xrl_ctx ctx)
     const HostOperators& ops = host_ops();
     upload_padded(ctx->ops.m2m, ops.m2m, 8);
     upload_padded(ctx->ops.l2l, ops.l2l, 8);
-    upload_padded(ctx->ops.m2l, ops.m2l, kNM2L);
     upload_tc_images(ctx->ops.m2l_tc, ops.m2l);
     XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
     XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    const char* e = getenv("XRL_M2L_SIMT");  // SIMT FP32 M2L (ablation); default tcgen05 3xTF32
-    ctx->m2l_simt = e && e[0] == '1';
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
-    XRL_CUDA(cudaFuncSetAttribute(k_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kM2LSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
 }
 
@@ -914,7 +994,11 @@ void upload_constants(xrl_ctx ctx)
 static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags)
 {
     xrl_ctx ctx = t->ctx;
-    cudaStream_t st = ctx->stream, side = ctx->side;
+    // XRL_M2L_DBG (profiling ablations, wrong results): 1 skip reductions, 2 skip A loads, 4 skip D reads
+    static const int m2l_dbg = [] { const char* e = getenv("XRL_M2L_DBG"); return e ? atoi(e) : 0; }();
+    // XRL_SERIAL=1 (profiling): everything on the main stream, so per-phase times are isolated
+    static const bool serial = [] { const char* e = getenv("XRL_SERIAL"); return e && e[0] == '1'; }();
+    cudaStream_t st = ctx->stream, side = serial ? ctx->stream : ctx->side;
     const int64_t n = t->n;
     const int64_t nl = t->p1 - t->p0, p0 = t->p0;
     const bool do_far = flags != XRL_MVM_NEAR_ONLY;
@@ -971,20 +1055,14 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
 
         phase_begin(ctx, PH_M2L, &ev, st);
         XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), st));
-        if (t->n_m2l_tiles > 0 && ctx->m2l_simt) {
-            k_m2l<<<t->n_m2l_tiles, 256, kM2LSmem, st>>>(t->m2l_tiles.p, t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l.p,
-                                                         t->mu.p, t->ell.p);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
-        } else if (t->n_m2l_tiles > 0) {
-            const int nblocks = (t->n_m2l_tiles + kTcR - 1) / kTcR;
-            const int grid = std::min(ctx->num_sms, nblocks);
+        if (t->n_m2l_tiles > 0) {
+            const int grid = std::min(ctx->num_sms, t->n_m2l_blocks);
             if (t->mu_img.n < (size_t)t->nbox * kImgFloats) t->mu_img.alloc((size_t)t->nbox * kImgFloats);
-            k_mu_img<<<nblk((int64_t)t->nbox * 1024, 256), 256, 0, st>>>(t->nbox, t->mu.p, t->mu_img.p);
+            k_mu_img<<<nblk((int64_t)t->nbox * kImgFloats, 256), 256, 0, st>>>(t->nbox, t->mu.p, t->mu_img.p);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
-            k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->m2l_tiles.p, t->n_m2l_tiles, t->m2l_tgt.p, t->m2l_srcb.p,
-                                                        ctx->ops.m2l_tc.p, t->mu_img.p, t->ell.p);
+            k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p, t->m2l_tgt.p,
+                                                        t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu_img.p, t->ell.p, m2l_dbg);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }

@@ -847,22 +847,33 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
             }
         }
         const int64_t nvk = (int64_t)ho.size();
-        std::vector<int4> tiles;
-        const int TP = 16;
+        // tiles: <= 21 pairs of one (chunk, offset) group (one 128-row tcgen05 MMA group each);
+        // blocks: runs of <= 16 tiles of one group (one operator load per block)
+        std::vector<int4> tiles, blocks;
+        const int TP = 21, BT = 16;
         int64_t i = 0;
         while (i < nvk) {
             int64_t j = i;
             while (j < nvk && ho[j] == ho[i]) ++j;  // same (chunk, offset)
-            for (int64_t s = i; s < j; s += TP)
+            for (int64_t s = i; s < j; s += TP) {
+                if ((int)tiles.size() == 0 || blocks.back().y == BT || blocks.back().z != (ho[i] & 511) ||
+                    blocks.back().w != (ho[i] >> 9) || s == i)
+                    blocks.push_back(make_int4((int)tiles.size(), 0, ho[i] & 511, ho[i] >> 9));
                 tiles.push_back(make_int4(ho[i] & 511, (int)s, (int)std::min<int64_t>(TP, j - s), ho[i] >> 9));
+                blocks.back().y += 1;
+            }
             i = j;
         }
         T->n_m2l_tiles = (int)tiles.size();
-        T->n_m2l_subtiles = 0;
-        for (const int4& tl : tiles) T->n_m2l_subtiles += (tl.z + 7) / 8;
+        T->n_m2l_subtiles = (int64_t)tiles.size();  // one tcgen05 MMA group (M = N = K = 128) per tile
         T->m2l_tiles.alloc(std::max<size_t>(1, tiles.size()));
         if (!tiles.empty())
             XRL_CUDA(cudaMemcpyAsync(T->m2l_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
+        T->n_m2l_blocks = (int)blocks.size();
+        T->m2l_blocks.alloc(std::max<size_t>(1, blocks.size()));
+        if (!blocks.empty())
+            XRL_CUDA(cudaMemcpyAsync(T->m2l_blocks.p, blocks.data(), sizeof(int4) * blocks.size(), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
     }
     // X targets (boxes with kept P2L pairs)
     {
@@ -878,7 +889,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     }
     // MVM scratch
     T->mu.alloc((size_t)nbox * kBoxStride);
-    T->ell.alloc((size_t)nbox * kBoxStride);
+    T->ell.alloc((size_t)nbox * kEllStride);
     T->xq.alloc((size_t)n * 8);
     XRL_CUDA(cudaMemsetAsync(T->mu.p, 0, T->mu.bytes(), st));
     XRL_CUDA(cudaMemsetAsync(T->xq.p, 0, T->xq.bytes(), st));

@@ -73,13 +73,13 @@ enum Phase { PH_PACK = 0, PH_P2M, PH_M2M, PH_M2L, PH_P2L, PH_L2L, PH_L2P, PH_P2P
 struct DeviceOperators {
     DBuf<float> m2m;   // [8][kNC (k, input)][kNCP (i, output, padded)]
     DBuf<float> l2l;   // [8][kNC][kNCP]
-    DBuf<float> m2l;   // [316][kNC][kNCP]
-    DBuf<float> m2l_tc;  // [316][2 (hi, lo)][128 x 128 tf32, tcgen05 core-matrix layout]
+    DBuf<float> m2l_tc;  // [316][2 (hi, lo)][128 x 128 tf32, tcgen05 canonical K-major layout]
     int m2l_index[343];
 };
 
 constexpr int kNCP = 128;            // padded coefficient count
-constexpr int kBoxStride = 728;      // floats per box expansion (121*6 padded to 16 B)
+constexpr int kBoxStride = 728;      // floats per box multipole mu[k][r] (121*6 padded to 16 B)
+constexpr int kEllStride = 768;      // floats per box local expansion ell[r][k] (r-major, k padded to 128)
 
 }  // namespace xrl
 
@@ -94,7 +94,6 @@ struct xrl_ctx_s {
     xrl::DeviceOperators ops;
     // timing
     bool timing = false;
-    bool m2l_simt = false;            // XRL_M2L_SIMT=1: SIMT FP32 M2L instead of tcgen05
     int num_sms = 148;
     int64_t launches = 0;
     int refs = 0;         // live trees
@@ -135,8 +134,10 @@ struct xrl_tree_s {
     int64_t nu = 0, nv = 0, nx = 0, nw = 0, np2p = 0;
     // M2L pairs sorted by (offset, target) and their tiles
     xrl::DBuf<int32_t> m2l_tgt, m2l_srcb;    // [nv]
-    xrl::DBuf<int4> m2l_tiles;               // (offset, pair begin, pair count, 0)
+    xrl::DBuf<int4> m2l_tiles;               // (offset, pair begin, pair count <= 21, chunk)
     int32_t n_m2l_tiles = 0;
+    xrl::DBuf<int4> m2l_blocks;              // (first tile, #tiles, offset, chunk): runs of one operator
+    int32_t n_m2l_blocks = 0;
     int64_t n_m2l_subtiles = 0;
     // boxes with non-empty X list, leaves with non-empty W list
     xrl::DBuf<int32_t> x_targets;
@@ -158,8 +159,9 @@ struct xrl_tree_s {
     std::vector<double> h_vert;              // [nv][3]
     std::vector<int32_t> h_tri;              // [n][3]
     // MVM scratch
-    xrl::DBuf<float> mu, ell;                // [nbox][kBoxStride]
-    xrl::DBuf<float> mu_img;                 // tcgen05 M2L: per-box TF32 hi/lo images (8 KB)
+    xrl::DBuf<float> mu;                     // [nbox][kBoxStride]  mu[k][r]
+    xrl::DBuf<float> ell;                    // [nbox][kEllStride] ell[r][k]
+    xrl::DBuf<float> mu_img;                 // tcgen05 M2L: per-box FP32 r-major images (3 KB)
     xrl::DBuf<float> xq;                     // [n][8] packed charges
     xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging
 };

@@ -1,0 +1,16 @@
+#!/bin/bash
+# One GPU pass: build, smoke, gpu tests, default bench, launch list of the bench command, ncu --set full of the hot kernels.
+# usage: tools/gpu_full.sh [tag]   (results under gpurun_out/<tag>/)
+T=${1:-run}
+O=gpurun_out/$T
+mkdir -p $O
+L=${LEAF:-512}
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build rc=$?" >> $O/status.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/status.txt
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/status.txt
+timeout 900 python bench.py > $O/bench.log 2>&1; echo "bench rc=$?" >> $O/status.txt
+if [ "${NCU:-1}" = "1" ]; then
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches.csv python bench.py --steps 3 --warmup 3 --leaf $L --no-cpu-baseline --gmres-iters 0 > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> $O/status.txt
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_m2l|k_p2p|k_near_spmv|k_l2p_m2p|k_p2m" -s 12 -c 6 -o $O/prof_full python tools/prof_mvm.py 4 3 $L > $O/ncu.log 2>&1; echo "ncu full rc=$?" >> $O/status.txt
+fi
+cat $O/status.txt

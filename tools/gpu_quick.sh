@@ -1,8 +1,16 @@
 #!/bin/bash
-# quick: parity tests + bench at given leaves (LEAVES env)
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/status.txt
-for L in ${LEAVES:-256 512}; do
-timeout 600 python bench.py --steps 5 --warmup 3 --leaf $L --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/bench_leaf$L.log 2>&1; echo "bench leaf$L rc=$?" >> gpurun_out/status.txt
-done
-cat gpurun_out/status.txt
+# Quick GPU iteration: build, smoke canary, parity tests, short bench (+ optional extra command in $EXTRA).
+# usage: tools/gpu_quick.sh <tag>
+T=${1:-quick}
+O=gpurun_out/$T
+mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build rc=$?" >> $O/status.txt
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; rc=$?; echo "smoke rc=$rc" >> $O/status.txt
+if [ $rc = 0 ]; then
+timeout 400 python -m pytest tests/test_gpu_parity.py -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/status.txt
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --gmres-iters 0 ${BENCH_ARGS} > $O/bench.log 2>&1; echo "bench rc=$?" >> $O/status.txt
+XRL_SERIAL=1 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --gmres-iters 0 ${BENCH_ARGS} > $O/bench_serial.log 2>&1; echo "bench serial rc=$?" >> $O/status.txt
+if [ -n "$EXTRA" ]; then bash -c "$EXTRA" > $O/extra.log 2>&1; echo "extra rc=$?" >> $O/status.txt; fi
+fi
+tail -n 3 $O/smoke.log $O/pytest_gpu.log
+cat $O/status.txt
