@@ -230,6 +230,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+// Bulk (TMA) reduction smem -> global, f32 add; bulk-group completion.
+__device__ __forceinline__ void bulk_red_add_f32(float* dst, const float* src, uint32_t bytes)
+{
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                 "r"(tc::smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // 32-byte (whole sector) read-only load, no L1 allocation
 __device__ __forceinline__ void ldg256(const float* p, float* v)
 {
@@ -296,7 +307,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
     float* stage = reinterpret_cast<float*>(opsm + 2 * kTcOpBytes);  // [128 rows][kTcStageLd]
     __shared__ uint64_t a_full[2], a_free[2], d_full[2], d_free[2], op_full;
     __shared__ uint32_t tbase;
-    __shared__ int rowdst[128];  // drain: target box of each accumulator row (-1: none)
     __shared__ int4 mma_blk;     // MMA warp: current block descriptor (uniform)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -401,6 +411,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             tc::fence_after();
             const uint32_t ta = tm + ((uint32_t)(32 * qd) << 16) + kTcColD + 128 * d;
             float* srow = stage + L * kTcStageLd;
+            bulk_wait_read0();  // this thread's previous bulk reduction has finished reading its stage row
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 float v[32];
@@ -416,21 +427,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             tc::fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&d_free[d]);  // accumulator d may be overwritten
-            rowdst[L] = cur_t;
-            named_bar_sync(1, 128);
-            for (int R = qd; R < 6 * kTcPairs; R += 4) {
-                const int t = rowdst[R];
-                if (t < 0 || (dbg & 1)) continue;
-                if (lane < 31) {
-                    const float4 v = *reinterpret_cast<const float4*>(stage + R * kTcStageLd + 4 * lane);
-                    red_add_v4(ell + (size_t)t * kEllStride + (R % 6) * 128 + 4 * lane, v.x, v.y, v.z, v.w);
-                }
+            if (cur_t >= 0 && !(dbg & 1)) {
+                // row (p, r) -> ell[t][r][0..123] with one bulk reduction (TMA, whole lines in L2)
+                tc::fence_proxy_async();
+                bulk_red_add_f32(ell + (size_t)cur_t * kEllStride + r * 128, srow, 124 * 4);
+                bulk_commit();
             }
-            named_bar_sync(1, 128);  // stage is reused by the next tile
             sq = nx;
             cur = nxt;
             cur_t = nxt_t;
         }
+        bulk_wait0();
     } else {
         // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform control
         // (block descriptors through shared memory, barrier waits voted with __all_sync) so the

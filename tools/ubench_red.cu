@@ -49,6 +49,36 @@ __global__ void k_contig_f32(float* buf, int iters)
         }
     }
 }
+__device__ __forceinline__ void red2(float* p, float a, float b)
+{
+    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+// (5) tcgen05.ld 16x256b-like layout: 4 lanes cover 32 B of one row, a warp 8 rows x 32 B per instruction (v2)
+__global__ void k_rows8_v2(float* buf, int iters)
+{
+    const int lane = threadIdx.x & 31, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int it = 0; it < iters; ++it) {
+        for (int g = 0; g < 4; ++g) {  // 4 groups of 8 rows = 32 rows per warp (as (1))
+            const int row = ((w * 32 + 8 * g + lane / 4) * 7 + it * 131) % kRows;
+            float* o = buf + (size_t)row * kRowF + 2 * (lane & 3);
+#pragma unroll 4
+            for (int q = 0; q < 16; ++q) red2(o + 8 * q, 1.f, 1.f);  // 128 floats per row (124 in (1))
+        }
+    }
+}
+// (6) 2 lanes cover 32 B of one row with v4: a warp 16 rows x 32 B per instruction
+__global__ void k_rows16_v4(float* buf, int iters)
+{
+    const int lane = threadIdx.x & 31, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int it = 0; it < iters; ++it) {
+        for (int g = 0; g < 2; ++g) {
+            const int row = ((w * 32 + 16 * g + lane / 2) * 7 + it * 131) % kRows;
+            float* o = buf + (size_t)row * kRowF + 4 * (lane & 1);
+#pragma unroll 4
+            for (int q = 0; q < 16; ++q) red4(o + 8 * q, 1.f, 1.f, 1.f, 1.f);
+        }
+    }
+}
 // (4) plain v4 stores, contiguous (reference)
 __global__ void k_store(float* buf, int iters)
 {
@@ -90,6 +120,8 @@ int main()
     run("rowlane_v4", [&] { k_rowlane<<<grid, block>>>(buf, iters); }, payload);
     run("contig_v4", [&] { k_contig_v4<<<grid, block>>>(buf, iters); }, warps * iters * 31 * 31 * 16.0);
     run("contig_f32", [&] { k_contig_f32<<<grid, block>>>(buf, iters); }, warps * iters * 124 * 128.0);
+    run("rows8_v2", [&] { k_rows8_v2<<<grid, block>>>(buf, iters); }, warps * iters * 32 * 128 * 4.0);
+    run("rows16_v4", [&] { k_rows16_v4<<<grid, block>>>(buf, iters); }, warps * iters * 32 * 128 * 4.0);
     run("store_v4", [&] { k_store<<<grid, block>>>(buf, iters); }, warps * iters * 31 * 31 * 16.0);
     printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
