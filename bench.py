@@ -261,6 +261,23 @@ def run_xrl(args):
     launches = ctx.launch_count() - launches0
     ctx.timing_enable(False)
     phases = ctx.timing()
+
+    # isolated kernel times: the same MVM with every kernel serialised on one stream (not the
+    # headline; explains it).  Kernels run alone, so per-kernel rooflines are not diluted by sharing.
+    ctx.set_sched(ctx.SCHED_SERIAL)
+    for _ in range(2):
+        xrl.mvm(tree, near, xd, y)
+    barrier()
+    ctx.timing_reset()
+    ctx.timing_enable(True)
+    iso_steps = max(3, min(args.steps, 10))
+    for s in range(iso_steps):
+        flush.zero_()
+        xrl.mvm(tree, near, xd, y)
+    barrier()
+    ctx.timing_enable(False)
+    phases_iso = ctx.timing()
+    ctx.set_sched(ctx.SCHED_FORK)
     ms = sum(a.elapsed_time(b) for a, b in ev)
     t_dev = torch.tensor([ms], device=dev, dtype=torch.float64)
     if world > 1:
@@ -294,7 +311,6 @@ def run_xrl(args):
     # roofline of the dominant kernel (+ the other hot kernels for reference)
     peaks = _peaks()
     clocks = clk.summary()
-    tot_phase = sum(v[0] for v in phases.values())
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s, SIMT FFMA (derivation: DESIGN.md)
@@ -303,48 +319,51 @@ def run_xrl(args):
     nnz = near.nnz()
     tkey = f"{CFG_NAMES[args.config]}_leaf{args.leaf}"
 
-    def per_launch_ms(ph):
-        ms_, cnt = phases[ph]
+    def per_launch_ms(ph, src=None):
+        ms_, cnt = (src or phases)[ph]
         return ms_ / max(cnt, 1)
 
+    def rate(ph, work, src=None):  # work units per launch / launch duration
+        return work / (per_launch_ms(ph, src) * 1e-3)
+
     roofs = {}
-    simt_m2l = os.environ.get("XRL_M2L_SIMT") == "1"
-    if phases["m2l"][1] and simt_m2l:
-        a = 2.0 * nc * nc * 6 * info["n_v_pairs"] / (per_launch_ms("m2l") * 1e-3) / 1e12
-        roofs["m2l"] = {"kernel": "k_m2l", "bound": "alu", "achieved": a, "peak": fp32_peak, "unit": "TFLOP/s",
-                        "frac": a / fp32_peak, "traffic": traffic_from_profiles("k_m2l", tkey),
-                        "algorithmic": f"2*121^2*6 = 175692 flops x {info['n_v_pairs']} V-list translations per launch",
-                        "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 flops x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
-    elif phases["m2l"][1]:
-        # tcgen05 3xTF32: per 16-pair tile 48 MMAs of M128 N96 K8 (2*128*96*8 flops each)
+    if phases["m2l"][1]:
+        # tcgen05 3xTF32: per 21-pair tile 48 MMAs of M128 N128 K8 (2*128*128*8 flops each)
         n_sub = _tc_subtiles(tree)
-        issued = n_sub * 48 * 2.0 * 128 * 96 * 8
+        issued = n_sub * 48 * 2.0 * 128 * 128 * 8
         tf32_peak = float(peaks.get("bf16_tflops", 1656.1)) * 0.5  # nominal tf32/bf16 dense ratio 1.1/2.25
-        a = issued / (per_launch_ms("m2l") * 1e-3) / 1e12
-        alg = 2.0 * nc * nc * 6 * info["n_v_pairs"] / (per_launch_ms("m2l") * 1e-3) / 1e12
+        a, ai = rate("m2l", issued) / 1e12, rate("m2l", issued, phases_iso) / 1e12
+        alg = rate("m2l", 2.0 * nc * nc * 6 * info["n_v_pairs"], phases_iso) / 1e12
         roofs["m2l"] = {"kernel": "k_m2l_tc", "bound": "tensor", "achieved": a, "peak": tf32_peak, "unit": "TFLOP/s",
                         "frac": a / tf32_peak, "traffic": traffic_from_profiles("k_m2l_tc", tkey),
-                        "algorithmic": f"issued tcgen05 kind::tf32 MMA flops: {n_sub} tiles x 48 x 2*128*96*8 per launch "
-                                       f"(3xTF32 split; FP32-equivalent algorithmic rate {alg:.1f} TFLOP/s = "
+                        "isolated": {"achieved": ai, "frac": ai / tf32_peak, "ms": per_launch_ms("m2l", phases_iso)},
+                        "algorithmic": f"issued tcgen05 kind::tf32 MMA flops: {n_sub} tiles x 48 x 2*128*128*8 per launch "
+                                       f"(3xTF32 split; isolated FP32-equivalent algorithmic rate {alg:.1f} TFLOP/s = "
                                        f"{alg / fp32_peak:.2f} of the FP32 SIMT peak)",
                         "peak_source": "tf32 dense = bf16_tflops (MEASURED_PEAKS.json) x 0.5 (nominal 1.1/2.25 PF)"}
     if phases["p2p"][1]:
-        a = 20.0 * info["n_p2p"] / (per_launch_ms("p2p") * 1e-3) / 1e12
+        w = 20.0 * info["n_p2p"]
+        a, ai = rate("p2p", w) / 1e12, rate("p2p", w, phases_iso) / 1e12
         roofs["p2p"] = {"kernel": "k_p2p", "bound": "alu", "achieved": a, "peak": fp32_peak, "unit": "TFLOP/s",
                         "frac": a / fp32_peak, "traffic": traffic_from_profiles("k_p2p", tkey),
+                        "isolated": {"achieved": ai, "frac": ai / fp32_peak, "ms": per_launch_ms("p2p", phases_iso)},
                         "algorithmic": f"20 flops x {info['n_p2p']} ordered panel pairs per launch",
-                        "peak_source": "as k_m2l"}
+                        "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 flops x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
     if phases["near"][1]:
         byts = 8.0 * nnz + 56.0 * n
-        a = byts / (per_launch_ms("near") * 1e-3) / 1e9
+        a, ai = rate("near", byts) / 1e9, rate("near", byts, phases_iso) / 1e9
         roofs["near"] = {"kernel": "k_near_spmv", "bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
                          "frac": a / hbm_peak, "traffic": traffic_from_profiles("k_near_spmv", tkey),
+                         "isolated": {"achieved": ai, "frac": ai / hbm_peak, "ms": per_launch_ms("near", phases_iso)},
                          "algorithmic": f"8 B x {nnz} nnz + 56 B x {n} rows (row_ptr, x, y) per launch",
                          "peak_source": "hbm_gbs, MEASURED_PEAKS.json"}
-    dom = max(roofs, key=lambda k: phases[k][0]) if roofs else max(phases, key=lambda k: phases[k][0])
+    # dominant kernel: largest isolated time (the work that bounds the step)
+    dom = max(roofs, key=lambda k: phases_iso[k][0]) if roofs else max(phases, key=lambda k: phases[k][0])
     roof = dict(roofs.get(dom) or {"kernel": "k_" + dom})
-    roof["share_of_step"] = phases[dom][0] / tot_phase if tot_phase else None
-    roof["others"] = {k: {kk: v[kk] for kk in ("achieved", "peak", "unit", "frac")} for k, v in roofs.items() if k != dom}
+    roof["share_of_step"] = phases[dom][0] / args.steps / ms_per_step if ms_per_step else None
+    roof["share_of_isolated_sum"] = phases_iso[dom][0] / sum(v[0] for v in phases_iso.values())
+    roof["others"] = {k: {kk: v[kk] for kk in ("achieved", "peak", "unit", "frac", "isolated")}
+                      for k, v in roofs.items() if k != dom}
 
     line = {
         "metric": METRIC, "value": value, "unit": "Mpanels/s", "n_gpus": world, "steps": args.steps,
@@ -365,6 +384,8 @@ def run_xrl(args):
         "clocks": clocks,
         "roofline": roof,
         "phases_ms_per_step": {k: v[0] / args.steps for k, v in phases.items()},
+        "phases_isolated_ms": {k: v[0] / iso_steps for k, v in phases_iso.items()},
+        "sched": "FMM chain on a high-priority stream; P2P then near SpMV on a low-priority side stream",
     }
     if world == 1 and args.gmres_iters > 0:
         line["gmres"] = gmres_iteration_time(xrl, tree, near, args)
@@ -381,7 +402,7 @@ def run_xrl(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["xrl", "reference"], default="xrl")
     ap.add_argument("--config", type=int, default=4)

@@ -197,9 +197,25 @@ xrl_status xrl_mvm_gathered(xrl_tree tree, xrl_near near, const void* x_full, vo
 xrl_status xrl_mvm_host(xrl_tree tree, xrl_near near, const void* x_host, void* y_host, int32_t nvec,
                         uint32_t flags);
 
-/* Per-phase device timing (CUDA events on the context stream) of the MVM
- * kernels, accumulated while enabled.  names: "pack","p2m","m2m","m2l","p2l",
- * "l2l","leaf"(L2P+M2P+P2P+near).  xrl_timing_get fills ms[i] and
+/* Kernel scheduling of xrl_mvm on this context (no effect on results beyond
+ * FP32 summation order of atomics):
+ *   XRL_SCHED_SERIAL (0)  every kernel on the context stream, in order (per-phase
+ *                         times are then isolated kernel times; profiling);
+ *   XRL_SCHED_FORK (1)    default: the FMM chain (P2M..L2L, L2P) on a library-owned
+ *                         high-priority stream, P2P then the near SpMV on a
+ *                         low-priority side stream forked after the charge pack,
+ *                         joined back into the context stream;
+ *   XRL_SCHED_LATE (2)    as 1, side stream forked when the M2L is launched.
+ * The XRL_SCHED environment variable, if set, overrides the default at context
+ * creation.  Errors: XRL_EINVAL for a null context or unknown mode. */
+#define XRL_SCHED_SERIAL 0
+#define XRL_SCHED_FORK 1
+#define XRL_SCHED_LATE 2
+xrl_status xrl_ctx_set_sched(xrl_ctx ctx, int32_t mode);
+
+/* Per-phase device timing (CUDA events on the stream each phase runs on) of
+ * the MVM kernels, accumulated while enabled.  names: "pack","p2m","m2m","m2l",
+ * "p2l","l2l","l2p_m2p","p2p","near".  xrl_timing_get fills ms[i] and
  * launches[i] for i < n (n = xrl_timing_count()). */
 xrl_status xrl_timing_enable(xrl_ctx ctx, int on);
 int32_t xrl_timing_count(void);

@@ -113,9 +113,18 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         c->rank = rank;
         c->world = world;
         c->stream = (cudaStream_t)cuda_stream;  // NULL = legacy default stream
-        XRL_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        // library-owned streams: `work` (highest priority) runs the FMM chain, `side` (lowest
+        // priority) the P2P / near SpMV, so their CTAs fill SMs the chain leaves free
+        int prio_lo = 0, prio_hi = 0;
+        XRL_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        XRL_CUDA(cudaStreamCreateWithPriority(&c->work, cudaStreamNonBlocking, prio_hi));
+        XRL_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_work, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        if (const char* e = getenv("XRL_SCHED")) c->sched = atoi(e);
+        if (const char* e = getenv("XRL_SERIAL"); e && e[0] == '1') c->sched = XRL_SCHED_SERIAL;
+        if (c->sched < XRL_SCHED_SERIAL || c->sched > XRL_SCHED_LATE) c->sched = XRL_SCHED_FORK;
         upload_constants(c);
         if (world > 1) {
             xrl_status st = comm_init(c, nccl_unique_id);
@@ -154,6 +163,8 @@ void xrl::ctx_release(xrl_ctx ctx)
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     comm_destroy(ctx);
     if (ctx->side) { cudaStreamSynchronize(ctx->side); cudaStreamDestroy(ctx->side); }
+    if (ctx->work) { cudaStreamSynchronize(ctx->work); cudaStreamDestroy(ctx->work); }
+    if (ctx->ev_work) cudaEventDestroy(ctx->ev_work);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -186,6 +197,16 @@ xrl_status xrl_timing_get(xrl_ctx ctx, double* ms, int64_t* launches)
 }
 
 int64_t xrl_launch_count(xrl_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+xrl_status xrl_ctx_set_sched(xrl_ctx ctx, int32_t mode)
+{
+    if (!ctx || mode < XRL_SCHED_SERIAL || mode > XRL_SCHED_LATE) {
+        set_error("xrl_ctx_set_sched: null context or bad mode %d", mode);
+        return XRL_EINVAL;
+    }
+    ctx->sched = mode;
+    return XRL_OK;
+}
 
 xrl_status xrl_timing_reset(xrl_ctx ctx)
 {

@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
 // level parallelism), shuffle reduction over the 8 lanes.
 __global__ void __launch_bounds__(256) k_near_spmv(int64_t n, int64_t r0, const int64_t* __restrict__ ptr,
                                                    const int32_t* __restrict__ col, const float* __restrict__ val,
-                                                   const float* __restrict__ xq, float2* __restrict__ y)
+                                                   const float* __restrict__ xq, int accumulate, float2* __restrict__ y)
 {
     // rows r0 .. r0+n-1 (owned range); y local [3][n]
     const int64_t lrow = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
@@ -616,7 +616,15 @@ __global__ void __launch_bounds__(256) k_near_spmv(int64_t n, int64_t r0, const 
         a[r] += __shfl_xor_sync(0xffffffffu, a[r], 2);
         a[r] += __shfl_xor_sync(0xffffffffu, a[r], 4);
     }
-    if (lrow < n && lane < 3) y[lane * n + lrow] = make_float2(a[2 * lane], a[2 * lane + 1]);
+    if (lrow < n && lane < 3) {
+        float2 o = make_float2(a[2 * lane], a[2 * lane + 1]);
+        if (accumulate) {
+            const float2 v = y[lane * n + lrow];
+            o.x += v.x;
+            o.y += v.y;
+        }
+        y[lane * n + lrow] = o;
+    }
 }
 
 // ------------------------------------------------------------------ P2P
@@ -1003,9 +1011,16 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
     xrl_ctx ctx = t->ctx;
     // XRL_M2L_DBG (profiling ablations, wrong results): 1 skip reductions, 2 skip A loads, 4 skip D reads
     static const int m2l_dbg = [] { const char* e = getenv("XRL_M2L_DBG"); return e ? atoi(e) : 0; }();
-    // XRL_SERIAL=1 (profiling): everything on the main stream, so per-phase times are isolated
-    static const bool serial = [] { const char* e = getenv("XRL_SERIAL"); return e && e[0] == '1'; }();
-    cudaStream_t st = ctx->stream, side = serial ? ctx->stream : ctx->side;
+    // Scheduling (xrl_ctx_set_sched): 0 = one stream (phases isolated, profiling); 1 (default) = P2P
+    // then the near SpMV on the low-priority side stream forked after the pack (the FP32-bound P2P
+    // shares SMs with the tensor-core M2L); 2 = forked when the M2L is launched.  The FMM chain runs
+    // on the library's high-priority work stream, joined back into ctx->stream.
+    const int sched = ctx->sched;
+    cudaStream_t st = sched ? ctx->work : ctx->stream, side = sched ? ctx->side : ctx->stream;
+    if (sched) {
+        XRL_CUDA(cudaEventRecord(ctx->ev_work, ctx->stream));
+        XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_work, 0));
+    }
     const int64_t n = t->n;
     const int64_t nl = t->p1 - t->p0, p0 = t->p0;
     const bool do_far = flags != XRL_MVM_NEAR_ONLY;
@@ -1019,28 +1034,34 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
     ctx->launches += 1;
     phase_end(ctx, PH_PACK, ev, st);
 
-    // fork: near SpMV and P2P depend only on the packed charges -> side stream,
-    // overlapping the upward pass and the M2L on the main stream.
-    XRL_CUDA(cudaEventRecord(ctx->ev_fork, st));
-    XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
-    if (do_near) {
-        phase_begin(ctx, PH_NEAR, &ev, side);
-        if (nl > 0) k_near_spmv<<<nblk(8 * nl, 256), 256, 0, side>>>(nl, p0, nr->row_ptr.p, nr->col.p, nr->val.p, t->xq.p, y);
-        XRL_LAUNCH_CHECK();
-        ctx->launches += 1;
-        phase_end(ctx, PH_NEAR, ev, side);
-    }
-    if (do_far) {
-        phase_begin(ctx, PH_P2P, &ev, side);
-        if (t->n_own_leaves > 0)
-            k_p2p<<<t->n_own_leaves, 128, 0, side>>>(t->own_leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
-                                                     t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
-                                                     invW, do_near ? 1 : 0, nl, p0, y);
-        XRL_LAUNCH_CHECK();
-        ctx->launches += 1;
-        phase_end(ctx, PH_P2P, ev, side);
-    }
-    XRL_CUDA(cudaEventRecord(ctx->ev_join, side));
+    // near SpMV and P2P depend only on the packed charges
+    auto launch_side = [&]() {
+        XRL_CUDA(cudaEventRecord(ctx->ev_fork, st));
+        XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+        // P2P (FP32-bound) first: it shares SMs well with the tensor-core M2L; the near SpMV
+        // (memory-bound) after it accumulates into y
+        if (do_far) {
+            phase_begin(ctx, PH_P2P, &ev, side);
+            if (t->n_own_leaves > 0)
+                k_p2p<<<t->n_own_leaves, 128, 0, side>>>(t->own_leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
+                                                         t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
+                                                         invW, 0, nl, p0, y);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+            phase_end(ctx, PH_P2P, ev, side);
+        }
+        if (do_near) {
+            phase_begin(ctx, PH_NEAR, &ev, side);
+            if (nl > 0) k_near_spmv<<<nblk(8 * nl, 256), 256, 0, side>>>(nl, p0, nr->row_ptr.p, nr->col.p, nr->val.p, t->xq.p,
+                                                                         do_far ? 1 : 0, y);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+            phase_end(ctx, PH_NEAR, ev, side);
+        }
+        XRL_CUDA(cudaEventRecord(ctx->ev_join, side));
+    };
+    const bool chain = do_far && t->nlevel > 1;
+    if (sched != 2 || !chain) launch_side();
 
     if (do_far && t->nlevel > 1) {
         phase_begin(ctx, PH_P2M, &ev, st);
@@ -1060,8 +1081,9 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         }
         phase_end(ctx, PH_M2M, ev, st);
 
-        phase_begin(ctx, PH_M2L, &ev, st);
         XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), st));
+        if (sched == 2) launch_side();
+        phase_begin(ctx, PH_M2L, &ev, st);
         if (t->n_m2l_tiles > 0) {
             const int grid = std::min(ctx->num_sms, t->n_m2l_blocks);
             if (t->mu_img.n < (size_t)t->nbox * kImgFloats) t->mu_img.alloc((size_t)t->nbox * kImgFloats);
@@ -1097,7 +1119,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         phase_end(ctx, PH_L2L, ev, st);
     }
     // join, then the local-expansion / W-list evaluation completes y
-    XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    if (sched) XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     if (do_far && t->nlevel > 1 && nl > 0) {
         phase_begin(ctx, PH_L2P, &ev, st);
         k_l2p_m2p<<<nblk(nl, 128), 128, 0, st>>>(nl, p0, t->panel_leaf.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
@@ -1105,6 +1127,10 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
         phase_end(ctx, PH_L2P, ev, st);
+    }
+    if (sched) {  // join the work stream back into the caller's stream
+        XRL_CUDA(cudaEventRecord(ctx->ev_work, st));
+        XRL_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_work, 0));
     }
 }
 

@@ -86,14 +86,16 @@ constexpr int kEllStride = 768;      // floats per box local expansion ell[r][k]
 struct xrl_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;      // library-owned side stream (near SpMV, P2P)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t work = nullptr;      // library-owned high-priority stream (FMM chain of xrl_mvm)
+    cudaStream_t side = nullptr;      // library-owned low-priority side stream (near SpMV, P2P)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_work = nullptr;
     bool own_stream = false;
     int rank = 0, world = 1;
     void* nccl_comm = nullptr;        // ncclComm_t when world > 1
     xrl::DeviceOperators ops;
     // timing
     bool timing = false;
+    int sched = XRL_SCHED_FORK;       // xrl_ctx_set_sched
     int num_sms = 148;
     int64_t launches = 0;
     int refs = 0;         // live trees

@@ -25,7 +25,7 @@ EXPORTS = [
     "xrl_tree_build", "xrl_tree_destroy", "xrl_tree_info", "xrl_tree_perm", "xrl_to_library_order",
     "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble", "xrl_near_destroy",
     "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_timing_enable", "xrl_timing_count",
-    "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count",
+    "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
     "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
@@ -122,6 +122,8 @@ def lib():
         L.xrl_timing_reset.argtypes = [P]
         L.xrl_launch_count.argtypes = [P]
         L.xrl_launch_count.restype = i64
+        L.xrl_ctx_set_sched.argtypes = [P, i32]
+        L.xrl_ctx_set_sched.restype = ctypes.c_int32
         L.xrl_topology_build.argtypes = [P, i32, P, pp]
         L.xrl_topology_info.argtypes = [P, ctypes.POINTER(TopoInfo)]
         L.xrl_topology_export.argtypes = [P] * 12
@@ -219,6 +221,12 @@ class Context:
 
     def sync(self):
         check(lib().xrl_ctx_sync(self.h))
+
+    SCHED_SERIAL, SCHED_FORK, SCHED_LATE = 0, 1, 2
+
+    def set_sched(self, mode: int):
+        """xrl_ctx_set_sched: 0 serial (isolated phase times), 1 fork (default), 2 late fork."""
+        check(lib().xrl_ctx_set_sched(self.h, int(mode)))
 
     def timing_enable(self, on=True):
         check(lib().xrl_timing_enable(self.h, int(on)))

@@ -11,4 +11,6 @@ for f in sys.argv[1:]:
     ph = {k: round(v, 3) for k, v in d.get("phases_ms_per_step", {}).items()}
     r = d.get("roofline", {})
     print(f"{f}: {d['value']:.1f} Mpanels/s {d['ms_per_step']:.3f} ms  e2e {d.get('e2e', {}).get('value', 0):.1f}  "
-          f"roof {r.get('kernel')} {r.get('frac', 0):.3f}\n   {ph}")
+          f"roof {r.get('kernel')} {r.get('frac', 0):.3f} (isolated {r.get('isolated', {}).get('frac', 0):.3f})\n   {ph}")
+    if "phases_isolated_ms" in d:
+        print("   isolated", {k: round(v, 3) for k, v in d["phases_isolated_ms"].items()})
