@@ -34,10 +34,6 @@ __constant__ RecTables<float> c_tab;
 namespace {
 
 
-__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d)
-{
-    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
-}
 
 __device__ __forceinline__ float3 box_center(int level, int ix, int iy, int iz)
 {
@@ -307,7 +303,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
     float* stage = reinterpret_cast<float*>(opsm + 2 * kTcOpBytes);  // [128 rows][kTcStageLd]
     __shared__ uint64_t a_full[2], a_free[2], d_full[2], d_free[2], op_full;
     __shared__ uint32_t tbase;
-    __shared__ int4 mma_blk;     // MMA warp: current block descriptor (uniform)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int h = 0; h < 2; ++h) {
@@ -865,6 +860,248 @@ __global__ void __launch_bounds__(128) k_p2p(
     }
 }
 
+// ------------------------------------------------------------------ P2P on tcgen05
+// Tensor-core P2P: for a tile of <= 128 targets t of one leaf and the flattened
+// U-list sources s, y[t][r] = sum_s G[t][s] q[s][r] with G = 1/|c_t - c_s|
+// (0 for s = t) is a (128 x S) x (S x 6) product.  CUDA cores build G (packed
+// f32x2 differences, MUFU rsqrt) and split it into TF32 hi (truncation) and lo
+// (exact remainder); tcgen05.st writes them into TMEM as the A operand (lane =
+// target); the charges of a 64-source chunk are staged in shared memory as the
+// B operand [q_hi (6) | 0 0 | q_lo (6) | 0 0] (N = 16, canonical K-major), so
+//     D[t][0..7]  += G_hi q_hi + G_lo q_hi,   D[t][8..15] += G_hi q_lo + G_lo q_lo
+// with 2 tcgen05.mma kind::tf32 M128 N16 K8 per 8 sources (3xTF32 accuracy).
+// The accumulation (6 FFMA per pair on CUDA cores) moves to the tensor core;
+// the CUDA cores do 3.5 FP32-pipe ops + 1 MUFU per pair (MUFU-bound).
+// Warp roles: 8 G warps (lane quarter w % 4, source half w / 4 of each chunk),
+// 4 producer warps (flatten the U list, stage positions and the charge image of
+// chunks into a ring of 3 slots, ahead of use), 1 MMA warp.  TMEM: G hi/lo
+// 128 columns per slot, D at column 384.  mbarriers per slot: staged (producers
+// -> G warps), g_full (G warps -> MMA), g_free (MMA commit -> producers, G warps).
+constexpr int kPtChunk = 64;                    // sources per chunk
+constexpr int kPtSlots = 3;
+constexpr int kPtThreads = 416;                 // 8 G + 4 producer + 1 MMA warps
+constexpr uint32_t kPtColD = 384;
+struct __align__(128) PtSlot {
+    float X[kPtChunk], Y[kPtChunk], Z[kPtChunk];  // source positions (target-leaf frame, W units)
+    float B[16 * kPtChunk];                        // charges, canonical K-major N16 x K64 (4 KB)
+    int flags;                                     // bit 0: last chunk, bit 1: chunk holds self pairs
+};
+
+__global__ void __launch_bounds__(kPtThreads, 1) k_p2p_tc(
+    const int4* __restrict__ ptiles, const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
+    const int32_t* __restrict__ iy, const int32_t* __restrict__ iz, const int32_t* __restrict__ pb,
+    const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
+    const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate, int64_t n, int64_t p0,
+    float2* __restrict__ y)
+{
+    __shared__ PtSlot slot[kPtSlots];
+    __shared__ uint64_t staged[kPtSlots], g_full[kPtSlots], g_free[kPtSlots], d_full;
+    __shared__ uint32_t tbase;
+    __shared__ int Uoff[kUWin + 1], Upb[kUWin], Uid[kUWin], wsum[2];
+    __shared__ float3 Ud[kUWin];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int4 tile = ptiles[blockIdx.x];
+    const int b = tile.x, t0 = tile.y, T = tile.z;
+    if (tid == 0) {
+        for (int k = 0; k < kPtSlots; ++k) {
+            tc::mbar_init(&staged[k], 2);
+            tc::mbar_init(&g_full[k], 8);
+            tc::mbar_init(&g_free[k], 1);
+        }
+        tc::mbar_init(&d_full, 1);
+    }
+    if (warp == 12) tc::tmem_alloc<512>(&tbase);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+
+    if (warp < 8) {
+        // ---------------- G warps: thread = target (TMEM lane), half of each chunk's sources
+        const uint32_t tm = tbase;
+        const int qd = warp & 3, hf = warp >> 2;
+        const int ti = 32 * qd + lane;
+        float tx = 1e18f, ty = 1e18f, tz = 1e18f;  // padding target: far away, discarded
+        if (ti < T) {
+            const float4 q = loc[t0 + ti];
+            tx = q.x; ty = q.y; tz = q.z;
+        }
+        const f2x txx = pk2(tx, tx), tyy = pk2(ty, ty), tzz = pk2(tz, tz);
+        const uint32_t ta = tm + ((uint32_t)(32 * qd) << 16);
+        for (int c = 0;; ++c) {
+            const int k = c % kPtSlots;
+            PtSlot& S = slot[k];
+            tc::mbar_wait(&staged[k], (c / kPtSlots) & 1);  // positions, flags, charge image of chunk c
+            // the MMAs of chunk c - kPtSlots are done with this slot's G columns
+            tc::mbar_wait(&g_free[k], ((c / kPtSlots) & 1) ^ 1);
+            tc::fence_after();
+            const int flags = S.flags;
+            const bool self = (flags & 2) != 0;
+            const uint32_t col = (uint32_t)(k * 128 + 32 * hf);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {  // 8 sources per tcgen05.st
+                float gh[8], gl[8];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int sidx = 32 * hf + 8 * g + 2 * e;
+                    const f2x dx = sub2(ld_shared_u64(&S.X[sidx]), txx);
+                    const f2x dy = sub2(ld_shared_u64(&S.Y[sidx]), tyy);
+                    const f2x dz = sub2(ld_shared_u64(&S.Z[sidx]), tzz);
+                    const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
+                    float ra = rsqrt_ftz(r2.x), rb = rsqrt_ftz(r2.y);
+                    if (self) {
+                        ra = r2.x > 0.f ? ra : 0.f;
+                        rb = r2.y > 0.f ? rb : 0.f;
+                    }
+                    const float ha = __uint_as_float(__float_as_uint(ra) & 0xFFFFE000u);
+                    const float hb = __uint_as_float(__float_as_uint(rb) & 0xFFFFE000u);
+                    gh[2 * e] = ha; gh[2 * e + 1] = hb;
+                    const float2 l = upk2(sub2(pk2(ra, rb), pk2(ha, hb)));
+                    gl[2 * e] = l.x; gl[2 * e + 1] = l.y;
+                }
+                tc::tmem_st8(ta + col + 8 * g, gh);
+                tc::tmem_st8(ta + col + 64 + 8 * g, gl);
+            }
+            tc::tmem_st_wait();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&g_full[k]);
+            if (flags & 1) break;
+        }
+        // accumulator complete: write y (warps with hf == 0)
+        tc::mbar_wait(&d_full, 0);
+        tc::fence_after();
+        float v[16];
+        tc::tmem_ld16(ta + kPtColD, v);
+        if (hf == 0 && ti < T) {
+            const int64_t kk = t0 + ti - p0;
+            float tot[6];
+#pragma unroll
+            for (int r = 0; r < 6; ++r) tot[r] = (v[r] + v[8 + r]) * invW;
+            if (accumulate) {
+                const float2 a = y[kk], cc = y[n + kk], d = y[2 * n + kk];
+                tot[0] += a.x; tot[1] += a.y; tot[2] += cc.x; tot[3] += cc.y; tot[4] += d.x; tot[5] += d.y;
+            }
+            y[kk] = make_float2(tot[0], tot[1]);
+            y[n + kk] = make_float2(tot[2], tot[3]);
+            y[2 * n + kk] = make_float2(tot[4], tot[5]);
+        }
+    } else if (warp < 12) {
+        // ---------------- producers (128 threads): U-list windows; group pg = 0/1 stages the even/odd
+        // chunks, one source per thread, with the next chunk's loads issued before the current one is
+        // stored (up to 4 chunks in flight)
+        const int pt = tid - 256, pw = warp - 8, pg = pt >> 6, ps = pt & 63;
+        const float3 cb = box_center(level[b], ix[b], iy[b], iz[b]);
+        const int64_t u0 = uptr[b], u1 = uptr[b + 1];
+        int cbase = 0;  // chunk index of the window's first chunk
+        for (int64_t w0 = u0; w0 < u1; w0 += kUWin) {
+            const int nu = (int)min((int64_t)kUWin, u1 - w0);
+            named_bar_sync(2, 128);  // previous window's tables no longer read
+            int sz = 0;
+            if (pt < kUWin) {
+                if (pt < nu) {
+                    const int sb = usrc[w0 + pt];
+                    Uid[pt] = sb;
+                    Upb[pt] = pb[sb];
+                    sz = pe[sb] - pb[sb];
+                    const float3 cs = box_center(level[sb], ix[sb], iy[sb], iz[sb]);
+                    Ud[pt] = make_float3(cs.x - cb.x, cs.y - cb.y, cs.z - cb.z);
+                }
+                int inc = sz;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                if (lane == 31) wsum[pw] = inc;
+                Uoff[pt + 1] = inc;
+            }
+            named_bar_sync(2, 128);
+            if (pt >= 32 && pt < kUWin) Uoff[pt + 1] += wsum[0];
+            if (pt == 0) Uoff[0] = 0;
+            named_bar_sync(2, 128);
+            const int total = Uoff[nu];
+            int self_lo = 0, self_hi = 0;
+            for (int i = 0; i < nu; ++i)
+                if (Uid[i] == b) { self_lo = Uoff[i]; self_hi = Uoff[i + 1]; }
+            const bool last_window = w0 + kUWin >= u1;
+            const int nch = (total + kPtChunk - 1) / kPtChunk;
+            auto fetch = [&](int cl, float* pv) {  // source ps of window chunk cl -> pv[0..8]
+                pv[0] = pv[1] = pv[2] = 1e18f;     // padding source: far away, zero charge
+                for (int r = 0; r < 6; ++r) pv[3 + r] = 0.f;
+                const int f = cl * kPtChunk + ps;
+                if (cl < nch && f < total) {
+                    const int li = find_seg(Uoff, nu, f);
+                    const int i = Upb[li] + (f - Uoff[li]);
+                    const float3 d = Ud[li];
+                    const float4 p = loc[i];
+                    pv[0] = p.x + d.x; pv[1] = p.y + d.y; pv[2] = p.z + d.z;
+                    const float4 q0 = reinterpret_cast<const float4*>(xq + 8 * (int64_t)i)[0];
+                    const float2 q1 = reinterpret_cast<const float2*>(xq + 8 * (int64_t)i)[2];
+                    pv[3] = q0.x; pv[4] = q0.y; pv[5] = q0.z; pv[6] = q0.w; pv[7] = q1.x; pv[8] = q1.y;
+                }
+            };
+            float cur[9], nxt[9];
+            fetch(pg, cur);
+            for (int cl = pg; cl < nch; cl += 2) {
+                fetch(cl + 2, nxt);  // in flight while this chunk waits for its slot
+                const int c = cbase + cl;
+                const int k = c % kPtSlots;
+                PtSlot& S = slot[k];
+                // slot k free: the MMAs (B image) and, before them, the G warps (positions) of chunk c - kPtSlots
+                tc::mbar_wait(&g_free[k], ((c / kPtSlots) & 1) ^ 1);
+                S.X[ps] = cur[0]; S.Y[ps] = cur[1]; S.Z[ps] = cur[2];
+                // B[n][k]: n = r (hi), 8 + r (lo); element at ((k/4)*2 + n/8)*128 + (n%8)*16 + (k%4)*4 bytes
+                float* Bk = S.B + (ps >> 2) * 64 + (ps & 3);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const float v = r < 6 ? cur[3 + r] : 0.f;
+                    const float h = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+                    Bk[r * 4] = h;
+                    Bk[32 + r * 4] = v - h;
+                }
+                if (ps == 0) {
+                    const int s0 = cl * kPtChunk, sn = min(kPtChunk, total - s0);
+                    const bool self = s0 < self_hi && s0 + sn > self_lo;
+                    S.flags = ((last_window && cl == nch - 1) ? 1 : 0) | (self ? 2 : 0);
+                }
+                tc::fence_proxy_async();  // charge image visible to the tensor core
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&staged[k]);
+#pragma unroll
+                for (int q = 0; q < 9; ++q) cur[q] = nxt[q];
+            }
+            cbase += nch;
+        }
+    } else {
+        // ---------------- MMA issuer (whole warp, one elected lane issues)
+        const uint32_t tmu = tbase;
+        const uint32_t idesc = tc::idesc_tf32(128, 16);
+        for (int c = 0;; ++c) {
+            const int k = c % kPtSlots;
+            mbar_wait_warp(&g_full[k], (c / kPtSlots) & 1);
+            tc::fence_after();
+            const int flags = slot[k].flags;
+            if (tc::elect_one()) {
+                const uint32_t bb = tc::smem_u32(slot[k].B);
+#pragma unroll
+                for (int ks = 0; ks < kPtChunk / 8; ++ks) {
+                    // B: K chunk (4 sources) = 256 B (LBO), 8-row group = 128 B (SBO)
+                    const uint64_t bd = tc::smem_desc(bb + 512 * ks, 256, 128);
+                    tc::mma_tf32_ts(tmu + kPtColD, tmu + k * 128 + 8 * ks, bd, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+                    tc::mma_tf32_ts(tmu + kPtColD, tmu + k * 128 + 64 + 8 * ks, bd, idesc, 1u);
+                }
+                tc::commit(&g_free[k]);
+                if (flags & 1) tc::commit(&d_full);
+            }
+            __syncwarp();
+            if (flags & 1) break;
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 12) tc::tmem_dealloc<512>(tbase);
+}
+
 // ------------------------------------------------------------------ L2P + M2P
 // One thread per target panel: y += (1/W) [ (1/s_b) sum ell_b Rt(u) + sum_{w in W(b)} (1/s_w) sum c mu_w It(u_w) ].
 __global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, int64_t p0, const int32_t* __restrict__ panel_leaf,
@@ -1042,7 +1279,11 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         // (memory-bound) after it accumulates into y
         if (do_far) {
             phase_begin(ctx, PH_P2P, &ev, side);
-            if (t->n_own_leaves > 0)
+            if (t->n_p2p_tiles > 0 && !ctx->p2p_simt)
+                k_p2p_tc<<<t->n_p2p_tiles, kPtThreads, 0, side>>>(t->p2p_tiles.p, t->blevel.p, t->bix.p, t->biy.p,
+                                                                  t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p,
+                                                                  t->loc.p, t->xq.p, invW, 0, nl, p0, y);
+            else if (t->n_own_leaves > 0)
                 k_p2p<<<t->n_own_leaves, 128, 0, side>>>(t->own_leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
                                                          t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
                                                          invW, 0, nl, p0, y);

@@ -800,6 +800,24 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         T->n_own_leaves = (int)own.size();
         T->own_leaves.alloc(std::max<size_t>(1, own.size()));
         if (!own.empty()) XRL_CUDA(cudaMemcpyAsync(T->own_leaves.p, own.data(), 4 * own.size(), cudaMemcpyHostToDevice, st));
+        // tensor-core P2P target tiles (leaf, first panel, #targets <= 128, #U sources), heaviest first
+        {
+            std::vector<int4> pt;
+            for (int L : own) {
+                int64_t ns = 0;
+                for (int64_t q = hup[L]; q < hup[L + 1]; ++q) ns += hpe[hus[q]] - hpb[hus[q]];
+                for (int t0 = hpb[L]; t0 < hpe[L]; t0 += 128)
+                    pt.push_back(make_int4(L, t0, std::min(128, hpe[L] - t0), (int)std::min<int64_t>(ns, INT32_MAX)));
+            }
+            std::stable_sort(pt.begin(), pt.end(), [](const int4& a, const int4& b) {
+                return (int64_t)a.z * a.w > (int64_t)b.z * b.w;
+            });
+            T->n_p2p_tiles = (int)pt.size();
+            T->p2p_tiles.alloc(std::max<size_t>(1, pt.size()));
+            if (!pt.empty())
+                XRL_CUDA(cudaMemcpyAsync(T->p2p_tiles.p, pt.data(), sizeof(int4) * pt.size(), cudaMemcpyHostToDevice, st));
+            XRL_CUDA(cudaStreamSynchronize(st));
+        }
         // relevant boxes: panel range meets [p0, p1) (owned subtrees and their ancestors)
         T->rel.assign(nbox, 0);
         for (int b = 0; b < nbox; ++b) T->rel[b] = hpb[b] < T->p1 && hpe[b] > T->p0;

@@ -96,6 +96,7 @@ struct xrl_ctx_s {
     // timing
     bool timing = false;
     int sched = XRL_SCHED_FORK;       // xrl_ctx_set_sched
+    bool p2p_simt = true;             // XRL_P2P_TC=1: experimental tensor-core P2P (k_p2p_tc)
     int num_sms = 148;
     int64_t launches = 0;
     int refs = 0;         // live trees
@@ -154,6 +155,8 @@ struct xrl_tree_s {
     std::vector<uint8_t> rel;                // box relevant to this rank
     xrl::DBuf<int32_t> own_leaves;           // owned leaves (Morton order)
     int32_t n_own_leaves = 0;
+    xrl::DBuf<int4> p2p_tiles;               // tensor-core P2P: (leaf, first panel, #targets <= 128, #sources)
+    int32_t n_p2p_tiles = 0;
     std::vector<int32_t> l2l_start;          // per-level offsets into l2l_boxes
     xrl::DBuf<int32_t> l2l_boxes;
     xrl::DBuf<float2> xfull;                 // gathered x (multi-rank MVM)
