@@ -53,52 +53,49 @@ __global__ void k_pack(int64_t n, const float2* __restrict__ x, float* __restric
 }
 
 // ------------------------------------------------------------------ P2M
-constexpr int kChunk = 64;
+constexpr int kChunk = 128;  // panels per P2M pass (one per thread)
+constexpr int kP2MSmem = kChunk * (kNC + 6) * 4;
 
 __global__ void __launch_bounds__(128) k_p2m(const int32_t* __restrict__ leaves, const int32_t* __restrict__ pb,
                                              const int32_t* __restrict__ pe, const int32_t* __restrict__ level,
                                              const float4* __restrict__ loc, const float* __restrict__ xq,
                                              float* __restrict__ mu)
 {
-    __shared__ float H[kChunk][kNC];
-    __shared__ float Q[kChunk][6];
+    extern __shared__ __align__(16) float p2m_sm[];
+    float(*H)[kNC] = reinterpret_cast<float(*)[kNC]>(p2m_sm);          // [kChunk][121]
+    float(*Q)[6] = reinterpret_cast<float(*)[6]>(p2m_sm + kChunk * kNC);  // [kChunk][6]
     const int b = leaves[blockIdx.x];
     const int s = pb[b], e = pe[b];
     const float inv_s = ldexpf(1.f, level[b]);
-    float acc[6];
-#pragma unroll
-    for (int j = 0; j < 6; ++j) acc[j] = 0.f;
+    float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // thread k < 121: mu[k][0..5]
+    const int k = threadIdx.x;
     for (int c0 = s; c0 < e; c0 += kChunk) {
         const int cn = min(kChunk, e - c0);
         if (threadIdx.x < cn) {
             const int i = c0 + threadIdx.x;
             float4 p = loc[i];
-            float h[kNC];
-            regular_harmonics<kP>(p.x * inv_s, p.y * inv_s, p.z * inv_s, c_tab, h);
-#pragma unroll
-            for (int k = 0; k < kNC; ++k) H[threadIdx.x][k] = h[k];
+            float* hrow = H[threadIdx.x];
+            regular_harmonics_visit<kP>(p.x * inv_s, p.y * inv_s, p.z * inv_s, c_tab,
+                                        [&](int kk, float v) { hrow[kk] = v; });
 #pragma unroll
             for (int r = 0; r < 6; ++r) Q[threadIdx.x][r] = xq[8 * (int64_t)i + r];
         }
         __syncthreads();
+        if (k < kNC) {
+            for (int p = 0; p < cn; ++p) {
+                const float hv = H[p][k];
 #pragma unroll
-        for (int j = 0; j < 6; ++j) {
-            const int o = threadIdx.x + 128 * j;
-            if (o < kNC * 6) {
-                const int k = o / 6, r = o % 6;
-                float a = acc[j];
-                for (int p = 0; p < cn; ++p) a += H[p][k] * Q[p][r];
-                acc[j] = a;
+                for (int r = 0; r < 6; ++r) acc[r] = fmaf(hv, Q[p][r], acc[r]);
             }
         }
         __syncthreads();
     }
     float* out = mu + (size_t)b * kBoxStride;
+    if (k < kNC) {
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        const int o = threadIdx.x + 128 * j;
-        if (o < kNC * 6) out[o] = acc[j];
-        else if (o < kBoxStride) out[o] = 0.f;
+        for (int r = 0; r < 6; ++r) out[6 * k + r] = acc[r];
+    } else if (k < kNC + 2) {
+        out[kNC * 6 + (k - kNC)] = 0.f;  // padding floats 726, 727
     }
 }
 
@@ -1116,14 +1113,12 @@ __global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, int64_t p0, const in
     const float4 tp = loc[i];
     float far[6] = {0, 0, 0, 0, 0, 0};
     {
-        float h[kNC];
-        regular_harmonics<kP>(tp.x * inv_sb, tp.y * inv_sb, tp.z * inv_sb, c_tab, h);
-        const float* L = ell + (size_t)b * kEllStride;  // ell[r][k]
+        // L2P: contract the local expansion ell[r][k] (warp-uniform leaf mostly: broadcast loads) on the fly
+        const float* L = ell + (size_t)b * kEllStride;
+        regular_harmonics_visit<kP>(tp.x * inv_sb, tp.y * inv_sb, tp.z * inv_sb, c_tab, [&](int k, float v) {
 #pragma unroll
-        for (int k = 0; k < kNC; ++k) {
-#pragma unroll
-            for (int r = 0; r < 6; ++r) far[r] = fmaf(__ldg(L + r * 128 + k), h[k], far[r]);
-        }
+            for (int r = 0; r < 6; ++r) far[r] = fmaf(__ldg(L + r * 128 + k), v, far[r]);
+        });
 #pragma unroll
         for (int r = 0; r < 6; ++r) far[r] *= inv_sb;
     }
@@ -1132,19 +1127,16 @@ __global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, int64_t p0, const in
         const int lw = level[w];
         const float3 cw = box_center(lw, ix[w], iy[w], iz[w]);
         const float inv_sw = ldexpf(1.f, lw);
-        float h[kNC];
-        irregular_harmonics<kP>((tp.x + cb.x - cw.x) * inv_sw, (tp.y + cb.y - cw.y) * inv_sw,
-                                (tp.z + cb.z - cw.z) * inv_sw, c_tab, h);
         const float2* M = reinterpret_cast<const float2*>(mu + (size_t)w * kBoxStride);
         float a[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int k = 0; k < kNC; ++k) {
-            const float hk = (degree_of(k) * degree_of(k) == k) ? h[k] : 2.f * h[k];
+        irregular_harmonics_visit<kP>((tp.x + cb.x - cw.x) * inv_sw, (tp.y + cb.y - cw.y) * inv_sw,
+                                      (tp.z + cb.z - cw.z) * inv_sw, c_tab, [&](int k, float v) {
+            const float hk = (degree_of(k) * degree_of(k) == k) ? v : 2.f * v;
             const float2 m0 = __ldg(M + 3 * k), m1 = __ldg(M + 3 * k + 1), m2 = __ldg(M + 3 * k + 2);
             a[0] = fmaf(m0.x, hk, a[0]); a[1] = fmaf(m0.y, hk, a[1]);
             a[2] = fmaf(m1.x, hk, a[2]); a[3] = fmaf(m1.y, hk, a[3]);
             a[4] = fmaf(m2.x, hk, a[4]); a[5] = fmaf(m2.y, hk, a[5]);
-        }
+        });
 #pragma unroll
         for (int r = 0; r < 6; ++r) far[r] = fmaf(a[r], inv_sw, far[r]);
     }
@@ -1233,6 +1225,7 @@ void upload_constants(xrl_ctx ctx)
     XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
+    XRL_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2MSmem));
 }
 
 }  // namespace xrl
@@ -1306,7 +1299,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
 
     if (do_far && t->nlevel > 1) {
         phase_begin(ctx, PH_P2M, &ev, st);
-        k_p2m<<<t->nleaf, 128, 0, st>>>(t->leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p, t->xq.p, t->mu.p);
+        k_p2m<<<t->nleaf, 128, kP2MSmem, st>>>(t->leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p, t->xq.p, t->mu.p);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
         phase_end(ctx, PH_P2M, ev, st);

@@ -130,6 +130,71 @@ XRL_HD void irregular_harmonics(T x, T y, T z, const Tab& tab, T* h)
     }
 }
 
+// Streaming variants: f(i, value) for every real coefficient i (same order of
+// evaluation, no (p+1)^2 array: L2P/M2P contract on the fly).
+template <int P, typename T, typename Tab, typename F>
+XRL_HD void regular_harmonics_visit(T x, T y, T z, const Tab& tab, F&& f)
+{
+    const T r2 = x * x + y * y + z * z;
+    T cr = T(1), ci = T(0);
+#pragma unroll
+    for (int m = 0; m <= P; ++m) {
+        if (m > 0) {
+            const T d = -tab.D[m];
+            const T nr = d * (x * cr - y * ci);
+            const T ni = d * (x * ci + y * cr);
+            cr = nr; ci = ni;
+        }
+        T pr = cr, pi = ci;
+        T qr = T(0), qi = T(0);
+        if (m == 0) f(0, cr);
+        else { f(hidx(m, m), cr); f(hidx(m, m) + 1, ci); }
+#pragma unroll
+        for (int n = 1; n <= P; ++n) {
+            if (n <= m) continue;
+            const T a = tab.A[n * (P + 1) + m] * z;
+            const T b = tab.B[n * (P + 1) + m] * r2;
+            const T nr = a * pr - b * qr;
+            const T ni = a * pi - b * qi;
+            qr = pr; qi = pi; pr = nr; pi = ni;
+            if (m == 0) f(n * n, nr);
+            else { f(hidx(n, m), nr); f(hidx(n, m) + 1, ni); }
+        }
+    }
+}
+
+template <int P, typename T, typename Tab, typename F>
+XRL_HD void irregular_harmonics_visit(T x, T y, T z, const Tab& tab, F&& f)
+{
+    const T r2 = x * x + y * y + z * z;
+    const T ir2 = T(1) / r2;
+    T cr = T(1) / std::sqrt(r2), ci = T(0);
+#pragma unroll
+    for (int m = 0; m <= P; ++m) {
+        if (m > 0) {
+            const T d = -tab.D[m] * ir2;
+            const T nr = d * (x * cr - y * ci);
+            const T ni = d * (x * ci + y * cr);
+            cr = nr; ci = ni;
+        }
+        T pr = cr, pi = ci;
+        T qr = T(0), qi = T(0);
+        if (m == 0) f(0, cr);
+        else { f(hidx(m, m), cr); f(hidx(m, m) + 1, ci); }
+#pragma unroll
+        for (int n = 1; n <= P; ++n) {
+            if (n <= m) continue;
+            const T a = tab.A[n * (P + 1) + m] * z;
+            const T b = tab.B[n * (P + 1) + m];
+            const T nr = (a * pr - b * qr) * ir2;
+            const T ni = (a * pi - b * qi) * ir2;
+            qr = pr; qi = pi; pr = nr; pi = ni;
+            if (m == 0) f(n * n, nr);
+            else { f(hidx(n, m), nr); f(hidx(n, m) + 1, ni); }
+        }
+    }
+}
+
 // Weight c of the real contraction phi*s = sum c_i mu_i It_i (M2P) and of
 // ell = sum q c_i It_i (P2L): 1 for m = 0, 2 for the (re, im) pair of m > 0.
 XRL_HD float cweight(int i)
