@@ -577,32 +577,56 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
 // (L2-resident) + 24 B of y per row.  8 lanes per row, 4 rows per warp; each
 // lane issues 4 independent (col, val) loads before their 4 gathers (memory-
 // level parallelism), shuffle reduction over the 8 lanes.
-__global__ void __launch_bounds__(256) k_near_spmv(int64_t n, int64_t r0, const int64_t* __restrict__ ptr,
-                                                   const int32_t* __restrict__ col, const float* __restrict__ val,
-                                                   const float* __restrict__ xq, int accumulate, float2* __restrict__ y)
+// 32-byte read-only load through L1 (the charge records are re-read by neighbouring rows)
+__device__ __forceinline__ void ldg256_l1(const float* p, float* v)
 {
-    // rows r0 .. r0+n-1 (owned range); y local [3][n]
-    const int64_t lrow = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+}
+
+__global__ void __launch_bounds__(256) k_near_spmv(int64_t n, int64_t r0, const int64_t* __restrict__ ptr,
+                                                   const int2* __restrict__ cv, const float* __restrict__ xq,
+                                                   int accumulate, float2* __restrict__ y)
+{
+    // rows r0 .. r0+n-1 (owned range); y local [3][n].  8 lanes per row, each lane keeps
+    // kNearU (col, val) loads and then kNearU gathers in flight (memory-level parallelism).
+    constexpr int kL = 8, kNearU = 4;
+    const int64_t lrow = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kL;
     const int64_t row = r0 + lrow;
-    const int lane = threadIdx.x & 7;
+    const int lane = threadIdx.x & (kL - 1);
     float a[6] = {0, 0, 0, 0, 0, 0};
     if (lrow < n) {
         const int64_t e = ptr[row + 1];
-#pragma unroll 4
-        for (int64_t j = ptr[row] + lane; j < e; j += 8) {
-            const float v = __ldcs(val + j);
-            const int64_t c = __ldcs(col + j);
-            const float4 q0 = reinterpret_cast<const float4*>(xq + 8 * c)[0];
-            const float2 q1 = reinterpret_cast<const float2*>(xq + 8 * c)[2];
-            a[0] = fmaf(v, q0.x, a[0]); a[1] = fmaf(v, q0.y, a[1]); a[2] = fmaf(v, q0.z, a[2]);
-            a[3] = fmaf(v, q0.w, a[3]); a[4] = fmaf(v, q1.x, a[4]); a[5] = fmaf(v, q1.y, a[5]);
+        for (int64_t j0 = ptr[row] + lane; j0 < e; j0 += kL * kNearU) {
+            int2 c[kNearU];
+#pragma unroll
+            for (int u = 0; u < kNearU; ++u) {
+                const int64_t j = j0 + (int64_t)u * kL;
+                c[u] = j < e ? __ldcs(cv + j) : make_int2(-1, 0);
+            }
+            float q[kNearU][8];
+#pragma unroll
+            for (int u = 0; u < kNearU; ++u) {
+                if (c[u].x >= 0) {
+                    ldg256_l1(xq + 8 * (int64_t)c[u].x, q[u]);  // the whole 32-byte charge record, one request
+                } else {
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) q[u][r] = 0.f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kNearU; ++u) {
+                const float v = __int_as_float(c[u].y);
+#pragma unroll
+                for (int r = 0; r < 6; ++r) a[r] = fmaf(v, q[u][r], a[r]);
+            }
         }
     }
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
-        a[r] += __shfl_xor_sync(0xffffffffu, a[r], 1);
-        a[r] += __shfl_xor_sync(0xffffffffu, a[r], 2);
-        a[r] += __shfl_xor_sync(0xffffffffu, a[r], 4);
+#pragma unroll
+        for (int o = 1; o < kL; o <<= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], o);
     }
     if (lrow < n && lane < 3) {
         float2 o = make_float2(a[2 * lane], a[2 * lane + 1]);
@@ -1286,7 +1310,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         }
         if (do_near) {
             phase_begin(ctx, PH_NEAR, &ev, side);
-            if (nl > 0) k_near_spmv<<<nblk(8 * nl, 256), 256, 0, side>>>(nl, p0, nr->row_ptr.p, nr->col.p, nr->val.p, t->xq.p,
+            if (nl > 0) k_near_spmv<<<nblk(8 * nl, 256), 256, 0, side>>>(nl, p0, nr->row_ptr.p, nr->cv.p, t->xq.p,
                                                                          do_far ? 1 : 0, y);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;

@@ -125,6 +125,13 @@ __global__ void k_near_search(int64_t n, TreeView tv, double eta, int64_t* cnt, 
     if (!FILL) cnt[k] = c;
 }
 
+__global__ void k_interleave(int64_t nnz, const int32_t* __restrict__ col, const float* __restrict__ val,
+                             int2* __restrict__ cv)
+{
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < nnz) cv[j] = make_int2(col[j], __float_as_int(val[j]));
+}
+
 __global__ void k_near_values(int64_t n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ cols,
                               const double* __restrict__ cent, const double* __restrict__ area,
                               const double* __restrict__ tverts, float* val, double* val64)
@@ -193,6 +200,12 @@ static xrl_status near_impl(xrl_tree t, double eta, xrl_near* out)
     k_near_values<<<nblk(n, 64), 64, 0, st>>>(n, N->row_ptr.p, N->col.p, t->cent.p, t->area.p, t->tverts.p,
                                               N->val.p, N->val64.p);
     XRL_LAUNCH_CHECK();
+    // interleaved (col, FP32 value) pairs for the SpMV: one 8-byte load per nonzero
+    N->cv.alloc(std::max<int64_t>(1, N->nnz));
+    if (N->nnz) {
+        k_interleave<<<nblk(N->nnz, 256), 256, 0, st>>>(N->nnz, N->col.p, N->val.p, N->cv.p);
+        XRL_LAUNCH_CHECK();
+    }
     XRL_CUDA(cudaStreamSynchronize(st));
     ++t->refs;
     *out = N.release();

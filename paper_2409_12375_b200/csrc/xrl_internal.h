@@ -182,6 +182,7 @@ struct xrl_near_s {
     xrl::DBuf<int64_t> row_ptr;
     xrl::DBuf<int32_t> col;
     xrl::DBuf<float> val;       // N_kl (FP32)
+    xrl::DBuf<int2> cv;         // (col, N_kl bits) interleaved for the SpMV
     xrl::DBuf<double> val64;    // P_kl (FP64, before subtraction)
 };
 
