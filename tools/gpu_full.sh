@@ -10,7 +10,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/status.txt
 timeout 900 python bench.py > $O/bench.log 2>&1; echo "bench rc=$?" >> $O/status.txt
 if [ "${NCU:-1}" = "1" ]; then
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file $O/launches.csv python bench.py --steps 3 --warmup 3 --leaf $L --no-cpu-baseline --gmres-iters 0 > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> $O/status.txt
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_m2l|k_p2p|k_near_spmv|k_l2p_m2p|k_p2m" -s 12 -c 6 -o $O/prof_full python tools/prof_mvm.py 4 3 $L > $O/ncu.log 2>&1; echo "ncu full rc=$?" >> $O/status.txt
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches.csv python bench.py --steps 3 --warmup 3 --leaf $L --no-cpu-baseline --gmres-iters 0 > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> $O/status.txt
+for K in k_m2l_tc k_p2p k_near_spmv k_l2p_m2p k_p2m; do
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^${K}\$|::${K}\$|${K}\(" -s 1 -c 1 -o $O/full_$K python tools/prof_mvm.py 4 3 $L > $O/ncu_$K.log 2>&1; echo "ncu full $K rc=$?" >> $O/status.txt
+done
 fi
 cat $O/status.txt
