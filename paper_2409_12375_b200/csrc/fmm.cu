@@ -17,7 +17,9 @@
 //   k_m2l_tc     V-list translations on tcgen05 (3xTF32, warp-specialised)
 //   k_p2l        X-list particle -> local
 //   k_l2l        parent -> child, per level (top-down)
-//   k_l2p_m2p    per target panel: L2P + M2P (W list), completes y
+//   k_ell_kmajor leaves' ell[r][k] -> ellk[k][8]
+//   k_l2p        per target panel: L2P
+//   k_m2p        W-list M2P (leaves with a W list), completes y
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1118,40 +1120,74 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_p2p_tc(
     if (warp == 9) tc::tmem_dealloc<512>(tbase);
 }
 
-// ------------------------------------------------------------------ L2P + M2P
-// One thread per target panel: y += (1/W) [ (1/s_b) sum ell_b Rt(u) + sum_{w in W(b)} (1/s_w) sum c mu_w It(u_w) ].
-__global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, int64_t p0, const int32_t* __restrict__ panel_leaf,
-                                                 const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
-                                                 const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
-                                                 const int64_t* __restrict__ wptr, const int32_t* __restrict__ wsrc,
-                                                 const float4* __restrict__ loc, const float* __restrict__ mu,
-                                                 const float* __restrict__ ell, float invW, float2* __restrict__ y)
+// ell[r][k] (r-major, M2L/L2L layout) -> ellk[k][8] (k-major, 6 RHS + 2 pad) for the leaves: the L2P
+// then reads one 32-byte record per coefficient instead of 6 scalars.
+__global__ void k_ell_kmajor(const int32_t* __restrict__ leaves, const float* __restrict__ ell, float* __restrict__ ellk)
+{
+    const int b = leaves[blockIdx.x];
+    const float* src = ell + (size_t)b * kEllStride;
+    float* dst = ellk + (size_t)b * kEllKStride;
+    for (int j = threadIdx.x; j < kNC * 8; j += blockDim.x) {
+        const int k = j >> 3, r = j & 7;
+        dst[j] = r < 6 ? src[r * 128 + k] : 0.f;
+    }
+}
+
+// ------------------------------------------------------------------ L2P (+ M2P below)
+// One thread per target panel: y += (1/W) (1/s_b) sum_k ellk_b[k] Rt_k(u).
+__global__ void __launch_bounds__(128) k_l2p(int64_t n, int64_t p0, const int32_t* __restrict__ panel_leaf,
+                                             const int32_t* __restrict__ level, const float4* __restrict__ loc,
+                                             const float* __restrict__ ellk, float invW, float2* __restrict__ y)
 {
     const int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // local index, panel p0 + li
     if (li >= n) return;
     const int64_t i = p0 + li;
     const int b = panel_leaf[i];
-    const int lb = level[b];
-    const float3 cb = box_center(lb, ix[b], iy[b], iz[b]);
-    const float inv_sb = ldexpf(1.f, lb);
+    const float inv_sb = ldexpf(1.f, level[b]);
     const float4 tp = loc[i];
     float far[6] = {0, 0, 0, 0, 0, 0};
     {
-        // L2P: contract the local expansion ell[r][k] (warp-uniform leaf mostly: broadcast loads) on the fly
-        const float* L = ell + (size_t)b * kEllStride;
+        // L2P: contract the k-major local expansion ellk[k][8] (one 256-bit load per coefficient) on the fly
+        const float* L = ellk + (size_t)b * kEllKStride;
         regular_harmonics_visit<kP>(tp.x * inv_sb, tp.y * inv_sb, tp.z * inv_sb, c_tab, [&](int k, float v) {
+            float l[8];
+            ldg256_l1(L + 8 * k, l);
 #pragma unroll
-            for (int r = 0; r < 6; ++r) far[r] = fmaf(__ldg(L + r * 128 + k), v, far[r]);
+            for (int r = 0; r < 6; ++r) far[r] = fmaf(l[r], v, far[r]);
         });
 #pragma unroll
         for (int r = 0; r < 6; ++r) far[r] *= inv_sb;
     }
-    for (int64_t wj = wptr[b]; wj < wptr[b + 1]; ++wj) {
-        const int w = wsrc[wj];
-        const int lw = level[w];
-        const float3 cw = box_center(lw, ix[w], iy[w], iz[w]);
-        const float inv_sw = ldexpf(1.f, lw);
-        const float2* M = reinterpret_cast<const float2*>(mu + (size_t)w * kBoxStride);
+    float2 a = y[li], c = y[n + li], d = y[2 * n + li];
+    y[li] = make_float2(fmaf(far[0], invW, a.x), fmaf(far[1], invW, a.y));
+    y[n + li] = make_float2(fmaf(far[2], invW, c.x), fmaf(far[3], invW, c.y));
+    y[2 * n + li] = make_float2(fmaf(far[4], invW, d.x), fmaf(far[5], invW, d.y));
+}
+
+__device__ __forceinline__ void red_add_v2(float* p, float a, float b)
+{
+    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+
+// M2P (W list, adaptive): one CTA per (owned leaf b, W box w) pair, thread per panel of b;
+// y += (1/W) (1/s_w) sum_k c_k mu_w[k] It_k(u_w), accumulated with red.global.add (pairs of one leaf
+// run concurrently).
+__global__ void __launch_bounds__(128) k_m2p(const int2* __restrict__ wpairs, int64_t p0, int64_t n,
+                                             const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
+                                             const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
+                                             const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
+                                             const float4* __restrict__ loc, const float* __restrict__ mu, float invW,
+                                             float2* __restrict__ y)
+{
+    const int2 pr = wpairs[blockIdx.x];
+    const int b = pr.x, w = pr.y;
+    const float3 cb = box_center(level[b], ix[b], iy[b], iz[b]);
+    const int lw = level[w];
+    const float3 cw = box_center(lw, ix[w], iy[w], iz[w]);
+    const float inv_sw = ldexpf(1.f, lw);
+    const float2* M = reinterpret_cast<const float2*>(mu + (size_t)w * kBoxStride);
+    for (int i = pb[b] + threadIdx.x; i < pe[b]; i += blockDim.x) {
+        const float4 tp = loc[i];
         float a[6] = {0, 0, 0, 0, 0, 0};
         irregular_harmonics_visit<kP>((tp.x + cb.x - cw.x) * inv_sw, (tp.y + cb.y - cw.y) * inv_sw,
                                       (tp.z + cb.z - cw.z) * inv_sw, c_tab, [&](int k, float v) {
@@ -1161,13 +1197,12 @@ __global__ void __launch_bounds__(128) k_l2p_m2p(int64_t n, int64_t p0, const in
             a[2] = fmaf(m1.x, hk, a[2]); a[3] = fmaf(m1.y, hk, a[3]);
             a[4] = fmaf(m2.x, hk, a[4]); a[5] = fmaf(m2.y, hk, a[5]);
         });
-#pragma unroll
-        for (int r = 0; r < 6; ++r) far[r] = fmaf(a[r], inv_sw, far[r]);
+        const float sc = inv_sw * invW;
+        const int64_t li = i - p0;
+        red_add_v2(reinterpret_cast<float*>(y + li), a[0] * sc, a[1] * sc);
+        red_add_v2(reinterpret_cast<float*>(y + n + li), a[2] * sc, a[3] * sc);
+        red_add_v2(reinterpret_cast<float*>(y + 2 * n + li), a[4] * sc, a[5] * sc);
     }
-    float2 a = y[li], c = y[n + li], d = y[2 * n + li];
-    y[li] = make_float2(fmaf(far[0], invW, a.x), fmaf(far[1], invW, a.y));
-    y[n + li] = make_float2(fmaf(far[2], invW, c.x), fmaf(far[3], invW, c.y));
-    y[2 * n + li] = make_float2(fmaf(far[4], invW, d.x), fmaf(far[5], invW, d.y));
 }
 
 __global__ void k_permute(int64_t n, int nvec, const int32_t* __restrict__ idx, const float2* __restrict__ in,
@@ -1380,8 +1415,18 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
     if (sched) XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     if (do_far && t->nlevel > 1 && nl > 0) {
         phase_begin(ctx, PH_L2P, &ev, st);
-        k_l2p_m2p<<<nblk(nl, 128), 128, 0, st>>>(nl, p0, t->panel_leaf.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
-                                                t->w_ptr.p, t->w_src.p, t->loc.p, t->mu.p, t->ell.p, invW, y);
+        if (t->ellk.n < (size_t)t->nbox * kEllKStride) t->ellk.alloc((size_t)t->nbox * kEllKStride);
+        if (t->n_own_leaves > 0) {
+            k_ell_kmajor<<<t->n_own_leaves, 256, 0, st>>>(t->own_leaves.p, t->ell.p, t->ellk.p);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+        k_l2p<<<nblk(nl, 128), 128, 0, st>>>(nl, p0, t->panel_leaf.p, t->blevel.p, t->loc.p, t->ellk.p, invW, y);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+        if (t->n_w_targets > 0)
+            k_m2p<<<t->n_w_targets, 128, 0, st>>>(t->w_targets.p, p0, nl, t->bpb.p, t->bpe.p, t->blevel.p, t->bix.p,
+                                                  t->biy.p, t->biz.p, t->loc.p, t->mu.p, invW, y);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
         phase_end(ctx, PH_L2P, ev, st);

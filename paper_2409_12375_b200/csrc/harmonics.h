@@ -132,12 +132,12 @@ XRL_HD void irregular_harmonics(T x, T y, T z, const Tab& tab, T* h)
 
 // Streaming variants: f(i, value) for every real coefficient i (same order of
 // evaluation, no (p+1)^2 array: L2P/M2P contract on the fly).
-template <int P, typename T, typename Tab, typename F>
+template <int P, bool kUnrollM = true, typename T, typename Tab, typename F>
 XRL_HD void regular_harmonics_visit(T x, T y, T z, const Tab& tab, F&& f)
 {
     const T r2 = x * x + y * y + z * z;
     T cr = T(1), ci = T(0);
-#pragma unroll
+#pragma unroll (kUnrollM ? P + 1 : 1)
     for (int m = 0; m <= P; ++m) {
         if (m > 0) {
             const T d = -tab.D[m];
@@ -163,13 +163,13 @@ XRL_HD void regular_harmonics_visit(T x, T y, T z, const Tab& tab, F&& f)
     }
 }
 
-template <int P, typename T, typename Tab, typename F>
+template <int P, bool kUnrollM = true, typename T, typename Tab, typename F>
 XRL_HD void irregular_harmonics_visit(T x, T y, T z, const Tab& tab, F&& f)
 {
     const T r2 = x * x + y * y + z * z;
     const T ir2 = T(1) / r2;
     T cr = T(1) / std::sqrt(r2), ci = T(0);
-#pragma unroll
+#pragma unroll (kUnrollM ? P + 1 : 1)
     for (int m = 0; m <= P; ++m) {
         if (m > 0) {
             const T d = -tab.D[m] * ir2;

@@ -951,6 +951,25 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         T->x_targets.alloc(std::max<size_t>(1, xt.size()));
         if (!xt.empty()) XRL_CUDA(cudaMemcpyAsync(T->x_targets.p, xt.data(), 4 * xt.size(), cudaMemcpyHostToDevice, st));
     }
+    // W pairs of the owned leaves (M2P: one CTA per pair)
+    {
+        std::vector<int64_t> hw(nbox + 1);
+        std::vector<int32_t> own(std::max(1, T->n_own_leaves));
+        XRL_CUDA(cudaMemcpyAsync(hw.data(), T->w_ptr.p, 8 * (nbox + 1), cudaMemcpyDeviceToHost, st));
+        if (T->n_own_leaves)
+            XRL_CUDA(cudaMemcpyAsync(own.data(), T->own_leaves.p, 4 * T->n_own_leaves, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<int32_t> hws(std::max<int64_t>(1, T->nw));
+        if (T->nw) XRL_CUDA(cudaMemcpyAsync(hws.data(), T->w_src.p, 4 * T->nw, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        std::vector<int2> wp;  // (target leaf, source box) pairs of the owned leaves
+        for (int i = 0; i < T->n_own_leaves; ++i)
+            for (int64_t q = hw[own[i]]; q < hw[own[i] + 1]; ++q) wp.push_back(make_int2(own[i], hws[q]));
+        T->n_w_targets = (int)wp.size();
+        T->w_targets.alloc(std::max<size_t>(1, wp.size()));
+        if (!wp.empty()) XRL_CUDA(cudaMemcpyAsync(T->w_targets.p, wp.data(), sizeof(int2) * wp.size(), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+    }
     // MVM scratch
     T->mu.alloc((size_t)nbox * kBoxStride);
     T->ell.alloc((size_t)nbox * kEllStride);

@@ -80,6 +80,7 @@ struct DeviceOperators {
 constexpr int kNCP = 128;            // padded coefficient count
 constexpr int kBoxStride = 728;      // floats per box multipole mu[k][r] (121*6 padded to 16 B)
 constexpr int kEllStride = 768;      // floats per box local expansion ell[r][k] (r-major, k padded to 128)
+constexpr int kEllKStride = 968;     // floats per leaf local expansion ellk[k][8] (k-major, for the L2P)
 
 }  // namespace xrl
 
@@ -145,6 +146,8 @@ struct xrl_tree_s {
     // boxes with non-empty X list, leaves with non-empty W list
     xrl::DBuf<int32_t> x_targets;
     int32_t n_x_targets = 0;
+    xrl::DBuf<int2> w_targets;               // (owned leaf, W-list box) pairs (M2P, one CTA each)
+    int32_t n_w_targets = 0;
     // parents per level for M2M/L2L: boxes with children, grouped by level
     std::vector<int32_t> par_start;          // host [nlevel+1] offsets into parents
     xrl::DBuf<int32_t> parents;
@@ -170,6 +173,7 @@ struct xrl_tree_s {
     // MVM scratch
     xrl::DBuf<float> mu;                     // [nbox][kBoxStride]  mu[k][r]
     xrl::DBuf<float> ell;                    // [nbox][kEllStride] ell[r][k]
+    xrl::DBuf<float> ellk;                   // [nbox][kEllKStride] ellk[k][8] (leaves, per MVM)
     xrl::DBuf<float> mu_img;                 // tcgen05 M2L: per-box FP32 r-major images (3 KB)
     xrl::DBuf<float> xq;                     // [n][8] packed charges
     xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging
