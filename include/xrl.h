@@ -328,6 +328,20 @@ xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b, void* x, int32_t 
 xrl_status xrl_port_rhs(xrl_topo topo, int32_t port, double volts, void* b);
 xrl_status xrl_port_currents(xrl_topo topo, const void* x, int32_t nrhs, double* i_ports);
 
+/* R/L extraction sweep (PAPER.md:152 solves the loop system at every frequency
+ * point and reports R and L).  For each freqs[j] > 0: the operator (xrl_operator_create with zs,
+ * sigma, zeta), the block diagonal-of-P preconditioner (block_size, <= 64), one GMRES (opts; NULL =
+ * restart 50, the paper's tolerance rule) with the n_ports unit-voltage port excitations as batched
+ * right-hand sides, the port currents give the admittance Y[:, q] = I(port q excited), and
+ * Z = Y^-1 (FP64), R = Re Z, L = Im Z / (2 pi f).  Host outputs, each may be NULL:
+ * z double [n_freq][n_ports][n_ports][2] (re, im), r and l double [n_freq][n_ports][n_ports],
+ * iters int32 and true_rre double [n_freq][n_ports].  Handles are borrowed.  Errors: XRL_EINVAL
+ * (no ports, n_freq < 1, f <= 0), XRL_ESINGULAR (singular Y), XRL_ENOCONV (some column did not
+ * converge; outputs still filled), plus those of the calls above. */
+xrl_status xrl_extract(xrl_tree tree, xrl_near near, xrl_topo topo, const double* zs, double sigma, double zeta,
+                       int32_t n_freq, const double* freqs, int32_t block_size, const xrl_gmres_opts* opts,
+                       double* z, double* r, double* l, int32_t* iters, double* true_rre);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
                   "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["abi.cu", "tree.cu", "near.cu", "fmm.cu", "solver.cu", "comm.cu", "operators.cpp", "topology.cpp"]
+SOURCES = ["abi.cu", "tree.cu", "near.cu", "fmm.cu", "solver.cu", "comm.cu", "operators.cpp", "topology.cpp",
+           "extract.cpp"]
 
 
 def _nccl_dirs():

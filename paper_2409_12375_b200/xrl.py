@@ -25,7 +25,7 @@ EXPORTS = [
     "xrl_tree_build", "xrl_tree_destroy", "xrl_tree_info", "xrl_tree_perm", "xrl_to_library_order",
     "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble", "xrl_near_destroy",
     "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_timing_enable", "xrl_timing_count",
-    "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched",
+    "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_extract",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
     "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
@@ -124,6 +124,8 @@ def lib():
         L.xrl_launch_count.restype = i64
         L.xrl_ctx_set_sched.argtypes = [P, i32]
         L.xrl_ctx_set_sched.restype = ctypes.c_int32
+        L.xrl_extract.argtypes = [P, P, P, P, ctypes.c_double, ctypes.c_double, i32, P, i32, P, P, P, P, P, P]
+        L.xrl_extract.restype = ctypes.c_int32
         L.xrl_topology_build.argtypes = [P, i32, P, pp]
         L.xrl_topology_info.argtypes = [P, ctypes.POINTER(TopoInfo)]
         L.xrl_topology_export.argtypes = [P] * 12
@@ -569,3 +571,27 @@ def gmres(op: Operator, pc, b, x=None, restart=50, max_iters=2000, tol=0.0):
                          _ptr(conv))
     check(st)
     return x, {"iters": iters, "rre": rre, "true_rre": trre, "converged": conv.astype(bool), "status": st}
+
+
+def extract(tree: Tree, near: Near, topo: Topology, freqs, zs=None, sigma=5.8e7, zeta=1e-4, block_size=64,
+            restart=50, max_iters=2000, tol=0.0):
+    """xrl_extract: R/L sweep.  Returns dict with z [n_freq][P][P] complex, r, l [n_freq][P][P],
+    iters, true_rre [n_freq][P] and the status (XRL_ENOCONV is reported, not raised)."""
+    freqs = np.ascontiguousarray(freqs, np.float64)
+    nf, npt = freqs.size, topo.info()["n_ports"]
+    z = np.zeros((nf, npt, npt, 2))
+    r = np.zeros((nf, npt, npt))
+    l_ = np.zeros((nf, npt, npt))
+    it = np.zeros((nf, npt), np.int32)
+    tr = np.zeros((nf, npt))
+    zsa = None
+    if zs is not None:
+        zz = np.broadcast_to(np.asarray(zs, dtype=np.complex128), (tree.n,))
+        zsa = np.ascontiguousarray(np.stack([zz.real, zz.imag], axis=1))
+    st = lib().xrl_extract(tree.h, near.h, topo.h, _ptr(zsa) if zsa is not None else None, sigma, zeta, nf,
+                           _ptr(freqs), block_size, ctypes.byref(GmresOpts(restart, max_iters, tol)), _ptr(z),
+                           _ptr(r), _ptr(l_), _ptr(it), _ptr(tr))
+    if st < 0:
+        check(st)
+    return {"freqs": freqs, "z": z[..., 0] + 1j * z[..., 1], "r": r, "l": l_, "iters": it, "true_rre": tr,
+            "status": st}
