@@ -305,7 +305,8 @@ xrl_status xrl_precond_export(xrl_precond pc, int32_t* n_blocks, int32_t* block_
 void xrl_precond_destroy(xrl_precond pc);
 
 /* Restarted GMRES (restart 50; relative residual 1e-4 above
- * 1 MHz, 1e-6 at or below, reading C-A8), left-preconditioned (Eq. 11), one
+ * 1 MHz, 1e-6 at or below, reading C-A8), preconditioned on the right (reading
+ * R15; the left form of Eq. 11 selectable), one
  * Krylov space per right-hand side, all columns stepping together so every
  * operator call is batched.  CGS2 orthogonalisation; Hessenberg/Givens in FP64.
  * tol <= 0 selects the paper's frequency rule.  b, x: device complex64
@@ -317,6 +318,9 @@ typedef struct {
     int32_t restart;
     int32_t max_iters;
     double tol;
+    int32_t right_precond;  /* 1: right (A M^-1 u = b, x = M^-1 u: GMRES minimises and tests the true
+                               residual; used when opts is NULL, reading R15); 0: left,
+                               the form of Eq. 11 (tests the preconditioned residual) */
 } xrl_gmres_opts;
 xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b, void* x, int32_t nrhs, const xrl_gmres_opts* opts,
                      int32_t* iters, double* rre, double* true_rre, int32_t* converged);

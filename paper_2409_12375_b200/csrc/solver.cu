@@ -323,6 +323,12 @@ __global__ void k_gscale(int64_t nl, int nrhs, const float2* __restrict__ a, int
 }
 
 // out = a - b
+__global__ void k_gaxpy(int64_t cnt, const float2* __restrict__ a, float2* __restrict__ x)  // x += a
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < cnt) { const float2 v = a[i]; x[i].x += v.x; x[i].y += v.y; }
+}
+
 __global__ void k_gsub(int64_t cnt, const float2* __restrict__ a, const float2* __restrict__ b, float2* __restrict__ out)
 {
     const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -610,6 +616,8 @@ xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_
     const int m = opts && opts->restart > 0 ? opts->restart : 50;
     const int maxit = opts && opts->max_iters > 0 ? opts->max_iters : 2000;
     double tol = opts ? opts->tol : 0;
+    // right preconditioning (A M^-1 u = b, x = M^-1 u; default when opts is NULL, reading R15)
+    const bool right = pc && (!opts || opts->right_precond);
     if (!(tol > 0)) tol = op->freq > 1e6 ? 1e-4 : 1e-6;  // PAPER.md:152, reading C-A8
     if (tol >= 1) { set_error("xrl_gmres: tol must be < 1"); return XRL_EINVAL; }
     API_TRY
@@ -641,11 +649,15 @@ xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_
             out.resize(nrhs);
             for (int r = 0; r < nrhs; ++r) out[r] = std::sqrt(std::max(h[r].x, 0.0));
         };
-        // reference: ||M^-1 b|| (preconditioned RRE) and ||b||
+        // reference: ||M^-1 b|| (left: preconditioned RRE) or ||b|| (right / none)
         std::vector<double> bnorm, pbnorm;
         norms(b, bnorm);
-        Mx(b, tmp.p);
-        norms(tmp.p, pbnorm);
+        if (right) {
+            pbnorm = bnorm;
+        } else {
+            Mx(b, tmp.p);
+            norms(tmp.p, pbnorm);
+        }
         std::vector<int> iters(nrhs, 0), conv(nrhs, 0);
         std::vector<double> rre(nrhs, 1.0);
         for (int r = 0; r < nrhs; ++r)
@@ -655,12 +667,13 @@ xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_
             bool all = true;
             for (int r = 0; r < nrhs; ++r) all = all && conv[r];
             if (all) break;
-            // r0 = M^-1 (b - A x)
+            // r0 = M^-1 (b - A x) (left) or b - A x (right)
             xrl_status s = op_apply(op, x, w.p, nrhs);
             if (s) return s;
             k_gsub<<<nblk(nrhs * nl, 256), 256, 0, st>>>(nrhs * nl, b, w.p, tmp.p);
             XRL_LAUNCH_CHECK();
-            Mx(tmp.p, w.p);
+            if (right) XRL_CUDA(cudaMemcpyAsync(w.p, tmp.p, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
+            else Mx(tmp.p, w.p);
             std::vector<double> beta;
             norms(w.p, beta);
             std::vector<double> sc(nrhs);
@@ -680,14 +693,21 @@ xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_
                 bool any = false;
                 for (int r = 0; r < nrhs; ++r) any = any || active[r];
                 if (!any) break;
-                // w = M^-1 A v_j  (batched over the columns)
+                // w = M^-1 A v_j (left) or A M^-1 v_j (right), batched over the columns
                 k_gscale<<<nblk(nl, 256), 256, 0, st>>>(nl, nrhs, V.p + (int64_t)j * nl, (int64_t)(m + 1) * nl,
                                                         ones.p, tmp.p, nl);
                 XRL_LAUNCH_CHECK();
-                s = op_apply(op, tmp.p, w.p, nrhs);
-                if (s) return s;
-                Mx(w.p, tmp.p);
-                XRL_CUDA(cudaMemcpyAsync(w.p, tmp.p, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
+                if (right) {
+                    Mx(tmp.p, w.p);
+                    s = op_apply(op, w.p, tmp.p, nrhs);
+                    if (s) return s;
+                    XRL_CUDA(cudaMemcpyAsync(w.p, tmp.p, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
+                } else {
+                    s = op_apply(op, tmp.p, w.p, nrhs);
+                    if (s) return s;
+                    Mx(w.p, tmp.p);
+                    XRL_CUDA(cudaMemcpyAsync(w.p, tmp.p, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
+                }
                 // CGS2
                 std::vector<std::vector<cd>> hcol(nrhs, std::vector<cd>(j + 2, 0.0));
                 for (int pass = 0; pass < 2; ++pass) {
@@ -753,8 +773,17 @@ xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_
                 for (int r = 0; r < nrhs; ++r)
                     for (int i = 0; i < jmax; ++i) hy2[(size_t)r * jmax + i] = hy[(size_t)r * m + i];
                 XRL_CUDA(cudaMemcpyAsync(dy.p, hy2.data(), 16 * hy2.size(), cudaMemcpyHostToDevice, st));
-                k_gupdate<<<nblk(nl, 256), 256, 0, st>>>(nl, m + 1, nrhs, V.p, dy.p, jmax, 1.f, x);
-                XRL_LAUNCH_CHECK();
+                if (right) {  // x += M^-1 (V y)
+                    XRL_CUDA(cudaMemsetAsync(tmp.p, 0, 8 * nrhs * nl, st));
+                    k_gupdate<<<nblk(nl, 256), 256, 0, st>>>(nl, m + 1, nrhs, V.p, dy.p, jmax, 1.f, tmp.p);
+                    XRL_LAUNCH_CHECK();
+                    Mx(tmp.p, w.p);
+                    k_gaxpy<<<nblk(nrhs * nl, 256), 256, 0, st>>>(nrhs * nl, w.p, x);
+                    XRL_LAUNCH_CHECK();
+                } else {
+                    k_gupdate<<<nblk(nl, 256), 256, 0, st>>>(nl, m + 1, nrhs, V.p, dy.p, jmax, 1.f, x);
+                    XRL_LAUNCH_CHECK();
+                }
                 XRL_CUDA(cudaStreamSynchronize(st));
             }
             if (j == 0) break;

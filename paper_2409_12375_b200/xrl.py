@@ -78,7 +78,8 @@ class TopoInfo(ctypes.Structure):
 
 
 class GmresOpts(ctypes.Structure):
-    _fields_ = [("restart", ctypes.c_int32), ("max_iters", ctypes.c_int32), ("tol", ctypes.c_double)]
+    _fields_ = [("restart", ctypes.c_int32), ("max_iters", ctypes.c_int32), ("tol", ctypes.c_double),
+                ("right_precond", ctypes.c_int32)]
 
 
 _lib = None
@@ -557,8 +558,9 @@ class Precond:
             pass
 
 
-def gmres(op: Operator, pc, b, x=None, restart=50, max_iters=2000, tol=0.0):
-    """xrl_gmres: returns (x, report dict).  tol <= 0 uses PAPER.md:152's rule."""
+def gmres(op: Operator, pc, b, x=None, restart=50, max_iters=2000, tol=0.0, right=True):
+    """xrl_gmres: returns (x, report dict).  tol <= 0 uses PAPER.md:152's rule; right=False selects
+    the left-preconditioned form of Eq. 11 (reading R15)."""
     import torch
     x = torch.zeros_like(b) if x is None else x
     nrhs = b.shape[0]
@@ -567,14 +569,14 @@ def gmres(op: Operator, pc, b, x=None, restart=50, max_iters=2000, tol=0.0):
     trre = np.zeros(nrhs)
     conv = np.zeros(nrhs, np.int32)
     st = lib().xrl_gmres(op.h, pc.h if pc is not None else None, _ptr(b), _ptr(x), nrhs,
-                         ctypes.byref(GmresOpts(restart, max_iters, tol)), _ptr(iters), _ptr(rre), _ptr(trre),
+                         ctypes.byref(GmresOpts(restart, max_iters, tol, int(right))), _ptr(iters), _ptr(rre), _ptr(trre),
                          _ptr(conv))
     check(st)
     return x, {"iters": iters, "rre": rre, "true_rre": trre, "converged": conv.astype(bool), "status": st}
 
 
 def extract(tree: Tree, near: Near, topo: Topology, freqs, zs=None, sigma=5.8e7, zeta=1e-4, block_size=64,
-            restart=50, max_iters=2000, tol=0.0):
+            restart=50, max_iters=2000, tol=0.0, right=True):
     """xrl_extract: R/L sweep.  Returns dict with z [n_freq][P][P] complex, r, l [n_freq][P][P],
     iters, true_rre [n_freq][P] and the status (XRL_ENOCONV is reported, not raised)."""
     freqs = np.ascontiguousarray(freqs, np.float64)
@@ -589,7 +591,7 @@ def extract(tree: Tree, near: Near, topo: Topology, freqs, zs=None, sigma=5.8e7,
         zz = np.broadcast_to(np.asarray(zs, dtype=np.complex128), (tree.n,))
         zsa = np.ascontiguousarray(np.stack([zz.real, zz.imag], axis=1))
     st = lib().xrl_extract(tree.h, near.h, topo.h, _ptr(zsa) if zsa is not None else None, sigma, zeta, nf,
-                           _ptr(freqs), block_size, ctypes.byref(GmresOpts(restart, max_iters, tol)), _ptr(z),
+                           _ptr(freqs), block_size, ctypes.byref(GmresOpts(restart, max_iters, tol, int(right))), _ptr(z),
                            _ptr(r), _ptr(l_), _ptr(it), _ptr(tr))
     if st < 0:
         check(st)
