@@ -12,11 +12,10 @@
 //   k_near_spmv  near correction CSR x (side stream)               (HBM)
 //   k_p2p        U-list direct sum, packed f32x2 (side stream)     (FP32 pipe)
 //   k_p2m        leaf multipoles mu = sum q Rt(u)                   (per leaf)
-//   k_m2m        child -> parent, per level (bottom-up)
-//   k_mu_img     mu[k][r] -> FP32 r-major image for the tensor-core M2L
+//   (M2M)        child -> parent per level on the tensor-core translation kernel (k_m2l_tc)
 //   k_m2l_tc     V-list translations on tcgen05 (3xTF32, warp-specialised)
 //   k_p2l        X-list particle -> local
-//   k_l2l        parent -> child, per level (top-down)
+//   (L2L)        parent -> child per level on k_m2l_tc
 //   k_ell_kmajor leaves' ell[r][k] -> ellk[k][8]
 //   k_l2p        per target panel: L2P
 //   k_m2p        W-list M2P (leaves with a W list), completes y
@@ -92,83 +91,17 @@ __global__ void __launch_bounds__(128) k_p2m(const int32_t* __restrict__ leaves,
         }
         __syncthreads();
     }
-    float* out = mu + (size_t)b * kBoxStride;
-    if (k < kNC) {
+    float* out = mu + (size_t)b * kMuStride;  // mu[r][k], k >= 121 zero
 #pragma unroll
-        for (int r = 0; r < 6; ++r) out[6 * k + r] = acc[r];
-    } else if (k < kNC + 2) {
-        out[kNC * 6 + (k - kNC)] = 0.f;  // padding floats 726, 727
-    }
+    for (int r = 0; r < 6; ++r) out[r * 128 + k] = k < kNC ? acc[r] : 0.f;
 }
 
-// ------------------------------------------------------------------ M2M / L2L
-// One CTA per output box; op layout [oct][k][kNCP] (i contiguous).
+// degree n of real coefficient index i = n*n + j
 __device__ __forceinline__ int degree_of(int i)
 {
     int n = 0;
     while ((n + 1) * (n + 1) <= i) ++n;
     return n;
-}
-
-__global__ void __launch_bounds__(128) k_m2m(const int32_t* __restrict__ parents, const int32_t* __restrict__ child,
-                                             const int32_t* __restrict__ nchild, const int32_t* __restrict__ ix,
-                                             const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
-                                             const float* __restrict__ op, float* __restrict__ mu)
-{
-    __shared__ float src[kBoxStride];
-    const int b = parents[blockIdx.x];
-    const int c0 = child[b], nc = nchild[b];
-    const int i = threadIdx.x;
-    const int kmax = (i < kNC) ? (degree_of(i) + 1) * (degree_of(i) + 1) : 0;
-    float acc[6] = {0, 0, 0, 0, 0, 0};
-    for (int c = c0; c < c0 + nc; ++c) {
-        __syncthreads();
-        for (int j = threadIdx.x; j < kBoxStride / 4; j += blockDim.x)
-            reinterpret_cast<float4*>(src)[j] = reinterpret_cast<const float4*>(mu + (size_t)c * kBoxStride)[j];
-        __syncthreads();
-        const int oct = (ix[c] & 1) | ((iy[c] & 1) << 1) | ((iz[c] & 1) << 2);
-        const float* T = op + (size_t)oct * kNC * kNCP;
-        for (int k = 0; k < kmax; ++k) {
-            const float t = T[k * kNCP + i];
-#pragma unroll
-            for (int r = 0; r < 6; ++r) acc[r] += t * src[6 * k + r];
-        }
-    }
-    if (i < kNC) {
-        float* out = mu + (size_t)b * kBoxStride + 6 * i;
-#pragma unroll
-        for (int r = 0; r < 6; ++r) out[r] = acc[r];
-    } else if (i == kNC) {
-        mu[(size_t)b * kBoxStride + 726] = 0.f;
-        mu[(size_t)b * kBoxStride + 727] = 0.f;
-    }
-}
-
-__global__ void __launch_bounds__(128) k_l2l(const int32_t* __restrict__ boxes, const int32_t* __restrict__ parent,
-                                             const int32_t* __restrict__ ix, const int32_t* __restrict__ iy,
-                                             const int32_t* __restrict__ iz, const float* __restrict__ op,
-                                             float* __restrict__ ell)
-{
-    __shared__ float src[kEllStride];  // parent ell[r][k]
-    const int b = boxes[blockIdx.x];
-    const int P = parent[b];
-    for (int j = threadIdx.x; j < kEllStride / 4; j += blockDim.x)
-        reinterpret_cast<float4*>(src)[j] = reinterpret_cast<const float4*>(ell + (size_t)P * kEllStride)[j];
-    __syncthreads();
-    const int i = threadIdx.x;
-    if (i >= kNC) return;
-    const int oct = (ix[b] & 1) | ((iy[b] & 1) << 1) | ((iz[b] & 1) << 2);
-    const float* T = op + (size_t)oct * kNC * kNCP;
-    const int n = degree_of(i);
-    float acc[6] = {0, 0, 0, 0, 0, 0};
-    for (int k = n * n; k < kNC; ++k) {
-        const float t = T[k * kNCP + i];
-#pragma unroll
-        for (int r = 0; r < 6; ++r) acc[r] += t * src[r * 128 + k];
-    }
-    float* out = ell + (size_t)b * kEllStride + i;
-#pragma unroll
-    for (int r = 0; r < 6; ++r) out[r * 128] += acc[r];
 }
 
 // ------------------------------------------------------------------ M2L on tcgen05
@@ -195,18 +128,7 @@ constexpr int kTcThreads = 288;                     // 4 loader + 4 drain + 1 MM
 constexpr int kTcOpBytes = 128 * 128 * 4;           // one operator part (hi or lo): 64 KB
 constexpr int kTcStageLd = 132;                     // drain stage row stride (floats; conflict-free STS.128)
 constexpr int kTcSmem = 2 * kTcOpBytes + 128 * kTcStageLd * 4 + 1024;  // operator hi + lo, drain stage (+ align)
-constexpr int kImgFloats = 6 * 128;                 // per box: r-major FP32 multipole image
 constexpr uint32_t kTcColAh = 0, kTcColAl = 128, kTcColD = 256;  // D buffers at 256 and 384
-
-// img[b][r][k] = mu[b][k][r] for k < 121, 0 for 121 <= k < 128.
-__global__ void k_mu_img(int nbox, const float* __restrict__ mu, float* __restrict__ img)
-{
-    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one per (box, r, k)
-    if (e >= (int64_t)nbox * kImgFloats) return;
-    const int b = (int)(e / kImgFloats), w = (int)(e % kImgFloats);
-    const int r = w >> 7, k = w & 127;
-    img[e] = k < kNC ? mu[(size_t)b * kBoxStride + 6 * k + r] : 0.f;
-}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar)
 {
@@ -323,7 +245,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
         const uint32_t ta = tm + ((uint32_t)(32 * warp) << 16);
         auto row_of = [&](const int4& tl, bool ok) -> const float* {
             if (!ok || !lane_ok || p >= tl.z || (dbg & 2)) return nullptr;
-            return bimg + (size_t)__ldg(srcb + tl.y + p) * kImgFloats + r * 128;
+            return bimg + (size_t)__ldg(srcb + tl.y + p) * kMuStride + r * 128;
         };
         float x[64];
         auto load_half = [&](const float* row, int h) {
@@ -1185,17 +1107,15 @@ __global__ void __launch_bounds__(128) k_m2p(const int2* __restrict__ wpairs, in
     const int lw = level[w];
     const float3 cw = box_center(lw, ix[w], iy[w], iz[w]);
     const float inv_sw = ldexpf(1.f, lw);
-    const float2* M = reinterpret_cast<const float2*>(mu + (size_t)w * kBoxStride);
+    const float* M = mu + (size_t)w * kMuStride;  // mu[r][k]
     for (int i = pb[b] + threadIdx.x; i < pe[b]; i += blockDim.x) {
         const float4 tp = loc[i];
         float a[6] = {0, 0, 0, 0, 0, 0};
         irregular_harmonics_visit<kP>((tp.x + cb.x - cw.x) * inv_sw, (tp.y + cb.y - cw.y) * inv_sw,
                                       (tp.z + cb.z - cw.z) * inv_sw, c_tab, [&](int k, float v) {
             const float hk = (degree_of(k) * degree_of(k) == k) ? v : 2.f * v;
-            const float2 m0 = __ldg(M + 3 * k), m1 = __ldg(M + 3 * k + 1), m2 = __ldg(M + 3 * k + 2);
-            a[0] = fmaf(m0.x, hk, a[0]); a[1] = fmaf(m0.y, hk, a[1]);
-            a[2] = fmaf(m1.x, hk, a[2]); a[3] = fmaf(m1.y, hk, a[3]);
-            a[4] = fmaf(m2.x, hk, a[4]); a[5] = fmaf(m2.y, hk, a[5]);
+#pragma unroll
+            for (int r = 0; r < 6; ++r) a[r] = fmaf(__ldg(M + r * 128 + k), hk, a[r]);
         });
         const float sc = inv_sw * invW;
         const int64_t li = i - p0;
@@ -1225,16 +1145,6 @@ const HostOperators& host_ops()
     return ops;
 }
 
-void upload_padded(DBuf<float>& dst, const std::vector<double>& src, int nmat)
-{
-    std::vector<float> h((size_t)nmat * kNC * kNCP, 0.f);
-    for (int m = 0; m < nmat; ++m)
-        for (int i = 0; i < kNC; ++i)
-            for (int k = 0; k < kNC; ++k)
-                h[(size_t)m * kNC * kNCP + (size_t)k * kNCP + i] = (float)src[(size_t)m * kNC * kNC + (size_t)i * kNC + k];
-    dst.alloc(h.size());
-    XRL_CUDA(cudaMemcpy(dst.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
-}
 
 float tf32_host(float x)
 {
@@ -1250,14 +1160,18 @@ float tf32_host(float x)
 // T[i][k] (i, k < 121, zero padded to 128) in the tcgen05 canonical K-major
 // (no swizzle) layout of a 128 (N = i) x 128 (K = k) B operand: element (i, k)
 // at float ((i/8)*32 + k/4)*32 + (i%8)*4 + k%4 of its part; [offset][hi|lo][16384].
-void upload_tc_images(DBuf<float>& dst, const std::vector<double>& src)
+void upload_tc_images(DBuf<float>& dst, const HostOperators& ops)
 {
     const size_t img = 128 * 128;
-    std::vector<float> h((size_t)kNM2L * 2 * img, 0.f);
-    for (int m = 0; m < kNM2L; ++m)
+    std::vector<float> h((size_t)kNOpImg * 2 * img, 0.f);
+    for (int m = 0; m < kNOpImg; ++m)
         for (int i = 0; i < kNC; ++i)
             for (int k = 0; k < kNC; ++k) {
-                const float a = (float)src[(size_t)m * kNC * kNC + (size_t)i * kNC + k];
+                // images 0..315 M2L offsets, 316..323 M2M octants, 324..331 L2L octants (T[i][k], FP64)
+                const double* T = m < kOpM2M ? &ops.m2l[(size_t)m * kNC * kNC]
+                                : m < kOpL2L ? &ops.m2m[(size_t)(m - kOpM2M) * kNC * kNC]
+                                             : &ops.l2l[(size_t)(m - kOpL2L) * kNC * kNC];
+                const float a = (float)T[(size_t)i * kNC + k];
                 const float hi = tf32_host(a);
                 const size_t e = ((size_t)(i / 8) * 32 + k / 4) * 32 + (i % 8) * 4 + k % 4;
                 h[(size_t)m * 2 * img + e] = hi;
@@ -1277,9 +1191,7 @@ void upload_constants(xrl_ctx ctx)
     fill_recurrence_tables(tab);
     XRL_CUDA(cudaMemcpyToSymbol(c_tab, &tab, sizeof(tab)));
     const HostOperators& ops = host_ops();
-    upload_padded(ctx->ops.m2m, ops.m2m, 8);
-    upload_padded(ctx->ops.l2l, ops.l2l, 8);
-    upload_tc_images(ctx->ops.m2l_tc, ops.m2l);
+    upload_tc_images(ctx->ops.m2l_tc, ops);
     XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
     XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
@@ -1288,6 +1200,19 @@ void upload_constants(xrl_ctx ctx)
 }
 
 }  // namespace xrl
+
+// One level of M2M or L2L on the tensor-core translation kernel: blocks lvl = (first, count) of the
+// tree's tr_* tile lists; src/dst are r-major expansion arrays (disjoint boxes of two levels).
+static void translate_level(xrl_tree t, std::pair<int, int> lvl, const float* src, float* dst, cudaStream_t st)
+{
+    if (lvl.second <= 0) return;
+    xrl_ctx ctx = t->ctx;
+    const int grid = std::min(ctx->num_sms, lvl.second);
+    k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->tr_blocks.p + lvl.first, lvl.second, t->tr_tiles.p, t->tr_tgt.p,
+                                                t->tr_src.p, ctx->ops.m2l_tc.p, src, dst, 0);
+    XRL_LAUNCH_CHECK();
+    ctx->launches += 1;
+}
 
 // x: full (gathered) triple [3][n]; y: owned slice [3][n_local] of panels [p0, p1).
 static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags)
@@ -1358,20 +1283,14 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
 
     if (do_far && t->nlevel > 1) {
         phase_begin(ctx, PH_P2M, &ev, st);
+        XRL_CUDA(cudaMemsetAsync(t->mu.p, 0, t->mu.bytes(), st));  // parents accumulate the M2M reductions
         k_p2m<<<t->nleaf, 128, kP2MSmem, st>>>(t->leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p, t->xq.p, t->mu.p);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
         phase_end(ctx, PH_P2M, ev, st);
 
         phase_begin(ctx, PH_M2M, &ev, st);
-        for (int l = t->nlevel - 2; l >= 2; --l) {
-            const int np = t->par_start[l + 1] - t->par_start[l];
-            if (np == 0) continue;
-            k_m2m<<<np, 128, 0, st>>>(t->parents.p + t->par_start[l], t->bchild.p, t->bnchild.p, t->bix.p, t->biy.p,
-                                      t->biz.p, ctx->ops.m2m.p, t->mu.p);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
-        }
+        for (int l = t->nlevel - 2; l >= 2; --l) translate_level(t, t->m2m_lvl[l], t->mu.p, t->mu.p, st);
         phase_end(ctx, PH_M2M, ev, st);
 
         XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), st));
@@ -1379,12 +1298,8 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         phase_begin(ctx, PH_M2L, &ev, st);
         if (t->n_m2l_tiles > 0) {
             const int grid = std::min(ctx->num_sms, t->n_m2l_blocks);
-            if (t->mu_img.n < (size_t)t->nbox * kImgFloats) t->mu_img.alloc((size_t)t->nbox * kImgFloats);
-            k_mu_img<<<nblk((int64_t)t->nbox * kImgFloats, 256), 256, 0, st>>>(t->nbox, t->mu.p, t->mu_img.p);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
             k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p, t->m2l_tgt.p,
-                                                        t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu_img.p, t->ell.p, m2l_dbg);
+                                                        t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu.p, t->ell.p, m2l_dbg);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -1401,14 +1316,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         phase_end(ctx, PH_P2L, ev, st);
 
         phase_begin(ctx, PH_L2L, &ev, st);
-        for (int l = 3; l < t->nlevel; ++l) {
-            const int b0 = t->l2l_start[l], nb = t->l2l_start[l + 1] - b0;
-            if (nb == 0) continue;
-            k_l2l<<<nb, 128, 0, st>>>(t->l2l_boxes.p + b0, t->bparent.p, t->bix.p, t->biy.p, t->biz.p, ctx->ops.l2l.p,
-                                      t->ell.p);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
-        }
+        for (int l = 3; l < t->nlevel; ++l) translate_level(t, t->l2l_lvl[l], t->ell.p, t->ell.p, st);
         phase_end(ctx, PH_L2L, ev, st);
     }
     // join, then the local-expansion / W-list evaluation completes y

@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 
 #include "xrl_internal.h"
@@ -880,6 +881,66 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         T->l2l_boxes.alloc(std::max<size_t>(1, l2l.size()));
         if (!l2l.empty()) XRL_CUDA(cudaMemcpyAsync(T->l2l_boxes.p, l2l.data(), 4 * l2l.size(), cudaMemcpyHostToDevice, st));
         XRL_CUDA(cudaStreamSynchronize(st));
+        // M2M and L2L as tensor-core translation tiles (the M2L kernel, operators 316.. in the image table):
+        // per level, (target, source, octant operator) pairs sorted by (operator, target), tiles of <= 21
+        // pairs of one operator, blocks of <= 16 tiles.  M2M: parent <- child (all boxes, every rank);
+        // L2L: child <- parent (relevant boxes of levels >= 3).
+        std::vector<int32_t> hx(nbox), hy(nbox), hz(nbox), hpar(nbox), hch(nbox), hnc(nbox);
+        XRL_CUDA(cudaMemcpyAsync(hx.data(), T->bix.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaMemcpyAsync(hy.data(), T->biy.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaMemcpyAsync(hz.data(), T->biz.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaMemcpyAsync(hpar.data(), T->bparent.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaMemcpyAsync(hch.data(), T->bchild.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaMemcpyAsync(hnc.data(), T->bnchild.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        auto oct = [&](int b) { return (hx[b] & 1) | ((hy[b] & 1) << 1) | ((hz[b] & 1) << 2); };
+        std::vector<int4> tiles, blocks;
+        std::vector<int32_t> ptgt, psrc;
+        auto emit_level = [&](std::vector<std::array<int, 3>>& pr) {  // (op, target, source)
+            std::sort(pr.begin(), pr.end());
+            const int first_block = (int)blocks.size();
+            size_t i = 0;
+            while (i < pr.size()) {
+                size_t j = i;
+                while (j < pr.size() && pr[j][0] == pr[i][0]) ++j;
+                for (size_t s0 = i; s0 < j; s0 += 21) {
+                    if (s0 == i || blocks.back().y == 16) blocks.push_back(make_int4((int)tiles.size(), 0, pr[i][0], 0));
+                    const int cnt = (int)std::min<size_t>(21, j - s0);
+                    tiles.push_back(make_int4(pr[i][0], (int)ptgt.size(), cnt, 0));
+                    for (int q = 0; q < cnt; ++q) { ptgt.push_back(pr[s0 + q][1]); psrc.push_back(pr[s0 + q][2]); }
+                    blocks.back().y += 1;
+                }
+                i = j;
+            }
+            return std::make_pair(first_block, (int)blocks.size() - first_block);
+        };
+        T->m2m_lvl.assign(nlev, {0, 0});
+        T->l2l_lvl.assign(nlev, {0, 0});
+        for (int l = nlev - 2; l >= 2; --l) {  // parents at level l
+            std::vector<std::array<int, 3>> pr;
+            for (int b = T->lvl_start[l]; b < T->lvl_start[l + 1]; ++b)
+                for (int c = hch[b]; hch[b] >= 0 && c < hch[b] + hnc[b]; ++c) pr.push_back({kOpM2M + oct(c), b, c});
+            T->m2m_lvl[l] = emit_level(pr);
+        }
+        for (int l = 3; l < nlev; ++l) {  // children at level l
+            std::vector<std::array<int, 3>> pr;
+            for (int q = T->l2l_start[l]; q < T->l2l_start[l + 1]; ++q) {
+                const int c = l2l[q];
+                pr.push_back({kOpL2L + oct(c), c, hpar[c]});
+            }
+            T->l2l_lvl[l] = emit_level(pr);
+        }
+        T->tr_tiles.alloc(std::max<size_t>(1, tiles.size()));
+        T->tr_blocks.alloc(std::max<size_t>(1, blocks.size()));
+        T->tr_tgt.alloc(std::max<size_t>(1, ptgt.size()));
+        T->tr_src.alloc(std::max<size_t>(1, psrc.size()));
+        if (!tiles.empty()) {
+            XRL_CUDA(cudaMemcpyAsync(T->tr_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
+            XRL_CUDA(cudaMemcpyAsync(T->tr_blocks.p, blocks.data(), sizeof(int4) * blocks.size(), cudaMemcpyHostToDevice, st));
+            XRL_CUDA(cudaMemcpyAsync(T->tr_tgt.p, ptgt.data(), 4 * ptgt.size(), cudaMemcpyHostToDevice, st));
+            XRL_CUDA(cudaMemcpyAsync(T->tr_src.p, psrc.data(), 4 * psrc.size(), cudaMemcpyHostToDevice, st));
+        }
+        XRL_CUDA(cudaStreamSynchronize(st));
     }
     // M2L pairs sorted by (offset, target)
     T->m2l_tgt.alloc(std::max<int64_t>(1, T->nv));
@@ -971,7 +1032,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         XRL_CUDA(cudaStreamSynchronize(st));
     }
     // MVM scratch
-    T->mu.alloc((size_t)nbox * kBoxStride);
+    T->mu.alloc((size_t)nbox * kMuStride);
     T->ell.alloc((size_t)nbox * kEllStride);
     T->xq.alloc((size_t)n * 8);
     XRL_CUDA(cudaMemsetAsync(T->mu.p, 0, T->mu.bytes(), st));

@@ -71,14 +71,12 @@ struct DBuf {
 enum Phase { PH_PACK = 0, PH_P2M, PH_M2M, PH_M2L, PH_P2L, PH_L2L, PH_L2P, PH_P2P, PH_NEAR, PH_COUNT };
 
 struct DeviceOperators {
-    DBuf<float> m2m;   // [8][kNC (k, input)][kNCP (i, output, padded)]
-    DBuf<float> l2l;   // [8][kNC][kNCP]
-    DBuf<float> m2l_tc;  // [316][2 (hi, lo)][128 x 128 tf32, tcgen05 canonical K-major layout]
+    DBuf<float> m2l_tc;  // [332: M2L 316, M2M 8, L2L 8][2 (hi, lo)][128 x 128 tf32, tcgen05 canonical K-major]
     int m2l_index[343];
 };
 
-constexpr int kNCP = 128;            // padded coefficient count
-constexpr int kBoxStride = 728;      // floats per box multipole mu[k][r] (121*6 padded to 16 B)
+constexpr int kMuStride = 768;       // floats per box multipole mu[r][k] (r-major, k padded to 128)
+constexpr int kOpM2M = 316, kOpL2L = 324, kNOpImg = 332;  // tensor-core operator images: M2L 0..315, M2M, L2L
 constexpr int kEllStride = 768;      // floats per box local expansion ell[r][k] (r-major, k padded to 128)
 constexpr int kEllKStride = 968;     // floats per leaf local expansion ellk[k][8] (k-major, for the L2P)
 
@@ -142,6 +140,10 @@ struct xrl_tree_s {
     int32_t n_m2l_tiles = 0;
     xrl::DBuf<int4> m2l_blocks;              // (first tile, #tiles, offset, chunk): runs of one operator
     int32_t n_m2l_blocks = 0;
+    // M2M / L2L translation tiles for the tensor-core kernel (all levels concatenated)
+    xrl::DBuf<int4> tr_tiles, tr_blocks;
+    xrl::DBuf<int32_t> tr_tgt, tr_src;
+    std::vector<std::pair<int, int>> m2m_lvl, l2l_lvl;  // per level: (first block, #blocks)
     int64_t n_m2l_subtiles = 0;
     // boxes with non-empty X list, leaves with non-empty W list
     xrl::DBuf<int32_t> x_targets;
@@ -171,10 +173,9 @@ struct xrl_tree_s {
     std::vector<double> h_vert;              // [nv][3]
     std::vector<int32_t> h_tri;              // [n][3]
     // MVM scratch
-    xrl::DBuf<float> mu;                     // [nbox][kBoxStride]  mu[k][r]
+    xrl::DBuf<float> mu;                     // [nbox][kMuStride]  mu[r][k]
     xrl::DBuf<float> ell;                    // [nbox][kEllStride] ell[r][k]
     xrl::DBuf<float> ellk;                   // [nbox][kEllKStride] ellk[k][8] (leaves, per MVM)
-    xrl::DBuf<float> mu_img;                 // tcgen05 M2L: per-box FP32 r-major images (3 KB)
     xrl::DBuf<float> xq;                     // [n][8] packed charges
     xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging
 };
