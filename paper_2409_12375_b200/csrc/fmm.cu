@@ -820,7 +820,8 @@ __global__ void __launch_bounds__(128) k_p2p(
 constexpr int kPtChunk = 64;                    // sources per chunk (one U leaf)
 constexpr int kPtSlots = 6;                     // shared-memory staging slots
 constexpr int kPtTSlots = 3;                    // TMEM G slots (128 columns each)
-constexpr int kPtThreads = 320;                 // 8 G + 1 producer + 1 MMA warps
+constexpr int kPtGW = 16;                       // G warps (4 per TMEM lane quarter)
+constexpr int kPtThreads = (kPtGW + 2) * 32;    // + 1 producer + 1 MMA warp
 constexpr uint32_t kPtColD = 384;               // two 16-column accumulators (tile parity)
 constexpr uint32_t kPtBytes = 3 * kPtChunk * 4 + 2 * kPtChunk * 32;  // positions + charge planes
 struct __align__(128) PtSlot {
@@ -829,6 +830,49 @@ struct __align__(128) PtSlot {
     float ux, uy, uz;                              // U leaf centre - target leaf centre
     int nvalid, flags;                             // flags: bit 0 last chunk, bit 1 own leaf (self pairs)
 };
+
+__device__ __forceinline__ void lds_v2_u64(const void* p, f2x& a, f2x& b)
+{
+    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"((unsigned)__cvta_generic_to_shared(p)));
+}
+
+// G for one thread's target and 16 sources (quarter hf of the chunk), TF32 hi/lo into TMEM columns col ..
+// (hi) and col + 64 .. (lo): per 2 sources 3 FADD2 + FMUL2 + 2 FFMA2 + 2 MUFU + 2 LOP3 + FADD2.
+template <bool kSelf, typename Slot>
+__device__ __forceinline__ void pt_g_half(const Slot& S, int hf, float ax, float ay, float az, uint32_t col)
+{
+    const f2x txx = pk2(ax, ax), tyy = pk2(ay, ay), tzz = pk2(az, az);
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {  // 8 sources per tcgen05.st
+        float gh[8], gl[8];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {  // 4 sources per 128-bit shared load
+            const int sidx = 16 * hf + 8 * g + 4 * e;
+            f2x x0, x1, y0, y1, z0, z1;
+            lds_v2_u64(&S.X[sidx], x0, x1);
+            lds_v2_u64(&S.Y[sidx], y0, y1);
+            lds_v2_u64(&S.Z[sidx], z0, z1);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const f2x dx = sub2(u ? x1 : x0, txx), dy = sub2(u ? y1 : y0, tyy), dz = sub2(u ? z1 : z0, tzz);
+                const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
+                float ra = rsqrt_ftz(r2.x), rb = rsqrt_ftz(r2.y);
+                if (kSelf) {
+                    ra = r2.x > 0.f ? ra : 0.f;
+                    rb = r2.y > 0.f ? rb : 0.f;
+                }
+                const float ha = __uint_as_float(__float_as_uint(ra) & 0xFFFFE000u);
+                const float hb = __uint_as_float(__float_as_uint(rb) & 0xFFFFE000u);
+                const int o = 4 * e + 2 * u;
+                gh[o] = ha; gh[o + 1] = hb;
+                const float2 l = upk2(sub2(pk2(ra, rb), pk2(ha, hb)));
+                gl[o] = l.x; gl[o + 1] = l.y;
+            }
+        }
+        tc::tmem_st8(col + 8 * g, gh);
+        tc::tmem_st8(col + 64 + 8 * g, gl);
+    }
+}
 
 // charges -> padded K-major B planes [hi | lo][npad / 4][8 rows][4 sources]: padded source i, RHS r < 6
 // at plane + (i/4)*32 + r*4 + i%4 (rows 6, 7 stay zero)
@@ -871,23 +915,23 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_p2p_tc(
             tc::mbar_init(&sfree[k], 1);
         }
         for (int k = 0; k < kPtTSlots; ++k) {
-            tc::mbar_init(&gfull[k], 8);
+            tc::mbar_init(&gfull[k], kPtGW);
             tc::mbar_init(&gfree[k], 1);
         }
         for (int k = 0; k < 2; ++k) {
             tc::mbar_init(&d_full[k], 1);
-            tc::mbar_init(&d_free[k], 8);
+            tc::mbar_init(&d_free[k], kPtGW);
         }
     }
-    if (warp == 9) tc::tmem_alloc<512>(&tbase);
+    if (warp == kPtGW + 1) tc::tmem_alloc<512>(&tbase);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
 
-    if (warp < 8) {
+    if (warp < kPtGW) {
         // ---------------- G warps: thread = target (TMEM lane), half of each chunk's sources
         const uint32_t tm = tbase;
-        const int qd = warp & 3, hf = warp >> 2;
+        const int qd = warp & 3, hf = warp >> 2;  // lane quarter, source quarter of the chunk
         const int ti = 32 * qd + lane;
         const uint32_t ta = tm + ((uint32_t)(32 * qd) << 16);
         int c = 0;
@@ -905,41 +949,13 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_p2p_tc(
                 tc::mbar_wait(&staged[k], (c / kPtSlots) & 1);
                 tc::mbar_wait(&gfree[tk], ((c / kPtTSlots) & 1) ^ 1);  // MMAs of chunk c - 3 done with TMEM slot tk
                 tc::fence_after();
-                const int flags = S.flags, nvalid = S.nvalid;
-                const bool self = (flags & 2) != 0;
+                const int flags = S.flags;
                 // target in the U leaf's frame: c_t - c_s = (t - Ud) - s
                 const float ax = tx - S.ux, ay = ty - S.uy, az = tz - S.uz;
-                const f2x txx = pk2(ax, ax), tyy = pk2(ay, ay), tzz = pk2(az, az);
-                const uint32_t col = (uint32_t)(tk * 128 + 32 * hf);
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {  // 8 sources per tcgen05.st
-                    float gh[8], gl[8];
-                    if (32 * hf + 8 * g < nvalid) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int sidx = 32 * hf + 8 * g + 2 * e;
-                            const f2x dx = sub2(ld_shared_u64(&S.X[sidx]), txx);
-                            const f2x dy = sub2(ld_shared_u64(&S.Y[sidx]), tyy);
-                            const f2x dz = sub2(ld_shared_u64(&S.Z[sidx]), tzz);
-                            const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
-                            float ra = rsqrt_ftz(r2.x), rb = rsqrt_ftz(r2.y);
-                            if (self) {
-                                ra = r2.x > 0.f ? ra : 0.f;
-                                rb = r2.y > 0.f ? rb : 0.f;
-                            }
-                            const float ha = __uint_as_float(__float_as_uint(ra) & 0xFFFFE000u);
-                            const float hb = __uint_as_float(__float_as_uint(rb) & 0xFFFFE000u);
-                            gh[2 * e] = ha; gh[2 * e + 1] = hb;
-                            const float2 l = upk2(sub2(pk2(ra, rb), pk2(ha, hb)));
-                            gl[2 * e] = l.x; gl[2 * e + 1] = l.y;
-                        }
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) gh[e] = gl[e] = 0.f;
-                    }
-                    tc::tmem_st8(ta + col + 8 * g, gh);
-                    tc::tmem_st8(ta + col + 64 + 8 * g, gl);
-                }
+                const uint32_t col = ta + (uint32_t)(tk * 128 + 16 * hf);
+                // padding sources of the chunk are far away with zero charge: no per-source masking
+                if (flags & 2) pt_g_half<true>(S, hf, ax, ay, az, col);
+                else pt_g_half<false>(S, hf, ax, ay, az, col);
                 tc::tmem_st_wait();
                 tc::fence_before();
                 __syncwarp();
@@ -969,7 +985,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_p2p_tc(
                 y[2 * n + kk] = make_float2(tot[4], tot[5]);
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == kPtGW) {
         // ---------------- producer: one chunk = 64 padded sources of one U leaf, bulk copies
         if (lane == 0) {
             int c = 0;
@@ -1039,7 +1055,7 @@ __global__ void __launch_bounds__(kPtThreads, 1) k_p2p_tc(
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 9) tc::tmem_dealloc<512>(tbase);
+    if (warp == kPtGW + 1) tc::tmem_dealloc<512>(tbase);
 }
 
 // ell[r][k] (r-major, M2L/L2L layout) -> ellk[k][8] (k-major, 6 RHS + 2 pad) for the leaves: the L2P
