@@ -509,44 +509,60 @@ __device__ __forceinline__ void ldg256_l1(const float* p, float* v)
                  : "l"(p));
 }
 
-__global__ void __launch_bounds__(256) k_near_spmv(int64_t n, int64_t r0, const int64_t* __restrict__ ptr,
+// One row's 8-lane share of the near SpMV with global gathers: lane loads kNearU (col, value) pairs, then
+// issues their kNearU 32-byte charge gathers with the next batch's pairs loaded behind them.
+template <int kNearU>
+__device__ __forceinline__ void near_row_global(int64_t j0, int64_t e, const int2* __restrict__ cv,
+                                                const float* __restrict__ xq, float* a)
+{
+    constexpr int kL = 8;
+    // software pipeline: the next batch's (col, val) loads are in flight while this batch's gathers land
+    int2 c[kNearU];
+#pragma unroll
+    for (int u = 0; u < kNearU; ++u) {
+        const int64_t j = j0 + (int64_t)u * kL;
+        c[u] = j < e ? __ldcs(cv + j) : make_int2(-1, 0);
+    }
+    while (j0 < e) {
+        float q[kNearU][8];
+#pragma unroll
+        for (int u = 0; u < kNearU; ++u) {
+            if (c[u].x >= 0) {
+                ldg256_l1(xq + 8 * (int64_t)c[u].x, q[u]);  // the whole 32-byte charge record, one request
+            } else {
+#pragma unroll
+                for (int r = 0; r < 8; ++r) q[u][r] = 0.f;
+            }
+        }
+        float v[kNearU];
+#pragma unroll
+        for (int u = 0; u < kNearU; ++u) v[u] = __int_as_float(c[u].y);
+        j0 += kL * kNearU;
+#pragma unroll
+        for (int u = 0; u < kNearU; ++u) {
+            const int64_t j = j0 + (int64_t)u * kL;
+            c[u] = j < e ? __ldcs(cv + j) : make_int2(-1, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kNearU; ++u)
+#pragma unroll
+            for (int r = 0; r < 6; ++r) a[r] = fmaf(v[u], q[u][r], a[r]);
+    }
+}
+
+__global__ void __launch_bounds__(256, 6) k_near_spmv(int64_t n, int64_t r0, const int64_t* __restrict__ ptr,
                                                    const int2* __restrict__ cv, const float* __restrict__ xq,
                                                    int accumulate, float2* __restrict__ y)
 {
-    // rows r0 .. r0+n-1 (owned range); y local [3][n].  8 lanes per row, each lane keeps
-    // kNearU (col, val) loads and then kNearU gathers in flight (memory-level parallelism).
+    // rows r0 .. r0+n-1 (owned range); y local [3][n].  8 lanes per row, each lane keeps kNearU gathers
+    // in flight with the next kNearU (col, val) loads issued behind them (memory-level parallelism;
+    // 6 CTAs of 256 per SM leave 40 registers for the two batches).
     constexpr int kL = 8, kNearU = 4;
     const int64_t lrow = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kL;
     const int64_t row = r0 + lrow;
     const int lane = threadIdx.x & (kL - 1);
     float a[6] = {0, 0, 0, 0, 0, 0};
-    if (lrow < n) {
-        const int64_t e = ptr[row + 1];
-        for (int64_t j0 = ptr[row] + lane; j0 < e; j0 += kL * kNearU) {
-            int2 c[kNearU];
-#pragma unroll
-            for (int u = 0; u < kNearU; ++u) {
-                const int64_t j = j0 + (int64_t)u * kL;
-                c[u] = j < e ? __ldcs(cv + j) : make_int2(-1, 0);
-            }
-            float q[kNearU][8];
-#pragma unroll
-            for (int u = 0; u < kNearU; ++u) {
-                if (c[u].x >= 0) {
-                    ldg256_l1(xq + 8 * (int64_t)c[u].x, q[u]);  // the whole 32-byte charge record, one request
-                } else {
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) q[u][r] = 0.f;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kNearU; ++u) {
-                const float v = __int_as_float(c[u].y);
-#pragma unroll
-                for (int r = 0; r < 6; ++r) a[r] = fmaf(v, q[u][r], a[r]);
-            }
-        }
-    }
+    if (lrow < n) near_row_global<kNearU>(ptr[row] + lane, ptr[row + 1], cv, xq, a);
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
 #pragma unroll
@@ -1286,8 +1302,9 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         }
         if (do_near) {
             phase_begin(ctx, PH_NEAR, &ev, side);
-            if (nl > 0) k_near_spmv<<<nblk(8 * nl, 256), 256, 0, side>>>(nl, p0, nr->row_ptr.p, nr->cv.p, t->xq.p,
-                                                                         do_far ? 1 : 0, y);
+            if (nl > 0)
+                k_near_spmv<<<nblk(8 * nl, 256), 256, 0, side>>>(nl, p0, nr->row_ptr.p, nr->cv.p, t->xq.p,
+                                                                 do_far ? 1 : 0, y);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
             phase_end(ctx, PH_NEAR, ev, side);

@@ -3,7 +3,7 @@
 # usage: tools/gpu_quick.sh <tag>
 T=${1:-quick}
 O=gpurun_out/$T
-mkdir -p $O
+rm -rf $O; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build rc=$?" >> $O/status.txt
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; rc=$?; echo "smoke rc=$rc" >> $O/status.txt
 if [ $rc = 0 ]; then
