@@ -415,7 +415,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["xrl", "reference"], default="xrl")
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--leaf", type=int, default=512)  # tuned for config 4
+    ap.add_argument("--leaf", type=int, default=352)  # tuned for config 4
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gmres-iters", type=int, default=20, help="GMRES iteration-time probe (N=1); 0 = off")
     ap.add_argument("--gmres-solve", type=int, default=0, help="also solve to tolerance with this iteration cap")

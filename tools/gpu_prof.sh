@@ -1,10 +1,10 @@
 #!/bin/bash
 # Isolated phase times (XRL_SERIAL=1 bench) + ncu --set full of selected kernels.
-# usage: KERNELS="k_m2l_tc|k_p2p" LEAF=512 tools/gpu_prof.sh <tag>
+# usage: KERNELS="k_m2l_tc|k_p2p" LEAF=352 tools/gpu_prof.sh <tag>
 T=${1:-prof}
 O=gpurun_out/$T
 mkdir -p $O
-L=${LEAF:-512}
+L=${LEAF:-352}
 K=${KERNELS:-k_m2l_tc|k_p2p}
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build rc=$?" >> $O/status.txt
 XRL_SERIAL=1 timeout 600 python bench.py --steps 10 --warmup 3 --leaf $L --no-cpu-baseline --gmres-iters 0 > $O/bench_serial.log 2>&1; echo "bench serial rc=$?" >> $O/status.txt
