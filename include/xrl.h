@@ -296,7 +296,16 @@ void xrl_operator_destroy(xrl_op op);
  * (<= 64), each diagonal block LU-inverted in FP64 and stored complex64.
  * XRL_ESINGULAR if a pivot falls below 1e-13 of the block's largest entry. */
 xrl_status xrl_precond_build(xrl_op op, int32_t block_size, xrl_precond* out);
-/* z = blockdiag(Q)^-1 v; device complex64 [nrhs][n_loops]. */
+/* Exact diagonal-of-P preconditioner: the same Q, factorised
+ * whole, as Eq. 11 applies it (where Pardiso factorises Q once
+ * per frequency).  Q is assembled on the host in FP64 complex, ordered by nested
+ * dissection (METIS; else approximate minimum degree) and factorised by a host
+ * sparse LU with partial pivoting (cuSOLVER low-level csrlu, loaded at run time);
+ * xrl_precond_apply then copies v to the host, solves, and copies z back
+ * (synchronous).  XRL_EINVAL if cuSOLVER cannot be loaded or n_loops >= 2^31,
+ * XRL_ESINGULAR on a zero pivot.  xrl_precond_export rejects this kind. */
+xrl_status xrl_precond_build_exact(xrl_op op, xrl_precond* out);
+/* z = blockdiag(Q)^-1 v (exact kind: Q^-1 v); device complex64 [nrhs][n_loops]. */
 xrl_status xrl_precond_apply(xrl_precond pc, const void* v, void* z, int32_t nrhs);
 /* Host export of the block partition and the inverse blocks (tests):
  * block_ptr int32 [n_blocks+1] (loop ranges), inv complex64 [n_blocks][bs][bs]
@@ -334,7 +343,8 @@ xrl_status xrl_port_currents(xrl_topo topo, const void* x, int32_t nrhs, double*
 
 /* R/L extraction sweep (PAPER.md:152 solves the loop system at every frequency
  * point and reports R and L).  For each freqs[j] > 0: the operator (xrl_operator_create with zs,
- * sigma, zeta), the block diagonal-of-P preconditioner (block_size, <= 64), one GMRES (opts; NULL =
+ * sigma, zeta), the diagonal-of-P preconditioner (block-Jacobi with block_size <= 64, 0 = 64; the
+ * exact Q^-1 of xrl_precond_build_exact if block_size < 0), one GMRES (opts; NULL =
  * restart 50, the paper's tolerance rule) with the n_ports unit-voltage port excitations as batched
  * right-hand sides, the port currents give the admittance Y[:, q] = I(port q excited), and
  * Z = Y^-1 (FP64), R = Re Z, L = Im Z / (2 pi f).  Host outputs, each may be NULL:

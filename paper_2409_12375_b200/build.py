@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
                   "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["abi.cu", "tree.cu", "near.cu", "fmm.cu", "solver.cu", "comm.cu", "operators.cpp", "topology.cpp",
-           "extract.cpp"]
+           "extract.cpp", "precond_exact.cpp"]
 
 
 def _nccl_dirs():
@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 print(f"--- {os.path.basename(o)}\n{log}")
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fopenmp", "-o", LIB + ".tmp"] + objs + [
-            "-lcudart", "-L" + NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + NCCL_LIB]
+            "-lcudart", "-ldl", "-L" + NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + NCCL_LIB]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -1,7 +1,8 @@
 // xrl_extract: the R/L extraction sweep, host orchestration over the C-ABI.
 //
 // For each frequency f ("solve ... at each frequency point"): the loop-space operator
-// (Eq. 8-9, xrl_operator_create), the block diagonal-of-P preconditioner (Eq. 10, xrl_precond_build),
+// (Eq. 8-9, xrl_operator_create), the diagonal-of-P preconditioner (Eq. 10: xrl_precond_build, or the
+// exact Q^-1 of xrl_precond_build_exact when block_size < 0),
 // one preconditioned GMRES with the n_ports port excitations batched as right-hand sides
 // (xrl_port_rhs, xrl_gmres), the port currents (xrl_port_currents) give the admittance
 // Y[:, q] = I(unit volts on port q); Z = Y^-1 (FP64 Gauss-Jordan, partial pivoting),
@@ -72,7 +73,7 @@ extern "C" xrl_status xrl_extract(xrl_tree tree, xrl_near near, xrl_topo topo, c
         xrl_op op = nullptr;
         xrl_precond pc = nullptr;
         xrl_status s = xrl_operator_create(tree, near, topo, zs, sigma, zeta, freqs[j], &op);
-        if (s == XRL_OK) s = xrl_precond_build(op, block_size > 0 ? block_size : 64, &pc);
+        if (s == XRL_OK) s = block_size < 0 ? xrl_precond_build_exact(op, &pc) : xrl_precond_build(op, block_size > 0 ? block_size : 64, &pc);
         for (int q = 0; q < np && s == XRL_OK; ++q) s = xrl_port_rhs(topo, q, 1.0, (char*)b + (size_t)q * nl * 8);
         if (s == XRL_OK && cudaMemset(x, 0, (size_t)np * nl * 8) != cudaSuccess) s = XRL_ECUDA;
         if (s == XRL_OK || s == XRL_ENOCONV) {

@@ -389,8 +389,29 @@ static xrl_status op_apply(xrl_op op, const float2* v, float2* w, int nrhs)
     return XRL_OK;
 }
 
+namespace xrl {
+void precond_diag(xrl_op op, std::vector<double2>& hd)
+{
+    xrl_tree t = op->tree;
+    cudaStream_t st = t->ctx->stream;
+    const int64_t n = t->n;
+    DBuf<double> pkk(n);
+    k_diag_p<<<nblk(n, 256), 256, 0, st>>>(n, op->near->row_ptr.p, op->near->col.p, op->near->val64.p, pkk.p);
+    XRL_LAUNCH_CHECK();
+    std::vector<double> hp(n);
+    XRL_CUDA(cudaMemcpyAsync(hp.data(), pkk.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    hd.resize(n);
+    for (int64_t i = 0; i < n; ++i) hd[i] = make_double2(op->zsa_h[2 * i], op->zsa_h[2 * i + 1] + op->alpha_im * hp[i]);
+}
+}  // namespace xrl
+
 static void pc_apply(xrl_precond pc, const float2* v, float2* z, int nrhs)
 {
+    if (pc->kind == 1) {
+        exact_apply(pc, v, z, nrhs);
+        return;
+    }
     xrl_tree t = pc->op->tree;
     const int nl = (int)pc->op->topo->n_loops;
     k_block_apply<<<pc->nblocks, kBS, 0, t->ctx->stream>>>(nl, nrhs, pc->bptr.p, pc->inv.p, v, z);
@@ -498,14 +519,8 @@ xrl_status xrl_precond_build(xrl_op op, int32_t block_size, xrl_precond* out)
         pc->bptr.alloc(pc->bptr_h.size());
         XRL_CUDA(cudaMemcpyAsync(pc->bptr.p, pc->bptr_h.data(), 4 * pc->bptr_h.size(), cudaMemcpyHostToDevice, st));
         // d_k = Z_s/A + j alpha P_kk
-        DBuf<double> pkk(n);
-        k_diag_p<<<nblk(n, 256), 256, 0, st>>>(n, op->near->row_ptr.p, op->near->col.p, op->near->val64.p, pkk.p);
-        XRL_LAUNCH_CHECK();
-        std::vector<double> hp(n);
-        XRL_CUDA(cudaMemcpyAsync(hp.data(), pkk.p, 8 * n, cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaStreamSynchronize(st));
-        std::vector<double2> hd(n);
-        for (int64_t i = 0; i < n; ++i) hd[i] = make_double2(op->zsa_h[2 * i], op->zsa_h[2 * i + 1] + op->alpha_im * hp[i]);
+        std::vector<double2> hd;
+        precond_diag(op, hd);
         DBuf<double2> dk(n);
         XRL_CUDA(cudaMemcpyAsync(dk.p, hd.data(), 16 * n, cudaMemcpyHostToDevice, st));
         pc->inv.alloc((size_t)pc->nblocks * kBS * kBS);
@@ -528,9 +543,28 @@ xrl_status xrl_precond_build(xrl_op op, int32_t block_size, xrl_precond* out)
     API_CATCH
 }
 
+xrl_status xrl_precond_build_exact(xrl_op op, xrl_precond* out)
+{
+    if (!op || !out) { set_error("xrl_precond_build_exact: null argument"); return XRL_EINVAL; }
+    *out = nullptr;
+    API_TRY
+        XRL_CUDA(cudaSetDevice(op->tree->ctx->device));
+        auto pc = std::make_unique<xrl_precond_s>();
+        pc->op = op;
+        pc->kind = 1;
+        pc->bs = 0;
+        const xrl_status s = exact_build(pc.get());
+        if (s != XRL_OK) return s;
+        ++op->topo->refs;
+        *out = pc.release();
+        return XRL_OK;
+    API_CATCH
+}
+
 void xrl_precond_destroy(xrl_precond pc)
 {
     if (!pc) return;
+    if (pc->kind == 1) exact_free(pc);
     --pc->op->topo->refs;
     delete pc;
 }
@@ -548,6 +582,7 @@ xrl_status xrl_precond_apply(xrl_precond pc, const void* v, void* z, int32_t nrh
 xrl_status xrl_precond_export(xrl_precond pc, int32_t* n_blocks, int32_t* block_size, int32_t* block_ptr, void* inv)
 {
     if (!pc) { set_error("xrl_precond_export: null handle"); return XRL_EINVAL; }
+    if (pc->kind != 0) { set_error("xrl_precond_export: not a block preconditioner"); return XRL_EINVAL; }
     API_TRY
         if (n_blocks) *n_blocks = pc->nblocks;
         if (block_size) *block_size = kBS;

@@ -232,6 +232,8 @@ struct xrl_op_s {
 
 struct xrl_precond_s {
     xrl_op op = nullptr;
+    int32_t kind = 0;                            // 0 block-Jacobi (k_block_*), 1 exact sparse LU (precond_exact.cpp)
+    void* exact = nullptr;                       // kind 1: factorisation state
     int32_t bs = 64, nblocks = 0;
     std::vector<int32_t> bptr_h;
     xrl::DBuf<int32_t> bptr;
@@ -239,6 +241,12 @@ struct xrl_precond_s {
 };
 
 namespace xrl {
+// diagonal-of-P preconditioner: d_k = Z_s,k/A_k + j alpha P_kk per panel (library order, FP64)
+void precond_diag(xrl_op op, std::vector<double2>& d);
+// exact Q^-1 (NEXT f2): build the factorisation into pc->exact, apply it, release it
+xrl_status exact_build(xrl_precond pc);
+void exact_apply(xrl_precond pc, const float2* v, float2* z, int nrhs);
+void exact_free(xrl_precond pc);
 // phase timing helpers (no-ops unless enabled)
 void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb, cudaStream_t st);
 void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb, cudaStream_t st);

@@ -28,7 +28,7 @@ EXPORTS = [
     "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_extract",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
-    "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
+    "xrl_precond_build_exact", "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
     "xrl_port_currents", "xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_gathered",
 ]
 
@@ -139,6 +139,7 @@ def lib():
         L.xrl_operator_destroy.argtypes = [P]
         L.xrl_operator_destroy.restype = None
         L.xrl_precond_build.argtypes = [P, i32, pp]
+        L.xrl_precond_build_exact.argtypes = [P, pp]
         L.xrl_precond_apply.argtypes = [P, P, P, i32]
         L.xrl_precond_export.argtypes = [P, P, P, P, P]
         L.xrl_precond_destroy.argtypes = [P]
@@ -152,7 +153,8 @@ def lib():
         for name in ("xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_gathered"):
             getattr(L, name).restype = ctypes.c_int32
         for name in ("xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_esi",
-                     "xrl_operator_create", "xrl_operator_apply", "xrl_precond_build", "xrl_precond_apply",
+                     "xrl_operator_create", "xrl_operator_apply", "xrl_precond_build", "xrl_precond_build_exact",
+                     "xrl_precond_apply",
                      "xrl_precond_export", "xrl_gmres", "xrl_port_rhs", "xrl_port_currents"):
             getattr(L, name).restype = ctypes.c_int32
         for name in ("xrl_ctx_create", "xrl_ctx_sync", "xrl_tree_build", "xrl_tree_info", "xrl_tree_perm",
@@ -524,12 +526,16 @@ class Operator:
 
 
 class Precond:
-    """xrl_precond_build: block-Jacobi diagonal-of-P preconditioner (Eq. 10)."""
+    """xrl_precond_build: block-Jacobi diagonal-of-P preconditioner (Eq. 10); exact=True:
+    xrl_precond_build_exact, the whole Q factorised (sparse LU, NEXT f2)."""
 
-    def __init__(self, op: Operator, block_size: int = 64):
+    def __init__(self, op: Operator, block_size: int = 64, exact: bool = False):
         self.op = op
         h = ctypes.c_void_p()
-        check(lib().xrl_precond_build(op.h, block_size, ctypes.byref(h)))
+        if exact:
+            check(lib().xrl_precond_build_exact(op.h, ctypes.byref(h)))
+        else:
+            check(lib().xrl_precond_build(op.h, block_size, ctypes.byref(h)))
         self.h = h
 
     def apply(self, v, z=None):
@@ -576,9 +582,12 @@ def gmres(op: Operator, pc, b, x=None, restart=50, max_iters=2000, tol=0.0, righ
 
 
 def extract(tree: Tree, near: Near, topo: Topology, freqs, zs=None, sigma=5.8e7, zeta=1e-4, block_size=64,
-            restart=50, max_iters=2000, tol=0.0, right=True):
+            restart=50, max_iters=2000, tol=0.0, right=True, exact=False):
     """xrl_extract: R/L sweep.  Returns dict with z [n_freq][P][P] complex, r, l [n_freq][P][P],
-    iters, true_rre [n_freq][P] and the status (XRL_ENOCONV is reported, not raised)."""
+    iters, true_rre [n_freq][P] and the status (XRL_ENOCONV is reported, not raised).  exact=True uses
+    the exact Q^-1 (xrl_precond_build_exact) instead of the block-Jacobi form."""
+    if exact:
+        block_size = -1
     freqs = np.ascontiguousarray(freqs, np.float64)
     nf, npt = freqs.size, topo.info()["n_ports"]
     z = np.zeros((nf, npt, npt, 2))

@@ -221,6 +221,11 @@ def test_extract_dc_bar_matches_single_solve(bar_all):
     # with a frequency-independent Z_s the partial inductance does not depend on f
     assert abs(res["l"][1, 0, 0] - res["l"][0, 0, 0]) / res["l"][0, 0, 0] < 1e-4
     assert np.all(res["true_rre"] < 1e-5)
+    # the same sweep with the exact Q^-1 (NEXT f2): same Z, a handful of iterations
+    rex = xrl.extract(tree, near, topo, [1e3, 2e3], zs=rdc, exact=True)
+    assert rex["status"] == 0, rex
+    assert abs(rex["z"][0, 0, 0] - Zo[0, 0]) / abs(Zo[0, 0]) < 1e-4
+    assert np.all(rex["iters"] <= 10) and np.all(rex["iters"] < res["iters"])
 
 
 def test_extract_coils_sweep_physics():
@@ -272,3 +277,56 @@ def test_gmres_right_vs_left_preconditioning(bar_all):
     assert rr["iters"][0] < rl["iters"][0] and rr["iters"][0] < r0["iters"][0]
     zr, zl = 1 / topo.port_currents(xr)[0, 0], 1 / topo.port_currents(xl)[0, 0]
     assert abs(zr - zl) / abs(zl) < 1e-4
+
+
+def test_precond_exact_apply_vs_oracle(bar_all):
+    """NEXT f2: the exact diag-of-P preconditioner applies Q^-1 of Eq. 10: against
+    the oracle's Q solved as one block (a dense FP64 solve), and Q (Q^-1 v) = v."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo, g, P = bar_all
+    freq = 1e8
+    op = xrl.Operator(tree, near, topo, freq, sigma=SIGMA, zeta=ZETA)
+    pc = xrl.Precond(op, exact=True)
+    ex = topo.export()
+    M, C = _oracle_C(m, g, ex)
+    nl = M.shape[0]
+    rng = np.random.default_rng(6)
+    v = (rng.random((2, nl)) - 0.5 + 1j * (rng.random((2, nl)) - 0.5)).astype(np.complex64)
+    z = pc.apply(torch.from_numpy(v).cuda()).cpu().numpy()
+    zs = lo.esi(SIGMA, ZETA, freq)
+    alpha = 1j * 2 * np.pi * freq * lo.MU0 / (4 * np.pi)
+    zref = lo.precond_apply(C, zs / g.area, alpha, np.diag(P), np.array([0, nl]), v.astype(np.complex128))
+    err = oracle.rel_l2(z, zref)
+    print("exact precond rel L2", err)
+    assert err <= 1e-5
+    with pytest.raises(xrl.XrlError):
+        pc.export()
+
+
+def test_gmres_exact_vs_block_precond_coils():
+    """Table IV's comparison on the coil pair (config 2, 2 ports, 100 MHz): GMRES with the exact Q^-1
+    needs no more iterations than with the block-Jacobi approximation, and both give the same port
+    impedance."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m = meshes.coils()
+    ctx, tree, near = cuda_setup(m)
+    topo = xrl.Topology(tree, [(p, q) for _, p, q in m.ports])
+    f = 1e8
+    op = xrl.Operator(tree, near, topo, f, sigma=SIGMA, zeta=5e-6)
+    nl = topo.n_loops
+    b = torch.zeros((2, nl), dtype=torch.complex64, device="cuda")
+    for p in range(2):
+        topo.port_rhs(p, 1.0, out=b[p:p + 1])
+    zs = {}
+    iters = {}
+    for kind in ("block", "exact"):
+        pc = xrl.Precond(op, 64, exact=(kind == "exact"))
+        x, rep = xrl.gmres(op, pc, b)
+        assert rep["converged"].all() and np.all(rep["true_rre"] < 1e-3)
+        zs[kind] = np.linalg.inv(topo.port_currents(x).T)
+        iters[kind] = int(rep["iters"].max())
+    print("coils 100 MHz iterations", iters)
+    assert iters["exact"] <= iters["block"]
+    assert np.abs(zs["exact"] - zs["block"]).max() / np.abs(zs["block"]).max() < 1e-3
