@@ -37,7 +37,7 @@ def _nccl_dirs():
 
 NCCL_INC, NCCL_LIB = _nccl_dirs()
 CUFLAGS = CUFLAGS + ["-I" + NCCL_INC]
-HEADERS = ["xrl_internal.h", "harmonics.h", "operators.h"]
+HEADERS = ["xrl_internal.h", "harmonics.h", "operators.h", "tcgen05.h"]
 
 
 def _stale(obj, src):

@@ -183,9 +183,10 @@ __device__ __forceinline__ bool elect_one()
 // Round-to-nearest (ties away) to TF32, as cvt.rna.tf32.f32.
 __device__ __forceinline__ float tf32_rna(float x)
 {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
+    // round to nearest, ties away from zero, to the 10 explicit mantissa bits TF32 keeps; on the bit
+    // pattern (sign-magnitude) this is one add and one mask.  Same result as cvt.rna.tf32.f32 for finite
+    // x, which ptxas expands with a non-finite test and a branch on sm_100a.
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 }  // namespace tc
