@@ -589,7 +589,8 @@ __global__ void __launch_bounds__(256, 6) k_near_spmv(int64_t n, int64_t r0, con
 // groups.  Only the target's own leaf needs the r = 0 (self) guard.
 // y += (1/W) sum_{l != k} x_l / r_kl.
 constexpr int kUWin = 64;
-constexpr int kSrcChunk = 512;
+constexpr int kSrcChunk = 1024;
+constexpr int kP2PSmem = (kSrcChunk * 12 > 128 * (4 * 6 + 1) * 2 ? kSrcChunk * 12 : 128 * (4 * 6 + 1) * 2) * 4;
 constexpr int kTPT = 8;
 constexpr int kTP2 = kTPT / 2;  // packed target pairs per thread
 
@@ -693,8 +694,7 @@ __global__ void __launch_bounds__(128) k_p2p(
 {
     // n, p0: owned panel range [p0, p0+n), y local [3][n]
     // the source staging buffers and the final reduction share one buffer
-    constexpr int kStageF = kSrcChunk * 12, kRedF = 128 * (kTP2 * 6 + 1) * 2;
-    __shared__ __align__(16) float smraw[kStageF > kRedF ? kStageF : kRedF];
+    extern __shared__ __align__(16) float smraw[];  // kP2PSmem: source staging, then the reduction
     float4* Sp = reinterpret_cast<float4*>(smraw);
     float4(*Sq)[2] = reinterpret_cast<float4(*)[2]>(smraw + 4 * kSrcChunk);
     f2x(*Red)[kTP2 * 6 + 1] = reinterpret_cast<f2x(*)[kTP2 * 6 + 1]>(smraw);  // packed target pairs
@@ -1225,6 +1225,7 @@ void upload_constants(xrl_ctx ctx)
     const HostOperators& ops = host_ops();
     upload_tc_images(ctx->ops.m2l_tc, ops);
     XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+    XRL_CUDA(cudaFuncSetAttribute(k_p2p, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2PSmem));
     XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
@@ -1293,7 +1294,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
                     nl, p0, y);
             }
             else if (t->n_own_leaves > 0)
-                k_p2p<<<t->n_own_leaves, 128, 0, side>>>(t->own_leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
+                k_p2p<<<t->n_own_leaves, 128, kP2PSmem, side>>>(t->own_leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
                                                          t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
                                                          invW, 0, nl, p0, y);
             XRL_LAUNCH_CHECK();
