@@ -115,6 +115,63 @@ def voxel_surface(occ: np.ndarray, origin, h):
     return verts.astype(np.float64), tris.astype(np.int32)
 
 
+def voxel_quads(occ: np.ndarray, origin, h):
+    """As voxel_surface, but the boundary squares stay rectangles: (verts, quads [n,4], normals [n,3]),
+    each quad (a, b, c, d) in cyclic order with (b-a) x (d-a) along the outward normal."""
+    occ = np.asarray(occ, dtype=bool)
+    nx, ny, nz = occ.shape
+    pad = np.zeros((nx + 2, ny + 2, nz + 2), dtype=bool)
+    pad[1:-1, 1:-1, 1:-1] = occ
+
+    def nid(i, j, k):
+        return (i * (ny + 1) + j) * (nz + 1) + k
+
+    quads, normals = [], []
+    for axis in range(3):
+        for sgn in (+1, -1):
+            nb = np.roll(pad, shift=-sgn, axis=axis)[1:-1, 1:-1, 1:-1]
+            i, j, k = np.nonzero(occ & ~nb)
+            if i.size == 0:
+                continue
+            base = [i, j, k]
+            base[axis] = base[axis] + (1 if sgn > 0 else 0)
+            u, v = [a for a in range(3) if a != axis]
+            c1 = list(base); c1[u] = c1[u] + 1
+            c2 = list(base); c2[u] = c2[u] + 1; c2[v] = c2[v] + 1
+            c3 = list(base); c3[v] = c3[v] + 1
+            quads.append(np.stack([nid(*base), nid(*c1), nid(*c2), nid(*c3)], axis=1))
+            nrm = np.zeros((i.size, 3))
+            nrm[:, axis] = sgn
+            normals.append(nrm)
+    quads = np.concatenate(quads, axis=0)
+    normals = np.concatenate(normals, axis=0)
+    used, inv = np.unique(quads.reshape(-1), return_inverse=True)
+    quads = inv.reshape(-1, 4)
+    kk = used % (nz + 1)
+    jj = (used // (nz + 1)) % (ny + 1)
+    ii = used // ((nz + 1) * (ny + 1))
+    verts = np.stack([origin[0] + ii * h[0], origin[1] + jj * h[1], origin[2] + kk * h[2]], axis=1)
+    a, b, d = verts[quads[:, 0]], verts[quads[:, 1]], verts[quads[:, 3]]
+    flip = np.einsum("ij,ij->i", np.cross(b - a, d - a), normals) < 0
+    quads[flip] = quads[flip][:, [0, 3, 2, 1]]
+    return verts.astype(np.float64), quads.astype(np.int32), normals
+
+
+def bar_hybrid(length=1000 * UM, side=100 * UM, cell=20 * UM) -> Mesh:
+    """Config 1 geometry as a hybrid mesh (NEXT f4): the four long faces keep their
+    `cell` squares as rectangle panels, the two end caps are split into triangles.  panels int32 [n][4]
+    (-1 in the last column for triangles); N = 4 (L/c)(s/c) + 4 (s/c)^2 = 1,100 at the defaults."""
+    nx, ny = int(round(length / cell)), int(round(side / cell))
+    occ = np.ones((nx, ny, ny), dtype=bool)
+    v, q, nrm = voxel_quads(occ, (0.0, 0.0, 0.0), (cell, cell, cell))
+    cap = np.abs(nrm[:, 0]) > 0.5
+    tri = np.concatenate([q[cap][:, [0, 1, 2]], q[cap][:, [0, 2, 3]]], axis=0)  # same winding as the quad
+    panels = np.concatenate([q[~cap], np.concatenate([tri, np.full((tri.shape[0], 1), -1)], axis=1)])
+    m = Mesh(v, panels.astype(np.int32), name="bar_hybrid")
+    m.meta = {"rectangles": int((~cap).sum()), "triangles": int(tri.shape[0])}
+    return m
+
+
 def merge(parts):
     """Concatenate (verts, tris, cond) parts without merging vertices."""
     vs, ts, cs = [], [], []

@@ -39,12 +39,16 @@ def lib():
         L = ctypes.CDLL(_SO)
         P = ctypes.c_void_p
         i64, i32, f64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_double
-        L.orc_geometry.argtypes = [i64, P, P, P, P, P]
+        L.orc_geometry.argtypes = [i64, P, P, i32, P, P, P]
         L.orc_tri_potential.argtypes = [P, P, P, P]
         L.orc_tri_potential.restype = f64
-        L.orc_p_entries.argtypes = [i64, P, P, P, P, P, f64, i64, P, i64, P, P]
-        L.orc_mvm_rows.argtypes = [i64, P, P, P, P, P, f64, i32, P, i64, P, P, i32]
-        L.orc_near_rows.argtypes = [i64, P, P, P, P, P, f64, i64, P, P, P, P, P, P]
+        L.orc_p_entries.argtypes = [i64, P, P, i32, P, P, P, f64, i32, i64, P, i64, P, P]
+        L.orc_mvm_rows.argtypes = [i64, P, P, i32, P, P, P, f64, i32, i32, P, i64, P, P, i32]
+        L.orc_near_rows.argtypes = [i64, P, P, i32, P, P, P, f64, i32, i64, P, P, P, P, P, P]
+        L.orc_panel_potential_ext.argtypes = [P, P, P, i32, i64]
+        L.orc_panel_potential_ext.restype = f64
+        L.orc_outer_rule_ext.argtypes = [P, P, i32, i64, P, P]
+        L.orc_outer_rule_ext.restype = ctypes.c_int
         L.orc_tie_audit.argtypes = [i64, P, P, f64, f64]
         L.orc_tie_audit.restype = i64
         L.orc_num_threads.restype = ctypes.c_int
@@ -57,17 +61,24 @@ def _p(a):
 
 
 class Geometry:
-    """FP64 per-panel data (centroid, area, longest edge) of a triangle mesh."""
+    """FP64 per-panel data (centroid, area, diameter D) of a triangle or hybrid triangle/rectangle mesh.
+    panels: int32 [n][3] triangles, or [n][4] with -1 in the last column for triangles and a planar
+    parallelogram (a, b, c, d in cyclic order) otherwise.  galerkin: the near rule of SPEC.md:345
+    (outer quadrature on self and vertex-adjacent pairs) instead of centroid collocation."""
 
-    def __init__(self, verts, tris):
+    def __init__(self, verts, tris, galerkin=False):
         self.verts = np.ascontiguousarray(verts, dtype=np.float64)
         self.tris = np.ascontiguousarray(tris, dtype=np.int32)
         n = self.tris.shape[0]
         self.n = n
+        self.stride = self.tris.shape[1]
+        assert self.stride in (3, 4)
+        self.galerkin = int(bool(galerkin))
         self.cent = np.empty((n, 3))
         self.area = np.empty(n)
         self.dmax = np.empty(n)
-        lib().orc_geometry(n, _p(self.verts), _p(self.tris), _p(self.cent), _p(self.area), _p(self.dmax))
+        lib().orc_geometry(n, _p(self.verts), _p(self.tris), self.stride, _p(self.cent), _p(self.area),
+                           _p(self.dmax))
 
 
 def tri_potential(r, v0, v1, v2) -> float:
@@ -76,12 +87,26 @@ def tri_potential(r, v0, v1, v2) -> float:
     return lib().orc_tri_potential(*[_p(x) for x in a])
 
 
+def panel_potential(r, g: Geometry, k: int) -> float:
+    """I(r; S_k) for panel k of g (triangle, or rectangle as its two diagonal triangles)."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    return lib().orc_panel_potential_ext(_p(r), _p(g.verts), _p(g.tris), g.stride, int(k))
+
+
+def outer_rule(g: Geometry, k: int):
+    """The Galerkin outer quadrature of panel k: points [m,3], weights [m] (sum 1)."""
+    x = np.empty((7, 3))
+    w = np.empty(7)
+    m = lib().orc_outer_rule_ext(_p(g.verts), _p(g.tris), g.stride, int(k), _p(x), _p(w))
+    return x[:m], w[:m]
+
+
 def p_entries(g: Geometry, rows, cols, eta=ETA):
     rows = np.ascontiguousarray(rows, dtype=np.int64)
     cols = np.ascontiguousarray(cols, dtype=np.int64)
     out = np.empty((rows.size, cols.size))
-    lib().orc_p_entries(g.n, _p(g.verts), _p(g.tris), _p(g.cent), _p(g.area), _p(g.dmax), eta,
-                        rows.size, _p(rows), cols.size, _p(cols), _p(out))
+    lib().orc_p_entries(g.n, _p(g.verts), _p(g.tris), g.stride, _p(g.cent), _p(g.area), _p(g.dmax), eta,
+                        g.galerkin, rows.size, _p(rows), cols.size, _p(cols), _p(out))
     return out
 
 
@@ -100,8 +125,8 @@ def mvm_rows(g: Geometry, x, rows=None, eta=ETA, nthreads=0):
         rows = np.arange(g.n, dtype=np.int64)
     rows = np.ascontiguousarray(rows, dtype=np.int64)
     y = np.empty((nvec, rows.size), dtype=np.complex128)
-    lib().orc_mvm_rows(g.n, _p(g.verts), _p(g.tris), _p(g.cent), _p(g.area), _p(g.dmax), eta,
-                       nvec, _p(xd), rows.size, _p(rows), _p(y.view(np.float64)), int(nthreads))
+    lib().orc_mvm_rows(g.n, _p(g.verts), _p(g.tris), g.stride, _p(g.cent), _p(g.area), _p(g.dmax), eta,
+                       g.galerkin, nvec, _p(xd), rows.size, _p(rows), _p(y.view(np.float64)), int(nthreads))
     return y
 
 
@@ -114,15 +139,15 @@ def near_rows(g: Geometry, rows=None, eta=ETA):
     rows = np.ascontiguousarray(rows, dtype=np.int64)
     L = lib()
     cnt = np.empty(rows.size, dtype=np.int64)
-    L.orc_near_rows(g.n, _p(g.verts), _p(g.tris), _p(g.cent), _p(g.area), _p(g.dmax), eta,
-                    rows.size, _p(rows), _p(cnt), None, None, None, None)
+    L.orc_near_rows(g.n, _p(g.verts), _p(g.tris), g.stride, _p(g.cent), _p(g.area), _p(g.dmax), eta,
+                    g.galerkin, rows.size, _p(rows), _p(cnt), None, None, None, None)
     ptr = np.zeros(rows.size + 1, dtype=np.int64)
     np.cumsum(cnt, out=ptr[1:])
     cols = np.empty(ptr[-1], dtype=np.int64)
     vals = np.empty(ptr[-1])
     inv_r = np.empty(ptr[-1])
-    L.orc_near_rows(g.n, _p(g.verts), _p(g.tris), _p(g.cent), _p(g.area), _p(g.dmax), eta,
-                    rows.size, _p(rows), _p(cnt), _p(ptr), _p(cols), _p(vals), _p(inv_r))
+    L.orc_near_rows(g.n, _p(g.verts), _p(g.tris), g.stride, _p(g.cent), _p(g.area), _p(g.dmax), eta,
+                    g.galerkin, rows.size, _p(rows), _p(cnt), _p(ptr), _p(cols), _p(vals), _p(inv_r))
     return ptr, cols, vals, inv_r
 
 

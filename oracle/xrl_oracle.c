@@ -13,6 +13,10 @@
  *   P_kl = 1/2 [ I(c_k; T_l)/A_l + I(c_l; T_k)/A_k ]   if (k,l) near   (near)
  *   P_kl = 1 / |c_k - c_l|                             otherwise       (far)
  *   y_t[k] = sum_l P_kl x_t[l],   t = 1..3, re and im separately.
+ * Panels are triangles or rectangles (a rectangle's I is the sum
+ * over its two diagonal triangles).  Galerkin option (NEXT f4):
+ * self and vertex-adjacent pairs average I over an outer quadrature of the
+ * observation panel instead of taking it at the centroid.
  * with I(r;T) = \int_T dS'/|r - r'| (Eq. 1 kernel, PAPER.md:88
  * Eq. 6 second term with j*omega*mu0/4pi pulled out as PAPER.md:144 says;
  * PAPER.md:116 "P directly computed on centroids" = particle format).
@@ -31,16 +35,51 @@
 
 /* ---------------------------------------------------------------- geometry */
 
+/* Panels: pv[stride*k + 0..2] triangle vertex indices; with stride 4 and
+ * pv[4k+3] >= 0 the panel is a rectangle (a planar parallelogram a, b, c, d in
+ * cyclic order; "hybrid of triangles and
+ * rectangles"). */
+static int orc_is_quad(const int32_t *pv, int32_t stride, int64_t k)
+{
+    return stride == 4 && pv[4 * k + 3] >= 0;
+}
+
+static double orc_len(const double *e)
+{
+    return sqrt((e[0] * e[0] + e[1] * e[1]) + e[2] * e[2]);
+}
+
 /* Panel geometry, PAPER.md:56 (centroid = PEEC circuit node).
- * centroid = ((v0 + v1) + v2) / 3 in this order; area = |(v1-v0)x(v2-v0)|/2;
- * D = longest edge length. */
-void orc_geometry(int64_t nt, const double *vert, const int32_t *tri,
+ * Triangle: centroid = ((v0 + v1) + v2) / 3 in this order; area =
+ * |(v1-v0)x(v2-v0)|/2; D = longest edge length.
+ * Rectangle (parallelogram a b c d): centroid = intersection of the diagonals
+ * = (a + c) * 0.5; area = |(b-a)x(d-a)|; D = the longer diagonal
+ * (the panel's diameter; reading R16). */
+void orc_geometry(int64_t nt, const double *vert, const int32_t *pv, int32_t stride,
                   double *cent, double *area, double *dmax)
 {
     for (int64_t k = 0; k < nt; ++k) {
-        const double *a = vert + 3 * (int64_t)tri[3 * k + 0];
-        const double *b = vert + 3 * (int64_t)tri[3 * k + 1];
-        const double *c = vert + 3 * (int64_t)tri[3 * k + 2];
+        const double *a = vert + 3 * (int64_t)pv[stride * k + 0];
+        const double *b = vert + 3 * (int64_t)pv[stride * k + 1];
+        const double *c = vert + 3 * (int64_t)pv[stride * k + 2];
+        if (orc_is_quad(pv, stride, k)) {
+            const double *q = vert + 3 * (int64_t)pv[4 * k + 3];
+            double e1[3], e2[3], d1[3], d2[3];
+            for (int d = 0; d < 3; ++d) {
+                cent[3 * k + d] = (a[d] + c[d]) * 0.5;
+                e1[d] = b[d] - a[d];
+                e2[d] = q[d] - a[d];
+                d1[d] = c[d] - a[d];
+                d2[d] = q[d] - b[d];
+            }
+            double cx = e1[1] * e2[2] - e1[2] * e2[1];
+            double cy = e1[2] * e2[0] - e1[0] * e2[2];
+            double cz = e1[0] * e2[1] - e1[1] * e2[0];
+            area[k] = sqrt(cx * cx + cy * cy + cz * cz);
+            double l1 = orc_len(d1), l2 = orc_len(d2);
+            dmax[k] = l1 > l2 ? l1 : l2;
+            continue;
+        }
         for (int d = 0; d < 3; ++d) cent[3 * k + d] = ((a[d] + b[d]) + c[d]) / 3.0;
         double e1[3], e2[3], e3[3];
         for (int d = 0; d < 3; ++d) { e1[d] = b[d] - a[d]; e2[d] = c[d] - a[d]; e3[d] = c[d] - b[d]; }
@@ -48,9 +87,7 @@ void orc_geometry(int64_t nt, const double *vert, const int32_t *tri,
         double cy = e1[2] * e2[0] - e1[0] * e2[2];
         double cz = e1[0] * e2[1] - e1[1] * e2[0];
         area[k] = 0.5 * sqrt(cx * cx + cy * cy + cz * cz);
-        double l1 = sqrt((e1[0] * e1[0] + e1[1] * e1[1]) + e1[2] * e1[2]);
-        double l2 = sqrt((e2[0] * e2[0] + e2[1] * e2[1]) + e2[2] * e2[2]);
-        double l3 = sqrt((e3[0] * e3[0] + e3[1] * e3[1]) + e3[2] * e3[2]);
+        double l1 = orc_len(e1), l2 = orc_len(e2), l3 = orc_len(e3);
         double m = l1 > l2 ? l1 : l2;
         dmax[k] = m > l3 ? m : l3;
     }
@@ -118,6 +155,88 @@ double orc_tri_potential(const double *r, const double *v0, const double *v1, co
     return sum_log - ah * sum_atan;
 }
 
+/* I(r; S_k) for panel k: a triangle, or a rectangle as its two triangles
+ * (a, b, c) + (a, c, d) split on the diagonal ac (additivity of the integral). */
+static double orc_panel_potential(const double *r, const double *vert, const int32_t *pv, int32_t stride, int64_t k)
+{
+    const double *a = vert + 3 * (int64_t)pv[stride * k + 0];
+    const double *b = vert + 3 * (int64_t)pv[stride * k + 1];
+    const double *c = vert + 3 * (int64_t)pv[stride * k + 2];
+    double I = orc_tri_potential(r, a, b, c);
+    if (orc_is_quad(pv, stride, k)) I += orc_tri_potential(r, a, c, vert + 3 * (int64_t)pv[4 * k + 3]);
+    return I;
+}
+
+/* Outer quadrature over panel k for the Galerkin near rule:
+ * triangles: Radon's 7-point degree-5 rule (centroid weight 9/40; points
+ * (a, a, 1-2a) with a = (6 -+ sqrt 15)/21, weights (155 -+ sqrt 15)/1200);
+ * rectangles: the 2 x 2 Gauss product rule (points a + s (b-a) + t (d-a), s, t
+ * = (1 -+ 1/sqrt 3)/2, weights 1/4).  Weights sum to 1 (the mean over the
+ * panel).  Returns the number of points. */
+static int orc_outer_rule(const double *vert, const int32_t *pv, int32_t stride, int64_t k, double *x, double *w)
+{
+    const double *a = vert + 3 * (int64_t)pv[stride * k + 0];
+    const double *b = vert + 3 * (int64_t)pv[stride * k + 1];
+    const double *c = vert + 3 * (int64_t)pv[stride * k + 2];
+    if (orc_is_quad(pv, stride, k)) {
+        const double *q = vert + 3 * (int64_t)pv[4 * k + 3];
+        const double g[2] = {(1.0 - 1.0 / sqrt(3.0)) / 2.0, (1.0 + 1.0 / sqrt(3.0)) / 2.0};
+        int m = 0;
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j, ++m) {
+                for (int d = 0; d < 3; ++d) x[3 * m + d] = a[d] + g[i] * (b[d] - a[d]) + g[j] * (q[d] - a[d]);
+                w[m] = 0.25;
+            }
+        return 4;
+    }
+    const double s15 = sqrt(15.0);
+    const double al[2] = {(6.0 - s15) / 21.0, (6.0 + s15) / 21.0};
+    const double wt[2] = {(155.0 - s15) / 1200.0, (155.0 + s15) / 1200.0};
+    for (int d = 0; d < 3; ++d) x[d] = (a[d] + b[d] + c[d]) / 3.0;
+    w[0] = 9.0 / 40.0;
+    int m = 1;
+    for (int s = 0; s < 2; ++s)
+        for (int v = 0; v < 3; ++v, ++m) {
+            /* barycentric (1-2a) on vertex v, a on the other two */
+            const double *P[3] = {a, b, c};
+            for (int d = 0; d < 3; ++d)
+                x[3 * m + d] = (1.0 - 2.0 * al[s]) * P[v][d] + al[s] * P[(v + 1) % 3][d] + al[s] * P[(v + 2) % 3][d];
+            w[m] = wt[s];
+        }
+    return 7;
+}
+
+/* Panels k and l share a vertex index (edge- or vertex-adjacent). */
+static int orc_adjacent(const int32_t *pv, int32_t stride, int64_t k, int64_t l)
+{
+    int nk = orc_is_quad(pv, stride, k) ? 4 : 3, nl = orc_is_quad(pv, stride, l) ? 4 : 3;
+    for (int i = 0; i < nk; ++i)
+        for (int j = 0; j < nl; ++j)
+            if (pv[stride * k + i] == pv[stride * l + j]) return 1;
+    return 0;
+}
+
+/* (1/A_k) int_{S_k} I(r; S_l) dS / A_l by the outer rule of panel k. */
+static double orc_galerkin_term(const double *vert, const int32_t *pv, int32_t stride, const double *area,
+                                int64_t k, int64_t l)
+{
+    double x[3 * 7], w[7];
+    int m = orc_outer_rule(vert, pv, stride, k, x, w);
+    double s = 0.0;
+    for (int q = 0; q < m; ++q) s += w[q] * orc_panel_potential(x + 3 * q, vert, pv, stride, l);
+    return s / area[l];
+}
+
+/* Test access to the panel integral and the outer rule (pins). */
+double orc_panel_potential_ext(const double *r, const double *vert, const int32_t *pv, int32_t stride, int64_t k)
+{
+    return orc_panel_potential(r, vert, pv, stride, k);
+}
+int orc_outer_rule_ext(const double *vert, const int32_t *pv, int32_t stride, int64_t k, double *x, double *w)
+{
+    return orc_outer_rule(vert, pv, stride, k, x, w);
+}
+
 /* ------------------------------------------------------- near criterion */
 
 /* (k,l), k != l, is near iff d^2 < (eta * max(D_k, D_l))^2 with
@@ -131,20 +250,24 @@ static int orc_is_near(const double *ck, const double *cl, double Dk, double Dl,
     return d2 < t * t;
 }
 
-/* Entry P_kl of the discrete operator (definition C1 above). */
-static double orc_pkl(int64_t k, int64_t l, const double *vert, const int32_t *tri,
-                      const double *cent, const double *area, const double *dmax, double eta)
+/* Entry P_kl of the discrete operator (definition C1 above).  galerkin != 0:
+ * self and vertex-adjacent pairs use the outer quadrature of SPEC.md:345
+ * instead of the centroid (symmetrised the same way); other near pairs stay
+ * centroid-collocated (reading R17). */
+static double orc_pkl(int64_t k, int64_t l, const double *vert, const int32_t *pv, int32_t stride,
+                      const double *cent, const double *area, const double *dmax, double eta, int galerkin)
 {
     const double *ck = cent + 3 * k, *cl = cent + 3 * l;
     if (k == l) {
-        return orc_tri_potential(ck, vert + 3 * (int64_t)tri[3 * k], vert + 3 * (int64_t)tri[3 * k + 1],
-                                 vert + 3 * (int64_t)tri[3 * k + 2]) / area[k];
+        if (galerkin) return orc_galerkin_term(vert, pv, stride, area, k, k);
+        return orc_panel_potential(ck, vert, pv, stride, k) / area[k];
     }
     if (orc_is_near(ck, cl, dmax[k], dmax[l], eta)) {
-        double Ikl = orc_tri_potential(ck, vert + 3 * (int64_t)tri[3 * l], vert + 3 * (int64_t)tri[3 * l + 1],
-                                       vert + 3 * (int64_t)tri[3 * l + 2]) / area[l];
-        double Ilk = orc_tri_potential(cl, vert + 3 * (int64_t)tri[3 * k], vert + 3 * (int64_t)tri[3 * k + 1],
-                                       vert + 3 * (int64_t)tri[3 * k + 2]) / area[k];
+        if (galerkin && orc_adjacent(pv, stride, k, l))
+            return 0.5 * (orc_galerkin_term(vert, pv, stride, area, k, l) +
+                          orc_galerkin_term(vert, pv, stride, area, l, k));
+        double Ikl = orc_panel_potential(ck, vert, pv, stride, l) / area[l];
+        double Ilk = orc_panel_potential(cl, vert, pv, stride, k) / area[k];
         return 0.5 * (Ikl + Ilk);
     }
     double dx = ck[0] - cl[0], dy = ck[1] - cl[1], dz = ck[2] - cl[2];
@@ -152,22 +275,22 @@ static double orc_pkl(int64_t k, int64_t l, const double *vert, const int32_t *t
 }
 
 /* Dense entries P[rows[i], cols[j]] (small cases / symmetry checks). */
-void orc_p_entries(int64_t nt, const double *vert, const int32_t *tri, const double *cent,
-                   const double *area, const double *dmax, double eta,
+void orc_p_entries(int64_t nt, const double *vert, const int32_t *pv, int32_t stride, const double *cent,
+                   const double *area, const double *dmax, double eta, int32_t galerkin,
                    int64_t nr, const int64_t *rows, int64_t nc, const int64_t *cols, double *out)
 {
     (void)nt;
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < nr; ++i)
         for (int64_t j = 0; j < nc; ++j)
-            out[i * nc + j] = orc_pkl(rows[i], cols[j], vert, tri, cent, area, dmax, eta);
+            out[i * nc + j] = orc_pkl(rows[i], cols[j], vert, pv, stride, cent, area, dmax, eta, galerkin);
 }
 
 /* Direct O(N^2) sum on selected target rows.
  * x: [nvec][nt] complex as interleaved (re,im) doubles; y: [nvec][nr] same.
  * y[v][i] = sum_l P_{rows[i], l} x[v][l]   (C4; P real -> re, im separately) */
-void orc_mvm_rows(int64_t nt, const double *vert, const int32_t *tri, const double *cent,
-                  const double *area, const double *dmax, double eta,
+void orc_mvm_rows(int64_t nt, const double *vert, const int32_t *pv, int32_t stride, const double *cent,
+                  const double *area, const double *dmax, double eta, int32_t galerkin,
                   int32_t nvec, const double *x, int64_t nr, const int64_t *rows, double *y,
                   int32_t nthreads)
 {
@@ -184,7 +307,7 @@ void orc_mvm_rows(int64_t nt, const double *vert, const int32_t *tri, const doub
             int64_t k = rows[i];
             for (int v = 0; v < 2 * nvec; ++v) acc[v] = 0.0;
             for (int64_t l = 0; l < nt; ++l) {
-                double p = orc_pkl(k, l, vert, tri, cent, area, dmax, eta);
+                double p = orc_pkl(k, l, vert, pv, stride, cent, area, dmax, eta, galerkin);
                 for (int v = 0; v < nvec; ++v) {
                     acc[2 * v + 0] += p * x[2 * ((int64_t)v * nt + l) + 0];
                     acc[2 * v + 1] += p * x[2 * ((int64_t)v * nt + l) + 1];
@@ -203,8 +326,8 @@ void orc_mvm_rows(int64_t nt, const double *vert, const int32_t *tri, const doub
  * with (k,l) near or l == k, and the near entry value P_kl (symmetrised
  * integral, self term on the diagonal).  Pass cols/vals = NULL to get the
  * per-row counts only (cnt[i]); otherwise row i is written at offset off[i]. */
-void orc_near_rows(int64_t nt, const double *vert, const int32_t *tri, const double *cent,
-                   const double *area, const double *dmax, double eta,
+void orc_near_rows(int64_t nt, const double *vert, const int32_t *pv, int32_t stride, const double *cent,
+                   const double *area, const double *dmax, double eta, int32_t galerkin,
                    int64_t nr, const int64_t *rows, int64_t *cnt, const int64_t *off,
                    int64_t *cols, double *vals, double *inv_r)
 {
@@ -217,7 +340,7 @@ void orc_near_rows(int64_t nt, const double *vert, const int32_t *tri, const dou
             if (!near) continue;
             if (cols) {
                 cols[off[i] + c] = l;
-                vals[off[i] + c] = orc_pkl(k, l, vert, tri, cent, area, dmax, eta);
+                vals[off[i] + c] = orc_pkl(k, l, vert, pv, stride, cent, area, dmax, eta, galerkin);
                 if (inv_r) {
                     if (l == k) inv_r[off[i] + c] = 0.0;
                     else {
