@@ -120,6 +120,15 @@ xrl_status xrl_nccl_unique_id(void* out128);
  * lists.  Errors: XRL_EINVAL, XRL_EGEOM (zero area / bad index), XRL_ECUDA. */
 xrl_status xrl_tree_build(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_tri,
                           const int32_t* tri, const xrl_fmm_opts* opts, xrl_tree* out);
+/* Hybrid triangle/rectangle meshes ("the hybrid of triangles and
+ * rectangles"; NEXT f4): pv host int32 [n_panel][4], pv[k][3] = -1 for a
+ * triangle, else a rectangle = planar parallelogram (v0 v1 v2 v3 in cyclic
+ * order; XRL_EGEOM if v2 - v1 != v3 - v0 beyond 1e-9 of its diameter).  A
+ * rectangle's centroid is the intersection of its diagonals, its D the longer
+ * diagonal; the near integrals split it on the diagonal v0-v2.  Otherwise as
+ * xrl_tree_build (the loop-space topology accepts triangle meshes only). */
+xrl_status xrl_tree_build_poly(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_panel,
+                               const int32_t* pv, const xrl_fmm_opts* opts, xrl_tree* out);
 void xrl_tree_destroy(xrl_tree tree);
 
 typedef struct {
@@ -167,6 +176,10 @@ xrl_status xrl_tree_export(xrl_tree tree, int32_t* box_level, int32_t* box_ijk /
  * N_kk = P_kk; CSR in library order, columns ascending. */
 typedef struct {
     double eta;
+    int32_t galerkin; /* 0: centroid collocation (the default above); 1: the Galerkin near rule of
+                         SPEC.md:345 (NEXT f4) -- self and vertex-adjacent pairs take the mean of
+                         I(x; S_l)/A_l over the observation panel (Radon 7-point rule on triangles,
+                         2 x 2 Gauss on rectangles), symmetrised the same way; other near pairs unchanged */
 } xrl_near_opts;
 xrl_status xrl_near_assemble(xrl_tree tree, const xrl_near_opts* opts, xrl_near* out);
 void xrl_near_destroy(xrl_near near);

@@ -1,5 +1,8 @@
 // xrl_near_assemble: near-pair search over the octree and FP64 analytic
-// single-triangle integrals -> near-field CSR.
+// single-triangle integrals -> near-field CSR.  Rectangle panels
+// (hybrid meshes, NEXT f4) integrate as their two diagonal triangles; the optional
+// Galerkin rule averages the self and vertex-adjacent entries over an
+// outer quadrature of the observation panel (reading R17).
 //
 // the near-field matrix is filled directly on panel
 // centroids (O(N_p)), with the Eq. 6 kernel.  Near pairs follow
@@ -132,29 +135,99 @@ __global__ void k_interleave(int64_t nnz, const int32_t* __restrict__ col, const
     if (j < nnz) cv[j] = make_int2(col[j], __float_as_int(val[j]));
 }
 
+// Panel l (library order): a triangle, or a rectangle as its triangles (v0, v1, v2) + (v0, v2, v3) split
+// on the diagonal v0-v2 (the integral is additive; tverts' 4th vertex is NaN for triangles).
+struct Panel {
+    V3 v[4];
+    bool quad;
+};
+__device__ __forceinline__ Panel load_panel(const double* __restrict__ tverts, int64_t l)
+{
+    const double* t = tverts + 12 * l;
+    Panel P;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) P.v[i] = {t[3 * i], t[3 * i + 1], t[3 * i + 2]};
+    P.quad = !isnan(t[9]);
+    return P;
+}
+__device__ __forceinline__ double panel_potential(V3 r, const Panel& P)
+{
+    double I = tri_potential(r, P.v[0], P.v[1], P.v[2]);
+    if (P.quad) I += tri_potential(r, P.v[0], P.v[2], P.v[3]);
+    return I;
+}
+
+// Galerkin near rule (NEXT f4): the mean of I(x; S_l) over the observation panel k by an outer
+// quadrature -- Radon's 7-point degree-5 rule on a triangle (centroid weight 9/40; (a, a, 1 - 2a) with
+// a = (6 -+ sqrt 15)/21, weights (155 -+ sqrt 15)/1200), the 2 x 2 Gauss product rule on a rectangle.
+__device__ double galerkin_term(const Panel& K, const Panel& L)
+{
+    double s = 0.0;
+    if (K.quad) {
+        const double g[2] = {(1.0 - 1.0 / sqrt(3.0)) / 2.0, (1.0 + 1.0 / sqrt(3.0)) / 2.0};
+        const V3 e1 = sub(K.v[1], K.v[0]), e2 = sub(K.v[3], K.v[0]);
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) {
+                const V3 x = {K.v[0].x + g[i] * e1.x + g[j] * e2.x, K.v[0].y + g[i] * e1.y + g[j] * e2.y,
+                              K.v[0].z + g[i] * e1.z + g[j] * e2.z};
+                s += 0.25 * panel_potential(x, L);
+            }
+        return s;
+    }
+    const double s15 = sqrt(15.0);
+    const double al[2] = {(6.0 - s15) / 21.0, (6.0 + s15) / 21.0};
+    const double wt[2] = {(155.0 - s15) / 1200.0, (155.0 + s15) / 1200.0};
+    const V3 c = {(K.v[0].x + K.v[1].x + K.v[2].x) / 3.0, (K.v[0].y + K.v[1].y + K.v[2].y) / 3.0,
+                  (K.v[0].z + K.v[1].z + K.v[2].z) / 3.0};
+    s = 9.0 / 40.0 * panel_potential(c, L);
+    for (int q = 0; q < 2; ++q)
+        for (int v = 0; v < 3; ++v) {
+            const V3 A = K.v[v], B = K.v[(v + 1) % 3], C = K.v[(v + 2) % 3];
+            const double b0 = 1.0 - 2.0 * al[q];
+            const V3 x = {b0 * A.x + al[q] * B.x + al[q] * C.x, b0 * A.y + al[q] * B.y + al[q] * C.y,
+                          b0 * A.z + al[q] * B.z + al[q] * C.z};
+            s += wt[q] * panel_potential(x, L);
+        }
+    return s;
+}
+
+__device__ __forceinline__ bool share_vertex(int4 a, int4 b)
+{
+    const int va[4] = {a.x, a.y, a.z, a.w}, vb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (va[i] >= 0 && va[i] == vb[j]) return true;
+    return false;
+}
+
 __global__ void k_near_values(int64_t n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ cols,
                               const double* __restrict__ cent, const double* __restrict__ area,
-                              const double* __restrict__ tverts, float* val, double* val64)
+                              const double* __restrict__ tverts, const int4* __restrict__ pvid, int galerkin,
+                              float* val, double* val64)
 {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const double* tk = tverts + 9 * k;
+    const Panel K = load_panel(tverts, k);
     const V3 ck = {cent[3 * k], cent[3 * k + 1], cent[3 * k + 2]};
-    const V3 k0 = {tk[0], tk[1], tk[2]}, k1 = {tk[3], tk[4], tk[5]}, k2 = {tk[6], tk[7], tk[8]};
     const double Ak = area[k];
     for (int64_t j = ptr[k]; j < ptr[k + 1]; ++j) {
         const int64_t l = cols[j];
         double v64, v32;
         if (l == k) {
-            v64 = tri_potential(ck, k0, k1, k2) / Ak;
+            v64 = (galerkin ? galerkin_term(K, K) : panel_potential(ck, K)) / Ak;
             v32 = v64;
         } else {
-            const double* tl = tverts + 9 * l;
+            const Panel L = load_panel(tverts, l);
             const V3 cl = {cent[3 * l], cent[3 * l + 1], cent[3 * l + 2]};
-            const V3 l0 = {tl[0], tl[1], tl[2]}, l1 = {tl[3], tl[4], tl[5]}, l2 = {tl[6], tl[7], tl[8]};
-            const double Ikl = tri_potential(ck, l0, l1, l2) / area[l];
-            const double Ilk = tri_potential(cl, k0, k1, k2) / Ak;
-            v64 = 0.5 * (Ikl + Ilk);
+            if (galerkin && share_vertex(pvid[k], pvid[l])) {
+                v64 = 0.5 * (galerkin_term(K, L) / area[l] + galerkin_term(L, K) / Ak);
+            } else {
+                const double Ikl = panel_potential(ck, L) / area[l];
+                const double Ilk = panel_potential(cl, K) / Ak;
+                v64 = 0.5 * (Ikl + Ilk);
+            }
             v32 = v64 - 1.0 / norm(sub(ck, cl));
         }
         val[j] = (float)v32;
@@ -166,7 +239,7 @@ inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 }  // namespace
 
-static xrl_status near_impl(xrl_tree t, double eta, xrl_near* out)
+static xrl_status near_impl(xrl_tree t, double eta, int galerkin, xrl_near* out)
 {
     xrl_ctx ctx = t->ctx;
     cudaStream_t st = ctx->stream;
@@ -198,7 +271,7 @@ static xrl_status near_impl(xrl_tree t, double eta, xrl_near* out)
     k_near_search<true><<<nblk(n, 128), 128, 0, st>>>(n, tv, eta, nullptr, N->row_ptr.p, N->col.p, ovf.p);
     XRL_LAUNCH_CHECK();
     k_near_values<<<nblk(n, 64), 64, 0, st>>>(n, N->row_ptr.p, N->col.p, t->cent.p, t->area.p, t->tverts.p,
-                                              N->val.p, N->val64.p);
+                                              t->pvid.p, galerkin, N->val.p, N->val64.p);
     XRL_LAUNCH_CHECK();
     // interleaved (col, FP32 value) pairs for the SpMV: one 8-byte load per nonzero
     N->cv.alloc(std::max<int64_t>(1, N->nnz));
@@ -219,9 +292,11 @@ xrl_status xrl_near_assemble(xrl_tree t, const xrl_near_opts* opts, xrl_near* ou
     if (!t || !out) { set_error("xrl_near_assemble: null argument"); return XRL_EINVAL; }
     *out = nullptr;
     double eta = opts ? opts->eta : 1.5;
+    const int galerkin = opts ? opts->galerkin : 0;
     if (!(eta > 0)) { set_error("xrl_near_assemble: eta must be > 0"); return XRL_EINVAL; }
+    if (galerkin != 0 && galerkin != 1) { set_error("xrl_near_assemble: galerkin must be 0 or 1"); return XRL_EINVAL; }
     try {
-        return near_impl(t, eta, out);
+        return near_impl(t, eta, galerkin, out);
     } catch (const CudaError& e) {
         return e.code;
     } catch (const std::bad_alloc&) {

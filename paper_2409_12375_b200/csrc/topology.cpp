@@ -470,6 +470,10 @@ xrl_status xrl_topology_build(xrl_tree t, int32_t n_ports, const xrl_port* ports
 {
     if (!t || !out || n_ports < 0 || (n_ports > 0 && !ports)) { set_error("xrl_topology_build: bad argument"); return XRL_EINVAL; }
     *out = nullptr;
+    if (t->stride != 3) {
+        set_error("xrl_topology_build: hybrid (rectangle) meshes are supported by the MVM path only");
+        return XRL_EUNSUPPORTED;
+    }
     try {
         return topo_impl(t, n_ports, ports, out);
     } catch (const CudaError& e) {

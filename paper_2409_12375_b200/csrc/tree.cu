@@ -23,19 +23,53 @@ constexpr int kMortonBits = 21;
 // ----------------------------------------------------------------- K1 geometry
 // Correctly rounded FP64, no contraction: the near criterion downstream must
 // reproduce the oracle's decisions bit for bit (reading R3).
+// Panels: tri[stride*k + 0..2]; stride 4 with tri[4k+3] >= 0 is a rectangle (planar parallelogram
+// a b c d in cyclic order): centroid = (a + c) * 0.5 (the diagonals' intersection),
+// area = |(b-a) x (d-a)|, D = the longer diagonal (reading R16).
+__device__ __forceinline__ double len_rn(const double* e)
+{
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(e[0], e[0]), __dmul_rn(e[1], e[1])), __dmul_rn(e[2], e[2])));
+}
+
 __global__ void k_geometry(int64_t n, int64_t nv, const double* __restrict__ vert, const int32_t* __restrict__ tri,
-                           double* cent, double* area, double* dmax, int* bad)
+                           int stride, double* cent, double* area, double* dmax, int* bad)
 {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
-    int i0 = tri[3 * k], i1 = tri[3 * k + 1], i2 = tri[3 * k + 2];
-    if (i0 < 0 || i1 < 0 || i2 < 0 || i0 >= nv || i1 >= nv || i2 >= nv) {
+    int i0 = tri[stride * k], i1 = tri[stride * k + 1], i2 = tri[stride * k + 2];
+    const int i3 = stride == 4 ? tri[4 * k + 3] : -1;
+    if (i0 < 0 || i1 < 0 || i2 < 0 || i0 >= nv || i1 >= nv || i2 >= nv || i3 >= nv) {
         atomicOr(bad, 1);
         return;
     }
     const double* a = vert + 3 * (int64_t)i0;
     const double* b = vert + 3 * (int64_t)i1;
     const double* c = vert + 3 * (int64_t)i2;
+    if (i3 >= 0) {
+        const double* q = vert + 3 * (int64_t)i3;
+        double e1[3], e2[3], d1[3], d2[3], sk[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            cent[3 * k + d] = __dmul_rn(__dadd_rn(a[d], c[d]), 0.5);
+            e1[d] = __dsub_rn(b[d], a[d]);
+            e2[d] = __dsub_rn(q[d], a[d]);
+            d1[d] = __dsub_rn(c[d], a[d]);
+            d2[d] = __dsub_rn(q[d], b[d]);
+            sk[d] = (c[d] - b[d]) - (q[d] - a[d]);  // parallelogram test: c - b == d - a
+        }
+        double cx = __dsub_rn(__dmul_rn(e1[1], e2[2]), __dmul_rn(e1[2], e2[1]));
+        double cy = __dsub_rn(__dmul_rn(e1[2], e2[0]), __dmul_rn(e1[0], e2[2]));
+        double cz = __dsub_rn(__dmul_rn(e1[0], e2[1]), __dmul_rn(e1[1], e2[0]));
+        const double ar = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz)));
+        const double l1 = len_rn(d1), l2 = len_rn(d2);
+        dmax[k] = l1 > l2 ? l1 : l2;
+        area[k] = ar;
+        if (!(ar > 0.0)) atomicOr(bad, 2);
+        // planar parallelogram: c - b == d - a within 1e-9 D
+        const double tol = 1e-9 * (l1 > l2 ? l1 : l2);
+        if (sqrt(sk[0] * sk[0] + sk[1] * sk[1] + sk[2] * sk[2]) > tol) atomicOr(bad, 8);  // (then planar too)
+        return;
+    }
     double e1[3], e2[3], e3[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -48,10 +82,7 @@ __global__ void k_geometry(int64_t n, int64_t nv, const double* __restrict__ ver
     double cy = __dsub_rn(__dmul_rn(e1[2], e2[0]), __dmul_rn(e1[0], e2[2]));
     double cz = __dsub_rn(__dmul_rn(e1[0], e2[1]), __dmul_rn(e1[1], e2[0]));
     double ar = __dmul_rn(0.5, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy)), __dmul_rn(cz, cz))));
-    auto len = [](const double* e) {
-        return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(e[0], e[0]), __dmul_rn(e[1], e[1])), __dmul_rn(e[2], e[2])));
-    };
-    double l1 = len(e1), l2 = len(e2), l3 = len(e3);
+    double l1 = len_rn(e1), l2 = len_rn(e2), l3 = len_rn(e3);
     double m = l1 > l2 ? l1 : l2;
     dmax[k] = m > l3 ? m : l3;
     area[k] = ar;
@@ -123,8 +154,8 @@ __global__ void k_dup_check(int64_t n, const uint64_t* __restrict__ key, const i
 
 __global__ void k_gather_panels(int64_t n, const int32_t* __restrict__ perm, const double* __restrict__ cent_o,
                                 const double* __restrict__ area_o, const double* __restrict__ dmax_o,
-                                const double* __restrict__ vert, const int32_t* __restrict__ tri, double* cent,
-                                double* area, double* dmax, double* tv, int32_t* iperm)
+                                const double* __restrict__ vert, const int32_t* __restrict__ tri, int stride,
+                                double* cent, double* area, double* dmax, double* tv, int4* pvid, int32_t* iperm)
 {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -134,10 +165,14 @@ __global__ void k_gather_panels(int64_t n, const int32_t* __restrict__ perm, con
     for (int d = 0; d < 3; ++d) cent[3 * i + d] = cent_o[3 * k + d];
     area[i] = area_o[k];
     dmax[i] = dmax_o[k];
+    const int v3 = stride == 4 ? tri[4 * k + 3] : -1;
+    pvid[i] = make_int4(tri[stride * k], tri[stride * k + 1], tri[stride * k + 2], v3);
 #pragma unroll
     for (int v = 0; v < 3; ++v)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) tv[9 * i + 3 * v + d] = vert[3 * (int64_t)tri[3 * k + v] + d];
+        for (int d = 0; d < 3; ++d) tv[12 * i + 3 * v + d] = vert[3 * (int64_t)tri[stride * k + v] + d];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) tv[12 * i + 9 + d] = v3 >= 0 ? vert[3 * (int64_t)v3 + d] : __longlong_as_double(0x7ff8000000000000LL);
 }
 
 // ----------------------------------------------------------------- K4 octree
@@ -480,7 +515,7 @@ inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 // ----------------------------------------------------------------- build
 static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* vert_h, int64_t n, const int32_t* tri_h,
-                                  const xrl_fmm_opts* opts, xrl_tree* out)
+                                  int stride, const xrl_fmm_opts* opts, xrl_tree* out)
 {
     cudaStream_t st = ctx->stream;
     XRL_CUDA(cudaSetDevice(ctx->device));
@@ -495,25 +530,27 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     T->n = n;
     T->leaf_max = opts ? opts->leaf_max : 64;
     T->h_vert.assign(vert_h, vert_h + 3 * n_vert);
-    T->h_tri.assign(tri_h, tri_h + 3 * n);
+    T->stride = stride;
+    if (stride == 3) T->h_tri.assign(tri_h, tri_h + 3 * n);
     T->max_depth = opts ? opts->max_depth : kMortonBits;
     T->part_rank = ctx->world > 1 ? ctx->rank : (opts ? opts->part_rank : 0);
     T->part_world = ctx->world > 1 ? ctx->world : (opts && opts->part_world > 0 ? opts->part_world : 1);
 
     DBuf<double> vert(3 * n_vert);
-    DBuf<int32_t> tri(3 * n);
+    DBuf<int32_t> tri(stride * n);
     XRL_CUDA(cudaMemcpyAsync(vert.p, vert_h, vert.bytes(), cudaMemcpyHostToDevice, st));
     XRL_CUDA(cudaMemcpyAsync(tri.p, tri_h, tri.bytes(), cudaMemcpyHostToDevice, st));
     DBuf<double> cent_o(3 * n), area_o(n), dmax_o(n);
     DBuf<int> bad(1);
     XRL_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-    k_geometry<<<nblk(n, 256), 256, 0, st>>>(n, n_vert, vert.p, tri.p, cent_o.p, area_o.p, dmax_o.p, bad.p);
+    k_geometry<<<nblk(n, 256), 256, 0, st>>>(n, n_vert, vert.p, tri.p, stride, cent_o.p, area_o.p, dmax_o.p, bad.p);
     XRL_LAUNCH_CHECK();
     int hbad = 0;
     XRL_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     XRL_CUDA(cudaStreamSynchronize(st));
     if (hbad & 1) { set_error("xrl_tree_build: vertex index out of range"); return XRL_EGEOM; }
-    if (hbad & 2) { set_error("xrl_tree_build: zero-area triangle"); return XRL_EGEOM; }
+    if (hbad & 2) { set_error("xrl_tree_build: zero-area panel"); return XRL_EGEOM; }
+    if (hbad & 8) { set_error("xrl_tree_build: rectangle panel is not a planar parallelogram"); return XRL_EGEOM; }
 
     // root cube
     const int nbb = 256;
@@ -549,9 +586,11 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     T->cent.alloc(3 * n);
     T->area.alloc(n);
     T->dmax.alloc(n);
-    T->tverts.alloc(9 * n);
-    k_gather_panels<<<nblk(n, 256), 256, 0, st>>>(n, T->perm.p, cent_o.p, area_o.p, dmax_o.p, vert.p, tri.p,
-                                                  T->cent.p, T->area.p, T->dmax.p, T->tverts.p, T->iperm.p);
+    T->tverts.alloc(12 * n);
+    T->pvid.alloc(n);
+    k_gather_panels<<<nblk(n, 256), 256, 0, st>>>(n, T->perm.p, cent_o.p, area_o.p, dmax_o.p, vert.p, tri.p, stride,
+                                                  T->cent.p, T->area.p, T->dmax.p, T->tverts.p, T->pvid.p,
+                                                  T->iperm.p);
     XRL_LAUNCH_CHECK();
 
     // octree, level by level
@@ -1073,8 +1112,23 @@ xrl_status xrl_partition_cuts(int64_t n, const double* w, int32_t world, int64_t
     return XRL_OK;
 }
 
+static xrl_status tree_build_checked(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_tri,
+                                     const int32_t* tri, int stride, const xrl_fmm_opts* opts, xrl_tree* out);
+
 xrl_status xrl_tree_build(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_tri, const int32_t* tri,
                           const xrl_fmm_opts* opts, xrl_tree* out)
+{
+    return tree_build_checked(ctx, n_vert, vert, n_tri, tri, 3, opts, out);
+}
+
+xrl_status xrl_tree_build_poly(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_panel, const int32_t* pv,
+                               const xrl_fmm_opts* opts, xrl_tree* out)
+{
+    return tree_build_checked(ctx, n_vert, vert, n_panel, pv, 4, opts, out);
+}
+
+static xrl_status tree_build_checked(xrl_ctx ctx, int64_t n_vert, const double* vert, int64_t n_tri,
+                                     const int32_t* tri, int stride, const xrl_fmm_opts* opts, xrl_tree* out)
 {
     if (!ctx || !vert || !tri || !out) { set_error("xrl_tree_build: null argument"); return XRL_EINVAL; }
     *out = nullptr;
@@ -1093,7 +1147,7 @@ xrl_status xrl_tree_build(xrl_ctx ctx, int64_t n_vert, const double* vert, int64
         }
     }
     try {
-        return tree_build_impl(ctx, n_vert, vert, n_tri, tri, opts, out);
+        return tree_build_impl(ctx, n_vert, vert, n_tri, tri, stride, opts, out);
     } catch (const CudaError& e) {
         return e.code;
     } catch (const std::bad_alloc&) {

@@ -121,7 +121,8 @@ struct xrl_tree_s {
     xrl::DBuf<double> cent;     // [n][3] FP64 centroids
     xrl::DBuf<double> area;     // [n]
     xrl::DBuf<double> dmax;     // [n]
-    xrl::DBuf<double> tverts;   // [n][9] triangle vertices
+    xrl::DBuf<double> tverts;   // [n][12] panel vertices (library order; 4th = NaN for triangles)
+    xrl::DBuf<int4> pvid;       // [n] panel vertex ids (w = -1 for triangles), library order
     xrl::DBuf<float4> loc;      // [n] local coords (W units) relative to leaf centre; w = unused
     xrl::DBuf<int32_t> panel_leaf;  // [n] leaf box of each panel
     // boxes (level order)
@@ -171,7 +172,8 @@ struct xrl_tree_s {
     xrl::DBuf<float2> xfull;                 // gathered x (multi-rank MVM)
     // host copies of the mesh (original order) for the topology build
     std::vector<double> h_vert;              // [nv][3]
-    std::vector<int32_t> h_tri;              // [n][3]
+    std::vector<int32_t> h_tri;              // [n][3] (triangle meshes; empty for hybrid meshes)
+    int32_t stride = 3;                      // 3: triangles; 4: hybrid panels pv[n][4] (-1: triangle)
     // MVM scratch
     xrl::DBuf<float> mu;                     // [nbox][kMuStride]  mu[r][k]
     xrl::DBuf<float> ell;                    // [nbox][kEllStride] ell[r][k]

@@ -22,7 +22,7 @@ STATUS = {0: "XRL_OK", 1: "XRL_ENOCONV", -1: "XRL_EINVAL", -2: "XRL_EDIM", -3: "
 # symbols declared in include/xrl.h (checked by tests/test_abi.py)
 EXPORTS = [
     "xrl_last_error", "xrl_version", "xrl_ctx_create", "xrl_ctx_sync", "xrl_ctx_destroy",
-    "xrl_tree_build", "xrl_tree_destroy", "xrl_tree_info", "xrl_tree_perm", "xrl_to_library_order",
+    "xrl_tree_build", "xrl_tree_build_poly", "xrl_tree_destroy", "xrl_tree_info", "xrl_tree_perm", "xrl_to_library_order",
     "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble", "xrl_near_destroy",
     "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_timing_enable", "xrl_timing_count",
     "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_extract",
@@ -45,7 +45,7 @@ class FmmOpts(ctypes.Structure):
 
 
 class NearOpts(ctypes.Structure):
-    _fields_ = [("eta", ctypes.c_double)]
+    _fields_ = [("eta", ctypes.c_double), ("galerkin", ctypes.c_int32)]
 
 
 class TreeInfo(ctypes.Structure):
@@ -102,6 +102,7 @@ def lib():
         L.xrl_ctx_destroy.argtypes = [P]
         L.xrl_ctx_destroy.restype = None
         L.xrl_tree_build.argtypes = [P, i64, P, i64, P, ctypes.POINTER(FmmOpts), pp]
+        L.xrl_tree_build_poly.argtypes = [P, i64, P, i64, P, ctypes.POINTER(FmmOpts), pp]
         L.xrl_tree_destroy.argtypes = [P]
         L.xrl_tree_destroy.restype = None
         L.xrl_tree_info.argtypes = [P, ctypes.POINTER(TreeInfo)]
@@ -157,7 +158,7 @@ def lib():
                      "xrl_precond_apply",
                      "xrl_precond_export", "xrl_gmres", "xrl_port_rhs", "xrl_port_currents"):
             getattr(L, name).restype = ctypes.c_int32
-        for name in ("xrl_ctx_create", "xrl_ctx_sync", "xrl_tree_build", "xrl_tree_info", "xrl_tree_perm",
+        for name in ("xrl_ctx_create", "xrl_ctx_sync", "xrl_tree_build", "xrl_tree_build_poly", "xrl_tree_info", "xrl_tree_perm",
                      "xrl_to_library_order", "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble",
                      "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_timing_enable", "xrl_timing_get",
                      "xrl_timing_reset"):
@@ -282,7 +283,8 @@ def distributed_context(device: int = 0, stream=None) -> Context:
 
 
 class Tree:
-    """xrl_tree_build over a triangle mesh (host FP64 verts [nv,3], int32 tris [n,3])."""
+    """xrl_tree_build over a triangle mesh (host FP64 verts [nv,3], int32 tris [n,3]); a [n,4] panel array
+    (-1 in the last column for triangles, else a rectangle) goes to xrl_tree_build_poly (hybrid mesh)."""
 
     def __init__(self, ctx: Context, verts, tris, p=10, leaf_max=64, max_depth=21, part_rank=None, part_world=None):
         self.ctx = ctx
@@ -292,8 +294,8 @@ class Tree:
             part_rank, part_world = (ctx.rank, ctx.world) if ctx.world > 1 else (0, 0)
         opts = FmmOpts(p, leaf_max, max_depth, part_rank or 0, part_world)
         h = ctypes.c_void_p()
-        check(lib().xrl_tree_build(ctx.h, v.shape[0], _ptr(v), t.shape[0], _ptr(t), ctypes.byref(opts),
-                                   ctypes.byref(h)))
+        build = lib().xrl_tree_build_poly if t.shape[1] == 4 else lib().xrl_tree_build
+        check(build(ctx.h, v.shape[0], _ptr(v), t.shape[0], _ptr(t), ctypes.byref(opts), ctypes.byref(h)))
         self.h = h
         self.n = t.shape[0]
         i = self.info()
@@ -352,10 +354,10 @@ class Tree:
 class Near:
     """xrl_near_assemble: near-field CSR (library order)."""
 
-    def __init__(self, tree: Tree, eta=1.5):
+    def __init__(self, tree: Tree, eta=1.5, galerkin=False):
         self.tree = tree
         h = ctypes.c_void_p()
-        check(lib().xrl_near_assemble(tree.h, ctypes.byref(NearOpts(eta)), ctypes.byref(h)))
+        check(lib().xrl_near_assemble(tree.h, ctypes.byref(NearOpts(eta, int(bool(galerkin)))), ctypes.byref(h)))
         self.h = h
 
     def nnz(self) -> int:

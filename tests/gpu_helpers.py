@@ -6,13 +6,13 @@ import oracle
 from inputs import meshes
 
 
-def cuda_setup(mesh, leaf_max=64, eta=oracle.ETA):
+def cuda_setup(mesh, leaf_max=64, eta=oracle.ETA, galerkin=False):
     import torch
     from paper_2409_12375_b200 import build, xrl
     build.build()
     ctx = xrl.Context(0)
     tree = xrl.Tree(ctx, mesh.verts, mesh.tris, leaf_max=leaf_max)
-    near = xrl.Near(tree, eta=eta)
+    near = xrl.Near(tree, eta=eta, galerkin=galerkin)
     return ctx, tree, near
 
 
@@ -28,6 +28,6 @@ def run_mvm(tree, near, x_user: np.ndarray, flags=0):
     return y.cpu().numpy()
 
 
-def oracle_rows(mesh, x, rows=None, nthreads=0):
-    g = oracle.Geometry(mesh.verts, mesh.tris)
+def oracle_rows(mesh, x, rows=None, nthreads=0, galerkin=False):
+    g = oracle.Geometry(mesh.verts, mesh.tris, galerkin=galerkin)
     return oracle.mvm_rows(g, x, rows, nthreads=nthreads)

@@ -257,3 +257,65 @@ def test_virtual_partition_concat_equals_full(cfg, world, leaf):
     err = oracle.rel_l2(y_cat, y_full)
     print("virtual partition", cfg, world, err, [p.shape[1] for p in parts])
     assert err < 1e-6
+
+
+# ---------------------------------------------------------------- NEXT f4: hybrid meshes, Galerkin near rule
+
+def _near_vs_oracle(m, tree, near, galerkin):
+    perm = tree.perm()
+    ptr, col, v32, v64 = near.export()
+    g = oracle.Geometry(m.verts, m.tris, galerkin=galerkin)
+    optr, ocol, oval, _ = oracle.near_rows(g)
+    for i in range(m.n):
+        k = perm[i]
+        order = np.argsort(perm[col[ptr[i]:ptr[i + 1]]])
+        assert np.array_equal(perm[col[ptr[i]:ptr[i + 1]]][order], ocol[optr[k]:optr[k + 1]]), i
+        np.testing.assert_allclose(v64[ptr[i]:ptr[i + 1]][order], oval[optr[k]:optr[k + 1]], rtol=1e-12)
+
+
+@pytest.mark.parametrize("galerkin", [False, True])
+def test_hybrid_mesh_near_and_full_mvm(galerkin):
+    """Hybrid bar (1,000 rectangles + 100 triangles, xrl_tree_build_poly): near pattern bit for bit and
+    FP64 near values to 1e-12 against the oracle, full MVM within the north-star tolerance; with the
+    Galerkin near rule as well."""
+    m = meshes.bar_hybrid()
+    ctx, tree, near = cuda_setup(m, galerkin=galerkin)
+    _near_vs_oracle(m, tree, near, galerkin)
+    x = meshes.make_x(1, m.n)
+    err = oracle.rel_l2(run_mvm(tree, near, x), oracle_rows(m, x, galerkin=galerkin))
+    print("hybrid galerkin", galerkin, "full", err)
+    assert err <= TOL_FULL
+
+
+def test_galerkin_near_rule_triangle_mesh(bar_setup):
+    """The Galerkin rule on the triangle bar: near values match the oracle's, full MVM within tolerance."""
+    m = bar_setup[0]
+    ctx, tree, near = cuda_setup(m, galerkin=True)
+    _near_vs_oracle(m, tree, near, True)
+    x = meshes.make_x(2, m.n)
+    err = oracle.rel_l2(run_mvm(tree, near, x), oracle_rows(m, x, galerkin=True))
+    print("bar galerkin full", err)
+    assert err <= TOL_FULL
+
+
+def test_hybrid_mesh_errors():
+    """A rectangle that is not a parallelogram is XRL_EGEOM; the loop-space topology rejects hybrid
+    meshes (XRL_EUNSUPPORTED); triangles-only [n][4] input equals the [n][3] path bit for bit."""
+    from paper_2409_12375_b200 import xrl
+    m = meshes.bar_hybrid()
+    ctx, tree, near = cuda_setup(m)
+    with pytest.raises(xrl.XrlError) as e:
+        xrl.Topology(tree, [])
+    assert e.value.code == -10
+    bad = m.verts.copy()
+    bad[m.tris[0, 2]] += np.array([1e-6, 0, 0])  # breaks the first rectangle (and its neighbours)
+    with pytest.raises(xrl.XrlError) as e:
+        xrl.Tree(ctx, bad, m.tris)
+    assert e.value.code == -4
+    mb = meshes.bar()
+    t4 = np.concatenate([mb.tris, np.full((mb.n, 1), -1, np.int32)], axis=1)
+    c3, tr3, n3 = cuda_setup(mb)
+    tr4 = xrl.Tree(c3, mb.verts, t4)
+    n4 = xrl.Near(tr4)
+    a, b = n3.export(), n4.export()
+    assert all(np.array_equal(u, v) for u, v in zip(a, b))
