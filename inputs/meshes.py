@@ -167,9 +167,14 @@ def bar_hybrid(length=1000 * UM, side=100 * UM, cell=20 * UM) -> Mesh:
     cap = np.abs(nrm[:, 0]) > 0.5
     tri = np.concatenate([q[cap][:, [0, 1, 2]], q[cap][:, [0, 2, 3]]], axis=0)  # same winding as the quad
     panels = np.concatenate([q[~cap], np.concatenate([tri, np.full((tri.shape[0], 1), -1)], axis=1)])
-    m = Mesh(v, panels.astype(np.int32), name="bar_hybrid")
-    m.meta = {"rectangles": int((~cap).sum()), "triangles": int(tri.shape[0])}
-    return m
+    panels = panels.astype(np.int32)
+    cen = np.array([v[p[p >= 0]].mean(axis=0) for p in panels])
+    minus = np.nonzero(np.isclose(cen[:, 0], 0.0, atol=1e-3 * cell))[0]
+    plus = np.nonzero(np.isclose(cen[:, 0], length, atol=1e-3 * cell))[0]
+    return Mesh(v, panels, "bar_hybrid", np.zeros(panels.shape[0], np.int32),
+                [("P1", plus.astype(np.int32), minus.astype(np.int32))],
+                {"length": length, "side": side, "cell": cell, "rectangles": int((~cap).sum()),
+                 "triangles": int(tri.shape[0])})
 
 
 def merge(parts):

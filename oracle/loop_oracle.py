@@ -39,13 +39,20 @@ def esi(sigma: float, zeta: float, f: float) -> complex:
     return complex(a / (1 - np.exp(-a / rdc)))
 
 
+def _corners(t):
+    """Vertex ids of a panel row ([3] triangle, or [4] with -1 for a triangle)."""
+    return [int(v) for v in t if v >= 0]
+
+
 def interior_edges(tris):
-    """Interior edges of a triangle mesh: list of (p, q, va, vb), p < q panels."""
+    """Interior edges of a triangle or hybrid triangle/rectangle mesh: list of (p, q, va, vb), p < q
+    panels."""
     tris = np.asarray(tris)
     d = {}
     for p, t in enumerate(tris):
-        for e in range(3):
-            a, b = int(t[e]), int(t[(e + 1) % 3])
+        c = _corners(t)
+        for e in range(len(c)):
+            a, b = c[e], c[(e + 1) % len(c)]
             k = (min(a, b), max(a, b))
             d.setdefault(k, []).append(p)
     out = []
@@ -70,7 +77,7 @@ def cm_maps(verts, tris, cent, branches):
     for e, (a, b) in enumerate(branches):
         if a < 0 or b < 0:
             continue
-        common = sorted(set(tris[a]) & set(tris[b]))
+        common = sorted(set(_corners(tris[a])) & set(_corners(tris[b])))
         assert len(common) == 2
         m = 0.5 * (verts[common[0]] + verts[common[1]])
         ra = m - cent[a]

@@ -72,14 +72,24 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
     const int64_t nv = (int64_t)t->h_vert.size() / 3;
 
     // ---- edges: group the 3n half-edges by vertex pair
+    // (triangles: 3 half-edges; rectangle panels of hybrid meshes: 4)
     struct HE { uint64_t key; int32_t panel; };
-    std::vector<HE> he(3 * n);
+    const int sv = t->stride;
+    auto corners = [&](int64_t i, int32_t* c) {  // library panel i -> its vertex ids, count
+        const int32_t* v = &t->h_tri[(int64_t)sv * perm[i]];
+        c[0] = v[0]; c[1] = v[1]; c[2] = v[2];
+        if (sv == 4 && v[3] >= 0) { c[3] = v[3]; return 4; }
+        return 3;
+    };
+    std::vector<HE> he;
+    he.reserve((size_t)sv * n);
     for (int64_t i = 0; i < n; ++i) {
-        const int32_t* v = &t->h_tri[3 * (int64_t)perm[i]];
-        for (int e = 0; e < 3; ++e) {
-            uint32_t a = v[e], b = v[(e + 1) % 3];
+        int32_t c[4];
+        const int nc = corners(i, c);
+        for (int e = 0; e < nc; ++e) {
+            uint32_t a = c[e], b = c[(e + 1) % nc];
             if (a > b) std::swap(a, b);
-            he[3 * i + e] = {((uint64_t)a << 32) | b, (int32_t)i};
+            he.push_back({((uint64_t)a << 32) | b, (int32_t)i});
         }
     }
     std::sort(he.begin(), he.end(), [](const HE& x, const HE& y) { return x.key < y.key || (x.key == y.key && x.panel < y.panel); });
@@ -201,8 +211,10 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
     {
         // a component is open if any of its panels has a vertex without a closed fan
         for (int64_t i = 0; i < n; ++i) {
-            const int32_t* v = &t->h_tri[3 * (int64_t)perm[i]];
-            if (vbad[v[0]] || vbad[v[1]] || vbad[v[2]]) comp_open[comp_of[i]] = 1;
+            int32_t c[4];
+            const int nc = corners(i, c);
+            for (int q = 0; q < nc; ++q)
+                if (vbad[c[q]]) comp_open[comp_of[i]] = 1;
         }
         std::vector<int> last(ncomp, -1);
         for (size_t i = 0; i < vloops.size(); ++i) last[vloop_comp[i]] = (int)i;
@@ -470,10 +482,7 @@ xrl_status xrl_topology_build(xrl_tree t, int32_t n_ports, const xrl_port* ports
 {
     if (!t || !out || n_ports < 0 || (n_ports > 0 && !ports)) { set_error("xrl_topology_build: bad argument"); return XRL_EINVAL; }
     *out = nullptr;
-    if (t->stride != 3) {
-        set_error("xrl_topology_build: hybrid (rectangle) meshes are supported by the MVM path only");
-        return XRL_EUNSUPPORTED;
-    }
+
     try {
         return topo_impl(t, n_ports, ports, out);
     } catch (const CudaError& e) {

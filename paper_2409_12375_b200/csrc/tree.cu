@@ -531,7 +531,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     T->leaf_max = opts ? opts->leaf_max : 64;
     T->h_vert.assign(vert_h, vert_h + 3 * n_vert);
     T->stride = stride;
-    if (stride == 3) T->h_tri.assign(tri_h, tri_h + 3 * n);
+    T->h_tri.assign(tri_h, tri_h + (int64_t)stride * n);
     T->max_depth = opts ? opts->max_depth : kMortonBits;
     T->part_rank = ctx->world > 1 ? ctx->rank : (opts ? opts->part_rank : 0);
     T->part_world = ctx->world > 1 ? ctx->world : (opts && opts->part_world > 0 ? opts->part_world : 1);

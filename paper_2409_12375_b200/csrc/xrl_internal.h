@@ -172,7 +172,7 @@ struct xrl_tree_s {
     xrl::DBuf<float2> xfull;                 // gathered x (multi-rank MVM)
     // host copies of the mesh (original order) for the topology build
     std::vector<double> h_vert;              // [nv][3]
-    std::vector<int32_t> h_tri;              // [n][3] (triangle meshes; empty for hybrid meshes)
+    std::vector<int32_t> h_tri;              // [n][stride] panel vertex ids (mesh order; -1: no 4th vertex)
     int32_t stride = 3;                      // 3: triangles; 4: hybrid panels pv[n][4] (-1: triangle)
     // MVM scratch
     xrl::DBuf<float> mu;                     // [nbox][kMuStride]  mu[r][k]

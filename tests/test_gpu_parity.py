@@ -299,14 +299,11 @@ def test_galerkin_near_rule_triangle_mesh(bar_setup):
 
 
 def test_hybrid_mesh_errors():
-    """A rectangle that is not a parallelogram is XRL_EGEOM; the loop-space topology rejects hybrid
-    meshes (XRL_EUNSUPPORTED); triangles-only [n][4] input equals the [n][3] path bit for bit."""
+    """A rectangle that is not a parallelogram is XRL_EGEOM; triangles-only [n][4] input equals the
+    [n][3] path bit for bit."""
     from paper_2409_12375_b200 import xrl
     m = meshes.bar_hybrid()
     ctx, tree, near = cuda_setup(m)
-    with pytest.raises(xrl.XrlError) as e:
-        xrl.Topology(tree, [])
-    assert e.value.code == -10
     bad = m.verts.copy()
     bad[m.tris[0, 2]] += np.array([1e-6, 0, 0])  # breaks the first rectangle (and its neighbours)
     with pytest.raises(xrl.XrlError) as e:

@@ -330,3 +330,25 @@ def test_gmres_exact_vs_block_precond_coils():
     print("coils 100 MHz iterations", iters)
     assert iters["exact"] <= iters["block"]
     assert np.abs(zs["exact"] - zs["block"]).max() / np.abs(zs["block"]).max() < 1e-3
+
+
+def test_hybrid_bar_extract_matches_oracle():
+    """NEXT f4 through the loop-space path: the hybrid bar (1,000 rectangles + 100 triangles) gives the
+    same port impedance as the oracle's dense FP64 solve on its own basis, and L within 2 % of the
+    thin-walled-tube closed form (block-Jacobi and exact preconditioners)."""
+    from paper_2409_12375_b200 import xrl
+    m = meshes.bar_hybrid()
+    ctx, tree, near = cuda_setup(m)
+    topo = xrl.Topology(tree, [(p, q) for _, p, q in m.ports])
+    g = oracle.Geometry(m.verts, m.tris)
+    P = oracle.dense_p(g)
+    rdc = 2 / (SIGMA * ZETA)
+    Zo, _ = lo.port_impedance(m.verts, m.tris, g.cent, g.area, P, [(m.ports[0][1], m.ports[0][2])], rdc, 1e3)
+    Lt = lo.bar_partial_inductance_tube(1e-3, 1e-4)
+    for exact in (False, True):
+        res = xrl.extract(tree, near, topo, [1e3], zs=rdc, exact=exact)
+        assert res["status"] == 0, res
+        z = res["z"][0, 0, 0]
+        print("hybrid bar exact", exact, "Z", z, "oracle", Zo[0, 0], "iters", res["iters"])
+        assert abs(z - Zo[0, 0]) / abs(Zo[0, 0]) < 1e-4
+        assert abs(res["l"][0, 0, 0] - Lt) / Lt < 0.02

@@ -102,3 +102,21 @@ def test_loop_system_structure(bar_dense):
     # the potential part is symmetric positive definite on this mesh (P SPD)
     Lp = lo.loop_system(C, P, np.zeros(m.n), 1.0)
     assert np.linalg.eigvalsh(0.5 * (Lp + Lp.T).real).min() > 0
+
+
+def test_hybrid_bar_loop_oracle_dc_inductance():
+    """NEXT f4 on the loop oracle: the hybrid bar (rectangles on the long faces, triangles on the caps)
+    has the closed-surface edge count E = V + F - 2, a KCL-exact loop basis, and its DC partial
+    inductance matches the thin-walled-tube closed form (like the all-triangle bar)."""
+    m = meshes.bar_hybrid()
+    e = lo.interior_edges(m.tris)
+    assert len(e) == m.verts.shape[0] + m.n - 2
+    g = oracle.Geometry(m.verts, m.tris)
+    P = oracle.dense_p(g)
+    rdc = 2 / (5.8e7 * 1e-4)
+    Z, info = lo.port_impedance(m.verts, m.tris, g.cent, g.area, P, [(m.ports[0][1], m.ports[0][2])], rdc, 1e3)
+    assert info["kcl"] < 1e-12
+    L = Z[0, 0].imag / (2 * np.pi * 1e3)
+    Lt = lo.bar_partial_inductance_tube(1e-3, 1e-4)
+    print("hybrid bar L", L, "tube", Lt)
+    assert abs(L - Lt) / Lt < 0.02
