@@ -371,7 +371,8 @@ def run_xrl(args):
     roof = dict(roofs.get(dom) or {"kernel": "k_" + dom})
     roof["share_of_step"] = phases[dom][0] / args.steps / ms_per_step if ms_per_step else None
     roof["share_of_isolated_sum"] = phases_iso[dom][0] / sum(v[0] for v in phases_iso.values())
-    roof["others"] = {k: {kk: v[kk] for kk in ("achieved", "peak", "unit", "frac", "isolated")}
+    roof["others"] = {k: {kk: v[kk] for kk in ("kernel", "bound", "achieved", "peak", "unit", "frac", "traffic",
+                                               "isolated", "algorithmic")}
                       for k, v in roofs.items() if k != dom}
 
     line = {
