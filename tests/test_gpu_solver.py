@@ -352,3 +352,31 @@ def test_hybrid_bar_extract_matches_oracle():
         print("hybrid bar exact", exact, "Z", z, "oracle", Zo[0, 0], "iters", res["iters"])
         assert abs(z - Zo[0, 0]) / abs(Zo[0, 0]) < 1e-4
         assert abs(res["l"][0, 0, 0] - Lt) / Lt < 0.02
+
+
+def test_hybrid_topology_box_and_c_maps():
+    """Rectangle panels in the loop-space topology: the closed box of 6 rectangles has 12 interior edges
+    and N_l = 7 loops (cycle rank 12 - 6 + 1); on the hybrid bar the library's C = M A_t
+    equals the oracle's Algorithm-1 product on the same loop basis and M is KCL-exact."""
+    from paper_2409_12375_b200 import xrl
+    V = np.array([[x, y, z] for x in (0.0, 1e-4) for y in (0.0, 1e-4) for z in (0.0, 1e-4)])
+    vid = lambda x, y, z: 4 * x + 2 * y + z  # noqa: E731
+    faces = [[vid(0, 0, 0), vid(0, 1, 0), vid(1, 1, 0), vid(1, 0, 0)], [vid(0, 0, 1), vid(1, 0, 1), vid(1, 1, 1), vid(0, 1, 1)],
+             [vid(0, 0, 0), vid(1, 0, 0), vid(1, 0, 1), vid(0, 0, 1)], [vid(0, 1, 0), vid(0, 1, 1), vid(1, 1, 1), vid(1, 1, 0)],
+             [vid(0, 0, 0), vid(0, 0, 1), vid(0, 1, 1), vid(0, 1, 0)], [vid(1, 0, 0), vid(1, 1, 0), vid(1, 1, 1), vid(1, 0, 1)]]
+    ctx = xrl.Context(0)
+    tb = xrl.Tree(ctx, V, np.array(faces, np.int32), leaf_max=4)
+    info = xrl.Topology(tb, []).info()
+    assert info["n_edges"] == 12 and info["n_loops"] == 7
+    m = meshes.bar_hybrid()
+    ctx, tree, near = cuda_setup(m)
+    topo = xrl.Topology(tree, [(p, q) for _, p, q in m.ports])
+    ex = topo.export()
+    g = oracle.Geometry(m.verts, m.tris)
+    M, C = _oracle_C(m, g, ex)
+    nl = topo.n_loops
+    assert nl == ex["c_ptr"].size - 1
+    rows = np.repeat(np.arange(nl), np.diff(ex["c_ptr"]))
+    for t in range(3):
+        Clt = sp.csr_matrix((ex["c_val"][:, t], (rows, ex["c_panel"])), shape=(nl, m.n))
+        assert np.abs((Clt - C[t]).toarray()).max() <= 1e-12 * np.abs(C[t].toarray()).max()
