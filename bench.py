@@ -149,9 +149,9 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Mpanels/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CFG_NAMES[args.config], "n_panels": mesh.n, "p": 10, "eta": 1.5,
-                   "parallelism": "host threads (OpenMP)"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CFG_NAMES[args.config], "n_panels": mesh.n, "p": 10, "leaf_max": args.leaf,
+                   "eta": 1.5, "parallelism": "host threads (OpenMP), rank 0 only"},
         "cpu_baseline": {"value": value, "unit": "Mpanels/s", "cores": cores, "kind": "oracle",
                          "sample": f"{per_step_rows} seeded target rows per step x all {mesh.n} sources (FP64 direct sum)"},
         "e2e": {"value": value, "unit": "Mpanels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
