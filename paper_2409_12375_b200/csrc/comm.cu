@@ -52,9 +52,11 @@ xrl_status gather_slices(xrl_tree t, const float2* x_local, float2* x_full)
         for (int r = 0; r < t->part_world; ++r) {
             const int64_t c0 = t->part_cuts[r], c1 = t->part_cuts[r + 1];
             if (c1 <= c0) continue;
-            const void* send = (r == ctx->rank) ? (const void*)(x_local + (size_t)v * nl) : nullptr;
-            XRL_NCCL(ncclBroadcast(send, x_full + (size_t)v * n + c0, (size_t)(c1 - c0) * 2, ncclFloat, r,
-                                   (ncclComm_t)ctx->nccl_comm, ctx->stream));
+            float2* recv = x_full + (size_t)v * n + c0;
+            // sendbuff is read on the root only; the other ranks pass their receive buffer (never NULL)
+            const void* send = (r == ctx->rank) ? (const void*)(x_local + (size_t)v * nl) : (const void*)recv;
+            XRL_NCCL(ncclBroadcast(send, recv, (size_t)(c1 - c0) * 2, ncclFloat, r, (ncclComm_t)ctx->nccl_comm,
+                                   ctx->stream));
         }
     XRL_NCCL(ncclGroupEnd());
     return XRL_OK;
