@@ -4,8 +4,9 @@
 // Pardiso and solves per GMRES iteration).  Here: Q assembled on the host in FP64 complex
 // (sparse, pattern = loops sharing a panel), nested-dissection (METIS) ordering, else approximate minimum
 // degree, then a host sparse LU with partial pivoting (cuSOLVER's low-level csrlu, the library analogue of
-// Pardiso), factorised once per operator; every apply copies v to the host, runs the two triangular solves
-// per right-hand side and copies z back (synchronous on the context stream).
+// Pardiso), factorised once per operator.  The factors P B Q^T = L U are moved to the GPU (FP64 complex
+// CSR) and every apply runs on the context stream: gather-permute v, cuSPARSE triangular solves with L
+// (unit diagonal) and U, scatter-permute into z (XRL_EXACT_HOST=1: the host solve instead, for checks).
 //
 // cuSOLVER/cuSPARSE are opened at run time (dlopen) on the first exact build, so the rest of libxrl never
 // depends on them; a missing library makes xrl_precond_build_exact fail with a message (no fallback).
@@ -19,6 +20,7 @@
 
 #include <cuComplex.h>
 #include <cuda_runtime.h>
+#include <cusparse.h>
 
 #include "xrl_internal.h"
 
@@ -49,6 +51,23 @@ struct Api {
     int (*destroyDescr)(MatDescr);
     int (*setType)(MatDescr, int);
     int (*setBase)(MatDescr, int);
+    int (*luNnz)(SpHandle, int*, int*, LuInfo);
+    int (*luExtract)(SpHandle, int*, int*, const MatDescr, cuDoubleComplex*, int*, int*, const MatDescr,
+                     cuDoubleComplex*, int*, int*, LuInfo, void*);
+    // cuSPARSE generic triangular solve
+    decltype(&cusparseCreate) spCreateH;
+    decltype(&cusparseDestroy) spDestroyH;
+    decltype(&cusparseSetStream) spSetStream;
+    decltype(&cusparseCreateCsr) createCsr;
+    decltype(&cusparseDestroySpMat) destroySpMat;
+    decltype(&cusparseSpMatSetAttribute) setAttr;
+    decltype(&cusparseCreateDnVec) createDnVec;
+    decltype(&cusparseDestroyDnVec) destroyDnVec;
+    decltype(&cusparseSpSV_createDescr) svCreate;
+    decltype(&cusparseSpSV_destroyDescr) svDestroy;
+    decltype(&cusparseSpSV_bufferSize) svBuffer;
+    decltype(&cusparseSpSV_analysis) svAnalysis;
+    decltype(&cusparseSpSV_solve) svSolve;
     std::string err;
 };
 
@@ -84,6 +103,21 @@ Api& api()
     a.destroyDescr = (decltype(a.destroyDescr))sym(hp, "cusparseDestroyMatDescr");
     a.setType = (decltype(a.setType))sym(hp, "cusparseSetMatType");
     a.setBase = (decltype(a.setBase))sym(hp, "cusparseSetMatIndexBase");
+    a.luNnz = (decltype(a.luNnz))sym(hs, "cusolverSpXcsrluNnzHost");
+    a.luExtract = (decltype(a.luExtract))sym(hs, "cusolverSpZcsrluExtractHost");
+    a.spCreateH = (decltype(a.spCreateH))sym(hp, "cusparseCreate");
+    a.spDestroyH = (decltype(a.spDestroyH))sym(hp, "cusparseDestroy");
+    a.spSetStream = (decltype(a.spSetStream))sym(hp, "cusparseSetStream");
+    a.createCsr = (decltype(a.createCsr))sym(hp, "cusparseCreateCsr");
+    a.destroySpMat = (decltype(a.destroySpMat))sym(hp, "cusparseDestroySpMat");
+    a.setAttr = (decltype(a.setAttr))sym(hp, "cusparseSpMatSetAttribute");
+    a.createDnVec = (decltype(a.createDnVec))sym(hp, "cusparseCreateDnVec");
+    a.destroyDnVec = (decltype(a.destroyDnVec))sym(hp, "cusparseDestroyDnVec");
+    a.svCreate = (decltype(a.svCreate))sym(hp, "cusparseSpSV_createDescr");
+    a.svDestroy = (decltype(a.svDestroy))sym(hp, "cusparseSpSV_destroyDescr");
+    a.svBuffer = (decltype(a.svBuffer))sym(hp, "cusparseSpSV_bufferSize");
+    a.svAnalysis = (decltype(a.svAnalysis))sym(hp, "cusparseSpSV_analysis");
+    a.svSolve = (decltype(a.svSolve))sym(hp, "cusparseSpSV_solve");
     a.metisnd = (decltype(a.metisnd))dlsym(hs, "cusolverSpXcsrmetisndHost");  // optional
     a.ok = ok;
     return a;
@@ -98,15 +132,47 @@ struct Exact {
     std::vector<char> work;
     std::vector<cuDoubleComplex> b, x;
     std::vector<float2> hv;
-    int64_t nnz_q = 0;
+    int64_t nnz_q = 0, nnz_l = 0, nnz_u = 0;
+    // device factors and triangular-solve state (P B Q^T = L U)
+    bool dev = false;
+    DBuf<int> gin, gout;                      // z-permutations: b[i] = v[gin[i]], z[gout[i]] = w[i]
+    DBuf<int> lp, lc, up, uc;
+    DBuf<cuDoubleComplex> lv, uv, db, dy;
+    DBuf<char> bufL, bufU;
+    cusparseHandle_t sh = nullptr;
+    cusparseSpMatDescr_t mL = nullptr, mU = nullptr;
+    cusparseDnVecDescr_t vB = nullptr, vY = nullptr;
+    cusparseSpSVDescr_t sL = nullptr, sU = nullptr;
     ~Exact()
     {
         Api& A = api();
+        if (sL) A.svDestroy(sL);
+        if (sU) A.svDestroy(sU);
+        if (vB) A.destroyDnVec(vB);
+        if (vY) A.destroyDnVec(vY);
+        if (mL) A.destroySpMat(mL);
+        if (mU) A.destroySpMat(mU);
+        if (sh) A.spDestroyH(sh);
         if (info) A.destroyLuInfo(info);
         if (descr) A.destroyDescr(descr);
         if (h) A.spDestroy(h);
     }
 };
+
+__global__ void k_exact_gather(int n, const float2* __restrict__ v, const int* __restrict__ gin, cuDoubleComplex* b)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const float2 w = v[gin[i]];
+        b[i] = make_cuDoubleComplex(w.x, w.y);
+    }
+}
+
+__global__ void k_exact_scatter(int n, const cuDoubleComplex* __restrict__ w, const int* __restrict__ gout, float2* z)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) z[gout[i]] = make_float2((float)w[i].x, (float)w[i].y);
+}
 
 }  // namespace
 
@@ -226,6 +292,69 @@ xrl_status exact_build(xrl_precond pc)
     if (zp >= 0) { set_error("xrl_precond_build_exact: singular Q (zero pivot at row %d)", zp); return XRL_ESINGULAR; }
     E->b.resize(N);
     E->x.resize(N);
+    static const bool host_only = getenv("XRL_EXACT_HOST") != nullptr;
+    if (!host_only) {
+        // ---- factors to the GPU: P B Q^T = L U (L unit lower, U upper); B = Q(perm, perm)
+        int nl_ = 0, nu_ = 0;
+        if (A.luNnz(E->h, &nl_, &nu_, E->info)) { set_error("xrl_precond_build_exact: LU nnz failed"); return XRL_ECUDA; }
+        std::vector<int> P(N), Qp(N), hlp(N + 1), hlc(nl_), hup(N + 1), huc(nu_);
+        std::vector<cuDoubleComplex> hlv(nl_), huv(nu_);
+        if (A.luExtract(E->h, P.data(), Qp.data(), E->descr, hlv.data(), hlp.data(), hlc.data(), E->descr, huv.data(),
+                        hup.data(), huc.data(), E->info, E->work.data())) {
+            set_error("xrl_precond_build_exact: LU extract failed");
+            return XRL_ECUDA;
+        }
+        E->nnz_l = nl_;
+        E->nnz_u = nu_;
+        // z = Qmat^-1 v:  b[i] = v[perm[P[i]]], L y = b, U w = y, z[perm[Q[i]]] = w[i]
+        std::vector<int> gi(N), go(N);
+        for (int i = 0; i < N; ++i) { gi[i] = E->perm[P[i]]; go[i] = E->perm[Qp[i]]; }
+        cudaStream_t st = op->tree->ctx->stream;
+        auto up_i = [&](DBuf<int>& d, const std::vector<int>& h) {
+            d.alloc(std::max<size_t>(1, h.size()));
+            XRL_CUDA(cudaMemcpyAsync(d.p, h.data(), 4 * h.size(), cudaMemcpyHostToDevice, st));
+        };
+        auto up_z = [&](DBuf<cuDoubleComplex>& d, const std::vector<cuDoubleComplex>& h) {
+            d.alloc(std::max<size_t>(1, h.size()));
+            XRL_CUDA(cudaMemcpyAsync(d.p, h.data(), 16 * h.size(), cudaMemcpyHostToDevice, st));
+        };
+        up_i(E->gin, gi); up_i(E->gout, go);
+        up_i(E->lp, hlp); up_i(E->lc, hlc); up_z(E->lv, hlv);
+        up_i(E->up, hup); up_i(E->uc, huc); up_z(E->uv, huv);
+        E->db.alloc(N);
+        E->dy.alloc(N);
+        XRL_CUDA(cudaStreamSynchronize(st));
+        const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+        cusparseFillMode_t lo = CUSPARSE_FILL_MODE_LOWER, upm = CUSPARSE_FILL_MODE_UPPER;
+        cusparseDiagType_t unit = CUSPARSE_DIAG_TYPE_UNIT, nonunit = CUSPARSE_DIAG_TYPE_NON_UNIT;
+        bool bad = A.spCreateH(&E->sh) || A.spSetStream(E->sh, st) ||
+                   A.createCsr(&E->mL, N, N, nl_, E->lp.p, E->lc.p, E->lv.p, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I,
+                               CUSPARSE_INDEX_BASE_ZERO, CUDA_C_64F) ||
+                   A.createCsr(&E->mU, N, N, nu_, E->up.p, E->uc.p, E->uv.p, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I,
+                               CUSPARSE_INDEX_BASE_ZERO, CUDA_C_64F) ||
+                   A.setAttr(E->mL, CUSPARSE_SPMAT_FILL_MODE, &lo, sizeof(lo)) ||
+                   A.setAttr(E->mL, CUSPARSE_SPMAT_DIAG_TYPE, &unit, sizeof(unit)) ||
+                   A.setAttr(E->mU, CUSPARSE_SPMAT_FILL_MODE, &upm, sizeof(upm)) ||
+                   A.setAttr(E->mU, CUSPARSE_SPMAT_DIAG_TYPE, &nonunit, sizeof(nonunit)) ||
+                   A.createDnVec(&E->vB, N, E->db.p, CUDA_C_64F) || A.createDnVec(&E->vY, N, E->dy.p, CUDA_C_64F) ||
+                   A.svCreate(&E->sL) || A.svCreate(&E->sU);
+        size_t szL = 0, szU = 0;
+        bad = bad || A.svBuffer(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mL, E->vB, E->vY, CUDA_C_64F,
+                                CUSPARSE_SPSV_ALG_DEFAULT, E->sL, &szL) ||
+              A.svBuffer(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mU, E->vY, E->vB, CUDA_C_64F,
+                         CUSPARSE_SPSV_ALG_DEFAULT, E->sU, &szU);
+        if (!bad) {
+            E->bufL.alloc(std::max<size_t>(szL, 16));
+            E->bufU.alloc(std::max<size_t>(szU, 16));
+            bad = A.svAnalysis(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mL, E->vB, E->vY, CUDA_C_64F,
+                               CUSPARSE_SPSV_ALG_DEFAULT, E->sL, E->bufL.p) ||
+                  A.svAnalysis(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mU, E->vY, E->vB, CUDA_C_64F,
+                               CUSPARSE_SPSV_ALG_DEFAULT, E->sU, E->bufU.p);
+        }
+        if (bad) { set_error("xrl_precond_build_exact: cuSPARSE triangular-solve setup failed"); return XRL_ECUDA; }
+        XRL_CUDA(cudaStreamSynchronize(st));
+        E->dev = true;
+    }
     pc->exact = E.release();
     return XRL_OK;
 }
@@ -236,6 +365,23 @@ void exact_apply(xrl_precond pc, const float2* v, float2* z, int nrhs)
     Api& A = api();
     cudaStream_t st = pc->op->tree->ctx->stream;
     const int N = E->n;
+    if (E->dev) {
+        const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+        for (int c = 0; c < nrhs; ++c) {
+            k_exact_gather<<<(N + 255) / 256, 256, 0, st>>>(N, v + (size_t)c * N, E->gin.p, E->db.p);
+            XRL_LAUNCH_CHECK();
+            if (A.svSolve(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mL, E->vB, E->vY, CUDA_C_64F,
+                          CUSPARSE_SPSV_ALG_DEFAULT, E->sL) ||
+                A.svSolve(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mU, E->vY, E->vB, CUDA_C_64F,
+                          CUSPARSE_SPSV_ALG_DEFAULT, E->sU)) {
+                set_error("xrl_precond_apply: cuSPARSE triangular solve failed");
+                throw CudaError{XRL_ECUDA};
+            }
+            k_exact_scatter<<<(N + 255) / 256, 256, 0, st>>>(N, E->db.p, E->gout.p, z + (size_t)c * N);
+            XRL_LAUNCH_CHECK();
+        }
+        return;
+    }
     E->hv.resize((size_t)nrhs * N);
     XRL_CUDA(cudaMemcpyAsync(E->hv.data(), v, 8 * E->hv.size(), cudaMemcpyDeviceToHost, st));
     XRL_CUDA(cudaStreamSynchronize(st));
