@@ -316,3 +316,19 @@ def test_hybrid_mesh_errors():
     n4 = xrl.Near(tr4)
     a, b = n3.export(), n4.export()
     assert all(np.array_equal(u, v) for u, v in zip(a, b))
+
+
+@pytest.mark.parametrize("npanel", [1, 2, 5])
+def test_degenerate_tiny_meshes(npanel):
+    """Degenerate sizes: 1, 2 and 5 panels (a single leaf, no far field, the self term alone for N = 1);
+    also leaf_max = 1 (every panel its own leaf, the deepest tree) on 5 panels."""
+    rng = np.random.default_rng(npanel)
+    V = rng.normal(size=(3 * npanel, 3)) * 1e-4
+    T = np.arange(3 * npanel, dtype=np.int32).reshape(-1, 3)
+    m = meshes.Mesh(V, T)
+    for leaf in (64, 1):
+        ctx, tree, near = cuda_setup(m, leaf_max=leaf)
+        x = meshes.make_x(1, m.n)
+        err = oracle.rel_l2(run_mvm(tree, near, x), oracle_rows(m, x))
+        print("tiny", npanel, leaf, err)
+        assert err < 1e-6
