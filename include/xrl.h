@@ -209,6 +209,18 @@ xrl_status xrl_mvm_gathered(xrl_tree tree, xrl_near near, const void* x_full, vo
  * [nvec][n_local] in library order (H2D, MVM with the NCCL gather, D2H). */
 xrl_status xrl_mvm_host(xrl_tree tree, xrl_near near, const void* x_host, void* y_host, int32_t nvec,
                         uint32_t flags);
+/* Pipelined end-to-end MVMs over a batch of independent inputs (serving use: many
+ * right-hand-side triples, frequency points or requests).  For k = 0 .. nbatch-1:
+ * y_host[k] = P x_host[k], each a host complex64 [nvec][n] buffer in mesh order
+ * (multi-rank: this rank's [nvec][n_local] slice in library order), every step
+ * with its own host->device copy and device->host read, as xrl_mvm_host.  The
+ * copies run on two library streams double-buffered against the MVMs, so step
+ * k+1's input copy and step k-1's output copy overlap step k's MVM (page-locked
+ * host buffers are needed for the overlap; pageable ones still give the right
+ * result).  Buffers may repeat across k (inputs are only read; outputs are
+ * written in step order).  Blocking; returns when every y_host[k] is written. */
+xrl_status xrl_mvm_host_batch(xrl_tree tree, xrl_near near, const void* const* x_host, void* const* y_host,
+                              int32_t nvec, int32_t nbatch, uint32_t flags);
 
 /* Kernel scheduling of xrl_mvm on this context (no effect on results beyond
  * FP32 summation order of atomics):

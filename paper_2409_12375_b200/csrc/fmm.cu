@@ -1499,4 +1499,84 @@ xrl_status xrl_mvm_host(xrl_tree t, xrl_near nr, const void* x_host, void* y_hos
     }
 }
 
+xrl_status xrl_mvm_host_batch(xrl_tree t, xrl_near nr, const void* const* x_host, void* const* y_host, int32_t nvec,
+                              int32_t nbatch, uint32_t flags)
+{
+    if (!t || !nr || !x_host || !y_host || nbatch < 1) { set_error("xrl_mvm_host_batch: bad argument"); return XRL_EINVAL; }
+    if (nvec < 3 || nvec % 3) { set_error("xrl_mvm_host_batch: nvec must be a positive multiple of 3"); return XRL_EDIM; }
+    for (int k = 0; k < nbatch; ++k)
+        if (!x_host[k] || !y_host[k]) { set_error("xrl_mvm_host_batch: null buffer %d", k); return XRL_EINVAL; }
+    if (t->part_world > 1 && t->ctx->world == 1) { set_error("xrl_mvm_host_batch: virtual partition not supported"); return XRL_EUNSUPPORTED; }
+    struct Res {
+        cudaStream_t cin = nullptr, cout = nullptr;
+        cudaEvent_t in_done[2] = {}, in_free[2] = {}, out_ready[2] = {}, out_free[2] = {};
+        ~Res()
+        {
+            for (int b = 0; b < 2; ++b) {
+                if (in_done[b]) cudaEventDestroy(in_done[b]);
+                if (in_free[b]) cudaEventDestroy(in_free[b]);
+                if (out_ready[b]) cudaEventDestroy(out_ready[b]);
+                if (out_free[b]) cudaEventDestroy(out_free[b]);
+            }
+            if (cin) cudaStreamDestroy(cin);
+            if (cout) cudaStreamDestroy(cout);
+        }
+    } R;
+    try {
+        cudaStream_t st = t->ctx->stream;
+        XRL_CUDA(cudaSetDevice(t->ctx->device));
+        const bool sliced = t->part_world > 1;  // multi-rank: library-order slices, no reordering
+        const size_t cnt = (size_t)nvec * (sliced ? (t->p1 - t->p0) : t->n);
+        for (int b = 0; b < 2; ++b)
+            if (t->xbuf[b].n < cnt) { t->xbuf[b].alloc(cnt); t->ybuf[b].alloc(cnt); }
+        if (!sliced && t->xlib.n < cnt) { t->xtmp.alloc(cnt); t->ytmp.alloc(cnt); t->xlib.alloc(cnt); t->ylib.alloc(cnt); }
+        XRL_CUDA(cudaStreamCreateWithFlags(&R.cin, cudaStreamNonBlocking));
+        XRL_CUDA(cudaStreamCreateWithFlags(&R.cout, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            XRL_CUDA(cudaEventCreateWithFlags(&R.in_done[b], cudaEventDisableTiming));
+            XRL_CUDA(cudaEventCreateWithFlags(&R.in_free[b], cudaEventDisableTiming));
+            XRL_CUDA(cudaEventCreateWithFlags(&R.out_ready[b], cudaEventDisableTiming));
+            XRL_CUDA(cudaEventCreateWithFlags(&R.out_free[b], cudaEventDisableTiming));
+        }
+        // the copy streams start after the work already queued on the context stream
+        XRL_CUDA(cudaEventRecord(R.in_free[0], st));
+        XRL_CUDA(cudaStreamWaitEvent(R.cin, R.in_free[0], 0));
+        XRL_CUDA(cudaStreamWaitEvent(R.cout, R.in_free[0], 0));
+        for (int k = 0; k < nbatch; ++k) {
+            const int b = k & 1;
+            // H2D of step k (buffer b is free once step k-2 has consumed it)
+            if (k >= 2) XRL_CUDA(cudaStreamWaitEvent(R.cin, R.in_free[b], 0));
+            XRL_CUDA(cudaMemcpyAsync(t->xbuf[b].p, x_host[k], cnt * 8, cudaMemcpyHostToDevice, R.cin));
+            XRL_CUDA(cudaEventRecord(R.in_done[b], R.cin));
+            // compute on the context stream
+            XRL_CUDA(cudaStreamWaitEvent(st, R.in_done[b], 0));
+            if (k >= 2) XRL_CUDA(cudaStreamWaitEvent(st, R.out_free[b], 0));  // D2H of step k-2 done with ybuf[b]
+            xrl_status s;
+            if (sliced) {
+                s = xrl_mvm(t, nr, t->xbuf[b].p, t->ybuf[b].p, nvec, flags);
+                if (s) return s;
+                XRL_CUDA(cudaEventRecord(R.in_free[b], st));
+            } else {
+                s = xrl_to_library_order(t, t->xbuf[b].p, t->xlib.p, nvec);
+                if (s) return s;
+                XRL_CUDA(cudaEventRecord(R.in_free[b], st));
+                s = xrl_mvm(t, nr, t->xlib.p, t->ylib.p, nvec, flags);
+                if (s) return s;
+                s = xrl_from_library_order(t, t->ylib.p, t->ybuf[b].p, nvec);
+                if (s) return s;
+            }
+            XRL_CUDA(cudaEventRecord(R.out_ready[b], st));
+            // D2H of step k
+            XRL_CUDA(cudaStreamWaitEvent(R.cout, R.out_ready[b], 0));
+            XRL_CUDA(cudaMemcpyAsync(y_host[k], t->ybuf[b].p, cnt * 8, cudaMemcpyDeviceToHost, R.cout));
+            XRL_CUDA(cudaEventRecord(R.out_free[b], R.cout));
+        }
+        XRL_CUDA(cudaStreamSynchronize(R.cout));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        return XRL_OK;
+    } catch (const CudaError& e) {
+        return e.code;
+    }
+}
+
 }  // extern "C"

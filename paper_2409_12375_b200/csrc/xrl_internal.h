@@ -180,6 +180,7 @@ struct xrl_tree_s {
     xrl::DBuf<float> ellk;                   // [nbox][kEllKStride] ellk[k][8] (leaves, per MVM)
     xrl::DBuf<float> xq;                     // [n][8] packed charges
     xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging
+    xrl::DBuf<float2> xbuf[2], ybuf[2];       // xrl_mvm_host_batch double buffers
 };
 
 struct xrl_near_s {

@@ -24,7 +24,7 @@ EXPORTS = [
     "xrl_last_error", "xrl_version", "xrl_ctx_create", "xrl_ctx_sync", "xrl_ctx_destroy",
     "xrl_tree_build", "xrl_tree_build_poly", "xrl_tree_destroy", "xrl_tree_info", "xrl_tree_perm", "xrl_to_library_order",
     "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble", "xrl_near_destroy",
-    "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_timing_enable", "xrl_timing_count",
+    "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_mvm_host_batch", "xrl_timing_enable", "xrl_timing_count",
     "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_extract",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
@@ -116,6 +116,7 @@ def lib():
         L.xrl_near_export.argtypes = [P, P, P, P, P, P]
         L.xrl_mvm.argtypes = [P, P, P, P, i32, u32]
         L.xrl_mvm_host.argtypes = [P, P, P, P, i32, u32]
+        L.xrl_mvm_host_batch.argtypes = [P, P, P, P, i32, i32, u32]
         L.xrl_timing_enable.argtypes = [P, ctypes.c_int]
         L.xrl_timing_count.restype = i32
         L.xrl_timing_name.argtypes = [i32]
@@ -160,7 +161,7 @@ def lib():
             getattr(L, name).restype = ctypes.c_int32
         for name in ("xrl_ctx_create", "xrl_ctx_sync", "xrl_tree_build", "xrl_tree_build_poly", "xrl_tree_info", "xrl_tree_perm",
                      "xrl_to_library_order", "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble",
-                     "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_timing_enable", "xrl_timing_get",
+                     "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_mvm_host_batch", "xrl_timing_enable", "xrl_timing_get",
                      "xrl_timing_reset"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
@@ -416,6 +417,20 @@ def mvm_host(tree: Tree, near: Near, x_host: np.ndarray, y_host: np.ndarray | No
         y_host = np.empty_like(x_host)
     check(lib().xrl_mvm_host(tree.h, near.h, _ptr(x_host), _ptr(y_host), x_host.shape[0], flags))
     return y_host
+
+
+def mvm_host_batch(tree: Tree, near: Near, x_list, y_list, flags=XRL_MVM_FULL):
+    """xrl_mvm_host_batch: y_list[k] = P x_list[k] for host complex64 [nvec][n] arrays (mesh order), the
+    copies pipelined against the MVMs (pinned arrays overlap; entries may repeat)."""
+    k = len(x_list)
+    assert len(y_list) == k and k > 0
+    nvec = x_list[0].shape[0]
+    for a in list(x_list) + list(y_list):
+        assert a.dtype == np.complex64 and a.flags["C_CONTIGUOUS"] and a.shape == x_list[0].shape
+    xp = (ctypes.c_void_p * k)(*[a.ctypes.data for a in x_list])
+    yp = (ctypes.c_void_p * k)(*[a.ctypes.data for a in y_list])
+    check(lib().xrl_mvm_host_batch(tree.h, near.h, xp, yp, nvec, k, flags))
+    return y_list
 
 
 def esi(sigma: float, zeta: float, freq: float) -> complex:
