@@ -125,7 +125,6 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         if (const char* e = getenv("XRL_SCHED")) c->sched = atoi(e);
         if (const char* e = getenv("XRL_SERIAL"); e && e[0] == '1') c->sched = XRL_SCHED_SERIAL;
         if (c->sched < XRL_SCHED_SERIAL || c->sched > XRL_SCHED_LATE) c->sched = XRL_SCHED_FORK;
-        if (const char* e = getenv("XRL_P2P_TC"); e && e[0] == '1') c->p2p_simt = false;
         upload_constants(c);
         if (world > 1) {
             xrl_status st = comm_init(c, nccl_unique_id);

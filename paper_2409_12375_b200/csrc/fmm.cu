@@ -817,263 +817,6 @@ __global__ void __launch_bounds__(128) k_p2p(
     }
 }
 
-// ------------------------------------------------------------------ P2P on tcgen05
-// Tensor-core P2P: for a tile of <= 128 targets t of one leaf and the U-list
-// sources s, y[t][r] = sum_s G[t][s] q[s][r] with G = 1/|c_t - c_s| (0 for
-// s = t) is a (128 x S) x (S x 6) product.  The sources are read in the padded
-// layout (tree.cu k_pad_positions: every leaf padded to a multiple of 64, padding
-// far away with zero charge), one 64-source chunk of one U leaf at a time:
-//   producer (1 thread): cp.async.bulk of the chunk's X/Y/Z planes (3 x 256 B)
-//     and its charge planes (2 x 2 KB: the B operand [q_hi | 0 0 | q_lo | 0 0],
-//     N = 16, canonical K-major) into a ring of 6 shared-memory slots;
-//   G warps (8; thread = target = TMEM lane, source half w / 4): packed f32x2
-//     differences to the target shifted into the U leaf's frame, MUFU rsqrt,
-//     TF32 hi (truncation) / lo split, tcgen05.st into a ring of 3 TMEM slots;
-//   MMA warp: D[t][0..15] += G_hi B + G_lo B (2 x tcgen05.mma kind::tf32 M128
-//     N16 K8 per 8 sources), 3xTF32 accuracy; y = (D[.][r] + D[.][8 + r]) / W.
-// The 6 FFMA/pair accumulation of the SIMT kernel moves to the tensor core; the
-// CUDA cores do 3.5 FP32-pipe ops + 1 MUFU per pair.
-constexpr int kPtChunk = 64;                    // sources per chunk (one U leaf)
-constexpr int kPtSlots = 6;                     // shared-memory staging slots
-constexpr int kPtTSlots = 3;                    // TMEM G slots (128 columns each)
-constexpr int kPtGW = 16;                       // G warps (4 per TMEM lane quarter)
-constexpr int kPtThreads = (kPtGW + 2) * 32;    // + 1 producer + 1 MMA warp
-constexpr uint32_t kPtColD = 384;               // two 16-column accumulators (tile parity)
-constexpr uint32_t kPtBytes = 3 * kPtChunk * 4 + 2 * kPtChunk * 32;  // positions + charge planes
-struct __align__(128) PtSlot {
-    float X[kPtChunk], Y[kPtChunk], Z[kPtChunk];  // local coordinates in the U leaf's frame (W units)
-    float Q[2 * kPtChunk * 8];                     // B operand: hi plane, lo plane [k/4][8 rows][4] (K-major, 4 KB)
-    float ux, uy, uz;                              // U leaf centre - target leaf centre
-    int nvalid, flags;                             // flags: bit 0 last chunk, bit 1 own leaf (self pairs)
-};
-
-__device__ __forceinline__ void lds_v2_u64(const void* p, f2x& a, f2x& b)
-{
-    asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"((unsigned)__cvta_generic_to_shared(p)));
-}
-
-// G for one thread's target and 16 sources (quarter hf of the chunk), TF32 hi/lo into TMEM columns col ..
-// (hi) and col + 64 .. (lo): per 2 sources 3 FADD2 + FMUL2 + 2 FFMA2 + 2 MUFU + 2 LOP3 + FADD2.
-template <bool kSelf, typename Slot>
-__device__ __forceinline__ void pt_g_half(const Slot& S, int hf, float ax, float ay, float az, uint32_t col)
-{
-    const f2x txx = pk2(ax, ax), tyy = pk2(ay, ay), tzz = pk2(az, az);
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {  // 8 sources per tcgen05.st
-        float gh[8], gl[8];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {  // 4 sources per 128-bit shared load
-            const int sidx = 16 * hf + 8 * g + 4 * e;
-            f2x x0, x1, y0, y1, z0, z1;
-            lds_v2_u64(&S.X[sidx], x0, x1);
-            lds_v2_u64(&S.Y[sidx], y0, y1);
-            lds_v2_u64(&S.Z[sidx], z0, z1);
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const f2x dx = sub2(u ? x1 : x0, txx), dy = sub2(u ? y1 : y0, tyy), dz = sub2(u ? z1 : z0, tzz);
-                const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
-                float ra = rsqrt_ftz(r2.x), rb = rsqrt_ftz(r2.y);
-                if (kSelf) {
-                    ra = r2.x > 0.f ? ra : 0.f;
-                    rb = r2.y > 0.f ? rb : 0.f;
-                }
-                const float ha = __uint_as_float(__float_as_uint(ra) & 0xFFFFE000u);
-                const float hb = __uint_as_float(__float_as_uint(rb) & 0xFFFFE000u);
-                const int o = 4 * e + 2 * u;
-                gh[o] = ha; gh[o + 1] = hb;
-                const float2 l = upk2(sub2(pk2(ra, rb), pk2(ha, hb)));
-                gl[o] = l.x; gl[o + 1] = l.y;
-            }
-        }
-        tc::tmem_st8(col + 8 * g, gh);
-        tc::tmem_st8(col + 64 + 8 * g, gl);
-    }
-}
-
-// charges -> padded K-major B planes [hi | lo][npad / 4][8 rows][4 sources]: padded source i, RHS r < 6
-// at plane + (i/4)*32 + r*4 + i%4 (rows 6, 7 stay zero)
-__global__ void k_pack_pad(int64_t n, const float* __restrict__ xq, const int32_t* __restrict__ ppos, int64_t npad,
-                           float* __restrict__ padq)
-{
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const float4 a = reinterpret_cast<const float4*>(xq + 8 * i)[0];
-    const float2 c = reinterpret_cast<const float2*>(xq + 8 * i)[2];
-    const float q[6] = {a.x, a.y, a.z, a.w, c.x, c.y};
-    const int64_t pi = ppos[i];
-    float* hi = padq + (pi >> 2) * 32 + (pi & 3);
-    float* lo = hi + npad * 8;
-#pragma unroll
-    for (int r = 0; r < 6; ++r) {
-        const float h = __uint_as_float(__float_as_uint(q[r]) & 0xFFFFE000u);
-        hi[r * 4] = h;
-        lo[r * 4] = q[r] - h;
-    }
-}
-
-__global__ void __launch_bounds__(kPtThreads, 1) k_p2p_tc(
-    const int4* __restrict__ ptiles, int ntiles, const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
-    const int32_t* __restrict__ iy, const int32_t* __restrict__ iz, const int32_t* __restrict__ pb,
-    const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
-    const int32_t* __restrict__ pstart, const float* __restrict__ padx, const float* __restrict__ pady,
-    const float* __restrict__ padz, const float* __restrict__ padq, int64_t npad, const float4* __restrict__ loc,
-    float invW, int accumulate, int64_t n, int64_t p0, float2* __restrict__ y)
-{
-    // persistent: CTA i handles target tiles i, i + gridDim.x, ... (Morton order: the CTAs in flight
-    // work on neighbouring leaves, whose U lists share sources in L2)
-    __shared__ PtSlot slot[kPtSlots];
-    __shared__ uint64_t staged[kPtSlots], sfree[kPtSlots], gfull[kPtTSlots], gfree[kPtTSlots], d_full[2], d_free[2];
-    __shared__ uint32_t tbase;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int k = 0; k < kPtSlots; ++k) {
-            tc::mbar_init(&staged[k], 1);
-            tc::mbar_init(&sfree[k], 1);
-        }
-        for (int k = 0; k < kPtTSlots; ++k) {
-            tc::mbar_init(&gfull[k], kPtGW);
-            tc::mbar_init(&gfree[k], 1);
-        }
-        for (int k = 0; k < 2; ++k) {
-            tc::mbar_init(&d_full[k], 1);
-            tc::mbar_init(&d_free[k], kPtGW);
-        }
-    }
-    if (warp == kPtGW + 1) tc::tmem_alloc<512>(&tbase);
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-
-    if (warp < kPtGW) {
-        // ---------------- G warps: thread = target (TMEM lane), half of each chunk's sources
-        const uint32_t tm = tbase;
-        const int qd = warp & 3, hf = warp >> 2;  // lane quarter, source quarter of the chunk
-        const int ti = 32 * qd + lane;
-        const uint32_t ta = tm + ((uint32_t)(32 * qd) << 16);
-        int c = 0;
-        for (int tl = blockIdx.x, tj = 0; tl < ntiles; tl += gridDim.x, ++tj) {
-            const int4 tile = ptiles[tl];
-            const int t0 = tile.y, T = tile.z;
-            float tx = 1e18f, ty = 1e18f, tz = 1e18f;  // padding target: far away, discarded
-            if (ti < T) {
-                const float4 q = loc[t0 + ti];
-                tx = q.x; ty = q.y; tz = q.z;
-            }
-            for (;; ++c) {
-                const int k = c % kPtSlots, tk = c % kPtTSlots;
-                PtSlot& S = slot[k];
-                tc::mbar_wait(&staged[k], (c / kPtSlots) & 1);
-                tc::mbar_wait(&gfree[tk], ((c / kPtTSlots) & 1) ^ 1);  // MMAs of chunk c - 3 done with TMEM slot tk
-                tc::fence_after();
-                const int flags = S.flags;
-                // target in the U leaf's frame: c_t - c_s = (t - Ud) - s
-                const float ax = tx - S.ux, ay = ty - S.uy, az = tz - S.uz;
-                const uint32_t col = ta + (uint32_t)(tk * 128 + 16 * hf);
-                // padding sources of the chunk are far away with zero charge: no per-source masking
-                if (flags & 2) pt_g_half<true>(S, hf, ax, ay, az, col);
-                else pt_g_half<false>(S, hf, ax, ay, az, col);
-                tc::tmem_st_wait();
-                tc::fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&gfull[tk]);
-                if (flags & 1) { ++c; break; }
-            }
-            // tile accumulator complete: write y (warps with hf == 0), hand the D buffer back
-            const int dp = tj & 1;
-            tc::mbar_wait(&d_full[dp], (tj >> 1) & 1);
-            tc::fence_after();
-            float v[16];
-            tc::tmem_ld16(ta + kPtColD + 16 * dp, v);
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&d_free[dp]);
-            if (hf == 0 && ti < T) {
-                const int64_t kk = t0 + ti - p0;
-                float tot[6];
-#pragma unroll
-                for (int r = 0; r < 6; ++r) tot[r] = (v[r] + v[8 + r]) * invW;
-                if (accumulate) {
-                    const float2 a = y[kk], cc = y[n + kk], d = y[2 * n + kk];
-                    tot[0] += a.x; tot[1] += a.y; tot[2] += cc.x; tot[3] += cc.y; tot[4] += d.x; tot[5] += d.y;
-                }
-                y[kk] = make_float2(tot[0], tot[1]);
-                y[n + kk] = make_float2(tot[2], tot[3]);
-                y[2 * n + kk] = make_float2(tot[4], tot[5]);
-            }
-        }
-    } else if (warp == kPtGW) {
-        // ---------------- producer: one chunk = 64 padded sources of one U leaf, bulk copies
-        if (lane == 0) {
-            int c = 0;
-            for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-                const int b = ptiles[tl].x;
-                const float3 cb = box_center(level[b], ix[b], iy[b], iz[b]);
-                const int64_t u0 = uptr[b], u1 = uptr[b + 1];
-                int64_t qlast = u1 - 1;  // last U leaf with panels
-                while (qlast > u0 && pe[usrc[qlast]] == pb[usrc[qlast]]) --qlast;
-                for (int64_t q = u0; q <= qlast; ++q) {
-                    const int u = usrc[q];
-                    const int nb = pe[u] - pb[u], ps = pstart[u];
-                    if (nb == 0) continue;
-                    const float3 cu = box_center(level[u], ix[u], iy[u], iz[u]);
-                    for (int j0 = 0; j0 < nb; j0 += kPtChunk, ++c) {
-                        const int k = c % kPtSlots;
-                        PtSlot& S = slot[k];
-                        tc::mbar_wait(&sfree[k], ((c / kPtSlots) & 1) ^ 1);  // MMAs of chunk c - 6 done with slot k
-                        S.ux = cu.x - cb.x; S.uy = cu.y - cb.y; S.uz = cu.z - cb.z;
-                        S.nvalid = min(kPtChunk, nb - j0);
-                        const bool last = q == qlast && j0 + kPtChunk >= nb;
-                        S.flags = (last ? 1 : 0) | (u == b ? 2 : 0);
-                        mbar_expect_tx(&staged[k], kPtBytes);
-                        const int64_t i0 = ps + j0;
-                        bulk_g2s(S.X, padx + i0, kPtChunk * 4, &staged[k]);
-                        bulk_g2s(S.Y, pady + i0, kPtChunk * 4, &staged[k]);
-                        bulk_g2s(S.Z, padz + i0, kPtChunk * 4, &staged[k]);
-                        bulk_g2s(S.Q, padq + i0 * 8, kPtChunk * 32, &staged[k]);
-                        bulk_g2s(S.Q + kPtChunk * 8, padq + ((size_t)npad + i0) * 8, kPtChunk * 32, &staged[k]);
-                    }
-                }
-            }
-        }
-    } else {
-        // ---------------- MMA issuer (whole warp, one elected lane issues)
-        const uint32_t tmu = tbase;
-        // tf32, M128 N16, B K-major: element (n, k) at (n/8)*2048 + (k/4)*128 + (n%8)*16 + (k%4)*4 bytes
-        const uint32_t idesc = tc::idesc_tf32(128, 16);
-        int c = 0;
-        for (int tl = blockIdx.x, tj = 0; tl < ntiles; tl += gridDim.x, ++tj) {
-            const int dp = tj & 1;
-            mbar_wait_warp(&d_free[dp], ((tj >> 1) & 1) ^ 1);  // the G warps have read this D buffer
-            tc::fence_after();
-            const uint32_t dcol = tmu + kPtColD + 16 * dp;
-            for (bool first = true;; ++c, first = false) {
-                const int k = c % kPtSlots, tk = c % kPtTSlots;
-                mbar_wait_warp(&staged[k], (c / kPtSlots) & 1);
-                mbar_wait_warp(&gfull[tk], (c / kPtTSlots) & 1);
-                tc::fence_after();
-                const int flags = slot[k].flags;
-                if (tc::elect_one()) {
-                    const uint32_t bq = tc::smem_u32(slot[k].Q);
-#pragma unroll
-                    for (int ks = 0; ks < kPtChunk / 8; ++ks) {
-                        const uint64_t bd = tc::smem_desc(bq + 256 * ks, 128, 2048);
-                        tc::mma_tf32_ts(dcol, tmu + tk * 128 + 8 * ks, bd, idesc, (first && ks == 0) ? 0u : 1u);
-                        tc::mma_tf32_ts(dcol, tmu + tk * 128 + 64 + 8 * ks, bd, idesc, 1u);
-                    }
-                    tc::commit(&gfree[tk]);
-                    tc::commit(&sfree[k]);
-                    if (flags & 1) tc::commit(&d_full[dp]);
-                }
-                __syncwarp();
-                if (flags & 1) { ++c; break; }
-            }
-        }
-    }
-    tc::fence_before();
-    __syncthreads();
-    if (warp == kPtGW + 1) tc::tmem_dealloc<512>(tbase);
-}
-
 // ell[r][k] (r-major, M2L/L2L layout) -> ellk[k][8] (k-major, 6 RHS + 2 pad) for the leaves: the L2P
 // then reads one 32-byte record per coefficient instead of 6 scalars.
 __global__ void k_ell_kmajor(const int32_t* __restrict__ leaves, const float* __restrict__ ell, float* __restrict__ ellk)
@@ -1284,16 +1027,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         // (memory-bound) after it accumulates into y
         if (do_far) {
             phase_begin(ctx, PH_P2P, &ev, side);
-            if (t->n_p2p_tiles > 0 && !ctx->p2p_simt) {
-                k_pack_pad<<<nblk(n, 256), 256, 0, side>>>(n, t->xq.p, t->ppos.p, t->npad, t->padq.p);
-                XRL_LAUNCH_CHECK();
-                ctx->launches += 1;
-                k_p2p_tc<<<std::min(ctx->num_sms, t->n_p2p_tiles), kPtThreads, 0, side>>>(
-                    t->p2p_tiles.p, t->n_p2p_tiles, t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p,
-                    t->u_src.p, t->pstart.p, t->padx.p, t->pady.p, t->padz.p, t->padq.p, t->npad, t->loc.p, invW, 0,
-                    nl, p0, y);
-            }
-            else if (t->n_own_leaves > 0)
+            if (t->n_own_leaves > 0)
                 k_p2p<<<t->n_own_leaves, 128, kP2PSmem, side>>>(t->own_leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
                                                          t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
                                                          invW, 0, nl, p0, y);

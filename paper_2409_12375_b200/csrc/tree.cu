@@ -428,29 +428,6 @@ __global__ void k_panel_leaf(int nleaf, const int32_t* __restrict__ leaves, cons
     }
 }
 
-// Tensor-core P2P source layout: every leaf's panels padded to a multiple of 64
-// (kPadChunk) in "padded order"; planes X/Y/Z of the local coordinates (FP32, W
-// units, relative to the panel's leaf centre; padding entries far away) and,
-// per MVM, the charge planes (k_pack_pad in fmm.cu).  ppos[i] = padded index.
-__global__ void k_pad_positions(int nleaf, const int32_t* __restrict__ leaves, const int32_t* __restrict__ pb,
-                                const int32_t* __restrict__ pe, const int32_t* __restrict__ pstart,
-                                const float4* __restrict__ loc, int64_t npad, float* __restrict__ px,
-                                float* __restrict__ py, float* __restrict__ pz, int32_t* __restrict__ ppos)
-{
-    const int b = leaves[blockIdx.x];
-    const int n0 = pb[b], nb = pe[b] - pb[b], s0 = pstart[b];
-    const int np = (nb + 63) & ~63;
-    for (int j = threadIdx.x; j < np; j += blockDim.x) {
-        float4 v = make_float4(1e18f, 1e18f, 1e18f, 0.f);
-        if (j < nb) {
-            v = loc[n0 + j];
-            ppos[n0 + j] = s0 + j;
-        }
-        px[s0 + j] = v.x;
-        py[s0 + j] = v.y;
-        pz[s0 + j] = v.z;
-    }
-}
 
 __global__ void k_box_dmax(int nbox, const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
                            const double* __restrict__ dmax, double* bd)
@@ -691,30 +668,6 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
                                            T->biz.p, T->cent.p, T->lo[0], T->lo[1], T->lo[2], invW,
                                            T->panel_leaf.p, T->loc.p);
     XRL_LAUNCH_CHECK();
-    {  // padded source layout for the tensor-core P2P
-        std::vector<int32_t> hpb_(nbox), hpe_(nbox);
-        XRL_CUDA(cudaMemcpyAsync(hpb_.data(), T->bpb.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaMemcpyAsync(hpe_.data(), T->bpe.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaStreamSynchronize(st));
-        std::vector<int32_t> hps(nbox, -1);
-        int64_t off = 0;
-        for (int32_t b : hleaves) {
-            hps[b] = (int32_t)off;
-            off += ((hpe_[b] - hpb_[b]) + 63) & ~63;
-        }
-        T->npad = off;
-        T->pstart.alloc(nbox);
-        XRL_CUDA(cudaMemcpyAsync(T->pstart.p, hps.data(), 4 * nbox, cudaMemcpyHostToDevice, st));
-        const size_t np = (size_t)std::max<int64_t>(64, off);
-        T->padx.alloc(np); T->pady.alloc(np); T->padz.alloc(np);
-        T->ppos.alloc(n);
-        T->padq.alloc(np * 16);
-        XRL_CUDA(cudaMemsetAsync(T->padq.p, 0, T->padq.bytes(), st));
-        k_pad_positions<<<T->nleaf, 128, 0, st>>>(T->nleaf, T->leaves.p, T->bpb.p, T->bpe.p, T->pstart.p, T->loc.p,
-                                                  off, T->padx.p, T->pady.p, T->padz.p, T->ppos.p);
-        XRL_LAUNCH_CHECK();
-        XRL_CUDA(cudaStreamSynchronize(st));
-    }
     T->bdmax.alloc(nbox);
     k_box_dmax<<<nbox, 128, 0, st>>>(nbox, T->bpb.p, T->bpe.p, T->dmax.p, T->bdmax.p);
     XRL_LAUNCH_CHECK();
@@ -888,22 +841,6 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         T->n_own_leaves = (int)own.size();
         T->own_leaves.alloc(std::max<size_t>(1, own.size()));
         if (!own.empty()) XRL_CUDA(cudaMemcpyAsync(T->own_leaves.p, own.data(), 4 * own.size(), cudaMemcpyHostToDevice, st));
-        // tensor-core P2P target tiles (leaf, first panel, #targets <= 128, #U sources)
-        {
-            std::vector<int4> pt;
-            for (int L : own) {
-                int64_t ns = 0;
-                for (int64_t q = hup[L]; q < hup[L + 1]; ++q) ns += hpe[hus[q]] - hpb[hus[q]];
-                for (int t0 = hpb[L]; t0 < hpe[L]; t0 += 128)
-                    pt.push_back(make_int4(L, t0, std::min(128, hpe[L] - t0), (int)std::min<int64_t>(ns, INT32_MAX)));
-            }
-            // Morton order (own leaves are in Morton order): neighbouring tiles share U-list sources in L2
-            T->n_p2p_tiles = (int)pt.size();
-            T->p2p_tiles.alloc(std::max<size_t>(1, pt.size()));
-            if (!pt.empty())
-                XRL_CUDA(cudaMemcpyAsync(T->p2p_tiles.p, pt.data(), sizeof(int4) * pt.size(), cudaMemcpyHostToDevice, st));
-            XRL_CUDA(cudaStreamSynchronize(st));
-        }
         // relevant boxes: panel range meets [p0, p1) (owned subtrees and their ancestors)
         T->rel.assign(nbox, 0);
         for (int b = 0; b < nbox; ++b) T->rel[b] = hpb[b] < T->p1 && hpe[b] > T->p0;

@@ -95,7 +95,6 @@ struct xrl_ctx_s {
     // timing
     bool timing = false;
     int sched = XRL_SCHED_FORK;       // xrl_ctx_set_sched
-    bool p2p_simt = true;             // XRL_P2P_TC=1: experimental tensor-core P2P (k_p2p_tc)
     int num_sms = 148;
     int64_t launches = 0;
     int refs = 0;         // live trees
@@ -161,12 +160,6 @@ struct xrl_tree_s {
     std::vector<uint8_t> rel;                // box relevant to this rank
     xrl::DBuf<int32_t> own_leaves;           // owned leaves (Morton order)
     int32_t n_own_leaves = 0;
-    xrl::DBuf<int4> p2p_tiles;               // tensor-core P2P: (leaf, first panel, #targets <= 128, #sources)
-    xrl::DBuf<int32_t> pstart, ppos;         // padded source layout: leaf start (multiple of 64), panel -> padded
-    xrl::DBuf<float> padx, pady, padz;       // padded local coordinates (W units)
-    xrl::DBuf<float> padq;                   // padded charge planes [4][npad][4] (TF32 hi 0..5, lo 0..5), per MVM
-    int64_t npad = 0;
-    int32_t n_p2p_tiles = 0;
     std::vector<int32_t> l2l_start;          // per-level offsets into l2l_boxes
     xrl::DBuf<int32_t> l2l_boxes;
     xrl::DBuf<float2> xfull;                 // gathered x (multi-rank MVM)
