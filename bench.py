@@ -405,6 +405,7 @@ def run_xrl(args):
         "e2e": {"value": e2e_value, "unit": "Mpanels/s", "h2d_bytes_per_step": int(xh.numel() * 8),
                 "d2h_bytes_per_step": int(yh.numel() * 8),
                 "api": "xrl_mvm_host_batch over the timed steps (copies double-buffered against the MVMs)",
+                "l2": "not flushed inside the batch; each step streams > 1.5 GB (near CSR + copies), above L2",
                 "unpipelined_value": e2e_single,
                 "unpipelined_api": "one blocking xrl_mvm_host call per step (L2 flushed between calls)"},
         "gpu_launches": launches,
