@@ -220,7 +220,7 @@ def test_host_api_e2e(bar_setup):
     assert oracle.rel_l2(y_host, y_dev) < 1e-6
 
 
-@pytest.mark.parametrize("cfg,nrows,leaf", [(2, 1024, 64), (3, 512, 64), (4, 256, 64), (4, 256, 352), (4, 256, 512), (5, 128, 352)])
+@pytest.mark.parametrize("cfg,nrows,leaf", [(2, 1024, 64), (2, 1024, 352), (3, 512, 64), (3, 512, 352), (4, 256, 64), (4, 256, 352), (4, 256, 512), (5, 128, 352)])
 def test_full_mvm_sampled_rows(cfg, nrows, leaf):
     """Full-size configs on sampled rows; (4, leaf 512) is bench.py's launch configuration."""
     m = meshes.make_config(cfg)
