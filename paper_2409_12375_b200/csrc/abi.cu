@@ -121,6 +121,8 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         XRL_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_work, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_m2l, cudaEventDisableTiming));
+        if (const char* e = getenv("XRL_FUSE"); e && e[0] == '0') c->fuse_p2p = false;
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         if (const char* e = getenv("XRL_SCHED")) c->sched = atoi(e);
         if (const char* e = getenv("XRL_SERIAL"); e && e[0] == '1') c->sched = XRL_SCHED_SERIAL;
@@ -166,6 +168,7 @@ void xrl::ctx_release(xrl_ctx ctx)
     if (ctx->work) { cudaStreamSynchronize(ctx->work); cudaStreamDestroy(ctx->work); }
     if (ctx->ev_work) cudaEventDestroy(ctx->ev_work);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_m2l) cudaEventDestroy(ctx->ev_m2l);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -124,10 +124,10 @@ __device__ __forceinline__ int degree_of(int i)
 // One persistent CTA per SM; blocks (runs of tiles with one (chunk, offset))
 // dealt round-robin, so all CTAs work inside one L2-resident target chunk.
 constexpr int kTcPairs = 21;                        // pairs per tile (126 of 128 TMEM lanes)
-constexpr int kTcThreads = 288;                     // 4 loader + 4 drain + 1 MMA warps
+constexpr int kTcThreads = 352;                     // 4 loader + 4 drain + 1 MMA warps + 2 fused-P2P warps
 constexpr int kTcOpBytes = 128 * 128 * 4;           // one operator part (hi or lo): 64 KB
 constexpr int kTcStageLd = 132;                     // drain stage row stride (floats; conflict-free STS.128)
-constexpr int kTcSmem = 2 * kTcOpBytes + 128 * kTcStageLd * 4 + 1024;  // operator hi + lo, drain stage (+ align)
+constexpr int kTcSmem = 2 * kTcOpBytes + 128 * kTcStageLd * 4 + 1024 + 512 * 12 * 4;  // operator hi + lo, drain stage (+ align), fused-P2P staging
 constexpr uint32_t kTcColAh = 0, kTcColAl = 128, kTcColD = 256;  // D buffers at 256 and 384
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar)
@@ -184,6 +184,41 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t phase)
 }
 
 
+// ---------------------------------------------------------------- P2P tasks (shared with k_m2l_tc)
+constexpr int kUWin = 64;
+// Shared-memory scratch of one P2P leaf task (window of U-list leaves).
+struct P2PWin {
+    int Uoff[kUWin + 1], Uid[kUWin], Upb[kUWin];
+    float3 Ud[kUWin];
+    int wsum[2];
+};
+
+template <int kNT, int kChunk, int kBar>
+__device__ void p2p_leaf(int b, int tid, float* smraw, P2PWin& W, const int32_t* __restrict__ level,
+                         const int32_t* __restrict__ ix, const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
+                         const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
+                         const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
+                         const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate,
+                         int64_t n, int64_t p0, float2* __restrict__ y);
+
+// P2P leaf tasks handed to the M2L kernel's two spare warps (leaves[counter++] while the M2L runs; the
+// standalone k_p2p takes the rest from the same counter).  leaves == nullptr: no fused P2P.
+struct P2PTasks {
+    const int32_t* leaves;
+    int nleaves;
+    int* counter;
+    const int32_t *level, *ix, *iy, *iz, *pb, *pe;
+    const int64_t* uptr;
+    const int32_t* usrc;
+    const float4* loc;
+    const float* xq;
+    float invW;
+    int64_t n, p0;
+    float2* y;
+};
+constexpr int kFuseChunk = 512;                          // sources staged per chunk by the fused P2P warps
+constexpr int kFuseSmem = kFuseChunk * 12 * 4;           // their staging / reduction buffer (bytes)
+
 // This CTA's tile sequence: blocks blockIdx.x, blockIdx.x + gridDim.x, ...; all tiles of each block.
 struct TileSeq {
     int bi, ti, tend;
@@ -213,14 +248,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                                                           const int32_t* __restrict__ srcb,
                                                           const float* __restrict__ opimg,
                                                           const float* __restrict__ bimg, float* __restrict__ ell,
-                                                          int dbg)
+                                                          int dbg, P2PTasks p2p)
 {
     extern __shared__ uint8_t tsm_raw[];
     uint8_t* opsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
     float* stage = reinterpret_cast<float*>(opsm + 2 * kTcOpBytes);  // [128 rows][kTcStageLd]
+    float* p2p_sm = stage + 128 * kTcStageLd;                          // fused P2P staging (kFuseSmem)
     __shared__ uint64_t a_full[2], a_free[2], d_full[2], d_free[2], op_full;
     __shared__ uint32_t tbase;
+    __shared__ int m2l_live, p2p_task;
+    __shared__ P2PWin p2p_win;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) m2l_live = 9;  // warps of the translation roles still running
     if (tid == 0) {
         for (int h = 0; h < 2; ++h) {
             tc::mbar_init(&a_full[h], 4);
@@ -236,7 +275,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
     tc::fence_after();
     const uint32_t tm = tbase;
 
-    if (warp < 4) {
+    if (warp >= 9) {
+        // ---------------- fused P2P: two warps take target-leaf tasks from the shared counter while the
+        // translation roles run (the M2L is bound by L2 traffic and leaves the FP32 pipes idle)
+        if (p2p.leaves) {
+            const int tp = tid - 9 * 32;
+            for (;;) {
+                if (tp == 0) p2p_task = *(volatile int*)&m2l_live > 0 ? atomicAdd(p2p.counter, 1) : INT_MAX;
+                asm volatile("bar.sync 1, 64;" ::: "memory");
+                const int task = p2p_task;
+                if (task >= p2p.nleaves) break;
+                p2p_leaf<64, kFuseChunk, 1>(p2p.leaves[task], tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
+                                            p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, 0, p2p.n,
+                                            p2p.p0, p2p.y);
+            }
+        }
+    } else if (warp < 4) {
         // ---------------- loaders: thread = TMEM lane L = (p, r).  A K-half of the multipole row
         // (64 floats, 8 x 256-bit loads: whole 32-byte sectors per lane) is prefetched into
         // registers half a tile ahead of its use; tile descriptors and source ids a tile ahead.
@@ -401,6 +455,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             }
         }
     }
+    if (warp < 9 && lane == 0) atomicSub(&m2l_live, 1);
     tc::fence_before();
     __syncthreads();
     if (warp == 8) tc::tmem_dealloc<512>(tbase);
@@ -588,7 +643,6 @@ __global__ void __launch_bounds__(256, 6) k_near_spmv(int64_t n, int64_t r0, con
 // memory re-based to the target leaf centre (W units), and split over the
 // groups.  Only the target's own leaf needs the r = 0 (self) guard.
 // y += (1/W) sum_{l != k} x_l / r_kl.
-constexpr int kUWin = 64;
 constexpr int kSrcChunk = 1024;
 constexpr int kP2PSmem = (kSrcChunk * 12 > 128 * (4 * 6 + 1) * 2 ? kSrcChunk * 12 : 128 * (4 * 6 + 1) * 2) * 4;
 constexpr int kTPT = 8;
@@ -685,29 +739,39 @@ __device__ __forceinline__ int first_in_class(int lo, int sg, int S)
     return lo + ((sg - r + S) % S);
 }
 
-__global__ void __launch_bounds__(128) k_p2p(
-    const int32_t* __restrict__ leaves, const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
+
+// P2P of one target leaf b by kNT threads (tid 0..kNT-1) synchronised with barrier kBar (0:
+// __syncthreads, else a named barrier of kNT threads); smraw: kChunk * 12 floats of staging, also the
+// reduction buffer (>= kNT * (kTP2 * 6 + 1) * 2 floats).
+template <int kNT, int kChunk, int kBar>
+__device__ void p2p_leaf(
+    int b, int tid, float* smraw, P2PWin& W, const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
     const int32_t* __restrict__ iy, const int32_t* __restrict__ iz, const int32_t* __restrict__ pb,
     const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
     const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate, int64_t n,
     int64_t p0, float2* __restrict__ y)
 {
+    static_assert(kNT >= kUWin && kChunk * 12 >= kNT * (kTP2 * 6 + 1) * 2, "P2P task shape");
     // n, p0: owned panel range [p0, p0+n), y local [3][n]
-    // the source staging buffers and the final reduction share one buffer
-    extern __shared__ __align__(16) float smraw[];  // kP2PSmem: source staging, then the reduction
+    // the source staging buffers and the final reduction share one buffer (smraw)
     float4* Sp = reinterpret_cast<float4*>(smraw);
-    float4(*Sq)[2] = reinterpret_cast<float4(*)[2]>(smraw + 4 * kSrcChunk);
+    float4(*Sq)[2] = reinterpret_cast<float4(*)[2]>(smraw + 4 * kChunk);
     f2x(*Red)[kTP2 * 6 + 1] = reinterpret_cast<f2x(*)[kTP2 * 6 + 1]>(smraw);  // packed target pairs
-    __shared__ int Uoff[kUWin + 1], Uid[kUWin], Upb[kUWin];
-    __shared__ float3 Ud[kUWin];
-    __shared__ int wsum[2];
-    const int b = leaves[blockIdx.x];
+    int* Uoff = W.Uoff;
+    int* Uid = W.Uid;
+    int* Upb = W.Upb;
+    float3* Ud = W.Ud;
+    int* wsum = W.wsum;
     const float3 cb = box_center(level[b], ix[b], iy[b], iz[b]);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int t0 = pb[b]; t0 < pe[b]; t0 += 128 * kTPT) {
-        const int T = min(128 * kTPT, pe[b] - t0);
+    const int lane = tid & 31, warp = tid >> 5;
+    auto sync = [&]() {
+        if (kBar == 0) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(kBar), "r"(kNT) : "memory");
+    };
+    for (int t0 = pb[b]; t0 < pe[b]; t0 += kNT * kTPT) {
+        const int T = min(kNT * kTPT, pe[b] - t0);
         const int NG = (T + kTPT - 1) / kTPT;
-        const int S = max(1, 128 / NG);
+        const int S = max(1, kNT / NG);
         const int tg = tid % NG, sg = tid / NG;
         const bool act = sg < S;
         f2x tx[kTP2], ty[kTP2], tz[kTP2];
@@ -735,7 +799,7 @@ __global__ void __launch_bounds__(128) k_p2p(
         }
         for (int64_t u0 = uptr[b]; u0 < uptr[b + 1]; u0 += kUWin) {
             const int nu = (int)min((int64_t)kUWin, uptr[b + 1] - u0);
-            __syncthreads();
+            sync();
             // window setup: ids, centre shifts and an exclusive prefix of the leaf sizes (2 warps)
             int sz = 0;
             if (tid < kUWin) {
@@ -756,19 +820,19 @@ __global__ void __launch_bounds__(128) k_p2p(
                 if (lane == 31) wsum[warp] = inc;
                 Uoff[tid + 1] = inc;  // provisional (warp-local)
             }
-            __syncthreads();
+            sync();
             if (tid >= 32 && tid < kUWin) Uoff[tid + 1] += wsum[0];
             if (tid == 0) Uoff[0] = 0;
-            __syncthreads();
+            sync();
             const int total = Uoff[nu];
             // the target leaf's own panels in the flattened window (needs the r = 0 guard)
             int self_lo = 0, self_hi = 0;
             for (int i = 0; i < nu; ++i)
                 if (Uid[i] == b) { self_lo = Uoff[i]; self_hi = Uoff[i + 1]; }
-            for (int s0 = 0; s0 < total; s0 += kSrcChunk) {
-                const int sn = min(kSrcChunk, total - s0);
-                if (s0 > 0) __syncthreads();
-                for (int j = tid; j < sn; j += 128) {
+            for (int s0 = 0; s0 < total; s0 += kChunk) {
+                const int sn = min(kChunk, total - s0);
+                if (s0 > 0) sync();
+                for (int j = tid; j < sn; j += kNT) {
                     const int f = s0 + j;
                     const int li = find_seg(Uoff, nu, f);
                     const int i = Upb[li] + (f - Uoff[li]);
@@ -779,7 +843,7 @@ __global__ void __launch_bounds__(128) k_p2p(
                     Sq[j][0] = q[0];
                     Sq[j][1] = q[1];
                 }
-                __syncthreads();
+                sync();
                 if (act) {
                     const int a0 = max(0, min(sn, self_lo - s0)), a1 = max(0, min(sn, self_hi - s0));
                     p2p_range<false>(first_in_class(0, sg, S), a0, S, Sp, Sq, tx, ty, tz, acc);
@@ -788,14 +852,14 @@ __global__ void __launch_bounds__(128) k_p2p(
                 }
             }
         }
-        __syncthreads();
+        sync();
 #pragma unroll
         for (int q = 0; q < kTP2; ++q)
 #pragma unroll
             for (int r = 0; r < 6; ++r) st_shared_u64(&Red[tid][q * 6 + r], acc[q][r]);
-        __syncthreads();
+        sync();
         // reduce over the S source groups: thread handles target index ti = tid, tid + 128, ...
-        for (int ti = tid; ti < T; ti += 128) {
+        for (int ti = tid; ti < T; ti += kNT) {
             const int g0 = ti / kTPT, q = (ti % kTPT) >> 1, h = ti & 1;
             float tot[6];
 #pragma unroll
@@ -813,8 +877,27 @@ __global__ void __launch_bounds__(128) k_p2p(
             y[n + k] = make_float2(tot[2], tot[3]);
             y[2 * n + k] = make_float2(tot[4], tot[5]);
         }
-        __syncthreads();
+        sync();
     }
+}
+
+// Standalone P2P: one CTA (128 threads) per leaf task; tasks are taken from a global counter shared with
+// the P2P warps fused into the M2L kernel (leaves[counter++]), so every owned leaf is done exactly once.
+__global__ void __launch_bounds__(128) k_p2p(
+    const int32_t* __restrict__ leaves, int nleaves, int* __restrict__ counter, const int32_t* __restrict__ level,
+    const int32_t* __restrict__ ix, const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
+    const int32_t* __restrict__ pb, const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr,
+    const int32_t* __restrict__ usrc, const float4* __restrict__ loc, const float* __restrict__ xq, float invW,
+    int accumulate, int64_t n, int64_t p0, float2* __restrict__ y)
+{
+    extern __shared__ __align__(16) float smraw[];  // kP2PSmem: source staging, then the reduction
+    __shared__ P2PWin W;
+    __shared__ int task;
+    if (threadIdx.x == 0) task = atomicAdd(counter, 1);
+    __syncthreads();
+    if (task >= nleaves) return;
+    p2p_leaf<128, kSrcChunk, 0>(leaves[task], threadIdx.x, smraw, W, level, ix, iy, iz, pb, pe, uptr, usrc, loc, xq,
+                                invW, accumulate, n, p0, y);
 }
 
 // ell[r][k] (r-major, M2L/L2L layout) -> ellk[k][8] (k-major, 6 RHS + 2 pad) for the leaves: the L2P
@@ -985,7 +1068,7 @@ static void translate_level(xrl_tree t, std::pair<int, int> lvl, const float* sr
     xrl_ctx ctx = t->ctx;
     const int grid = std::min(ctx->num_sms, lvl.second);
     k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->tr_blocks.p + lvl.first, lvl.second, t->tr_tiles.p, t->tr_tgt.p,
-                                                t->tr_src.p, ctx->ops.m2l_tc.p, src, dst, 0);
+                                                t->tr_src.p, ctx->ops.m2l_tc.p, src, dst, 0, P2PTasks{});
     XRL_LAUNCH_CHECK();
     ctx->launches += 1;
 }
@@ -1018,23 +1101,31 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
     XRL_LAUNCH_CHECK();
     ctx->launches += 1;
     phase_end(ctx, PH_PACK, ev, st);
+    XRL_CUDA(cudaMemsetAsync(t->p2p_counter.p, 0, sizeof(int), st));  // P2P leaf tasks (before the fork)
 
-    // near SpMV and P2P depend only on the packed charges
-    auto launch_side = [&]() {
+    // near SpMV and P2P depend only on the packed charges.  With the fused P2P (P2P leaf tasks also taken
+    // by two warps of the M2L kernel) the near SpMV, which accumulates into y after the P2P wrote it,
+    // waits for the M2L kernel as well.
+    const bool chain = do_far && t->nlevel > 1;
+    const bool fuse = sched != 0 && ctx->fuse_p2p && chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0;
+    auto launch_p2p = [&]() {
         XRL_CUDA(cudaEventRecord(ctx->ev_fork, st));
         XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
-        // P2P (FP32-bound) first: it shares SMs well with the tensor-core M2L; the near SpMV
-        // (memory-bound) after it accumulates into y
+        // P2P (FP32-bound) first: it shares SMs well with the tensor-core M2L
         if (do_far) {
             phase_begin(ctx, PH_P2P, &ev, side);
             if (t->n_own_leaves > 0)
-                k_p2p<<<t->n_own_leaves, 128, kP2PSmem, side>>>(t->own_leaves.p, t->blevel.p, t->bix.p, t->biy.p, t->biz.p,
-                                                         t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
-                                                         invW, 0, nl, p0, y);
+                k_p2p<<<t->n_own_leaves, 128, kP2PSmem, side>>>(t->own_leaves.p, t->n_own_leaves, t->p2p_counter.p,
+                                                         t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
+                                                         t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW,
+                                                         0, nl, p0, y);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
             phase_end(ctx, PH_P2P, ev, side);
         }
+    };
+    auto launch_near = [&]() {
+        if (fuse) XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_m2l, 0));  // fused P2P tasks done
         if (do_near) {
             phase_begin(ctx, PH_NEAR, &ev, side);
             if (nl > 0)
@@ -1046,8 +1137,10 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         }
         XRL_CUDA(cudaEventRecord(ctx->ev_join, side));
     };
-    const bool chain = do_far && t->nlevel > 1;
-    if (sched != 2 || !chain) launch_side();
+    if (sched != 2 || !chain) {
+        launch_p2p();
+        if (!fuse) launch_near();
+    }
 
     if (do_far && t->nlevel > 1) {
         phase_begin(ctx, PH_P2M, &ev, st);
@@ -1062,16 +1155,29 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         phase_end(ctx, PH_M2M, ev, st);
 
         XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), st));
-        if (sched == 2) launch_side();
+        if (sched == 2) {
+            launch_p2p();
+            if (!fuse) launch_near();
+        }
         phase_begin(ctx, PH_M2L, &ev, st);
         if (t->n_m2l_tiles > 0) {
             const int grid = std::min(ctx->num_sms, t->n_m2l_blocks);
+            P2PTasks tasks{};
+            if (fuse)
+                tasks = P2PTasks{t->own_leaves.p, t->n_own_leaves, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
+                                 t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW, nl, p0,
+                                 y};
             k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p, t->m2l_tgt.p,
-                                                        t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu.p, t->ell.p, m2l_dbg);
+                                                        t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu.p, t->ell.p, m2l_dbg,
+                                                        tasks);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
         phase_end(ctx, PH_M2L, ev, st);
+        if (fuse) {
+            XRL_CUDA(cudaEventRecord(ctx->ev_m2l, st));
+            launch_near();
+        }
 
         phase_begin(ctx, PH_P2L, &ev, st);
         if (t->n_x_targets > 0) {

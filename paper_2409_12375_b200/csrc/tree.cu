@@ -840,6 +840,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         for (int64_t i = l0; i < l1; ++i) own.push_back(lf[i].second);
         T->n_own_leaves = (int)own.size();
         T->own_leaves.alloc(std::max<size_t>(1, own.size()));
+        T->p2p_counter.alloc(1);
         if (!own.empty()) XRL_CUDA(cudaMemcpyAsync(T->own_leaves.p, own.data(), 4 * own.size(), cudaMemcpyHostToDevice, st));
         // relevant boxes: panel range meets [p0, p1) (owned subtrees and their ancestors)
         T->rel.assign(nbox, 0);

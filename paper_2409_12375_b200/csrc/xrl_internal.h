@@ -87,7 +87,8 @@ struct xrl_ctx_s {
     cudaStream_t stream = nullptr;
     cudaStream_t work = nullptr;      // library-owned high-priority stream (FMM chain of xrl_mvm)
     cudaStream_t side = nullptr;      // library-owned low-priority side stream (near SpMV, P2P)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_work = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_work = nullptr, ev_m2l = nullptr;
+    bool fuse_p2p = true;             // P2P warps inside the M2L kernel (XRL_FUSE=0: off)
     bool own_stream = false;
     int rank = 0, world = 1;
     void* nccl_comm = nullptr;        // ncclComm_t when world > 1
@@ -159,6 +160,7 @@ struct xrl_tree_s {
     std::vector<int32_t> part_cuts;          // panel offsets of all ranks [world+1]
     std::vector<uint8_t> rel;                // box relevant to this rank
     xrl::DBuf<int32_t> own_leaves;           // owned leaves (Morton order)
+    xrl::DBuf<int> p2p_counter;              // P2P leaf-task counter (reset per MVM)
     int32_t n_own_leaves = 0;
     std::vector<int32_t> l2l_start;          // per-level offsets into l2l_boxes
     xrl::DBuf<int32_t> l2l_boxes;
