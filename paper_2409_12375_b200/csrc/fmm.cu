@@ -124,7 +124,7 @@ __device__ __forceinline__ int degree_of(int i)
 // One persistent CTA per SM; blocks (runs of tiles with one (chunk, offset))
 // dealt round-robin, so all CTAs work inside one L2-resident target chunk.
 constexpr int kTcPairs = 21;                        // pairs per tile (126 of 128 TMEM lanes)
-constexpr int kTcThreads = 352;                     // 4 loader + 4 drain + 1 MMA warps + 2 fused-P2P warps
+constexpr int kTcThreads = 384;                     // 4 loader + 4 drain + 1 MMA warps + 3 fused-P2P warps
 constexpr int kTcOpBytes = 128 * 128 * 4;           // one operator part (hi or lo): 64 KB
 constexpr int kTcStageLd = 132;                     // drain stage row stride (floats; conflict-free STS.128)
 constexpr int kTcSmem = 2 * kTcOpBytes + 128 * kTcStageLd * 4 + 1024 + 512 * 12 * 4;  // operator hi + lo, drain stage (+ align), fused-P2P staging
@@ -282,10 +282,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             const int tp = tid - 9 * 32;
             for (;;) {
                 if (tp == 0) p2p_task = *(volatile int*)&m2l_live > 0 ? atomicAdd(p2p.counter, 1) : INT_MAX;
-                asm volatile("bar.sync 1, 64;" ::: "memory");
+                asm volatile("bar.sync 1, 96;" ::: "memory");
                 const int task = p2p_task;
                 if (task >= p2p.nleaves) break;
-                p2p_leaf<64, kFuseChunk, 1>(p2p.leaves[task], tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
+                p2p_leaf<96, kFuseChunk, 1>(p2p.leaves[task], tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
                                             p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, 0, p2p.n,
                                             p2p.p0, p2p.y);
             }
