@@ -371,6 +371,8 @@ def run_xrl(args):
                         "frac": a / fp32_peak, "traffic": traffic_from_profiles("k_p2p", tkey),
                         "isolated": {"achieved": ai, "frac": ai / fp32_peak, "ms": per_launch_ms("p2p", phases_iso)},
                         "algorithmic": f"20 flops x {info['n_p2p']} ordered panel pairs per launch",
+                        "note": "in-step: the standalone k_p2p launch; some leaf tasks run in k_m2l_tc's three spare "
+                                "warps (fused path), so the in-step rate mixes both; isolated = unfused serial pass",
                         "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 flops x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
     if phases["near"][1]:
         byts = 8.0 * nnz + 56.0 * n
@@ -386,7 +388,7 @@ def run_xrl(args):
     roof["share_of_step"] = phases[dom][0] / args.steps / ms_per_step if ms_per_step else None
     roof["share_of_isolated_sum"] = phases_iso[dom][0] / sum(v[0] for v in phases_iso.values())
     roof["others"] = {k: {kk: v[kk] for kk in ("kernel", "bound", "achieved", "peak", "unit", "frac", "traffic",
-                                               "isolated", "algorithmic")}
+                                               "isolated", "algorithmic") if kk in v}
                       for k, v in roofs.items() if k != dom}
 
     line = {
