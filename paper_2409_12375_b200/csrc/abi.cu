@@ -122,6 +122,7 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_work, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_m2l, cudaEventDisableTiming));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_p2p, cudaEventDisableTiming));
         if (const char* e = getenv("XRL_FUSE"); e && e[0] == '0') c->fuse_p2p = false;
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         if (const char* e = getenv("XRL_SCHED")) c->sched = atoi(e);
@@ -169,6 +170,7 @@ void xrl::ctx_release(xrl_ctx ctx)
     if (ctx->ev_work) cudaEventDestroy(ctx->ev_work);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_m2l) cudaEventDestroy(ctx->ev_m2l);
+    if (ctx->ev_p2p) cudaEventDestroy(ctx->ev_p2p);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -564,6 +564,12 @@ __device__ __forceinline__ void ldg256_l1(const float* p, float* v)
                  : "l"(p));
 }
 
+// y += (a, b) as one vector L2 reduction (the L2P and the near SpMV may run concurrently into y)
+__device__ __forceinline__ void red_add2(float2* p, float a, float b)
+{
+    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+
 // One row's 8-lane share of the near SpMV with global gathers: lane loads kNearU (col, value) pairs, then
 // issues their kNearU 32-byte charge gathers with the next batch's pairs loaded behind them.
 template <int kNearU>
@@ -624,13 +630,8 @@ __global__ void __launch_bounds__(256, 6) k_near_spmv(int64_t n, int64_t r0, con
         for (int o = 1; o < kL; o <<= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], o);
     }
     if (lrow < n && lane < 3) {
-        float2 o = make_float2(a[2 * lane], a[2 * lane + 1]);
-        if (accumulate) {
-            const float2 v = y[lane * n + lrow];
-            o.x += v.x;
-            o.y += v.y;
-        }
-        y[lane * n + lrow] = o;
+        if (accumulate) red_add2(y + lane * n + lrow, a[2 * lane], a[2 * lane + 1]);
+        else y[lane * n + lrow] = make_float2(a[2 * lane], a[2 * lane + 1]);
     }
 }
 
@@ -938,10 +939,9 @@ __global__ void __launch_bounds__(128) k_l2p(int64_t n, int64_t p0, const int32_
 #pragma unroll
         for (int r = 0; r < 6; ++r) far[r] *= inv_sb;
     }
-    float2 a = y[li], c = y[n + li], d = y[2 * n + li];
-    y[li] = make_float2(fmaf(far[0], invW, a.x), fmaf(far[1], invW, a.y));
-    y[n + li] = make_float2(fmaf(far[2], invW, c.x), fmaf(far[3], invW, c.y));
-    y[2 * n + li] = make_float2(fmaf(far[4], invW, d.x), fmaf(far[5], invW, d.y));
+    red_add2(y + li, far[0] * invW, far[1] * invW);
+    red_add2(y + n + li, far[2] * invW, far[3] * invW);
+    red_add2(y + 2 * n + li, far[4] * invW, far[5] * invW);
 }
 
 __device__ __forceinline__ void red_add_v2(float* p, float a, float b)
@@ -1123,6 +1123,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
             ctx->launches += 1;
             phase_end(ctx, PH_P2P, ev, side);
         }
+        XRL_CUDA(cudaEventRecord(ctx->ev_p2p, side));  // y holds the P2P part: the L2P may add to it
     };
     auto launch_near = [&]() {
         if (fuse) XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_m2l, 0));  // fused P2P tasks done
@@ -1193,8 +1194,9 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         for (int l = 3; l < t->nlevel; ++l) translate_level(t, t->l2l_lvl[l], t->ell.p, t->ell.p, st);
         phase_end(ctx, PH_L2L, ev, st);
     }
-    // join, then the local-expansion / W-list evaluation completes y
-    if (sched) XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    // after the P2P wrote y, the local-expansion / W-list evaluation adds to it (vector L2 reductions, so it
+    // may overlap the near SpMV, which adds the same way); join the side stream at the end
+    if (sched) XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_p2p, 0));
     if (do_far && t->nlevel > 1 && nl > 0) {
         phase_begin(ctx, PH_L2P, &ev, st);
         if (t->ellk.n < (size_t)t->nbox * kEllKStride) t->ellk.alloc((size_t)t->nbox * kEllKStride);
@@ -1213,7 +1215,8 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         ctx->launches += 1;
         phase_end(ctx, PH_L2P, ev, st);
     }
-    if (sched) {  // join the work stream back into the caller's stream
+    if (sched) {  // join the side stream, then the work stream back into the caller's stream
+        XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
         XRL_CUDA(cudaEventRecord(ctx->ev_work, st));
         XRL_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_work, 0));
     }

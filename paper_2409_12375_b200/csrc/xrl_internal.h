@@ -87,7 +87,7 @@ struct xrl_ctx_s {
     cudaStream_t stream = nullptr;
     cudaStream_t work = nullptr;      // library-owned high-priority stream (FMM chain of xrl_mvm)
     cudaStream_t side = nullptr;      // library-owned low-priority side stream (near SpMV, P2P)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_work = nullptr, ev_m2l = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_work = nullptr, ev_m2l = nullptr, ev_p2p = nullptr;
     bool fuse_p2p = true;             // P2P warps inside the M2L kernel (XRL_FUSE=0: off)
     bool own_stream = false;
     int rank = 0, world = 1;
