@@ -1115,7 +1115,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         if (do_far) {
             phase_begin(ctx, PH_P2P, &ev, side);
             if (t->n_own_leaves > 0)
-                k_p2p<<<t->n_own_leaves, 128, kP2PSmem, side>>>(t->own_leaves.p, t->n_own_leaves, t->p2p_counter.p,
+                k_p2p<<<t->n_own_leaves, 128, kP2PSmem, side>>>(t->p2p_leaves.p, t->n_own_leaves, t->p2p_counter.p,
                                                          t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
                                                          t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW,
                                                          0, nl, p0, y);
@@ -1165,7 +1165,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
             const int grid = std::min(ctx->num_sms, t->n_m2l_blocks);
             P2PTasks tasks{};
             if (fuse)
-                tasks = P2PTasks{t->own_leaves.p, t->n_own_leaves, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
+                tasks = P2PTasks{t->p2p_leaves.p, t->n_own_leaves, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
                                  t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW, nl, p0,
                                  y};
             k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p, t->m2l_tgt.p,
