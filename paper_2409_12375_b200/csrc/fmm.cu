@@ -194,7 +194,7 @@ struct P2PWin {
 };
 
 template <int kNT, int kChunk, int kBar>
-__device__ void p2p_leaf(int b, int tid, float* smraw, P2PWin& W, const int32_t* __restrict__ level,
+__device__ void p2p_leaf(int b, int tb, int te, int tid, float* smraw, P2PWin& W, const int32_t* __restrict__ level,
                          const int32_t* __restrict__ ix, const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
                          const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
                          const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
@@ -204,8 +204,8 @@ __device__ void p2p_leaf(int b, int tid, float* smraw, P2PWin& W, const int32_t*
 // P2P leaf tasks handed to the M2L kernel's two spare warps (leaves[counter++] while the M2L runs; the
 // standalone k_p2p takes the rest from the same counter).  leaves == nullptr: no fused P2P.
 struct P2PTasks {
-    const int32_t* leaves;
-    int nleaves;
+    const int2* tasks;  // (leaf, target offset << 16 | count)
+    int ntasks;
     int* counter;
     const int32_t *level, *ix, *iy, *iz, *pb, *pe;
     const int64_t* uptr;
@@ -278,14 +278,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
     if (warp >= 9) {
         // ---------------- fused P2P: two warps take target-leaf tasks from the shared counter while the
         // translation roles run (the M2L is bound by L2 traffic and leaves the FP32 pipes idle)
-        if (p2p.leaves) {
+        if (p2p.tasks) {
             const int tp = tid - 9 * 32;
             for (;;) {
                 if (tp == 0) p2p_task = *(volatile int*)&m2l_live > 0 ? atomicAdd(p2p.counter, 1) : INT_MAX;
                 asm volatile("bar.sync 1, 96;" ::: "memory");
                 const int task = p2p_task;
-                if (task >= p2p.nleaves) break;
-                p2p_leaf<96, kFuseChunk, 1>(p2p.leaves[task], tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
+                if (task >= p2p.ntasks) break;
+                const int2 tk = p2p.tasks[task];
+                const int tb = p2p.pb[tk.x] + (tk.y >> 16);
+                p2p_leaf<96, kFuseChunk, 1>(tk.x, tb, tb + (tk.y & 0xffff), tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
                                             p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, 0, p2p.n,
                                             p2p.p0, p2p.y);
             }
@@ -741,12 +743,12 @@ __device__ __forceinline__ int first_in_class(int lo, int sg, int S)
 }
 
 
-// P2P of one target leaf b by kNT threads (tid 0..kNT-1) synchronised with barrier kBar (0:
+// P2P of targets [tb, te) of leaf b by kNT threads (tid 0..kNT-1) synchronised with barrier kBar (0:
 // __syncthreads, else a named barrier of kNT threads); smraw: kChunk * 12 floats of staging, also the
 // reduction buffer (>= kNT * (kTP2 * 6 + 1) * 2 floats).
 template <int kNT, int kChunk, int kBar>
 __device__ void p2p_leaf(
-    int b, int tid, float* smraw, P2PWin& W, const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
+    int b, int tb, int te, int tid, float* smraw, P2PWin& W, const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
     const int32_t* __restrict__ iy, const int32_t* __restrict__ iz, const int32_t* __restrict__ pb,
     const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
     const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate, int64_t n,
@@ -769,8 +771,8 @@ __device__ void p2p_leaf(
         if (kBar == 0) __syncthreads();
         else asm volatile("bar.sync %0, %1;" ::"r"(kBar), "r"(kNT) : "memory");
     };
-    for (int t0 = pb[b]; t0 < pe[b]; t0 += kNT * kTPT) {
-        const int T = min(kNT * kTPT, pe[b] - t0);
+    for (int t0 = tb; t0 < te; t0 += kNT * kTPT) {
+        const int T = min(kNT * kTPT, te - t0);
         const int NG = (T + kTPT - 1) / kTPT;
         const int S = max(1, kNT / NG);
         const int tg = tid % NG, sg = tid / NG;
@@ -885,7 +887,7 @@ __device__ void p2p_leaf(
 // Standalone P2P: one CTA (128 threads) per leaf task; tasks are taken from a global counter shared with
 // the P2P warps fused into the M2L kernel (leaves[counter++]), so every owned leaf is done exactly once.
 __global__ void __launch_bounds__(128) k_p2p(
-    const int32_t* __restrict__ leaves, int nleaves, int* __restrict__ counter, const int32_t* __restrict__ level,
+    const int2* __restrict__ tasks, int ntasks, int* __restrict__ counter, const int32_t* __restrict__ level,
     const int32_t* __restrict__ ix, const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
     const int32_t* __restrict__ pb, const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr,
     const int32_t* __restrict__ usrc, const float4* __restrict__ loc, const float* __restrict__ xq, float invW,
@@ -896,8 +898,10 @@ __global__ void __launch_bounds__(128) k_p2p(
     __shared__ int task;
     if (threadIdx.x == 0) task = atomicAdd(counter, 1);
     __syncthreads();
-    if (task >= nleaves) return;
-    p2p_leaf<128, kSrcChunk, 0>(leaves[task], threadIdx.x, smraw, W, level, ix, iy, iz, pb, pe, uptr, usrc, loc, xq,
+    if (task >= ntasks) return;
+    const int2 tk = tasks[task];
+    const int tb = pb[tk.x] + (tk.y >> 16);
+    p2p_leaf<128, kSrcChunk, 0>(tk.x, tb, tb + (tk.y & 0xffff), threadIdx.x, smraw, W, level, ix, iy, iz, pb, pe, uptr, usrc, loc, xq,
                                 invW, accumulate, n, p0, y);
 }
 
@@ -1115,7 +1119,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
         if (do_far) {
             phase_begin(ctx, PH_P2P, &ev, side);
             if (t->n_own_leaves > 0)
-                k_p2p<<<t->n_own_leaves, 128, kP2PSmem, side>>>(t->p2p_leaves.p, t->n_own_leaves, t->p2p_counter.p,
+                k_p2p<<<t->n_p2p_tasks, 128, kP2PSmem, side>>>(t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p,
                                                          t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
                                                          t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW,
                                                          0, nl, p0, y);
@@ -1165,7 +1169,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
             const int grid = std::min(ctx->num_sms, t->n_m2l_blocks);
             P2PTasks tasks{};
             if (fuse)
-                tasks = P2PTasks{t->p2p_leaves.p, t->n_own_leaves, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
+                tasks = P2PTasks{t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
                                  t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW, nl, p0,
                                  y};
             k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p, t->m2l_tgt.p,

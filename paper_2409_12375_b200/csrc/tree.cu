@@ -842,21 +842,29 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         T->own_leaves.alloc(std::max<size_t>(1, own.size()));
         T->p2p_counter.alloc(1);
         if (!own.empty()) XRL_CUDA(cudaMemcpyAsync(T->own_leaves.p, own.data(), 4 * own.size(), cudaMemcpyHostToDevice, st));
-        // P2P task order: longest first (targets x U-list sources), so the dynamically scheduled tasks end
-        // together (all P2P sources, 48 B per panel, stay resident in L2, so the order costs no locality)
+        // P2P tasks: (leaf, target range), longest first (targets x U-list sources) so the dynamically
+        // scheduled tasks end together (all P2P sources, 48 B per panel, stay resident in L2, so the order
+        // costs no locality).  Leaves above 256 targets are cut into 256 + rest: with 8 targets per thread
+        // a task of T <= 256 keeps >= 93 % of its 128 threads busy (T = 352 in one task: 69 %).
         {
-            std::vector<std::pair<int64_t, int32_t>> cost;
+            std::vector<std::pair<int64_t, int2>> cost;
             for (int32_t L : own) {
                 int64_t src = 0;
                 for (int64_t q = hup[L]; q < hup[L + 1]; ++q) src += hpe[hus[q]] - hpb[hus[q]];
-                cost.push_back({-(int64_t)(hpe[L] - hpb[L]) * src, L});
+                const int nt = hpe[L] - hpb[L];
+                for (int o = 0; o < nt;) {
+                    const int c = (nt - o > 256) ? 256 : nt - o;
+                    cost.push_back({-(int64_t)c * src, make_int2(L, (o << 16) | c)});
+                    o += c;
+                }
             }
-            std::stable_sort(cost.begin(), cost.end());
-            std::vector<int32_t> ord;
+            std::stable_sort(cost.begin(), cost.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+            std::vector<int2> ord;
             for (auto& c : cost) ord.push_back(c.second);
-            T->p2p_leaves.alloc(std::max<size_t>(1, ord.size()));
+            T->n_p2p_tasks = (int)ord.size();
+            T->p2p_tasks.alloc(std::max<size_t>(1, ord.size()));
             if (!ord.empty())
-                XRL_CUDA(cudaMemcpyAsync(T->p2p_leaves.p, ord.data(), 4 * ord.size(), cudaMemcpyHostToDevice, st));
+                XRL_CUDA(cudaMemcpyAsync(T->p2p_tasks.p, ord.data(), sizeof(int2) * ord.size(), cudaMemcpyHostToDevice, st));
             XRL_CUDA(cudaStreamSynchronize(st));
         }
         // relevant boxes: panel range meets [p0, p1) (owned subtrees and their ancestors)

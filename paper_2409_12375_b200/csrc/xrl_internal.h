@@ -161,7 +161,8 @@ struct xrl_tree_s {
     std::vector<uint8_t> rel;                // box relevant to this rank
     xrl::DBuf<int32_t> own_leaves;           // owned leaves (Morton order)
     xrl::DBuf<int> p2p_counter;              // P2P leaf-task counter (reset per MVM)
-    xrl::DBuf<int32_t> p2p_leaves;           // owned leaves in P2P task order (longest first)
+    xrl::DBuf<int2> p2p_tasks;               // P2P tasks (leaf, target offset << 16 | count), longest first
+    int32_t n_p2p_tasks = 0;
     int32_t n_own_leaves = 0;
     std::vector<int32_t> l2l_start;          // per-level offsets into l2l_boxes
     xrl::DBuf<int32_t> l2l_boxes;
