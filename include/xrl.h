@@ -237,6 +237,11 @@ xrl_status xrl_mvm_host_batch(xrl_tree tree, xrl_near near, const void* const* x
 #define XRL_SCHED_FORK 1
 #define XRL_SCHED_LATE 2
 xrl_status xrl_ctx_set_sched(xrl_ctx ctx, int32_t mode);
+/* Fused P2P (default on; XRL_FUSE=0 at context creation turns it off): in the
+ * forked schedules, three spare warps of the M2L kernel take P2P leaf tasks from
+ * the counter the standalone P2P kernel uses.  Results equal the unfused path up
+ * to FP32 summation order.  Errors: XRL_EINVAL for a null context. */
+xrl_status xrl_ctx_set_fuse(xrl_ctx ctx, int32_t on);
 
 /* Per-phase device timing (CUDA events on the stream each phase runs on) of
  * the MVM kernels, accumulated while enabled.  names: "pack","p2m","m2m","m2l",

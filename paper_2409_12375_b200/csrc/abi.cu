@@ -213,6 +213,13 @@ xrl_status xrl_ctx_set_sched(xrl_ctx ctx, int32_t mode)
     return XRL_OK;
 }
 
+xrl_status xrl_ctx_set_fuse(xrl_ctx ctx, int32_t on)
+{
+    if (!ctx) { set_error("xrl_ctx_set_fuse: null context"); return XRL_EINVAL; }
+    ctx->fuse_p2p = on != 0;
+    return XRL_OK;
+}
+
 xrl_status xrl_timing_reset(xrl_ctx ctx)
 {
     if (!ctx) { set_error("null ctx"); return XRL_EINVAL; }

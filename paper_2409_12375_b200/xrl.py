@@ -25,7 +25,7 @@ EXPORTS = [
     "xrl_tree_build", "xrl_tree_build_poly", "xrl_tree_destroy", "xrl_tree_info", "xrl_tree_perm", "xrl_to_library_order",
     "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble", "xrl_near_destroy",
     "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_mvm_host_batch", "xrl_timing_enable", "xrl_timing_count",
-    "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_extract",
+    "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_ctx_set_fuse", "xrl_extract",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
     "xrl_precond_build_exact", "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
@@ -127,6 +127,8 @@ def lib():
         L.xrl_launch_count.restype = i64
         L.xrl_ctx_set_sched.argtypes = [P, i32]
         L.xrl_ctx_set_sched.restype = ctypes.c_int32
+        L.xrl_ctx_set_fuse.argtypes = [P, i32]
+        L.xrl_ctx_set_fuse.restype = ctypes.c_int32
         L.xrl_extract.argtypes = [P, P, P, P, ctypes.c_double, ctypes.c_double, i32, P, i32, P, P, P, P, P, P]
         L.xrl_extract.restype = ctypes.c_int32
         L.xrl_topology_build.argtypes = [P, i32, P, pp]
@@ -234,6 +236,10 @@ class Context:
     def set_sched(self, mode: int):
         """xrl_ctx_set_sched: 0 serial (isolated phase times), 1 fork (default), 2 late fork."""
         check(lib().xrl_ctx_set_sched(self.h, int(mode)))
+
+    def set_fuse(self, on: bool):
+        """xrl_ctx_set_fuse: P2P leaf tasks also in the M2L kernel's spare warps (default on)."""
+        check(lib().xrl_ctx_set_fuse(self.h, int(bool(on))))
 
     def timing_enable(self, on=True):
         check(lib().xrl_timing_enable(self.h, int(on)))

@@ -351,3 +351,27 @@ def test_host_batch_pipelined_equals_single_calls(bar_setup):
     xrl.mvm_host_batch(tree, near, [xs[k % 2] for k in range(6)], [y2[k % 2] for k in range(6)])
     for k in range(2):
         assert oracle.rel_l2(y2[k], ys[k]) < 1e-6
+
+
+@pytest.mark.parametrize("cfg,leaf", [(1, 16), (2, 352)])
+def test_schedules_agree(cfg, leaf):
+    """Fused P2P tasks (default), unfused, serial and late-fork schedules give the same y up to FP32
+    summation order, and the fused result matches the oracle on sampled rows."""
+    from paper_2409_12375_b200 import xrl
+    m = meshes.make_config(cfg)
+    ctx, tree, near = cuda_setup(m, leaf_max=leaf)
+    x = meshes.make_x(cfg, m.n)
+    y0 = run_mvm(tree, near, x)
+    out = {}
+    for name, sched, fuse in (("unfused", 1, False), ("serial", 0, True), ("late", 2, True)):
+        ctx.set_sched(sched)
+        ctx.set_fuse(fuse)
+        out[name] = run_mvm(tree, near, x)
+    ctx.set_sched(1)
+    ctx.set_fuse(True)
+    for name, y in out.items():
+        err = oracle.rel_l2(y, y0)
+        print(cfg, name, err)
+        assert err < 1e-6, name
+    rows = np.random.default_rng(7).choice(m.n, size=min(256, m.n), replace=False)
+    assert oracle.rel_l2(y0[:, rows], oracle_rows(m, x, rows)) <= TOL_FULL
