@@ -189,6 +189,13 @@ void xrl_near_destroy(xrl_near near);
  * always written. */
 xrl_status xrl_near_export(xrl_near near, int64_t* row_ptr, int32_t* col, float* val32,
                            double* val64, int64_t* nnz);
+/* Selected rows of the CSR (tests on full-size meshes): rows host int64 [nrows]
+ * (library order); cnt host int64 [nrows] receives each row's length; col,
+ * val32, val64 (any may be NULL) receive the rows concatenated in the given
+ * order (call once with NULL arrays to size them).  XRL_EINVAL for a row out
+ * of range. */
+xrl_status xrl_near_export_rows(xrl_near near, int64_t nrows, const int64_t* rows, int64_t* cnt, int32_t* col,
+                                float* val32, double* val64);
 
 /* The hot path: y = P x (flags select diagnostic parts).
  * x, y: device complex64 [nvec][n_local] in library order (this rank's slice
@@ -313,7 +320,10 @@ xrl_status xrl_esi(double sigma, double zeta, double freq_hz, double* zs_re, dou
  *   A v = M sum_t A_t [ diag(Z_s/A) + alpha P ] A_t^T M^T v,  alpha = j omega mu0/(4 pi)
  * applied as u_t = C_t^T v (C_t = M A_t), P u_t by xrl_mvm, w = sum_t C_t y_t.
  * zs: per-panel complex Z_s (double [n][2], mesh order) or NULL to use
- * xrl_esi(sigma, zeta, freq) for every panel.  Handles are borrowed. */
+ * xrl_esi(sigma, zeta, freq) for every panel.  Handles are borrowed.
+ * Single-rank trees only: XRL_EUNSUPPORTED if the tree is partitioned
+ * (part_world > 1; the loop-space vectors are not sharded);
+ * xrl_extract has the same restriction. */
 xrl_status xrl_operator_create(xrl_tree tree, xrl_near near, xrl_topo topo, const double* zs, double sigma,
                                double zeta, double freq_hz, xrl_op* out);
 /* w = A v; v, w device complex64 [nrhs][n_loops], must not alias. */

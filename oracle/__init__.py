@@ -22,13 +22,30 @@ ETA = 1.5  # near criterion factor, reading R3
 _lib = None
 
 
+def _stale() -> bool:
+    return not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC)
+
+
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc: FP64, -ffp-contract=off, OpenMP."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
-               "-std=c11", "-o", _SO + ".tmp", _SRC, "-lm"]
-        subprocess.check_call(cmd)
-        os.replace(_SO + ".tmp", _SO)
+    """Compile the oracle with gcc: FP64, -ffp-contract=off, OpenMP.
+
+    Safe under concurrent callers (e.g. the spawned ranks of the gloo tests):
+    an exclusive file lock serialises the compilers, each writes its own
+    per-process temporary and the rename into place is atomic."""
+    if not (force or _stale()):
+        return _SO
+    import fcntl
+    with open(_SO + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if force or _stale():  # another process may have built it while we waited
+                tmp = "%s.%d.tmp" % (_SO, os.getpid())
+                cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
+                       "-std=c11", "-o", tmp, _SRC, "-lm"]
+                subprocess.check_call(cmd)
+                os.replace(tmp, _SO)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
     return _SO
 
 
@@ -51,6 +68,8 @@ def lib():
         L.orc_outer_rule_ext.restype = ctypes.c_int
         L.orc_tie_audit.argtypes = [i64, P, P, f64, f64]
         L.orc_tie_audit.restype = i64
+        L.orc_tie_audit_rows.argtypes = [i64, P, P, f64, f64, i64, P]
+        L.orc_tie_audit_rows.restype = i64
         L.orc_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -153,6 +172,12 @@ def near_rows(g: Geometry, rows=None, eta=ETA):
 
 def tie_audit(g: Geometry, eta=ETA, rel=1e-9) -> int:
     return int(lib().orc_tie_audit(g.n, _p(g.cent), _p(g.dmax), eta, rel))
+
+
+def tie_audit_rows(g: Geometry, rows, eta=ETA, rel=1e-9) -> int:
+    """Tie audit of the selected target rows against every source panel."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    return int(lib().orc_tie_audit_rows(g.n, _p(g.cent), _p(g.dmax), eta, rel, rows.size, _p(rows)))
 
 
 def num_threads() -> int:

@@ -11,8 +11,10 @@ following the paper step by step, on small meshes:
   * loop_system():  Eq. 7-9: M sum_t A_t (diag(Z_s/A) + alpha P) A_t^T M^T,
                     alpha = j omega mu0/(4 pi), P the oracle's dense P
   * port_impedance(): dense solve (numpy LU) and Z_port = V / I_port
-  * precond_blocks(): Eq. 10 Q = sum_t C_t diag(Z_s/A + alpha P_kk) C_t^T and
-                    its diagonal blocks inverted (numpy LU), applied block-wise
+  * precond_q():     Eq. 10 Q = sum_t C_t diag(Z_s/A + alpha P_kk) C_t^T
+  * precond_q_diag_l(): the diagonal-of-L baseline of PAPER.md:120-122
+  * precond_apply() / block_solve(): Eq. 11 with Q's diagonal blocks inverted
+                    (numpy LU), applied block-wise (one block = the exact Q^-1)
 
 It never imports paper_2409_12375_b200.  Library data (branch orientation,
 loop matrix, block partition) enters only as plain input arrays where the
@@ -218,14 +220,48 @@ def port_impedance(verts, tris, cent, area, P, ports, zs, freq):
     return np.linalg.inv(Y), {"n_loops": M.shape[0], "kcl": kcl_residual(M, ends, nn)}
 
 
-def precond_apply(C, zsa, alpha, pkk, block_ptr, v):
-    """Eq. 10 in block-Jacobi form: Q = sum_t C_t diag(zsa + alpha P_kk) C_t^T,
-    z_B = Q_BB^{-1} v_B for each block [block_ptr[i], block_ptr[i+1])."""
+def precond_q(C, zsa, alpha, pkk):
+    """Eq. 10, the diagonal-of-P preconditioner as a sparse
+    matrix: Q = Z_s + M (sum_t A_t P_d A_t^T) M^T with the jw mu0/4pi factor
+    alpha on the P_d term (reading C-A7) and Z_s = M (sum_t A_t diag(Z_s/A)
+    A_t^T) M^T the ESI part of Eq. 8, i.e. with C_t = M A_t,
+        Q = sum_t C_t diag(zsa + alpha P_kk) C_t^T."""
     d = np.asarray(zsa) + alpha * np.asarray(pkk)
     Q = 0
     for t in range(3):
         Ct = sp.csr_matrix(C[t])
         Q = Q + Ct @ sp.diags(d) @ Ct.T
+    return sp.csr_matrix(Q)
+
+
+def precond_q_diag_l(M, A, zsa, alpha, P):
+    """The traditional diagonal-of-L preconditioner:
+    Q_L = Z_s + jw L_d with L_d "formed by the diagonal entries of the
+    edge-edge interaction matrix" L = sum_t A_t P A_t^T (the edge matrix of
+    Eq. 5/7 with mu0/4pi pulled out, reading C-A7), mapped to loops like
+    Eq. 7:  Q_L = M [ sum_t A_t diag(zsa) A_t^T + alpha diag(L_ee) ] M^T.
+    A: the 3 branch x panel maps of Algorithm 1 (physical branches only);
+    P: the dense (or any indexable) panel matrix -- only the entries P_ij of
+    the two panels of each edge are used."""
+    Zs = 0
+    for t in range(3):
+        At = sp.csr_matrix(A[t])
+        Zs = Zs + At @ sp.diags(np.asarray(zsa)) @ At.T
+    nb = A[0].shape[0]
+    Ld = np.zeros(nb)
+    for t in range(3):
+        At = sp.csr_matrix(A[t])
+        for e in range(nb):
+            cols = At.indices[At.indptr[e]:At.indptr[e + 1]]
+            vals = At.data[At.indptr[e]:At.indptr[e + 1]]
+            Ld[e] += sum(vals[a] * vals[b] * P[cols[a], cols[b]] for a in range(len(cols)) for b in range(len(cols)))
+    M = sp.csr_matrix(M)
+    return sp.csr_matrix(M @ (Zs + alpha * sp.diags(Ld)) @ M.T)
+
+
+def block_solve(Q, block_ptr, v):
+    """z_B = Q_BB^{-1} v_B for each block [block_ptr[i], block_ptr[i+1]) of a
+    sparse Q (dense LU per block, numpy).  v: [..., N_l]."""
     Q = sp.csr_matrix(Q)
     z = np.zeros_like(v, dtype=complex)
     for i in range(len(block_ptr) - 1):
@@ -233,6 +269,12 @@ def precond_apply(C, zsa, alpha, pkk, block_ptr, v):
         QB = Q[a:b, a:b].toarray()
         z[..., a:b] = np.linalg.solve(QB, v[..., a:b].T).T
     return z
+
+
+def precond_apply(C, zsa, alpha, pkk, block_ptr, v):
+    """Eq. 10-11 in block-Jacobi form (reading C-A10): z_B = Q_BB^{-1} v_B
+    with Q of precond_q; block_ptr = [0, N_l] is the exact Q^{-1} v."""
+    return block_solve(precond_q(C, zsa, alpha, pkk), block_ptr, v)
 
 
 def bar_partial_inductance_tube(length, side):

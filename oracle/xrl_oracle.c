@@ -373,6 +373,27 @@ int64_t orc_tie_audit(int64_t nt, const double *cent, const double *dmax, double
     return ties;
 }
 
+/* The tie audit restricted to target rows: pairs (rows[i], l), l != rows[i],
+ * all l, within `rel` of the threshold (full-size configs, sampled rows). */
+int64_t orc_tie_audit_rows(int64_t nt, const double *cent, const double *dmax, double eta, double rel,
+                           int64_t nr, const int64_t *rows)
+{
+    int64_t ties = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : ties)
+    for (int64_t i = 0; i < nr; ++i) {
+        const int64_t k = rows[i];
+        for (int64_t l = 0; l < nt; ++l) {
+            if (l == k) continue;
+            const double *ck = cent + 3 * k, *cl = cent + 3 * l;
+            double dx = ck[0] - cl[0], dy = ck[1] - cl[1], dz = ck[2] - cl[2];
+            double d = sqrt((dx * dx + dy * dy) + dz * dz);
+            double t = eta * (dmax[k] > dmax[l] ? dmax[k] : dmax[l]);
+            if (fabs(d - t) < rel * t) ++ties;
+        }
+    }
+    return ties;
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP

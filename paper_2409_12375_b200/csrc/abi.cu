@@ -108,7 +108,13 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
             set_error("device %d is sm_%d%d; this library is built for sm_100a only", device, prop.major, prop.minor);
             return XRL_ECUDA;
         }
-        auto* c = new xrl_ctx_s();
+        // owned by a guard until fully initialised: any failure below (a throwing XRL_CUDA, a failed
+        // communicator) releases the streams and events created so far through ctx_release
+        struct Guard {
+            xrl_ctx c;
+            ~Guard() { if (c) { c->dead = true; ctx_release(c); } }
+        } guard{new xrl_ctx_s()};
+        xrl_ctx c = guard.c;
         c->device = device;
         c->rank = rank;
         c->world = world;
@@ -131,8 +137,9 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         upload_constants(c);
         if (world > 1) {
             xrl_status st = comm_init(c, nccl_unique_id);
-            if (st) { delete c; return st; }
+            if (st) return st;
         }
+        guard.c = nullptr;
         *out = c;
         return XRL_OK;
     XRL_CATCH

@@ -55,8 +55,13 @@ xrl_status gather_slices(xrl_tree t, const float2* x_local, float2* x_full)
             float2* recv = x_full + (size_t)v * n + c0;
             // sendbuff is read on the root only; the other ranks pass their receive buffer (never NULL)
             const void* send = (r == ctx->rank) ? (const void*)(x_local + (size_t)v * nl) : (const void*)recv;
-            XRL_NCCL(ncclBroadcast(send, recv, (size_t)(c1 - c0) * 2, ncclFloat, r, (ncclComm_t)ctx->nccl_comm,
-                                   ctx->stream));
+            const ncclResult_t e = ncclBroadcast(send, recv, (size_t)(c1 - c0) * 2, ncclFloat, r,
+                                                 (ncclComm_t)ctx->nccl_comm, ctx->stream);
+            if (e != ncclSuccess) {
+                ncclGroupEnd();  // close the group before reporting, so later NCCL calls are not captured by it
+                set_error("NCCL error %s in ncclBroadcast (gather_slices)", ncclGetErrorString(e));
+                return XRL_ENCCL;
+            }
         }
     XRL_NCCL(ncclGroupEnd());
     return XRL_OK;

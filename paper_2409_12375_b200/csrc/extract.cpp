@@ -54,6 +54,11 @@ extern "C" xrl_status xrl_extract(xrl_tree tree, xrl_near near, xrl_topo topo, c
         xrl::set_error("xrl_extract: null argument or n_freq < 1");
         return XRL_EINVAL;
     }
+    if (tree->part_world > 1) {
+        xrl::set_error("xrl_extract: the extraction sweep runs on single-rank trees only (part_world = %d)",
+                       tree->part_world);
+        return XRL_EUNSUPPORTED;
+    }
     const int np = topo->n_ports;
     if (np < 1) { xrl::set_error("xrl_extract: the topology has no ports"); return XRL_EINVAL; }
     for (int j = 0; j < n_freq; ++j)

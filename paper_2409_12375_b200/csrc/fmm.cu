@@ -110,7 +110,7 @@ __device__ __forceinline__ int degree_of(int i)
 // 128 x 128 x 128 product
 //     D[(p, r)][i] = sum_k A[(p, r)][k] B[i][k],   A = mu_s(p)[r][k], B = T_o[i][k]
 // with row (p, r) = 6 p + r (126 rows used), i.e. the 6 RHS of 21 source
-// multipoles against one operator.  Roles (288 threads, warp-specialised):
+// multipoles against one operator.  Roles (384 threads, warp-specialised):
 //   warps 0-3 (loaders, thread = TMEM lane (p, r)): LDG the FP32 multipole row
 //     (r-major image, 512 B), split it into TF32 hi/lo and tcgen05.st them into
 //     TMEM (A_hi, A_lo), one K-half (64 columns) at a time, one tile ahead;
@@ -119,7 +119,9 @@ __device__ __forceinline__ int degree_of(int i)
 //     hi/lo (128 KB, canonical K-major layout) stays in shared memory for a block
 //     of tiles with the same offset (cp.async.bulk);
 //   warps 4-7 (drain, thread = TMEM lane): tcgen05.ld the 121 coefficients of
-//     row (p, r) and red.global.add.v4 them into ell[t(p)][r][0..120] (r-major).
+//     row (p, r) into a shared-memory stage and reduce it into ell[t(p)][r][0..123]
+//     (r-major) with one TMA bulk reduction (cp.reduce.async.bulk .add.f32) per row;
+//   warps 9-11 (fused P2P): P2P target-leaf tasks from the counter shared with k_p2p.
 // mbarriers: a_full/a_free per K-half (A), d_full/d_free per accumulator, op_full.
 // One persistent CTA per SM; blocks (runs of tiles with one (chunk, offset))
 // dealt round-robin, so all CTAs work inside one L2-resident target chunk.
@@ -201,10 +203,10 @@ __device__ void p2p_leaf(int b, int tb, int te, int tid, float* smraw, P2PWin& W
                          const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate,
                          int64_t n, int64_t p0, float2* __restrict__ y);
 
-// P2P leaf tasks handed to the M2L kernel's two spare warps (leaves[counter++] while the M2L runs; the
+// P2P leaf tasks handed to the M2L kernel's three spare warps (leaves[counter++] while the M2L runs; the
 // standalone k_p2p takes the rest from the same counter).  leaves == nullptr: no fused P2P.
 struct P2PTasks {
-    const int2* tasks;  // (leaf, target offset << 16 | count)
+    const int4* tasks;  // (leaf, first target panel, #targets, -)
     int ntasks;
     int* counter;
     const int32_t *level, *ix, *iy, *iz, *pb, *pe;
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
     const uint32_t tm = tbase;
 
     if (warp >= 9) {
-        // ---------------- fused P2P: two warps take target-leaf tasks from the shared counter while the
+        // ---------------- fused P2P: three warps take target-leaf tasks from the shared counter while the
         // translation roles run (the M2L is bound by L2 traffic and leaves the FP32 pipes idle)
         if (p2p.tasks) {
             const int tp = tid - 9 * 32;
@@ -285,9 +287,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                 asm volatile("bar.sync 1, 96;" ::: "memory");
                 const int task = p2p_task;
                 if (task >= p2p.ntasks) break;
-                const int2 tk = p2p.tasks[task];
-                const int tb = p2p.pb[tk.x] + (tk.y >> 16);
-                p2p_leaf<96, kFuseChunk, 1>(tk.x, tb, tb + (tk.y & 0xffff), tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
+                const int4 tk = p2p.tasks[task];
+                p2p_leaf<96, kFuseChunk, 1>(tk.x, tk.y, tk.y + tk.z, tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
                                             p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, 0, p2p.n,
                                             p2p.p0, p2p.y);
             }
@@ -357,8 +358,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
         }
     } else if (warp < 8) {
         // ---------------- drain: thread = TMEM lane L = (p, r) reads its accumulator row into a
-        // shared-memory stage; then each warp reduces whole rows into ell with one contiguous
-        // red.global.add.v4 per row (31 lanes x 16 B; ~2.3x the L2 reduction rate of row-per-lane)
+        // shared-memory stage; then each thread reduces its whole row into ell with one TMA bulk
+        // reduction (asynchronous: frees the drain warps; tools/ubench_red.cu measured the variants)
         const int L = tid - 128, p = L / 6, r = L % 6;
         const bool lane_ok = L < 6 * kTcPairs;
         const int qd = warp - 4;  // lane quarter (warp % 4)
@@ -887,7 +888,7 @@ __device__ void p2p_leaf(
 // Standalone P2P: one CTA (128 threads) per leaf task; tasks are taken from a global counter shared with
 // the P2P warps fused into the M2L kernel (leaves[counter++]), so every owned leaf is done exactly once.
 __global__ void __launch_bounds__(128) k_p2p(
-    const int2* __restrict__ tasks, int ntasks, int* __restrict__ counter, const int32_t* __restrict__ level,
+    const int4* __restrict__ tasks, int ntasks, int* __restrict__ counter, const int32_t* __restrict__ level,
     const int32_t* __restrict__ ix, const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
     const int32_t* __restrict__ pb, const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr,
     const int32_t* __restrict__ usrc, const float4* __restrict__ loc, const float* __restrict__ xq, float invW,
@@ -899,9 +900,8 @@ __global__ void __launch_bounds__(128) k_p2p(
     if (threadIdx.x == 0) task = atomicAdd(counter, 1);
     __syncthreads();
     if (task >= ntasks) return;
-    const int2 tk = tasks[task];
-    const int tb = pb[tk.x] + (tk.y >> 16);
-    p2p_leaf<128, kSrcChunk, 0>(tk.x, tb, tb + (tk.y & 0xffff), threadIdx.x, smraw, W, level, ix, iy, iz, pb, pe, uptr, usrc, loc, xq,
+    const int4 tk = tasks[task];
+    p2p_leaf<128, kSrcChunk, 0>(tk.x, tk.y, tk.y + tk.z, threadIdx.x, smraw, W, level, ix, iy, iz, pb, pe, uptr, usrc, loc, xq,
                                 invW, accumulate, n, p0, y);
 }
 
@@ -1081,8 +1081,18 @@ static void translate_level(xrl_tree t, std::pair<int, int> lvl, const float* sr
 static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags)
 {
     xrl_ctx ctx = t->ctx;
-    // XRL_M2L_DBG (profiling ablations, wrong results): 1 skip reductions, 2 skip A loads, 4 skip D reads
-    static const int m2l_dbg = [] { const char* e = getenv("XRL_M2L_DBG"); return e ? atoi(e) : 0; }();
+#ifdef XRL_PROFILING_ABLATION
+    // XRL_M2L_DBG (profiling ablations, WRONG RESULTS; only in a library built with
+    // -DXRL_PROFILING_ABLATION): 1 skip reductions, 2 skip A loads, 4 skip D reads
+    static const int m2l_dbg = [] {
+        const char* e = getenv("XRL_M2L_DBG");
+        const int v = e ? atoi(e) : 0;
+        if (v) fprintf(stderr, "xrl: XRL_M2L_DBG=%d -- M2L ablation active, MVM results are wrong\n", v);
+        return v;
+    }();
+#else
+    constexpr int m2l_dbg = 0;  // the shipped library has no ablation switch
+#endif
     // Scheduling (xrl_ctx_set_sched): 0 = one stream (phases isolated, profiling); 1 (default) = P2P
     // then the near SpMV on the low-priority side stream forked after the pack (the FP32-bound P2P
     // shares SMs with the tensor-core M2L); 2 = forked when the M2L is launched.  The FMM chain runs
@@ -1108,7 +1118,7 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
     XRL_CUDA(cudaMemsetAsync(t->p2p_counter.p, 0, sizeof(int), st));  // P2P leaf tasks (before the fork)
 
     // near SpMV and P2P depend only on the packed charges.  With the fused P2P (P2P leaf tasks also taken
-    // by two warps of the M2L kernel) the near SpMV, which accumulates into y after the P2P wrote it,
+    // by three warps of the M2L kernel) the near SpMV, which accumulates into y after the P2P wrote it,
     // waits for the M2L kernel as well.
     const bool chain = do_far && t->nlevel > 1;
     const bool fuse = sched != 0 && ctx->fuse_p2p && chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0;

@@ -12,6 +12,8 @@
 // the self term N_kk = P_kk.
 #include <cmath>
 
+#include <vector>
+
 #include "xrl_internal.h"
 
 using namespace xrl;
@@ -328,6 +330,37 @@ xrl_status xrl_near_export(xrl_near nr, int64_t* row_ptr, int32_t* col, float* v
         if (col && nr->nnz) XRL_CUDA(cudaMemcpyAsync(col, nr->col.p, 4 * nr->nnz, cudaMemcpyDeviceToHost, st));
         if (val32 && nr->nnz) XRL_CUDA(cudaMemcpyAsync(val32, nr->val.p, 4 * nr->nnz, cudaMemcpyDeviceToHost, st));
         if (val64 && nr->nnz) XRL_CUDA(cudaMemcpyAsync(val64, nr->val64.p, 8 * nr->nnz, cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        return XRL_OK;
+    } catch (const CudaError& e) {
+        return e.code;
+    }
+}
+
+xrl_status xrl_near_export_rows(xrl_near nr, int64_t nrows, const int64_t* rows, int64_t* cnt, int32_t* col,
+                                float* val32, double* val64)
+{
+    if (!nr || nrows < 0 || (nrows > 0 && (!rows || !cnt))) { set_error("xrl_near_export_rows: bad argument"); return XRL_EINVAL; }
+    const int64_t n = nr->tree->n;
+    for (int64_t i = 0; i < nrows; ++i)
+        if (rows[i] < 0 || rows[i] >= n) { set_error("xrl_near_export_rows: row %lld out of range", (long long)rows[i]); return XRL_EINVAL; }
+    try {
+        cudaStream_t st = nr->tree->ctx->stream;
+        XRL_CUDA(cudaSetDevice(nr->tree->ctx->device));
+        std::vector<int64_t> ptr(n + 1);
+        XRL_CUDA(cudaMemcpyAsync(ptr.data(), nr->row_ptr.p, 8 * (n + 1), cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        int64_t off = 0;
+        for (int64_t i = 0; i < nrows; ++i) {
+            const int64_t b = ptr[rows[i]], c = ptr[rows[i] + 1] - b;
+            cnt[i] = c;
+            if (c > 0) {
+                if (col) XRL_CUDA(cudaMemcpyAsync(col + off, nr->col.p + b, 4 * c, cudaMemcpyDeviceToHost, st));
+                if (val32) XRL_CUDA(cudaMemcpyAsync(val32 + off, nr->val.p + b, 4 * c, cudaMemcpyDeviceToHost, st));
+                if (val64) XRL_CUDA(cudaMemcpyAsync(val64 + off, nr->val64.p + b, 8 * c, cudaMemcpyDeviceToHost, st));
+            }
+            off += c;
+        }
         XRL_CUDA(cudaStreamSynchronize(st));
         return XRL_OK;
     } catch (const CudaError& e) {

@@ -444,6 +444,12 @@ xrl_status xrl_operator_create(xrl_tree t, xrl_near nr, xrl_topo T, const double
     *out = nullptr;
     if (nr->tree != t || T->tree != t) { set_error("xrl_operator_create: handles from different trees"); return XRL_EPROVENANCE; }
     if (freq < 0) { set_error("xrl_operator_create: negative frequency"); return XRL_EINVAL; }
+    if (t->part_world > 1) {
+        // the loop-space vectors are not sharded: the operator feeds full [3 nrhs][n] panel vectors to the MVM
+        set_error("xrl_operator_create: the loop-space operator runs on single-rank trees only (part_world = %d)",
+                  t->part_world);
+        return XRL_EUNSUPPORTED;
+    }
     if (!zs && (!(sigma > 0) || !(zeta > 0))) { set_error("xrl_operator_create: need zs or sigma, zeta > 0"); return XRL_EINVAL; }
     API_TRY
         XRL_CUDA(cudaSetDevice(t->ctx->device));

@@ -847,24 +847,26 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         // costs no locality).  Leaves above 256 targets are cut into 256 + rest: with 8 targets per thread
         // a task of T <= 256 keeps >= 93 % of its 128 threads busy (T = 352 in one task: 69 %).
         {
-            std::vector<std::pair<int64_t, int2>> cost;
+            // (any leaf size: the first target is an absolute panel index, so a leaf of any size -- leaf_max
+            // is unbounded -- is cut into as many 256-target tasks as it needs)
+            std::vector<std::pair<int64_t, int4>> cost;
             for (int32_t L : own) {
                 int64_t src = 0;
                 for (int64_t q = hup[L]; q < hup[L + 1]; ++q) src += hpe[hus[q]] - hpb[hus[q]];
                 const int nt = hpe[L] - hpb[L];
                 for (int o = 0; o < nt;) {
                     const int c = (nt - o > 256) ? 256 : nt - o;
-                    cost.push_back({-(int64_t)c * src, make_int2(L, (o << 16) | c)});
+                    cost.push_back({-(int64_t)c * src, make_int4(L, hpb[L] + o, c, 0)});
                     o += c;
                 }
             }
             std::stable_sort(cost.begin(), cost.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-            std::vector<int2> ord;
+            std::vector<int4> ord;
             for (auto& c : cost) ord.push_back(c.second);
             T->n_p2p_tasks = (int)ord.size();
             T->p2p_tasks.alloc(std::max<size_t>(1, ord.size()));
             if (!ord.empty())
-                XRL_CUDA(cudaMemcpyAsync(T->p2p_tasks.p, ord.data(), sizeof(int2) * ord.size(), cudaMemcpyHostToDevice, st));
+                XRL_CUDA(cudaMemcpyAsync(T->p2p_tasks.p, ord.data(), sizeof(int4) * ord.size(), cudaMemcpyHostToDevice, st));
             XRL_CUDA(cudaStreamSynchronize(st));
         }
         // relevant boxes: panel range meets [p0, p1) (owned subtrees and their ancestors)

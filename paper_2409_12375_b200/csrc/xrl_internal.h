@@ -161,7 +161,7 @@ struct xrl_tree_s {
     std::vector<uint8_t> rel;                // box relevant to this rank
     xrl::DBuf<int32_t> own_leaves;           // owned leaves (Morton order)
     xrl::DBuf<int> p2p_counter;              // P2P leaf-task counter (reset per MVM)
-    xrl::DBuf<int2> p2p_tasks;               // P2P tasks (leaf, target offset << 16 | count), longest first
+    xrl::DBuf<int4> p2p_tasks;               // P2P tasks (leaf, first target panel, #targets <= 256, 0), longest first
     int32_t n_p2p_tasks = 0;
     int32_t n_own_leaves = 0;
     std::vector<int32_t> l2l_start;          // per-level offsets into l2l_boxes

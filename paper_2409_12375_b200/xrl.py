@@ -24,7 +24,7 @@ EXPORTS = [
     "xrl_last_error", "xrl_version", "xrl_ctx_create", "xrl_ctx_sync", "xrl_ctx_destroy",
     "xrl_tree_build", "xrl_tree_build_poly", "xrl_tree_destroy", "xrl_tree_info", "xrl_tree_perm", "xrl_to_library_order",
     "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble", "xrl_near_destroy",
-    "xrl_near_export", "xrl_mvm", "xrl_mvm_host", "xrl_mvm_host_batch", "xrl_timing_enable", "xrl_timing_count",
+    "xrl_near_export", "xrl_near_export_rows", "xrl_mvm", "xrl_mvm_host", "xrl_mvm_host_batch", "xrl_timing_enable", "xrl_timing_count",
     "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_ctx_set_fuse", "xrl_extract",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
@@ -114,6 +114,7 @@ def lib():
         L.xrl_near_destroy.argtypes = [P]
         L.xrl_near_destroy.restype = None
         L.xrl_near_export.argtypes = [P, P, P, P, P, P]
+        L.xrl_near_export_rows.argtypes = [P, i64, P, P, P, P, P]
         L.xrl_mvm.argtypes = [P, P, P, P, i32, u32]
         L.xrl_mvm_host.argtypes = [P, P, P, P, i32, u32]
         L.xrl_mvm_host_batch.argtypes = [P, P, P, P, i32, i32, u32]
@@ -382,6 +383,20 @@ class Near:
         v64 = np.empty(max(nnz.value, 1), dtype=np.float64)
         check(lib().xrl_near_export(self.h, _ptr(ptr), _ptr(col), _ptr(v32), _ptr(v64), ctypes.byref(nnz)))
         k = nnz.value
+        return ptr, col[:k], v32[:k], v64[:k]
+
+    def export_rows(self, rows):
+        """Selected library-order rows: (ptr, col, v32, v64) over those rows only."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        cnt = np.empty(max(rows.size, 1), dtype=np.int64)
+        check(lib().xrl_near_export_rows(self.h, rows.size, _ptr(rows), _ptr(cnt), None, None, None))
+        ptr = np.zeros(rows.size + 1, dtype=np.int64)
+        np.cumsum(cnt[:rows.size], out=ptr[1:])
+        k = int(ptr[-1])
+        col = np.empty(max(k, 1), dtype=np.int32)
+        v32 = np.empty(max(k, 1), dtype=np.float32)
+        v64 = np.empty(max(k, 1), dtype=np.float64)
+        check(lib().xrl_near_export_rows(self.h, rows.size, _ptr(rows), _ptr(cnt), _ptr(col), _ptr(v32), _ptr(v64)))
         return ptr, col[:k], v32[:k], v64[:k]
 
     def close(self):

@@ -380,3 +380,71 @@ def test_hybrid_topology_box_and_c_maps():
     for t in range(3):
         Clt = sp.csr_matrix((ex["c_val"][:, t], (rows, ex["c_panel"])), shape=(nl, m.n))
         assert np.abs((Clt - C[t]).toarray()).max() <= 1e-12 * np.abs(C[t].toarray()).max()
+
+
+@pytest.fixture(scope="module")
+def coils_all():
+    from paper_2409_12375_b200 import xrl
+    m = meshes.coils()
+    ctx, tree, near = cuda_setup(m)
+    topo = xrl.Topology(tree, [(p, q) for _, p, q in m.ports])
+    return m, ctx, tree, near, topo
+
+
+def test_gmres_coils_a_posteriori_oracle_residual(coils_all):
+    """the GPU GMRES solution of the config-2 system (2 ports, 100 MHz) is checked against
+    the exact discrete system with ONE ORACLE MVM: w = sum_t C_t (diag(Z_s/A) u_t + alpha P u_t),
+    u_t = C_t^T x, with P u_t the oracle's FP64 direct O(N^2) sum and C_t = M A_t from the oracle's
+    Algorithm-1 maps on the library's loop matrix; ||b - w|| / ||b|| <= 10 tol (tol = 1e-4 above 1 MHz)."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo = coils_all
+    f = 1e8
+    zeta = 5e-6
+    op = xrl.Operator(tree, near, topo, f, sigma=SIGMA, zeta=zeta)
+    pc = xrl.Precond(op, exact=True)
+    nl = topo.n_loops
+    b = torch.zeros((2, nl), dtype=torch.complex64, device="cuda")
+    for p in range(2):
+        topo.port_rhs(p, 1.0, out=b[p:p + 1])
+    x, rep = xrl.gmres(op, pc, b)
+    assert rep["converged"].all()
+    xh = x.cpu().numpy().astype(np.complex128)
+    bh = b.cpu().numpy().astype(np.complex128)
+    g = oracle.Geometry(m.verts, m.tris)
+    M, C = _oracle_C(m, g, topo.export())
+    u = np.concatenate([(C[t].T @ xh.T).T for t in range(3)])           # [3*2][n], mesh order
+    pu = oracle.mvm_rows(g, u)
+    zsa = lo.esi(SIGMA, zeta, f) / g.area
+    alpha = 1j * 2 * np.pi * f * lo.MU0 / (4 * np.pi)
+    w = sum((C[t] @ (zsa[None, :] * u[2 * t:2 * t + 2] + alpha * pu[2 * t:2 * t + 2]).T).T for t in range(3))
+    rres = np.linalg.norm(bh - w, axis=1) / np.linalg.norm(bh, axis=1)
+    print("coils a-posteriori oracle residual", rres, "GMRES true_rre", rep["true_rre"], "iters", rep["iters"])
+    assert np.all(rres <= 10 * 1e-4)
+    Z = np.linalg.inv(topo.port_currents(x).T)
+    assert abs(Z[0, 1] - Z[1, 0]) / abs(Z[0, 1]) < 1e-3
+
+
+def test_extract_coils_ten_frequencies(coils_all):
+    """BASELINE config 2: the full preconditioned solve at 10 log-spaced frequencies 1 MHz - 10 GHz (copper
+    sigma = 5.8e7, zeta = 5 um; tolerance rule C-A8: 1e-6 at 1 MHz, 1e-4 above), with the exact
+    diag-of-P Q^-1 of Eq. 10-11: every point converges, Z is reciprocal and passive, L positive-definite,
+    R rises and self L falls with frequency (skin effect)."""
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo = coils_all
+    freqs = np.logspace(6, 10, 10)
+    res = xrl.extract(tree, near, topo, freqs, sigma=SIGMA, zeta=5e-6, exact=True)
+    print("coils 10-frequency sweep: iters", res["iters"].tolist(), "true_rre", res["true_rre"].max())
+    for j, f in enumerate(freqs):
+        print(f"  f={f:.3e}  R11={res['r'][j, 0, 0]:.4f}  L11={res['l'][j, 0, 0] * 1e9:.3f} nH  "
+              f"L12={res['l'][j, 0, 1] * 1e9:.3f} nH")
+    assert res["status"] == 0, res
+    for j in range(len(freqs)):
+        Z, L = res["z"][j], res["l"][j]
+        assert abs(Z[0, 1] - Z[1, 0]) / abs(Z[0, 1]) < 1e-2
+        assert np.all(np.linalg.eigvalsh(0.5 * (Z.real + Z.real.T)) > 0)
+        assert np.all(np.linalg.eigvalsh(0.5 * (L + L.T)) > 0)
+    for p in range(2):
+        assert np.all(np.diff(res["r"][:, p, p]) > -1e-3 * res["r"][0, p, p])
+        assert np.all(np.diff(res["l"][:, p, p]) < 1e-3 * res["l"][0, p, p])
+    assert np.all(res["true_rre"][0] <= 1e-5)

@@ -120,3 +120,127 @@ def test_hybrid_bar_loop_oracle_dc_inductance():
     Lt = lo.bar_partial_inductance_tube(1e-3, 1e-4)
     print("hybrid bar L", L, "tube", Lt)
     assert abs(L - Lt) / Lt < 0.02
+
+
+# ---------------------------------------------------------------- C7: the Eq. 10 preconditioner oracle
+
+def _bar_system():
+    m = meshes.bar()
+    g = oracle.Geometry(m.verts, m.tris)
+    P = oracle.dense_p(g)
+    br, kinds = lo.build_graph(m.tris, [(m.ports[0][1], m.ports[0][2])])
+    M, ends, nn = lo.loop_basis(m.n, br, kinds)
+    A = lo.cm_maps(m.verts, m.tris, g.cent, br)
+    phys = sp.diags((kinds == 0).astype(float))
+    A = [phys @ A[t] for t in range(3)]
+    C = [M @ A[t] for t in range(3)]
+    return m, g, P, M, A, C
+
+
+@pytest.fixture(scope="module")
+def bar_system():
+    return _bar_system()
+
+
+def test_precond_omega_zero_is_resistive_part(bar_system):
+    """SPEC.md:443 (C7): at omega = 0 the diagonal-of-P Q of Eq. 10 is the ESI part Z_s of Eq. 8 exactly:
+    it equals the dense loop system (an independent dense product, loop_system) with alpha = 0, for any
+    P; the diagonal-of-L Q_L reduces to the same matrix."""
+    m, g, P, M, A, C = bar_system
+    zsa = lo.esi(5.8e7, 100e-6, 0.0) / g.area
+    Q = lo.precond_q(C, zsa, 0.0, np.diag(P)).toarray()
+    Z0 = lo.loop_system(C, P, zsa, 0.0)
+    assert np.abs(Q - Z0).max() <= 1e-12 * np.abs(Z0).max()
+    QL = lo.precond_q_diag_l(M, A, zsa, 0.0, P).toarray()
+    assert np.abs(QL - Z0).max() <= 1e-12 * np.abs(Z0).max()
+
+
+def test_precond_one_loop_strip_by_hand():
+    """SPEC.md:442 (C7): the 2-panel strip of unit right triangles T0 = (0,0),(1,0),(0,1) and
+    T1 = (1,0),(1,1),(0,1) with a port (+ on T0, - on T1) has one loop; Q is 1 x 1 and, by hand,
+    Q = sum_t [(m - c0)_t^2 d0 + (m - c1)_t^2 d1] = (d0 + d1)/18 with the shared-edge midpoint
+    m = (1/2, 1/2), centroids (1/3, 1/3), (2/3, 2/3), and d_k = Z_s/A_k + alpha P_kk,
+    A_k = 1/2, P_kk = 4.814459846328 (the right-isosceles centroid self term, golden pin 2).
+    So apply(v) = 18 v / (d0 + d1)."""
+    v = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0]], float)
+    t = np.array([[0, 1, 2], [1, 3, 2]], np.int32)
+    g = oracle.Geometry(v, t)
+    br, kinds = lo.build_graph(t, [([0], [1])])
+    M, ends, nn = lo.loop_basis(2, br, kinds)
+    assert M.shape[0] == 1
+    A = lo.cm_maps(v, t, g.cent, br)
+    C = [M @ A[k] for k in range(3)]
+    zs, alpha = 0.37 + 0.11j, 2.5j
+    pkk = np.array([4.814459846328, 4.814459846328])
+    d = zs / 0.5 + alpha * pkk
+    q_hand = (d[0] + d[1]) / 18.0
+    Q = lo.precond_q(C, np.full(2, zs) / g.area, alpha, np.diag(oracle.dense_p(g)))
+    assert Q.shape == (1, 1)
+    assert abs(Q[0, 0] - q_hand) <= 1e-11 * abs(q_hand)
+    vv = np.array([[1.0 + 2.0j]])
+    z = lo.precond_apply(C, np.full(2, zs) / g.area, alpha, np.diag(oracle.dense_p(g)), [0, 1], vv)
+    assert abs(z[0, 0] - vv[0, 0] / q_hand) <= 1e-11 * abs(vv[0, 0] / q_hand)
+
+
+def test_precond_whole_block_round_trip(bar_system):
+    """SPEC.md:460 (C7): with one block (the exact Q^-1 of Eq. 11), apply(Q x) = x to 1e-9, where Q x is
+    formed by the dense product sum_t C_t (diag(zsa) + alpha diag(P_kk)) C_t^T (loop_system with the
+    diagonal of P), independent of precond_q's sparse assembly; the diag-of-L Q_L likewise against its
+    dense edge-space product M (sum_t A_t diag(zsa) A_t^T + alpha diag(sum_t A_t P A_t^T)) M^T."""
+    m, g, P, M, A, C = bar_system
+    f = 1e8
+    zsa = lo.esi(5.8e7, 100e-6, f) / g.area
+    alpha = 1j * 2 * np.pi * f * lo.MU0 / (4 * np.pi)
+    nl = M.shape[0]
+    rng = np.random.default_rng(11)
+    x = rng.normal(size=(2, nl)) + 1j * rng.normal(size=(2, nl))
+    Qd = lo.loop_system(C, np.diag(np.diag(P)), zsa, alpha)
+    z = lo.precond_apply(C, zsa, alpha, np.diag(P), [0, nl], (Qd @ x.T).T)
+    assert np.linalg.norm(z - x) <= 1e-9 * np.linalg.norm(x)
+    Md = M.toarray()
+    Ad = [A[t].toarray() for t in range(3)]
+    Le = sum(Ad[t] @ P @ Ad[t].T for t in range(3))
+    Zs = sum(Ad[t] @ np.diag(zsa) @ Ad[t].T for t in range(3))
+    QLd = Md @ (Zs + alpha * np.diag(np.diag(Le))) @ Md.T
+    QL = lo.precond_q_diag_l(M, A, zsa, alpha, P)
+    assert np.abs(QL.toarray() - QLd).max() <= 1e-12 * np.abs(QLd).max()
+    zl = lo.block_solve(QL, [0, nl], (QLd @ x.T).T)
+    assert np.linalg.norm(zl - x) <= 1e-9 * np.linalg.norm(x)
+
+
+def test_precond_blocks_solve_their_diagonal_blocks(bar_system):
+    """Block-Jacobi (reading C-A10): for a 64-loop partition, each output block z_B solves Q_BB z_B = v_B
+    with Q_BB cut from the dense product (not from precond_q)."""
+    m, g, P, M, A, C = bar_system
+    f = 1e6
+    zsa = lo.esi(5.8e7, 100e-6, f) / g.area
+    alpha = 1j * 2 * np.pi * f * lo.MU0 / (4 * np.pi)
+    nl = M.shape[0]
+    bptr = list(range(0, nl, 64)) + [nl]
+    v = np.random.default_rng(2).normal(size=(1, nl)) + 0j
+    z = lo.precond_apply(C, zsa, alpha, np.diag(P), bptr, v)
+    Qd = lo.loop_system(C, np.diag(np.diag(P)), zsa, alpha)
+    for a, b in zip(bptr[:-1], bptr[1:]):
+        r = Qd[a:b, a:b] @ z[0, a:b] - v[0, a:b]
+        assert np.linalg.norm(r) <= 1e-10 * np.linalg.norm(v[0, a:b])
+
+
+def test_precond_pattern_frequency_invariant(bar_system):
+    """SPEC.md:467 (C7): Q's sparsity pattern is the same at every frequency (only values change); the
+    diag-of-L source matrix before the loop mapping is diagonal (N_e entries) while diag-of-P
+    couples the edges of each panel."""
+    m, g, P, M, A, C = bar_system
+    pats = []
+    for f in (1e3, 1e6, 1e9, 1e10):
+        zsa = lo.esi(5.8e7, 100e-6, f) / g.area
+        alpha = 1j * 2 * np.pi * f * lo.MU0 / (4 * np.pi)
+        Q = lo.precond_q(C, zsa, alpha, np.diag(P))
+        Q.eliminate_zeros()
+        Q.sort_indices()
+        pats.append((Q.indptr.copy(), Q.indices.copy()))
+    for ip, ix in pats[1:]:
+        assert np.array_equal(ip, pats[0][0]) and np.array_equal(ix, pats[0][1])
+    nphys = A[0].getnnz(axis=1).astype(bool).sum()
+    Ad = [A[t].toarray() for t in range(3)]
+    edge_p = sum(Ad[t] @ np.diag(np.diag(P)) @ Ad[t].T for t in range(3))
+    assert np.count_nonzero(edge_p) > nphys  # diag-of-P: same-panel edges coupled

@@ -326,3 +326,48 @@ def test_hybrid_mesh_p_symmetric_and_far_entries():
     diff = np.argwhere(Pg != P)
     assert all(k == l or pv[k] & pv[l] for k, l in diff)
     assert len(diff) > m.n
+
+
+def test_galerkin_adjacent_rectangle_triangle_pair_against_double_integral():
+    """Pins the Galerkin near rule on a vertex/edge-adjacent pair of DIFFERENT panel types (rectangle k on
+    a long face, triangle l on the end cap, sharing an edge; A_k = 2 A_l): the oracle's symmetrised entry
+    1/2 [rule_k I(.; S_l)/A_l + rule_l I(.; S_k)/A_k] must approximate the exact Galerkin entry
+    (1/(A_k A_l)) int_{S_k} int_{S_l} dS dS'/|r - r'| to the outer rules' accuracy (< 3 %).  The exact value
+    is an independent nested quadrature: scipy dblquad over S_k of the polar-coordinate inner integral
+    (tests/quadrature.py) over S_l.  Swapping A_k and A_l in either term moves the entry by ~25-50 % and a
+    wrong rule/panel pairing by more, so a normalisation slip fails here."""
+    from scipy.integrate import dblquad
+    from tests.quadrature import tri_potential_quad
+    m = meshes.bar_hybrid(length=200e-6, side=40e-6, cell=20e-6)
+    gg = oracle.Geometry(m.verts, m.tris, galerkin=True)
+    quads = [k for k in range(m.n) if m.tris[k, 3] >= 0]
+    tris = [k for k in range(m.n) if m.tris[k, 3] < 0]
+    pair = None
+    for k in quads:
+        sk = set(m.tris[k])
+        for l in tris:
+            if len(sk & set(m.tris[l, :3])) == 2:
+                pair = (k, l)
+                break
+        if pair:
+            break
+    k, l = pair
+    V = m.verts
+    a, b, c, d = (V[i] for i in m.tris[k])
+    ta, tb, tc = (V[i] for i in m.tris[l, :3])
+    Ak = np.linalg.norm(np.cross(b - a, d - a))
+    Al = 0.5 * np.linalg.norm(np.cross(tb - ta, tc - ta))
+    assert Ak == pytest.approx(2 * Al, rel=1e-12)
+
+    def inner(r):
+        return tri_potential_quad(r, ta, tb, tc, epsrel=1e-8)
+    val, err = dblquad(lambda t, s: inner(a + s * (b - a) + t * (d - a)), 0, 1, 0, 1, epsabs=0, epsrel=1e-5)
+    exact = val * Ak / (Ak * Al)  # ds dt = dS / A_k
+    pg = oracle.p_entries(gg, [k], [l])[0, 0]
+    assert pg == pytest.approx(oracle.p_entries(gg, [l], [k])[0, 0], rel=1e-13)
+    print("galerkin rect-tri pair", pg, exact, (pg - exact) / exact)
+    assert abs(pg - exact) / exact < 0.03
+    # collocation for contrast: the centroid entry is farther from the Galerkin value
+    gc = oracle.Geometry(m.verts, m.tris)
+    pc = oracle.p_entries(gc, [k], [l])[0, 0]
+    assert abs(pg - exact) < abs(pc - exact)
