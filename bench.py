@@ -375,12 +375,17 @@ def run_xrl(args):
                                 "warps (fused path), so the in-step rate mixes both; isolated = unfused serial pass",
                         "peak_source": f"{nsm} SMs x 128 FP32 lanes x 2 flops x {sm_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"}
     if phases["near"][1]:
-        byts = 8.0 * nnz + 56.0 * n
+        ni = near.info()
+        nl_ = tree.n_local
+        byts = 6.0 * ni["n_entries"] + 4.0 * ni["n_union"] + 12.0 * ni["n_groups"] + 24.0 * nl_ + 48.0 * nl_
         a, ai = rate("near", byts) / 1e9, rate("near", byts, phases_iso) / 1e9
-        roofs["near"] = {"kernel": "k_near_spmv", "bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": a / hbm_peak, "traffic": traffic_from_profiles("k_near_spmv", tkey),
+        roofs["near"] = {"kernel": "k_near_blk", "bound": "hbm", "achieved": a, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": a / hbm_peak, "traffic": traffic_from_profiles("k_near_blk", tkey),
                          "isolated": {"achieved": ai, "frac": ai / hbm_peak, "ms": per_launch_ms("near", phases_iso)},
-                         "algorithmic": f"8 B x {nnz} nnz + 56 B x {n} rows (row_ptr, x, y) per launch",
+                         "algorithmic": f"6 B x {ni['n_entries']} padded entries (FP32 value + u16 union position; "
+                                        f"{nnz} nnz) + 4 B x {ni['n_union']} union columns + 12 B x {ni['n_groups']} "
+                                        f"groups + 24 B x {nl_} rows of x (read once) + 48 B x {nl_} rows of y "
+                                        f"(read-modify-write) per launch",
                          "peak_source": "hbm_gbs, MEASURED_PEAKS.json"}
     # dominant kernel: largest isolated time (the work that bounds the step)
     dom = max(roofs, key=lambda k: phases_iso[k][0]) if roofs else max(phases, key=lambda k: phases[k][0])

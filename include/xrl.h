@@ -93,8 +93,8 @@ void xrl_ctx_destroy(xrl_ctx ctx);
  * part_rank / part_world: Morton-range partition of the targets (SURVEY
  * §8(e)).  On a multi-rank context they must equal its rank / world (or be
  * 0 / 0).  On a single-rank context part_world > 1 builds rank part_rank's
- * share only ("virtual partition", for testing the sharded path on one GPU
- * through xrl_mvm_gathered).  0 / 0 = no partition. */
+ * share ("virtual rank": k such trees on one context run the sharded MVM on
+ * one GPU through xrl_mvm_vranks).  0 / 0 = no partition. */
 typedef struct {
     int32_t p;
     int32_t leaf_max;
@@ -189,6 +189,11 @@ void xrl_near_destroy(xrl_near near);
  * always written. */
 xrl_status xrl_near_export(xrl_near near, int64_t* row_ptr, int32_t* col, float* val32,
                            double* val64, int64_t* nnz);
+/* Sizes of the near field (any pointer may be NULL): nnz of the CSR (all rows), and of the
+ * row-group format the SpMV streams for this rank's rows: groups of <= 32
+ * consecutive rows, padded entries (FP32 value + u16 position in the group's column
+ * union; 6 B each) and the total length of the column unions (int32 each). */
+xrl_status xrl_near_info(xrl_near near, int64_t* nnz, int64_t* n_groups, int64_t* n_entries, int64_t* n_union);
 /* Selected rows of the CSR (tests on full-size meshes): rows host int64 [nrows]
  * (library order); cnt host int64 [nrows] receives each row's length; col,
  * val32, val64 (any may be NULL) receive the rows concatenated in the given
@@ -199,16 +204,61 @@ xrl_status xrl_near_export_rows(xrl_near near, int64_t nrows, const int64_t* row
 
 /* The hot path: y = P x (flags select diagnostic parts).
  * x, y: device complex64 [nvec][n_local] in library order (this rank's slice
- * [offset, offset + n_local) on a multi-rank context: the slices are
- * gathered with NCCL inside the call), must not alias;
+ * [offset, offset + n_local) on a multi-rank context), must not alias;
  * nvec a multiple of 3 (each triple of complex components = 6 real RHS through
- * one tree traversal).  Enqueued on the context stream. */
+ * one tree traversal).  Enqueued on the context stream.
+ * Multi-rank (plans built at setup from the shared tree and near
+ * pattern): each rank packs its own charges, receives the halo of
+ * remote charges its P2P / P2L / near rows read (grouped ncclSend/ncclRecv),
+ * runs P2M on its own leaves and M2M on its subtrees, all-reduces the partial
+ * multipoles of the boxes that straddle a cut, receives the local-essential-
+ * tree multipoles (grouped send/recv), then computes its slice of y.  All calls
+ * are collective over the context's communicator.  XRL_EUNSUPPORTED for a
+ * partitioned tree on a single-rank context (use xrl_mvm_vranks). */
 xrl_status xrl_mvm(xrl_tree tree, xrl_near near, const void* x, void* y, int32_t nvec, uint32_t flags);
 
-/* As xrl_mvm, but x is already the full vector [nvec][n] (library order) and y
- * this rank's slice [nvec][n_local]; no communication.  Used for the virtual
- * partition on one GPU and by tests. */
-xrl_status xrl_mvm_gathered(xrl_tree tree, xrl_near near, const void* x_full, void* y, int32_t nvec, uint32_t flags);
+/* Virtual ranks: the sharded MVM of k trees partitioned 0..k-1 of one mesh
+ * (xrl_fmm_opts part_rank = r, part_world = k) built on ONE single-rank
+ * context, run in one call on one GPU with the same plans and kernels as the
+ * multi-rank xrl_mvm; the exchanges are device copies between the trees'
+ * buffers instead of NCCL.  x[r], y[r]: device complex64 [nvec][n_local(r)]
+ * (rank r's slice in library order).  The ranks' phases are serialised on the
+ * context stream; rank_ms (host double [k], may be NULL) receives each rank's
+ * device time (its kernels alone on the GPU, summed over the phases) and
+ * exch_ms (may be NULL) the device-copy time of the exchanges -- the inputs of
+ * the multi-GPU projection.  k = 1 with an unpartitioned tree
+ * is the plain MVM.  Errors: XRL_EINVAL (trees not one k-way partition,
+ * aliasing), XRL_EPROVENANCE (near/tree or context mismatch), XRL_EDIM. */
+xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* nears, const void* const* x,
+                          void* const* y, int32_t nvec, uint32_t flags, double* rank_ms, double* exch_ms);
+
+/* Host function (no GPU): the exchange plan of rank `rank` of a `world`-way
+ * partition, from a tree and near pattern given as plain host arrays -- the
+ * code xrl_tree_build / xrl_near_assemble run on a partitioned tree, exported
+ * for CPU multi-process tests.  Boxes b < nbox: panel range [pb[b], pe[b]),
+ * child[b] < 0 for leaves; CSR lists by target box (int64 ptr [nbox+1], int32
+ * sources): V (M2L), X (P2L source leaves), W (M2P), U (P2P source leaves);
+ * near pattern near_ptr int64 [n+1] / near_col int32 (library order); cuts
+ * int32 [world+1] panel offsets.  Outputs: *n_shared and shared [n_shared]
+ * (boxes straddling a cut); let_roff / let_soff int64 [world+1] and
+ * let_ridx / let_sidx (boxes received from / sent to each peer, ascending);
+ * halo_roff / halo_soff int64 [world+1] and halo_ridx / halo_sidx (panels).
+ * Call once with the index arrays NULL to size them. */
+xrl_status xrl_plan_exchange(int32_t nbox, const int32_t* pb, const int32_t* pe, const int32_t* child,
+                             const int64_t* v_ptr, const int32_t* v_src, const int64_t* x_ptr,
+                             const int32_t* x_src, const int64_t* w_ptr, const int32_t* w_src,
+                             const int64_t* u_ptr, const int32_t* u_src, int64_t n, const int64_t* near_ptr,
+                             const int32_t* near_col, int32_t world, const int32_t* cuts, int32_t rank,
+                             int64_t* n_shared, int32_t* shared, int64_t* let_roff, int32_t* let_ridx,
+                             int64_t* let_soff, int32_t* let_sidx, int64_t* halo_roff, int32_t* halo_ridx,
+                             int64_t* halo_soff, int32_t* halo_sidx);
+
+/* Per-MVM exchange volume of a partitioned tree (records per triple; 0 on a
+ * single-rank tree): halo panels sent / received (32 B each: the 6 RHS + pad),
+ * LET boxes sent / received (3 KB each: 6 x 128 floats) and shared boxes
+ * all-reduced (3 KB each).  Any pointer may be NULL. */
+xrl_status xrl_exchange_info(xrl_tree tree, xrl_near near, int64_t* halo_send, int64_t* halo_recv,
+                             int64_t* let_send, int64_t* let_recv, int64_t* shared);
 
 /* End-to-end variant with HOST complex64 buffers [nvec][n] in the mesh's
  * original panel order: H2D copy, reorder, MVM, reorder, D2H copy.  Blocking.

@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
                   "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["abi.cu", "tree.cu", "near.cu", "fmm.cu", "solver.cu", "comm.cu", "operators.cpp", "topology.cpp",
-           "extract.cpp", "precond_exact.cu"]
+           "extract.cpp", "precond_exact.cu", "exchange.cu"]
 
 
 def _nccl_dirs():

@@ -1,14 +1,7 @@
-// Multi-GPU plumbing: NCCL communicator of a multi-rank context
-// and the per-MVM gather of the rank-owned slices of x.
-//
-// Each rank owns a contiguous Morton range of leaves (panels [p0, p1),
-// tree.cu).  An MVM needs the charges of every panel (P2M of all leaves, P2P
-// and near-field sources outside the range), so the owned slices of the three
-// complex components are gathered into the full vectors with one NCCL group of
-// per-rank broadcasts (slices have different lengths, so ncclAllGather's equal
-// counts do not fit).  The rest of the MVM is rank-local: the upward pass is
-// computed redundantly, M2L/P2L/L2L only for boxes meeting the owned range,
-// P2P/L2P/near only for owned targets.
+// Multi-GPU plumbing: NCCL communicator of a multi-rank context and the transport of
+// the sharded MVM's exchanges (plans in exchange.cu): the halo of x and the local-essential-tree
+// multipoles as grouped ncclSend/ncclRecv, the multipoles of the boxes that straddle a cut as one
+// ncclAllReduce.  NVLink/NVSwitch carries them; the volumes are small.
 #include <nccl.h>
 
 #include "xrl_internal.h"
@@ -42,28 +35,37 @@ void comm_destroy(xrl_ctx ctx)
     ctx->nccl_comm = nullptr;
 }
 
-xrl_status gather_slices(xrl_tree t, const float2* x_local, float2* x_full)
+// Grouped point-to-point exchange of packed records: to each peer q the records
+// sbuf[soff[q] .. soff[q+1]) and from each peer q into rbuf[roff[q] .. roff[q+1]) (rec_floats floats per
+// record); the plans are symmetric by construction (exchange.cu), so every send has its matching receive.
+xrl_status nccl_exchange(xrl_ctx ctx, const float* sbuf, const std::vector<int64_t>& soff, float* rbuf,
+                         const std::vector<int64_t>& roff, int rec_floats, cudaStream_t st)
 {
-    xrl_ctx ctx = t->ctx;
-    if (!ctx->nccl_comm) { set_error("gather_slices: context has no communicator"); return XRL_ENCCL; }
-    const int64_t n = t->n, nl = t->p1 - t->p0;
+    if (!ctx->nccl_comm) { set_error("nccl_exchange: context has no communicator"); return XRL_ENCCL; }
+    ncclComm_t comm = (ncclComm_t)ctx->nccl_comm;
     XRL_NCCL(ncclGroupStart());
-    for (int v = 0; v < 3; ++v)
-        for (int r = 0; r < t->part_world; ++r) {
-            const int64_t c0 = t->part_cuts[r], c1 = t->part_cuts[r + 1];
-            if (c1 <= c0) continue;
-            float2* recv = x_full + (size_t)v * n + c0;
-            // sendbuff is read on the root only; the other ranks pass their receive buffer (never NULL)
-            const void* send = (r == ctx->rank) ? (const void*)(x_local + (size_t)v * nl) : (const void*)recv;
-            const ncclResult_t e = ncclBroadcast(send, recv, (size_t)(c1 - c0) * 2, ncclFloat, r,
-                                                 (ncclComm_t)ctx->nccl_comm, ctx->stream);
-            if (e != ncclSuccess) {
-                ncclGroupEnd();  // close the group before reporting, so later NCCL calls are not captured by it
-                set_error("NCCL error %s in ncclBroadcast (gather_slices)", ncclGetErrorString(e));
-                return XRL_ENCCL;
-            }
+    for (int q = 0; q < ctx->world; ++q) {
+        if (q == ctx->rank) continue;
+        ncclResult_t e = ncclSuccess;
+        const int64_t ns = soff[q + 1] - soff[q], nr = roff[q + 1] - roff[q];
+        if (ns > 0) e = ncclSend(sbuf + soff[q] * rec_floats, (size_t)ns * rec_floats, ncclFloat, q, comm, st);
+        if (e == ncclSuccess && nr > 0)
+            e = ncclRecv(rbuf + roff[q] * rec_floats, (size_t)nr * rec_floats, ncclFloat, q, comm, st);
+        if (e != ncclSuccess) {
+            ncclGroupEnd();  // close the group before reporting, so later NCCL calls are not captured by it
+            set_error("NCCL error %s in the MVM exchange", ncclGetErrorString(e));
+            return XRL_ENCCL;
         }
+    }
     XRL_NCCL(ncclGroupEnd());
+    return XRL_OK;
+}
+
+xrl_status nccl_allreduce_sum(xrl_ctx ctx, float* buf, size_t count, cudaStream_t st)
+{
+    if (!ctx->nccl_comm) { set_error("nccl_allreduce_sum: context has no communicator"); return XRL_ENCCL; }
+    if (count == 0) return XRL_OK;
+    XRL_NCCL(ncclAllReduce(buf, buf, count, ncclFloat, ncclSum, (ncclComm_t)ctx->nccl_comm, st));
     return XRL_OK;
 }
 

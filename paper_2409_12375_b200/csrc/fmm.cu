@@ -554,12 +554,22 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
 }
 
 // ------------------------------------------------------------------ near-field SpMV
-// y = N x for the 6 real RHS (N: FP32 CSR of the near correction and the self
-// terms).  HBM-bound: 8 B per nonzero (col + val) + the gathered charges
-// (L2-resident) + 24 B of y per row.  8 lanes per row, 4 rows per warp; each
-// lane issues 4 independent (col, val) loads before their 4 gathers (memory-
-// level parallelism), shuffle reduction over the 8 lanes.
-// 32-byte read-only load through L1 (the charge records are re-read by neighbouring rows)
+// y += N x for the 6 real RHS (N: the near correction and the self terms) over the
+// row-group format of near.cu (build_near_groups).  One WARP per group (persistent over groups, no
+// CTA-wide barrier):
+//   * the group's column union (<= kNearCap records; ~385 for ~3,200 entries of 32 rows on config 4) is
+//     staged once in the warp's slice of shared memory, 24 B per record (the 6 RHS);
+//   * the group's padded entries are contiguous, so the 32 lanes stream them evenly -- lane l takes 4-entry
+//     chunks l, l + 32, ... (float4 values + ushort4 union positions + the chunk's u8 segment id: 6.25 B per
+//     entry, no per-entry column index, no per-entry L2 gather), whatever the row lengths;
+//   * per warp step the 32 chunk partials are combined by a segmented shuffle scan over the (sorted)
+//     segment ids and each run's tail lane adds it to the warp's per-segment accumulator in shared memory;
+//   * finally one lane per segment adds its row total into y with vector L2 reductions (a row cut into
+//     segments adds from several groups; the L2P / M2P add concurrently).
+constexpr int kNearWarps = 8;  // warps per CTA
+constexpr int kNearSmem = kNearWarps * (kNearCap * 24 + kNearGrpSeg * 6 * 4);
+
+// 32-byte read-only load through L1
 __device__ __forceinline__ void ldg256_l1(const float* p, float* v)
 {
     asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -573,68 +583,130 @@ __device__ __forceinline__ void red_add2(float2* p, float a, float b)
     asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
-// One row's 8-lane share of the near SpMV with global gathers: lane loads kNearU (col, value) pairs, then
-// issues their kNearU 32-byte charge gathers with the next batch's pairs loaded behind them.
-template <int kNearU>
-__device__ __forceinline__ void near_row_global(int64_t j0, int64_t e, const int2* __restrict__ cv,
-                                                const float* __restrict__ xq, float* a)
+// streaming loads (entries are read once per MVM: no L1 allocation)
+__device__ __forceinline__ float4 ldg_stream4(const float* p)
 {
-    constexpr int kL = 8;
-    // software pipeline: the next batch's (col, val) loads are in flight while this batch's gathers land
-    int2 c[kNearU];
-#pragma unroll
-    for (int u = 0; u < kNearU; ++u) {
-        const int64_t j = j0 + (int64_t)u * kL;
-        c[u] = j < e ? __ldcs(cv + j) : make_int2(-1, 0);
-    }
-    while (j0 < e) {
-        float q[kNearU][8];
-#pragma unroll
-        for (int u = 0; u < kNearU; ++u) {
-            if (c[u].x >= 0) {
-                ldg256_l1(xq + 8 * (int64_t)c[u].x, q[u]);  // the whole 32-byte charge record, one request
-            } else {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) q[u][r] = 0.f;
-            }
-        }
-        float v[kNearU];
-#pragma unroll
-        for (int u = 0; u < kNearU; ++u) v[u] = __int_as_float(c[u].y);
-        j0 += kL * kNearU;
-#pragma unroll
-        for (int u = 0; u < kNearU; ++u) {
-            const int64_t j = j0 + (int64_t)u * kL;
-            c[u] = j < e ? __ldcs(cv + j) : make_int2(-1, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < kNearU; ++u)
-#pragma unroll
-            for (int r = 0; r < 6; ++r) a[r] = fmaf(v[u], q[u][r], a[r]);
-    }
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ldg_stream_u64(const uint16_t* p)
+{
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
 }
 
-__global__ void __launch_bounds__(256, 6) k_near_spmv(int64_t n, int64_t r0, const int64_t* __restrict__ ptr,
-                                                   const int2* __restrict__ cv, const float* __restrict__ xq,
-                                                   int accumulate, float2* __restrict__ y)
+__device__ __forceinline__ void near_fma(const float2 (*X)[3], int j, float v, float* a)
 {
-    // rows r0 .. r0+n-1 (owned range); y local [3][n].  8 lanes per row, each lane keeps kNearU gathers
-    // in flight with the next kNearU (col, val) loads issued behind them (memory-level parallelism;
-    // 6 CTAs of 256 per SM leave 40 registers for the two batches).
-    constexpr int kL = 8, kNearU = 4;
-    const int64_t lrow = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kL;
-    const int64_t row = r0 + lrow;
-    const int lane = threadIdx.x & (kL - 1);
-    float a[6] = {0, 0, 0, 0, 0, 0};
-    if (lrow < n) near_row_global<kNearU>(ptr[row] + lane, ptr[row + 1], cv, xq, a);
+    const float2 q0 = X[j][0], q1 = X[j][1], q2 = X[j][2];
+    a[0] = fmaf(v, q0.x, a[0]); a[1] = fmaf(v, q0.y, a[1]);
+    a[2] = fmaf(v, q1.x, a[2]); a[3] = fmaf(v, q1.y, a[3]);
+    a[4] = fmaf(v, q2.x, a[4]); a[5] = fmaf(v, q2.y, a[5]);
+}
+
+constexpr int kNearUnroll = 6;                  // chunks in flight per lane
+constexpr int kNearRec = (kNearCap + 31) / 32;  // union records per lane and group
+
+__global__ void __launch_bounds__(kNearWarps * 32, 2) k_near_blk(
+    int ngroups, const int32_t* __restrict__ grp_seg, const int64_t* __restrict__ grp_u,
+    const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_off, const float* __restrict__ eval,
+    const uint16_t* __restrict__ eidx, const uint8_t* __restrict__ cseg, const int32_t* __restrict__ ucol,
+    const float* __restrict__ xq, int64_t nl, float2* __restrict__ y)
+{
+    extern __shared__ __align__(16) float near_sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float2(*X)[3] = reinterpret_cast<float2(*)[3]>(near_sm + warp * kNearCap * 6);
+    float(*acc)[6] = reinterpret_cast<float(*)[6]>(near_sm + kNearWarps * kNearCap * 6 + warp * kNearGrpSeg * 6);
+    const int stride = gridDim.x * kNearWarps;
+    // the union columns of a group, lane-strided into registers (-1: none)
+    auto load_cols = [&](int g, int (&c)[kNearRec]) {
+        int64_t u0 = 0;
+        int nu = 0;
+        if (g < ngroups) { u0 = __ldg(grp_u + g); nu = (int)(__ldg(grp_u + g + 1) - u0); }
 #pragma unroll
-    for (int r = 0; r < 6; ++r) {
+        for (int k = 0; k < kNearRec; ++k) c[k] = 32 * k + lane < nu ? __ldg(ucol + u0 + 32 * k + lane) : -1;
+    };
+    int col[kNearRec];
+    int g = blockIdx.x * kNearWarps + warp;
+    load_cols(g, col);
+    for (; g < ngroups; g += stride) {
+        // stage this group's union records (their columns were loaded one group ahead)
 #pragma unroll
-        for (int o = 1; o < kL; o <<= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], o);
-    }
-    if (lrow < n && lane < 3) {
-        if (accumulate) red_add2(y + lane * n + lrow, a[2 * lane], a[2 * lane + 1]);
-        else y[lane * n + lrow] = make_float2(a[2 * lane], a[2 * lane + 1]);
+        for (int k0 = 0; k0 < kNearRec; k0 += 4) {
+            float q[4][8];
+#pragma unroll
+            for (int k = k0; k < k0 + 4 && k < kNearRec; ++k)
+                if (col[k] >= 0) ldg256_l1(xq + 8 * (int64_t)col[k], q[k - k0]);
+#pragma unroll
+            for (int k = k0; k < k0 + 4 && k < kNearRec; ++k)
+                if (col[k] >= 0) {
+                    float2* d = X[32 * k + lane];
+                    d[0] = make_float2(q[k - k0][0], q[k - k0][1]);
+                    d[1] = make_float2(q[k - k0][2], q[k - k0][3]);
+                    d[2] = make_float2(q[k - k0][4], q[k - k0][5]);
+                }
+        }
+        load_cols(g + stride, col);  // the next group's columns, in flight during this group
+#pragma unroll
+        for (int r = 0; r < 6; ++r) acc[lane][r] = 0.f;
+        __syncwarp();
+        const int s0 = __ldg(grp_seg + g), ns = __ldg(grp_seg + g + 1) - s0;
+        const int64_t c0 = __ldg(seg_off + s0) >> 2, c1 = __ldg(seg_off + s0 + ns) >> 2;  // chunk range
+        for (int64_t cb = c0; cb < c1; cb += 32 * kNearUnroll) {
+            float4 v[kNearUnroll];
+            uint2 ix[kNearUnroll];
+            int sid[kNearUnroll];
+#pragma unroll
+            for (int u = 0; u < kNearUnroll; ++u) {
+                const int64_t c = cb + 32 * u + lane;
+                if (c < c1) {
+                    v[u] = ldg_stream4(eval + 4 * c);
+                    ix[u] = ldg_stream_u64(eidx + 4 * c);
+                    sid[u] = __ldg(cseg + c);
+                } else {
+                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    ix[u] = make_uint2(0u, 0u);
+                    sid[u] = 255;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kNearUnroll; ++u) {
+                if (cb + 32 * u >= c1) break;  // warp-uniform
+                float a[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                near_fma(X, ix[u].x & 0xffff, v[u].x, a);
+                near_fma(X, ix[u].x >> 16, v[u].y, a);
+                near_fma(X, ix[u].y & 0xffff, v[u].z, a);
+                near_fma(X, ix[u].y >> 16, v[u].w, a);
+                // segmented inclusive scan over the lanes (segment ids ascend with the lane)
+                const int k = sid[u];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int ku = __shfl_up_sync(0xffffffffu, k, o);
+                    float up[6];
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) up[r] = __shfl_up_sync(0xffffffffu, a[r], o);
+                    if (lane >= o && ku == k) {
+#pragma unroll
+                        for (int r = 0; r < 6; ++r) a[r] += up[r];
+                    }
+                }
+                const int kn = __shfl_down_sync(0xffffffffu, k, 1);
+                if (k != 255 && (lane == 31 || kn != k)) {
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) acc[k][r] += a[r];
+                }
+                __syncwarp();
+            }
+        }
+        if (lane < ns) {
+            const int64_t row = __ldg(seg_row + s0 + lane);
+            red_add2(y + row, acc[lane][0], acc[lane][1]);
+            red_add2(y + nl + row, acc[lane][2], acc[lane][3]);
+            red_add2(y + 2 * nl + row, acc[lane][4], acc[lane][5]);
+        }
+        __syncwarp();  // the stage and the accumulators are reused by the next group
     }
 }
 
@@ -1060,6 +1132,7 @@ void upload_constants(xrl_ctx ctx)
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2MSmem));
+    XRL_CUDA(cudaFuncSetAttribute(k_near_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, kNearSmem));
 }
 
 }  // namespace xrl
@@ -1077,10 +1150,183 @@ static void translate_level(xrl_tree t, std::pair<int, int> lvl, const float* sr
     ctx->launches += 1;
 }
 
-// x: full (gathered) triple [3][n]; y: owned slice [3][n_local] of panels [p0, p1).
-static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags)
+// ------------------------------------------------------------------ the MVM, phase by phase
+// One triple (6 real RHS) through the tree.  Phases (each enqueued, none blocking):
+//   begin  -> pack the owned charges -> [halo of x]                            (work stream)
+//   side   -> P2P, then the near SpMV unless it waits for the fused P2P       (side stream)
+//   up     -> P2M (own leaves), M2M -> [shared-box all-reduce, LET]          (work stream)
+//   down   -> M2L (+ fused P2P warps), near, P2L, L2L, L2P, M2P, join       (work stream)
+// [..]: only on a partitioned tree; the exchanges run over NCCL (xrl_mvm) or as device copies between
+// the trees of one process (xrl_mvm_vranks).  Single-rank trees own every panel and exchange nothing.
+struct Mvm {
+    xrl_tree t;
+    xrl_near nr;
+    float2* y;
+    uint32_t flags;
+    int sched;
+    cudaStream_t st, side;
+    bool do_far, do_near, chain, fuse, side_done;
+    int64_t nl, p0;
+    float invW;
+};
+
+static Mvm mvm_make(xrl_tree t, xrl_near nr, float2* y, uint32_t flags, int sched)
 {
     xrl_ctx ctx = t->ctx;
+    Mvm M;
+    M.t = t;
+    M.nr = nr;
+    M.y = y;
+    M.flags = flags;
+    M.sched = sched;
+    M.st = sched ? ctx->work : ctx->stream;
+    M.side = sched ? ctx->side : ctx->stream;
+    M.do_far = flags != XRL_MVM_NEAR_ONLY;
+    M.do_near = flags != XRL_MVM_FAR_ONLY;
+    M.chain = M.do_far && t->nlevel > 1;
+    M.fuse = sched != 0 && ctx->fuse_p2p && M.chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0;
+    M.side_done = false;
+    M.nl = t->p1 - t->p0;
+    M.p0 = t->p0;
+    M.invW = (float)(1.0 / t->W);
+    return M;
+}
+
+// x: this rank's slice [3][n_local] (the whole vector on a single-rank tree)
+static void mvm_begin(Mvm& M, const float2* x)
+{
+    xrl_tree t = M.t;
+    xrl_ctx ctx = t->ctx;
+    if (M.sched) {
+        XRL_CUDA(cudaEventRecord(ctx->ev_work, ctx->stream));
+        XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_work, 0));
+    }
+    cudaEvent_t ev;
+    phase_begin(ctx, PH_PACK, &ev, M.st);
+    if (M.nl > 0) {
+        k_pack<<<nblk(M.nl, 256), 256, 0, M.st>>>(M.nl, x, t->xq.p + 8 * M.p0);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    phase_end(ctx, PH_PACK, ev, M.st);
+    XRL_CUDA(cudaMemsetAsync(t->p2p_counter.p, 0, sizeof(int), M.st));  // P2P leaf tasks (before the fork)
+}
+
+// halo of x, step 1: pack the records peers read (work stream)
+static void halo_pack(Mvm& M)
+{
+    xrl_near N = M.nr;
+    gather_records(N->halo_soff.back(), 8, N->halo_sidx.p, M.t->xq.p, N->halo_sbuf.p, M.st);
+    M.t->ctx->launches += N->halo_soff.back() > 0;
+}
+// step 3 (after the transport): scatter the received records into the charges
+static void halo_unpack(Mvm& M)
+{
+    xrl_near N = M.nr;
+    scatter_records(N->halo_roff.back(), 8, N->halo_ridx.p, N->halo_rbuf.p, M.t->xq.p, M.st);
+    M.t->ctx->launches += N->halo_roff.back() > 0;
+}
+
+static void launch_near(Mvm& M)
+{
+    xrl_tree t = M.t;
+    xrl_ctx ctx = t->ctx;
+    xrl_near nr = M.nr;
+    cudaEvent_t ev;
+    if (M.do_near) {
+        phase_begin(ctx, PH_NEAR, &ev, M.side);
+        // the SpMV adds into y: in the near-only mode it starts from zero
+        if (!M.do_far && M.nl > 0) XRL_CUDA(cudaMemsetAsync(M.y, 0, sizeof(float2) * 3 * (size_t)M.nl, M.side));
+        if (nr->n_groups > 0) {
+            const int grid = std::min((nr->n_groups + kNearWarps - 1) / kNearWarps, 2 * ctx->num_sms);
+            k_near_blk<<<grid, kNearWarps * 32, kNearSmem, M.side>>>(nr->n_groups, nr->grp_seg.p, nr->grp_u.p,
+                                                                      nr->seg_row.p, nr->seg_off.p, nr->eval.p,
+                                                                      nr->eidx.p, nr->cseg.p, nr->ucol.p, t->xq.p,
+                                                                      M.nl, M.y);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+        phase_end(ctx, PH_NEAR, ev, M.side);
+    }
+    XRL_CUDA(cudaEventRecord(ctx->ev_join, M.side));
+}
+
+// fork the side stream: the P2P (FP32-bound; shares SMs well with the tensor-core M2L), then the near
+// SpMV unless it must wait for the P2P tasks fused into the M2L kernel
+static void mvm_side(Mvm& M)
+{
+    xrl_tree t = M.t;
+    xrl_ctx ctx = t->ctx;
+    cudaEvent_t ev;
+    M.side_done = true;
+    XRL_CUDA(cudaEventRecord(ctx->ev_fork, M.st));
+    XRL_CUDA(cudaStreamWaitEvent(M.side, ctx->ev_fork, 0));
+    if (M.do_far) {
+        phase_begin(ctx, PH_P2P, &ev, M.side);
+        if (t->n_own_leaves > 0) {
+            k_p2p<<<t->n_p2p_tasks, 128, kP2PSmem, M.side>>>(t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p,
+                                                            t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
+                                                            t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
+                                                            M.invW, 0, M.nl, M.p0, M.y);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+        phase_end(ctx, PH_P2P, ev, M.side);
+    }
+    XRL_CUDA(cudaEventRecord(ctx->ev_p2p, M.side));  // y holds the P2P part: the L2P may add to it
+    if (!M.fuse) launch_near(M);
+}
+
+// upward pass: P2M of the own leaves, M2M of the relevant boxes
+static void mvm_up(Mvm& M)
+{
+    xrl_tree t = M.t;
+    xrl_ctx ctx = t->ctx;
+    if (!M.chain) return;
+    cudaEvent_t ev;
+    phase_begin(ctx, PH_P2M, &ev, M.st);
+    XRL_CUDA(cudaMemsetAsync(t->mu.p, 0, t->mu.bytes(), M.st));  // parents accumulate the M2M reductions
+    if (t->n_own_leaves > 0) {
+        k_p2m<<<t->n_own_leaves, 128, kP2MSmem, M.st>>>(t->own_leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p,
+                                                         t->xq.p, t->mu.p);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    phase_end(ctx, PH_P2M, ev, M.st);
+    phase_begin(ctx, PH_M2M, &ev, M.st);
+    for (int l = t->nlevel - 2; l >= 2; --l) translate_level(t, t->m2m_lvl[l], t->mu.p, t->mu.p, M.st);
+    phase_end(ctx, PH_M2M, ev, M.st);
+}
+
+// multipole exchange, step 1: pack the shared boxes' partial multipoles and the LET boxes peers need
+static void mu_pack(Mvm& M)
+{
+    xrl_tree t = M.t;
+    gather_records((int64_t)t->shared_boxes.size(), kMuStride, t->sh_idx.p, t->mu.p, t->sh_buf.p, M.st);
+    t->ctx->launches += !t->shared_boxes.empty();
+}
+// step 2 (after the shared all-reduce): full multipoles of the shared boxes back into mu; pack the LET
+static void mu_shared_unpack_let_pack(Mvm& M)
+{
+    xrl_tree t = M.t;
+    scatter_records((int64_t)t->shared_boxes.size(), kMuStride, t->sh_idx.p, t->sh_buf.p, t->mu.p, M.st);
+    gather_records(t->let_soff.back(), kMuStride, t->let_sidx.p, t->mu.p, t->let_sbuf.p, M.st);
+    t->ctx->launches += !t->shared_boxes.empty() + (t->let_soff.back() > 0);
+}
+// step 3 (after the LET transport): the received multipoles into mu
+static void let_unpack(Mvm& M)
+{
+    xrl_tree t = M.t;
+    scatter_records(t->let_roff.back(), kMuStride, t->let_ridx.p, t->let_rbuf.p, t->mu.p, M.st);
+    t->ctx->launches += t->let_roff.back() > 0;
+}
+
+// downward pass and the join
+static void mvm_down(Mvm& M)
+{
+    xrl_tree t = M.t;
+    xrl_ctx ctx = t->ctx;
+    cudaEvent_t ev;
 #ifdef XRL_PROFILING_ABLATION
     // XRL_M2L_DBG (profiling ablations, WRONG RESULTS; only in a library built with
     // -DXRL_PROFILING_ABLATION): 1 skip reductions, 2 skip A loads, 4 skip D reads
@@ -1093,147 +1339,159 @@ static void mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint
 #else
     constexpr int m2l_dbg = 0;  // the shipped library has no ablation switch
 #endif
-    // Scheduling (xrl_ctx_set_sched): 0 = one stream (phases isolated, profiling); 1 (default) = P2P
-    // then the near SpMV on the low-priority side stream forked after the pack (the FP32-bound P2P
-    // shares SMs with the tensor-core M2L); 2 = forked when the M2L is launched.  The FMM chain runs
-    // on the library's high-priority work stream, joined back into ctx->stream.
-    const int sched = ctx->sched;
-    cudaStream_t st = sched ? ctx->work : ctx->stream, side = sched ? ctx->side : ctx->stream;
-    if (sched) {
-        XRL_CUDA(cudaEventRecord(ctx->ev_work, ctx->stream));
-        XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_work, 0));
-    }
-    const int64_t n = t->n;
-    const int64_t nl = t->p1 - t->p0, p0 = t->p0;
-    const bool do_far = flags != XRL_MVM_NEAR_ONLY;
-    const bool do_near = flags != XRL_MVM_FAR_ONLY;
-    const float invW = (float)(1.0 / t->W);
-    cudaEvent_t ev;
-
-    phase_begin(ctx, PH_PACK, &ev, st);
-    k_pack<<<nblk(n, 256), 256, 0, st>>>(n, x, t->xq.p);
-    XRL_LAUNCH_CHECK();
-    ctx->launches += 1;
-    phase_end(ctx, PH_PACK, ev, st);
-    XRL_CUDA(cudaMemsetAsync(t->p2p_counter.p, 0, sizeof(int), st));  // P2P leaf tasks (before the fork)
-
-    // near SpMV and P2P depend only on the packed charges.  With the fused P2P (P2P leaf tasks also taken
-    // by three warps of the M2L kernel) the near SpMV, which accumulates into y after the P2P wrote it,
-    // waits for the M2L kernel as well.
-    const bool chain = do_far && t->nlevel > 1;
-    const bool fuse = sched != 0 && ctx->fuse_p2p && chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0;
-    auto launch_p2p = [&]() {
-        XRL_CUDA(cudaEventRecord(ctx->ev_fork, st));
-        XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
-        // P2P (FP32-bound) first: it shares SMs well with the tensor-core M2L
-        if (do_far) {
-            phase_begin(ctx, PH_P2P, &ev, side);
-            if (t->n_own_leaves > 0)
-                k_p2p<<<t->n_p2p_tasks, 128, kP2PSmem, side>>>(t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p,
-                                                         t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
-                                                         t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW,
-                                                         0, nl, p0, y);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
-            phase_end(ctx, PH_P2P, ev, side);
-        }
-        XRL_CUDA(cudaEventRecord(ctx->ev_p2p, side));  // y holds the P2P part: the L2P may add to it
-    };
-    auto launch_near = [&]() {
-        if (fuse) XRL_CUDA(cudaStreamWaitEvent(side, ctx->ev_m2l, 0));  // fused P2P tasks done
-        if (do_near) {
-            phase_begin(ctx, PH_NEAR, &ev, side);
-            if (nl > 0)
-                k_near_spmv<<<nblk(8 * nl, 256), 256, 0, side>>>(nl, p0, nr->row_ptr.p, nr->cv.p, t->xq.p,
-                                                                 do_far ? 1 : 0, y);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
-            phase_end(ctx, PH_NEAR, ev, side);
-        }
-        XRL_CUDA(cudaEventRecord(ctx->ev_join, side));
-    };
-    if (sched != 2 || !chain) {
-        launch_p2p();
-        if (!fuse) launch_near();
-    }
-
-    if (do_far && t->nlevel > 1) {
-        phase_begin(ctx, PH_P2M, &ev, st);
-        XRL_CUDA(cudaMemsetAsync(t->mu.p, 0, t->mu.bytes(), st));  // parents accumulate the M2M reductions
-        k_p2m<<<t->nleaf, 128, kP2MSmem, st>>>(t->leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p, t->xq.p, t->mu.p);
-        XRL_LAUNCH_CHECK();
-        ctx->launches += 1;
-        phase_end(ctx, PH_P2M, ev, st);
-
-        phase_begin(ctx, PH_M2M, &ev, st);
-        for (int l = t->nlevel - 2; l >= 2; --l) translate_level(t, t->m2m_lvl[l], t->mu.p, t->mu.p, st);
-        phase_end(ctx, PH_M2M, ev, st);
-
-        XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), st));
-        if (sched == 2) {
-            launch_p2p();
-            if (!fuse) launch_near();
-        }
-        phase_begin(ctx, PH_M2L, &ev, st);
+    if (M.chain) {
+        XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), M.st));
+        if (!M.side_done) mvm_side(M);  // XRL_SCHED_LATE, or the virtual-rank driver
+        phase_begin(ctx, PH_M2L, &ev, M.st);
         if (t->n_m2l_tiles > 0) {
             const int grid = std::min(ctx->num_sms, t->n_m2l_blocks);
             P2PTasks tasks{};
-            if (fuse)
+            if (M.fuse)
                 tasks = P2PTasks{t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
-                                 t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, invW, nl, p0,
-                                 y};
-            k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p, t->m2l_tgt.p,
-                                                        t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu.p, t->ell.p, m2l_dbg,
-                                                        tasks);
+                                 t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, M.invW, M.nl,
+                                 M.p0, M.y};
+            k_m2l_tc<<<grid, kTcThreads, kTcSmem, M.st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p,
+                                                          t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu.p,
+                                                          t->ell.p, m2l_dbg, tasks);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
-        phase_end(ctx, PH_M2L, ev, st);
-        if (fuse) {
-            XRL_CUDA(cudaEventRecord(ctx->ev_m2l, st));
-            launch_near();
+        phase_end(ctx, PH_M2L, ev, M.st);
+        if (M.fuse) {
+            XRL_CUDA(cudaEventRecord(ctx->ev_m2l, M.st));
+            XRL_CUDA(cudaStreamWaitEvent(M.side, ctx->ev_m2l, 0));  // fused P2P tasks done
+            launch_near(M);
         }
-
-        phase_begin(ctx, PH_P2L, &ev, st);
+        phase_begin(ctx, PH_P2L, &ev, M.st);
         if (t->n_x_targets > 0) {
-            k_p2l<<<t->n_x_targets, 128, kP2LSmem, st>>>(t->x_targets.p, t->x_ptr.p, t->x_src.p, t->blevel.p, t->bix.p,
-                                                         t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->loc.p, t->xq.p,
-                                                         t->ell.p);
+            k_p2l<<<t->n_x_targets, 128, kP2LSmem, M.st>>>(t->x_targets.p, t->x_ptr.p, t->x_src.p, t->blevel.p,
+                                                           t->bix.p, t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->loc.p,
+                                                           t->xq.p, t->ell.p);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
-        phase_end(ctx, PH_P2L, ev, st);
-
-        phase_begin(ctx, PH_L2L, &ev, st);
-        for (int l = 3; l < t->nlevel; ++l) translate_level(t, t->l2l_lvl[l], t->ell.p, t->ell.p, st);
-        phase_end(ctx, PH_L2L, ev, st);
+        phase_end(ctx, PH_P2L, ev, M.st);
+        phase_begin(ctx, PH_L2L, &ev, M.st);
+        for (int l = 3; l < t->nlevel; ++l) translate_level(t, t->l2l_lvl[l], t->ell.p, t->ell.p, M.st);
+        phase_end(ctx, PH_L2L, ev, M.st);
+    } else if (!M.side_done) {
+        mvm_side(M);
     }
     // after the P2P wrote y, the local-expansion / W-list evaluation adds to it (vector L2 reductions, so it
     // may overlap the near SpMV, which adds the same way); join the side stream at the end
-    if (sched) XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_p2p, 0));
-    if (do_far && t->nlevel > 1 && nl > 0) {
-        phase_begin(ctx, PH_L2P, &ev, st);
+    if (M.sched) XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_p2p, 0));
+    if (M.chain && M.nl > 0) {
+        phase_begin(ctx, PH_L2P, &ev, M.st);
         if (t->ellk.n < (size_t)t->nbox * kEllKStride) t->ellk.alloc((size_t)t->nbox * kEllKStride);
         if (t->n_own_leaves > 0) {
-            k_ell_kmajor<<<t->n_own_leaves, 256, 0, st>>>(t->own_leaves.p, t->ell.p, t->ellk.p);
+            k_ell_kmajor<<<t->n_own_leaves, 256, 0, M.st>>>(t->own_leaves.p, t->ell.p, t->ellk.p);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
-        k_l2p<<<nblk(nl, 128), 128, 0, st>>>(nl, p0, t->panel_leaf.p, t->blevel.p, t->loc.p, t->ellk.p, invW, y);
+        k_l2p<<<nblk(M.nl, 128), 128, 0, M.st>>>(M.nl, M.p0, t->panel_leaf.p, t->blevel.p, t->loc.p, t->ellk.p,
+                                                 M.invW, M.y);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
-        if (t->n_w_targets > 0)
-            k_m2p<<<t->n_w_targets, 128, 0, st>>>(t->w_targets.p, p0, nl, t->bpb.p, t->bpe.p, t->blevel.p, t->bix.p,
-                                                  t->biy.p, t->biz.p, t->loc.p, t->mu.p, invW, y);
-        XRL_LAUNCH_CHECK();
-        ctx->launches += 1;
-        phase_end(ctx, PH_L2P, ev, st);
+        if (t->n_w_targets > 0) {
+            k_m2p<<<t->n_w_targets, 128, 0, M.st>>>(t->w_targets.p, M.p0, M.nl, t->bpb.p, t->bpe.p, t->blevel.p,
+                                                    t->bix.p, t->biy.p, t->biz.p, t->loc.p, t->mu.p, M.invW, M.y);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+        }
+        phase_end(ctx, PH_L2P, ev, M.st);
     }
-    if (sched) {  // join the side stream, then the work stream back into the caller's stream
-        XRL_CUDA(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-        XRL_CUDA(cudaEventRecord(ctx->ev_work, st));
+    if (M.sched) {  // join the side stream, then the work stream back into the caller's stream
+        XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_join, 0));
+        XRL_CUDA(cudaEventRecord(ctx->ev_work, M.st));
         XRL_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_work, 0));
     }
+}
+
+// One triple on this process's tree: x this rank's slice [3][n_local], y the same.  On a partitioned
+// multi-rank tree the exchanges run over NCCL between the phases.
+static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags)
+{
+    xrl_ctx ctx = t->ctx;
+    Mvm M = mvm_make(t, nr, y, flags, ctx->sched);
+    const bool dist = t->part_world > 1;
+    mvm_begin(M, x);
+    if (dist) {
+        halo_pack(M);
+        xrl_status s = nccl_exchange(ctx, nr->halo_sbuf.p, nr->halo_soff, nr->halo_rbuf.p, nr->halo_roff, 8, M.st);
+        if (s) return s;
+        halo_unpack(M);
+    }
+    if (M.sched != XRL_SCHED_LATE || !M.chain) mvm_side(M);
+    mvm_up(M);
+    if (dist && M.chain) {
+        mu_pack(M);
+        xrl_status s = nccl_allreduce_sum(ctx, t->sh_buf.p, t->shared_boxes.size() * (size_t)kMuStride, M.st);
+        if (s) return s;
+        mu_shared_unpack_let_pack(M);
+        s = nccl_exchange(ctx, t->let_sbuf.p, t->let_soff, t->let_rbuf.p, t->let_roff, kMuStride, M.st);
+        if (s) return s;
+        let_unpack(M);
+    }
+    mvm_down(M);
+    return XRL_OK;
+}
+
+// Per-rank device times of the virtual-rank driver (events on the context stream, serial schedule).
+struct VTimer {
+    xrl_ctx ctx;
+    bool on;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;  // (slot, (begin, end))
+    cudaEvent_t b = nullptr;
+    void begin()
+    {
+        if (!on) return;
+        XRL_CUDA(cudaEventCreate(&b));
+        XRL_CUDA(cudaEventRecord(b, ctx->stream));
+    }
+    void end(int slot)
+    {
+        if (!on) return;
+        cudaEvent_t e;
+        XRL_CUDA(cudaEventCreate(&e));
+        XRL_CUDA(cudaEventRecord(e, ctx->stream));
+        ev.push_back({slot, {b, e}});
+    }
+    void collect(double* ms)
+    {
+        if (!on) return;
+        XRL_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (auto& p : ev) {
+            float v = 0.f;
+            XRL_CUDA(cudaEventElapsedTime(&v, p.second.first, p.second.second));
+            ms[p.first] += v;
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        ev.clear();
+    }
+};
+
+// Device-copy transport of one exchange between the k trees of a virtual-rank run: rank q's send
+// segment for r -> rank r's receive segment from q.
+template <typename SOff, typename ROff, typename SBuf, typename RBuf>
+static xrl_status vcopy(int k, const std::vector<Mvm>& Ms, SOff soff, ROff roff, SBuf sbuf, RBuf rbuf, int w,
+                        cudaStream_t st)
+{
+    for (int r = 0; r < k; ++r)
+        for (int q = 0; q < k; ++q) {
+            if (q == r) continue;
+            const std::vector<int64_t>& so = soff(Ms[q]);
+            const std::vector<int64_t>& ro = roff(Ms[r]);
+            const int64_t cnt = so[r + 1] - so[r];
+            if (cnt != ro[q + 1] - ro[q]) {
+                set_error("xrl_mvm_vranks: exchange plans of ranks %d and %d disagree", q, r);
+                return XRL_EINVAL;
+            }
+            if (cnt > 0)
+                XRL_CUDA(cudaMemcpyAsync(rbuf(Ms[r]) + ro[q] * w, sbuf(Ms[q]) + so[r] * w, sizeof(float) * cnt * w,
+                                         cudaMemcpyDeviceToDevice, st));
+        }
+    return XRL_OK;
 }
 
 extern "C" {
@@ -1246,24 +1504,16 @@ xrl_status xrl_mvm(xrl_tree t, xrl_near nr, const void* x, void* y, int32_t nvec
     if (x == y) { set_error("xrl_mvm: x and y alias"); return XRL_EINVAL; }
     if (flags > XRL_MVM_FAR_ONLY) { set_error("xrl_mvm: bad flags"); return XRL_EINVAL; }
     if (((uintptr_t)x | (uintptr_t)y) & 15) { set_error("xrl_mvm: vectors must be 16-byte aligned"); return XRL_EINVAL; }
+    if (t->part_world > 1 && t->ctx->world == 1) {
+        set_error("xrl_mvm: a partitioned tree on a single-rank context (virtual rank) runs through xrl_mvm_vranks");
+        return XRL_EUNSUPPORTED;
+    }
     try {
         XRL_CUDA(cudaSetDevice(t->ctx->device));
         const int64_t nl = t->p1 - t->p0;
-        if (t->part_world == 1) {
-            for (int v = 0; v < nvec; v += 3)
-                mvm_triple(t, nr, (const float2*)x + (size_t)v * t->n, (float2*)y + (size_t)v * t->n, flags);
-            return XRL_OK;
-        }
-        if (t->ctx->world == 1) {
-            set_error("xrl_mvm: virtual partition (part_world > 1 on a single-rank context) needs xrl_mvm_gathered");
-            return XRL_EUNSUPPORTED;
-        }
-        if (t->xfull.n < (size_t)3 * t->n) t->xfull.alloc((size_t)3 * t->n);
         for (int v = 0; v < nvec; v += 3) {
-            // gather the owned slices of the 3 components into the full vectors (NCCL over NVLink)
-            xrl_status s = gather_slices(t, (const float2*)x + (size_t)v * nl, t->xfull.p);
+            xrl_status s = mvm_triple(t, nr, (const float2*)x + (size_t)v * nl, (float2*)y + (size_t)v * nl, flags);
             if (s) return s;
-            mvm_triple(t, nr, t->xfull.p, (float2*)y + (size_t)v * nl, flags);
         }
         return XRL_OK;
     } catch (const CudaError& e) {
@@ -1271,22 +1521,124 @@ xrl_status xrl_mvm(xrl_tree t, xrl_near nr, const void* x, void* y, int32_t nvec
     }
 }
 
-xrl_status xrl_mvm_gathered(xrl_tree t, xrl_near nr, const void* x_full, void* y, int32_t nvec, uint32_t flags)
+xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* nears, const void* const* x,
+                          void* const* y, int32_t nvec, uint32_t flags, double* rank_ms, double* exch_ms)
 {
-    if (!t || !nr || !x_full || !y) { set_error("xrl_mvm_gathered: null argument"); return XRL_EINVAL; }
-    if (nr->tree != t) { set_error("xrl_mvm_gathered: near handle built from another tree"); return XRL_EPROVENANCE; }
-    if (nvec < 3 || nvec % 3) { set_error("xrl_mvm_gathered: nvec=%d must be a positive multiple of 3", nvec); return XRL_EDIM; }
-    if (x_full == y) { set_error("xrl_mvm_gathered: x and y alias"); return XRL_EINVAL; }
-    if (flags > XRL_MVM_FAR_ONLY) { set_error("xrl_mvm_gathered: bad flags"); return XRL_EINVAL; }
+    if (k < 1 || !trees || !nears || !x || !y) { set_error("xrl_mvm_vranks: bad argument"); return XRL_EINVAL; }
+    if (nvec < 3 || nvec % 3) { set_error("xrl_mvm_vranks: nvec=%d must be a positive multiple of 3", nvec); return XRL_EDIM; }
+    if (flags > XRL_MVM_FAR_ONLY) { set_error("xrl_mvm_vranks: bad flags"); return XRL_EINVAL; }
+    for (int r = 0; r < k; ++r) {
+        if (!trees[r] || !nears[r] || !x[r] || !y[r]) { set_error("xrl_mvm_vranks: null handle or vector %d", r); return XRL_EINVAL; }
+        if (nears[r]->tree != trees[r]) { set_error("xrl_mvm_vranks: near %d built from another tree", r); return XRL_EPROVENANCE; }
+        if (trees[r]->ctx != trees[0]->ctx || trees[r]->ctx->world != 1) {
+            set_error("xrl_mvm_vranks: all trees must share one single-rank context");
+            return XRL_EPROVENANCE;
+        }
+        if (trees[r]->part_world != (k > 1 ? k : 1) || trees[r]->part_rank != (k > 1 ? r : 0) || trees[r]->n != trees[0]->n) {
+            set_error("xrl_mvm_vranks: tree %d is not rank %d of a %d-way partition of one mesh", r, r, k);
+            return XRL_EINVAL;
+        }
+        if (x[r] == y[r] || (((uintptr_t)x[r] | (uintptr_t)y[r]) & 15)) {
+            set_error("xrl_mvm_vranks: vectors of rank %d alias or are not 16-byte aligned", r);
+            return XRL_EINVAL;
+        }
+    }
+    xrl_ctx ctx = trees[0]->ctx;
     try {
-        XRL_CUDA(cudaSetDevice(t->ctx->device));
-        const int64_t nl = t->p1 - t->p0;
-        for (int v = 0; v < nvec; v += 3)
-            mvm_triple(t, nr, (const float2*)x_full + (size_t)v * t->n, (float2*)y + (size_t)v * nl, flags);
-        return XRL_OK;
+        XRL_CUDA(cudaSetDevice(ctx->device));
+        if (rank_ms) for (int r = 0; r < k; ++r) rank_ms[r] = 0;
+        if (exch_ms) *exch_ms = 0;
+        // serial schedule per rank (its kernels in order on the context stream) so each rank's device time is
+        // measured alone, as if it had the GPU to itself; the exchanges are device copies on the same stream
+        const int sched_saved = ctx->sched;
+        ctx->sched = XRL_SCHED_SERIAL;
+        VTimer tm{ctx, rank_ms != nullptr || exch_ms != nullptr};
+        std::vector<double> ms(k + 1, 0.0);
+        cudaStream_t st = ctx->stream;
+        xrl_status s = XRL_OK;
+        for (int v = 0; v < nvec && !s; v += 3) {
+            std::vector<Mvm> Ms;
+            for (int r = 0; r < k; ++r) {
+                const int64_t nl = trees[r]->p1 - trees[r]->p0;
+                Ms.push_back(mvm_make(trees[r], nears[r], (float2*)y[r] + (size_t)v * nl, flags, XRL_SCHED_SERIAL));
+            }
+            const bool dist = k > 1;
+            for (int r = 0; r < k; ++r) {
+                const int64_t nl = trees[r]->p1 - trees[r]->p0;
+                tm.begin();
+                mvm_begin(Ms[r], (const float2*)x[r] + (size_t)v * nl);
+                if (dist) halo_pack(Ms[r]);
+                tm.end(r);
+            }
+            if (dist) {
+                tm.begin();
+                s = vcopy(k, Ms, [](const Mvm& M) -> const std::vector<int64_t>& { return M.nr->halo_soff; },
+                          [](const Mvm& M) -> const std::vector<int64_t>& { return M.nr->halo_roff; },
+                          [](const Mvm& M) -> const float* { return M.nr->halo_sbuf.p; },
+                          [](const Mvm& M) -> float* { return M.nr->halo_rbuf.p; }, 8, st);
+                tm.end(k);
+                if (s) break;
+            }
+            for (int r = 0; r < k; ++r) {
+                tm.begin();
+                if (dist) halo_unpack(Ms[r]);
+                mvm_up(Ms[r]);
+                if (dist && Ms[r].chain) mu_pack(Ms[r]);
+                tm.end(r);
+            }
+            if (dist && Ms[0].chain) {
+                // all-reduce of the shared boxes: sum into rank 0's buffer, copy back to every rank
+                tm.begin();
+                const size_t cnt = trees[0]->shared_boxes.size() * (size_t)kMuStride;
+                for (int r = 1; r < k; ++r) {
+                    if (trees[r]->shared_boxes != trees[0]->shared_boxes) { set_error("xrl_mvm_vranks: shared boxes differ"); s = XRL_EINVAL; break; }
+                    add_into((int64_t)cnt, trees[r]->sh_buf.p, trees[0]->sh_buf.p, st);
+                }
+                for (int r = 1; r < k && !s; ++r)
+                    if (cnt) XRL_CUDA(cudaMemcpyAsync(trees[r]->sh_buf.p, trees[0]->sh_buf.p, 4 * cnt, cudaMemcpyDeviceToDevice, st));
+                tm.end(k);
+                if (s) break;
+                for (int r = 0; r < k; ++r) {
+                    tm.begin();
+                    mu_shared_unpack_let_pack(Ms[r]);
+                    tm.end(r);
+                }
+                tm.begin();
+                s = vcopy(k, Ms, [](const Mvm& M) -> const std::vector<int64_t>& { return M.t->let_soff; },
+                          [](const Mvm& M) -> const std::vector<int64_t>& { return M.t->let_roff; },
+                          [](const Mvm& M) -> const float* { return M.t->let_sbuf.p; },
+                          [](const Mvm& M) -> float* { return M.t->let_rbuf.p; }, kMuStride, st);
+                tm.end(k);
+                if (s) break;
+            }
+            for (int r = 0; r < k; ++r) {
+                tm.begin();
+                if (dist && Ms[r].chain) let_unpack(Ms[r]);
+                mvm_down(Ms[r]);
+                tm.end(r);
+            }
+        }
+        tm.collect(ms.data());
+        ctx->sched = sched_saved;
+        if (rank_ms) for (int r = 0; r < k; ++r) rank_ms[r] = ms[r];
+        if (exch_ms) *exch_ms = ms[k];
+        return s;
     } catch (const CudaError& e) {
         return e.code;
     }
+}
+
+xrl_status xrl_exchange_info(xrl_tree t, xrl_near nr, int64_t* halo_send, int64_t* halo_recv, int64_t* let_send,
+                             int64_t* let_recv, int64_t* shared)
+{
+    if (!t) { set_error("xrl_exchange_info: null tree"); return XRL_EINVAL; }
+    const bool dist = t->part_world > 1;
+    if (halo_send) *halo_send = dist && nr ? nr->halo_soff.back() : 0;
+    if (halo_recv) *halo_recv = dist && nr ? nr->halo_roff.back() : 0;
+    if (let_send) *let_send = dist ? t->let_soff.back() : 0;
+    if (let_recv) *let_recv = dist ? t->let_roff.back() : 0;
+    if (shared) *shared = dist ? (int64_t)t->shared_boxes.size() : 0;
+    return XRL_OK;
 }
 
 xrl_status xrl_to_library_order(xrl_tree t, const void* x_user, void* x_lib, int32_t nvec)

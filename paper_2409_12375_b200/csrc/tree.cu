@@ -887,8 +887,9 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         XRL_CUDA(cudaStreamSynchronize(st));
         // M2M and L2L as tensor-core translation tiles (the M2L kernel, operators 316.. in the image table):
         // per level, (target, source, octant operator) pairs sorted by (operator, target), tiles of <= 21
-        // pairs of one operator, blocks of <= 16 tiles.  M2M: parent <- child (all boxes, every rank);
-        // L2L: child <- parent (relevant boxes of levels >= 3).
+        // pairs of one operator, blocks of <= 16 tiles.  M2M: parent <- child for the relevant children
+        // (a rank's P2M covers its own leaves only, so a box straddling a cut gets a partial multipole,
+        // summed over the ranks per MVM, exchange.cu); L2L: child <- parent (relevant boxes of levels >= 3).
         std::vector<int32_t> hx(nbox), hy(nbox), hz(nbox), hpar(nbox), hch(nbox), hnc(nbox);
         XRL_CUDA(cudaMemcpyAsync(hx.data(), T->bix.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
         XRL_CUDA(cudaMemcpyAsync(hy.data(), T->biy.p, 4 * nbox, cudaMemcpyDeviceToHost, st));
@@ -923,7 +924,8 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         for (int l = nlev - 2; l >= 2; --l) {  // parents at level l
             std::vector<std::array<int, 3>> pr;
             for (int b = T->lvl_start[l]; b < T->lvl_start[l + 1]; ++b)
-                for (int c = hch[b]; hch[b] >= 0 && c < hch[b] + hnc[b]; ++c) pr.push_back({kOpM2M + oct(c), b, c});
+                for (int c = hch[b]; hch[b] >= 0 && c < hch[b] + hnc[b]; ++c)
+                    if (T->rel[c]) pr.push_back({kOpM2M + oct(c), b, c});  // (partial) multipoles of own subtrees
             T->m2m_lvl[l] = emit_level(pr);
         }
         for (int l = 3; l < nlev; ++l) {  // children at level l
@@ -1035,6 +1037,8 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         if (!wp.empty()) XRL_CUDA(cudaMemcpyAsync(T->w_targets.p, wp.data(), sizeof(int2) * wp.size(), cudaMemcpyHostToDevice, st));
         XRL_CUDA(cudaStreamSynchronize(st));
     }
+    // multi-rank exchange plan: shared boxes, LET lists, remote leaves for the halo (exchange.cu)
+    if (T->part_world > 1) build_let_plan(T.get(), hpb, hpe, hchild, st);
     // MVM scratch
     T->mu.alloc((size_t)nbox * kMuStride);
     T->ell.alloc((size_t)nbox * kEllStride);

@@ -79,6 +79,8 @@ constexpr int kMuStride = 768;       // floats per box multipole mu[r][k] (r-maj
 constexpr int kOpM2M = 316, kOpL2L = 324, kNOpImg = 332;  // tensor-core operator images: M2L 0..315, M2M, L2L
 constexpr int kEllStride = 768;      // floats per box local expansion ell[r][k] (r-major, k padded to 128)
 constexpr int kEllKStride = 968;     // floats per leaf local expansion ellk[k][8] (k-major, for the L2P)
+constexpr int kNearGrpSeg = 32;      // near SpMV: segments (rows) per group = CTA threads / 8
+constexpr int kNearCap = 512;        // near SpMV: max column union per group (a warp's shared-memory stage)
 
 }  // namespace xrl
 
@@ -166,7 +168,14 @@ struct xrl_tree_s {
     int32_t n_own_leaves = 0;
     std::vector<int32_t> l2l_start;          // per-level offsets into l2l_boxes
     xrl::DBuf<int32_t> l2l_boxes;
-    xrl::DBuf<float2> xfull;                 // gathered x (multi-rank MVM)
+    // multi-rank exchange plan (exchange.cu; part_world > 1)
+    std::vector<int32_t> shared_boxes;       // boxes straddling a cut (partial multipoles, all-reduced)
+    xrl::DBuf<int32_t> sh_idx;
+    xrl::DBuf<float> sh_buf;                 // [n_shared][kMuStride]
+    std::vector<int64_t> let_soff, let_roff; // [world+1] box offsets per peer in the send / receive lists
+    xrl::DBuf<int32_t> let_sidx, let_ridx;   // own boxes peers need / peers' boxes this rank needs
+    xrl::DBuf<float> let_sbuf, let_rbuf;     // [n][kMuStride]
+    std::vector<std::vector<int32_t>> halo_leaves;  // [rank] remote leaves its P2P / P2L read (all ranks)
     // host copies of the mesh (original order) for the topology build
     std::vector<double> h_vert;              // [nv][3]
     std::vector<int32_t> h_tri;              // [n][stride] panel vertex ids (mesh order; -1: no 4th vertex)
@@ -187,8 +196,22 @@ struct xrl_near_s {
     xrl::DBuf<int64_t> row_ptr;
     xrl::DBuf<int32_t> col;
     xrl::DBuf<float> val;       // N_kl (FP32)
-    xrl::DBuf<int2> cv;         // (col, N_kl bits) interleaved for the SpMV
     xrl::DBuf<double> val64;    // P_kl (FP64, before subtraction)
+    // row-group format of the owned rows for the SpMV (near.cu build_near_groups)
+    int32_t n_groups = 0;
+    int64_t n_entries = 0, n_union = 0;
+    xrl::DBuf<int32_t> grp_seg;   // [n_groups+1] first segment of each group
+    xrl::DBuf<int64_t> grp_u;     // [n_groups+1] offset of each group's column union in ucol
+    xrl::DBuf<int32_t> seg_row;   // [nseg] local row (row - p0) of each segment
+    xrl::DBuf<int64_t> seg_off;   // [nseg+1] padded entry offsets (multiples of 4)
+    xrl::DBuf<int32_t> ucol;      // [n_union] sorted column unions, group after group
+    xrl::DBuf<float> eval;        // [n_entries] N_kl (FP32), 0 in the padding
+    xrl::DBuf<uint16_t> eidx;     // [n_entries] position of the column in the group's union
+    xrl::DBuf<uint8_t> cseg;      // [n_entries / 4] segment (within its group) of each 4-entry chunk
+    // halo of x (exchange.cu; part_world > 1): panels peers read from this rank / this rank reads
+    std::vector<int64_t> halo_soff, halo_roff;  // [world+1] panel offsets per peer
+    xrl::DBuf<int32_t> halo_sidx, halo_ridx;
+    xrl::DBuf<float> halo_sbuf, halo_rbuf;      // [n][8] packed charge records
 };
 
 struct xrl_topo_s {
@@ -254,6 +277,15 @@ void upload_constants(xrl_ctx ctx);
 void ctx_release(xrl_ctx ctx);     // delete if dead and unreferenced
 xrl_status comm_init(xrl_ctx ctx, const void* unique_id);
 void comm_destroy(xrl_ctx ctx);
-xrl_status gather_slices(xrl_tree t, const float2* x_local, float2* x_full);
+// multi-rank exchanges (exchange.cu plans and pack kernels, comm.cu NCCL transport)
+void build_let_plan(xrl_tree T, const std::vector<int32_t>& hpb, const std::vector<int32_t>& hpe,
+                    const std::vector<int32_t>& hchild, cudaStream_t st);
+void build_halo_plan(xrl_tree t, xrl_near N, cudaStream_t st);
+void gather_records(int64_t cnt, int w, const int32_t* idx, const float* src, float* dst, cudaStream_t st);
+void scatter_records(int64_t cnt, int w, const int32_t* idx, const float* src, float* dst, cudaStream_t st);
+void add_into(int64_t cnt, const float* a, float* acc, cudaStream_t st);
+xrl_status nccl_exchange(xrl_ctx ctx, const float* sbuf, const std::vector<int64_t>& soff, float* rbuf,
+                         const std::vector<int64_t>& roff, int rec_floats, cudaStream_t st);
+xrl_status nccl_allreduce_sum(xrl_ctx ctx, float* buf, size_t count, cudaStream_t st);
 void tree_release(xrl_tree t);
 }  // namespace xrl

@@ -24,12 +24,12 @@ EXPORTS = [
     "xrl_last_error", "xrl_version", "xrl_ctx_create", "xrl_ctx_sync", "xrl_ctx_destroy",
     "xrl_tree_build", "xrl_tree_build_poly", "xrl_tree_destroy", "xrl_tree_info", "xrl_tree_perm", "xrl_to_library_order",
     "xrl_from_library_order", "xrl_tree_export", "xrl_near_assemble", "xrl_near_destroy",
-    "xrl_near_export", "xrl_near_export_rows", "xrl_mvm", "xrl_mvm_host", "xrl_mvm_host_batch", "xrl_timing_enable", "xrl_timing_count",
+    "xrl_near_export", "xrl_near_export_rows", "xrl_near_info", "xrl_mvm", "xrl_mvm_host", "xrl_mvm_host_batch", "xrl_timing_enable", "xrl_timing_count",
     "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_ctx_set_fuse", "xrl_extract",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
     "xrl_precond_build_exact", "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
-    "xrl_port_currents", "xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_gathered",
+    "xrl_port_currents", "xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_vranks", "xrl_exchange_info", "xrl_plan_exchange",
 ]
 
 
@@ -115,6 +115,7 @@ def lib():
         L.xrl_near_destroy.restype = None
         L.xrl_near_export.argtypes = [P, P, P, P, P, P]
         L.xrl_near_export_rows.argtypes = [P, i64, P, P, P, P, P]
+        L.xrl_near_info.argtypes = [P, P, P, P, P]
         L.xrl_mvm.argtypes = [P, P, P, P, i32, u32]
         L.xrl_mvm_host.argtypes = [P, P, P, P, i32, u32]
         L.xrl_mvm_host_batch.argtypes = [P, P, P, P, i32, i32, u32]
@@ -154,8 +155,11 @@ def lib():
         L.xrl_port_currents.argtypes = [P, P, i32, P]
         L.xrl_partition_cuts.argtypes = [i64, P, i32, P]
         L.xrl_nccl_unique_id.argtypes = [P]
-        L.xrl_mvm_gathered.argtypes = [P, P, P, P, i32, u32]
-        for name in ("xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_gathered"):
+        L.xrl_mvm_vranks.argtypes = [i32, P, P, P, P, i32, u32, P, P]
+        L.xrl_exchange_info.argtypes = [P, P, P, P, P, P, P]
+        L.xrl_plan_exchange.argtypes = [i32] + [P] * 11 + [i64, P, P, i32, P, i32] + [P] * 10
+        for name in ("xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_vranks", "xrl_exchange_info",
+                     "xrl_plan_exchange"):
             getattr(L, name).restype = ctypes.c_int32
         for name in ("xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_esi",
                      "xrl_operator_create", "xrl_operator_apply", "xrl_precond_build", "xrl_precond_build_exact",
@@ -385,6 +389,11 @@ class Near:
         k = nnz.value
         return ptr, col[:k], v32[:k], v64[:k]
 
+    def info(self) -> dict:
+        v = [ctypes.c_int64() for _ in range(4)]
+        check(lib().xrl_near_info(self.h, *[ctypes.byref(a) for a in v]))
+        return dict(zip(("nnz", "n_groups", "n_entries", "n_union"), [int(a.value) for a in v]))
+
     def export_rows(self, rows):
         """Selected library-order rows: (ptr, col, v32, v64) over those rows only."""
         rows = np.ascontiguousarray(rows, dtype=np.int64)
@@ -421,14 +430,68 @@ def mvm(tree: Tree, near: Near, x, y=None, flags=XRL_MVM_FULL):
     return y
 
 
-def mvm_gathered(tree: Tree, near: Near, x_full, y=None, flags=XRL_MVM_FULL):
-    """xrl_mvm_gathered: full x [nvec][n] -> this rank's slice [nvec][n_local]."""
+def mvm_vranks(trees, nears, xs, ys=None, flags=XRL_MVM_FULL, timing=False):
+    """xrl_mvm_vranks: the sharded MVM of k virtual ranks on one GPU.  trees[r] / nears[r]: rank r of a
+    k-way partition (Tree(..., part_rank=r, part_world=k)) on one single-rank context; xs[r]: rank r's
+    slice [nvec][n_local(r)] (library order).  Returns ys (and, with timing=True, (rank_ms [k],
+    exchange_ms))."""
     import torch
-    _dev_vec(x_full, tree.n, "x_full")
-    if y is None:
-        y = torch.empty((x_full.shape[0], tree.n_local), dtype=torch.complex64, device=x_full.device)
-    check(lib().xrl_mvm_gathered(tree.h, near.h, _ptr(x_full), _ptr(y), x_full.shape[0], flags))
-    return y
+    k = len(trees)
+    if ys is None:
+        ys = [torch.empty_like(x) for x in xs]
+    for r in range(k):
+        _dev_vec(xs[r], trees[r].n_local, "x")
+        _dev_vec(ys[r], trees[r].n_local, "y")
+    th = (ctypes.c_void_p * k)(*[t.h.value for t in trees])
+    nh = (ctypes.c_void_p * k)(*[n.h.value for n in nears])
+    xp = (ctypes.c_void_p * k)(*[x.data_ptr() for x in xs])
+    yp = (ctypes.c_void_p * k)(*[y.data_ptr() for y in ys])
+    rms = np.zeros(k)
+    ems = ctypes.c_double()
+    check(lib().xrl_mvm_vranks(k, th, nh, xp, yp, xs[0].shape[0], flags, _ptr(rms) if timing else None,
+                               ctypes.byref(ems) if timing else None))
+    return (ys, rms, ems.value) if timing else ys
+
+
+def plan_exchange(tree: dict, near_ptr, near_col, cuts, rank) -> dict:
+    """xrl_plan_exchange (host, no GPU): rank `rank`'s exchange plan for a tree given as host arrays
+    (dict with pb, pe, child, v_ptr/v_src, x_ptr/x_src, w_ptr/w_src, u_ptr/u_src) and a near pattern."""
+    a = {k: np.ascontiguousarray(tree[k], dtype=np.int64 if k.endswith("_ptr") else np.int32)
+         for k in ("pb", "pe", "child", "v_ptr", "v_src", "x_ptr", "x_src", "w_ptr", "w_src", "u_ptr", "u_src")}
+    for k in ("v_src", "x_src", "w_src", "u_src"):
+        if a[k].size == 0:
+            a[k] = np.zeros(1, np.int32)
+    near_ptr = np.ascontiguousarray(near_ptr, dtype=np.int64)
+    near_col = np.ascontiguousarray(near_col, dtype=np.int32)
+    cuts = np.ascontiguousarray(cuts, dtype=np.int32)
+    world = cuts.size - 1
+    nbox = a["pb"].size
+    n = near_ptr.size - 1
+    nsh = ctypes.c_int64()
+    offs = {k: np.zeros(world + 1, np.int64) for k in ("let_roff", "let_soff", "halo_roff", "halo_soff")}
+
+    def call(sh, lr, ls, hr, hs):
+        check(lib().xrl_plan_exchange(nbox, *[_ptr(a[k]) for k in ("pb", "pe", "child", "v_ptr", "v_src", "x_ptr",
+                                                                     "x_src", "w_ptr", "w_src", "u_ptr", "u_src")],
+                                      n, _ptr(near_ptr), _ptr(near_col), world, _ptr(cuts), rank, ctypes.byref(nsh),
+                                      _ptr(sh), _ptr(offs["let_roff"]), _ptr(lr), _ptr(offs["let_soff"]), _ptr(ls),
+                                      _ptr(offs["halo_roff"]), _ptr(hr), _ptr(offs["halo_soff"]), _ptr(hs)))
+    call(None, None, None, None, None)
+    out = {"shared": np.zeros(max(nsh.value, 1), np.int32)}
+    for k in ("let_r", "let_s", "halo_r", "halo_s"):
+        out[k + "idx"] = np.zeros(max(int(offs[k + "off"][-1]), 1), np.int32)
+    call(out["shared"], out["let_ridx"], out["let_sidx"], out["halo_ridx"], out["halo_sidx"])
+    out["shared"] = out["shared"][:nsh.value]
+    for k in ("let_r", "let_s", "halo_r", "halo_s"):
+        out[k + "idx"] = out[k + "idx"][:int(offs[k + "off"][-1])]
+        out[k + "off"] = offs[k + "off"]
+    return out
+
+
+def exchange_info(tree, near=None) -> dict:
+    v = [ctypes.c_int64() for _ in range(5)]
+    check(lib().xrl_exchange_info(tree.h, near.h if near is not None else None, *[ctypes.byref(a) for a in v]))
+    return dict(zip(("halo_send", "halo_recv", "let_send", "let_recv", "shared"), [int(a.value) for a in v]))
 
 
 def mvm_host(tree: Tree, near: Near, x_host: np.ndarray, y_host: np.ndarray | None = None, flags=XRL_MVM_FULL):

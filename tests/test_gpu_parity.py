@@ -236,10 +236,12 @@ def test_full_mvm_sampled_rows(cfg, nrows, leaf):
     assert err <= TOL_FULL
 
 
-@pytest.mark.parametrize("cfg,world,leaf", [(1, 2, 64), (1, 3, 16), (2, 4, 64)])
-def test_virtual_partition_concat_equals_full(cfg, world, leaf):
-    """Sharded MVM on one GPU: rank r's restricted passes from the
-    gathered x give exactly its slice of the full MVM; slices tile [0, n)."""
+@pytest.mark.parametrize("cfg,world,leaf", [(1, 2, 64), (1, 3, 16), (2, 4, 64), (2, 8, 352), (3, 8, 352)])
+def test_virtual_ranks_equal_single_gpu(cfg, world, leaf):
+    """Sharded MVM on one GPU through xrl_mvm_vranks: k trees partitioned 0..k-1, each with
+    its own charges only; the halo of x, the shared-box multipole all-reduce and the LET exchange run as
+    device copies between the trees.  The concatenated rank slices equal the single-GPU MVM to 1e-6 (FP32
+    summation order) and the oracle on sampled rows; every exchange list is non-trivial for k > 1."""
     import torch
     from paper_2409_12375_b200 import xrl
     m = meshes.make_config(cfg)
@@ -247,18 +249,34 @@ def test_virtual_partition_concat_equals_full(cfg, world, leaf):
     x = meshes.make_x(cfg, m.n)
     xl = tree.to_library_order(torch.from_numpy(x).cuda())
     y_full = xrl.mvm(tree, near, xl).cpu().numpy()
-    parts, off = [], 0
+    trees, nears, xs, off = [], [], [], 0
     for r in range(world):
         tr = xrl.Tree(ctx, m.verts, m.tris, leaf_max=leaf, part_rank=r, part_world=world)
-        nr = xrl.Near(tr)
+        trees.append(tr)
+        nears.append(xrl.Near(tr))
         assert tr.offset == off and tr.n_local > 0
-        parts.append(xrl.mvm_gathered(tr, nr, xl).cpu().numpy())
+        xs.append(xl[:, off:off + tr.n_local].contiguous())
         off += tr.n_local
     assert off == m.n
-    y_cat = np.concatenate(parts, axis=1)
+    ys, rank_ms, exch_ms = xrl.mvm_vranks(trees, nears, xs, timing=True)
+    y_cat = torch.cat(ys, dim=1).cpu().numpy()
     err = oracle.rel_l2(y_cat, y_full)
-    print("virtual partition", cfg, world, err, [p.shape[1] for p in parts])
+    info = [xrl.exchange_info(t, n) for t, n in zip(trees, nears)]
+    print("virtual ranks", cfg, world, err, [t.n_local for t in trees], info, rank_ms, exch_ms)
     assert err < 1e-6
+    assert sum(i["halo_send"] for i in info) == sum(i["halo_recv"] for i in info) > 0
+    if m.n > 10000:
+        assert sum(i["let_send"] for i in info) == sum(i["let_recv"] for i in info) > 0
+        assert info[0]["shared"] > 0
+        rows = np.random.default_rng(7).choice(m.n, size=256, replace=False)
+        perm = tree.perm()
+        y_user = np.empty_like(y_cat)
+        y_user[:, perm] = y_cat
+        assert oracle.rel_l2(y_user[:, rows], oracle_rows(m, x, rows)) <= TOL_FULL
+    assert np.all(rank_ms > 0)
+    # the other flags go through the same exchanges
+    yn = torch.cat(xrl.mvm_vranks(trees, nears, xs, flags=1), dim=1).cpu().numpy()
+    assert oracle.rel_l2(yn, xrl.mvm(tree, near, xl, flags=1).cpu().numpy()) < 1e-6
 
 
 # ---------------------------------------------------------------- NEXT f4: hybrid meshes, Galerkin near rule
