@@ -190,10 +190,10 @@ void xrl_near_destroy(xrl_near near);
 xrl_status xrl_near_export(xrl_near near, int64_t* row_ptr, int32_t* col, float* val32,
                            double* val64, int64_t* nnz);
 /* Sizes of the near field (any pointer may be NULL): nnz of the CSR (all rows), and of the
- * row-group format the SpMV streams for this rank's rows: groups of <= 32
- * consecutive rows, padded entries (FP32 value + u16 position in the group's column
- * union; 6 B each) and the total length of the column unions (int32 each). */
-xrl_status xrl_near_info(xrl_near near, int64_t* nnz, int64_t* n_groups, int64_t* n_entries, int64_t* n_union);
+ * segment format the SpMV streams for this rank's rows: segments (runs of
+ * <= 256 entries of one row whose columns share their upper 16 bits) and padded entries
+ * (FP32 value + u16 lower column bits; 6 B each). */
+xrl_status xrl_near_info(xrl_near near, int64_t* nnz, int64_t* n_segments, int64_t* n_entries);
 /* Selected rows of the CSR (tests on full-size meshes): rows host int64 [nrows]
  * (library order); cnt host int64 [nrows] receives each row's length; col,
  * val32, val64 (any may be NULL) receive the rows concatenated in the given
@@ -395,6 +395,21 @@ xrl_status xrl_precond_build(xrl_op op, int32_t block_size, xrl_precond* out);
  * (synchronous).  XRL_EINVAL if cuSOLVER cannot be loaded or n_loops >= 2^31,
  * XRL_ESINGULAR on a zero pivot.  xrl_precond_export rejects this kind. */
 xrl_status xrl_precond_build_exact(xrl_op op, xrl_precond* out);
+/* Preconditioner of a given kind (Table IV's comparison):
+ *   XRL_PRECOND_DIAG_P (0): Eq. 10's Q = Z_s + M sum_t A_t P_d A_t^T M^T;
+ *   XRL_PRECOND_DIAG_L (1): the traditional diagonal-of-L preconditioner of
+ *     PAPER.md:120-122, Q_L = Z_s + j omega L_d mapped to loops,
+ *     Q_L = M [sum_t A_t diag(Z_s/A) A_t^T + alpha diag(L_ee)] M^T with
+ *     L_ee the diagonal of the edge-edge matrix sum_t A_t P A_t^T (each edge's
+ *     two panels: their P self terms and their mutual near entry).
+ * block_size 1..64: block-Jacobi (FP64 Gauss-Jordan per block, complex64
+ * storage); -1: the whole Q factorised (as xrl_precond_build_exact).
+ * Errors as xrl_precond_build / xrl_precond_build_exact, plus XRL_EINVAL for
+ * a bad kind and XRL_EGEOM if an edge's panel pair is missing from the near
+ * field. */
+#define XRL_PRECOND_DIAG_P 0
+#define XRL_PRECOND_DIAG_L 1
+xrl_status xrl_precond_build_kind(xrl_op op, int32_t kind, int32_t block_size, xrl_precond* out);
 /* z = blockdiag(Q)^-1 v (exact kind: Q^-1 v); device complex64 [nrhs][n_loops]. */
 xrl_status xrl_precond_apply(xrl_precond pc, const void* v, void* z, int32_t nrhs);
 /* Host export of the block partition and the inverse blocks (tests):

@@ -555,21 +555,14 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
 
 // ------------------------------------------------------------------ near-field SpMV
 // y += N x for the 6 real RHS (N: the near correction and the self terms) over the
-// row-group format of near.cu (build_near_groups).  One WARP per group (persistent over groups, no
-// CTA-wide barrier):
-//   * the group's column union (<= kNearCap records; ~385 for ~3,200 entries of 32 rows on config 4) is
-//     staged once in the warp's slice of shared memory, 24 B per record (the 6 RHS);
-//   * the group's padded entries are contiguous, so the 32 lanes stream them evenly -- lane l takes 4-entry
-//     chunks l, l + 32, ... (float4 values + ushort4 union positions + the chunk's u8 segment id: 6.25 B per
-//     entry, no per-entry column index, no per-entry L2 gather), whatever the row lengths;
-//   * per warp step the 32 chunk partials are combined by a segmented shuffle scan over the (sorted)
-//     segment ids and each run's tail lane adds it to the warp's per-segment accumulator in shared memory;
-//   * finally one lane per segment adds its row total into y with vector L2 reductions (a row cut into
-//     segments adds from several groups; the L2P / M2P add concurrently).
-constexpr int kNearWarps = 8;  // warps per CTA
-constexpr int kNearSmem = kNearWarps * (kNearCap * 24 + kNearGrpSeg * 6 * 4);
+// segment format of near.cu (build_near_segments): 8 lanes per segment, 4 segments per warp.  A lane streams
+// its 4-entry chunks (chunks l8, l8 + 8, ...) as one float4 of values + one ushort4 of column offsets (6 B per
+// entry instead of 8 for int32 column + value), keeps the next chunk's loads in flight behind the current
+// chunk's 4 gathers of 32-byte charge records (L1-cached: neighbouring rows share their near columns), and
+// the 8 lanes reduce with shuffles; the segment total is added into y with vector L2 reductions (a row with
+// several segments adds several times; the L2P / M2P add concurrently).
 
-// 32-byte read-only load through L1
+// 32-byte read-only load through L1 (the charge records are re-read by neighbouring rows)
 __device__ __forceinline__ void ldg256_l1(const float* p, float* v)
 {
     asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -583,130 +576,113 @@ __device__ __forceinline__ void red_add2(float2* p, float a, float b)
     asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
-// streaming loads (entries are read once per MVM: no L1 allocation)
-__device__ __forceinline__ float4 ldg_stream4(const float* p)
+// streaming loads of the near entries: read once per MVM, so no L1 allocation and L2 evict-first (the
+// 1.2 GB stream must not evict the 61 MB of charge records the gathers re-read from L2)
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ldg_stream4(const float* p, uint64_t pol)
 {
     float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
     return v;
 }
-__device__ __forceinline__ uint2 ldg_stream_u64(const uint16_t* p)
+__device__ __forceinline__ uint2 ldg_stream_u64(const uint16_t* p, uint64_t pol)
 {
     uint2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
     return v;
 }
-
-__device__ __forceinline__ void near_fma(const float2 (*X)[3], int j, float v, float* a)
+// 32-byte charge-record gather through L1, L2 evict-last
+__device__ __forceinline__ void ldg256_l1_keep(const float* p, float* v, uint64_t pol)
 {
-    const float2 q0 = X[j][0], q1 = X[j][1], q2 = X[j][2];
-    a[0] = fmaf(v, q0.x, a[0]); a[1] = fmaf(v, q0.y, a[1]);
-    a[2] = fmaf(v, q1.x, a[2]); a[3] = fmaf(v, q1.y, a[3]);
-    a[4] = fmaf(v, q2.x, a[4]); a[5] = fmaf(v, q2.y, a[5]);
+    asm volatile("ld.global.nc.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p), "l"(pol));
 }
 
-constexpr int kNearUnroll = 6;                  // chunks in flight per lane
-constexpr int kNearRec = (kNearCap + 31) / 32;  // union records per lane and group
-
-__global__ void __launch_bounds__(kNearWarps * 32, 2) k_near_blk(
-    int ngroups, const int32_t* __restrict__ grp_seg, const int64_t* __restrict__ grp_u,
-    const int32_t* __restrict__ seg_row, const int64_t* __restrict__ seg_off, const float* __restrict__ eval,
-    const uint16_t* __restrict__ eidx, const uint8_t* __restrict__ cseg, const int32_t* __restrict__ ucol,
-    const float* __restrict__ xq, int64_t nl, float2* __restrict__ y)
+// Persistent 8-lane teams: team t takes segments t, t + T, ...; a segment's header is loaded one segment
+// ahead and the first chunk of the next segment is loaded during the current segment's last chunk, so the
+// (header -> chunk -> gather) chain of one segment overlaps the previous one (segments are short: ~75
+// entries, 2-3 chunks per lane).
+__global__ void __launch_bounds__(256, 4) k_near_seg(int64_t nseg, const int32_t* __restrict__ seg_row,
+                                                    const int32_t* __restrict__ seg_base,
+                                                    const int64_t* __restrict__ seg_off, const float* __restrict__ eval,
+                                                    const uint16_t* __restrict__ eoff, const float* __restrict__ xq,
+                                                    int64_t nl, float2* __restrict__ y)
 {
-    extern __shared__ __align__(16) float near_sm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float2(*X)[3] = reinterpret_cast<float2(*)[3]>(near_sm + warp * kNearCap * 6);
-    float(*acc)[6] = reinterpret_cast<float(*)[6]>(near_sm + kNearWarps * kNearCap * 6 + warp * kNearGrpSeg * 6);
-    const int stride = gridDim.x * kNearWarps;
-    // the union columns of a group, lane-strided into registers (-1: none)
-    auto load_cols = [&](int g, int (&c)[kNearRec]) {
-        int64_t u0 = 0;
-        int nu = 0;
-        if (g < ngroups) { u0 = __ldg(grp_u + g); nu = (int)(__ldg(grp_u + g + 1) - u0); }
-#pragma unroll
-        for (int k = 0; k < kNearRec; ++k) c[k] = 32 * k + lane < nu ? __ldg(ucol + u0 + 32 * k + lane) : -1;
-    };
-    int col[kNearRec];
-    int g = blockIdx.x * kNearWarps + warp;
-    load_cols(g, col);
-    for (; g < ngroups; g += stride) {
-        // stage this group's union records (their columns were loaded one group ahead)
-#pragma unroll
-        for (int k0 = 0; k0 < kNearRec; k0 += 4) {
+    const int64_t team = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+    const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) >> 3;
+    const int l8 = threadIdx.x & 7;
+    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+    int64_t s = team;
+    int64_t b0 = 0, b1 = 0;  // entry range of segment s
+    int32_t base = 0;
+    if (s < nseg) { b0 = __ldg(seg_off + s); b1 = __ldg(seg_off + s + 1); base = __ldg(seg_base + s); }
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint2 o = make_uint2(0u, 0u);
+    if (s < nseg && b0 + 4 * l8 < b1) { v = ldg_stream4(eval + b0 + 4 * l8, pol_stream); o = ldg_stream_u64(eoff + b0 + 4 * l8, pol_stream); }
+    while (s < nseg) {
+        const int64_t sn = s + nteams;
+        int64_t n0 = 0, n1 = 0;
+        int32_t nbase = 0;
+        if (sn < nseg) { n0 = __ldg(seg_off + sn); n1 = __ldg(seg_off + sn + 1); nbase = __ldg(seg_base + sn); }
+        const int32_t row = __ldg(seg_row + s);
+        const float* xb = xq + 8 * (int64_t)base;
+        float a[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const int nit = (int)((b1 - b0 + 31) >> 5);  // chunk rounds of the team (uniform over its 8 lanes)
+        for (int it = 0; it < nit; ++it) {
+            const int64_t pos = b0 + 32 * it + 4 * l8;
+            if (pos >= b1) {  // a lane past its segment's end gathers record `base` with weight 0 (no branches)
+                v = make_float4(0.f, 0.f, 0.f, 0.f);
+                o = make_uint2(0u, 0u);
+            }
             float q[4][8];
-#pragma unroll
-            for (int k = k0; k < k0 + 4 && k < kNearRec; ++k)
-                if (col[k] >= 0) ldg256_l1(xq + 8 * (int64_t)col[k], q[k - k0]);
-#pragma unroll
-            for (int k = k0; k < k0 + 4 && k < kNearRec; ++k)
-                if (col[k] >= 0) {
-                    float2* d = X[32 * k + lane];
-                    d[0] = make_float2(q[k - k0][0], q[k - k0][1]);
-                    d[1] = make_float2(q[k - k0][2], q[k - k0][3]);
-                    d[2] = make_float2(q[k - k0][4], q[k - k0][5]);
-                }
-        }
-        load_cols(g + stride, col);  // the next group's columns, in flight during this group
-#pragma unroll
-        for (int r = 0; r < 6; ++r) acc[lane][r] = 0.f;
-        __syncwarp();
-        const int s0 = __ldg(grp_seg + g), ns = __ldg(grp_seg + g + 1) - s0;
-        const int64_t c0 = __ldg(seg_off + s0) >> 2, c1 = __ldg(seg_off + s0 + ns) >> 2;  // chunk range
-        for (int64_t cb = c0; cb < c1; cb += 32 * kNearUnroll) {
-            float4 v[kNearUnroll];
-            uint2 ix[kNearUnroll];
-            int sid[kNearUnroll];
-#pragma unroll
-            for (int u = 0; u < kNearUnroll; ++u) {
-                const int64_t c = cb + 32 * u + lane;
-                if (c < c1) {
-                    v[u] = ldg_stream4(eval + 4 * c);
-                    ix[u] = ldg_stream_u64(eidx + 4 * c);
-                    sid[u] = __ldg(cseg + c);
-                } else {
-                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    ix[u] = make_uint2(0u, 0u);
-                    sid[u] = 255;
-                }
+            ldg256_l1_keep(xb + 8 * (o.x & 0xffff), q[0], pol_keep);
+            ldg256_l1_keep(xb + 8 * (o.x >> 16), q[1], pol_keep);
+            ldg256_l1_keep(xb + 8 * (o.y & 0xffff), q[2], pol_keep);
+            ldg256_l1_keep(xb + 8 * (o.y >> 16), q[3], pol_keep);
+            const float w0 = v.x, w1 = v.y, w2 = v.z, w3 = v.w;
+            // the next chunk: this segment's, else the next segment's first
+            const int64_t np = it + 1 < nit ? pos + 32 : n0 + 4 * l8;
+            const int64_t ne = it + 1 < nit ? b1 : n1;
+            if ((it + 1 < nit || sn < nseg) && np < ne) {
+                v = ldg_stream4(eval + np, pol_stream);
+                o = ldg_stream_u64(eoff + np, pol_stream);
             }
 #pragma unroll
-            for (int u = 0; u < kNearUnroll; ++u) {
-                if (cb + 32 * u >= c1) break;  // warp-uniform
-                float a[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                near_fma(X, ix[u].x & 0xffff, v[u].x, a);
-                near_fma(X, ix[u].x >> 16, v[u].y, a);
-                near_fma(X, ix[u].y & 0xffff, v[u].z, a);
-                near_fma(X, ix[u].y >> 16, v[u].w, a);
-                // segmented inclusive scan over the lanes (segment ids ascend with the lane)
-                const int k = sid[u];
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int ku = __shfl_up_sync(0xffffffffu, k, o);
-                    float up[6];
-#pragma unroll
-                    for (int r = 0; r < 6; ++r) up[r] = __shfl_up_sync(0xffffffffu, a[r], o);
-                    if (lane >= o && ku == k) {
-#pragma unroll
-                        for (int r = 0; r < 6; ++r) a[r] += up[r];
-                    }
-                }
-                const int kn = __shfl_down_sync(0xffffffffu, k, 1);
-                if (k != 255 && (lane == 31 || kn != k)) {
-#pragma unroll
-                    for (int r = 0; r < 6; ++r) acc[k][r] += a[r];
-                }
-                __syncwarp();
+            for (int r = 0; r < 6; ++r) {
+                a[r] = fmaf(w0, q[0][r], a[r]);
+                a[r] = fmaf(w1, q[1][r], a[r]);
+                a[r] = fmaf(w2, q[2][r], a[r]);
+                a[r] = fmaf(w3, q[3][r], a[r]);
             }
         }
-        if (lane < ns) {
-            const int64_t row = __ldg(seg_row + s0 + lane);
-            red_add2(y + row, acc[lane][0], acc[lane][1]);
-            red_add2(y + nl + row, acc[lane][2], acc[lane][3]);
-            red_add2(y + 2 * nl + row, acc[lane][4], acc[lane][5]);
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+#pragma unroll
+            for (int d = 1; d < 8; d <<= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], d);
         }
-        __syncwarp();  // the stage and the accumulators are reused by the next group
+        if (l8 < 3) {
+            const float re = l8 == 0 ? a[0] : (l8 == 1 ? a[2] : a[4]);  // (no dynamic register indexing)
+            const float im = l8 == 0 ? a[1] : (l8 == 1 ? a[3] : a[5]);
+            red_add2(y + l8 * nl + row, re, im);
+        }
+        s = sn;
+        b0 = n0;
+        b1 = n1;
+        base = nbase;
     }
 }
 
@@ -1132,7 +1108,6 @@ void upload_constants(xrl_ctx ctx)
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2MSmem));
-    XRL_CUDA(cudaFuncSetAttribute(k_near_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, kNearSmem));
 }
 
 }  // namespace xrl
@@ -1237,11 +1212,10 @@ static void launch_near(Mvm& M)
         phase_begin(ctx, PH_NEAR, &ev, M.side);
         // the SpMV adds into y: in the near-only mode it starts from zero
         if (!M.do_far && M.nl > 0) XRL_CUDA(cudaMemsetAsync(M.y, 0, sizeof(float2) * 3 * (size_t)M.nl, M.side));
-        if (nr->n_groups > 0) {
-            const int grid = std::min((nr->n_groups + kNearWarps - 1) / kNearWarps, 2 * ctx->num_sms);
-            k_near_blk<<<grid, kNearWarps * 32, kNearSmem, M.side>>>(nr->n_groups, nr->grp_seg.p, nr->grp_u.p,
-                                                                      nr->seg_row.p, nr->seg_off.p, nr->eval.p,
-                                                                      nr->eidx.p, nr->cseg.p, nr->ucol.p, t->xq.p,
+        if (nr->n_segs > 0) {
+            const int grid = (int)std::min<int64_t>(nblk(8 * nr->n_segs, 256), 4 * ctx->num_sms);
+            k_near_seg<<<grid, 256, 0, M.side>>>(nr->n_segs, nr->seg_row.p, nr->seg_base.p,
+                                                                      nr->seg_off.p, nr->eval.p, nr->eoff.p, t->xq.p,
                                                                       M.nl, M.y);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;

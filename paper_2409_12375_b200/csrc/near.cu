@@ -233,186 +233,133 @@ __global__ void k_near_values(int64_t n, const int64_t* __restrict__ ptr, const 
 
 inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
-// ---------------------------------------------------------------- row-group format of the near SpMV
-// (SURVEY §8(a) a12).  Owned rows are cut into segments (a row, or a piece of <= kNearCap entries of a
-// long row) and consecutive segments into groups of <= kNearGrpSeg segments whose column union fits the
-// SpMV's shared-memory stage (<= kNearCap columns).  A group stores the sorted union of its columns once
-// (int32) and, per entry, the FP32 value and the u16 position of its column in that union; each
-// segment's entries are padded to a multiple of 4 (value 0, index repeated) so the SpMV reads them as
-// float4 / ushort4.  Neighbouring rows in Morton order share most near columns (config 4: a 32-row group
-// touches ~385 distinct columns for ~3,200 entries), so the kernel stages each union record once in
-// shared memory instead of gathering it per entry.
+// ---------------------------------------------------------------- segment format of the near SpMV
+// (SURVEY §8(a) a12).  The owned rows' entries are cut into segments: a run of one row's (ascending) columns
+// that share their upper 16 bits, at most kNearSegLen entries long.  A segment stores its row, the column
+// base (upper bits) and per entry the FP32 value and the u16 lower column bits: 6 B per entry instead of
+// 8 B for (int32 column, FP32 value).  Near columns of a Morton-ordered row are clustered, so a row has
+// ~1.4 segments on config 4; the length cap bounds the work of the 8 lanes a segment gets.  Each segment's
+// entries are padded to a multiple of 4 (value 0, offset repeated) for float4 / ushort4 loads and stored
+// lane-interleaved within blocks of 32 (k_seg_fill), so a warp's gathers touch consecutive columns.
 
-// keys (group << 32 | col) of every entry of every owned segment; one warp per segment
-__global__ void k_blk_keys(int nseg, const int32_t* __restrict__ seg_grp, const int64_t* __restrict__ seg_src,
-                           const int32_t* __restrict__ seg_cnt, const int64_t* __restrict__ seg_key0,
-                           const int32_t* __restrict__ col, uint64_t* __restrict__ key)
+__global__ void k_seg_count(int64_t r0, int64_t nr, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                            int64_t* __restrict__ cnt)
 {
-    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (s >= nseg) return;
-    const uint64_t g = (uint64_t)seg_grp[s] << 32;
-    const int64_t src = seg_src[s], dst = seg_key0[s];
-    for (int i = lane; i < seg_cnt[s]; i += 32) key[dst + i] = g | (uint32_t)col[src + i];
-}
-
-// unique flags of the sorted keys
-__global__ void k_blk_flag(int64_t m, const uint64_t* __restrict__ key, int64_t* __restrict__ flag)
-{
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j < m) flag[j] = (j == 0 || key[j] != key[j - 1]) ? 1 : 0;
-}
-
-// union columns and each group's union offset
-__global__ void k_blk_union(int64_t m, const uint64_t* __restrict__ key, const int64_t* __restrict__ pos,
-                            int32_t* __restrict__ ucol, int64_t* __restrict__ grp_u)
-{
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= m) return;
-    if (j == 0 || key[j] != key[j - 1]) {
-        ucol[pos[j]] = (int32_t)(key[j] & 0xffffffffu);
-        if (j == 0 || (key[j] >> 32) != (key[j - 1] >> 32)) grp_u[key[j] >> 32] = pos[j];
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    const int64_t r = r0 + i;
+    int64_t c = 0;
+    int len = 0, hi = -1;
+    for (int64_t j = ptr[r]; j < ptr[r + 1]; ++j) {
+        const int h = col[j] >> 16;
+        if (h != hi || len == kNearSegLen) { ++c; hi = h; len = 0; }
+        ++len;
     }
+    cnt[i] = c;
 }
 
-// padded entries: FP32 value and u16 union position of every entry, and the chunks' segment ids;
-// one warp per segment
-__global__ void k_blk_entries(int nseg, const int32_t* __restrict__ seg_grp, const int32_t* __restrict__ grp_seg,
-                              const int64_t* __restrict__ seg_src, const int32_t* __restrict__ seg_cnt,
-                              const int64_t* __restrict__ seg_off, const int64_t* __restrict__ grp_u,
-                              const int32_t* __restrict__ ucol, const int32_t* __restrict__ col,
-                              const float* __restrict__ val, float* __restrict__ eval, uint16_t* __restrict__ eidx,
-                              uint8_t* __restrict__ cseg)
+__global__ void k_seg_emit(int64_t r0, int64_t nr, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                           const int64_t* __restrict__ start, int32_t* __restrict__ seg_row, int32_t* __restrict__ seg_base,
+                           int64_t* __restrict__ seg_src, int32_t* __restrict__ seg_cnt, int64_t* __restrict__ seg_pad)
 {
-    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (s >= nseg) return;
-    const int g = seg_grp[s];
-    for (int64_t c = seg_off[s] / 4 + lane; c < seg_off[s + 1] / 4; c += 32) cseg[c] = (uint8_t)(s - grp_seg[g]);
-    const int64_t u0 = grp_u[g], nu = grp_u[g + 1] - u0, src = seg_src[s], dst = seg_off[s];
-    const int cnt = seg_cnt[s], padded = (int)(seg_off[s + 1] - dst);
-    const int32_t* U = ucol + u0;
-    for (int i = lane; i < padded; i += 32) {
-        const int ii = i < cnt ? i : cnt - 1;  // padding repeats the last index (keeps indices ascending)
-        const int32_t c = col[src + ii];
-        int64_t lo = 0, hi = nu - 1;  // U[lo] == c (c is in the union)
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (U[mid] < c) lo = mid + 1; else hi = mid;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nr) return;
+    const int64_t r = r0 + i;
+    int64_t s = start[i] - 1;
+    int len = 0, hi = -1;
+    auto close = [&]() {
+        if (s >= start[i]) { seg_cnt[s] = len; seg_pad[s] = (len + 3) & ~3; }
+    };
+    for (int64_t j = ptr[r]; j < ptr[r + 1]; ++j) {
+        const int h = col[j] >> 16;
+        if (h != hi || len == kNearSegLen) {
+            close();
+            ++s;
+            seg_row[s] = (int32_t)i;
+            seg_base[s] = h << 16;
+            seg_src[s] = j;
+            hi = h;
+            len = 0;
         }
-        eidx[dst + i] = (uint16_t)lo;
-        eval[dst + i] = i < cnt ? val[src + ii] : 0.f;
+        ++len;
     }
+    close();
 }
 
+// one warp per segment: FP32 values and u16 lower column bits; the padding repeats the last offset with
+// value 0 (keeps every gather inside the segment's column block)
+__global__ void k_seg_fill(int64_t nseg, const int32_t* __restrict__ seg_base, const int64_t* __restrict__ seg_src,
+                           const int32_t* __restrict__ seg_cnt, const int64_t* __restrict__ seg_off,
+                           const int32_t* __restrict__ col, const float* __restrict__ val, float* __restrict__ eval,
+                           uint16_t* __restrict__ eoff)
+{
+    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= nseg) return;
+    const int64_t src = seg_src[s], dst = seg_off[s], padded = seg_off[s + 1] - dst;
+    const int32_t base = seg_base[s];
+    const int cnt = seg_cnt[s];
+    for (int64_t i = lane; i < padded; i += 32) {
+        // within each block of 32 stored entries (8 chunks of 4: one per lane of the segment), chunk l holds the
+        // logical entries l, l + nc, l + 2 nc, l + 3 nc (nc = chunks in the block), so the 8 lanes' u-th
+        // gathers hit 8 consecutive columns (one or two cache lines) instead of a strided set
+        const int64_t blk = i & ~int64_t(31);
+        const int nc = (int)((padded - blk < 32 ? padded - blk : 32) >> 2);
+        const int q = (int)(i - blk), l = q >> 2, u = q & 3;
+        const int64_t e = blk + u * nc + l;
+        const int64_t j = src + (e < cnt ? e : cnt - 1);
+        eval[dst + i] = e < cnt ? val[j] : 0.f;
+        eoff[dst + i] = (uint16_t)(col[j] - base);
+    }
+}
 }  // namespace
 
-// Row-group format (above) for the owned rows [t->p0, t->p1) of the CSR in N; hp: host row pointer.
-// Groups start as runs of <= kNearGrpSeg segments; a group whose column union exceeds kNearCap (the
-// SpMV's shared-memory stage) is split in two and the unions are recomputed, until every union fits
-// (segments have <= kNearCap entries, so a one-segment group always fits).
-static void build_near_groups(xrl_tree t, xrl_near N, const std::vector<int64_t>& hp, cudaStream_t st)
+// Segment format (above) for the owned rows [t->p0, t->p1) of the CSR in N.
+template <typename T>
+static void exclusive_sum(const T* in, T* out, int64_t n, cudaStream_t st)
 {
-    std::vector<int32_t> seg_row, seg_cnt;
-    std::vector<int64_t> seg_src;
-    for (int64_t r = t->p0; r < t->p1; ++r)
-        for (int64_t e = hp[r]; e < hp[r + 1];) {
-            const int cnt = (int)std::min<int64_t>(kNearCap, hp[r + 1] - e);
-            seg_row.push_back((int32_t)(r - t->p0));
-            seg_cnt.push_back(cnt);
-            seg_src.push_back(e);
-            e += cnt;
-        }
-    const int nseg = (int)seg_row.size();
-    std::vector<int32_t> grp_seg;  // group boundaries (first segment of each group), refined below
-    for (int s = 0; s < nseg; s += kNearGrpSeg) grp_seg.push_back(s);
-    std::vector<int64_t> seg_off(nseg + 1, 0), seg_key0(nseg + 1, 0);
-    for (int s = 0; s < nseg; ++s) {
-        seg_off[s + 1] = seg_off[s] + ((seg_cnt[s] + 3) & ~3);
-        seg_key0[s + 1] = seg_key0[s] + seg_cnt[s];
-    }
-    const int64_t m = seg_key0[nseg], off = seg_off[nseg];
-    N->n_entries = off;
-    N->seg_row.alloc(std::max(1, nseg));
-    N->seg_off.alloc(nseg + 1);
-    N->eval.alloc(std::max<int64_t>(4, off));
-    N->eidx.alloc(std::max<int64_t>(4, off));
-    N->cseg.alloc(std::max<int64_t>(1, off / 4));
-    if (nseg == 0) {
-        N->n_groups = 0;
-        N->grp_seg.alloc(1);
-        N->grp_u.alloc(1);
-        XRL_CUDA(cudaMemsetAsync(N->grp_seg.p, 0, 4, st));
-        XRL_CUDA(cudaMemsetAsync(N->grp_u.p, 0, 8, st));
-        N->ucol.alloc(1);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, st);
+    DBuf<char> tmp(std::max<size_t>(tb, 1));
+    XRL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, st));
+}
+
+static void build_near_segments(xrl_tree t, xrl_near N, cudaStream_t st)
+{
+    const int64_t r0 = t->p0, nr = t->p1 - t->p0;
+    N->n_segs = 0;
+    N->n_entries = 0;
+    if (nr <= 0) {
+        N->seg_off.alloc(1);
+        XRL_CUDA(cudaMemsetAsync(N->seg_off.p, 0, 8, st));
         XRL_CUDA(cudaStreamSynchronize(st));
         return;
     }
-    DBuf<int32_t> d_sgrp(nseg), d_scnt(nseg);
-    DBuf<int64_t> d_ssrc(nseg), d_skey(nseg);
-    XRL_CUDA(cudaMemcpyAsync(N->seg_row.p, seg_row.data(), 4 * nseg, cudaMemcpyHostToDevice, st));
-    XRL_CUDA(cudaMemcpyAsync(N->seg_off.p, seg_off.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, st));
-    XRL_CUDA(cudaMemcpyAsync(d_scnt.p, seg_cnt.data(), 4 * nseg, cudaMemcpyHostToDevice, st));
-    XRL_CUDA(cudaMemcpyAsync(d_ssrc.p, seg_src.data(), 8 * nseg, cudaMemcpyHostToDevice, st));
-    XRL_CUDA(cudaMemcpyAsync(d_skey.p, seg_key0.data(), 8 * nseg, cudaMemcpyHostToDevice, st));
-    DBuf<uint64_t> key(m), key2(m);
-    DBuf<int64_t> flag(m), pos(m);
-    DBuf<char> tmp;
-    std::vector<int64_t> gu;
-    for (int iter = 0;; ++iter) {
-        const int ng = (int)grp_seg.size();
-        std::vector<int32_t> seg_grp(nseg);
-        for (int g = 0; g < ng; ++g)
-            for (int s = grp_seg[g]; s < (g + 1 < ng ? grp_seg[g + 1] : nseg); ++s) seg_grp[s] = g;
-        XRL_CUDA(cudaMemcpyAsync(d_sgrp.p, seg_grp.data(), 4 * nseg, cudaMemcpyHostToDevice, st));
-        int gbits = 1;
-        while ((1 << gbits) < ng + 1) ++gbits;
-        k_blk_keys<<<nblk((int64_t)nseg * 32, 256), 256, 0, st>>>(nseg, d_sgrp.p, d_ssrc.p, d_scnt.p, d_skey.p,
-                                                                   N->col.p, key.p);
-        XRL_LAUNCH_CHECK();
-        size_t tb = 0, tb2 = 0;
-        cub::DeviceRadixSort::SortKeys(nullptr, tb, key.p, key2.p, (int)m, 0, 32 + gbits, st);
-        cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag.p, pos.p, (int)m, st);
-        if (tmp.n < std::max(tb, tb2)) tmp.alloc(std::max(tb, tb2));
-        XRL_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, key.p, key2.p, (int)m, 0, 32 + gbits, st));
-        k_blk_flag<<<nblk(m, 256), 256, 0, st>>>(m, key2.p, flag.p);
-        XRL_LAUNCH_CHECK();
-        XRL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, flag.p, pos.p, (int)m, st));
-        int64_t last[2] = {0, 0};
-        XRL_CUDA(cudaMemcpyAsync(&last[0], pos.p + m - 1, 8, cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaMemcpyAsync(&last[1], flag.p + m - 1, 8, cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaStreamSynchronize(st));
-        const int64_t nu = last[0] + last[1];
-        N->ucol.alloc(nu);
-        N->grp_u.alloc(ng + 1);
-        k_blk_union<<<nblk(m, 256), 256, 0, st>>>(m, key2.p, pos.p, N->ucol.p, N->grp_u.p);
-        XRL_LAUNCH_CHECK();
-        XRL_CUDA(cudaMemcpyAsync(N->grp_u.p + ng, &nu, 8, cudaMemcpyHostToDevice, st));
-        gu.assign(ng + 1, 0);
-        XRL_CUDA(cudaMemcpyAsync(gu.data(), N->grp_u.p, 8 * (ng + 1), cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaStreamSynchronize(st));
-        // split the groups whose union does not fit the stage
-        std::vector<int32_t> refined;
-        bool split = false;
-        for (int g = 0; g < ng; ++g) {
-            const int a = grp_seg[g], b = g + 1 < ng ? grp_seg[g + 1] : nseg;
-            refined.push_back(a);
-            if (gu[g + 1] - gu[g] > kNearCap && b - a > 1) {
-                refined.push_back(a + (b - a) / 2);
-                split = true;
-            }
-        }
-        if (!split) {
-            N->n_groups = ng;
-            N->n_union = nu;
-            grp_seg.push_back(nseg);
-            N->grp_seg.alloc(ng + 1);
-            XRL_CUDA(cudaMemcpyAsync(N->grp_seg.p, grp_seg.data(), 4 * (ng + 1), cudaMemcpyHostToDevice, st));
-            break;
-        }
-        grp_seg.swap(refined);
-    }
-    k_blk_entries<<<nblk((int64_t)nseg * 32, 256), 256, 0, st>>>(nseg, d_sgrp.p, N->grp_seg.p, d_ssrc.p, d_scnt.p,
-                                                                  N->seg_off.p, N->grp_u.p, N->ucol.p, N->col.p,
-                                                                  N->val.p, N->eval.p, N->eidx.p, N->cseg.p);
+    DBuf<int64_t> cnt(nr + 1), start(nr + 1);
+    XRL_CUDA(cudaMemsetAsync(cnt.p + nr, 0, 8, st));
+    k_seg_count<<<nblk(nr, 256), 256, 0, st>>>(r0, nr, N->row_ptr.p, N->col.p, cnt.p);
+    XRL_LAUNCH_CHECK();
+    exclusive_sum(cnt.p, start.p, nr + 1, st);
+    int64_t nseg = 0;
+    XRL_CUDA(cudaMemcpyAsync(&nseg, start.p + nr, 8, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    N->n_segs = nseg;
+    N->seg_row.alloc(nseg);
+    N->seg_base.alloc(nseg);
+    N->seg_off.alloc(nseg + 1);
+    DBuf<int64_t> src(nseg), pad(nseg + 1);
+    DBuf<int32_t> scnt(nseg);
+    XRL_CUDA(cudaMemsetAsync(pad.p + nseg, 0, 8, st));
+    k_seg_emit<<<nblk(nr, 256), 256, 0, st>>>(r0, nr, N->row_ptr.p, N->col.p, start.p, N->seg_row.p, N->seg_base.p,
+                                              src.p, scnt.p, pad.p);
+    XRL_LAUNCH_CHECK();
+    exclusive_sum(pad.p, N->seg_off.p, nseg + 1, st);
+    XRL_CUDA(cudaMemcpyAsync(&N->n_entries, N->seg_off.p + nseg, 8, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    N->eval.alloc(std::max<int64_t>(4, N->n_entries));
+    N->eoff.alloc(std::max<int64_t>(4, N->n_entries));
+    k_seg_fill<<<nblk(nseg * 32, 256), 256, 0, st>>>(nseg, N->seg_base.p, src.p, scnt.p, N->seg_off.p, N->col.p,
+                                                    N->val.p, N->eval.p, N->eoff.p);
     XRL_LAUNCH_CHECK();
     XRL_CUDA(cudaStreamSynchronize(st));
 }
@@ -451,8 +398,8 @@ static xrl_status near_impl(xrl_tree t, double eta, int galerkin, xrl_near* out)
     k_near_values<<<nblk(n, 64), 64, 0, st>>>(n, N->row_ptr.p, N->col.p, t->cent.p, t->area.p, t->tverts.p,
                                               t->pvid.p, galerkin, N->val.p, N->val64.p);
     XRL_LAUNCH_CHECK();
-    // the row-group format the SpMV streams (owned rows)
-    build_near_groups(t, N.get(), hp, st);
+    // the segment format the SpMV streams (owned rows)
+    build_near_segments(t, N.get(), st);
     // the halo of x a partitioned tree's MVM exchanges (near columns + remote P2P / P2L leaves)
     if (t->part_world > 1) build_halo_plan(t, N.get(), st);
     ++t->refs;
@@ -510,13 +457,12 @@ xrl_status xrl_near_export(xrl_near nr, int64_t* row_ptr, int32_t* col, float* v
     }
 }
 
-xrl_status xrl_near_info(xrl_near nr, int64_t* nnz, int64_t* n_groups, int64_t* n_entries, int64_t* n_union)
+xrl_status xrl_near_info(xrl_near nr, int64_t* nnz, int64_t* n_segments, int64_t* n_entries)
 {
     if (!nr) { set_error("xrl_near_info: null handle"); return XRL_EINVAL; }
     if (nnz) *nnz = nr->nnz;
-    if (n_groups) *n_groups = nr->n_groups;
+    if (n_segments) *n_segments = nr->n_segs;
     if (n_entries) *n_entries = nr->n_entries;
-    if (n_union) *n_union = nr->n_union;
     return XRL_OK;
 }
 

@@ -178,17 +178,17 @@ __global__ void k_exact_scatter(int n, const cuDoubleComplex* __restrict__ w, co
 
 namespace xrl {
 
-xrl_status exact_build(xrl_precond pc)
+void assemble_q(xrl_op op, int qkind, std::vector<std::vector<int32_t>>& rc,
+                std::vector<std::vector<std::complex<double>>>& rv)
 {
-    Api& A = api();
-    if (!A.ok) { set_error("xrl_precond_build_exact: %s", A.err.c_str()); return XRL_EINVAL; }
-    xrl_op op = pc->op;
     xrl_topo T = op->topo;
     const int64_t n = op->tree->n, nl = T->n_loops;
-    if (nl >= ((int64_t)1 << 31)) { set_error("xrl_precond_build_exact: too many loops for 32-bit LU"); return XRL_EINVAL; }
+    // panel part: Q_ab = sum_k d_k (c_a(k) . c_b(k)) over panels k shared by loops a, b, with
+    //   diag-of-P (Eq. 10): d_k = Z_s,k / A_k + j alpha P_kk;  diag-of-L: d_k = Z_s,k / A_k (the ESI part only)
     std::vector<double2> d;
     precond_diag(op, d);
-    // ---- assemble Q (CSR, FP64 complex): Q_ab = sum_k d_k (c_a(k) . c_b(k)) over panels k shared by a, b
+    if (qkind == 1)
+        for (int64_t k = 0; k < n; ++k) d[k] = make_double2(op->zsa_h[2 * k], op->zsa_h[2 * k + 1]);
     const std::vector<int64_t>& cp = T->c_ptr_h;
     const std::vector<int32_t>& cc = T->c_col_h;
     const std::vector<double>& cv = T->c_val_h;
@@ -206,13 +206,42 @@ xrl_status exact_build(xrl_precond pc)
                 kq[f] = q;
             }
     }
-    std::vector<std::vector<int32_t>> rc(nl);
-    std::vector<std::vector<std::complex<double>>> rv(nl);
+    // branch part of diag-of-L: alpha L_ee M_ae M_be over the physical edges (branch e < n_edges is edge e)
+    std::vector<double> lee;
+    std::vector<int64_t> bp;   // edge -> loops (transpose of M restricted to edges)
+    std::vector<int32_t> bl;
+    std::vector<int8_t> bs;
+    if (qkind == 1) {
+        precond_ldiag(op, lee);
+        const int64_t ne = T->n_edges;
+        bp.assign(ne + 1, 0);
+        for (int64_t a = 0; a < nl; ++a)
+            for (int64_t q = T->m_ptr[a]; q < T->m_ptr[a + 1]; ++q)
+                if (T->m_idx[q] < ne) ++bp[T->m_idx[q] + 1];
+        for (int64_t e = 0; e < ne; ++e) bp[e + 1] += bp[e];
+        bl.resize(bp[ne]);
+        bs.resize(bp[ne]);
+        std::vector<int64_t> fill(bp.begin(), bp.end() - 1);
+        for (int64_t a = 0; a < nl; ++a)
+            for (int64_t q = T->m_ptr[a]; q < T->m_ptr[a + 1]; ++q)
+                if (T->m_idx[q] < ne) {
+                    const int64_t f = fill[T->m_idx[q]]++;
+                    bl[f] = (int32_t)a;
+                    bs[f] = T->m_val[q];
+                }
+    }
+    const double alpha = op->alpha_im;
+    rc.assign(nl, {});
+    rv.assign(nl, {});
 #pragma omp parallel
     {
         std::vector<std::complex<double>> acc(nl, 0.0);
         std::vector<char> mark(nl, 0);
         std::vector<int32_t> touched;
+        auto add = [&](int32_t b, std::complex<double> v) {
+            if (!mark[b]) { mark[b] = 1; touched.push_back(b); acc[b] = 0.0; }
+            acc[b] += v;
+        };
 #pragma omp for schedule(dynamic, 256)
         for (int64_t a = 0; a < nl; ++a) {
             touched.clear();
@@ -221,13 +250,17 @@ xrl_status exact_build(xrl_precond pc)
                 const double* ca = &cv[3 * q];
                 const std::complex<double> dk(d[k].x, d[k].y);
                 for (int64_t f = kp[k]; f < kp[k + 1]; ++f) {
-                    const int32_t b = kl[f];
                     const double* cb = &cv[3 * kq[f]];
-                    const double s = ca[0] * cb[0] + ca[1] * cb[1] + ca[2] * cb[2];
-                    if (!mark[b]) { mark[b] = 1; touched.push_back(b); acc[b] = 0.0; }
-                    acc[b] += dk * s;
+                    add(kl[f], dk * (ca[0] * cb[0] + ca[1] * cb[1] + ca[2] * cb[2]));
                 }
             }
+            if (qkind == 1)
+                for (int64_t q = T->m_ptr[a]; q < T->m_ptr[a + 1]; ++q) {
+                    const int32_t e = T->m_idx[q];
+                    if (e >= T->n_edges) continue;
+                    const std::complex<double> le(0.0, alpha * lee[e] * T->m_val[q]);
+                    for (int64_t f = bp[e]; f < bp[e + 1]; ++f) add(bl[f], le * (double)bs[f]);
+                }
             std::sort(touched.begin(), touched.end());
             rc[a] = touched;
             rv[a].resize(touched.size());
@@ -237,6 +270,19 @@ xrl_status exact_build(xrl_precond pc)
             }
         }
     }
+}
+
+xrl_status exact_build(xrl_precond pc)
+{
+    Api& A = api();
+    if (!A.ok) { set_error("xrl_precond_build_exact: %s", A.err.c_str()); return XRL_EINVAL; }
+    xrl_op op = pc->op;
+    xrl_topo T = op->topo;
+    const int64_t nl = T->n_loops;
+    if (nl >= ((int64_t)1 << 31)) { set_error("xrl_precond_build_exact: too many loops for 32-bit LU"); return XRL_EINVAL; }
+    std::vector<std::vector<int32_t>> rc;
+    std::vector<std::vector<std::complex<double>>> rv;
+    assemble_q(op, pc->qkind, rc, rv);
     const int N = (int)nl;
     std::vector<int> qp(N + 1, 0);
     for (int a = 0; a < N; ++a) qp[a + 1] = qp[a] + (int)rc[a].size();

@@ -127,11 +127,12 @@ constexpr int kBS = 64;
 
 // One CTA per block: assemble Q_BB = sum_k d_k c_a(k).c_b(k) (FP64 complex),
 // invert in place by Gauss-Jordan with partial pivoting, store transposed.
+// qdense != nullptr: the blocks come pre-assembled (FP64 complex, [block][kBS][kBS] row-major; any Q kind)
 __global__ void __launch_bounds__(256) k_block_inverse(const int32_t* __restrict__ bptr, const int64_t* __restrict__ clp,
                                                        const int32_t* __restrict__ clc, const double* __restrict__ clv,
                                                        const int64_t* __restrict__ cpp, const int32_t* __restrict__ cpc,
-                                                       const double2* __restrict__ dk, float2* __restrict__ inv,
-                                                       int* singular)
+                                                       const double2* __restrict__ dk, const double2* __restrict__ qdense,
+                                                       float2* __restrict__ inv, int* singular)
 {
     extern __shared__ double2 Qsm[];
     double2 (*Q)[kBS + 1] = reinterpret_cast<double2 (*)[kBS + 1]>(Qsm);
@@ -144,8 +145,12 @@ __global__ void __launch_bounds__(256) k_block_inverse(const int32_t* __restrict
     const int tid = threadIdx.x;
     for (int i = tid; i < kBS * (kBS + 1); i += blockDim.x) (&Q[0][0])[i] = make_double2(0, 0);
     __syncthreads();
+    if (qdense) {
+        const double2* qb = qdense + (size_t)blk * kBS * kBS;
+        for (int i = tid; i < m * m; i += blockDim.x) Q[i / m][i % m] = qb[(i / m) * kBS + i % m];
+    }
     // assembly: thread per row a
-    for (int a = tid; a < m; a += blockDim.x) {
+    for (int a = tid; a < m && !qdense; a += blockDim.x) {
         const int la = l0 + a;
         for (int64_t q = clp[la]; q < clp[la + 1]; ++q) {
             const int k = clc[q];
@@ -390,6 +395,66 @@ static xrl_status op_apply(xrl_op op, const float2* v, float2* w, int nrhs)
 }
 
 namespace xrl {
+// Diagonal of the edge-edge matrix L = sum_t A_t P A_t^T (the diagonal-of-L baseline):
+// for edge e between panels p < q with midpoint m, A(e, p) = m - c_p, A(e, q) = c_q - m (Alg. 1), so
+// L_ee = |m - c_p|^2 P_pp + |c_q - m|^2 P_qq + 2 (m - c_p).(c_q - m) P_pq, with P_pq from the near CSR
+// (edge-adjacent panels are always near).
+__global__ void k_edge_ldiag(int64_t ne, const int32_t* __restrict__ ei, const int32_t* __restrict__ ej,
+                             const double* __restrict__ mid, const double* __restrict__ cent,
+                             const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                             const double* __restrict__ val64, double* __restrict__ lee, int* missing)
+{
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    const int p = ei[e], q = ej[e];
+    auto entry = [&](int r, int c) -> double {
+        int64_t lo = ptr[r], hi = ptr[r + 1] - 1;
+        while (lo < hi) {
+            const int64_t md = (lo + hi) >> 1;
+            if (col[md] < c) lo = md + 1; else hi = md;
+        }
+        if (lo < ptr[r + 1] && col[lo] == c) return val64[lo];
+        atomicExch(missing, 1);
+        return 0.0;
+    };
+    double ap = 0, aq = 0, apq = 0;
+    for (int d = 0; d < 3; ++d) {
+        const double a = mid[3 * e + d] - cent[3 * (int64_t)p + d], b = cent[3 * (int64_t)q + d] - mid[3 * e + d];
+        ap += a * a;
+        aq += b * b;
+        apq += a * b;
+    }
+    lee[e] = ap * entry(p, p) + aq * entry(q, q) + 2.0 * apq * entry(p, q);
+}
+
+void precond_ldiag(xrl_op op, std::vector<double>& lee)
+{
+    xrl_tree t = op->tree;
+    xrl_topo T = op->topo;
+    cudaStream_t st = t->ctx->stream;
+    const int64_t ne = T->n_edges;
+    lee.assign(ne, 0.0);
+    if (ne == 0) return;
+    DBuf<int32_t> ei(ne), ej(ne);
+    DBuf<double> mid(3 * ne), out(ne);
+    DBuf<int> miss(1);
+    XRL_CUDA(cudaMemcpyAsync(ei.p, T->edge_i.data(), 4 * ne, cudaMemcpyHostToDevice, st));
+    XRL_CUDA(cudaMemcpyAsync(ej.p, T->edge_j.data(), 4 * ne, cudaMemcpyHostToDevice, st));
+    XRL_CUDA(cudaMemcpyAsync(mid.p, T->edge_mid.data(), 24 * ne, cudaMemcpyHostToDevice, st));
+    XRL_CUDA(cudaMemsetAsync(miss.p, 0, 4, st));
+    k_edge_ldiag<<<nblk(ne, 256), 256, 0, st>>>(ne, ei.p, ej.p, mid.p, t->cent.p, op->near->row_ptr.p, op->near->col.p,
+                                                op->near->val64.p, out.p, miss.p);
+    XRL_LAUNCH_CHECK();
+    int hm = 0;
+    XRL_CUDA(cudaMemcpyAsync(lee.data(), out.p, 8 * ne, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaMemcpyAsync(&hm, miss.p, 4, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    if (hm) {
+        set_error("diag-of-L: an edge's panel pair is not in the near field (eta too small)");
+        throw CudaError{XRL_EGEOM};
+    }
+}
+
 void precond_diag(xrl_op op, std::vector<double2>& hd)
 {
     xrl_tree t = op->tree;
@@ -505,47 +570,102 @@ xrl_status xrl_operator_apply(xrl_op op, const void* v, void* w, int32_t nrhs)
     API_CATCH
 }
 
+static xrl_status precond_build_blocks(xrl_op op, int32_t qkind, int32_t block_size, xrl_precond* out)
+{
+    xrl_tree t = op->tree;
+    xrl_topo T = op->topo;
+    cudaStream_t st = t->ctx->stream;
+    XRL_CUDA(cudaSetDevice(t->ctx->device));
+    const int64_t n = t->n, nl = T->n_loops;
+    auto pc = std::make_unique<xrl_precond_s>();
+    pc->op = op;
+    pc->qkind = qkind;
+    pc->bs = block_size;
+    for (int64_t l = 0; l < nl; l += block_size) pc->bptr_h.push_back((int32_t)l);
+    pc->bptr_h.push_back((int32_t)nl);
+    pc->nblocks = (int32_t)pc->bptr_h.size() - 1;
+    pc->bptr.alloc(pc->bptr_h.size());
+    XRL_CUDA(cudaMemcpyAsync(pc->bptr.p, pc->bptr_h.data(), 4 * pc->bptr_h.size(), cudaMemcpyHostToDevice, st));
+    DBuf<double2> dk, qd;
+    if (qkind == 0) {
+        // d_k = Z_s/A + j alpha P_kk; the blocks are assembled on the GPU from C = M A_t
+        std::vector<double2> hd;
+        precond_diag(op, hd);
+        dk.alloc(n);
+        XRL_CUDA(cudaMemcpyAsync(dk.p, hd.data(), 16 * n, cudaMemcpyHostToDevice, st));
+    } else {
+        // any other Q (diag-of-L): assembled sparse on the host, its diagonal blocks uploaded dense
+        std::vector<std::vector<int32_t>> rc;
+        std::vector<std::vector<std::complex<double>>> rv;
+        assemble_q(op, qkind, rc, rv);
+        std::vector<double2> h((size_t)pc->nblocks * kBS * kBS, make_double2(0, 0));
+        for (int b = 0; b < pc->nblocks; ++b) {
+            const int l0 = pc->bptr_h[b], l1 = pc->bptr_h[b + 1];
+            for (int a = l0; a < l1; ++a)
+                for (size_t i = 0; i < rc[a].size(); ++i)
+                    if (rc[a][i] >= l0 && rc[a][i] < l1)
+                        h[((size_t)b * kBS + (a - l0)) * kBS + (rc[a][i] - l0)] =
+                            make_double2(rv[a][i].real(), rv[a][i].imag());
+        }
+        qd.alloc(h.size());
+        XRL_CUDA(cudaMemcpyAsync(qd.p, h.data(), 16 * h.size(), cudaMemcpyHostToDevice, st));
+    }
+    pc->inv.alloc((size_t)pc->nblocks * kBS * kBS);
+    DBuf<int> sing(1);
+    XRL_CUDA(cudaMemsetAsync(sing.p, 0, 4, st));
+    if (pc->nblocks > 0) {
+        const int smem = kBS * (kBS + 1) * (int)sizeof(double2);
+        XRL_CUDA(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        k_block_inverse<<<pc->nblocks, 256, smem, st>>>(pc->bptr.p, T->cl_ptr.p, T->cl_col.p, T->cl_val64.p, T->cp_ptr.p,
+                                                     T->cp_col.p, dk.p, qd.p, pc->inv.p, sing.p);
+        XRL_LAUNCH_CHECK();
+    }
+    int hs = 0;
+    XRL_CUDA(cudaMemcpyAsync(&hs, sing.p, 4, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    if (hs) { set_error("xrl_precond_build: singular block %d (pivot below 1e-13 of the block max)", hs - 1); return XRL_ESINGULAR; }
+    ++T->refs;
+    *out = pc.release();
+    return XRL_OK;
+}
+
+static xrl_status precond_build_exact_kind(xrl_op op, int32_t qkind, xrl_precond* out)
+{
+    XRL_CUDA(cudaSetDevice(op->tree->ctx->device));
+    auto pc = std::make_unique<xrl_precond_s>();
+    pc->op = op;
+    pc->kind = 1;
+    pc->qkind = qkind;
+    pc->bs = 0;
+    const xrl_status s = exact_build(pc.get());
+    if (s != XRL_OK) return s;
+    ++op->topo->refs;
+    *out = pc.release();
+    return XRL_OK;
+}
+
 xrl_status xrl_precond_build(xrl_op op, int32_t block_size, xrl_precond* out)
 {
     if (!op || !out) { set_error("xrl_precond_build: null argument"); return XRL_EINVAL; }
     *out = nullptr;
     if (block_size < 1 || block_size > kBS) { set_error("xrl_precond_build: block_size must be 1..%d", kBS); return XRL_EINVAL; }
     API_TRY
-        xrl_tree t = op->tree;
-        xrl_topo T = op->topo;
-        cudaStream_t st = t->ctx->stream;
-        XRL_CUDA(cudaSetDevice(t->ctx->device));
-        const int64_t n = t->n, nl = T->n_loops;
-        auto pc = std::make_unique<xrl_precond_s>();
-        pc->op = op;
-        pc->bs = block_size;
-        for (int64_t l = 0; l < nl; l += block_size) pc->bptr_h.push_back((int32_t)l);
-        pc->bptr_h.push_back((int32_t)nl);
-        pc->nblocks = (int32_t)pc->bptr_h.size() - 1;
-        pc->bptr.alloc(pc->bptr_h.size());
-        XRL_CUDA(cudaMemcpyAsync(pc->bptr.p, pc->bptr_h.data(), 4 * pc->bptr_h.size(), cudaMemcpyHostToDevice, st));
-        // d_k = Z_s/A + j alpha P_kk
-        std::vector<double2> hd;
-        precond_diag(op, hd);
-        DBuf<double2> dk(n);
-        XRL_CUDA(cudaMemcpyAsync(dk.p, hd.data(), 16 * n, cudaMemcpyHostToDevice, st));
-        pc->inv.alloc((size_t)pc->nblocks * kBS * kBS);
-        DBuf<int> sing(1);
-        XRL_CUDA(cudaMemsetAsync(sing.p, 0, 4, st));
-        if (pc->nblocks > 0) {
-            const int smem = kBS * (kBS + 1) * (int)sizeof(double2);
-            XRL_CUDA(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            k_block_inverse<<<pc->nblocks, 256, smem, st>>>(pc->bptr.p, T->cl_ptr.p, T->cl_col.p, T->cl_val64.p, T->cp_ptr.p,
-                                                         T->cp_col.p, dk.p, pc->inv.p, sing.p);
-            XRL_LAUNCH_CHECK();
-        }
-        int hs = 0;
-        XRL_CUDA(cudaMemcpyAsync(&hs, sing.p, 4, cudaMemcpyDeviceToHost, st));
-        XRL_CUDA(cudaStreamSynchronize(st));
-        if (hs) { set_error("xrl_precond_build: singular block %d (pivot below 1e-13 of the block max)", hs - 1); return XRL_ESINGULAR; }
-        ++T->refs;
-        *out = pc.release();
-        return XRL_OK;
+        return precond_build_blocks(op, 0, block_size, out);
+    API_CATCH
+}
+
+xrl_status xrl_precond_build_kind(xrl_op op, int32_t kind, int32_t block_size, xrl_precond* out)
+{
+    if (!op || !out) { set_error("xrl_precond_build_kind: null argument"); return XRL_EINVAL; }
+    *out = nullptr;
+    if (kind != XRL_PRECOND_DIAG_P && kind != XRL_PRECOND_DIAG_L) { set_error("xrl_precond_build_kind: bad kind %d", kind); return XRL_EINVAL; }
+    if (block_size != -1 && (block_size < 1 || block_size > kBS)) {
+        set_error("xrl_precond_build_kind: block_size must be -1 (exact) or 1..%d", kBS);
+        return XRL_EINVAL;
+    }
+    API_TRY
+        if (block_size < 0) return precond_build_exact_kind(op, kind, out);
+        return precond_build_blocks(op, kind, block_size, out);
     API_CATCH
 }
 
@@ -554,16 +674,7 @@ xrl_status xrl_precond_build_exact(xrl_op op, xrl_precond* out)
     if (!op || !out) { set_error("xrl_precond_build_exact: null argument"); return XRL_EINVAL; }
     *out = nullptr;
     API_TRY
-        XRL_CUDA(cudaSetDevice(op->tree->ctx->device));
-        auto pc = std::make_unique<xrl_precond_s>();
-        pc->op = op;
-        pc->kind = 1;
-        pc->bs = 0;
-        const xrl_status s = exact_build(pc.get());
-        if (s != XRL_OK) return s;
-        ++op->topo->refs;
-        *out = pc.release();
-        return XRL_OK;
+        return precond_build_exact_kind(op, 0, out);
     API_CATCH
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <complex>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -79,8 +80,7 @@ constexpr int kMuStride = 768;       // floats per box multipole mu[r][k] (r-maj
 constexpr int kOpM2M = 316, kOpL2L = 324, kNOpImg = 332;  // tensor-core operator images: M2L 0..315, M2M, L2L
 constexpr int kEllStride = 768;      // floats per box local expansion ell[r][k] (r-major, k padded to 128)
 constexpr int kEllKStride = 968;     // floats per leaf local expansion ellk[k][8] (k-major, for the L2P)
-constexpr int kNearGrpSeg = 32;      // near SpMV: segments (rows) per group = CTA threads / 8
-constexpr int kNearCap = 512;        // near SpMV: max column union per group (a warp's shared-memory stage)
+constexpr int kNearSegLen = 256;     // near SpMV: max entries per segment (8 lanes each)
 
 }  // namespace xrl
 
@@ -197,17 +197,13 @@ struct xrl_near_s {
     xrl::DBuf<int32_t> col;
     xrl::DBuf<float> val;       // N_kl (FP32)
     xrl::DBuf<double> val64;    // P_kl (FP64, before subtraction)
-    // row-group format of the owned rows for the SpMV (near.cu build_near_groups)
-    int32_t n_groups = 0;
-    int64_t n_entries = 0, n_union = 0;
-    xrl::DBuf<int32_t> grp_seg;   // [n_groups+1] first segment of each group
-    xrl::DBuf<int64_t> grp_u;     // [n_groups+1] offset of each group's column union in ucol
-    xrl::DBuf<int32_t> seg_row;   // [nseg] local row (row - p0) of each segment
-    xrl::DBuf<int64_t> seg_off;   // [nseg+1] padded entry offsets (multiples of 4)
-    xrl::DBuf<int32_t> ucol;      // [n_union] sorted column unions, group after group
+    // segment format of the owned rows for the SpMV (near.cu build_near_segments)
+    int64_t n_segs = 0, n_entries = 0;
+    xrl::DBuf<int32_t> seg_row;   // [n_segs] local row (row - p0)
+    xrl::DBuf<int32_t> seg_base;  // [n_segs] column base (upper 16 bits)
+    xrl::DBuf<int64_t> seg_off;   // [n_segs+1] padded entry offsets (multiples of 4)
     xrl::DBuf<float> eval;        // [n_entries] N_kl (FP32), 0 in the padding
-    xrl::DBuf<uint16_t> eidx;     // [n_entries] position of the column in the group's union
-    xrl::DBuf<uint8_t> cseg;      // [n_entries / 4] segment (within its group) of each 4-entry chunk
+    xrl::DBuf<uint16_t> eoff;     // [n_entries] column - base
     // halo of x (exchange.cu; part_world > 1): panels peers read from this rank / this rank reads
     std::vector<int64_t> halo_soff, halo_roff;  // [world+1] panel offsets per peer
     xrl::DBuf<int32_t> halo_sidx, halo_ridx;
@@ -256,6 +252,7 @@ struct xrl_op_s {
 struct xrl_precond_s {
     xrl_op op = nullptr;
     int32_t kind = 0;                            // 0 block-Jacobi (k_block_*), 1 exact sparse LU (precond_exact.cpp)
+    int32_t qkind = 0;                           // Q: 0 diagonal-of-P (Eq. 10), 1 diagonal-of-L
     void* exact = nullptr;                       // kind 1: factorisation state
     int32_t bs = 64, nblocks = 0;
     std::vector<int32_t> bptr_h;
@@ -266,6 +263,11 @@ struct xrl_precond_s {
 namespace xrl {
 // diagonal-of-P preconditioner: d_k = Z_s,k/A_k + j alpha P_kk per panel (library order, FP64)
 void precond_diag(xrl_op op, std::vector<double2>& d);
+// diag-of-L: L_ee = (sum_t A_t P A_t^T)_ee per edge (host vector, FP64)
+void precond_ldiag(xrl_op op, std::vector<double>& lee);
+// sparse Q of kind qkind (0 diag-of-P Eq. 10, 1 diag-of-L) on the host: rows rc[a] (ascending), values rv[a]
+void assemble_q(xrl_op op, int qkind, std::vector<std::vector<int32_t>>& rc,
+                std::vector<std::vector<std::complex<double>>>& rv);
 // exact Q^-1 (NEXT f2): build the factorisation into pc->exact, apply it, release it
 xrl_status exact_build(xrl_precond pc);
 void exact_apply(xrl_precond pc, const float2* v, float2* z, int nrhs);

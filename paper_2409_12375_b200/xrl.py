@@ -28,7 +28,7 @@ EXPORTS = [
     "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_ctx_set_fuse", "xrl_extract",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
-    "xrl_precond_build_exact", "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
+    "xrl_precond_build_exact", "xrl_precond_build_kind", "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
     "xrl_port_currents", "xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_vranks", "xrl_exchange_info", "xrl_plan_exchange",
 ]
 
@@ -115,7 +115,7 @@ def lib():
         L.xrl_near_destroy.restype = None
         L.xrl_near_export.argtypes = [P, P, P, P, P, P]
         L.xrl_near_export_rows.argtypes = [P, i64, P, P, P, P, P]
-        L.xrl_near_info.argtypes = [P, P, P, P, P]
+        L.xrl_near_info.argtypes = [P, P, P, P]
         L.xrl_mvm.argtypes = [P, P, P, P, i32, u32]
         L.xrl_mvm_host.argtypes = [P, P, P, P, i32, u32]
         L.xrl_mvm_host_batch.argtypes = [P, P, P, P, i32, i32, u32]
@@ -146,6 +146,7 @@ def lib():
         L.xrl_operator_destroy.restype = None
         L.xrl_precond_build.argtypes = [P, i32, pp]
         L.xrl_precond_build_exact.argtypes = [P, pp]
+        L.xrl_precond_build_kind.argtypes = [P, i32, i32, pp]
         L.xrl_precond_apply.argtypes = [P, P, P, i32]
         L.xrl_precond_export.argtypes = [P, P, P, P, P]
         L.xrl_precond_destroy.argtypes = [P]
@@ -162,7 +163,7 @@ def lib():
                      "xrl_plan_exchange"):
             getattr(L, name).restype = ctypes.c_int32
         for name in ("xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_esi",
-                     "xrl_operator_create", "xrl_operator_apply", "xrl_precond_build", "xrl_precond_build_exact",
+                     "xrl_operator_create", "xrl_operator_apply", "xrl_precond_build", "xrl_precond_build_exact", "xrl_precond_build_kind",
                      "xrl_precond_apply",
                      "xrl_precond_export", "xrl_gmres", "xrl_port_rhs", "xrl_port_currents"):
             getattr(L, name).restype = ctypes.c_int32
@@ -390,9 +391,9 @@ class Near:
         return ptr, col[:k], v32[:k], v64[:k]
 
     def info(self) -> dict:
-        v = [ctypes.c_int64() for _ in range(4)]
+        v = [ctypes.c_int64() for _ in range(3)]
         check(lib().xrl_near_info(self.h, *[ctypes.byref(a) for a in v]))
-        return dict(zip(("nnz", "n_groups", "n_entries", "n_union"), [int(a.value) for a in v]))
+        return dict(zip(("nnz", "n_segments", "n_entries"), [int(a.value) for a in v]))
 
     def export_rows(self, rows):
         """Selected library-order rows: (ptr, col, v32, v64) over those rows only."""
@@ -628,12 +629,17 @@ class Operator:
 
 class Precond:
     """xrl_precond_build: block-Jacobi diagonal-of-P preconditioner (Eq. 10); exact=True:
-    xrl_precond_build_exact, the whole Q factorised (sparse LU, NEXT f2)."""
+    xrl_precond_build_exact, the whole Q factorised (sparse LU, NEXT f2); kind="diag_l": the
+    diagonal-of-L baseline of PAPER.md:120-122 (xrl_precond_build_kind)."""
 
-    def __init__(self, op: Operator, block_size: int = 64, exact: bool = False):
+    KINDS = {"diag_p": 0, "diag_l": 1}
+
+    def __init__(self, op: Operator, block_size: int = 64, exact: bool = False, kind: str = "diag_p"):
         self.op = op
         h = ctypes.c_void_p()
-        if exact:
+        if kind != "diag_p":
+            check(lib().xrl_precond_build_kind(op.h, self.KINDS[kind], -1 if exact else block_size, ctypes.byref(h)))
+        elif exact:
             check(lib().xrl_precond_build_exact(op.h, ctypes.byref(h)))
         else:
             check(lib().xrl_precond_build(op.h, block_size, ctypes.byref(h)))

@@ -448,3 +448,58 @@ def test_extract_coils_ten_frequencies(coils_all):
         assert np.all(np.diff(res["r"][:, p, p]) > -1e-3 * res["r"][0, p, p])
         assert np.all(np.diff(res["l"][:, p, p]) < 1e-3 * res["l"][0, p, p])
     assert np.all(res["true_rre"][0] <= 1e-5)
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_precond_diag_l_apply_vs_oracle(bar_all, exact):
+    """NEXT f2: the diagonal-of-L baseline through xrl_precond_build_kind -- block-Jacobi
+    and whole-Q -- against the oracle's Q_L = M (sum_t A_t diag(Z_s/A) A_t^T + alpha diag(L_ee)) M^T
+    (oracle/loop_oracle.precond_q_diag_l, pinned in tests/test_oracle_loop.py) on the library's blocks."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo, g, P = bar_all
+    freq = 1e8
+    op = xrl.Operator(tree, near, topo, freq, sigma=SIGMA, zeta=ZETA)
+    pc = xrl.Precond(op, 64, exact=exact, kind="diag_l")
+    ex = topo.export()
+    br = [tuple(b) for b in ex["branch_nodes"]]
+    A = lo.cm_maps(m.verts, m.tris, g.cent, br)
+    nl = len(ex["m_ptr"]) - 1
+    rows = np.repeat(np.arange(nl), np.diff(ex["m_ptr"]))
+    M = sp.csr_matrix((ex["m_sign"].astype(float), (rows, ex["m_branch"])), shape=(nl, len(br)))
+    phys = sp.diags((ex["branch_kind"] == 0).astype(float))
+    A = [phys @ A[t] for t in range(3)]
+    zs = lo.esi(SIGMA, ZETA, freq)
+    alpha = 1j * 2 * np.pi * freq * lo.MU0 / (4 * np.pi)
+    QL = lo.precond_q_diag_l(M, A, zs / g.area, alpha, P)
+    bptr = [0, nl] if exact else list(range(0, nl, 64)) + [nl]
+    v = (np.random.default_rng(8).random((2, nl)) - 0.5 + 1j * (np.random.default_rng(9).random((2, nl)) - 0.5))
+    v = v.astype(np.complex64)
+    z = pc.apply(torch.from_numpy(v).cuda()).cpu().numpy()
+    zref = lo.block_solve(QL, bptr, v.astype(np.complex128))
+    err = oracle.rel_l2(z, zref)
+    print("diag-of-L exact" if exact else "diag-of-L block", err)
+    assert err <= 1e-5
+
+
+def test_diag_p_beats_diag_l_iterations(coils_all):
+    """Table IV's comparison ("the number of iterations is halved") on the coil pair at
+    100 MHz and tol 1e-6 (the tolerance of the paper's Table IV run): GMRES with the exact diag-of-P Q^-1
+    needs fewer iterations than with the exact diag-of-L Q_L^-1, and both give the same port impedance."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo = coils_all
+    op = xrl.Operator(tree, near, topo, 1e8, sigma=SIGMA, zeta=5e-6)
+    b = torch.zeros((2, topo.n_loops), dtype=torch.complex64, device="cuda")
+    for p in range(2):
+        topo.port_rhs(p, 1.0, out=b[p:p + 1])
+    it, zz = {}, {}
+    for kind in ("diag_p", "diag_l"):
+        pc = xrl.Precond(op, exact=True, kind=kind)
+        x, rep = xrl.gmres(op, pc, b, tol=1e-6, max_iters=3000)
+        it[kind] = int(rep["iters"].max())
+        zz[kind] = np.linalg.inv(topo.port_currents(x).T)
+        print(kind, rep)
+    print("Table IV analogue (coils, 100 MHz, tol 1e-6): iterations", it)
+    assert it["diag_p"] < it["diag_l"]
+    assert np.abs(zz["diag_p"] - zz["diag_l"]).max() / np.abs(zz["diag_p"]).max() < 1e-3
