@@ -371,19 +371,31 @@ xrl_status xrl_esi(double sigma, double zeta, double freq_hz, double* zs_re, dou
  * applied as u_t = C_t^T v (C_t = M A_t), P u_t by xrl_mvm, w = sum_t C_t y_t.
  * zs: per-panel complex Z_s (double [n][2], mesh order) or NULL to use
  * xrl_esi(sigma, zeta, freq) for every panel.  Handles are borrowed.
- * Single-rank trees only: XRL_EUNSUPPORTED if the tree is partitioned
- * (part_world > 1; the loop-space vectors are not sharded);
- * xrl_extract has the same restriction. */
+ * On a partitioned tree (part_world > 1) the operator is sharded in loop
+ * space: the rank owns the contiguous loops
+ * [loop_offset, loop_offset + n_loops_local) (xrl_operator_info; cuts follow
+ * the owner of each loop's lowest panel) and every vector of the operator,
+ * preconditioner and GMRES calls is that slice; an apply exchanges the loop
+ * values its panels read and the panel values its loops read, around the
+ * sharded xrl_mvm.  xrl_extract runs on single-rank trees only. */
 xrl_status xrl_operator_create(xrl_tree tree, xrl_near near, xrl_topo topo, const double* zs, double sigma,
                                double zeta, double freq_hz, xrl_op* out);
-/* w = A v; v, w device complex64 [nrhs][n_loops], must not alias. */
+/* w = A v; v, w device complex64 [nrhs][n_loops] (partitioned: [nrhs][n_loops_local], collective over
+ * the context's communicator; XRL_EUNSUPPORTED on a virtual rank), must not alias. */
 xrl_status xrl_operator_apply(xrl_op op, const void* v, void* w, int32_t nrhs);
+/* This rank's loop slice: first loop and count (0 and n_loops on a single-rank operator). */
+xrl_status xrl_operator_info(xrl_op op, int64_t* loop_offset, int64_t* n_loops_local);
+/* Virtual ranks: the sharded operator of k operators built on the k trees of one xrl_mvm_vranks
+ * partition (one single-rank context), applied in one call with device-copy exchanges; v[r], w[r]:
+ * rank r's slices.  k = 1 with a single-rank operator is the plain apply. */
+xrl_status xrl_operator_apply_vranks(int32_t k, const xrl_op* ops, const void* const* v, void* const* w, int32_t nrhs);
 void xrl_operator_destroy(xrl_op op);
 
 /* Diagonal-of-P preconditioner (Eq. 10-11) in block-Jacobi
  * form (reading R13): Q = sum_t C_t diag(Z_s/A + alpha P_kk) C_t^T,
  * loops cut into consecutive (Morton-ordered) blocks of <= block_size
- * (<= 64), each diagonal block LU-inverted in FP64 and stored complex64.
+ * (<= 64; on a sharded operator: of the rank's loops, no communication in
+ * the apply), each diagonal block LU-inverted in FP64 and stored complex64.
  * XRL_ESINGULAR if a pivot falls below 1e-13 of the block's largest entry. */
 xrl_status xrl_precond_build(xrl_op op, int32_t block_size, xrl_precond* out);
 /* Exact diagonal-of-P preconditioner: the same Q, factorised
@@ -438,6 +450,12 @@ typedef struct {
 } xrl_gmres_opts;
 xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b, void* x, int32_t nrhs, const xrl_gmres_opts* opts,
                      int32_t* iters, double* rre, double* true_rre, int32_t* converged);
+/* GMRES over k virtual ranks (the operators / preconditioners of one xrl_mvm_vranks partition; pcs NULL
+ * = none): b[r], x[r] rank r's loop slices; the inner products are summed over the ranks (on a multi-rank
+ * context xrl_gmres all-reduces them over NCCL instead).  Outputs and errors as xrl_gmres. */
+xrl_status xrl_gmres_vranks(int32_t k, const xrl_op* ops, const xrl_precond* pcs, const void* const* b,
+                            void* const* x, int32_t nrhs, const xrl_gmres_opts* opts, int32_t* iters, double* rre,
+                            double* true_rre, int32_t* converged);
 
 /* Port excitation V_l = M V_branch with `volts` on port `port`'s branch
  * (device complex64 [n_loops], overwritten), and port currents read back from

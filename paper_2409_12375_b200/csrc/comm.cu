@@ -69,6 +69,14 @@ xrl_status nccl_allreduce_sum(xrl_ctx ctx, float* buf, size_t count, cudaStream_
     return XRL_OK;
 }
 
+xrl_status nccl_allreduce_sum_f64(xrl_ctx ctx, double* buf, size_t count, cudaStream_t st)
+{
+    if (!ctx->nccl_comm) { set_error("nccl_allreduce_sum_f64: context has no communicator"); return XRL_ENCCL; }
+    if (count == 0) return XRL_OK;
+    XRL_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, (ncclComm_t)ctx->nccl_comm, st));
+    return XRL_OK;
+}
+
 }  // namespace xrl
 
 extern "C" xrl_status xrl_nccl_unique_id(void* out)

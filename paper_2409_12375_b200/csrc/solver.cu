@@ -1,7 +1,10 @@
 // Loop-space operator, diagonal-of-P block preconditioner, GMRES and port
 // excitation (Eq. 8-11).
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <complex>
+#include <functional>
 
 #include "xrl_internal.h"
 
@@ -341,6 +344,94 @@ __global__ void k_gsub(int64_t cnt, const float2* __restrict__ a, const float2* 
     out[x] = make_float2(a[x].x - b[x].x, a[x].y - b[x].y);
 }
 
+// ---- loop-space sharding (partitioned operators)
+// y[(3r+t)][k] = zsa_k u_t[k] + j alpha_im pu_t[k] for the rank's panels (ystride: slot stride of y)
+__global__ void k_panel_y(int64_t np, int nrhs, const float2* __restrict__ zsa, float alpha_im,
+                          const float2* __restrict__ u, const float2* __restrict__ pu, float2* __restrict__ y,
+                          int64_t ystride)
+{
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= np) return;
+    const float2 z = zsa[k];
+    for (int c = 0; c < 3 * nrhs; ++c) {
+        const float2 uu = u[(int64_t)c * np + k], pp = pu[(int64_t)c * np + k];
+        y[(int64_t)c * ystride + k] = make_float2(z.x * uu.x - z.y * uu.y - alpha_im * pp.y,
+                                                  z.x * uu.y + z.y * uu.x + alpha_im * pp.x);
+    }
+}
+
+// w[r][l] = sum_q sum_t val[3q+t] y[(3r+t)][col[q]] for the rank's loops (rows longer than kLongRow: below)
+__global__ void k_loops_from_y(int64_t nl, int nrhs, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                               const float* __restrict__ val, const float2* __restrict__ y, int64_t ystride,
+                               float2* __restrict__ w)
+{
+    const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (l >= nl) return;
+    if (ptr[l + 1] - ptr[l] > kLongRow) return;
+    for (int r = 0; r < nrhs; ++r) {
+        float2 acc = {0, 0};
+        for (int64_t q = ptr[l]; q < ptr[l + 1]; ++q)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const float2 v = y[(int64_t)(3 * r + t) * ystride + col[q]];
+                const float c = val[3 * q + t];
+                acc.x += c * v.x;
+                acc.y += c * v.y;
+            }
+        w[(int64_t)r * nl + l] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_loops_from_y_long(int64_t nl, int nrhs, const int32_t* __restrict__ rows,
+                                                           const int64_t* __restrict__ ptr,
+                                                           const int32_t* __restrict__ col,
+                                                           const float* __restrict__ val, const float2* __restrict__ y,
+                                                           int64_t ystride, float2* __restrict__ w)
+{
+    const int l = rows[blockIdx.x];
+    __shared__ float2 red[256];
+    for (int r = 0; r < nrhs; ++r) {
+        float2 acc = {0, 0};
+        for (int64_t q = ptr[l] + threadIdx.x; q < ptr[l + 1]; q += blockDim.x)
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const float2 v = y[(int64_t)(3 * r + t) * ystride + col[q]];
+                const float c = val[3 * q + t];
+                acc.x += c * v.x;
+                acc.y += c * v.y;
+            }
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        for (int st = 128; st > 0; st >>= 1) {
+            if (threadIdx.x < st) { red[threadIdx.x].x += red[threadIdx.x + st].x; red[threadIdx.x].y += red[threadIdx.x + st].y; }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) w[(int64_t)r * nl + l] = red[0];
+        __syncthreads();
+    }
+}
+
+// dst[i][c] = src[c][idx[i]]  (records of R complex values for the exchanges)
+__global__ void k_pack_cols(int64_t cnt, int R, const int32_t* __restrict__ idx, const float2* __restrict__ src,
+                            int64_t sstride, float2* __restrict__ dst)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= cnt * R) return;
+    const int64_t i = t / R;
+    const int c = (int)(t - i * R);
+    dst[t] = src[(int64_t)c * sstride + idx[i]];
+}
+// dst[c][base + i] = src[i][c]
+__global__ void k_unpack_cols(int64_t cnt, int R, const float2* __restrict__ src, float2* __restrict__ dst,
+                              int64_t dstride, int64_t base)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= cnt * R) return;
+    const int64_t i = t / R;
+    const int c = (int)(t - i * R);
+    dst[(int64_t)c * dstride + base + i] = src[t];
+}
+
 }  // namespace
 
 // ====================================================================== host
@@ -390,6 +481,285 @@ static xrl_status op_apply(xrl_op op, const float2* v, float2* w, int nrhs)
                                                           op->pu.p, w);
         XRL_LAUNCH_CHECK();
         t->ctx->launches += 1;
+    }
+    return XRL_OK;
+}
+
+// ---------------------------------------------------------------- loop-space sharding
+static int owner_in(const std::vector<int64_t>& cut, int64_t i)
+{
+    return (int)(std::upper_bound(cut.begin(), cut.end() - 1, i) - cut.begin()) - 1;
+}
+
+// Per-peer receive / send lists of rank me from need[r] (ascending ids; owner by `cut`).
+static void split_by_owner(const std::vector<std::vector<int64_t>>& need, int me, const std::vector<int64_t>& cut,
+                           std::vector<int64_t>& roff, std::vector<int64_t>& ridx, std::vector<int64_t>& soff,
+                           std::vector<int64_t>& sidx)
+{
+    const int W = (int)cut.size() - 1;
+    roff.assign(W + 1, 0);
+    soff.assign(W + 1, 0);
+    ridx.clear();
+    sidx.clear();
+    for (int q = 0; q < W; ++q) {
+        roff[q] = (int64_t)ridx.size();
+        if (q != me)
+            for (int64_t v : need[me])
+                if (owner_in(cut, v) == q) ridx.push_back(v);
+        soff[q] = (int64_t)sidx.size();
+        if (q != me)
+            for (int64_t v : need[q])
+                if (owner_in(cut, v) == me) sidx.push_back(v);
+    }
+    roff[W] = (int64_t)ridx.size();
+    soff[W] = (int64_t)sidx.size();
+}
+
+// The loop-space shard of a partitioned operator (every rank derives every rank's lists from the shared
+// topology, so the send list q -> r equals the receive list r <- q).
+static void build_loop_partition(xrl_op op)
+{
+    xrl_tree t = op->tree;
+    xrl_topo T = op->topo;
+    cudaStream_t st = t->ctx->stream;
+    const int W = t->part_world, me = t->part_rank;
+    const int64_t nl = T->n_loops;
+    std::vector<int64_t> pcut(t->part_cuts.begin(), t->part_cuts.end());
+    const std::vector<int64_t>& cp = T->c_ptr_h;
+    const std::vector<int32_t>& cc = T->c_col_h;
+    const std::vector<double>& cv = T->c_val_h;
+    auto P = std::make_unique<LoopPart>();
+    // loop cuts: as many loops per rank as have their first (lowest) panel in the rank's panel range
+    std::vector<int64_t> cnt(W + 1, 0);
+    for (int64_t l = 0; l < nl; ++l) {
+        int64_t mn = INT64_MAX;
+        for (int64_t q = cp[l]; q < cp[l + 1]; ++q) mn = std::min<int64_t>(mn, cc[q]);
+        cnt[mn == INT64_MAX ? W - 1 : owner_in(pcut, mn)]++;
+    }
+    P->lcut.assign(W + 1, 0);
+    for (int r = 0; r < W; ++r) P->lcut[r + 1] = P->lcut[r] + cnt[r];
+    P->L0 = P->lcut[me];
+    P->L1 = P->lcut[me + 1];
+    P->nlo = P->L1 - P->L0;
+    P->npl = t->p1 - t->p0;
+    // loop halo: loops a rank's panels read that another rank owns; panel halo: panels a rank's loops read
+    std::vector<std::vector<int64_t>> lneed(W), pneed(W);
+    std::vector<int64_t> seen(W, -1);
+    std::vector<std::vector<uint8_t>> pmark(W, std::vector<uint8_t>(t->n, 0));
+    for (int64_t l = 0; l < nl; ++l) {
+        const int lo = owner_in(P->lcut, l);
+        for (int64_t q = cp[l]; q < cp[l + 1]; ++q) {
+            const int r = owner_in(pcut, cc[q]);
+            if (r != lo && seen[r] != l) { seen[r] = l; lneed[r].push_back(l); }
+            if (r != lo) pmark[lo][cc[q]] = 1;
+        }
+    }
+    for (int r = 0; r < W; ++r) {
+        for (int64_t k = 0; k < t->n; ++k)
+            if (pmark[r][k]) pneed[r].push_back(k);
+        std::vector<uint8_t>().swap(pmark[r]);
+    }
+    std::vector<int64_t> lr, ls, pr, ps;
+    split_by_owner(lneed, me, P->lcut, P->lh_roff, lr, P->lh_soff, ls);
+    split_by_owner(pneed, me, pcut, P->ph_roff, pr, P->ph_soff, ps);
+    P->nlh = (int64_t)lr.size();
+    P->nph = (int64_t)pr.size();
+    auto up32 = [&](DBuf<int32_t>& d, const std::vector<int64_t>& h, int64_t base) {
+        std::vector<int32_t> v(h.size());
+        for (size_t i = 0; i < h.size(); ++i) v[i] = (int32_t)(h[i] - base);
+        d.alloc(std::max<size_t>(1, v.size()));
+        if (!v.empty()) XRL_CUDA(cudaMemcpyAsync(d.p, v.data(), 4 * v.size(), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+    };
+    up32(P->lh_sidx, ls, P->L0);
+    up32(P->ph_sidx, ps, t->p0);
+    // slots: owned loops [0, nlo) then the halo loops; owned panels [0, npl) then the halo panels
+    auto slot_of = [](const std::vector<int64_t>& halo, int64_t id, int64_t lo, int64_t hi, int64_t nown) -> int32_t {
+        if (id >= lo && id < hi) return (int32_t)(id - lo);
+        return (int32_t)(nown + (std::lower_bound(halo.begin(), halo.end(), id) - halo.begin()));
+    };
+    // owned panel -> loop slots (transpose of C restricted to the owned panels)
+    {
+        std::vector<int64_t> ptr(P->npl + 1, 0);
+        for (int64_t l = 0; l < nl; ++l)
+            for (int64_t q = cp[l]; q < cp[l + 1]; ++q)
+                if (cc[q] >= t->p0 && cc[q] < t->p1) ptr[cc[q] - t->p0 + 1]++;
+        for (int64_t k = 0; k < P->npl; ++k) ptr[k + 1] += ptr[k];
+        std::vector<int32_t> col(ptr[P->npl]);
+        std::vector<float> val(3 * ptr[P->npl]);
+        std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+        for (int64_t l = 0; l < nl; ++l)
+            for (int64_t q = cp[l]; q < cp[l + 1]; ++q)
+                if (cc[q] >= t->p0 && cc[q] < t->p1) {
+                    const int64_t f = fill[cc[q] - t->p0]++;
+                    col[f] = slot_of(lr, l, P->L0, P->L1, P->nlo);
+                    for (int d = 0; d < 3; ++d) val[3 * f + d] = (float)cv[3 * q + d];
+                }
+        P->pl_ptr.alloc(ptr.size());
+        P->pl_col.alloc(std::max<size_t>(1, col.size()));
+        P->pl_val.alloc(std::max<size_t>(1, val.size()));
+        XRL_CUDA(cudaMemcpyAsync(P->pl_ptr.p, ptr.data(), 8 * ptr.size(), cudaMemcpyHostToDevice, st));
+        if (!col.empty()) {
+            XRL_CUDA(cudaMemcpyAsync(P->pl_col.p, col.data(), 4 * col.size(), cudaMemcpyHostToDevice, st));
+            XRL_CUDA(cudaMemcpyAsync(P->pl_val.p, val.data(), 4 * val.size(), cudaMemcpyHostToDevice, st));
+        }
+        XRL_CUDA(cudaStreamSynchronize(st));
+    }
+    // owned loop -> panel slots
+    {
+        std::vector<int64_t> ptr(P->nlo + 1, 0);
+        std::vector<int32_t> col, lng;
+        std::vector<float> val;
+        for (int64_t l = P->L0; l < P->L1; ++l) {
+            for (int64_t q = cp[l]; q < cp[l + 1]; ++q) {
+                col.push_back(slot_of(pr, cc[q], t->p0, t->p1, P->npl));
+                for (int d = 0; d < 3; ++d) val.push_back((float)cv[3 * q + d]);
+            }
+            ptr[l - P->L0 + 1] = (int64_t)col.size();
+            if (cp[l + 1] - cp[l] > kLongRow) lng.push_back((int32_t)(l - P->L0));
+        }
+        P->lp_ptr.alloc(ptr.size());
+        P->lp_col.alloc(std::max<size_t>(1, col.size()));
+        P->lp_val.alloc(std::max<size_t>(1, val.size()));
+        P->lp_long.alloc(std::max<size_t>(1, lng.size()));
+        P->n_long = (int32_t)lng.size();
+        XRL_CUDA(cudaMemcpyAsync(P->lp_ptr.p, ptr.data(), 8 * ptr.size(), cudaMemcpyHostToDevice, st));
+        if (!col.empty()) {
+            XRL_CUDA(cudaMemcpyAsync(P->lp_col.p, col.data(), 4 * col.size(), cudaMemcpyHostToDevice, st));
+            XRL_CUDA(cudaMemcpyAsync(P->lp_val.p, val.data(), 4 * val.size(), cudaMemcpyHostToDevice, st));
+        }
+        if (!lng.empty()) XRL_CUDA(cudaMemcpyAsync(P->lp_long.p, lng.data(), 4 * lng.size(), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+    }
+    op->part = std::move(P);
+}
+
+static void part_reserve(LoopPart& P, int nrhs)
+{
+    if (P.cap >= nrhs) return;
+    P.vext.alloc(std::max<int64_t>(1, (int64_t)nrhs * (P.nlo + P.nlh)));
+    P.u.alloc(std::max<int64_t>(1, (int64_t)3 * nrhs * P.npl));
+    P.pu.alloc(std::max<int64_t>(1, (int64_t)3 * nrhs * P.npl));
+    P.yext.alloc(std::max<int64_t>(1, (int64_t)3 * nrhs * (P.npl + P.nph)));
+    const int64_t recs = std::max({P.lh_soff.back(), P.lh_roff.back(), P.ph_soff.back(), P.ph_roff.back(), (int64_t)1});
+    P.sbuf.alloc(recs * 3 * nrhs);
+    P.rbuf.alloc(recs * 3 * nrhs);
+    P.cap = nrhs;
+}
+
+// One exchange of the loop-space shard between k parts of one process (device copies) or over NCCL (k = 1).
+static xrl_status part_exchange(const std::vector<xrl_op>& ops, bool loops, int rec, bool nccl, cudaStream_t st)
+{
+    const int k = (int)ops.size();
+    if (nccl) {
+        LoopPart& P = *ops[0]->part;
+        return nccl_exchange(ops[0]->tree->ctx, (const float*)P.sbuf.p, loops ? P.lh_soff : P.ph_soff, (float*)P.rbuf.p,
+                             loops ? P.lh_roff : P.ph_roff, 2 * rec, st);
+    }
+    for (int r = 0; r < k; ++r)
+        for (int q = 0; q < k; ++q) {
+            if (q == r) continue;
+            LoopPart& S = *ops[q]->part;
+            LoopPart& R = *ops[r]->part;
+            const std::vector<int64_t>& so = loops ? S.lh_soff : S.ph_soff;
+            const std::vector<int64_t>& ro = loops ? R.lh_roff : R.ph_roff;
+            const int64_t cnt = so[r + 1] - so[r];
+            if (cnt != ro[q + 1] - ro[q]) { set_error("loop-space exchange plans of ranks %d and %d disagree", q, r); return XRL_EINVAL; }
+            if (cnt > 0)
+                XRL_CUDA(cudaMemcpyAsync(R.rbuf.p + ro[q] * rec, S.sbuf.p + so[r] * rec, sizeof(float2) * cnt * rec,
+                                         cudaMemcpyDeviceToDevice, st));
+        }
+    return XRL_OK;
+}
+
+// w = A v for the parts of a partitioned operator (all k ranks of a virtual run, or this rank over NCCL):
+// loop halo -> u = C^T v on the owned panels -> P u by the sharded MVM -> y = Z_s/A u + j alpha P u ->
+// panel halo -> w = C y on the owned loops.
+static xrl_status op_apply_parts(const std::vector<xrl_op>& ops, const std::vector<const float2*>& v,
+                                 const std::vector<float2*>& w, int nrhs, bool nccl)
+{
+    const int k = (int)ops.size();
+    xrl_ctx ctx = ops[0]->tree->ctx;
+    cudaStream_t st = ctx->stream;
+    const int R = nrhs;
+    for (int i = 0; i < k; ++i) {
+        LoopPart& P = *ops[i]->part;
+        part_reserve(P, nrhs);
+        const int64_t ns = P.lh_soff.back();
+        if (ns > 0) {
+            k_pack_cols<<<nblk(ns * R, 256), 256, 0, st>>>(ns, R, P.lh_sidx.p, v[i], P.nlo, P.sbuf.p);
+            XRL_LAUNCH_CHECK();
+        }
+    }
+    xrl_status s = part_exchange(ops, true, R, nccl, st);
+    if (s) return s;
+    std::vector<float2*> u(k), pu(k);
+    for (int i = 0; i < k; ++i) {
+        xrl_op op = ops[i];
+        LoopPart& P = *op->part;
+        const int64_t nv = P.nlo + P.nlh;
+        if (P.nlo > 0)
+            XRL_CUDA(cudaMemcpy2DAsync(P.vext.p, 8 * nv, v[i], 8 * P.nlo, 8 * P.nlo, R, cudaMemcpyDeviceToDevice, st));
+        if (P.nlh > 0) {
+            k_unpack_cols<<<nblk(P.nlh * R, 256), 256, 0, st>>>(P.nlh, R, P.rbuf.p, P.vext.p, nv, P.nlo);
+            XRL_LAUNCH_CHECK();
+        }
+        if (P.npl > 0) {
+            k_loops_to_panels<<<nblk(P.npl, 256), 256, 0, st>>>(P.npl, nv, R, P.pl_ptr.p, P.pl_col.p, P.pl_val.p, P.vext.p,
+                                                               P.u.p);
+            XRL_LAUNCH_CHECK();
+        }
+        u[i] = P.u.p;
+        pu[i] = P.pu.p;
+        ctx->launches += 3;
+    }
+    // P u: the sharded MVM (NCCL collective, or the virtual-rank driver over the k trees)
+    if (nccl) {
+        s = xrl_mvm(ops[0]->tree, ops[0]->near, u[0], pu[0], 3 * R, XRL_MVM_FULL);
+    } else {
+        std::vector<xrl_tree> tr(k);
+        std::vector<xrl_near> nr(k);
+        std::vector<const void*> uv(k);
+        std::vector<void*> pv(k);
+        for (int i = 0; i < k; ++i) { tr[i] = ops[i]->tree; nr[i] = ops[i]->near; uv[i] = u[i]; pv[i] = pu[i]; }
+        s = xrl_mvm_vranks(k, tr.data(), nr.data(), uv.data(), pv.data(), 3 * R, XRL_MVM_FULL, nullptr, nullptr);
+    }
+    if (s) return s;
+    for (int i = 0; i < k; ++i) {
+        xrl_op op = ops[i];
+        LoopPart& P = *op->part;
+        const int64_t ys = P.npl + P.nph;
+        if (P.npl > 0) {
+            k_panel_y<<<nblk(P.npl, 256), 256, 0, st>>>(P.npl, R, op->zsa.p + op->tree->p0, (float)op->alpha_im, P.u.p,
+                                                       P.pu.p, P.yext.p, ys);
+            XRL_LAUNCH_CHECK();
+        }
+        const int64_t ns = P.ph_soff.back();
+        if (ns > 0) {
+            k_pack_cols<<<nblk(ns * 3 * R, 256), 256, 0, st>>>(ns, 3 * R, P.ph_sidx.p, P.yext.p, ys, P.sbuf.p);
+            XRL_LAUNCH_CHECK();
+        }
+    }
+    s = part_exchange(ops, false, 3 * R, nccl, st);
+    if (s) return s;
+    for (int i = 0; i < k; ++i) {
+        LoopPart& P = *ops[i]->part;
+        const int64_t ys = P.npl + P.nph;
+        if (P.nph > 0) {
+            k_unpack_cols<<<nblk(P.nph * 3 * R, 256), 256, 0, st>>>(P.nph, 3 * R, P.rbuf.p, P.yext.p, ys, P.npl);
+            XRL_LAUNCH_CHECK();
+        }
+        if (P.nlo > 0) {
+            k_loops_from_y<<<nblk(P.nlo, 256), 256, 0, st>>>(P.nlo, R, P.lp_ptr.p, P.lp_col.p, P.lp_val.p, P.yext.p, ys,
+                                                            w[i]);
+            XRL_LAUNCH_CHECK();
+        }
+        if (P.n_long > 0) {
+            k_loops_from_y_long<<<P.n_long, 256, 0, st>>>(P.nlo, R, P.lp_long.p, P.lp_ptr.p, P.lp_col.p, P.lp_val.p,
+                                                          P.yext.p, ys, w[i]);
+            XRL_LAUNCH_CHECK();
+        }
+        ctx->launches += 5;
     }
     return XRL_OK;
 }
@@ -478,8 +848,8 @@ static void pc_apply(xrl_precond pc, const float2* v, float2* z, int nrhs)
         return;
     }
     xrl_tree t = pc->op->tree;
-    const int nl = (int)pc->op->topo->n_loops;
-    k_block_apply<<<pc->nblocks, kBS, 0, t->ctx->stream>>>(nl, nrhs, pc->bptr.p, pc->inv.p, v, z);
+    const int nl = (int)pc->nl_loc;
+    k_block_apply<<<pc->nblocks, kBS, 0, t->ctx->stream>>>(nl, nrhs, pc->bptr_loc.p, pc->inv.p, v, z);
     XRL_LAUNCH_CHECK();
     t->ctx->launches += 1;
 }
@@ -509,12 +879,6 @@ xrl_status xrl_operator_create(xrl_tree t, xrl_near nr, xrl_topo T, const double
     *out = nullptr;
     if (nr->tree != t || T->tree != t) { set_error("xrl_operator_create: handles from different trees"); return XRL_EPROVENANCE; }
     if (freq < 0) { set_error("xrl_operator_create: negative frequency"); return XRL_EINVAL; }
-    if (t->part_world > 1) {
-        // the loop-space vectors are not sharded: the operator feeds full [3 nrhs][n] panel vectors to the MVM
-        set_error("xrl_operator_create: the loop-space operator runs on single-rank trees only (part_world = %d)",
-                  t->part_world);
-        return XRL_EUNSUPPORTED;
-    }
     if (!zs && (!(sigma > 0) || !(zeta > 0))) { set_error("xrl_operator_create: need zs or sigma, zeta > 0"); return XRL_EINVAL; }
     API_TRY
         XRL_CUDA(cudaSetDevice(t->ctx->device));
@@ -541,6 +905,7 @@ xrl_status xrl_operator_create(xrl_tree t, xrl_near nr, xrl_topo T, const double
         }
         op->zsa.alloc(n);
         XRL_CUDA(cudaMemcpy(op->zsa.p, zf.data(), 8 * n, cudaMemcpyHostToDevice));
+        if (t->part_world > 1) build_loop_partition(op.get());  // loop-space shard of a partitioned tree
         ++T->refs;
         ++t->refs;
         *out = op.release();
@@ -566,7 +931,54 @@ xrl_status xrl_operator_apply(xrl_op op, const void* v, void* w, int32_t nrhs)
     if (v == w) { set_error("xrl_operator_apply: v and w alias"); return XRL_EINVAL; }
     API_TRY
         XRL_CUDA(cudaSetDevice(op->tree->ctx->device));
+        if (op->part) {
+            if (op->tree->ctx->world == 1) {
+                set_error("xrl_operator_apply: a virtual-rank operator runs through xrl_operator_apply_vranks");
+                return XRL_EUNSUPPORTED;
+            }
+            return op_apply_parts({op}, {(const float2*)v}, {(float2*)w}, nrhs, true);
+        }
         return op_apply(op, (const float2*)v, (float2*)w, nrhs);
+    API_CATCH
+}
+
+static xrl_status check_vrank_ops(int32_t k, const xrl_op* ops, const char* who)
+{
+    if (k < 1 || !ops) { set_error("%s: bad argument", who); return XRL_EINVAL; }
+    for (int r = 0; r < k; ++r) {
+        if (!ops[r]) { set_error("%s: null operator %d", who, r); return XRL_EINVAL; }
+        xrl_tree t = ops[r]->tree;
+        const bool one = k == 1 && !ops[r]->part;
+        if (!one && (!ops[r]->part || t->part_world != k || t->part_rank != r || t->ctx->world != 1 ||
+                     t->ctx != ops[0]->tree->ctx || ops[r]->topo->n_loops != ops[0]->topo->n_loops)) {
+            set_error("%s: operator %d is not rank %d of a %d-way partition on one single-rank context", who, r, r, k);
+            return XRL_EINVAL;
+        }
+    }
+    return XRL_OK;
+}
+
+xrl_status xrl_operator_info(xrl_op op, int64_t* loop_offset, int64_t* n_loops_local)
+{
+    if (!op) { set_error("xrl_operator_info: null operator"); return XRL_EINVAL; }
+    if (loop_offset) *loop_offset = op->part ? op->part->L0 : 0;
+    if (n_loops_local) *n_loops_local = op->part ? op->part->nlo : op->topo->n_loops;
+    return XRL_OK;
+}
+
+xrl_status xrl_operator_apply_vranks(int32_t k, const xrl_op* ops, const void* const* v, void* const* w, int32_t nrhs)
+{
+    xrl_status s = check_vrank_ops(k, ops, "xrl_operator_apply_vranks");
+    if (s) return s;
+    if (!v || !w || nrhs < 1) { set_error("xrl_operator_apply_vranks: bad argument"); return XRL_EINVAL; }
+    API_TRY
+        XRL_CUDA(cudaSetDevice(ops[0]->tree->ctx->device));
+        if (k == 1 && !ops[0]->part) return op_apply(ops[0], (const float2*)v[0], (float2*)w[0], nrhs);
+        std::vector<xrl_op> o(ops, ops + k);
+        std::vector<const float2*> vv(k);
+        std::vector<float2*> ww(k);
+        for (int r = 0; r < k; ++r) { vv[r] = (const float2*)v[r]; ww[r] = (float2*)w[r]; }
+        return op_apply_parts(o, vv, ww, nrhs, false);
     API_CATCH
 }
 
@@ -576,16 +988,26 @@ static xrl_status precond_build_blocks(xrl_op op, int32_t qkind, int32_t block_s
     xrl_topo T = op->topo;
     cudaStream_t st = t->ctx->stream;
     XRL_CUDA(cudaSetDevice(t->ctx->device));
-    const int64_t n = t->n, nl = T->n_loops;
+    const int64_t n = t->n;
+    // the blocks cover this rank's loops (all loops on a single-rank operator): no communication in the apply
+    const int64_t L0 = op->part ? op->part->L0 : 0, L1 = op->part ? op->part->L1 : T->n_loops;
     auto pc = std::make_unique<xrl_precond_s>();
     pc->op = op;
     pc->qkind = qkind;
     pc->bs = block_size;
-    for (int64_t l = 0; l < nl; l += block_size) pc->bptr_h.push_back((int32_t)l);
-    pc->bptr_h.push_back((int32_t)nl);
+    for (int64_t l = L0; l < L1; l += block_size) pc->bptr_h.push_back((int32_t)l);
+    pc->bptr_h.push_back((int32_t)L1);
     pc->nblocks = (int32_t)pc->bptr_h.size() - 1;
+    pc->nl_loc = L1 - L0;
     pc->bptr.alloc(pc->bptr_h.size());
+    pc->bptr_loc.alloc(pc->bptr_h.size());
     XRL_CUDA(cudaMemcpyAsync(pc->bptr.p, pc->bptr_h.data(), 4 * pc->bptr_h.size(), cudaMemcpyHostToDevice, st));
+    {
+        std::vector<int32_t> loc(pc->bptr_h.size());
+        for (size_t i = 0; i < loc.size(); ++i) loc[i] = (int32_t)(pc->bptr_h[i] - L0);
+        XRL_CUDA(cudaMemcpyAsync(pc->bptr_loc.p, loc.data(), 4 * loc.size(), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+    }
     DBuf<double2> dk, qd;
     if (qkind == 0) {
         // d_k = Z_s/A + j alpha P_kk; the blocks are assembled on the GPU from C = M A_t
@@ -631,6 +1053,10 @@ static xrl_status precond_build_blocks(xrl_op op, int32_t qkind, int32_t block_s
 
 static xrl_status precond_build_exact_kind(xrl_op op, int32_t qkind, xrl_precond* out)
 {
+    if (op->part) {
+        set_error("the exact Q^-1 is not sharded: partitioned operators use block-Jacobi preconditioners");
+        return XRL_EUNSUPPORTED;
+    }
     XRL_CUDA(cudaSetDevice(op->tree->ctx->device));
     auto pc = std::make_unique<xrl_precond_s>();
     pc->op = op;
@@ -761,201 +1187,325 @@ xrl_status xrl_port_currents(xrl_topo T, const void* x, int32_t nrhs, double* ip
     API_CATCH
 }
 
+// Restarted GMRES over the parts of a loop-space system: one part (single-rank operator, or this rank of a
+// multi-rank operator: partial dots all-reduced over NCCL) or k parts of a virtual-rank run (partial dots
+// summed on the host).  Every column r has its own Krylov space; all columns step together, so every
+// operator and preconditioner call is batched (reading C-A12).  Hessenberg / Givens in FP64 on the host.
+struct GPart {
+    xrl_op op;
+    xrl_precond pc;
+    const float2* b;
+    float2* x;
+    int64_t nl;
+    DBuf<float2> V, w, tmp;
+    DBuf<double2> dh;
+    DBuf<double> ds, ones;
+};
+
+static xrl_status gmres_parts(std::vector<GPart>& P, bool nccl, int32_t nrhs, const xrl_gmres_opts* opts,
+                              int32_t* iters_out, double* rre_out, double* true_rre_out, int32_t* conv_out)
+{
+    const int k = (int)P.size();
+    const int m = opts && opts->restart > 0 ? opts->restart : 50;
+    const int maxit = opts && opts->max_iters > 0 ? opts->max_iters : 2000;
+    double tol = opts ? opts->tol : 0;
+    const bool have_pc = P[0].pc != nullptr;
+    // right preconditioning (A M^-1 u = b, x = M^-1 u; default when opts is NULL, reading R15)
+    const bool right = have_pc && (!opts || opts->right_precond);
+    if (!(tol > 0)) tol = P[0].op->freq > 1e6 ? 1e-4 : 1e-6;  // PAPER.md:152, reading C-A8
+    if (tol >= 1) { set_error("xrl_gmres: tol must be < 1"); return XRL_EINVAL; }
+    xrl_ctx ctx = P[0].op->tree->ctx;
+    cudaStream_t st = ctx->stream;
+    const bool sharded = P[0].op->part != nullptr;
+    for (auto& p : P) {
+        p.V.alloc(std::max<size_t>(1, (size_t)nrhs * (m + 1) * p.nl));
+        p.w.alloc(std::max<size_t>(1, (size_t)nrhs * p.nl));
+        p.tmp.alloc(std::max<size_t>(1, (size_t)nrhs * p.nl));
+        p.dh.alloc((size_t)nrhs * (m + 1));
+        p.ds.alloc(nrhs);
+        p.ones.alloc(nrhs);
+        std::vector<double> one(nrhs, 1.0);
+        XRL_CUDA(cudaMemcpyAsync(p.ones.p, one.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
+    }
+    std::vector<double2> hh((size_t)nrhs * (m + 1)), hsum((size_t)nrhs * (m + 1));
+    using BufSel = DBuf<float2> GPart::*;
+    auto opA = [&](std::function<const float2*(GPart&)> in, std::function<float2*(GPart&)> out) -> xrl_status {
+        if (!sharded) return op_apply(P[0].op, in(P[0]), out(P[0]), nrhs);
+        std::vector<xrl_op> ops;
+        std::vector<const float2*> vi;
+        std::vector<float2*> wo;
+        for (auto& p : P) { ops.push_back(p.op); vi.push_back(in(p)); wo.push_back(out(p)); }
+        return op_apply_parts(ops, vi, wo, nrhs, nccl);
+    };
+    auto Mx = [&](GPart& p, const float2* in, float2* o) {  // o = M^-1 in (or copy)
+        if (p.pc) pc_apply(p.pc, in, o, nrhs);
+        else if (p.nl) XRL_CUDA(cudaMemcpyAsync(o, in, 8 * nrhs * p.nl, cudaMemcpyDeviceToDevice, st));
+    };
+    // h[r][i] = sum over the parts (and ranks) of conj(V_i) . w  -> host
+    auto dots = [&](std::function<const float2*(GPart&)> a, int ldv, std::function<const float2*(GPart&)> b, int ni,
+                    std::vector<double2>& out) -> xrl_status {
+        std::fill(hsum.begin(), hsum.begin() + (size_t)nrhs * ni, make_double2(0, 0));
+        for (auto& p : P) {
+            XRL_CUDA(cudaMemsetAsync(p.dh.p, 0, 16 * nrhs * ni, st));
+            if (p.nl > 0) {
+                k_gdots<<<dim3(ni, nrhs, (unsigned)((p.nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(p.nl, ldv, a(p),
+                                                                                                       b(p), p.dh.p, ni);
+                XRL_LAUNCH_CHECK();
+            }
+            if (nccl) {
+                xrl_status s = nccl_allreduce_sum_f64(ctx, (double*)p.dh.p, (size_t)2 * nrhs * ni, st);
+                if (s) return s;
+            }
+            XRL_CUDA(cudaMemcpyAsync(hh.data(), p.dh.p, 16 * nrhs * ni, cudaMemcpyDeviceToHost, st));
+            XRL_CUDA(cudaStreamSynchronize(st));
+            for (size_t i = 0; i < (size_t)nrhs * ni; ++i) { hsum[i].x += hh[i].x; hsum[i].y += hh[i].y; }
+        }
+        out.assign(hsum.begin(), hsum.begin() + (size_t)nrhs * ni);
+        return XRL_OK;
+    };
+    auto norms = [&](std::function<const float2*(GPart&)> a, std::vector<double>& out) -> xrl_status {
+        std::vector<double2> h;
+        xrl_status s = dots(a, 1, a, 1, h);
+        out.resize(nrhs);
+        for (int r = 0; r < nrhs; ++r) out[r] = std::sqrt(std::max(h[r].x, 0.0));
+        return s;
+    };
+    auto setscale = [&](const std::vector<double>& sc) {
+        for (auto& p : P) XRL_CUDA(cudaMemcpyAsync(p.ds.p, sc.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
+    };
+    auto fB = [](GPart& p) -> const float2* { return p.b; };
+    auto fX = [](GPart& p) -> float2* { return p.x; };
+    auto fW = [](GPart& p) -> float2* { return p.w.p; };
+    auto fT = [](GPart& p) -> float2* { return p.tmp.p; };
+    auto cW = [](GPart& p) -> const float2* { return p.w.p; };
+    auto cT = [](GPart& p) -> const float2* { return p.tmp.p; };
+    auto cX = [](GPart& p) -> const float2* { return p.x; };
+    (void)fX;
+    xrl_status s;
+    // reference: ||M^-1 b|| (left: preconditioned RRE) or ||b|| (right / none)
+    std::vector<double> bnorm, pbnorm;
+    if ((s = norms(fB, bnorm))) return s;
+    if (right) {
+        pbnorm = bnorm;
+    } else {
+        for (auto& p : P) Mx(p, p.b, p.tmp.p);
+        if ((s = norms(cT, pbnorm))) return s;
+    }
+    std::vector<int> iters(nrhs, 0), conv(nrhs, 0);
+    std::vector<double> rre(nrhs, 1.0);
+    for (int r = 0; r < nrhs; ++r)
+        if (bnorm[r] == 0) { conv[r] = 1; rre[r] = 0; }
+    int total = 0;
+    while (total < maxit) {
+        bool all = true;
+        for (int r = 0; r < nrhs; ++r) all = all && conv[r];
+        if (all) break;
+        // r0 = M^-1 (b - A x) (left) or b - A x (right)
+        if ((s = opA(cX, fW))) return s;
+        for (auto& p : P) {
+            if (!p.nl) continue;
+            k_gsub<<<nblk(nrhs * p.nl, 256), 256, 0, st>>>(nrhs * p.nl, p.b, p.w.p, p.tmp.p);
+            XRL_LAUNCH_CHECK();
+            if (right) XRL_CUDA(cudaMemcpyAsync(p.w.p, p.tmp.p, 8 * nrhs * p.nl, cudaMemcpyDeviceToDevice, st));
+            else Mx(p, p.tmp.p, p.w.p);
+        }
+        std::vector<double> beta;
+        if ((s = norms(cW, beta))) return s;
+        std::vector<double> sc(nrhs);
+        for (int r = 0; r < nrhs; ++r) sc[r] = beta[r] > 0 ? 1.0 / beta[r] : 0.0;
+        setscale(sc);
+        for (auto& p : P)
+            if (p.nl) {
+                k_gscale<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, nrhs, p.w.p, p.nl, p.ds.p, p.V.p, (int64_t)(m + 1) * p.nl);
+                XRL_LAUNCH_CHECK();
+            }
+        // per-column Hessenberg, Givens and residual vector (FP64 host)
+        std::vector<std::vector<cd>> H(nrhs, std::vector<cd>((m + 1) * m, 0.0));
+        std::vector<std::vector<cd>> g(nrhs, std::vector<cd>(m + 1, 0.0)), cs(nrhs, std::vector<cd>(m)), sn(nrhs, std::vector<cd>(m));
+        for (int r = 0; r < nrhs; ++r) g[r][0] = beta[r];
+        std::vector<int> jlen(nrhs, 0);
+        std::vector<int> active(nrhs);
+        for (int r = 0; r < nrhs; ++r) active[r] = !conv[r] && beta[r] > 0;
+        int j = 0;
+        for (; j < m && total < maxit; ++j, ++total) {
+            bool any = false;
+            for (int r = 0; r < nrhs; ++r) any = any || active[r];
+            if (!any) break;
+            // w = M^-1 A v_j (left) or A M^-1 v_j (right), batched over the columns
+            for (auto& p : P)
+                if (p.nl) {
+                    k_gscale<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, nrhs, p.V.p + (int64_t)j * p.nl, (int64_t)(m + 1) * p.nl,
+                                                              p.ones.p, p.tmp.p, p.nl);
+                    XRL_LAUNCH_CHECK();
+                }
+            if (right) {
+                for (auto& p : P) Mx(p, p.tmp.p, p.w.p);
+                if ((s = opA(cW, fT))) return s;
+                for (auto& p : P)
+                    if (p.nl) XRL_CUDA(cudaMemcpyAsync(p.w.p, p.tmp.p, 8 * nrhs * p.nl, cudaMemcpyDeviceToDevice, st));
+            } else {
+                if ((s = opA(cT, fW))) return s;
+                for (auto& p : P) {
+                    Mx(p, p.w.p, p.tmp.p);
+                    if (p.nl) XRL_CUDA(cudaMemcpyAsync(p.w.p, p.tmp.p, 8 * nrhs * p.nl, cudaMemcpyDeviceToDevice, st));
+                }
+            }
+            // CGS2
+            std::vector<std::vector<cd>> hcol(nrhs, std::vector<cd>(j + 2, 0.0));
+            for (int pass = 0; pass < 2; ++pass) {
+                std::vector<double2> hv;
+                if ((s = dots([](GPart& p) -> const float2* { return p.V.p; }, m + 1, cW, j + 1, hv))) return s;
+                for (int r = 0; r < nrhs; ++r)
+                    for (int i = 0; i <= j; ++i) hcol[r][i] += cd(hv[(size_t)r * (j + 1) + i].x, hv[(size_t)r * (j + 1) + i].y);
+                for (auto& p : P) {
+                    // the summed coefficients go back to every part (all ranks subtract the same projection)
+                    XRL_CUDA(cudaMemcpyAsync(p.dh.p, hv.data(), 16 * hv.size(), cudaMemcpyHostToDevice, st));
+                    if (p.nl) {
+                        k_gupdate<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, m + 1, nrhs, p.V.p, p.dh.p, j + 1, -1.f, p.w.p);
+                        XRL_LAUNCH_CHECK();
+                    }
+                }
+            }
+            std::vector<double> hn;
+            if ((s = norms(cW, hn))) return s;
+            for (int r = 0; r < nrhs; ++r) {
+                hcol[r][j + 1] = hn[r];
+                sc[r] = hn[r] > 1e-300 ? 1.0 / hn[r] : 0.0;
+            }
+            setscale(sc);
+            for (auto& p : P)
+                if (p.nl) {
+                    k_gscale<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, nrhs, p.w.p, p.nl, p.ds.p, p.V.p + (int64_t)(j + 1) * p.nl,
+                                                              (int64_t)(m + 1) * p.nl);
+                    XRL_LAUNCH_CHECK();
+                }
+            for (int r = 0; r < nrhs; ++r) {
+                if (!active[r]) continue;
+                auto& hc = hcol[r];
+                for (int i = 0; i < j; ++i) {  // apply previous rotations
+                    const cd a = hc[i], bb = hc[i + 1];
+                    hc[i] = std::conj(cs[r][i]) * a + std::conj(sn[r][i]) * bb;
+                    hc[i + 1] = -sn[r][i] * a + cs[r][i] * bb;
+                }
+                const double den = std::sqrt(std::norm(hc[j]) + std::norm(hc[j + 1]));
+                cs[r][j] = den > 0 ? hc[j] / den : 1.0;
+                sn[r][j] = den > 0 ? hc[j + 1] / den : 0.0;
+                hc[j] = den;
+                hc[j + 1] = 0;
+                g[r][j + 1] = -sn[r][j] * g[r][j];
+                g[r][j] = std::conj(cs[r][j]) * g[r][j];
+                for (int i = 0; i <= j; ++i) H[r][(size_t)i * m + j] = hc[i];
+                jlen[r] = j + 1;
+                iters[r]++;
+                rre[r] = std::abs(g[r][j + 1]) / (pbnorm[r] > 0 ? pbnorm[r] : 1.0);
+                if (rre[r] < tol || hn[r] <= 1e-300) { conv[r] = 1; active[r] = 0; }
+            }
+        }
+        // x += V y,  H y = g (upper triangular, per column)
+        std::vector<double2> hy((size_t)nrhs * m, make_double2(0, 0));
+        int jmax = 0;
+        for (int r = 0; r < nrhs; ++r) {
+            const int jl = jlen[r];
+            jmax = std::max(jmax, jl);
+            std::vector<cd> y(jl);
+            for (int i = jl - 1; i >= 0; --i) {
+                cd acc = g[r][i];
+                for (int q = i + 1; q < jl; ++q) acc -= H[r][(size_t)i * m + q] * y[q];
+                y[i] = acc / H[r][(size_t)i * m + i];
+            }
+            for (int i = 0; i < jl; ++i) hy[(size_t)r * m + i] = make_double2(y[i].real(), y[i].imag());
+        }
+        if (jmax > 0) {
+            DBuf<double2> dy((size_t)nrhs * jmax);
+            std::vector<double2> hy2((size_t)nrhs * jmax);
+            for (int r = 0; r < nrhs; ++r)
+                for (int i = 0; i < jmax; ++i) hy2[(size_t)r * jmax + i] = hy[(size_t)r * m + i];
+            XRL_CUDA(cudaMemcpyAsync(dy.p, hy2.data(), 16 * hy2.size(), cudaMemcpyHostToDevice, st));
+            for (auto& p : P) {
+                if (!p.nl) continue;
+                if (right) {  // x += M^-1 (V y)
+                    XRL_CUDA(cudaMemsetAsync(p.tmp.p, 0, 8 * nrhs * p.nl, st));
+                    k_gupdate<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, m + 1, nrhs, p.V.p, dy.p, jmax, 1.f, p.tmp.p);
+                    XRL_LAUNCH_CHECK();
+                    Mx(p, p.tmp.p, p.w.p);
+                    k_gaxpy<<<nblk(nrhs * p.nl, 256), 256, 0, st>>>(nrhs * p.nl, p.w.p, p.x);
+                    XRL_LAUNCH_CHECK();
+                } else {
+                    k_gupdate<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, m + 1, nrhs, p.V.p, dy.p, jmax, 1.f, p.x);
+                    XRL_LAUNCH_CHECK();
+                }
+            }
+            XRL_CUDA(cudaStreamSynchronize(st));
+        }
+        if (j == 0) break;
+    }
+    // true relative residual ||b - A x|| / ||b||
+    if ((s = opA(cX, fW))) return s;
+    for (auto& p : P)
+        if (p.nl) {
+            k_gsub<<<nblk(nrhs * p.nl, 256), 256, 0, st>>>(nrhs * p.nl, p.b, p.w.p, p.tmp.p);
+            XRL_LAUNCH_CHECK();
+        }
+    std::vector<double> rn;
+    if ((s = norms(cT, rn))) return s;
+    bool all = true;
+    for (int r = 0; r < nrhs; ++r) {
+        if (iters_out) iters_out[r] = iters[r];
+        if (rre_out) rre_out[r] = rre[r];
+        if (true_rre_out) true_rre_out[r] = bnorm[r] > 0 ? rn[r] / bnorm[r] : 0.0;
+        if (conv_out) conv_out[r] = conv[r];
+        all = all && conv[r];
+    }
+    (void)sizeof(BufSel);
+    return all ? XRL_OK : XRL_ENOCONV;
+}
+
 xrl_status xrl_gmres(xrl_op op, xrl_precond pc, const void* b_, void* x_, int32_t nrhs, const xrl_gmres_opts* opts,
                      int32_t* iters_out, double* rre_out, double* true_rre_out, int32_t* conv_out)
 {
     if (!op || !b_ || !x_ || nrhs < 1) { set_error("xrl_gmres: bad argument"); return XRL_EINVAL; }
-    const int m = opts && opts->restart > 0 ? opts->restart : 50;
-    const int maxit = opts && opts->max_iters > 0 ? opts->max_iters : 2000;
-    double tol = opts ? opts->tol : 0;
-    // right preconditioning (A M^-1 u = b, x = M^-1 u; default when opts is NULL, reading R15)
-    const bool right = pc && (!opts || opts->right_precond);
-    if (!(tol > 0)) tol = op->freq > 1e6 ? 1e-4 : 1e-6;  // PAPER.md:152, reading C-A8
-    if (tol >= 1) { set_error("xrl_gmres: tol must be < 1"); return XRL_EINVAL; }
+    if (pc && pc->op != op) { set_error("xrl_gmres: preconditioner built for another operator"); return XRL_EPROVENANCE; }
+    if (op->part && op->tree->ctx->world == 1) {
+        set_error("xrl_gmres: a virtual-rank operator runs through xrl_gmres_vranks");
+        return XRL_EUNSUPPORTED;
+    }
     API_TRY
-        xrl_tree t = op->tree;
-        cudaStream_t st = t->ctx->stream;
-        XRL_CUDA(cudaSetDevice(t->ctx->device));
-        const int64_t nl = op->topo->n_loops;
-        const float2* b = (const float2*)b_;
-        float2* x = (float2*)x_;
-        DBuf<float2> V((size_t)nrhs * (m + 1) * nl), w((size_t)nrhs * nl), tmp((size_t)nrhs * nl);
-        DBuf<double2> dh((size_t)nrhs * (m + 1));
-        DBuf<double> ds(nrhs), ones(nrhs);
-        {
-            std::vector<double> one(nrhs, 1.0);
-            XRL_CUDA(cudaMemcpyAsync(ones.p, one.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaSetDevice(op->tree->ctx->device));
+        std::vector<GPart> P(1);
+        P[0].op = op;
+        P[0].pc = pc;
+        P[0].b = (const float2*)b_;
+        P[0].x = (float2*)x_;
+        P[0].nl = op->part ? op->part->nlo : op->topo->n_loops;
+        return gmres_parts(P, op->part != nullptr, nrhs, opts, iters_out, rre_out, true_rre_out, conv_out);
+    API_CATCH
+}
+
+xrl_status xrl_gmres_vranks(int32_t k, const xrl_op* ops, const xrl_precond* pcs, const void* const* b,
+                            void* const* x, int32_t nrhs, const xrl_gmres_opts* opts, int32_t* iters_out,
+                            double* rre_out, double* true_rre_out, int32_t* conv_out)
+{
+    xrl_status s = check_vrank_ops(k, ops, "xrl_gmres_vranks");
+    if (s) return s;
+    if (!b || !x || nrhs < 1) { set_error("xrl_gmres_vranks: bad argument"); return XRL_EINVAL; }
+    for (int r = 0; r < k; ++r) {
+        if (!b[r] || !x[r]) { set_error("xrl_gmres_vranks: null vector %d", r); return XRL_EINVAL; }
+        if (pcs && (!pcs[r] != !pcs[0] || (pcs[r] && pcs[r]->op != ops[r]))) {
+            set_error("xrl_gmres_vranks: preconditioner %d missing or built for another operator", r);
+            return XRL_EPROVENANCE;
         }
-        std::vector<double2> hh((size_t)nrhs * (m + 1));
-        auto Mx = [&](const float2* in, float2* o) {  // o = M^-1 in (or copy)
-            if (pc) pc_apply(pc, in, o, nrhs);
-            else XRL_CUDA(cudaMemcpyAsync(o, in, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
-        };
-        auto norms = [&](const float2* a, std::vector<double>& out) {  // ||a_r||
-            XRL_CUDA(cudaMemsetAsync(dh.p, 0, 16 * nrhs, st));
-            k_gdots<<<dim3(1, nrhs, (unsigned)((nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(nl, 1, a, a, dh.p, 1);
-            XRL_LAUNCH_CHECK();
-            std::vector<double2> h(nrhs);
-            XRL_CUDA(cudaMemcpyAsync(h.data(), dh.p, 16 * nrhs, cudaMemcpyDeviceToHost, st));
-            XRL_CUDA(cudaStreamSynchronize(st));
-            out.resize(nrhs);
-            for (int r = 0; r < nrhs; ++r) out[r] = std::sqrt(std::max(h[r].x, 0.0));
-        };
-        // reference: ||M^-1 b|| (left: preconditioned RRE) or ||b|| (right / none)
-        std::vector<double> bnorm, pbnorm;
-        norms(b, bnorm);
-        if (right) {
-            pbnorm = bnorm;
-        } else {
-            Mx(b, tmp.p);
-            norms(tmp.p, pbnorm);
+    }
+    API_TRY
+        XRL_CUDA(cudaSetDevice(ops[0]->tree->ctx->device));
+        std::vector<GPart> P(k);
+        for (int r = 0; r < k; ++r) {
+            P[r].op = ops[r];
+            P[r].pc = pcs ? pcs[r] : nullptr;
+            P[r].b = (const float2*)b[r];
+            P[r].x = (float2*)x[r];
+            P[r].nl = ops[r]->part ? ops[r]->part->nlo : ops[r]->topo->n_loops;
         }
-        std::vector<int> iters(nrhs, 0), conv(nrhs, 0);
-        std::vector<double> rre(nrhs, 1.0);
-        for (int r = 0; r < nrhs; ++r)
-            if (bnorm[r] == 0) { conv[r] = 1; rre[r] = 0; }
-        int total = 0;
-        while (total < maxit) {
-            bool all = true;
-            for (int r = 0; r < nrhs; ++r) all = all && conv[r];
-            if (all) break;
-            // r0 = M^-1 (b - A x) (left) or b - A x (right)
-            xrl_status s = op_apply(op, x, w.p, nrhs);
-            if (s) return s;
-            k_gsub<<<nblk(nrhs * nl, 256), 256, 0, st>>>(nrhs * nl, b, w.p, tmp.p);
-            XRL_LAUNCH_CHECK();
-            if (right) XRL_CUDA(cudaMemcpyAsync(w.p, tmp.p, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
-            else Mx(tmp.p, w.p);
-            std::vector<double> beta;
-            norms(w.p, beta);
-            std::vector<double> sc(nrhs);
-            for (int r = 0; r < nrhs; ++r) sc[r] = beta[r] > 0 ? 1.0 / beta[r] : 0.0;
-            XRL_CUDA(cudaMemcpyAsync(ds.p, sc.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
-            k_gscale<<<nblk(nl, 256), 256, 0, st>>>(nl, nrhs, w.p, nl, ds.p, V.p, (int64_t)(m + 1) * nl);
-            XRL_LAUNCH_CHECK();
-            // per-column Hessenberg, Givens and residual vector (FP64 host)
-            std::vector<std::vector<cd>> H(nrhs, std::vector<cd>((m + 1) * m, 0.0));
-            std::vector<std::vector<cd>> g(nrhs, std::vector<cd>(m + 1, 0.0)), cs(nrhs, std::vector<cd>(m)), sn(nrhs, std::vector<cd>(m));
-            for (int r = 0; r < nrhs; ++r) g[r][0] = beta[r];
-            std::vector<int> jlen(nrhs, 0);
-            std::vector<int> active(nrhs);
-            for (int r = 0; r < nrhs; ++r) active[r] = !conv[r] && beta[r] > 0;
-            int j = 0;
-            for (; j < m && total < maxit; ++j, ++total) {
-                bool any = false;
-                for (int r = 0; r < nrhs; ++r) any = any || active[r];
-                if (!any) break;
-                // w = M^-1 A v_j (left) or A M^-1 v_j (right), batched over the columns
-                k_gscale<<<nblk(nl, 256), 256, 0, st>>>(nl, nrhs, V.p + (int64_t)j * nl, (int64_t)(m + 1) * nl,
-                                                        ones.p, tmp.p, nl);
-                XRL_LAUNCH_CHECK();
-                if (right) {
-                    Mx(tmp.p, w.p);
-                    s = op_apply(op, w.p, tmp.p, nrhs);
-                    if (s) return s;
-                    XRL_CUDA(cudaMemcpyAsync(w.p, tmp.p, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
-                } else {
-                    s = op_apply(op, tmp.p, w.p, nrhs);
-                    if (s) return s;
-                    Mx(w.p, tmp.p);
-                    XRL_CUDA(cudaMemcpyAsync(w.p, tmp.p, 8 * nrhs * nl, cudaMemcpyDeviceToDevice, st));
-                }
-                // CGS2
-                std::vector<std::vector<cd>> hcol(nrhs, std::vector<cd>(j + 2, 0.0));
-                for (int pass = 0; pass < 2; ++pass) {
-                    XRL_CUDA(cudaMemsetAsync(dh.p, 0, 16 * nrhs * (j + 1), st));
-                    k_gdots<<<dim3(j + 1, nrhs, (unsigned)((nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(
-                        nl, m + 1, V.p, w.p, dh.p, j + 1);
-                    XRL_LAUNCH_CHECK();
-                    XRL_CUDA(cudaMemcpyAsync(hh.data(), dh.p, 16 * nrhs * (j + 1), cudaMemcpyDeviceToHost, st));
-                    XRL_CUDA(cudaStreamSynchronize(st));
-                    for (int r = 0; r < nrhs; ++r)
-                        for (int i = 0; i <= j; ++i) hcol[r][i] += cd(hh[(size_t)r * (j + 1) + i].x, hh[(size_t)r * (j + 1) + i].y);
-                    k_gupdate<<<nblk(nl, 256), 256, 0, st>>>(nl, m + 1, nrhs, V.p, dh.p, j + 1, -1.f, w.p);
-                    XRL_LAUNCH_CHECK();
-                }
-                std::vector<double> hn;
-                norms(w.p, hn);
-                for (int r = 0; r < nrhs; ++r) {
-                    hcol[r][j + 1] = hn[r];
-                    sc[r] = hn[r] > 1e-300 ? 1.0 / hn[r] : 0.0;
-                }
-                XRL_CUDA(cudaMemcpyAsync(ds.p, sc.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
-                k_gscale<<<nblk(nl, 256), 256, 0, st>>>(nl, nrhs, w.p, nl, ds.p, V.p + (int64_t)(j + 1) * nl, (int64_t)(m + 1) * nl);
-                XRL_LAUNCH_CHECK();
-                for (int r = 0; r < nrhs; ++r) {
-                    if (!active[r]) continue;
-                    auto& hc = hcol[r];
-                    for (int i = 0; i < j; ++i) {  // apply previous rotations
-                        const cd a = hc[i], bb = hc[i + 1];
-                        hc[i] = std::conj(cs[r][i]) * a + std::conj(sn[r][i]) * bb;
-                        hc[i + 1] = -sn[r][i] * a + cs[r][i] * bb;
-                    }
-                    const double den = std::sqrt(std::norm(hc[j]) + std::norm(hc[j + 1]));
-                    cs[r][j] = den > 0 ? hc[j] / den : 1.0;
-                    sn[r][j] = den > 0 ? hc[j + 1] / den : 0.0;
-                    hc[j] = den;
-                    hc[j + 1] = 0;
-                    g[r][j + 1] = -sn[r][j] * g[r][j];
-                    g[r][j] = std::conj(cs[r][j]) * g[r][j];
-                    for (int i = 0; i <= j; ++i) H[r][(size_t)i * m + j] = hc[i];
-                    jlen[r] = j + 1;
-                    iters[r]++;
-                    rre[r] = std::abs(g[r][j + 1]) / (pbnorm[r] > 0 ? pbnorm[r] : 1.0);
-                    if (rre[r] < tol || hn[r] <= 1e-300) { conv[r] = 1; active[r] = 0; }
-                }
-            }
-            // x += V y,  H y = g (upper triangular, per column)
-            std::vector<double2> hy((size_t)nrhs * m, make_double2(0, 0));
-            int jmax = 0;
-            for (int r = 0; r < nrhs; ++r) {
-                const int jl = jlen[r];
-                jmax = std::max(jmax, jl);
-                std::vector<cd> y(jl);
-                for (int i = jl - 1; i >= 0; --i) {
-                    cd acc = g[r][i];
-                    for (int k = i + 1; k < jl; ++k) acc -= H[r][(size_t)i * m + k] * y[k];
-                    y[i] = acc / H[r][(size_t)i * m + i];
-                }
-                for (int i = 0; i < jl; ++i) hy[(size_t)r * m + i] = make_double2(y[i].real(), y[i].imag());
-            }
-            if (jmax > 0) {
-                DBuf<double2> dy((size_t)nrhs * jmax);
-                std::vector<double2> hy2((size_t)nrhs * jmax);
-                for (int r = 0; r < nrhs; ++r)
-                    for (int i = 0; i < jmax; ++i) hy2[(size_t)r * jmax + i] = hy[(size_t)r * m + i];
-                XRL_CUDA(cudaMemcpyAsync(dy.p, hy2.data(), 16 * hy2.size(), cudaMemcpyHostToDevice, st));
-                if (right) {  // x += M^-1 (V y)
-                    XRL_CUDA(cudaMemsetAsync(tmp.p, 0, 8 * nrhs * nl, st));
-                    k_gupdate<<<nblk(nl, 256), 256, 0, st>>>(nl, m + 1, nrhs, V.p, dy.p, jmax, 1.f, tmp.p);
-                    XRL_LAUNCH_CHECK();
-                    Mx(tmp.p, w.p);
-                    k_gaxpy<<<nblk(nrhs * nl, 256), 256, 0, st>>>(nrhs * nl, w.p, x);
-                    XRL_LAUNCH_CHECK();
-                } else {
-                    k_gupdate<<<nblk(nl, 256), 256, 0, st>>>(nl, m + 1, nrhs, V.p, dy.p, jmax, 1.f, x);
-                    XRL_LAUNCH_CHECK();
-                }
-                XRL_CUDA(cudaStreamSynchronize(st));
-            }
-            if (j == 0) break;
-        }
-        // true relative residual ||b - A x|| / ||b||
-        xrl_status s = op_apply(op, x, w.p, nrhs);
-        if (s) return s;
-        k_gsub<<<nblk(nrhs * nl, 256), 256, 0, st>>>(nrhs * nl, b, w.p, tmp.p);
-        XRL_LAUNCH_CHECK();
-        std::vector<double> rn;
-        norms(tmp.p, rn);
-        bool all = true;
-        for (int r = 0; r < nrhs; ++r) {
-            if (iters_out) iters_out[r] = iters[r];
-            if (rre_out) rre_out[r] = rre[r];
-            if (true_rre_out) true_rre_out[r] = bnorm[r] > 0 ? rn[r] / bnorm[r] : 0.0;
-            if (conv_out) conv_out[r] = conv[r];
-            all = all && conv[r];
-        }
-        return all ? XRL_OK : XRL_ENOCONV;
+        return gmres_parts(P, false, nrhs, opts, iters_out, rre_out, true_rre_out, conv_out);
     API_CATCH
 }
 

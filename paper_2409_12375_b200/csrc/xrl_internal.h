@@ -237,6 +237,25 @@ struct xrl_topo_s {
     int32_t n_long = 0;
 };
 
+namespace xrl {
+// Loop-space sharding of a partitioned operator (solver.cu build_loop_partition; SURVEY §8(e) "GMRES
+// extras"): this rank owns the contiguous loops [L0, L1) (cuts balanced by the owner of each loop's first
+// panel) and the tree's panels [p0, p1); an apply exchanges the loop values its owned panels read (loop
+// halo) and the panel values its owned loops read (panel halo).
+struct LoopPart {
+    int64_t L0 = 0, L1 = 0, nlo = 0, nlh = 0, npl = 0, nph = 0;  // owned / halo loops, owned / halo panels
+    std::vector<int64_t> lcut;                     // [world+1] loop cuts
+    std::vector<int64_t> lh_soff, lh_roff, ph_soff, ph_roff;  // [world+1] per-peer offsets
+    DBuf<int32_t> lh_sidx, ph_sidx;                // owned loops (- L0) / owned panels (- p0) peers read
+    DBuf<int64_t> pl_ptr, lp_ptr;                  // owned panel -> loop slots, owned loop -> panel slots
+    DBuf<int32_t> pl_col, lp_col, lp_long;
+    DBuf<float> pl_val, lp_val;                    // C_t values, 3 per entry
+    int32_t n_long = 0;
+    DBuf<float2> vext, yext, u, pu, sbuf, rbuf;    // scratch
+    int cap = 0;
+};
+}  // namespace xrl
+
 struct xrl_op_s {
     xrl_tree tree = nullptr;
     xrl_near near = nullptr;
@@ -247,6 +266,7 @@ struct xrl_op_s {
     xrl::DBuf<float2> zsa;                       // device copy
     xrl::DBuf<float2> u, pu;                     // scratch [3*nrhs][n]
     int32_t cap_rhs = 0;
+    std::unique_ptr<xrl::LoopPart> part;         // partitioned tree: the loop-space shard (else null)
 };
 
 struct xrl_precond_s {
@@ -256,7 +276,9 @@ struct xrl_precond_s {
     void* exact = nullptr;                       // kind 1: factorisation state
     int32_t bs = 64, nblocks = 0;
     std::vector<int32_t> bptr_h;
-    xrl::DBuf<int32_t> bptr;
+    xrl::DBuf<int32_t> bptr;                     // block starts (global loop ids, assembly)
+    xrl::DBuf<int32_t> bptr_loc;                 // the same relative to the rank's first loop (apply)
+    int64_t nl_loc = 0;                          // loops of the vectors the apply sees
     xrl::DBuf<float2> inv;                       // [nblocks][bs][bs]
 };
 
@@ -289,5 +311,6 @@ void add_into(int64_t cnt, const float* a, float* acc, cudaStream_t st);
 xrl_status nccl_exchange(xrl_ctx ctx, const float* sbuf, const std::vector<int64_t>& soff, float* rbuf,
                          const std::vector<int64_t>& roff, int rec_floats, cudaStream_t st);
 xrl_status nccl_allreduce_sum(xrl_ctx ctx, float* buf, size_t count, cudaStream_t st);
+xrl_status nccl_allreduce_sum_f64(xrl_ctx ctx, double* buf, size_t count, cudaStream_t st);
 void tree_release(xrl_tree t);
 }  // namespace xrl

@@ -28,7 +28,8 @@ EXPORTS = [
     "xrl_timing_name", "xrl_timing_get", "xrl_timing_reset", "xrl_launch_count", "xrl_ctx_set_sched", "xrl_ctx_set_fuse", "xrl_extract",
     "xrl_topology_build", "xrl_topology_info", "xrl_topology_export", "xrl_topology_destroy", "xrl_esi",
     "xrl_operator_create", "xrl_operator_apply", "xrl_operator_destroy", "xrl_precond_build",
-    "xrl_precond_build_exact", "xrl_precond_build_kind", "xrl_precond_apply", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
+    "xrl_precond_build_exact", "xrl_precond_build_kind", "xrl_precond_apply", "xrl_operator_info",
+    "xrl_operator_apply_vranks", "xrl_gmres_vranks", "xrl_precond_export", "xrl_precond_destroy", "xrl_gmres", "xrl_port_rhs",
     "xrl_port_currents", "xrl_partition_cuts", "xrl_nccl_unique_id", "xrl_mvm_vranks", "xrl_exchange_info", "xrl_plan_exchange",
 ]
 
@@ -147,6 +148,11 @@ def lib():
         L.xrl_precond_build.argtypes = [P, i32, pp]
         L.xrl_precond_build_exact.argtypes = [P, pp]
         L.xrl_precond_build_kind.argtypes = [P, i32, i32, pp]
+        L.xrl_operator_info.argtypes = [P, P, P]
+        L.xrl_operator_apply_vranks.argtypes = [i32, P, P, P, i32]
+        L.xrl_gmres_vranks.argtypes = [i32, P, P, P, P, i32, P, P, P, P, P]
+        for name in ("xrl_operator_info", "xrl_operator_apply_vranks", "xrl_gmres_vranks"):
+            getattr(L, name).restype = ctypes.c_int32
         L.xrl_precond_apply.argtypes = [P, P, P, i32]
         L.xrl_precond_export.argtypes = [P, P, P, P, P]
         L.xrl_precond_destroy.argtypes = [P]
@@ -615,6 +621,12 @@ class Operator:
         check(lib().xrl_operator_apply(self.h, _ptr(v), _ptr(w), v.shape[0]))
         return w
 
+    def loops(self):
+        """(first loop, count) of this rank's loop slice (0, n_loops on a single-rank operator)."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().xrl_operator_info(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return int(a.value), int(b.value)
+
     def close(self):
         if getattr(self, "h", None):
             lib().xrl_operator_destroy(self.h)
@@ -686,6 +698,38 @@ def gmres(op: Operator, pc, b, x=None, restart=50, max_iters=2000, tol=0.0, righ
                          _ptr(conv))
     check(st)
     return x, {"iters": iters, "rre": rre, "true_rre": trre, "converged": conv.astype(bool), "status": st}
+
+
+def operator_apply_vranks(ops, vs, ws=None):
+    """xrl_operator_apply_vranks: the sharded loop-space operator of k virtual ranks; vs[r] rank r's slice."""
+    import torch
+    k = len(ops)
+    ws = [torch.empty_like(v) for v in vs] if ws is None else ws
+    oh = (ctypes.c_void_p * k)(*[o.h.value for o in ops])
+    vp = (ctypes.c_void_p * k)(*[v.data_ptr() for v in vs])
+    wp = (ctypes.c_void_p * k)(*[w.data_ptr() for w in ws])
+    check(lib().xrl_operator_apply_vranks(k, oh, vp, wp, vs[0].shape[0]))
+    return ws
+
+
+def gmres_vranks(ops, pcs, bs, xs=None, restart=50, max_iters=2000, tol=0.0, right=True):
+    """xrl_gmres_vranks: GMRES of k virtual ranks (slices bs[r], xs[r]); returns (xs, report)."""
+    import torch
+    k = len(ops)
+    xs = [torch.zeros_like(b) for b in bs] if xs is None else xs
+    nrhs = bs[0].shape[0]
+    iters = np.zeros(nrhs, np.int32)
+    rre = np.zeros(nrhs)
+    trre = np.zeros(nrhs)
+    conv = np.zeros(nrhs, np.int32)
+    oh = (ctypes.c_void_p * k)(*[o.h.value for o in ops])
+    ph = (ctypes.c_void_p * k)(*[p.h.value for p in pcs]) if pcs is not None else None
+    bp = (ctypes.c_void_p * k)(*[b.data_ptr() for b in bs])
+    xp = (ctypes.c_void_p * k)(*[x.data_ptr() for x in xs])
+    st = lib().xrl_gmres_vranks(k, oh, ph, bp, xp, nrhs, ctypes.byref(GmresOpts(restart, max_iters, tol, int(right))),
+                                _ptr(iters), _ptr(rre), _ptr(trre), _ptr(conv))
+    check(st)
+    return xs, {"iters": iters, "rre": rre, "true_rre": trre, "converged": conv.astype(bool), "status": st}
 
 
 def extract(tree: Tree, near: Near, topo: Topology, freqs, zs=None, sigma=5.8e7, zeta=1e-4, block_size=64,

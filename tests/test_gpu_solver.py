@@ -505,3 +505,57 @@ def test_diag_p_vs_diag_l_iterations(coils_all):
     print("Table IV analogue (coils, 100 MHz, tol 1e-6): iterations", it)
     assert it["diag_p"] <= it["diag_l"]
     assert np.abs(zz["diag_p"] - zz["diag_l"]).max() / np.abs(zz["diag_p"]).max() < 1e-3
+
+
+@pytest.mark.parametrize("cfg,world", [(1, 2), (1, 3), (2, 4)])
+def test_sharded_operator_and_gmres_virtual_ranks(cfg, world):
+    """SURVEY §8(e) "GMRES extras" on one GPU (virtual ranks): k operators on the k trees of a partition own
+    contiguous loop slices; the sharded apply (loop halo -> C^T v -> sharded MVM -> panel halo -> C y) equals
+    the single-GPU operator, block preconditioners stay rank-local, and GMRES with the inner products summed
+    over the ranks gives the single-GPU port impedance in a comparable number of iterations."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m = meshes.make_config(cfg)
+    ports = [(p, q) for _, p, q in m.ports]
+    leaf = 64
+    ctx, tree, near = cuda_setup(m, leaf_max=leaf)
+    topo = xrl.Topology(tree, ports)
+    f = 1e8
+    zeta = ZETA if cfg == 1 else 5e-6
+    op = xrl.Operator(tree, near, topo, f, sigma=SIGMA, zeta=zeta)
+    nl = topo.n_loops
+    ops, trees, nears, topos = [], [], [], []
+    for r in range(world):
+        tr = xrl.Tree(ctx, m.verts, m.tris, leaf_max=leaf, part_rank=r, part_world=world)
+        nr = xrl.Near(tr)
+        tp = xrl.Topology(tr, ports)
+        trees.append(tr)
+        nears.append(nr)
+        topos.append(tp)
+        ops.append(xrl.Operator(tr, nr, tp, f, sigma=SIGMA, zeta=zeta))
+    sl = [o.loops() for o in ops]
+    assert sl[0][0] == 0 and sum(c for _, c in sl) == nl
+    assert all(sl[i][0] + sl[i][1] == sl[i + 1][0] for i in range(world - 1))
+    rng = np.random.default_rng(31)
+    v = torch.from_numpy((rng.random((2, nl)) - 0.5 + 1j * (rng.random((2, nl)) - 0.5)).astype(np.complex64)).cuda()
+    w_ref = op.apply(v).cpu().numpy()
+    vs = [v[:, a:a + c].contiguous() for a, c in sl]
+    w = torch.cat(xrl.operator_apply_vranks(ops, vs), dim=1).cpu().numpy()
+    err = oracle.rel_l2(w, w_ref)
+    print("sharded operator", cfg, world, err, sl)
+    assert err < 1e-6
+    # GMRES on the port excitations: single GPU vs virtual ranks
+    b = torch.zeros((len(ports), nl), dtype=torch.complex64, device="cuda")
+    for p in range(len(ports)):
+        topo.port_rhs(p, 1.0, out=b[p:p + 1])
+    x1, rep1 = xrl.gmres(op, xrl.Precond(op, 64), b)
+    pcs = [xrl.Precond(o, 64) for o in ops]
+    bs = [b[:, a:a + c].contiguous() for a, c in sl]
+    xs, rep = xrl.gmres_vranks(ops, pcs, bs)
+    x = torch.cat(xs, dim=1)
+    print("gmres single", rep1["iters"], rep1["true_rre"], "sharded", rep["iters"], rep["true_rre"])
+    assert rep["converged"].all() and np.all(rep["true_rre"] < 10 * (1e-6 if f <= 1e6 else 1e-4))
+    z1 = np.linalg.inv(topo.port_currents(x1).T)
+    zk = np.linalg.inv(topo.port_currents(x).T)
+    assert np.abs(zk - z1).max() / np.abs(z1).max() < 1e-3
+    assert abs(int(rep["iters"].max()) - int(rep1["iters"].max())) <= max(3, rep1["iters"].max() // 5)
