@@ -269,6 +269,40 @@ def leaf64_line(xrl, mesh, x_user, ctx, dev, flush, args):
     return out
 
 
+def multi_gpu_projection(xrl, mesh, ctx, x_lib, ms_1gpu, args, k=8):
+    """Projected k-GPU time of the sharded MVM from k virtual ranks on this GPU (tools/vrank_projection.py
+    has the full sweep): each rank's phase groups timed alone on the GPU with the production
+    schedule through xrl_mvm_vranks (the same plans, exchanges and kernels as the NCCL path), plus the
+    exchange volume over NVLink 5 (900 GB/s per direction) and 15 us latency per exchange (3 exchanges)."""
+    import numpy as np
+    import torch
+    trees, nears, xs, off = [], [], [], 0
+    for r in range(k):
+        tr = xrl.Tree(ctx, mesh.verts, mesh.tris, leaf_max=args.leaf, part_rank=r, part_world=k)
+        trees.append(tr)
+        nears.append(xrl.Near(tr))
+        xs.append(x_lib[:, off:off + tr.n_local].contiguous())
+        off += tr.n_local
+    ys = [torch.empty_like(v) for v in xs]
+    for _ in range(2):
+        xrl.mvm_vranks(trees, nears, xs, ys)
+    runs = [xrl.mvm_vranks(trees, nears, xs, ys, timing=True)[1] for _ in range(5)]
+    rank_ms = np.median(np.array(runs), axis=0)
+    info = [xrl.exchange_info(t, n) for t, n in zip(trees, nears)]
+    byts = [32 * (i["halo_send"] + i["halo_recv"]) + 3072 * (i["let_send"] + i["let_recv"]) + 2 * 3072 * i["shared"]
+            for i in info]
+    comm_ms = 1e3 * (max(byts) / 900e9 + 3 * 15e-6)
+    t_k = float(rank_ms.max()) + comm_ms
+    out = {"k": k, "projected_ms": t_k, "rank_ms": [round(float(v), 4) for v in rank_ms], "comm_ms": comm_ms,
+           "max_rank_bytes": int(max(byts)), "speedup_vs_1gpu": ms_1gpu / t_k,
+           "projected_value": mesh.n / (t_k * 1e-3) / 1e6, "unit": "Mpanels/s",
+           "how": "virtual ranks on one GPU (xrl_mvm_vranks), max over ranks + exchange bytes / 900 GB/s + 3 x 15 us; "
+                  "a projection, not a multi-GPU measurement"}
+    del ys, xs, nears, trees
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_xrl(args):
     import numpy as np
     import torch
@@ -514,6 +548,8 @@ def run_xrl(args):
         line["gmres"] = gmres_iteration_time(xrl, tree, near, args)
     if world == 1 and not args.no_leaf64 and args.leaf != 64:
         line["leaf64"] = leaf64_line(xrl, mesh, x_user, ctx, dev, flush, args)
+    if world == 1 and args.project > 1:
+        line["multi_gpu_projection"] = multi_gpu_projection(xrl, mesh, ctx, x_lib, ms_per_step, args, args.project)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(mesh, x_user)
     if rank == 0:
@@ -534,6 +570,7 @@ def main():
     ap.add_argument("--leaf", type=int, default=352)  # tuned for config 4
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-leaf64", action="store_true", help="skip the leaf-64 line (N=1)")
+    ap.add_argument("--project", type=int, default=8, help="virtual-rank projection to this many GPUs (N=1; 0 = off)")
     ap.add_argument("--gmres-iters", type=int, default=20, help="GMRES iteration-time probe (N=1); 0 = off")
     ap.add_argument("--gmres-solve", type=int, default=0, help="also solve to tolerance with this iteration cap")
     args = ap.parse_args()

@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             int4 bk = __ldg(blocks + bi);
             bk.y = __shfl_sync(0xffffffffu, bk.y, 0);  // warp-uniform (keeps the MMA operands in uniform registers)
             bk.z = __shfl_sync(0xffffffffu, bk.z, 0);
+            if (bk.y <= 0) { --nb; continue; }  // padding block of the balanced order: no operator load
             if (j > 0) {  // every MMA reading the previous operator must be complete
                 mbar_wait_warp(&d_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc::fence_after();
@@ -1318,7 +1319,7 @@ static void mvm_down(Mvm& M)
         if (!M.side_done) mvm_side(M);  // XRL_SCHED_LATE, or the virtual-rank driver
         phase_begin(ctx, PH_M2L, &ev, M.st);
         if (t->n_m2l_tiles > 0) {
-            const int grid = std::min(ctx->num_sms, t->n_m2l_blocks);
+            const int grid = t->m2l_grid;  // the grid the block order was balanced for (tree.cu)
             P2PTasks tasks{};
             if (M.fuse)
                 tasks = P2PTasks{t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
@@ -1522,10 +1523,21 @@ xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* near
         XRL_CUDA(cudaSetDevice(ctx->device));
         if (rank_ms) for (int r = 0; r < k; ++r) rank_ms[r] = 0;
         if (exch_ms) *exch_ms = 0;
-        // serial schedule per rank (its kernels in order on the context stream) so each rank's device time is
-        // measured alone, as if it had the GPU to itself; the exchanges are device copies on the same stream
-        const int sched_saved = ctx->sched;
-        ctx->sched = XRL_SCHED_SERIAL;
+        // The ranks' phase groups run one after the other with the context's schedule (default: the forked /
+        // fused one a real rank uses); each group forks from and joins back into the context stream, so its
+        // events there bracket that rank's work alone on the GPU.  The exchanges are device copies on the
+        // context stream between the groups.
+        const int sched = ctx->sched;
+        auto fork = [&]() {
+            if (!sched) return;
+            XRL_CUDA(cudaEventRecord(ctx->ev_work, ctx->stream));
+            XRL_CUDA(cudaStreamWaitEvent(ctx->work, ctx->ev_work, 0));
+        };
+        auto join = [&]() {
+            if (!sched) return;
+            XRL_CUDA(cudaEventRecord(ctx->ev_work, ctx->work));
+            XRL_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_work, 0));
+        };
         VTimer tm{ctx, rank_ms != nullptr || exch_ms != nullptr};
         std::vector<double> ms(k + 1, 0.0);
         cudaStream_t st = ctx->stream;
@@ -1534,14 +1546,16 @@ xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* near
             std::vector<Mvm> Ms;
             for (int r = 0; r < k; ++r) {
                 const int64_t nl = trees[r]->p1 - trees[r]->p0;
-                Ms.push_back(mvm_make(trees[r], nears[r], (float2*)y[r] + (size_t)v * nl, flags, XRL_SCHED_SERIAL));
+                Ms.push_back(mvm_make(trees[r], nears[r], (float2*)y[r] + (size_t)v * nl, flags,
+                                      sched == XRL_SCHED_LATE ? XRL_SCHED_FORK : sched));
             }
             const bool dist = k > 1;
             for (int r = 0; r < k; ++r) {
                 const int64_t nl = trees[r]->p1 - trees[r]->p0;
                 tm.begin();
-                mvm_begin(Ms[r], (const float2*)x[r] + (size_t)v * nl);
+                mvm_begin(Ms[r], (const float2*)x[r] + (size_t)v * nl);  // (forks the work stream)
                 if (dist) halo_pack(Ms[r]);
+                join();
                 tm.end(r);
             }
             if (dist) {
@@ -1555,9 +1569,11 @@ xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* near
             }
             for (int r = 0; r < k; ++r) {
                 tm.begin();
+                fork();
                 if (dist) halo_unpack(Ms[r]);
                 mvm_up(Ms[r]);
                 if (dist && Ms[r].chain) mu_pack(Ms[r]);
+                join();
                 tm.end(r);
             }
             if (dist && Ms[0].chain) {
@@ -1574,7 +1590,9 @@ xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* near
                 if (s) break;
                 for (int r = 0; r < k; ++r) {
                     tm.begin();
+                    fork();
                     mu_shared_unpack_let_pack(Ms[r]);
+                    join();
                     tm.end(r);
                 }
                 tm.begin();
@@ -1587,13 +1605,13 @@ xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* near
             }
             for (int r = 0; r < k; ++r) {
                 tm.begin();
+                fork();
                 if (dist && Ms[r].chain) let_unpack(Ms[r]);
-                mvm_down(Ms[r]);
+                mvm_down(Ms[r]);  // (joins the side and work streams back into the context stream)
                 tm.end(r);
             }
         }
         tm.collect(ms.data());
-        ctx->sched = sched_saved;
         if (rank_ms) for (int r = 0; r < k; ++r) rank_ms[r] = ms[r];
         if (exch_ms) *exch_ms = ms[k];
         return s;

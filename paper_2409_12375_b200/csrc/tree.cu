@@ -488,6 +488,38 @@ void exclusive_scan(const T* in, T* out, int64_t n, cudaStream_t st)
 
 inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
+// Static load balance of the persistent translation kernel (k_m2l_tc): CTA c of a grid of G takes blocks
+// c, c + G, c + 2G, ...  Blocks (first tile, #tiles, operator, chunk) are assigned to the G CTAs by
+// longest-processing-time (weight: its tiles + 1 for the 128 KB operator load), chunk after chunk so that
+// all CTAs stay inside one L2-resident target chunk, and laid out in that strided order, padded with empty
+// blocks (0 tiles; the kernel skips them).  Round-robin over runs of 1-16 tiles left the last CTA with up
+// to twice the mean on small (per-rank) workloads.
+std::vector<int4> balance_blocks(const std::vector<int4>& blocks, int G)
+{
+    if (blocks.empty() || G <= 1) return blocks;
+    std::vector<std::vector<int4>> per(G);
+    std::vector<int64_t> load(G, 0);
+    size_t i = 0;
+    while (i < blocks.size()) {
+        size_t j = i;
+        while (j < blocks.size() && blocks[j].w == blocks[i].w) ++j;  // one chunk
+        std::vector<int4> ch(blocks.begin() + i, blocks.begin() + j);
+        std::stable_sort(ch.begin(), ch.end(), [](const int4& a, const int4& b) { return a.y > b.y; });
+        for (const int4& bk : ch) {
+            const int c = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+            per[c].push_back(bk);
+            load[c] += bk.y + 1;
+        }
+        i = j;
+    }
+    size_t len = 0;
+    for (auto& v : per) len = std::max(len, v.size());
+    std::vector<int4> out(len * G, make_int4(0, 0, 0, 0));
+    for (int c = 0; c < G; ++c)
+        for (size_t q = 0; q < per[c].size(); ++q) out[q * G + c] = per[c][q];
+    return out;
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------- build
@@ -917,6 +949,11 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
                 }
                 i = j;
             }
+            // balance this level's blocks over its persistent grid (translate_level: min(num_sms, #blocks))
+            std::vector<int4> lvl(blocks.begin() + first_block, blocks.end());
+            lvl = balance_blocks(lvl, std::min<int>(ctx->num_sms, (int)lvl.size()));
+            blocks.resize(first_block);
+            blocks.insert(blocks.end(), lvl.begin(), lvl.end());
             return std::make_pair(first_block, (int)blocks.size() - first_block);
         };
         T->m2m_lvl.assign(nlev, {0, 0});
@@ -1000,6 +1037,8 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         T->m2l_tiles.alloc(std::max<size_t>(1, tiles.size()));
         if (!tiles.empty())
             XRL_CUDA(cudaMemcpyAsync(T->m2l_tiles.p, tiles.data(), sizeof(int4) * tiles.size(), cudaMemcpyHostToDevice, st));
+        T->m2l_grid = std::min<int>(ctx->num_sms, (int)blocks.size());
+        blocks = balance_blocks(blocks, T->m2l_grid);
         T->n_m2l_blocks = (int)blocks.size();
         T->m2l_blocks.alloc(std::max<size_t>(1, blocks.size()));
         if (!blocks.empty())

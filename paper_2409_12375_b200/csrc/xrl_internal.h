@@ -142,7 +142,8 @@ struct xrl_tree_s {
     xrl::DBuf<int4> m2l_tiles;               // (offset, pair begin, pair count <= 21, chunk)
     int32_t n_m2l_tiles = 0;
     xrl::DBuf<int4> m2l_blocks;              // (first tile, #tiles, offset, chunk): runs of one operator
-    int32_t n_m2l_blocks = 0;
+    int32_t n_m2l_blocks = 0;                // (padded: balance_blocks in tree.cu)
+    int32_t m2l_grid = 0;                    // persistent grid the block order is balanced for
     // M2M / L2L translation tiles for the tensor-core kernel (all levels concatenated)
     xrl::DBuf<int4> tr_tiles, tr_blocks;
     xrl::DBuf<int32_t> tr_tgt, tr_src;

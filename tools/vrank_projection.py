@@ -2,14 +2,14 @@
 
 Only one B200 is available to this build, so the k-GPU time is projected from measurements of the real
 sharded code path: k trees partitioned 0..k-1 of the same mesh run through xrl_mvm_vranks (the same
-plans, exchanges and kernels as the multi-rank xrl_mvm; exchanges as device copies).  Each rank's phases
-run alone on the whole GPU (serial schedule), so its measured device time is what one GPU would spend on
-that rank's share.  The projection is
+plans, exchanges and kernels as the multi-rank xrl_mvm; exchanges as device copies).  Each rank's phase
+groups run alone on the whole GPU with the production (forked, fused) schedule, so its measured device
+time is what one GPU would spend on that rank's share.  The projection is
     t(k) = max_r t_rank(r) + t_comm(k),
     t_comm = max_r (bytes sent + received by r) / 900 GB/s (NVLink 5 per direction) + 3 x 15 us
              (three dependent exchanges: halo, shared all-reduce, LET; latency per exchange),
 with no overlap of communication and compute assumed (conservative).  The single-GPU references are the
-same serial schedule at k = 1 and the default (forked, fused) schedule of xrl_mvm.
+same driver at k = 1 and xrl_mvm itself.
 
     python tools/vrank_projection.py [--config 4] [--leaf 352] [--ks 1,2,4,8] [--reps 5] [--out file.json]
 """
@@ -83,6 +83,13 @@ def main():
             _, rms, ems = xrl.mvm_vranks(trees, nears, xs, ys, timing=True)
             rank_ms.append(rms)
             exch_ms.append(ems)
+        # per-phase device times (event spans per phase, summed over the ranks, per rank on average)
+        ctx.timing_reset()
+        ctx.timing_enable(True)
+        xrl.mvm_vranks(trees, nears, xs, ys)
+        torch.cuda.synchronize()
+        ctx.timing_enable(False)
+        phases = {kk: vv[0] / k for kk, vv in ctx.timing().items()}
         rank_med = np.median(np.array(rank_ms), axis=0)
         info = [xrl.exchange_info(t, n) for t, n in zip(trees, nears)]
         byts = [32 * (i["halo_send"] + i["halo_recv"]) + 3072 * (i["let_send"] + i["let_recv"]) +
@@ -94,7 +101,7 @@ def main():
                         "imbalance": float(rank_med.max() / rank_med.mean()),
                         "n_local": [t.n_local for t in trees], "exchange": info, "bytes_per_rank": byts,
                         "t_comm_ms": 1e3 * comm_s, "exchange_copy_ms_on_one_gpu": float(np.median(exch_ms)),
-                        "t_projected_ms": t_k, "setup_s": round(setup, 2)}
+                        "t_projected_ms": t_k, "setup_s": round(setup, 2), "phases_ms_per_rank": phases}
         print(json.dumps({k: res["ks"][k]}), flush=True)
         del ys, xs, nears, trees
         torch.cuda.empty_cache()
