@@ -223,10 +223,11 @@ xrl_status xrl_mvm(xrl_tree tree, xrl_near near, const void* x, void* y, int32_t
  * multi-rank xrl_mvm; the exchanges are device copies between the trees'
  * buffers instead of NCCL.  x[r], y[r]: device complex64 [nvec][n_local(r)]
  * (rank r's slice in library order).  The ranks' phases are serialised on the
- * context stream; rank_ms (host double [k], may be NULL) receives each rank's
- * device time (its kernels alone on the GPU, summed over the phases) and
- * exch_ms (may be NULL) the device-copy time of the exchanges -- the inputs of
- * the multi-GPU projection.  k = 1 with an unpartitioned tree
+ * context stream.  rank_ms (host double [k], may be NULL) receives each rank's
+ * device time: a timing pass before the real one runs each rank's whole MVM
+ * alone on the GPU in the multi-rank order (P2P forked early), the three
+ * transports left out; exch_ms (may be NULL) receives the device-copy time of
+ * the exchanges -- the inputs of the multi-GPU projection.  k = 1 with an unpartitioned tree
  * is the plain MVM.  Errors: XRL_EINVAL (trees not one k-way partition,
  * aliasing), XRL_EPROVENANCE (near/tree or context mismatch), XRL_EDIM. */
 xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* nears, const void* const* x,

@@ -1538,10 +1538,37 @@ xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* near
             XRL_CUDA(cudaEventRecord(ctx->ev_work, ctx->work));
             XRL_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_work, 0));
         };
-        VTimer tm{ctx, rank_ms != nullptr || exch_ms != nullptr};
+        VTimer tm{ctx, exch_ms != nullptr || (rank_ms && k == 1)};
         std::vector<double> ms(k + 1, 0.0);
         cudaStream_t st = ctx->stream;
         xrl_status s = XRL_OK;
+        if (rank_ms && k > 1) {
+            // timing pass (before the real one, whose results it does not touch): each rank's whole MVM alone on
+            // the GPU in the production order -- pack, halo unpack, P2P forked early onto the side stream, up
+            // pass, multipole unpack/pack, down pass -- with the three transports left out (their receive
+            // buffers hold whatever the previous call left: the work is data-independent); the transports are
+            // timed in the real pass (exch_ms) and modelled over NVLink by the projection
+            VTimer rt{ctx, true};
+            for (int r = 0; r < k; ++r) {
+                Mvm M = mvm_make(trees[r], nears[r], (float2*)y[r], flags, sched);
+                rt.begin();
+                mvm_begin(M, (const float2*)x[r]);
+                halo_pack(M);
+                halo_unpack(M);
+                if (M.sched != XRL_SCHED_LATE || !M.chain) mvm_side(M);
+                mvm_up(M);
+                if (M.chain) {
+                    mu_pack(M);
+                    mu_shared_unpack_let_pack(M);
+                    let_unpack(M);
+                }
+                mvm_down(M);
+                rt.end(r);
+            }
+            std::vector<double> rms(k + 1, 0.0);
+            rt.collect(rms.data());
+            for (int r = 0; r < k; ++r) rank_ms[r] = rms[r] * (nvec / 3);
+        }
         for (int v = 0; v < nvec && !s; v += 3) {
             std::vector<Mvm> Ms;
             for (int r = 0; r < k; ++r) {
@@ -1612,7 +1639,7 @@ xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* near
             }
         }
         tm.collect(ms.data());
-        if (rank_ms) for (int r = 0; r < k; ++r) rank_ms[r] = ms[r];
+        if (rank_ms && k == 1) rank_ms[0] = ms[0];
         if (exch_ms) *exch_ms = ms[k];
         return s;
     } catch (const CudaError& e) {

@@ -857,7 +857,9 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
             for (int64_t q = hup[L]; q < hup[L + 1]; ++q) src += hpe[hus[q]] - hpb[hus[q]];
             double m2l = 0;
             for (int a = L; a >= 0; a = hpar[a]) m2l += double(hvp[a + 1] - hvp[a]) * nL / double(hpe[a] - hpb[a]);
-            w[i] = 20.0 * nL * src + 175692.0 * m2l + 4000.0 * nL;
+            // measured device costs on config 4 (B200, leaf 352), in units of one P2P pair (0.52 ns): an M2L
+            // translation on tcgen05 ~1.04 us = 2,000 pairs; P2M + L2P + near rows of a panel ~0.67 ns = 1.3 pairs
+            w[i] = nL * src + 2000.0 * m2l + 1.3 * nL;
         }
         std::vector<int64_t> cuts(T->part_world + 1);
         xrl_partition_cuts((int64_t)w.size(), w.data(), T->part_world, cuts.data());

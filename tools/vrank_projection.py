@@ -108,7 +108,7 @@ def main():
     t1 = res["ks"].get(1, {}).get("t_projected_ms")
     for k, v in res["ks"].items():
         if t1:
-            v["speedup_vs_serial_k1"] = t1 / v["t_projected_ms"]
+            v["speedup_vs_k1"] = t1 / v["t_projected_ms"]
         v["speedup_vs_forked_1gpu"] = t_fork / v["t_projected_ms"]
         v["projected_mpanels_s"] = m.n / (v["t_projected_ms"] * 1e-3) / 1e6
     js = json.dumps(res, indent=1)
