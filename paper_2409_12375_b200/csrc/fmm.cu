@@ -1047,6 +1047,22 @@ __global__ void k_permute(int64_t n, int nvec, const int32_t* __restrict__ idx, 
 
 inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
+// zero the 768-float expansion records of the listed boxes (one CTA of 192 threads, float4 stores, per box)
+__global__ void k_zero_boxes(const int32_t* __restrict__ ids, float* __restrict__ e)
+{
+    reinterpret_cast<float4*>(e + (size_t)ids[blockIdx.x] * kMuStride)[threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+static void zero_boxes(xrl_ctx ctx, const xrl::DBuf<int32_t>& ids, int n, int nbox, xrl::DBuf<float>& e, cudaStream_t st)
+{
+    if (n == nbox) {
+        XRL_CUDA(cudaMemsetAsync(e.p, 0, e.bytes(), st));
+    } else if (n > 0) {
+        k_zero_boxes<<<n, kMuStride / 4, 0, st>>>(ids.p, e.p);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+}
+
 // Operators are built once per process in FP64 on the host.
 const HostOperators& host_ops()
 {
@@ -1260,7 +1276,7 @@ static void mvm_up(Mvm& M)
     if (!M.chain) return;
     cudaEvent_t ev;
     phase_begin(ctx, PH_P2M, &ev, M.st);
-    XRL_CUDA(cudaMemsetAsync(t->mu.p, 0, t->mu.bytes(), M.st));  // parents accumulate the M2M reductions
+    zero_boxes(ctx, t->mu_zero, t->n_mu_zero, t->nbox, t->mu, M.st);  // parents accumulate the M2M reductions
     if (t->n_own_leaves > 0) {
         k_p2m<<<t->n_own_leaves, 128, kP2MSmem, M.st>>>(t->own_leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p,
                                                          t->xq.p, t->mu.p);
@@ -1315,7 +1331,7 @@ static void mvm_down(Mvm& M)
     constexpr int m2l_dbg = 0;  // the shipped library has no ablation switch
 #endif
     if (M.chain) {
-        XRL_CUDA(cudaMemsetAsync(t->ell.p, 0, t->ell.bytes(), M.st));
+        zero_boxes(ctx, t->ell_zero, t->n_ell_zero, t->nbox, t->ell, M.st);
         if (!M.side_done) mvm_side(M);  // XRL_SCHED_LATE, or the virtual-rank driver
         phase_begin(ctx, PH_M2L, &ev, M.st);
         if (t->n_m2l_tiles > 0) {

@@ -906,6 +906,23 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         // relevant boxes: panel range meets [p0, p1) (owned subtrees and their ancestors)
         T->rel.assign(nbox, 0);
         for (int b = 0; b < nbox; ++b) T->rel[b] = hpb[b] < T->p1 && hpe[b] > T->p0;
+        // expansions to zero per MVM: multipoles of the relevant non-leaf boxes (the P2M overwrites the leaves'
+        // whole records; LET boxes are overwritten by the exchange), local expansions of the relevant boxes
+        {
+            std::vector<int32_t> mz, ez;
+            for (int b = 0; b < nbox; ++b)
+                if (T->rel[b]) {
+                    ez.push_back(b);
+                    if (hchild[b] >= 0) mz.push_back(b);
+                }
+            T->n_mu_zero = (int32_t)mz.size();
+            T->n_ell_zero = (int32_t)ez.size();
+            T->mu_zero.alloc(std::max<size_t>(1, mz.size()));
+            T->ell_zero.alloc(std::max<size_t>(1, ez.size()));
+            if (!mz.empty()) XRL_CUDA(cudaMemcpyAsync(T->mu_zero.p, mz.data(), 4 * mz.size(), cudaMemcpyHostToDevice, st));
+            if (!ez.empty()) XRL_CUDA(cudaMemcpyAsync(T->ell_zero.p, ez.data(), 4 * ez.size(), cudaMemcpyHostToDevice, st));
+            XRL_CUDA(cudaStreamSynchronize(st));
+        }
         // L2L lists per level (levels >= 3)
         std::vector<int32_t> l2l;
         T->l2l_start.assign(nlev + 1, 0);

@@ -162,6 +162,8 @@ struct xrl_tree_s {
     int32_t p0 = 0, p1 = 0;
     std::vector<int32_t> part_cuts;          // panel offsets of all ranks [world+1]
     std::vector<uint8_t> rel;                // box relevant to this rank
+    xrl::DBuf<int32_t> mu_zero, ell_zero;    // boxes whose mu / ell records are zeroed per MVM
+    int32_t n_mu_zero = 0, n_ell_zero = 0;
     xrl::DBuf<int32_t> own_leaves;           // owned leaves (Morton order)
     xrl::DBuf<int> p2p_counter;              // P2P leaf-task counter (reset per MVM)
     xrl::DBuf<int4> p2p_tasks;               // P2P tasks (leaf, first target panel, #targets <= 256, 0), longest first
