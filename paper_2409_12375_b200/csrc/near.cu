@@ -407,6 +407,17 @@ static xrl_status near_impl(xrl_tree t, double eta, int galerkin, xrl_near* out)
     return XRL_OK;
 }
 
+void xrl::near_release(xrl_near nr)
+{
+    if (!nr->dead || nr->refs > 0) return;
+    xrl_tree t = nr->tree;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    delete nr;
+    --t->refs;
+    tree_release(t);
+}
+
 extern "C" {
 
 xrl_status xrl_near_assemble(xrl_tree t, const xrl_near_opts* opts, xrl_near* out)
@@ -430,12 +441,8 @@ xrl_status xrl_near_assemble(xrl_tree t, const xrl_near_opts* opts, xrl_near* ou
 void xrl_near_destroy(xrl_near nr)
 {
     if (!nr) return;
-    xrl_tree t = nr->tree;
-    cudaSetDevice(t->ctx->device);
-    cudaStreamSynchronize(t->ctx->stream);
-    delete nr;
-    --t->refs;
-    tree_release(t);
+    nr->dead = true;
+    near_release(nr);  // deferred while operators built on it are alive
 }
 
 xrl_status xrl_near_export(xrl_near nr, int64_t* row_ptr, int32_t* col, float* val32, double* val64, int64_t* nnz)

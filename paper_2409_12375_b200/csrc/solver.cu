@@ -854,6 +854,23 @@ static void pc_apply(xrl_precond pc, const float2* v, float2* z, int nrhs)
     t->ctx->launches += 1;
 }
 
+void xrl::op_release(xrl_op op)
+{
+    if (!op->dead || op->refs > 0) return;
+    xrl_tree t = op->tree;
+    xrl_topo T = op->topo;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    xrl_near nr = op->near;
+    delete op;
+    --T->refs;
+    topo_release(T);
+    --nr->refs;
+    near_release(nr);
+    --t->refs;
+    tree_release(t);
+}
+
 #define API_TRY try {
 #define API_CATCH                                   \
     }                                               \
@@ -907,6 +924,7 @@ xrl_status xrl_operator_create(xrl_tree t, xrl_near nr, xrl_topo T, const double
         XRL_CUDA(cudaMemcpy(op->zsa.p, zf.data(), 8 * n, cudaMemcpyHostToDevice));
         if (t->part_world > 1) build_loop_partition(op.get());  // loop-space shard of a partitioned tree
         ++T->refs;
+        ++nr->refs;
         ++t->refs;
         *out = op.release();
         return XRL_OK;
@@ -916,13 +934,8 @@ xrl_status xrl_operator_create(xrl_tree t, xrl_near nr, xrl_topo T, const double
 void xrl_operator_destroy(xrl_op op)
 {
     if (!op) return;
-    xrl_tree t = op->tree;
-    cudaSetDevice(t->ctx->device);
-    cudaStreamSynchronize(t->ctx->stream);
-    --op->topo->refs;
-    delete op;
-    --t->refs;
-    tree_release(t);
+    op->dead = true;
+    op_release(op);  // deferred while preconditioners built on it are alive
 }
 
 xrl_status xrl_operator_apply(xrl_op op, const void* v, void* w, int32_t nrhs)
@@ -1046,7 +1059,7 @@ static xrl_status precond_build_blocks(xrl_op op, int32_t qkind, int32_t block_s
     XRL_CUDA(cudaMemcpyAsync(&hs, sing.p, 4, cudaMemcpyDeviceToHost, st));
     XRL_CUDA(cudaStreamSynchronize(st));
     if (hs) { set_error("xrl_precond_build: singular block %d (pivot below 1e-13 of the block max)", hs - 1); return XRL_ESINGULAR; }
-    ++T->refs;
+    ++op->refs;
     *out = pc.release();
     return XRL_OK;
 }
@@ -1065,7 +1078,7 @@ static xrl_status precond_build_exact_kind(xrl_op op, int32_t qkind, xrl_precond
     pc->bs = 0;
     const xrl_status s = exact_build(pc.get());
     if (s != XRL_OK) return s;
-    ++op->topo->refs;
+    ++op->refs;
     *out = pc.release();
     return XRL_OK;
 }
@@ -1108,8 +1121,10 @@ void xrl_precond_destroy(xrl_precond pc)
 {
     if (!pc) return;
     if (pc->kind == 1) exact_free(pc);
-    --pc->op->topo->refs;
+    xrl_op op = pc->op;
     delete pc;
+    --op->refs;
+    op_release(op);
 }
 
 xrl_status xrl_precond_apply(xrl_precond pc, const void* v, void* z, int32_t nrhs)

@@ -476,6 +476,15 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
     return XRL_OK;
 }
 
+void xrl::topo_release(xrl_topo T)
+{
+    if (!T->dead || T->refs > 0) return;
+    xrl_tree t = T->tree;
+    delete T;
+    --t->refs;
+    tree_release(t);
+}
+
 extern "C" {
 
 xrl_status xrl_topology_build(xrl_tree t, int32_t n_ports, const xrl_port* ports, xrl_topo* out)
@@ -496,10 +505,8 @@ xrl_status xrl_topology_build(xrl_tree t, int32_t n_ports, const xrl_port* ports
 void xrl_topology_destroy(xrl_topo T)
 {
     if (!T) return;
-    xrl_tree t = T->tree;
-    delete T;
-    --t->refs;
-    tree_release(t);
+    T->dead = true;
+    topo_release(T);  // deferred while operators built on it are alive
 }
 
 xrl_status xrl_topology_info(xrl_topo T, xrl_topo_info_t* info)

@@ -1096,7 +1096,19 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         XRL_CUDA(cudaStreamSynchronize(st));
     }
     // multi-rank exchange plan: shared boxes, LET lists, remote leaves for the halo (exchange.cu)
-    if (T->part_world > 1) build_let_plan(T.get(), hpb, hpe, hchild, st);
+    if (T->part_world > 1) {
+        build_let_plan(T.get(), hpb, hpe, hchild, st);
+        // the shared boxes this rank is not relevant to enter the all-reduce with a zero partial multipole
+        std::vector<int32_t> mz(T->n_mu_zero);
+        if (T->n_mu_zero) XRL_CUDA(cudaMemcpyAsync(mz.data(), T->mu_zero.p, 4 * mz.size(), cudaMemcpyDeviceToHost, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+        for (int32_t b : T->shared_boxes)
+            if (!T->rel[b]) mz.push_back(b);
+        T->n_mu_zero = (int32_t)mz.size();
+        T->mu_zero.alloc(std::max<size_t>(1, mz.size()));
+        if (!mz.empty()) XRL_CUDA(cudaMemcpyAsync(T->mu_zero.p, mz.data(), 4 * mz.size(), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaStreamSynchronize(st));
+    }
     // MVM scratch
     T->mu.alloc((size_t)nbox * kMuStride);
     T->ell.alloc((size_t)nbox * kEllStride);

@@ -194,6 +194,8 @@ struct xrl_tree_s {
 
 struct xrl_near_s {
     xrl_tree tree = nullptr;
+    int refs = 0;                                // live operators
+    bool dead = false;                           // destroy requested (deferred while refs > 0)
     double eta = 1.5;
     int64_t nnz = 0;
     xrl::DBuf<int64_t> row_ptr;
@@ -215,7 +217,8 @@ struct xrl_near_s {
 
 struct xrl_topo_s {
     xrl_tree tree = nullptr;
-    int refs = 0;
+    int refs = 0;                                // live operators
+    bool dead = false;                           // destroy requested (deferred while refs > 0)
     int64_t n_edges = 0, n_branches = 0, n_loops = 0, nnz_c = 0;
     int32_t n_ports = 0, n_components = 0;
     int64_t n_vertex_loops = 0, n_fund_loops = 0, n_terminal_loops = 0;
@@ -260,6 +263,8 @@ struct LoopPart {
 }  // namespace xrl
 
 struct xrl_op_s {
+    int refs = 0;                                // live preconditioners
+    bool dead = false;                           // destroy requested (deferred while refs > 0)
     xrl_tree tree = nullptr;
     xrl_near near = nullptr;
     xrl_topo topo = nullptr;
@@ -316,4 +321,7 @@ xrl_status nccl_exchange(xrl_ctx ctx, const float* sbuf, const std::vector<int64
 xrl_status nccl_allreduce_sum(xrl_ctx ctx, float* buf, size_t count, cudaStream_t st);
 xrl_status nccl_allreduce_sum_f64(xrl_ctx ctx, double* buf, size_t count, cudaStream_t st);
 void tree_release(xrl_tree t);
+void topo_release(xrl_topo T);     // delete if dead and unreferenced (then release its tree)
+void near_release(xrl_near nr);    // likewise for near fields
+void op_release(xrl_op op);        // likewise for operators (then release topology and tree)
 }  // namespace xrl

@@ -559,3 +559,23 @@ def test_sharded_operator_and_gmres_virtual_ranks(cfg, world):
     zk = np.linalg.inv(topo.port_currents(x).T)
     assert np.abs(zk - z1).max() / np.abs(z1).max() < 1e-3
     assert abs(int(rep["iters"].max()) - int(rep1["iters"].max())) <= max(3, rep1["iters"].max() // 5)
+
+
+def test_handles_released_in_any_order():
+    """Handle lifetimes (the C-ABI's deferred release): destroying the tree, topology and operator before the
+    preconditioner built on them leaves the preconditioner usable; the last destroy frees everything."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m = meshes.bar()
+    ctx, tree, near = cuda_setup(m)
+    topo = xrl.Topology(tree, [(p, q) for _, p, q in m.ports])
+    op = xrl.Operator(tree, near, topo, 1e8, sigma=SIGMA, zeta=ZETA)
+    pcs = [xrl.Precond(op, 64), xrl.Precond(op, 64, kind="diag_l")]
+    v = torch.ones((1, topo.n_loops), dtype=torch.complex64, device="cuda")
+    z0 = [pc.apply(v).cpu().numpy() for pc in pcs]
+    for h in (topo, op, near, tree):
+        h.close()
+    for pc, z in zip(pcs, z0):
+        assert np.array_equal(pc.apply(v).cpu().numpy(), z)
+    for pc in pcs:
+        pc.close()
