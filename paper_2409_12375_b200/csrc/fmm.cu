@@ -221,27 +221,60 @@ struct P2PTasks {
 constexpr int kFuseChunk = 512;                          // sources staged per chunk by the fused P2P warps
 constexpr int kFuseSmem = kFuseChunk * 12 * 4;           // their staging / reduction buffer (bytes)
 
-// This CTA's tile sequence: blocks blockIdx.x, blockIdx.x + gridDim.x, ...; all tiles of each block.
+// This CTA's tile sequence: blocks blockIdx.x, blockIdx.x + gridDim.x, ...; all tiles of each block.  In a
+// multi-level launch (lvr != nullptr) `lev` is the level of the current block: level v owns the block rows
+// [lvr[v], lvr[v+1]) (row = block index / gridDim.x).
 struct TileSeq {
-    int bi, ti, tend;
+    int bi, ti, tend, lev;
     bool ok;
-    __device__ TileSeq(const int4* __restrict__ blocks, int nblocks) : bi(blockIdx.x), ti(0), tend(0), ok(false)
+    __device__ void find(const int4* __restrict__ blocks, int nblocks, const int* __restrict__ lvr)
     {
+        ok = false;
         for (; bi < nblocks; bi += gridDim.x) {
             const int4 bk = __ldg(blocks + bi);
-            if (bk.y > 0) { ti = bk.x; tend = bk.x + bk.y; ok = true; return; }
+            if (bk.y > 0) { ti = bk.x; tend = bk.x + bk.y; ok = true; break; }
+        }
+        if (ok && lvr) {
+            const int row = bi / gridDim.x;
+            while (row >= __ldg(lvr + lev + 1)) ++lev;
         }
     }
-    __device__ void advance(const int4* __restrict__ blocks, int nblocks)
+    __device__ TileSeq(const int4* __restrict__ blocks, int nblocks, const int* __restrict__ lvr = nullptr)
+        : bi(blockIdx.x), ti(0), tend(0), lev(0), ok(false)
+    {
+        find(blocks, nblocks, lvr);
+    }
+    __device__ void advance(const int4* __restrict__ blocks, int nblocks, const int* __restrict__ lvr = nullptr)
     {
         if (++ti < tend) return;
-        ok = false;
-        for (bi += gridDim.x; bi < nblocks; bi += gridDim.x) {
-            const int4 bk = __ldg(blocks + bi);
-            if (bk.y > 0) { ti = bk.x; tend = bk.x + bk.y; ok = true; return; }
-        }
+        bi += gridDim.x;
+        find(blocks, nblocks, lvr);
     }
 };
+
+// Grid barrier of a multi-level launch: the loaders of every CTA wait until all CTAs have drained level
+// lv - 1 (done[lv - 1] == gridDim.x; one CTA per SM, all resident).  A watchdog traps instead of hanging.
+__device__ __forceinline__ void wait_level(const int* done, int lv)
+{
+    if (!done || lv <= 0) return;
+    long long spins = 0;
+    for (;;) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(done + lv - 1) : "memory");
+        if (v >= (int)gridDim.x) break;
+        __nanosleep(64);
+        if (++spins > (1ll << 26)) asm volatile("trap;");
+    }
+}
+
+// 32-byte load through L2 (coherent: data written earlier in the same launch by other CTAs)
+__device__ __forceinline__ void ldg256_coherent(const float* p, float* v)
+{
+    asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p)
+                 : "memory");
+}
 
 // blocks[j] = {first tile, #tiles, offset, chunk}; tiles[t] = {offset, first pair, #pairs, chunk}
 __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict__ blocks, int nblocks,
@@ -250,7 +283,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                                                           const int32_t* __restrict__ srcb,
                                                           const float* __restrict__ opimg,
                                                           const float* __restrict__ bimg, float* __restrict__ ell,
-                                                          int dbg, P2PTasks p2p)
+                                                          int dbg, P2PTasks p2p, const int* __restrict__ lvr,
+                                                          int* __restrict__ lv_done, int nlv)
 {
     extern __shared__ uint8_t tsm_raw[];
     uint8_t* opsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
@@ -309,21 +343,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 if (row) {
-                    ldg256(row + 64 * h + 8 * c, x + 8 * c);
+                    if (lvr) ldg256_coherent(row + 64 * h + 8 * c, x + 8 * c);  // written in this launch
+                    else ldg256(row + 64 * h + 8 * c, x + 8 * c);
                 } else {
 #pragma unroll
                     for (int q = 0; q < 8; ++q) x[8 * c + q] = 0.f;
                 }
             }
         };
-        TileSeq s0(blocks, nblocks);
+        auto level_gate = [&](int lv) {  // the previous level is complete in every CTA
+            if (lane == 0) wait_level(lv_done, lv);
+            __syncwarp();
+        };
+        TileSeq s0(blocks, nblocks, lvr);
+        if (s0.ok) level_gate(s0.lev);
         const float* row0 = row_of(s0.ok ? __ldg(tiles + s0.ti) : make_int4(0, 0, 0, 0), s0.ok);
         load_half(row0, 0);
         TileSeq s1 = s0;
-        s1.advance(blocks, nblocks);
+        s1.advance(blocks, nblocks, lvr);
         int4 tl1 = s1.ok ? __ldg(tiles + s1.ti) : make_int4(0, 0, 0, 0);
         for (int j = 0; s0.ok; ++j) {
             const float* row1 = nullptr;
+            // the next tile opens a new level: its rows are read only after the grid barrier, which needs this
+            // tile fully handed to the MMA first (no prefetch across levels)
+            const bool defer = s1.ok && s1.lev != s0.lev;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 // the MMAs of the previous tile must be done with this K-half of A
@@ -346,14 +389,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                 if (lane == 0) mbar_arrive(&a_full[h]);
                 if (h == 0) {
                     load_half(row0, 1);
-                    row1 = row_of(tl1, s1.ok);
-                } else {
+                    if (!defer) row1 = row_of(tl1, s1.ok);
+                } else if (!defer) {
                     load_half(row1, 0);
                 }
             }
             s0 = s1;
             row0 = row1;
-            s1.advance(blocks, nblocks);
+            if (defer) {
+                level_gate(s0.lev);
+                row0 = row_of(tl1, true);
+                load_half(row0, 0);
+            }
+            s1.advance(blocks, nblocks, lvr);
             if (s1.ok) tl1 = __ldg(tiles + s1.ti);
         }
     } else if (warp < 8) {
@@ -363,12 +411,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
         const int L = tid - 128, p = L / 6, r = L % 6;
         const bool lane_ok = L < 6 * kTcPairs;
         const int qd = warp - 4;  // lane quarter (warp % 4)
-        TileSeq sq(blocks, nblocks);
+        // multi-level launch: after its last tile of a level, every drain thread waits for its bulk reductions
+        // to complete and fences them; then one thread marks the level (and any level this CTA had no tile
+        // in) done for the other CTAs' loaders
+        int signaled = 0;
+        auto signal_upto = [&](int lv) {  // levels [signaled, lv) are complete in this CTA
+            if (!lv_done || lv <= signaled) return;
+            bulk_wait0();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (L == 0)
+                for (int v = signaled; v < lv; ++v) atomicAdd(lv_done + v, 1);
+            signaled = lv;
+        };
+        TileSeq sq(blocks, nblocks, lvr);
+        if (sq.ok) signal_upto(sq.lev);
         int4 cur = sq.ok ? __ldg(tiles + sq.ti) : make_int4(0, 0, 0, 0);
         int cur_t = (sq.ok && lane_ok && p < cur.z) ? __ldg(tgt + cur.y + p) : -1;
         for (int j = 0; sq.ok; ++j) {
             TileSeq nx = sq;
-            nx.advance(blocks, nblocks);
+            nx.advance(blocks, nblocks, lvr);
             int nxt_t = -1;
             int4 nxt = make_int4(0, 0, 0, 0);
             if (nx.ok) {
@@ -402,10 +465,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                 bulk_red_add_f32(ell + (size_t)cur_t * kEllStride + r * 128, srow, 124 * 4);
                 bulk_commit();
             }
+            if (nx.ok && nx.lev != sq.lev) signal_upto(nx.lev);
             sq = nx;
             cur = nxt;
             cur_t = nxt_t;
         }
+        if (lvr) signal_upto(nlv);
         bulk_wait0();
     } else {
         // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform control
@@ -1129,15 +1194,17 @@ void upload_constants(xrl_ctx ctx)
 
 }  // namespace xrl
 
-// One level of M2M or L2L on the tensor-core translation kernel: blocks lvl = (first, count) of the
-// tree's tr_* tile lists; src/dst are r-major expansion arrays (disjoint boxes of two levels).
-static void translate_level(xrl_tree t, std::pair<int, int> lvl, const float* src, float* dst, cudaStream_t st)
+// All M2M levels (bottom-up) or all L2L levels (top-down) in one launch of the tensor-core translation
+// kernel: the pass's blocks are balanced per level over one persistent grid and the CTAs meet at a grid
+// barrier between levels (TransPass, tree.cu); src/dst are r-major expansion arrays.
+static void translate_pass(xrl_tree t, xrl::TransPass& P, const float* src, float* dst, cudaStream_t st)
 {
-    if (lvl.second <= 0) return;
+    if (P.nblocks <= 0 || P.nlev <= 0) return;
     xrl_ctx ctx = t->ctx;
-    const int grid = std::min(ctx->num_sms, lvl.second);
-    k_m2l_tc<<<grid, kTcThreads, kTcSmem, st>>>(t->tr_blocks.p + lvl.first, lvl.second, t->tr_tiles.p, t->tr_tgt.p,
-                                                t->tr_src.p, ctx->ops.m2l_tc.p, src, dst, 0, P2PTasks{});
+    XRL_CUDA(cudaMemsetAsync(P.done.p, 0, sizeof(int) * P.nlev, st));
+    k_m2l_tc<<<P.grid, kTcThreads, kTcSmem, st>>>(t->tr_blocks.p + P.first, P.nblocks, t->tr_tiles.p, t->tr_tgt.p,
+                                                  t->tr_src.p, ctx->ops.m2l_tc.p, src, dst, 0, P2PTasks{}, P.rows.p,
+                                                  P.done.p, P.nlev);
     XRL_LAUNCH_CHECK();
     ctx->launches += 1;
 }
@@ -1285,7 +1352,7 @@ static void mvm_up(Mvm& M)
     }
     phase_end(ctx, PH_P2M, ev, M.st);
     phase_begin(ctx, PH_M2M, &ev, M.st);
-    for (int l = t->nlevel - 2; l >= 2; --l) translate_level(t, t->m2m_lvl[l], t->mu.p, t->mu.p, M.st);
+    translate_pass(t, t->m2m_pass, t->mu.p, t->mu.p, M.st);
     phase_end(ctx, PH_M2M, ev, M.st);
 }
 
@@ -1343,7 +1410,7 @@ static void mvm_down(Mvm& M)
                                  M.p0, M.y};
             k_m2l_tc<<<grid, kTcThreads, kTcSmem, M.st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p,
                                                           t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu.p,
-                                                          t->ell.p, m2l_dbg, tasks);
+                                                          t->ell.p, m2l_dbg, tasks, nullptr, nullptr, 0);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -1363,7 +1430,7 @@ static void mvm_down(Mvm& M)
         }
         phase_end(ctx, PH_P2L, ev, M.st);
         phase_begin(ctx, PH_L2L, &ev, M.st);
-        for (int l = 3; l < t->nlevel; ++l) translate_level(t, t->l2l_lvl[l], t->ell.p, t->ell.p, M.st);
+        translate_pass(t, t->l2l_pass, t->ell.p, t->ell.p, M.st);
         phase_end(ctx, PH_L2L, ev, M.st);
     } else if (!M.side_done) {
         mvm_side(M);

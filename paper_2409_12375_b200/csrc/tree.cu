@@ -968,12 +968,28 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
                 }
                 i = j;
             }
-            // balance this level's blocks over its persistent grid (translate_level: min(num_sms, #blocks))
-            std::vector<int4> lvl(blocks.begin() + first_block, blocks.end());
-            lvl = balance_blocks(lvl, std::min<int>(ctx->num_sms, (int)lvl.size()));
-            blocks.resize(first_block);
-            blocks.insert(blocks.end(), lvl.begin(), lvl.end());
             return std::make_pair(first_block, (int)blocks.size() - first_block);
+        };
+        // One launch per pass (all M2M levels bottom-up, all L2L levels top-down): each level's blocks are
+        // LPT-balanced over the pass's persistent grid G and padded to whole rows of G, so the kernel knows a
+        // block's level from its row; CTAs meet at a grid barrier between levels (k_m2l_tc).
+        auto pack_pass = [&](std::vector<std::pair<int, int>>& lv, TransPass& P) {
+            int G = 1;
+            for (auto& r : lv) G = std::max(G, std::min(ctx->num_sms, r.second));
+            std::vector<int4> out;
+            std::vector<int32_t> rows(1, 0);
+            for (auto& r : lv) {
+                std::vector<int4> b(blocks.begin() + r.first, blocks.begin() + r.first + r.second);
+                b = balance_blocks(b, G);
+                if (!b.empty() && (int)b.size() < G) b.resize(G, make_int4(0, 0, 0, 0));
+                out.insert(out.end(), b.begin(), b.end());
+                rows.push_back(rows.back() + (int)(b.size() / G));
+            }
+            P.grid = G;
+            P.nlev = (int)lv.size();
+            P.nblocks = (int)out.size();
+            P.rows_h = rows;
+            return out;
         };
         T->m2m_lvl.assign(nlev, {0, 0});
         T->l2l_lvl.assign(nlev, {0, 0});
@@ -991,6 +1007,22 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
                 pr.push_back({kOpL2L + oct(c), c, hpar[c]});
             }
             T->l2l_lvl[l] = emit_level(pr);
+        }
+        {
+            std::vector<std::pair<int, int>> mlv, llv;
+            for (int l = nlev - 2; l >= 2; --l) mlv.push_back(T->m2m_lvl[l]);
+            for (int l = 3; l < nlev; ++l) llv.push_back(T->l2l_lvl[l]);
+            std::vector<int4> mb = pack_pass(mlv, T->m2m_pass), lb = pack_pass(llv, T->l2l_pass);
+            T->m2m_pass.first = 0;
+            T->l2l_pass.first = (int)mb.size();
+            blocks = mb;
+            blocks.insert(blocks.end(), lb.begin(), lb.end());
+            for (TransPass* P : {&T->m2m_pass, &T->l2l_pass}) {
+                P->rows.alloc(P->rows_h.size());
+                XRL_CUDA(cudaMemcpyAsync(P->rows.p, P->rows_h.data(), 4 * P->rows_h.size(), cudaMemcpyHostToDevice, st));
+                P->done.alloc(std::max(1, P->nlev));
+            }
+            XRL_CUDA(cudaStreamSynchronize(st));
         }
         T->tr_tiles.alloc(std::max<size_t>(1, tiles.size()));
         T->tr_blocks.alloc(std::max<size_t>(1, blocks.size()));

@@ -84,6 +84,17 @@ constexpr int kNearSegLen = 256;     // near SpMV: max entries per segment (8 la
 
 }  // namespace xrl
 
+namespace xrl {
+// One launch of the translation kernel over several dependent levels (all M2M levels, or all L2L levels):
+// blocks [first, first + nblocks) of tr_blocks, level v owning block rows [rows[v], rows[v+1]) of the grid.
+struct TransPass {
+    int first = 0, nblocks = 0, grid = 1, nlev = 0;
+    std::vector<int32_t> rows_h;
+    DBuf<int32_t> rows;  // [nlev+1] cumulative block rows per level
+    DBuf<int> done;      // [nlev] CTAs done with each level (zeroed per launch)
+};
+}  // namespace xrl
+
 struct xrl_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -147,7 +158,8 @@ struct xrl_tree_s {
     // M2M / L2L translation tiles for the tensor-core kernel (all levels concatenated)
     xrl::DBuf<int4> tr_tiles, tr_blocks;
     xrl::DBuf<int32_t> tr_tgt, tr_src;
-    std::vector<std::pair<int, int>> m2m_lvl, l2l_lvl;  // per level: (first block, #blocks)
+    std::vector<std::pair<int, int>> m2m_lvl, l2l_lvl;  // per level: (first block, #blocks) before packing
+    xrl::TransPass m2m_pass, l2l_pass;                 // the packed multi-level launches
     int64_t n_m2l_subtiles = 0;
     // boxes with non-empty X list, leaves with non-empty W list
     xrl::DBuf<int32_t> x_targets;
