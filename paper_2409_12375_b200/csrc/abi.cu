@@ -136,6 +136,9 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         if (c->sched < XRL_SCHED_SERIAL || c->sched > XRL_SCHED_LATE) c->sched = XRL_SCHED_FORK;
         upload_constants(c);
         if (world > 1) {
+            XRL_CUDA(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, prio_hi));
+            XRL_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+            XRL_CUDA(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
             xrl_status st = comm_init(c, nccl_unique_id);
             if (st) return st;
         }
@@ -179,6 +182,9 @@ void xrl::ctx_release(xrl_ctx ctx)
     if (ctx->ev_m2l) cudaEventDestroy(ctx->ev_m2l);
     if (ctx->ev_p2p) cudaEventDestroy(ctx->ev_p2p);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->comm) { cudaStreamSynchronize(ctx->comm); cudaStreamDestroy(ctx->comm); }
+    if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+    if (ctx->ev_comm) cudaEventDestroy(ctx->ev_comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

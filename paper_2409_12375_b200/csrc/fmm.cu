@@ -1227,6 +1227,7 @@ struct Mvm {
     bool do_far, do_near, chain, fuse, side_done;
     int64_t nl, p0;
     float invW;
+    cudaEvent_t halo = nullptr;  // multi-rank, overlapped halo: the P2P / P2L wait for it
 };
 
 static Mvm mvm_make(xrl_tree t, xrl_near nr, float2* y, uint32_t flags, int sched)
@@ -1271,18 +1272,18 @@ static void mvm_begin(Mvm& M, const float2* x)
     XRL_CUDA(cudaMemsetAsync(t->p2p_counter.p, 0, sizeof(int), M.st));  // P2P leaf tasks (before the fork)
 }
 
-// halo of x, step 1: pack the records peers read (work stream)
-static void halo_pack(Mvm& M)
+// halo of x, step 1: pack the records peers read (work stream unless given)
+static void halo_pack(Mvm& M, cudaStream_t st = nullptr)
 {
     xrl_near N = M.nr;
-    gather_records(N->halo_soff.back(), 8, N->halo_sidx.p, M.t->xq.p, N->halo_sbuf.p, M.st);
+    gather_records(N->halo_soff.back(), 8, N->halo_sidx.p, M.t->xq.p, N->halo_sbuf.p, st ? st : M.st);
     M.t->ctx->launches += N->halo_soff.back() > 0;
 }
 // step 3 (after the transport): scatter the received records into the charges
-static void halo_unpack(Mvm& M)
+static void halo_unpack(Mvm& M, cudaStream_t st = nullptr)
 {
     xrl_near N = M.nr;
-    scatter_records(N->halo_roff.back(), 8, N->halo_ridx.p, N->halo_rbuf.p, M.t->xq.p, M.st);
+    scatter_records(N->halo_roff.back(), 8, N->halo_ridx.p, N->halo_rbuf.p, M.t->xq.p, st ? st : M.st);
     M.t->ctx->launches += N->halo_roff.back() > 0;
 }
 
@@ -1319,6 +1320,7 @@ static void mvm_side(Mvm& M)
     M.side_done = true;
     XRL_CUDA(cudaEventRecord(ctx->ev_fork, M.st));
     XRL_CUDA(cudaStreamWaitEvent(M.side, ctx->ev_fork, 0));
+    if (M.halo) XRL_CUDA(cudaStreamWaitEvent(M.side, M.halo, 0));  // the P2P reads remote charges
     if (M.do_far) {
         phase_begin(ctx, PH_P2P, &ev, M.side);
         if (t->n_own_leaves > 0) {
@@ -1420,6 +1422,7 @@ static void mvm_down(Mvm& M)
             XRL_CUDA(cudaStreamWaitEvent(M.side, ctx->ev_m2l, 0));  // fused P2P tasks done
             launch_near(M);
         }
+        if (M.halo) XRL_CUDA(cudaStreamWaitEvent(M.st, M.halo, 0));  // the P2L reads remote leaves' charges
         phase_begin(ctx, PH_P2L, &ev, M.st);
         if (t->n_x_targets > 0) {
             k_p2l<<<t->n_x_targets, 128, kP2LSmem, M.st>>>(t->x_targets.p, t->x_ptr.p, t->x_src.p, t->blevel.p,
@@ -1473,24 +1476,53 @@ static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y
     Mvm M = mvm_make(t, nr, y, flags, ctx->sched);
     const bool dist = t->part_world > 1;
     mvm_begin(M, x);
+    // the NCCL exchanges run on the library's comm stream (one stream, so every rank issues them in the same
+    // order): the halo of x overlaps the up pass, which reads only the rank's own charges
+    const bool overlap = dist && M.sched != XRL_SCHED_SERIAL && ctx->comm;
+    cudaStream_t cs = overlap ? ctx->comm : M.st;
     if (dist) {
-        halo_pack(M);
-        xrl_status s = nccl_exchange(ctx, nr->halo_sbuf.p, nr->halo_soff, nr->halo_rbuf.p, nr->halo_roff, 8, M.st);
+        if (overlap) {
+            XRL_CUDA(cudaEventRecord(ctx->ev_comm, M.st));
+            XRL_CUDA(cudaStreamWaitEvent(cs, ctx->ev_comm, 0));
+        }
+        halo_pack(M, cs);
+        xrl_status s = nccl_exchange(ctx, nr->halo_sbuf.p, nr->halo_soff, nr->halo_rbuf.p, nr->halo_roff, 8, cs);
         if (s) return s;
-        halo_unpack(M);
+        halo_unpack(M, cs);
+        if (overlap) {
+            XRL_CUDA(cudaEventRecord(ctx->ev_halo, cs));
+            M.halo = ctx->ev_halo;
+        }
     }
     if (M.sched != XRL_SCHED_LATE || !M.chain) mvm_side(M);
     mvm_up(M);
     if (dist && M.chain) {
         mu_pack(M);
-        xrl_status s = nccl_allreduce_sum(ctx, t->sh_buf.p, t->shared_boxes.size() * (size_t)kMuStride, M.st);
+        if (overlap) {
+            XRL_CUDA(cudaEventRecord(ctx->ev_comm, M.st));
+            XRL_CUDA(cudaStreamWaitEvent(cs, ctx->ev_comm, 0));
+        }
+        xrl_status s = nccl_allreduce_sum(ctx, t->sh_buf.p, t->shared_boxes.size() * (size_t)kMuStride, cs);
         if (s) return s;
+        if (overlap) {
+            XRL_CUDA(cudaEventRecord(ctx->ev_comm, cs));
+            XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_comm, 0));
+        }
         mu_shared_unpack_let_pack(M);
-        s = nccl_exchange(ctx, t->let_sbuf.p, t->let_soff, t->let_rbuf.p, t->let_roff, kMuStride, M.st);
+        if (overlap) {
+            XRL_CUDA(cudaEventRecord(ctx->ev_comm, M.st));
+            XRL_CUDA(cudaStreamWaitEvent(cs, ctx->ev_comm, 0));
+        }
+        s = nccl_exchange(ctx, t->let_sbuf.p, t->let_soff, t->let_rbuf.p, t->let_roff, kMuStride, cs);
         if (s) return s;
+        if (overlap) {
+            XRL_CUDA(cudaEventRecord(ctx->ev_comm, cs));
+            XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_comm, 0));
+        }
         let_unpack(M);
     }
     mvm_down(M);
+    if (overlap) XRL_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));  // (already implied; explicit join)
     return XRL_OK;
 }
 

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 TOL_FULL = 2e-5
 TOL_NEAR = 1e-6
 S_ROWS = 4096
-BENCH_LEAF = 352  # bench.py's launch configuration (leaf_max)
+BENCH_LEAF = 384  # bench.py's launch configuration (leaf_max)
 
 _cache = {}
 

@@ -223,7 +223,7 @@ def test_host_api_e2e(bar_setup):
 
 @pytest.mark.parametrize("cfg,nrows,leaf", [(2, 1024, 64), (4, 256, 512)])
 def test_full_mvm_sampled_rows(cfg, nrows, leaf):
-    """Other leaf sizes on sampled rows (the 4096-row and full config-2 checks at the bench's leaf 352 are
+    """Other leaf sizes on sampled rows (the 4096-row and full config-2 checks at the bench's leaf (384) are
     in test_gpu_fullsize.py)."""
     m = meshes.make_config(cfg)
     ctx, tree, near = cuda_setup(m, leaf_max=leaf)
@@ -236,7 +236,7 @@ def test_full_mvm_sampled_rows(cfg, nrows, leaf):
     assert err <= TOL_FULL
 
 
-@pytest.mark.parametrize("cfg,world,leaf", [(1, 2, 64), (1, 3, 16), (2, 4, 64), (2, 8, 352), (3, 8, 352)])
+@pytest.mark.parametrize("cfg,world,leaf", [(1, 2, 64), (1, 3, 16), (2, 4, 64), (2, 8, 384), (3, 8, 384)])
 def test_virtual_ranks_equal_single_gpu(cfg, world, leaf):
     """Sharded MVM on one GPU through xrl_mvm_vranks: k trees partitioned 0..k-1, each with
     its own charges only; the halo of x, the shared-box multipole all-reduce and the LET exchange run as

@@ -4,7 +4,7 @@
 T=${1:-run}
 O=gpurun_out/$T
 mkdir -p $O
-L=${LEAF:-352}
+L=${LEAF:-384}
 nproc > $O/nproc.txt; lscpu > $O/lscpu.txt 2>&1; nvidia-smi > $O/nvidia-smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build rc=$?" >> $O/status.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/status.txt
