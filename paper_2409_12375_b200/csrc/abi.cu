@@ -135,10 +135,12 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         if (const char* e = getenv("XRL_SERIAL"); e && e[0] == '1') c->sched = XRL_SCHED_SERIAL;
         if (c->sched < XRL_SCHED_SERIAL || c->sched > XRL_SCHED_LATE) c->sched = XRL_SCHED_FORK;
         upload_constants(c);
+        // the exchanges' stream (NCCL on a multi-rank context; the virtual-rank timing pass uses it for the same
+        // overlap on a single-rank one)
+        XRL_CUDA(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, prio_hi));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
         if (world > 1) {
-            XRL_CUDA(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, prio_hi));
-            XRL_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
-            XRL_CUDA(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
             xrl_status st = comm_init(c, nccl_unique_id);
             if (st) return st;
         }

@@ -1469,11 +1469,13 @@ static void mvm_down(Mvm& M)
 }
 
 // One triple on this process's tree: x this rank's slice [3][n_local], y the same.  On a partitioned
-// multi-rank tree the exchanges run over NCCL between the phases.
-static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags)
+// multi-rank tree the exchanges run over NCCL between the phases.  transports = false (the virtual-rank
+// timing pass): the same phases, streams and overlap with the three transports left out.
+static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y, uint32_t flags,
+                             bool transports = true)
 {
     xrl_ctx ctx = t->ctx;
-    Mvm M = mvm_make(t, nr, y, flags, ctx->sched);
+    Mvm M = mvm_make(t, nr, y, flags, ctx->sched == XRL_SCHED_LATE && !transports ? XRL_SCHED_FORK : ctx->sched);
     const bool dist = t->part_world > 1;
     mvm_begin(M, x);
     // the NCCL exchanges run on the library's comm stream (one stream, so every rank issues them in the same
@@ -1486,8 +1488,10 @@ static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y
             XRL_CUDA(cudaStreamWaitEvent(cs, ctx->ev_comm, 0));
         }
         halo_pack(M, cs);
-        xrl_status s = nccl_exchange(ctx, nr->halo_sbuf.p, nr->halo_soff, nr->halo_rbuf.p, nr->halo_roff, 8, cs);
-        if (s) return s;
+        if (transports) {
+            xrl_status s = nccl_exchange(ctx, nr->halo_sbuf.p, nr->halo_soff, nr->halo_rbuf.p, nr->halo_roff, 8, cs);
+            if (s) return s;
+        }
         halo_unpack(M, cs);
         if (overlap) {
             XRL_CUDA(cudaEventRecord(ctx->ev_halo, cs));
@@ -1502,8 +1506,10 @@ static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y
             XRL_CUDA(cudaEventRecord(ctx->ev_comm, M.st));
             XRL_CUDA(cudaStreamWaitEvent(cs, ctx->ev_comm, 0));
         }
-        xrl_status s = nccl_allreduce_sum(ctx, t->sh_buf.p, t->shared_boxes.size() * (size_t)kMuStride, cs);
-        if (s) return s;
+        if (transports) {
+            xrl_status s = nccl_allreduce_sum(ctx, t->sh_buf.p, t->shared_boxes.size() * (size_t)kMuStride, cs);
+            if (s) return s;
+        }
         if (overlap) {
             XRL_CUDA(cudaEventRecord(ctx->ev_comm, cs));
             XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_comm, 0));
@@ -1513,8 +1519,10 @@ static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y
             XRL_CUDA(cudaEventRecord(ctx->ev_comm, M.st));
             XRL_CUDA(cudaStreamWaitEvent(cs, ctx->ev_comm, 0));
         }
-        s = nccl_exchange(ctx, t->let_sbuf.p, t->let_soff, t->let_rbuf.p, t->let_roff, kMuStride, cs);
-        if (s) return s;
+        if (transports) {
+            xrl_status s = nccl_exchange(ctx, t->let_sbuf.p, t->let_soff, t->let_rbuf.p, t->let_roff, kMuStride, cs);
+            if (s) return s;
+        }
         if (overlap) {
             XRL_CUDA(cudaEventRecord(ctx->ev_comm, cs));
             XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_comm, 0));
@@ -1665,20 +1673,10 @@ xrl_status xrl_mvm_vranks(int32_t k, const xrl_tree* trees, const xrl_near* near
             // timed in the real pass (exch_ms) and modelled over NVLink by the projection
             VTimer rt{ctx, true};
             for (int r = 0; r < k; ++r) {
-                Mvm M = mvm_make(trees[r], nears[r], (float2*)y[r], flags, sched);
                 rt.begin();
-                mvm_begin(M, (const float2*)x[r]);
-                halo_pack(M);
-                halo_unpack(M);
-                if (M.sched != XRL_SCHED_LATE || !M.chain) mvm_side(M);
-                mvm_up(M);
-                if (M.chain) {
-                    mu_pack(M);
-                    mu_shared_unpack_let_pack(M);
-                    let_unpack(M);
-                }
-                mvm_down(M);
+                s = mvm_triple(trees[r], nears[r], (const float2*)x[r], (float2*)y[r], flags, false);
                 rt.end(r);
+                if (s) return s;
             }
             std::vector<double> rms(k + 1, 0.0);
             rt.collect(rms.data());
