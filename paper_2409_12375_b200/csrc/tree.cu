@@ -955,12 +955,21 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         auto emit_level = [&](std::vector<std::array<int, 3>>& pr) {  // (op, target, source)
             std::sort(pr.begin(), pr.end());
             const int first_block = (int)blocks.size();
+            // tiles per block: up to 16 (one 128 KB operator load per block), fewer when the level has few tiles,
+            // so that its blocks spread over all SMs (a rank's share of a level can be a few dozen tiles)
+            int64_t ntile = 0;
+            for (size_t i = 0, j; i < pr.size(); i = j) {
+                for (j = i; j < pr.size() && pr[j][0] == pr[i][0]; ++j) {
+                }
+                ntile += (int64_t)(j - i + 20) / 21;
+            }
+            const int bt = (int)std::max<int64_t>(1, std::min<int64_t>(16, (ntile + ctx->num_sms - 1) / ctx->num_sms));
             size_t i = 0;
             while (i < pr.size()) {
                 size_t j = i;
                 while (j < pr.size() && pr[j][0] == pr[i][0]) ++j;
                 for (size_t s0 = i; s0 < j; s0 += 21) {
-                    if (s0 == i || blocks.back().y == 16) blocks.push_back(make_int4((int)tiles.size(), 0, pr[i][0], 0));
+                    if (s0 == i || blocks.back().y == bt) blocks.push_back(make_int4((int)tiles.size(), 0, pr[i][0], 0));
                     const int cnt = (int)std::min<size_t>(21, j - s0);
                     tiles.push_back(make_int4(pr[i][0], (int)ptgt.size(), cnt, 0));
                     for (int q = 0; q < cnt; ++q) { ptgt.push_back(pr[s0 + q][1]); psrc.push_back(pr[s0 + q][2]); }
