@@ -140,6 +140,7 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         XRL_CUDA(cudaStreamCreateWithPriority(&c->comm, cudaStreamNonBlocking, prio_hi));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_comm, cudaEventDisableTiming));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_p2l, cudaEventDisableTiming));
         if (world > 1) {
             xrl_status st = comm_init(c, nccl_unique_id);
             if (st) return st;
@@ -187,6 +188,7 @@ void xrl::ctx_release(xrl_ctx ctx)
     if (ctx->comm) { cudaStreamSynchronize(ctx->comm); cudaStreamDestroy(ctx->comm); }
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     if (ctx->ev_comm) cudaEventDestroy(ctx->ev_comm);
+    if (ctx->ev_p2l) cudaEventDestroy(ctx->ev_p2l);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

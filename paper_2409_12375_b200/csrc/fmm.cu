@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
 #pragma unroll
     for (int jj = 0; jj < 6; ++jj) {
         const int o = threadIdx.x + 128 * jj;
-        if (o < kNC * 6) out[(o % 6) * 128 + o / 6] += acc[jj];
+        if (o < kNC * 6) atomicAdd(out + (o % 6) * 128 + o / 6, acc[jj]);  // may run beside the M2L's reductions
     }
 }
 
@@ -1228,6 +1228,7 @@ struct Mvm {
     int64_t nl, p0;
     float invW;
     cudaEvent_t halo = nullptr;  // multi-rank, overlapped halo: the P2P / P2L wait for it
+    bool p2l_early = false;      // the P2L ran on the comm stream during the up pass (L2L waits for ev_p2l)
 };
 
 static Mvm mvm_make(xrl_tree t, xrl_near nr, float2* y, uint32_t flags, int sched)
@@ -1337,13 +1338,38 @@ static void mvm_side(Mvm& M)
     if (!M.fuse) launch_near(M);
 }
 
-// upward pass: P2M of the own leaves, M2M of the relevant boxes
+static void launch_p2l(Mvm& M, cudaStream_t st)
+{
+    xrl_tree t = M.t;
+    xrl_ctx ctx = t->ctx;
+    cudaEvent_t ev;
+    phase_begin(ctx, PH_P2L, &ev, st);
+    if (t->n_x_targets > 0) {
+        k_p2l<<<t->n_x_targets, 128, kP2LSmem, st>>>(t->x_targets.p, t->x_ptr.p, t->x_src.p, t->blevel.p, t->bix.p,
+                                                     t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->loc.p, t->xq.p, t->ell.p);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    phase_end(ctx, PH_P2L, ev, st);
+}
+
+// upward pass: P2M of the own leaves, M2M of the relevant boxes.  In the forked schedules the local
+// expansions are zeroed here and the P2L (X list: a few, latency-bound CTAs) runs on the comm stream beside the
+// up pass instead of between the M2L and the L2L; it adds into ell atomically, the L2L waits for it.
 static void mvm_up(Mvm& M)
 {
     xrl_tree t = M.t;
     xrl_ctx ctx = t->ctx;
     if (!M.chain) return;
     cudaEvent_t ev;
+    if (M.sched != XRL_SCHED_SERIAL && ctx->comm && ctx->ev_p2l) {
+        zero_boxes(ctx, t->ell_zero, t->n_ell_zero, t->nbox, t->ell, M.st);
+        XRL_CUDA(cudaEventRecord(ctx->ev_p2l, M.st));
+        XRL_CUDA(cudaStreamWaitEvent(ctx->comm, ctx->ev_p2l, 0));  // (the halo, if any, is already on comm)
+        launch_p2l(M, ctx->comm);
+        XRL_CUDA(cudaEventRecord(ctx->ev_p2l, ctx->comm));
+        M.p2l_early = true;
+    }
     phase_begin(ctx, PH_P2M, &ev, M.st);
     zero_boxes(ctx, t->mu_zero, t->n_mu_zero, t->nbox, t->mu, M.st);  // parents accumulate the M2M reductions
     if (t->n_own_leaves > 0) {
@@ -1400,7 +1426,7 @@ static void mvm_down(Mvm& M)
     constexpr int m2l_dbg = 0;  // the shipped library has no ablation switch
 #endif
     if (M.chain) {
-        zero_boxes(ctx, t->ell_zero, t->n_ell_zero, t->nbox, t->ell, M.st);
+        if (!M.p2l_early) zero_boxes(ctx, t->ell_zero, t->n_ell_zero, t->nbox, t->ell, M.st);
         if (!M.side_done) mvm_side(M);  // XRL_SCHED_LATE, or the virtual-rank driver
         phase_begin(ctx, PH_M2L, &ev, M.st);
         if (t->n_m2l_tiles > 0) {
@@ -1422,16 +1448,12 @@ static void mvm_down(Mvm& M)
             XRL_CUDA(cudaStreamWaitEvent(M.side, ctx->ev_m2l, 0));  // fused P2P tasks done
             launch_near(M);
         }
-        if (M.halo) XRL_CUDA(cudaStreamWaitEvent(M.st, M.halo, 0));  // the P2L reads remote leaves' charges
-        phase_begin(ctx, PH_P2L, &ev, M.st);
-        if (t->n_x_targets > 0) {
-            k_p2l<<<t->n_x_targets, 128, kP2LSmem, M.st>>>(t->x_targets.p, t->x_ptr.p, t->x_src.p, t->blevel.p,
-                                                           t->bix.p, t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->loc.p,
-                                                           t->xq.p, t->ell.p);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
+        if (M.p2l_early) {
+            XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_p2l, 0));
+        } else {
+            if (M.halo) XRL_CUDA(cudaStreamWaitEvent(M.st, M.halo, 0));  // the P2L reads remote leaves' charges
+            launch_p2l(M, M.st);
         }
-        phase_end(ctx, PH_P2L, ev, M.st);
         phase_begin(ctx, PH_L2L, &ev, M.st);
         translate_pass(t, t->l2l_pass, t->ell.p, t->ell.p, M.st);
         phase_end(ctx, PH_L2L, ev, M.st);

@@ -102,7 +102,7 @@ struct xrl_ctx_s {
     cudaStream_t side = nullptr;      // library-owned low-priority side stream (near SpMV, P2P)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_work = nullptr, ev_m2l = nullptr, ev_p2p = nullptr;
     cudaStream_t comm = nullptr;      // library-owned stream of a multi-rank context's NCCL exchanges
-    cudaEvent_t ev_halo = nullptr, ev_comm = nullptr;
+    cudaEvent_t ev_halo = nullptr, ev_comm = nullptr, ev_p2l = nullptr;
     bool fuse_p2p = true;             // P2P warps inside the M2L kernel (XRL_FUSE=0: off)
     bool own_stream = false;
     int rank = 0, world = 1;
