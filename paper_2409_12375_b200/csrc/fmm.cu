@@ -1497,7 +1497,7 @@ static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y
                              bool transports = true)
 {
     xrl_ctx ctx = t->ctx;
-    Mvm M = mvm_make(t, nr, y, flags, ctx->sched == XRL_SCHED_LATE && !transports ? XRL_SCHED_FORK : ctx->sched);
+    Mvm M = mvm_make(t, nr, y, flags, ctx->sched);
     const bool dist = t->part_world > 1;
     mvm_begin(M, x);
     // the NCCL exchanges run on the library's comm stream (one stream, so every rank issues them in the same

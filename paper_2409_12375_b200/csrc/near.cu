@@ -407,6 +407,23 @@ static xrl_status near_impl(xrl_tree t, double eta, int galerkin, xrl_near* out)
     return XRL_OK;
 }
 
+// Near-field row lengths (the first pass of the assembly) for the partition's cost model (tree.cu).
+std::vector<int64_t> xrl::near_row_counts(xrl_tree t, double eta, cudaStream_t st)
+{
+    const int64_t n = t->n;
+    TreeView tv{t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bchild.p, t->bnchild.p, t->bpb.p, t->bpe.p,
+                t->bdmax.p, t->cent.p, t->dmax.p, t->lo[0], t->lo[1], t->lo[2], t->W};
+    DBuf<int64_t> cnt(n);
+    DBuf<int> ovf(1);
+    XRL_CUDA(cudaMemsetAsync(ovf.p, 0, 4, st));
+    k_near_search<false><<<nblk(n, 128), 128, 0, st>>>(n, tv, eta, cnt.p, nullptr, nullptr, ovf.p);
+    XRL_LAUNCH_CHECK();
+    std::vector<int64_t> h(n);
+    XRL_CUDA(cudaMemcpyAsync(h.data(), cnt.p, 8 * n, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaStreamSynchronize(st));
+    return h;
+}
+
 void xrl::near_release(xrl_near nr)
 {
     if (!nr->dead || nr->refs > 0) return;

@@ -850,6 +850,10 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         for (int32_t b : hleaves) lf.push_back({hpb[b], b});
         std::sort(lf.begin(), lf.end());
         std::vector<double> w(lf.size());
+        // near-field rows differ by an order of magnitude in length (coarse ground-plane panels see many fine
+        // trace panels): a partitioned tree counts them (default eta) for the SpMV's share of the cost
+        std::vector<int64_t> nnz_row;
+        if (T->part_world > 1) nnz_row = near_row_counts(T.get(), 1.5, st);
         for (size_t i = 0; i < lf.size(); ++i) {
             const int L = lf[i].second;
             const double nL = hpe[L] - hpb[L];
@@ -857,9 +861,13 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
             for (int64_t q = hup[L]; q < hup[L + 1]; ++q) src += hpe[hus[q]] - hpb[hus[q]];
             double m2l = 0;
             for (int a = L; a >= 0; a = hpar[a]) m2l += double(hvp[a + 1] - hvp[a]) * nL / double(hpe[a] - hpb[a]);
-            // measured device costs on config 4 (B200, leaf 352), in units of one P2P pair (0.52 ns): an M2L
-            // translation on tcgen05 ~1.04 us = 2,000 pairs; P2M + L2P + near rows of a panel ~0.67 ns = 1.3 pairs
-            w[i] = nL * src + 2000.0 * m2l + 1.3 * nL;
+            // measured device costs on config 4 (B200), in units of one P2P pair (0.52 ns): an M2L translation on
+            // tcgen05 ~1.05 ns = 2 pairs (175,692 flops at 168 TFLOP/s); P2M + L2P of a panel ~0.35 ns = 0.7; a near
+            // nonzero 3.1 ps = 0.006
+            double nnz = 0;
+            if (!nnz_row.empty())
+                for (int32_t p = hpb[L]; p < hpe[L]; ++p) nnz += (double)nnz_row[p];
+            w[i] = nL * src + 2.0 * m2l + 0.7 * nL + 0.006 * nnz;
         }
         std::vector<int64_t> cuts(T->part_world + 1);
         xrl_partition_cuts((int64_t)w.size(), w.data(), T->part_world, cuts.data());

@@ -337,5 +337,6 @@ xrl_status nccl_allreduce_sum_f64(xrl_ctx ctx, double* buf, size_t count, cudaSt
 void tree_release(xrl_tree t);
 void topo_release(xrl_topo T);     // delete if dead and unreferenced (then release its tree)
 void near_release(xrl_near nr);    // likewise for near fields
+std::vector<int64_t> near_row_counts(xrl_tree t, double eta, cudaStream_t st);  // near.cu
 void op_release(xrl_op op);        // likewise for operators (then release topology and tree)
 }  // namespace xrl
