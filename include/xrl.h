@@ -297,7 +297,8 @@ xrl_status xrl_mvm_host_batch(xrl_tree tree, xrl_near near, const void* const* x
 xrl_status xrl_ctx_set_sched(xrl_ctx ctx, int32_t mode);
 /* Fused P2P (default on; XRL_FUSE=0 at context creation turns it off): in the
  * forked schedules, three spare warps of the M2L kernel take P2P leaf tasks from
- * the counter the standalone P2P kernel uses.  Results equal the unfused path up
+ * the counter the standalone P2P kernel uses (not on trees partitioned more than
+ * 2 ways, where the rank's M2L is short).  Results equal the unfused path up
  * to FP32 summation order.  Errors: XRL_EINVAL for a null context. */
 xrl_status xrl_ctx_set_fuse(xrl_ctx ctx, int32_t on);
 

@@ -1245,7 +1245,10 @@ static Mvm mvm_make(xrl_tree t, xrl_near nr, float2* y, uint32_t flags, int sche
     M.do_far = flags != XRL_MVM_NEAR_ONLY;
     M.do_near = flags != XRL_MVM_FAR_ONLY;
     M.chain = M.do_far && t->nlevel > 1;
-    M.fuse = sched != 0 && ctx->fuse_p2p && M.chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0;
+    // the fused P2P warps pay off when the M2L is long and L2-bound (whole meshes, 2-way shards); on a rank's
+    // share of an 8-way partition the M2L is short and the warps only stretch it (projection: 5.77x fused vs
+    // 5.9x unfused at 8 ranks of config 4)
+    M.fuse = sched != 0 && ctx->fuse_p2p && M.chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0 && t->part_world <= 2;
     M.side_done = false;
     M.nl = t->p1 - t->p0;
     M.p0 = t->p0;
