@@ -385,8 +385,11 @@ xrl_status xrl_operator_create(xrl_tree tree, xrl_near near, xrl_topo topo, cons
 /* w = A v; v, w device complex64 [nrhs][n_loops] (partitioned: [nrhs][n_loops_local], collective over
  * the context's communicator; XRL_EUNSUPPORTED on a virtual rank), must not alias. */
 xrl_status xrl_operator_apply(xrl_op op, const void* v, void* w, int32_t nrhs);
-/* This rank's loop slice: first loop and count (0 and n_loops on a single-rank operator). */
-xrl_status xrl_operator_info(xrl_op op, int64_t* loop_offset, int64_t* n_loops_local);
+/* This rank's loop slice: first loop and count (0 and n_loops on a single-rank operator), and the
+ * apply's exchange volume per right-hand side: loop values and panel values sent + received (any
+ * pointer may be NULL). */
+xrl_status xrl_operator_info(xrl_op op, int64_t* loop_offset, int64_t* n_loops_local, int64_t* loop_halo,
+                             int64_t* panel_halo);
 /* Virtual ranks: the sharded operator of k operators built on the k trees of one xrl_mvm_vranks
  * partition (one single-rank context), applied in one call with device-copy exchanges; v[r], w[r]:
  * rank r's slices.  k = 1 with a single-rank operator is the plain apply. */

@@ -971,11 +971,14 @@ static xrl_status check_vrank_ops(int32_t k, const xrl_op* ops, const char* who)
     return XRL_OK;
 }
 
-xrl_status xrl_operator_info(xrl_op op, int64_t* loop_offset, int64_t* n_loops_local)
+xrl_status xrl_operator_info(xrl_op op, int64_t* loop_offset, int64_t* n_loops_local, int64_t* loop_halo,
+                             int64_t* panel_halo)
 {
     if (!op) { set_error("xrl_operator_info: null operator"); return XRL_EINVAL; }
     if (loop_offset) *loop_offset = op->part ? op->part->L0 : 0;
     if (n_loops_local) *n_loops_local = op->part ? op->part->nlo : op->topo->n_loops;
+    if (loop_halo) *loop_halo = op->part ? op->part->lh_soff.back() + op->part->lh_roff.back() : 0;
+    if (panel_halo) *panel_halo = op->part ? op->part->ph_soff.back() + op->part->ph_roff.back() : 0;
     return XRL_OK;
 }
 

@@ -148,7 +148,7 @@ def lib():
         L.xrl_precond_build.argtypes = [P, i32, pp]
         L.xrl_precond_build_exact.argtypes = [P, pp]
         L.xrl_precond_build_kind.argtypes = [P, i32, i32, pp]
-        L.xrl_operator_info.argtypes = [P, P, P]
+        L.xrl_operator_info.argtypes = [P, P, P, P, P]
         L.xrl_operator_apply_vranks.argtypes = [i32, P, P, P, i32]
         L.xrl_gmres_vranks.argtypes = [i32, P, P, P, P, i32, P, P, P, P, P]
         for name in ("xrl_operator_info", "xrl_operator_apply_vranks", "xrl_gmres_vranks"):
@@ -624,7 +624,13 @@ class Operator:
     def loops(self):
         """(first loop, count) of this rank's loop slice (0, n_loops on a single-rank operator)."""
         a, b = ctypes.c_int64(), ctypes.c_int64()
-        check(lib().xrl_operator_info(self.h, ctypes.byref(a), ctypes.byref(b)))
+        check(lib().xrl_operator_info(self.h, ctypes.byref(a), ctypes.byref(b), None, None))
+        return int(a.value), int(b.value)
+
+    def halo(self):
+        """Exchange volume of one apply per right-hand side: (loop values, panel values) sent + received."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().xrl_operator_info(self.h, None, None, ctypes.byref(a), ctypes.byref(b)))
         return int(a.value), int(b.value)
 
     def close(self):
