@@ -59,7 +59,7 @@ def main():
                                       .astype(np.complex64)).cuda()
         sl = [o.loops() for o in ops]
         bs = [b_full[:, s0:s0 + c].contiguous() for s0, c in sl]
-        xrl.gmres_vranks(ops, pcs, bs, max_iters=2, tol=1e-30)  # warm-up
+        xrl.gmres_vranks(ops, pcs, bs, max_iters=a.iters, tol=1e-30)  # warm-up (Krylov basis allocated)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -68,6 +68,14 @@ def main():
         torch.cuda.synchronize()
         it = int(rep["iters"][0])
         ms_iter_all = e0.elapsed_time(e1) / max(it, 1)
+        if k == 1:  # the single-GPU solver itself (xrl_gmres), beside the one-rank xrl_gmres_vranks
+            xrl.gmres(ops[0], pcs[0], bs[0], max_iters=a.iters, tol=1e-30)
+            torch.cuda.synchronize()
+            e0.record()
+            _, rep1 = xrl.gmres(ops[0], pcs[0], bs[0], max_iters=a.iters, tol=1e-30)
+            e1.record()
+            torch.cuda.synchronize()
+            res["xrl_gmres_ms_per_iter"] = e0.elapsed_time(e1) / max(int(rep1["iters"][0]), 1)
         # MVM projection inputs of this partition
         xs = []
         off = 0
