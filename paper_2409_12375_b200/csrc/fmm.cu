@@ -1019,427 +1019,6 @@ __global__ void __launch_bounds__(128) k_p2p(
                                 invW, accumulate, n, p0, y);
 }
 
-// ------------------------------------------------------------------ P2P on tcgen05
-// y_t += (1/W) sum_s G(t, s) q_s with G = 1/r: the kernel G is built on the CUDA cores (one target per
-// TMEM lane, two sources per packed FP32 instruction, MUFU rsqrt) and written to TMEM as the A operand,
-// split TF32 hi + lo; the charges are the B operand (precomputed TF32 hi/lo quad records, k_quads, copied
-// to shared memory with cp.async.bulk); the product sum_s G q runs on the tensor core (3xTF32, M128 N8G
-// K8, FP32 accumulation in TMEM).  Per pair the CUDA cores do 3 FADD2/2 + FMUL2/2 + 2 FFMA2/2 + FADD2/2
-// + LOP + MUFU instead of also the six accumulation FMAs, so the MUFU rsqrt (8 cycles per warp per 32
-// pairs) becomes the floor.
-//   Rows: a task (leaf, <= 128 targets) fills the 128 lanes as G = min(4, 128 / T) groups of T targets;
-//   group g takes the g-th run of C source slots of each chunk and owns the D columns 8g..8g+7, so small
-//   leaves still keep the lanes busy (the off-diagonal column blocks are wasted tensor work, G <= 4).
-//   Source slots are panel quads (4 panels, quad-aligned in the global order): a U-list leaf [pb, pe)
-//   covers quads pb/4 .. (pe-1)/4; slots of panels outside the leaf get far coordinates (G = 0).
-// Roles (192 threads): warps 0-3 compute (thread = TMEM lane = row), warp 4 loads (task fetch one task
-// ahead; per chunk one bulk copy of the planned coordinates and one of each source quad's charge record;
-// the plan, k_p2p_plan, is built once per tree), warp 5 issues the MMAs.
-// Pipeline: kPS shared-memory stages (coordinates, charge records; mbarriers src_full: loader -> compute /
-// MMA with the bytes as complete_tx, empty: MMA commit -> loader) deep enough to cover the copy latency,
-// and kPT TMEM stages (A_hi, A_lo; a_full: compute -> MMA, a_free: MMA commit -> compute); d_full (MMA
-// commit after a task's last chunk -> compute) and d_free (compute epilogue -> MMA).
-constexpr int kPC = 32;                                  // source slots per group per chunk
-constexpr int kPS = 8;                                   // shared-memory stages (coordinates + charge records)
-constexpr int kPT = 3;                                   // TMEM stages (A_hi, A_lo)
-constexpr int kPQuad = 256;                              // bytes per charge quad record (hi 8x4, lo 8x4 floats)
-constexpr int kPSlotLd = kPC + 4;                        // coordinate row stride per group (floats)
-constexpr int kPBBytes = 4 * (kPC / 4) * kPQuad;         // charge records per stage (G <= 4): 8 KB
-constexpr int kPCoordBytes = 3 * 4 * kPSlotLd * 4;       // x, y, z per stage
-constexpr int kPStageBytes = kPBBytes + kPCoordBytes;
-constexpr int kPTcSmem = kPS * kPStageBytes + 128 * 6 * 4 + 1024;
-constexpr uint32_t kPColD = 0, kPColA = 32;              // D: 32 columns (8G); TMEM stage s: A_hi at 32 + 64 s, A_lo + 32
-constexpr uint32_t kPTmemCols = 256;
-constexpr float kFar = 1e30f;                            // r^2 overflows to +inf: G = rsqrt(inf) = 0
-
-// charge quad records: rec[q] = {hi[r][i], lo[r][i]} (r = 0..7 RHS, i = 0..3 panel 4q + i), canonical
-// K-major core matrices (8 rows r x 16 bytes) for the B operand; quads [q0, q1)
-__global__ void k_quads(int64_t q0, int64_t q1, int64_t n, const float* __restrict__ xq, float* __restrict__ bq)
-{
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // (quad, r)
-    const int64_t q = q0 + (j >> 3);
-    const int r = (int)(j & 7);
-    if (q >= q1) return;
-    float v[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t p = 4 * q + i;
-        v[i] = p < n ? __ldg(xq + 8 * p + r) : 0.f;
-    }
-    float4 hi, lo;
-    hi.x = tc::tf32_rna(v[0]); lo.x = v[0] - hi.x;
-    hi.y = tc::tf32_rna(v[1]); lo.y = v[1] - hi.y;
-    hi.z = tc::tf32_rna(v[2]); lo.z = v[2] - hi.z;
-    hi.w = tc::tf32_rna(v[3]); lo.w = v[3] - hi.w;
-    float4* o = reinterpret_cast<float4*>(bq + 64 * q);
-    o[r] = hi;
-    o[8 + r] = lo;
-}
-// the same for the quads holding the listed panels (halo records of a sharded MVM)
-__global__ void k_quads_idx(int64_t m, const int32_t* __restrict__ idx, int64_t n, const float* __restrict__ xq,
-                            float* __restrict__ bq)
-{
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= 8 * m) return;
-    const int64_t q = idx[j >> 3] >> 2;
-    const int r = (int)(j & 7);
-    float v[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t p = 4 * q + i;
-        v[i] = p < n ? __ldg(xq + 8 * p + r) : 0.f;
-    }
-    float4 hi, lo;
-    hi.x = tc::tf32_rna(v[0]); lo.x = v[0] - hi.x;
-    hi.y = tc::tf32_rna(v[1]); lo.y = v[1] - hi.y;
-    hi.z = tc::tf32_rna(v[2]); lo.z = v[2] - hi.z;
-    hi.w = tc::tf32_rna(v[3]); lo.w = v[3] - hi.w;
-    float4* o = reinterpret_cast<float4*>(bq + 64 * q);
-    o[r] = hi;
-    o[8 + r] = lo;
-}
-
-struct PChunk {          // per-stage chunk header (loader -> compute / MMA)
-    int tb, tg, flags, b;  // first target panel; T | G << 16; bit0 first, bit1 last, bit2 self, bit3 end; leaf
-};
-
-__device__ __forceinline__ void ld_shared_v2u64(const void* p, f2x& a, f2x& b)
-{
-    asm volatile("ld.shared.v2.b64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "r"((unsigned)__cvta_generic_to_shared(p)));
-}
-// 16-byte asynchronous copy global -> shared (LDGSTS, L2 only) and the mbarrier arrival that fires when the
-// thread's prior copies have landed (the pending count is raised now and dropped on completion)
-__device__ __forceinline__ void cp_async16(void* dst, const void* src)
-{
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar)
-{
-    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-// G for the two sources of a packed pair (FTZ rsqrt; kSelf: the r = 0 self pair gives 0)
-template <bool kSelf>
-__device__ __forceinline__ void g_pair(f2x tx, f2x ty, f2x tz, f2x sx, f2x sy, f2x sz, float& g0, float& g1)
-{
-    const f2x dx = sub2(tx, sx), dy = sub2(ty, sy), dz = sub2(tz, sz);
-    const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
-    g0 = rsqrt_ftz(r2.x);
-    g1 = rsqrt_ftz(r2.y);
-    if (kSelf) {
-        g0 = r2.x > 0.f ? g0 : 0.f;
-        g1 = r2.y > 0.f ? g1 : 0.f;
-    }
-}
-
-template <bool kSelf>
-__device__ __forceinline__ void g_chunk(const float* sx, const float* sy, const float* sz, f2x tx, f2x ty, f2x tz,
-                                        float* hi, float* lo)
-{
-#pragma unroll
-    for (int k = 0; k < kPC; k += 4) {
-        f2x x01, x23, y01, y23, z01, z23;
-        ld_shared_v2u64(sx + k, x01, x23);
-        ld_shared_v2u64(sy + k, y01, y23);
-        ld_shared_v2u64(sz + k, z01, z23);
-        float g[4];
-        g_pair<kSelf>(tx, ty, tz, x01, y01, z01, g[0], g[1]);
-        g_pair<kSelf>(tx, ty, tz, x23, y23, z23, g[2], g[3]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) hi[k + i] = tc::tf32_rna(g[i]);
-        const f2x l01 = sub2(pk2(g[0], g[1]), pk2(hi[k], hi[k + 1]));
-        const f2x l23 = sub2(pk2(g[2], g[3]), pk2(hi[k + 2], hi[k + 3]));
-        const float2 a = upk2(l01), c = upk2(l23);
-        lo[k] = a.x; lo[k + 1] = a.y; lo[k + 2] = c.x; lo[k + 3] = c.y;
-    }
-}
-
-__global__ void __launch_bounds__(192, 2) k_p2p_tc(
-    const int4* __restrict__ tasks, int ntasks, int* __restrict__ counter, const int4* __restrict__ pmeta,
-    const int64_t* __restrict__ pcbase, const float* __restrict__ pchunks, const float4* __restrict__ loc,
-    const float* __restrict__ bq, float invW, int accumulate, int64_t n, int64_t p0, float2* __restrict__ y)
-{
-    extern __shared__ __align__(16) uint8_t psm_raw[];
-    uint8_t* psm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(psm_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar_src[kPS], bar_empty[kPS], bar_a[kPT], bar_afree[kPT], bar_d, bar_dfree;
-    __shared__ PChunk hdr[kPS];
-    __shared__ uint32_t tmem_base;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* red = reinterpret_cast<float*>(psm + kPS * kPStageBytes);  // [128][6] epilogue
-    auto stage_b = [&](int s) { return psm + s * kPStageBytes; };
-    auto stage_c = [&](int s) { return reinterpret_cast<float*>(psm + s * kPStageBytes + kPBBytes); };
-
-    // zero the charge stages once (slots never written in a chunk are multiplied by G = 0: keep them finite)
-    for (int i = threadIdx.x; i < kPS * kPStageBytes / 16; i += blockDim.x)
-        reinterpret_cast<float4*>(psm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kPS; ++s) {
-            tc::mbar_init(&bar_src[s], 1);
-            tc::mbar_init(&bar_empty[s], 1);
-        }
-        for (int s = 0; s < kPT; ++s) {
-            tc::mbar_init(&bar_a[s], 4);
-            tc::mbar_init(&bar_afree[s], 1);
-        }
-        tc::mbar_init(&bar_d, 1);
-        tc::mbar_init(&bar_dfree, 4);
-    }
-    if (warp == 0) tc::tmem_alloc<kPTmemCols>(&tmem_base);
-    tc::fence_proxy_async();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    const uint32_t tm = tmem_base;
-
-    if (warp == 4) {
-        // ---------------------------------------------------------------- loader
-        // per chunk: one bulk copy of the planned coordinates ([3][G][kPSlotLd], target frame) and one
-        // 256-byte copy per source quad of its charge record; the next task is claimed one task ahead
-        int chunk = 0;
-        int task = 0;
-        if (lane == 0) task = atomicAdd(counter, 1);
-        task = __shfl_sync(0xffffffffu, task, 0);
-        while (task < ntasks) {
-            const int4 tk = __ldg(tasks + task);
-            const int4 md = __ldg(pmeta + task);  // (#chunks, G, first, end chunk holding the leaf's own panels)
-            const float* rec0 = pchunks + __ldg(pcbase + task);
-            int next = 0;
-            if (lane == 0) next = atomicAdd(counter, 1);
-            next = __shfl_sync(0xffffffffu, next, 0);
-            const int nch = md.x, G = md.y;
-            const int recf = 116 * G;  // floats per chunk record: coordinates 108 G + quad ids 8 G
-            // quad ids kQD chunks ahead (the plan streams from HBM: one dependent load per chunk would bound
-            // the loop by the load latency)
-            auto qid = [&](int c) {
-                return (c < nch && lane < 8 * G)
-                           ? __ldg(reinterpret_cast<const int*>(rec0 + (int64_t)c * recf) + 108 * G + lane)
-                           : -1;
-            };
-            constexpr int kQD = 8;
-            int qr[kQD];
-#pragma unroll
-            for (int i = 0; i < kQD; ++i) qr[i] = qid(i);
-            for (int c = 0; c < nch; ++c) {
-                const int q = qr[0];
-#pragma unroll
-                for (int i = 0; i + 1 < kQD; ++i) qr[i] = qr[i + 1];
-                qr[kQD - 1] = qid(c + kQD);
-                const int s = chunk % kPS, rnd = chunk / kPS;
-                if (rnd > 0) tc::mbar_wait(&bar_empty[s], (rnd - 1) & 1);
-                // coordinates: 27 G 16-byte pieces; charge records: 16 pieces per quad, two quads per instruction
-                const float* rc = rec0 + (int64_t)c * recf;
-                for (int i = lane; i < 27 * G; i += 32) cp_async16(stage_c(s) + 4 * i, rc + 4 * i);
-                for (int j = 0; j < 8 * G; j += 2) {
-                    const int jq = j + (lane >> 4);
-                    const int qv = __shfl_sync(0xffffffffu, q, jq);
-                    if (qv >= 0)
-                        cp_async16(stage_b(s) + jq * kPQuad + 16 * (lane & 15), bq + 64 * (int64_t)qv + 4 * (lane & 15));
-                }
-                cp_async_arrive(&bar_src[s]);
-                if (lane == 0)
-                    hdr[s] = PChunk{tk.y, tk.z | (G << 16),
-                                    (c == 0 ? 1 : 0) | (c == nch - 1 ? 2 : 0) | (c >= md.z && c < md.w ? 4 : 0), tk.x};
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_src[s]);
-                ++chunk;
-            }
-            task = next;
-        }
-        const int s = chunk % kPS, rnd = chunk / kPS;
-        if (rnd > 0) tc::mbar_wait(&bar_empty[s], (rnd - 1) & 1);
-        if (lane == 0) {
-            hdr[s] = PChunk{0, 0, 8, 0};
-            mbar_arrive(&bar_src[s]);
-        }
-    } else if (warp == 5) {
-        // ---------------------------------------------------------------- MMA issuer
-        if (lane == 0) {
-            int chunk = 0, ntask = 0;
-            for (;;) {
-                const int s = chunk % kPS, rnd = chunk / kPS;
-                tc::mbar_wait(&bar_src[s], rnd & 1);
-                const PChunk h = hdr[s];
-                if (h.flags & 8) break;
-                const int G = h.tg >> 16;
-                const int sa = chunk % kPT;
-                if ((h.flags & 1) && ntask > 0) tc::mbar_wait(&bar_dfree, (ntask - 1) & 1);
-                tc::mbar_wait(&bar_a[sa], (chunk / kPT) & 1);
-                tc::fence_after();
-                tc::fence_proxy_async();  // charge records landed through the generic proxy (cp.async)
-                const uint32_t idesc = tc::idesc_tf32(128, 8 * G);
-                const uint32_t sb = tc::smem_u32(stage_b(s));
-                const uint32_t ah = tm + kPColA + 64 * sa, al = ah + 32;
-#pragma unroll
-                for (int j = 0; j < kPC / 8; ++j) {
-                    // K step j: slots 8j..8j+7 = quads 2j, 2j+1 (LBO = one record), groups SBO = 8 records
-                    const uint64_t bh = tc::smem_desc(sb + 2 * j * kPQuad, kPQuad, (kPC / 4) * kPQuad);
-                    const uint64_t bl = tc::smem_desc(sb + 2 * j * kPQuad + 128, kPQuad, (kPC / 4) * kPQuad);
-                    tc::mma_tf32_ts(tm + kPColD, ah + 8 * j, bh, idesc, ((h.flags & 1) && j == 0) ? 0u : 1u);
-                    tc::mma_tf32_ts(tm + kPColD, ah + 8 * j, bl, idesc, 1u);
-                    tc::mma_tf32_ts(tm + kPColD, al + 8 * j, bh, idesc, 1u);
-                }
-                tc::commit(&bar_empty[s]);
-                tc::commit(&bar_afree[sa]);
-                if (h.flags & 2) {
-                    tc::commit(&bar_d);
-                    ++ntask;
-                }
-                ++chunk;
-            }
-        }
-        __syncwarp();
-    } else {
-        // ---------------------------------------------------------------- compute (warps 0-3)
-        const int m = 32 * warp + lane;  // TMEM lane = row
-        const uint32_t tq = tm + ((uint32_t)(32 * warp) << 16);
-        int chunk = 0, ntask = 0;
-        f2x tx = 0, ty = 0, tz = 0;
-        int gx = 0, gy = 0, gz = 0, g = 0, T = 1, G = 1, tb = 0;
-        for (;;) {
-            const int s = chunk % kPS, rnd = chunk / kPS;
-            tc::mbar_wait(&bar_src[s], rnd & 1);
-            const PChunk h = hdr[s];
-            if (h.flags & 8) break;
-            if (h.flags & 1) {
-                T = h.tg & 0xFFFF;
-                G = h.tg >> 16;
-                tb = h.tb;
-                g = m / T;
-                const int t = m - g * T;
-                float4 p = make_float4(-kFar, -kFar, -kFar, 0.f);
-                if (g < G) p = __ldg(loc + tb + t);
-                tx = pk2(p.x, p.x);
-                ty = pk2(p.y, p.y);
-                tz = pk2(p.z, p.z);
-                const int gr = g < G ? g : 0;
-                gx = gr * kPSlotLd;
-                gy = (G + gr) * kPSlotLd;
-                gz = (2 * G + gr) * kPSlotLd;
-            }
-            const float* C = stage_c(s);
-            float hi[kPC], lo[kPC];
-            if (h.flags & 4) g_chunk<true>(C + gx, C + gy, C + gz, tx, ty, tz, hi, lo);
-            else g_chunk<false>(C + gx, C + gy, C + gz, tx, ty, tz, hi, lo);
-            const int sa = chunk % kPT;
-            if (chunk >= kPT) {
-                tc::mbar_wait(&bar_afree[sa], ((chunk / kPT) - 1) & 1);
-                tc::fence_after();
-            }
-            tc::tmem_st32(tq + kPColA + 64 * sa, hi);
-            tc::tmem_st32(tq + kPColA + 64 * sa + 32, lo);
-            tc::tmem_st_wait();
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_a[sa]);
-            ++chunk;
-            if (h.flags & 2) {
-                // epilogue: D row m, column block g -> red / y
-                tc::mbar_wait(&bar_d, ntask & 1);
-                tc::fence_after();
-                float v[32];
-                tc::tmem_ld32(tq + kPColD, v);
-                float o[6];
-#pragma unroll
-                for (int r = 0; r < 6; ++r) o[r] = g == 0 ? v[r] : g == 1 ? v[8 + r] : g == 2 ? v[16 + r] : v[24 + r];
-                tc::fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_dfree);
-                ++ntask;
-                if (G > 1) {
-#pragma unroll
-                    for (int r = 0; r < 6; ++r) red[m * 6 + r] = o[r];
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (m < T) {
-                        for (int gg = 1; gg < G; ++gg)
-#pragma unroll
-                            for (int r = 0; r < 6; ++r) o[r] += red[(gg * T + m) * 6 + r];
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                }
-                if (m < T) {
-                    const int64_t k = tb + m - p0;
-#pragma unroll
-                    for (int r = 0; r < 6; ++r) o[r] *= invW;
-                    if (accumulate) {
-                        const float2 a = y[k], c = y[n + k], d = y[2 * n + k];
-                        o[0] += a.x; o[1] += a.y; o[2] += c.x; o[3] += c.y; o[4] += d.x; o[5] += d.y;
-                    }
-                    y[k] = make_float2(o[0], o[1]);
-                    y[n + k] = make_float2(o[2], o[3]);
-                    y[2 * n + k] = make_float2(o[4], o[5]);
-                }
-            }
-        }
-    }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (warp == 0) tc::tmem_dealloc<kPTmemCols>(tm);
-}
-
-// The P2P plan of k_p2p_tc (built once per tree): per task, its U-list source quads (quad-aligned panel
-// ranges of the U-list leaves, flattened in list order) cut into chunks of G groups x 8 quads; per chunk
-// the source coordinates in the target leaf's frame ([3][G][kPSlotLd] floats; panels of a quad outside
-// its leaf and the chunk's padding at +-far: G = 0) and the 8 G global quad ids (-1: padding).
-// tu[e] = (leaf, first quad, flattened prefix, first panel) for the task's entries [tuoff[i], tuoff[i+1])
-// (the last one a sentinel holding the total).
-__global__ void k_p2p_plan(const int4* __restrict__ tasks, const int4* __restrict__ pmeta,
-                           const int64_t* __restrict__ pcbase, const int* __restrict__ tuoff,
-                           const int4* __restrict__ tu, const int32_t* __restrict__ pe,
-                           const int32_t* __restrict__ level, const int32_t* __restrict__ ix,
-                           const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
-                           const float4* __restrict__ loc, float* __restrict__ pchunks)
-{
-    const int task = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int4 tk = tasks[task];
-    const int4 md = pmeta[task];
-    const int nch = md.x, G = md.y;
-    const int e0 = tuoff[task], e1 = tuoff[task + 1] - 1;  // entries [e0, e1), sentinel e1
-    const int totq = tu[e1].z;
-    const float3 cb = box_center(level[tk.x], ix[tk.x], iy[tk.x], iz[tk.x]);
-    const int g = lane >> 3, lq = lane & 7;
-    for (int c = warp; c < nch; c += blockDim.x >> 5) {
-        float* rec = pchunks + pcbase[task] + (int64_t)c * 116 * G;
-        if (g >= G) continue;
-        const int f = (c * G + g) * 8 + lq;
-        float px[4], py[4], pz[4];
-        int qid = -1;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) px[i] = py[i] = pz[i] = kFar;
-        if (f < totq) {
-            int lo = e0, hi = e1 - 1;  // last entry with prefix <= f
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (tu[mid].z <= f) lo = mid; else hi = mid - 1;
-            }
-            const int4 e = tu[lo];
-            const int64_t gq = (int64_t)e.y + (f - e.z);
-            const int s = e.x, a = e.w, b = pe[s];
-            const float3 cs = box_center(level[s], ix[s], iy[s], iz[s]);
-            const float3 d = make_float3(cs.x - cb.x, cs.y - cb.y, cs.z - cb.z);
-            qid = (int)gq;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int64_t p = 4 * gq + i;
-                if (p >= a && p < b) {
-                    const float4 v = loc[p];
-                    px[i] = v.x + d.x; py[i] = v.y + d.y; pz[i] = v.z + d.z;
-                }
-            }
-        }
-        reinterpret_cast<float4*>(rec + (0 * G + g) * kPSlotLd)[lq] = make_float4(px[0], px[1], px[2], px[3]);
-        reinterpret_cast<float4*>(rec + (1 * G + g) * kPSlotLd)[lq] = make_float4(py[0], py[1], py[2], py[3]);
-        reinterpret_cast<float4*>(rec + (2 * G + g) * kPSlotLd)[lq] = make_float4(pz[0], pz[1], pz[2], pz[3]);
-        reinterpret_cast<int*>(rec)[108 * G + lane] = qid;
-    }
-}
-
 // ell[r][k] (r-major, M2L/L2L layout) -> ellk[k][8] (k-major, 6 RHS + 2 pad) for the leaves: the L2P
 // then reads one 32-byte record per coefficient instead of 6 scalars.
 __global__ void k_ell_kmajor(const int32_t* __restrict__ leaves, const float* __restrict__ ell, float* __restrict__ ellk)
@@ -1607,58 +1186,10 @@ void upload_constants(xrl_ctx ctx)
     upload_tc_images(ctx->ops.m2l_tc, ops);
     XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2p, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2PSmem));
-    XRL_CUDA(cudaFuncSetAttribute(k_p2p_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kPTcSmem));
     XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2m, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2MSmem));
-}
-
-
-// The tensor-core P2P plan of a tree (k_p2p_plan): tasks ord (leaf, first target, #targets <= 128), U lists
-// (hup, hus) and leaf panel ranges (hpb, hpe) on the host.
-void p2p_plan_build(xrl_tree T, const std::vector<int4>& ord, const std::vector<int64_t>& hup,
-                    const std::vector<int32_t>& hus, const std::vector<int32_t>& hpb, const std::vector<int32_t>& hpe,
-                    cudaStream_t st)
-{
-    const int nt = (int)ord.size();
-    std::vector<int4> meta(std::max(1, nt)), tu;
-    std::vector<int64_t> cbase(std::max(1, nt));
-    std::vector<int> tuoff(nt + 1);
-    int64_t tot = 0;
-    for (int i = 0; i < nt; ++i) {
-        const int L = ord[i].x, G = std::min(4, 128 / ord[i].z);
-        tuoff[i] = (int)tu.size();
-        int pref = 0, s0 = 0, s1 = 0;
-        for (int64_t q = hup[L]; q < hup[L + 1]; ++q) {
-            const int s = hus[q], qa = hpb[s] >> 2, qb = (hpe[s] + 3) >> 2;
-            if (s == L) { s0 = pref; s1 = pref + (qb - qa); }
-            tu.push_back(make_int4(s, qa, pref, hpb[s]));
-            pref += qb - qa;
-        }
-        tu.push_back(make_int4(-1, 0, pref, 0));
-        const int per = 8 * G, nch = (pref + per - 1) / per;
-        meta[i] = make_int4(nch, G, s1 > s0 ? s0 / per : 0, s1 > s0 ? (s1 - 1) / per + 1 : 0);
-        cbase[i] = tot;
-        tot += (int64_t)nch * 116 * G;
-    }
-    tuoff[nt] = (int)tu.size();
-    T->p2p_meta.alloc(meta.size());
-    T->p2p_cbase.alloc(cbase.size());
-    T->p2p_chunks.alloc(std::max<int64_t>(4, tot));
-    T->p2p_plan_bytes = 4 * tot;
-    if (nt == 0) return;
-    DBuf<int4> dtu(tu.size()), dtasks(nt);
-    DBuf<int> dtuoff(tuoff.size());
-    XRL_CUDA(cudaMemcpyAsync(T->p2p_meta.p, meta.data(), sizeof(int4) * nt, cudaMemcpyHostToDevice, st));
-    XRL_CUDA(cudaMemcpyAsync(T->p2p_cbase.p, cbase.data(), 8 * nt, cudaMemcpyHostToDevice, st));
-    XRL_CUDA(cudaMemcpyAsync(dtu.p, tu.data(), sizeof(int4) * tu.size(), cudaMemcpyHostToDevice, st));
-    XRL_CUDA(cudaMemcpyAsync(dtuoff.p, tuoff.data(), 4 * tuoff.size(), cudaMemcpyHostToDevice, st));
-    XRL_CUDA(cudaMemcpyAsync(dtasks.p, ord.data(), sizeof(int4) * nt, cudaMemcpyHostToDevice, st));
-    k_p2p_plan<<<nt, 256, 0, st>>>(dtasks.p, T->p2p_meta.p, T->p2p_cbase.p, dtuoff.p, dtu.p, T->bpe.p, T->blevel.p,
-                                   T->bix.p, T->biy.p, T->biz.p, T->loc.p, T->p2p_chunks.p);
-    XRL_LAUNCH_CHECK();
-    XRL_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace xrl
@@ -1783,16 +1314,6 @@ static void launch_near(Mvm& M)
     XRL_CUDA(cudaEventRecord(ctx->ev_join, M.side));
 }
 
-// XRL_P2P_TC=0: the SIMT P2P (k_p2p) instead of the tensor-core one
-static bool p2p_tc_enabled()
-{
-    static const bool on = [] {
-        const char* e = std::getenv("XRL_P2P_TC");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 // fork the side stream: the P2P (FP32-bound; shares SMs well with the tensor-core M2L), then the near
 // SpMV unless it must wait for the P2P tasks fused into the M2L kernel
 static void mvm_side(Mvm& M)
@@ -1806,26 +1327,7 @@ static void mvm_side(Mvm& M)
     if (M.halo) XRL_CUDA(cudaStreamWaitEvent(M.side, M.halo, 0));  // the P2P reads remote charges
     if (M.do_far) {
         phase_begin(ctx, PH_P2P, &ev, M.side);
-        if (t->n_own_leaves > 0 && p2p_tc_enabled()) {
-            // charge quad records of the owned panels and of the halo (the P2P's sources), then the
-            // tensor-core P2P on a persistent grid (2 CTAs per SM)
-            const int64_t q0 = M.p0 >> 2, q1 = (M.p0 + M.nl + 3) >> 2;
-            k_quads<<<nblk(8 * (q1 - q0), 256), 256, 0, M.side>>>(q0, q1, t->n, t->xq.p, t->bq.p);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
-            const int64_t nh = M.nr->halo_roff.empty() ? 0 : M.nr->halo_roff.back();
-            if (nh > 0) {
-                k_quads_idx<<<nblk(8 * nh, 256), 256, 0, M.side>>>(nh, M.nr->halo_ridx.p, t->n, t->xq.p, t->bq.p);
-                XRL_LAUNCH_CHECK();
-                ctx->launches += 1;
-            }
-            const int grid = std::min(t->n_p2p_tasks, 2 * ctx->num_sms);
-            k_p2p_tc<<<grid, 192, kPTcSmem, M.side>>>(t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p, t->p2p_meta.p,
-                                                      t->p2p_cbase.p, t->p2p_chunks.p, t->loc.p, t->bq.p, M.invW, 0,
-                                                      M.nl, M.p0, M.y);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
-        } else if (t->n_own_leaves > 0) {
+        if (t->n_own_leaves > 0) {
             k_p2p<<<t->n_p2p_tasks, 128, kP2PSmem, M.side>>>(t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p,
                                                             t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
                                                             t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,

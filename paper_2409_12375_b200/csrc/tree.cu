@@ -897,7 +897,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
                 for (int64_t q = hup[L]; q < hup[L + 1]; ++q) src += hpe[hus[q]] - hpb[hus[q]];
                 const int nt = hpe[L] - hpb[L];
                 for (int o = 0; o < nt;) {
-                    const int c = (nt - o > 128) ? 128 : nt - o;
+                    const int c = (nt - o > 256) ? 256 : nt - o;
                     cost.push_back({-(int64_t)c * src, make_int4(L, hpb[L] + o, c, 0)});
                     o += c;
                 }
@@ -905,7 +905,6 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
             std::stable_sort(cost.begin(), cost.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
             std::vector<int4> ord;
             for (auto& c : cost) ord.push_back(c.second);
-            p2p_plan_build(T.get(), ord, hup, hus, hpb, hpe, st);
             T->n_p2p_tasks = (int)ord.size();
             T->p2p_tasks.alloc(std::max<size_t>(1, ord.size()));
             if (!ord.empty())
@@ -1165,8 +1164,6 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     T->xq.alloc((size_t)n * 8);
     XRL_CUDA(cudaMemsetAsync(T->mu.p, 0, T->mu.bytes(), st));
     XRL_CUDA(cudaMemsetAsync(T->xq.p, 0, T->xq.bytes(), st));
-    T->bq.alloc((size_t)((n + 3) / 4) * 64);
-    XRL_CUDA(cudaMemsetAsync(T->bq.p, 0, T->bq.bytes(), st));
     XRL_CUDA(cudaStreamSynchronize(st));
     cref.keep = true;
     *out = T.release();

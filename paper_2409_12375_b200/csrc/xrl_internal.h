@@ -202,11 +202,6 @@ struct xrl_tree_s {
     xrl::DBuf<float> ell;                    // [nbox][kEllStride] ell[r][k]
     xrl::DBuf<float> ellk;                   // [nbox][kEllKStride] ellk[k][8] (leaves, per MVM)
     xrl::DBuf<float> xq;                     // [n][8] packed charges
-    xrl::DBuf<float> bq;                     // [ceil(n/4)][64] charge quad records (TF32 hi/lo, k_p2p_tc)
-    xrl::DBuf<int4> p2p_meta;                // per P2P task: (#chunks, G, first, end self chunk) (k_p2p_tc plan)
-    xrl::DBuf<int64_t> p2p_cbase;            // per P2P task: first float of its chunk records
-    xrl::DBuf<float> p2p_chunks;             // chunk records: coordinates [3][G][36] + quad ids [8G]
-    int64_t p2p_plan_bytes = 0;
     xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging
     xrl::DBuf<float2> xbuf[2], ybuf[2];       // xrl_mvm_host_batch double buffers
 };
@@ -325,9 +320,6 @@ void exact_free(xrl_precond pc);
 void phase_begin(xrl_ctx ctx, int ph, cudaEvent_t* evb, cudaStream_t st);
 void phase_end(xrl_ctx ctx, int ph, cudaEvent_t evb, cudaStream_t st);
 void upload_constants(xrl_ctx ctx);
-void p2p_plan_build(xrl_tree T, const std::vector<int4>& ord, const std::vector<int64_t>& hup,
-                    const std::vector<int32_t>& hus, const std::vector<int32_t>& hpb, const std::vector<int32_t>& hpe,
-                    cudaStream_t st);
 void ctx_release(xrl_ctx ctx);     // delete if dead and unreferenced
 xrl_status comm_init(xrl_ctx ctx, const void* unique_id);
 void comm_destroy(xrl_ctx ctx);
