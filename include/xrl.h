@@ -420,7 +420,10 @@ xrl_status xrl_precond_build_exact(xrl_op op, xrl_precond* out);
  *     L_ee the diagonal of the edge-edge matrix sum_t A_t P A_t^T (each edge's
  *     two panels: their P self terms and their mutual near entry).
  * block_size 1..64: block-Jacobi (FP64 Gauss-Jordan per block, complex64
- * storage); -1: the whole Q factorised (as xrl_precond_build_exact).
+ * storage); -1: the whole Q factorised (as xrl_precond_build_exact); -2: an
+ * incomplete LU(0) of the whole Q (reverse Cuthill-McKee order, FP64 complex,
+ * factorised on the GPU by cuSPARSE csrilu02 -- no host factorisation), applied
+ * by the same two GPU triangular solves.
  * Errors as xrl_precond_build / xrl_precond_build_exact, plus XRL_EINVAL for
  * a bad kind and XRL_EGEOM if an edge's panel pair is missing from the near
  * field. */

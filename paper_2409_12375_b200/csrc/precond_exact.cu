@@ -68,6 +68,16 @@ struct Api {
     decltype(&cusparseSpSV_bufferSize) svBuffer;
     decltype(&cusparseSpSV_analysis) svAnalysis;
     decltype(&cusparseSpSV_solve) svSolve;
+    // incomplete LU(0) on the GPU (legacy csrilu02, complex FP64)
+    int (*iluCreate)(void**);
+    int (*iluDestroy)(void*);
+    int (*iluBuffer)(cusparseHandle_t, int, int, const MatDescr, cuDoubleComplex*, const int*, const int*, void*, int*);
+    int (*iluAnalysis)(cusparseHandle_t, int, int, const MatDescr, const cuDoubleComplex*, const int*, const int*,
+                       void*, int, void*);
+    int (*iluFactor)(cusparseHandle_t, int, int, const MatDescr, cuDoubleComplex*, const int*, const int*, void*, int,
+                     void*);
+    int (*iluZeroPivot)(cusparseHandle_t, void*, int*);
+    int (*rcm)(SpHandle, int, int, const MatDescr, const int*, const int*, int*);
     std::string err;
 };
 
@@ -119,6 +129,13 @@ Api& api()
     a.svAnalysis = (decltype(a.svAnalysis))sym(hp, "cusparseSpSV_analysis");
     a.svSolve = (decltype(a.svSolve))sym(hp, "cusparseSpSV_solve");
     a.metisnd = (decltype(a.metisnd))dlsym(hs, "cusolverSpXcsrmetisndHost");  // optional
+    a.iluCreate = (decltype(a.iluCreate))sym(hp, "cusparseCreateCsrilu02Info");
+    a.iluDestroy = (decltype(a.iluDestroy))sym(hp, "cusparseDestroyCsrilu02Info");
+    a.iluBuffer = (decltype(a.iluBuffer))sym(hp, "cusparseZcsrilu02_bufferSize");
+    a.iluAnalysis = (decltype(a.iluAnalysis))sym(hp, "cusparseZcsrilu02_analysis");
+    a.iluFactor = (decltype(a.iluFactor))sym(hp, "cusparseZcsrilu02");
+    a.iluZeroPivot = (decltype(a.iluZeroPivot))sym(hp, "cusparseXcsrilu02_zeroPivot");
+    a.rcm = (decltype(a.rcm))sym(hs, "cusolverSpXcsrsymrcmHost");
     a.ok = ok;
     return a;
 }
@@ -143,9 +160,11 @@ struct Exact {
     cusparseSpMatDescr_t mL = nullptr, mU = nullptr;
     cusparseDnVecDescr_t vB = nullptr, vY = nullptr;
     cusparseSpSVDescr_t sL = nullptr, sU = nullptr;
+    void* ilu_info = nullptr;
     ~Exact()
     {
         Api& A = api();
+        if (ilu_info) A.iluDestroy(ilu_info);
         if (sL) A.svDestroy(sL);
         if (sU) A.svDestroy(sU);
         if (vB) A.destroyDnVec(vB);
@@ -272,6 +291,83 @@ void assemble_q(xrl_op op, int qkind, std::vector<std::vector<int32_t>>& rc,
     }
 }
 
+// ILU(0) of B = Q(perm, perm) on the GPU (cuSPARSE csrilu02, FP64 complex, in place on B's pattern): the
+// incomplete factors L (unit lower) and U share B's arrays; the apply is the exact path's two triangular
+// solves with gin = gout = perm.
+static xrl_status ilu_build(xrl_precond pc, std::unique_ptr<Exact>& E, const std::vector<int>& bp,
+                            const std::vector<int>& bc, const std::vector<cuDoubleComplex>& bv)
+{
+    Api& A = api();
+    const int N = E->n, nnz = (int)bc.size();
+    cudaStream_t st = pc->op->tree->ctx->stream;
+    E->gin.alloc(N);
+    E->gout.alloc(N);
+    XRL_CUDA(cudaMemcpyAsync(E->gin.p, E->perm.data(), 4 * (size_t)N, cudaMemcpyHostToDevice, st));
+    XRL_CUDA(cudaMemcpyAsync(E->gout.p, E->perm.data(), 4 * (size_t)N, cudaMemcpyHostToDevice, st));
+    E->lp.alloc(N + 1);
+    E->lc.alloc(std::max(1, nnz));
+    E->lv.alloc(std::max(1, nnz));
+    XRL_CUDA(cudaMemcpyAsync(E->lp.p, bp.data(), 4 * (size_t)(N + 1), cudaMemcpyHostToDevice, st));
+    XRL_CUDA(cudaMemcpyAsync(E->lc.p, bc.data(), 4 * (size_t)nnz, cudaMemcpyHostToDevice, st));
+    XRL_CUDA(cudaMemcpyAsync(E->lv.p, bv.data(), 16 * (size_t)nnz, cudaMemcpyHostToDevice, st));
+    E->db.alloc(N);
+    E->dy.alloc(N);
+    if (A.spCreateH(&E->sh) || A.spSetStream(E->sh, st) || A.iluCreate(&E->ilu_info)) {
+        set_error("xrl_precond_build_kind: cuSPARSE ILU(0) setup failed");
+        return XRL_ECUDA;
+    }
+    int bytes = 0;
+    if (A.iluBuffer(E->sh, N, nnz, E->descr, E->lv.p, E->lp.p, E->lc.p, E->ilu_info, &bytes)) {
+        set_error("xrl_precond_build_kind: ILU(0) buffer size failed");
+        return XRL_ECUDA;
+    }
+    DBuf<char> buf(std::max(bytes, 16));
+    const int policy = 1;  // CUSPARSE_SOLVE_POLICY_USE_LEVEL
+    if (A.iluAnalysis(E->sh, N, nnz, E->descr, E->lv.p, E->lp.p, E->lc.p, E->ilu_info, policy, buf.p) ||
+        A.iluFactor(E->sh, N, nnz, E->descr, E->lv.p, E->lp.p, E->lc.p, E->ilu_info, policy, buf.p)) {
+        set_error("xrl_precond_build_kind: ILU(0) factorisation failed");
+        return XRL_ECUDA;
+    }
+    int zp = -1;
+    const int zs = A.iluZeroPivot(E->sh, E->ilu_info, &zp);  // synchronises
+    if (zs == 3 /* CUSPARSE_STATUS_ZERO_PIVOT */ || zp >= 0) {
+        set_error("xrl_precond_build_kind: ILU(0) zero pivot at row %d", zp);
+        return XRL_ESINGULAR;
+    }
+    E->nnz_l = E->nnz_u = nnz;
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+    cusparseFillMode_t lo = CUSPARSE_FILL_MODE_LOWER, upm = CUSPARSE_FILL_MODE_UPPER;
+    cusparseDiagType_t unit = CUSPARSE_DIAG_TYPE_UNIT, nonunit = CUSPARSE_DIAG_TYPE_NON_UNIT;
+    bool bad = A.createCsr(&E->mL, N, N, nnz, E->lp.p, E->lc.p, E->lv.p, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I,
+                           CUSPARSE_INDEX_BASE_ZERO, CUDA_C_64F) ||
+               A.createCsr(&E->mU, N, N, nnz, E->lp.p, E->lc.p, E->lv.p, CUSPARSE_INDEX_32I, CUSPARSE_INDEX_32I,
+                           CUSPARSE_INDEX_BASE_ZERO, CUDA_C_64F) ||
+               A.setAttr(E->mL, CUSPARSE_SPMAT_FILL_MODE, &lo, sizeof(lo)) ||
+               A.setAttr(E->mL, CUSPARSE_SPMAT_DIAG_TYPE, &unit, sizeof(unit)) ||
+               A.setAttr(E->mU, CUSPARSE_SPMAT_FILL_MODE, &upm, sizeof(upm)) ||
+               A.setAttr(E->mU, CUSPARSE_SPMAT_DIAG_TYPE, &nonunit, sizeof(nonunit)) ||
+               A.createDnVec(&E->vB, N, E->db.p, CUDA_C_64F) || A.createDnVec(&E->vY, N, E->dy.p, CUDA_C_64F) ||
+               A.svCreate(&E->sL) || A.svCreate(&E->sU);
+    size_t szL = 0, szU = 0;
+    bad = bad || A.svBuffer(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mL, E->vB, E->vY, CUDA_C_64F,
+                            CUSPARSE_SPSV_ALG_DEFAULT, E->sL, &szL) ||
+          A.svBuffer(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mU, E->vY, E->vB, CUDA_C_64F,
+                     CUSPARSE_SPSV_ALG_DEFAULT, E->sU, &szU);
+    if (!bad) {
+        E->bufL.alloc(std::max<size_t>(szL, 16));
+        E->bufU.alloc(std::max<size_t>(szU, 16));
+        bad = A.svAnalysis(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mL, E->vB, E->vY, CUDA_C_64F,
+                           CUSPARSE_SPSV_ALG_DEFAULT, E->sL, E->bufL.p) ||
+              A.svAnalysis(E->sh, CUSPARSE_OPERATION_NON_TRANSPOSE, &one, E->mU, E->vY, E->vB, CUDA_C_64F,
+                           CUSPARSE_SPSV_ALG_DEFAULT, E->sU, E->bufU.p);
+    }
+    if (bad) { set_error("xrl_precond_build_kind: cuSPARSE triangular-solve setup failed"); return XRL_ECUDA; }
+    XRL_CUDA(cudaStreamSynchronize(st));
+    E->dev = true;
+    pc->exact = E.release();
+    return XRL_OK;
+}
+
 xrl_status exact_build(xrl_precond pc)
 {
     Api& A = api();
@@ -299,7 +395,16 @@ xrl_status exact_build(xrl_precond pc)
     }
     // ---- fill-reducing ordering (Q's pattern is symmetric)
     E->perm.resize(N);
-    int st = A.metisnd ? A.metisnd(E->h, N, nnz, E->descr, qp.data(), qc.data(), nullptr, E->perm.data()) : 1;
+    // (ILU(0): reverse Cuthill-McKee, a bandwidth ordering -- nested dissection orders the separators last,
+    // which suits a complete factorisation but leaves an incomplete one with the weakest couplings)
+    int st = 1;
+    if (pc->ilu) {
+        static const bool natural = getenv("XRL_ILU_NATURAL") != nullptr;
+        st = natural ? 1 : A.rcm(E->h, N, nnz, E->descr, qp.data(), qc.data(), E->perm.data());
+        if (st) std::iota(E->perm.begin(), E->perm.end(), 0);
+        st = 0;
+    }
+    if (st) st = A.metisnd ? A.metisnd(E->h, N, nnz, E->descr, qp.data(), qc.data(), nullptr, E->perm.data()) : 1;
     if (st) st = A.symamd(E->h, N, nnz, E->descr, qp.data(), qc.data(), E->perm.data());
     if (st) std::iota(E->perm.begin(), E->perm.end(), 0);
     std::vector<int> inv(N);
@@ -321,6 +426,7 @@ xrl_status exact_build(xrl_precond pc)
             }
         }
     }
+    if (pc->ilu) return ilu_build(pc, E, bp, bc, bv);
     // ---- LU with partial pivoting (threshold 1), factorised once
     size_t internal = 0, wbytes = 0;
     if (A.createLuInfo(&E->info) || A.luAnalysis(E->h, N, nnz, E->descr, bp.data(), bc.data(), E->info) ||

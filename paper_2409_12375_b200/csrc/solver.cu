@@ -1067,7 +1067,7 @@ static xrl_status precond_build_blocks(xrl_op op, int32_t qkind, int32_t block_s
     return XRL_OK;
 }
 
-static xrl_status precond_build_exact_kind(xrl_op op, int32_t qkind, xrl_precond* out)
+static xrl_status precond_build_exact_kind(xrl_op op, int32_t qkind, xrl_precond* out, int ilu = 0)
 {
     if (op->part) {
         set_error("the exact Q^-1 is not sharded: partitioned operators use block-Jacobi preconditioners");
@@ -1078,6 +1078,7 @@ static xrl_status precond_build_exact_kind(xrl_op op, int32_t qkind, xrl_precond
     pc->op = op;
     pc->kind = 1;
     pc->qkind = qkind;
+    pc->ilu = ilu;
     pc->bs = 0;
     const xrl_status s = exact_build(pc.get());
     if (s != XRL_OK) return s;
@@ -1101,12 +1102,12 @@ xrl_status xrl_precond_build_kind(xrl_op op, int32_t kind, int32_t block_size, x
     if (!op || !out) { set_error("xrl_precond_build_kind: null argument"); return XRL_EINVAL; }
     *out = nullptr;
     if (kind != XRL_PRECOND_DIAG_P && kind != XRL_PRECOND_DIAG_L) { set_error("xrl_precond_build_kind: bad kind %d", kind); return XRL_EINVAL; }
-    if (block_size != -1 && (block_size < 1 || block_size > kBS)) {
-        set_error("xrl_precond_build_kind: block_size must be -1 (exact) or 1..%d", kBS);
+    if (block_size != -1 && block_size != -2 && (block_size < 1 || block_size > kBS)) {
+        set_error("xrl_precond_build_kind: block_size must be -1 (exact), -2 (ILU(0)) or 1..%d", kBS);
         return XRL_EINVAL;
     }
     API_TRY
-        if (block_size < 0) return precond_build_exact_kind(op, kind, out);
+        if (block_size < 0) return precond_build_exact_kind(op, kind, out, block_size == -2);
         return precond_build_blocks(op, kind, block_size, out);
     API_CATCH
 }

@@ -293,7 +293,8 @@ struct xrl_op_s {
 
 struct xrl_precond_s {
     xrl_op op = nullptr;
-    int32_t kind = 0;                            // 0 block-Jacobi (k_block_*), 1 exact sparse LU (precond_exact.cpp)
+    int32_t kind = 0;                            // 0 block-Jacobi (k_block_*), 1 whole Q (precond_exact.cu)
+    int32_t ilu = 0;                             // kind 1: 0 exact sparse LU (host), 1 ILU(0) on the GPU
     int32_t qkind = 0;                           // Q: 0 diagonal-of-P (Eq. 10), 1 diagonal-of-L
     void* exact = nullptr;                       // kind 1: factorisation state
     int32_t bs = 64, nblocks = 0;

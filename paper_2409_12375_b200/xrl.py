@@ -648,14 +648,18 @@ class Operator:
 class Precond:
     """xrl_precond_build: block-Jacobi diagonal-of-P preconditioner (Eq. 10); exact=True:
     xrl_precond_build_exact, the whole Q factorised (sparse LU, NEXT f2); kind="diag_l": the
-    diagonal-of-L baseline of PAPER.md:120-122 (xrl_precond_build_kind)."""
+    diagonal-of-L baseline of PAPER.md:120-122 (xrl_precond_build_kind); ilu=True: ILU(0) of the whole Q
+    on the GPU (cuSPARSE), no host factorisation."""
 
     KINDS = {"diag_p": 0, "diag_l": 1}
 
-    def __init__(self, op: Operator, block_size: int = 64, exact: bool = False, kind: str = "diag_p"):
+    def __init__(self, op: Operator, block_size: int = 64, exact: bool = False, kind: str = "diag_p",
+                 ilu: bool = False):
         self.op = op
         h = ctypes.c_void_p()
-        if kind != "diag_p":
+        if ilu:  # ILU(0) of the whole Q on the GPU (xrl_precond_build_kind, block_size -2)
+            check(lib().xrl_precond_build_kind(op.h, self.KINDS[kind], -2, ctypes.byref(h)))
+        elif kind != "diag_p":
             check(lib().xrl_precond_build_kind(op.h, self.KINDS[kind], -1 if exact else block_size, ctypes.byref(h)))
         elif exact:
             check(lib().xrl_precond_build_exact(op.h, ctypes.byref(h)))

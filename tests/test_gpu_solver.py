@@ -507,6 +507,29 @@ def test_diag_p_vs_diag_l_iterations(coils_all):
     assert np.abs(zz["diag_p"] - zz["diag_l"]).max() / np.abs(zz["diag_p"]).max() < 1e-3
 
 
+def test_ilu0_precond_coils(coils_all):
+    """The whole-Q ILU(0) factorised on the GPU (block_size -2): on the coil pair at 100 MHz it converges
+    (fewer iterations than block-Jacobi, more than the exact Q^-1) to the same port impedance as the exact
+    preconditioner."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m, ctx, tree, near, topo = coils_all
+    op = xrl.Operator(tree, near, topo, 1e8, sigma=SIGMA, zeta=5e-6)
+    b = torch.zeros((2, topo.n_loops), dtype=torch.complex64, device="cuda")
+    for p in range(2):
+        topo.port_rhs(p, 1.0, out=b[p:p + 1])
+    it, zz = {}, {}
+    for name, pc in (("ilu0", xrl.Precond(op, kind="diag_p", ilu=True)), ("exact", xrl.Precond(op, exact=True)),
+                     ("block", xrl.Precond(op, 64))):
+        x, rep = xrl.gmres(op, pc, b, tol=1e-6, max_iters=3000)
+        assert rep["converged"].all(), name
+        it[name] = int(rep["iters"].max())
+        zz[name] = np.linalg.inv(topo.port_currents(x).T)
+    print("coils 100 MHz, tol 1e-6: iterations", it)
+    assert it["exact"] <= it["ilu0"] < it["block"]
+    assert np.abs(zz["ilu0"] - zz["exact"]).max() / np.abs(zz["exact"]).max() < 1e-3
+
+
 @pytest.mark.parametrize("cfg,world", [(1, 2), (1, 3), (2, 4)])
 def test_sharded_operator_and_gmres_virtual_ranks(cfg, world):
     """SURVEY §8(e) "GMRES extras" on one GPU (virtual ranks): k operators on the k trees of a partition own

@@ -1,7 +1,7 @@
 """Table IV analogue: setup time and GMRES iterations of the diagonal-
 of-P preconditioner (Eq. 10) against the traditional diagonal-of-L one, each as
-block-Jacobi (64-loop blocks, GPU) and as the whole Q factorised (host sparse LU, the paper's Pardiso
-role), plus no preconditioner, at the paper's Table IV tolerance 1e-6 (right preconditioning, restart 50).
+block-Jacobi (64-loop blocks, GPU), as the whole Q factorised (host sparse LU, the paper's Pardiso
+role) and as an incomplete LU(0) of the whole Q factorised on the GPU, plus no preconditioner, at the paper's Table IV tolerance 1e-6 (right preconditioning, restart 50).
 
     python tools/table4.py [--configs 1,2,4] [--freq 1e8] [--max-iters 1000] [--out file.json]
 
@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--max-iters", type=int, default=1000)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only-ilu", action="store_true")
     a = ap.parse_args()
     out = {"tol": a.tol, "freq_hz": a.freq, "restart": 50, "rows": []}
     for cfg in [int(c) for c in a.configs.split(",")]:
@@ -50,10 +51,13 @@ def main():
             rng = np.random.default_rng(1404)
             b = torch.from_numpy((rng.random((1, nl)) - 0.5 + 1j * (rng.random((1, nl)) - 0.5)).astype(np.complex64)).cuda()
             rhs = "1 random loop vector (seed 1404)"
-        for kind, exact in (("none", False), ("diag_p", False), ("diag_l", False), ("diag_p", True), ("diag_l", True)):
+        for kind, exact in (("none", False), ("diag_p", False), ("diag_l", False), ("diag_p", True), ("diag_l", True),
+                            ("diag_p", "ilu"), ("diag_l", "ilu")):
+            if a.only_ilu and exact != "ilu":
+                continue
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            pc = None if kind == "none" else xrl.Precond(op, 64, exact=exact, kind=kind)
+            pc = None if kind == "none" else xrl.Precond(op, 64, exact=exact is True, kind=kind, ilu=exact == "ilu")
             torch.cuda.synchronize()
             setup = time.perf_counter() - t0
             t0 = time.perf_counter()
@@ -61,7 +65,8 @@ def main():
             torch.cuda.synchronize()
             solve = time.perf_counter() - t0
             row = {"config": cfg, "n_panels": m.n, "n_loops": nl, "rhs": rhs,
-                   "preconditioner": kind + (" (exact Q^-1)" if exact else " (block-Jacobi 64)" if kind != "none" else ""),
+                   "preconditioner": kind + (" (ILU(0) on the GPU)" if exact == "ilu" else " (exact Q^-1)" if exact
+                                             else " (block-Jacobi 64)" if kind != "none" else ""),
                    "setup_s": round(setup, 3), "iters": rep["iters"].tolist(), "converged": rep["converged"].tolist(),
                    "true_rre": [float(v) for v in rep["true_rre"]], "solve_s": round(solve, 3)}
             print(json.dumps(row), flush=True)
