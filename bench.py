@@ -297,10 +297,12 @@ def multi_gpu_projection(xrl, mesh, ctx, x_lib, ms_1gpu, args, k=8):
     info = [xrl.exchange_info(t, n) for t, n in zip(trees, nears)]
     byts = [32 * (i["halo_send"] + i["halo_recv"]) + 3072 * (i["let_send"] + i["let_recv"]) + 2 * 3072 * i["shared"]
             for i in info]
-    # the halo overlaps the up pass (comm stream); the all-reduce and the LET are on the critical path
-    halo_ms = 1e3 * (max(32 * (i["halo_send"] + i["halo_recv"]) for i in info) / 900e9 + 15e-6)
+    # the halo overlaps the up pass (comm stream); the all-reduce and the LET are on the critical path.  NVLink 5
+    # is 900 GB/s per direction: a rank's sends and receives of one exchange proceed concurrently, so an
+    # exchange costs max(sent, received) bytes / 900 GB/s; the shared-box all-reduce moves 2x its bytes each way
+    halo_ms = 1e3 * (max(32 * max(i["halo_send"], i["halo_recv"]) for i in info) / 900e9 + 15e-6)
     up_ms = ph.get("pack", 0.0) + ph.get("p2m", 0.0) + ph.get("m2m", 0.0)
-    mu_ms = 1e3 * max(3072 * (i["let_send"] + i["let_recv"]) + 2 * 3072 * i["shared"] for i in info) / 900e9
+    mu_ms = 1e3 * max(3072 * max(i["let_send"], i["let_recv"]) + 2 * 3072 * i["shared"] for i in info) / 900e9
     comm_ms = max(0.0, halo_ms - up_ms) + mu_ms + 1e3 * 2 * 15e-6
     t_k = float(rank_ms.max()) + comm_ms
     out = {"k": k, "projected_ms": t_k, "rank_ms": [round(float(v), 4) for v in rank_ms], "comm_ms": comm_ms,
@@ -308,7 +310,8 @@ def multi_gpu_projection(xrl, mesh, ctx, x_lib, ms_1gpu, args, k=8):
            "projected_value": mesh.n / (t_k * 1e-3) / 1e6, "unit": "Mpanels/s",
            "halo_ms": halo_ms, "up_pass_ms": up_ms,
            "how": "virtual ranks on one GPU (xrl_mvm_vranks): max over ranks of each rank's MVM alone + the exposed "
-                  "exchange time over NVLink 5 (900 GB/s, 15 us per exchange; the halo overlaps the up pass); "
+                  "exchange time over NVLink 5 (900 GB/s per direction: max(sent, received) per exchange, 15 us "
+                  "each; the halo overlaps the up pass); "
                   "a projection, not a multi-GPU measurement"}
     del ys, xs, nears, trees
     torch.cuda.empty_cache()

@@ -90,7 +90,7 @@ def main():
         # the operator's loop / panel halos (8 B per loop value, 24 B per panel value, one RHS), 5 all-reduces
         comm = 0.0
         if k > 1:
-            mu = max(3072 * (i["let_send"] + i["let_recv"]) + 2 * 3072 * i["shared"] for i in info) / 900e9
+            mu = max(3072 * max(i["let_send"], i["let_recv"]) + 2 * 3072 * i["shared"] for i in info) / 900e9
             op_halo = 2 * LAT + max(8 * o.halo()[0] + 24 * o.halo()[1] for o in ops) / 900e9
             comm = mu + 2 * LAT + op_halo + 5 * LAT
         proj = ms_iter_all / k * imb + 1e3 * comm

@@ -6,8 +6,9 @@ plans, exchanges and kernels as the multi-rank xrl_mvm; exchanges as device copi
 groups run alone on the whole GPU with the production (forked, fused) schedule, so its measured device
 time is what one GPU would spend on that rank's share.  The projection is
     t(k) = max_r t_rank(r) + t_comm(k),
-    t_comm = max(0, t_halo - t_up) + (LET + shared bytes of the busiest rank) / 900 GB/s + 2 x 15 us,
-    t_halo = halo bytes of the busiest rank / 900 GB/s (NVLink 5 per direction) + 15 us:
+    t_comm = max(0, t_halo - t_up) + (max(LET sent, received) + 2 x shared bytes of the busiest rank) / 900 GB/s
+             + 2 x 15 us,
+    t_halo = max(halo sent, received) of the busiest rank / 900 GB/s (NVLink 5, per direction) + 15 us:
 the halo of x overlaps the up pass (xrl_mvm issues it on its comm stream while P2M / M2M read only the rank's
 own charges), the shared-box all-reduce and the LET exchange are on the critical path.  The single-GPU references are the
 same driver at k = 1 and xrl_mvm itself.
@@ -64,7 +65,7 @@ def main():
     del near, tree, y
     torch.cuda.empty_cache()
     res = {"config": a.config, "n_panels": m.n, "leaf_max": a.leaf, "t1_forked_ms": t_fork,
-           "model": "t(k) = max_r t_rank(r) + max(0, t_halo - t_up) + (LET + shared bytes) / 900 GB/s + 2 x 15 us", "ks": {}}
+           "model": "t(k) = max_r t_rank(r) + max(0, t_halo - t_up) + (max(LET sent, recv) + 2 shared bytes) / 900 GB/s + 2 x 15 us", "ks": {}}
     for k in [int(v) for v in a.ks.split(",")]:
         t0 = time.perf_counter()
         trees, nears, xs, off = [], [], [], 0
@@ -97,9 +98,10 @@ def main():
                 2 * 3072 * i["shared"] for i in info]
         # the halo overlaps the up pass (P2M + M2M read only the rank's own charges; xrl_mvm issues the halo on
         # its comm stream): only what exceeds the up pass is exposed; the all-reduce and the LET are not overlapped
-        halo_s = max(32 * (i["halo_send"] + i["halo_recv"]) for i in info) / (NVLINK_GBS * 1e9) + LAT_S
+        # NVLink 5 is full duplex (900 GB/s per direction): an exchange costs max(sent, received) / 900 GB/s
+        halo_s = max(32 * max(i["halo_send"], i["halo_recv"]) for i in info) / (NVLINK_GBS * 1e9) + LAT_S
         up_s = 1e-3 * (phases.get("p2m", 0.0) + phases.get("m2m", 0.0) + phases.get("pack", 0.0))
-        mu_s = max(3072 * (i["let_send"] + i["let_recv"]) + 2 * 3072 * i["shared"] for i in info) / (NVLINK_GBS * 1e9)
+        mu_s = max(3072 * max(i["let_send"], i["let_recv"]) + 2 * 3072 * i["shared"] for i in info) / (NVLINK_GBS * 1e9)
         comm_s = (max(0.0, halo_s - up_s) + mu_s + 2 * LAT_S) if k > 1 else 0.0
         t_k = float(rank_med.max()) + 1e3 * comm_s
         res["ks"][k] = {"rank_ms": rank_med.tolist(), "t_rank_max_ms": float(rank_med.max()),
