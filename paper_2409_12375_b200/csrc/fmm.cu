@@ -1019,6 +1019,286 @@ __global__ void __launch_bounds__(128) k_p2p(
                                 invW, accumulate, n, p0, y);
 }
 
+// ------------------------------------------------------------------ two triples in one P2P / near pass
+// xrl_mvm with nvec = 6k runs the triples in pairs: the P2P computes r and 1/r once per pair for 12 right-hand
+// sides (per pair 3 FADD2/2 + FMUL2/2 + FFMA2 + 6 FFMA2 per target pair instead of twice 3 + 3: 25 % fewer
+// FP32-pipe instructions per right-hand side) and the near SpMV streams its 6-byte entries once for both.
+// The second triple's charges are packed into xq2; 4 targets per thread keep the accumulators at 48 registers.
+constexpr int kTPT12 = 8;
+constexpr int kTP212 = kTPT12 / 2;
+constexpr int kSrcChunk12 = 512;
+constexpr int kP2PSmem12 = (kSrcChunk12 * 20 > 128 * (kTP212 * 12 + 1) * 2 ? kSrcChunk12 * 20 : 128 * (kTP212 * 12 + 1) * 2) * 4;
+
+template <bool kSelf>
+__device__ __forceinline__ void p2p_range12(int j0, int j1, int S, const float4* __restrict__ Sp,
+                                            const float4 (*__restrict__ Sq)[4], const f2x* tx, const f2x* ty,
+                                            const f2x* tz, f2x (*acc)[12])
+{
+#pragma unroll 2
+    for (int j = j0; j < j1; j += S) {
+        const float4 sp = Sp[j];
+        const float4 q0 = Sq[j][0], q1 = Sq[j][1], q2 = Sq[j][2], q3 = Sq[j][3];
+        const f2x sx = pk2(sp.x, sp.x), sy = pk2(sp.y, sp.y), sz = pk2(sp.z, sp.z);
+        const float c[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y};
+#pragma unroll
+        for (int q = 0; q < kTP212; ++q) {
+            const f2x dx = sub2(tx[q], sx), dy = sub2(ty[q], sy), dz = sub2(tz[q], sz);
+            const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
+            float ra = rsqrt_ftz(r2.x), rb = rsqrt_ftz(r2.y);
+            if (kSelf) {
+                ra = r2.x > 0.f ? ra : 0.f;
+                rb = r2.y > 0.f ? rb : 0.f;
+            }
+            const f2x ri = pk2(ra, rb);
+#pragma unroll
+            for (int r = 0; r < 12; ++r) fma2_acc(acc[q][r], pk2(c[r], c[r]), ri);
+        }
+    }
+}
+
+// p2p_leaf for two triples: targets [tb, te) of leaf b, charges xq (triple 1) and xq2 (triple 2), results
+// stored into y and y2 (each [3][n], accumulate as p2p_leaf).  128 threads, __syncthreads.
+__device__ void p2p_leaf12(int b, int tb, int te, int tid, float* smraw, P2PWin& W, const int32_t* __restrict__ level,
+                           const int32_t* __restrict__ ix, const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
+                           const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
+                           const int64_t* __restrict__ uptr, const int32_t* __restrict__ usrc,
+                           const float4* __restrict__ loc, const float* __restrict__ xq, const float* __restrict__ xq2,
+                           float invW, int accumulate, int64_t n, int64_t p0, float2* __restrict__ y,
+                           float2* __restrict__ y2)
+{
+    constexpr int kNT = 128, kChunk = kSrcChunk12;
+    float4* Sp = reinterpret_cast<float4*>(smraw);
+    float4(*Sq)[4] = reinterpret_cast<float4(*)[4]>(smraw + 4 * kChunk);
+    f2x(*Red)[kTP212 * 12 + 1] = reinterpret_cast<f2x(*)[kTP212 * 12 + 1]>(smraw);
+    int* Uoff = W.Uoff;
+    int* Uid = W.Uid;
+    int* Upb = W.Upb;
+    float3* Ud = W.Ud;
+    int* wsum = W.wsum;
+    const float3 cb = box_center(level[b], ix[b], iy[b], iz[b]);
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int t0 = tb; t0 < te; t0 += kNT * kTPT12) {
+        const int T = min(kNT * kTPT12, te - t0);
+        const int NG = (T + kTPT12 - 1) / kTPT12;
+        const int S = max(1, kNT / NG);
+        const int tg = tid % NG, sg = tid / NG;
+        const bool act = sg < S;
+        f2x tx[kTP212], ty[kTP212], tz[kTP212];
+        f2x acc[kTP212][12];
+#pragma unroll
+        for (int q = 0; q < kTP212; ++q) {
+            float4 p[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ti = tg * kTPT12 + 2 * q + h;
+                p[h] = make_float4(1e18f, 1e18f, 1e18f, 0.f);
+                if (act && ti < T) p[h] = loc[t0 + ti];
+            }
+            float2* tp = reinterpret_cast<float2*>(smraw) + (tid * kTP212 + q) * 3;
+            tp[0] = make_float2(p[0].x, p[1].x);
+            tp[1] = make_float2(p[0].y, p[1].y);
+            tp[2] = make_float2(p[0].z, p[1].z);
+            tx[q] = ld_shared_u64(tp);
+            ty[q] = ld_shared_u64(tp + 1);
+            tz[q] = ld_shared_u64(tp + 2);
+#pragma unroll
+            for (int r = 0; r < 12; ++r) acc[q][r] = 0ull;
+        }
+        for (int64_t u0 = uptr[b]; u0 < uptr[b + 1]; u0 += kUWin) {
+            const int nu = (int)min((int64_t)kUWin, uptr[b + 1] - u0);
+            __syncthreads();
+            int sz = 0;
+            if (tid < kUWin) {
+                if (tid < nu) {
+                    const int s = usrc[u0 + tid];
+                    Uid[tid] = s;
+                    Upb[tid] = pb[s];
+                    sz = pe[s] - pb[s];
+                    const float3 cs = box_center(level[s], ix[s], iy[s], iz[s]);
+                    Ud[tid] = make_float3(cs.x - cb.x, cs.y - cb.y, cs.z - cb.z);
+                }
+                int inc = sz;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                if (lane == 31) wsum[warp] = inc;
+                Uoff[tid + 1] = inc;
+            }
+            __syncthreads();
+            if (tid >= 32 && tid < kUWin) Uoff[tid + 1] += wsum[0];
+            if (tid == 0) Uoff[0] = 0;
+            __syncthreads();
+            const int total = Uoff[nu];
+            int self_lo = 0, self_hi = 0;
+            for (int i = 0; i < nu; ++i)
+                if (Uid[i] == b) { self_lo = Uoff[i]; self_hi = Uoff[i + 1]; }
+            for (int s0 = 0; s0 < total; s0 += kChunk) {
+                const int sn = min(kChunk, total - s0);
+                if (s0 > 0) __syncthreads();
+                for (int j = tid; j < sn; j += kNT) {
+                    const int f = s0 + j;
+                    const int li = find_seg(Uoff, nu, f);
+                    const int i = Upb[li] + (f - Uoff[li]);
+                    const float3 d = Ud[li];
+                    const float4 p = loc[i];
+                    Sp[j] = make_float4(p.x + d.x, p.y + d.y, p.z + d.z, 0.f);
+                    const float4* qa = reinterpret_cast<const float4*>(xq + 8 * (int64_t)i);
+                    const float4* qb = reinterpret_cast<const float4*>(xq2 + 8 * (int64_t)i);
+                    Sq[j][0] = qa[0];
+                    Sq[j][1] = qa[1];
+                    Sq[j][2] = qb[0];
+                    Sq[j][3] = qb[1];
+                }
+                __syncthreads();
+                if (act) {
+                    const int a0 = max(0, min(sn, self_lo - s0)), a1 = max(0, min(sn, self_hi - s0));
+                    p2p_range12<false>(first_in_class(0, sg, S), a0, S, Sp, Sq, tx, ty, tz, acc);
+                    p2p_range12<true>(first_in_class(a0, sg, S), a1, S, Sp, Sq, tx, ty, tz, acc);
+                    p2p_range12<false>(first_in_class(a1, sg, S), sn, S, Sp, Sq, tx, ty, tz, acc);
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kTP212; ++q)
+#pragma unroll
+            for (int r = 0; r < 12; ++r) st_shared_u64(&Red[tid][q * 12 + r], acc[q][r]);
+        __syncthreads();
+        for (int ti = tid; ti < T; ti += kNT) {
+            const int g0 = ti / kTPT12, q = (ti % kTPT12) >> 1, h = ti & 1;
+            float tot[12];
+#pragma unroll
+            for (int r = 0; r < 12; ++r) {
+                float f = 0.f;
+                for (int gg = 0; gg < S; ++gg) f += reinterpret_cast<const float*>(&Red[g0 + gg * NG][q * 12 + r])[h];
+                tot[r] = f * invW;
+            }
+            const int64_t k = t0 + ti - p0;
+            if (accumulate) {
+                const float2 a = y[k], c = y[n + k], d = y[2 * n + k];
+                const float2 a2 = y2[k], c2 = y2[n + k], d2 = y2[2 * n + k];
+                tot[0] += a.x; tot[1] += a.y; tot[2] += c.x; tot[3] += c.y; tot[4] += d.x; tot[5] += d.y;
+                tot[6] += a2.x; tot[7] += a2.y; tot[8] += c2.x; tot[9] += c2.y; tot[10] += d2.x; tot[11] += d2.y;
+            }
+            y[k] = make_float2(tot[0], tot[1]);
+            y[n + k] = make_float2(tot[2], tot[3]);
+            y[2 * n + k] = make_float2(tot[4], tot[5]);
+            y2[k] = make_float2(tot[6], tot[7]);
+            y2[n + k] = make_float2(tot[8], tot[9]);
+            y2[2 * n + k] = make_float2(tot[10], tot[11]);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(128) k_p2p12(
+    const int4* __restrict__ tasks, int ntasks, int* __restrict__ counter, const int32_t* __restrict__ level,
+    const int32_t* __restrict__ ix, const int32_t* __restrict__ iy, const int32_t* __restrict__ iz,
+    const int32_t* __restrict__ pb, const int32_t* __restrict__ pe, const int64_t* __restrict__ uptr,
+    const int32_t* __restrict__ usrc, const float4* __restrict__ loc, const float* __restrict__ xq,
+    const float* __restrict__ xq2, float invW, int64_t n, int64_t p0, float2* __restrict__ y, float2* __restrict__ y2)
+{
+    extern __shared__ __align__(16) float smraw[];
+    __shared__ P2PWin W;
+    __shared__ int task;
+    if (threadIdx.x == 0) task = atomicAdd(counter, 1);
+    __syncthreads();
+    if (task >= ntasks) return;
+    const int4 tk = tasks[task];
+    p2p_leaf12(tk.x, tk.y, tk.y + tk.z, threadIdx.x, smraw, W, level, ix, iy, iz, pb, pe, uptr, usrc, loc, xq, xq2,
+               invW, 0, n, p0, y, y2);
+}
+
+// the near SpMV of k_near_seg for two triples: one pass over the entries, gathers from xq and xq2
+__global__ void __launch_bounds__(256, 3) k_near_seg12(int64_t nseg, const int32_t* __restrict__ seg_row,
+                                                       const int32_t* __restrict__ seg_base,
+                                                       const int64_t* __restrict__ seg_off,
+                                                       const float* __restrict__ eval, const uint16_t* __restrict__ eoff,
+                                                       const float* __restrict__ xq, const float* __restrict__ xq2,
+                                                       int64_t nl, float2* __restrict__ y, float2* __restrict__ y2)
+{
+    const int64_t team = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+    const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) >> 3;
+    const int l8 = threadIdx.x & 7;
+    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+    int64_t s = team;
+    int64_t b0 = 0, b1 = 0;
+    int32_t base = 0;
+    if (s < nseg) { b0 = __ldg(seg_off + s); b1 = __ldg(seg_off + s + 1); base = __ldg(seg_base + s); }
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint2 o = make_uint2(0u, 0u);
+    if (s < nseg && b0 + 4 * l8 < b1) { v = ldg_stream4(eval + b0 + 4 * l8, pol_stream); o = ldg_stream_u64(eoff + b0 + 4 * l8, pol_stream); }
+    while (s < nseg) {
+        const int64_t sn = s + nteams;
+        int64_t n0 = 0, n1 = 0;
+        int32_t nbase = 0;
+        if (sn < nseg) { n0 = __ldg(seg_off + sn); n1 = __ldg(seg_off + sn + 1); nbase = __ldg(seg_base + sn); }
+        const int32_t row = __ldg(seg_row + s);
+        const float* xb = xq + 8 * (int64_t)base;
+        const float* xb2 = xq2 + 8 * (int64_t)base;
+        float a[12];
+#pragma unroll
+        for (int r = 0; r < 12; ++r) a[r] = 0.f;
+        const int nit = (int)((b1 - b0 + 31) >> 5);
+        for (int it = 0; it < nit; ++it) {
+            const int64_t pos = b0 + 32 * it + 4 * l8;
+            if (pos >= b1) {
+                v = make_float4(0.f, 0.f, 0.f, 0.f);
+                o = make_uint2(0u, 0u);
+            }
+            const uint32_t c0 = o.x & 0xffff, c1 = o.x >> 16, c2 = o.y & 0xffff, c3 = o.y >> 16;
+            const float w0 = v.x, w1 = v.y, w2 = v.z, w3 = v.w;
+            const int64_t np = it + 1 < nit ? pos + 32 : n0 + 4 * l8;
+            const int64_t ne = it + 1 < nit ? b1 : n1;
+            if ((it + 1 < nit || sn < nseg) && np < ne) {
+                v = ldg_stream4(eval + np, pol_stream);
+                o = ldg_stream_u64(eoff + np, pol_stream);
+            }
+            float q[4][8];
+            ldg256_l1_keep(xb + 8 * c0, q[0], pol_keep);
+            ldg256_l1_keep(xb + 8 * c1, q[1], pol_keep);
+            ldg256_l1_keep(xb + 8 * c2, q[2], pol_keep);
+            ldg256_l1_keep(xb + 8 * c3, q[3], pol_keep);
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+                a[r] = fmaf(w0, q[0][r], a[r]);
+                a[r] = fmaf(w1, q[1][r], a[r]);
+                a[r] = fmaf(w2, q[2][r], a[r]);
+                a[r] = fmaf(w3, q[3][r], a[r]);
+            }
+            ldg256_l1_keep(xb2 + 8 * c0, q[0], pol_keep);
+            ldg256_l1_keep(xb2 + 8 * c1, q[1], pol_keep);
+            ldg256_l1_keep(xb2 + 8 * c2, q[2], pol_keep);
+            ldg256_l1_keep(xb2 + 8 * c3, q[3], pol_keep);
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+                a[6 + r] = fmaf(w0, q[0][r], a[6 + r]);
+                a[6 + r] = fmaf(w1, q[1][r], a[6 + r]);
+                a[6 + r] = fmaf(w2, q[2][r], a[6 + r]);
+                a[6 + r] = fmaf(w3, q[3][r], a[6 + r]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 12; ++r) {
+#pragma unroll
+            for (int d = 1; d < 8; d <<= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], d);
+        }
+        if (l8 < 6) {
+            const int c = l8 % 3;
+            float re, im;
+            if (l8 < 3) { re = c == 0 ? a[0] : (c == 1 ? a[2] : a[4]); im = c == 0 ? a[1] : (c == 1 ? a[3] : a[5]); }
+            else { re = c == 0 ? a[6] : (c == 1 ? a[8] : a[10]); im = c == 0 ? a[7] : (c == 1 ? a[9] : a[11]); }
+            red_add2((l8 < 3 ? y : y2) + c * nl + row, re, im);
+        }
+        s = sn;
+        b0 = n0;
+        b1 = n1;
+        base = nbase;
+    }
+}
+
 // ell[r][k] (r-major, M2L/L2L layout) -> ellk[k][8] (k-major, 6 RHS + 2 pad) for the leaves: the L2P
 // then reads one 32-byte record per coefficient instead of 6 scalars.
 __global__ void k_ell_kmajor(const int32_t* __restrict__ leaves, const float* __restrict__ ell, float* __restrict__ ellk)
@@ -1186,6 +1466,7 @@ void upload_constants(xrl_ctx ctx)
     upload_tc_images(ctx->ops.m2l_tc, ops);
     XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2p, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2PSmem));
+    XRL_CUDA(cudaFuncSetAttribute(k_p2p12, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2PSmem12));
     XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
     for (int i = 0; i < 343; ++i) ctx->ops.m2l_index[i] = ops.m2l_index[i];
     XRL_CUDA(cudaFuncSetAttribute(k_p2l, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2LSmem));
@@ -1229,6 +1510,9 @@ struct Mvm {
     float invW;
     cudaEvent_t halo = nullptr;  // multi-rank, overlapped halo: the P2P / P2L wait for it
     bool p2l_early = false;      // the P2L ran on the comm stream during the up pass (L2L waits for ev_p2l)
+    float* xq = nullptr;         // this triple's packed charges (t->xq, or t->xq2 for the second of a pair)
+    const float* xq2 = nullptr;  // pair mode (first triple): the second triple's charges; the side stream's
+    float2* y2 = nullptr;        //   P2P / near SpMV serve both triples and also write y2
 };
 
 static Mvm mvm_make(xrl_tree t, xrl_near nr, float2* y, uint32_t flags, int sched)
@@ -1253,6 +1537,7 @@ static Mvm mvm_make(xrl_tree t, xrl_near nr, float2* y, uint32_t flags, int sche
     M.nl = t->p1 - t->p0;
     M.p0 = t->p0;
     M.invW = (float)(1.0 / t->W);
+    M.xq = t->xq.p;
     return M;
 }
 
@@ -1268,7 +1553,7 @@ static void mvm_begin(Mvm& M, const float2* x)
     cudaEvent_t ev;
     phase_begin(ctx, PH_PACK, &ev, M.st);
     if (M.nl > 0) {
-        k_pack<<<nblk(M.nl, 256), 256, 0, M.st>>>(M.nl, x, t->xq.p + 8 * M.p0);
+        k_pack<<<nblk(M.nl, 256), 256, 0, M.st>>>(M.nl, x, M.xq + 8 * M.p0);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
     }
@@ -1301,7 +1586,14 @@ static void launch_near(Mvm& M)
         phase_begin(ctx, PH_NEAR, &ev, M.side);
         // the SpMV adds into y: in the near-only mode it starts from zero
         if (!M.do_far && M.nl > 0) XRL_CUDA(cudaMemsetAsync(M.y, 0, sizeof(float2) * 3 * (size_t)M.nl, M.side));
-        if (nr->n_segs > 0) {
+        if (!M.do_far && M.nl > 0 && M.y2) XRL_CUDA(cudaMemsetAsync(M.y2, 0, sizeof(float2) * 3 * (size_t)M.nl, M.side));
+        if (nr->n_segs > 0 && M.xq2) {
+            const int grid = (int)std::min<int64_t>(nblk(8 * nr->n_segs, 256), 3 * ctx->num_sms);
+            k_near_seg12<<<grid, 256, 0, M.side>>>(nr->n_segs, nr->seg_row.p, nr->seg_base.p, nr->seg_off.p,
+                                                   nr->eval.p, nr->eoff.p, M.xq, M.xq2, M.nl, M.y, M.y2);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+        } else if (nr->n_segs > 0) {
             const int grid = (int)std::min<int64_t>(nblk(8 * nr->n_segs, 256), 4 * ctx->num_sms);
             k_near_seg<<<grid, 256, 0, M.side>>>(nr->n_segs, nr->seg_row.p, nr->seg_base.p,
                                                                       nr->seg_off.p, nr->eval.p, nr->eoff.p, t->xq.p,
@@ -1327,10 +1619,17 @@ static void mvm_side(Mvm& M)
     if (M.halo) XRL_CUDA(cudaStreamWaitEvent(M.side, M.halo, 0));  // the P2P reads remote charges
     if (M.do_far) {
         phase_begin(ctx, PH_P2P, &ev, M.side);
-        if (t->n_own_leaves > 0) {
+        if (t->n_own_leaves > 0 && M.xq2) {
+            k_p2p12<<<t->n_p2p_tasks, 128, kP2PSmem12, M.side>>>(t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p,
+                                                                t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
+                                                                t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, M.xq,
+                                                                M.xq2, M.invW, M.nl, M.p0, M.y, M.y2);
+            XRL_LAUNCH_CHECK();
+            ctx->launches += 1;
+        } else if (t->n_own_leaves > 0) {
             k_p2p<<<t->n_p2p_tasks, 128, kP2PSmem, M.side>>>(t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p,
                                                             t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
-                                                            t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p,
+                                                            t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, M.xq,
                                                             M.invW, 0, M.nl, M.p0, M.y);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
@@ -1349,7 +1648,7 @@ static void launch_p2l(Mvm& M, cudaStream_t st)
     phase_begin(ctx, PH_P2L, &ev, st);
     if (t->n_x_targets > 0) {
         k_p2l<<<t->n_x_targets, 128, kP2LSmem, st>>>(t->x_targets.p, t->x_ptr.p, t->x_src.p, t->blevel.p, t->bix.p,
-                                                     t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->loc.p, t->xq.p, t->ell.p);
+                                                     t->biy.p, t->biz.p, t->bpb.p, t->bpe.p, t->loc.p, M.xq, t->ell.p);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
     }
@@ -1377,7 +1676,7 @@ static void mvm_up(Mvm& M)
     zero_boxes(ctx, t->mu_zero, t->n_mu_zero, t->nbox, t->mu, M.st);  // parents accumulate the M2M reductions
     if (t->n_own_leaves > 0) {
         k_p2m<<<t->n_own_leaves, 128, kP2MSmem, M.st>>>(t->own_leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p,
-                                                         t->xq.p, t->mu.p);
+                                                         M.xq, t->mu.p);
         XRL_LAUNCH_CHECK();
         ctx->launches += 1;
     }
@@ -1437,7 +1736,7 @@ static void mvm_down(Mvm& M)
             P2PTasks tasks{};
             if (M.fuse)
                 tasks = P2PTasks{t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
-                                 t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, t->xq.p, M.invW, M.nl,
+                                 t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, M.xq, M.invW, M.nl,
                                  M.p0, M.y};
             k_m2l_tc<<<grid, kTcThreads, kTcSmem, M.st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p,
                                                           t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu.p,
@@ -1559,6 +1858,51 @@ static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y
     return XRL_OK;
 }
 
+// Two triples of a single-rank tree: the side stream's P2P and near SpMV serve both (k_p2p12, k_near_seg12:
+// one pass over the U lists and the near entries for 12 right-hand sides); the FMM expansions (mu, ell: one
+// triple's worth of tree scratch) run for the first triple, then for the second, on the work stream.
+static void mvm_pair(xrl_tree t, xrl_near nr, const float2* xa, float2* ya, const float2* xb, float2* yb,
+                     uint32_t flags)
+{
+    xrl_ctx ctx = t->ctx;
+    if (t->xq2.n < t->xq.n) {
+        t->xq2.alloc(t->xq.n);
+        XRL_CUDA(cudaMemsetAsync(t->xq2.p, 0, t->xq2.bytes(), ctx->stream));
+    }
+    Mvm A = mvm_make(t, nr, ya, flags, ctx->sched);
+    A.xq2 = t->xq2.p;
+    A.y2 = yb;
+    A.fuse = false;
+    mvm_begin(A, xa);
+    if (A.nl > 0) {
+        k_pack<<<nblk(A.nl, 256), 256, 0, A.st>>>(A.nl, xb, t->xq2.p + 8 * A.p0);
+        XRL_LAUNCH_CHECK();
+        ctx->launches += 1;
+    }
+    if (A.sched != XRL_SCHED_LATE || !A.chain) mvm_side(A);
+    mvm_up(A);
+    mvm_down(A);
+    Mvm B = mvm_make(t, nr, yb, flags, ctx->sched);
+    B.xq = t->xq2.p;
+    B.fuse = false;
+    B.side_done = true;  // its P2P / near ran with A's (ev_p2p, ev_join still mark them)
+    if (B.sched) {
+        XRL_CUDA(cudaEventRecord(ctx->ev_work, ctx->stream));
+        XRL_CUDA(cudaStreamWaitEvent(B.st, ctx->ev_work, 0));
+    }
+    mvm_up(B);
+    mvm_down(B);
+}
+
+static bool pair_enabled()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("XRL_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // Per-rank device times of the virtual-rank driver (events on the context stream, serial schedule).
 struct VTimer {
     xrl_ctx ctx;
@@ -1634,9 +1978,17 @@ xrl_status xrl_mvm(xrl_tree t, xrl_near nr, const void* x, void* y, int32_t nvec
     try {
         XRL_CUDA(cudaSetDevice(t->ctx->device));
         const int64_t nl = t->p1 - t->p0;
-        for (int v = 0; v < nvec; v += 3) {
-            xrl_status s = mvm_triple(t, nr, (const float2*)x + (size_t)v * nl, (float2*)y + (size_t)v * nl, flags);
+        for (int v = 0; v < nvec;) {
+            const float2* xv = (const float2*)x + (size_t)v * nl;
+            float2* yv = (float2*)y + (size_t)v * nl;
+            if (nvec - v >= 6 && t->part_world == 1 && pair_enabled()) {
+                mvm_pair(t, nr, xv, yv, xv + 3 * nl, yv + 3 * nl, flags);
+                v += 6;
+                continue;
+            }
+            xrl_status s = mvm_triple(t, nr, xv, yv, flags);
             if (s) return s;
+            v += 3;
         }
         return XRL_OK;
     } catch (const CudaError& e) {

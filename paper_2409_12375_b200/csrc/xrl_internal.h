@@ -202,6 +202,7 @@ struct xrl_tree_s {
     xrl::DBuf<float> ell;                    // [nbox][kEllStride] ell[r][k]
     xrl::DBuf<float> ellk;                   // [nbox][kEllKStride] ellk[k][8] (leaves, per MVM)
     xrl::DBuf<float> xq;                     // [n][8] packed charges
+    xrl::DBuf<float> xq2;                    // [n][8] the second triple's charges (xrl_mvm pairs, lazily)
     xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging
     xrl::DBuf<float2> xbuf[2], ybuf[2];       // xrl_mvm_host_batch double buffers
 };

@@ -395,3 +395,28 @@ def test_schedules_agree(cfg, leaf):
         assert err < 1e-6, name
     rows = np.random.default_rng(7).choice(m.n, size=min(256, m.n), replace=False)
     assert oracle.rel_l2(y0[:, rows], oracle_rows(m, x, rows)) <= TOL_FULL
+
+
+@pytest.mark.parametrize("cfg,leaf,nvec", [(1, 16, 6), (2, 64, 9), (2, 384, 12)])
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_paired_triples_equal_single_triples(cfg, leaf, nvec, flags):
+    """xrl_mvm with nvec = 6k runs the triples in pairs (one P2P / near pass for 12 right-hand sides,
+    k_p2p12 / k_near_seg12); each triple of the result equals the same triple run alone (nvec = 3) up to
+    the FP32 summation order, for the full, near-only and far-only products, and the paired full product
+    matches the oracle on sampled rows (north-star bound)."""
+    import torch
+    from paper_2409_12375_b200 import xrl
+    m = meshes.make_config(cfg)
+    ctx, tree, near = cuda_setup(m, leaf_max=leaf)
+    rng = np.random.default_rng(17)
+    x = (rng.standard_normal((nvec, m.n)) + 1j * rng.standard_normal((nvec, m.n))).astype(np.complex64)
+    y = run_mvm(tree, near, x, flags=flags)
+    for v in range(0, nvec, 3):
+        y1 = run_mvm(tree, near, np.ascontiguousarray(x[v:v + 3]), flags=flags)
+        err = np.linalg.norm(y[v:v + 3] - y1) / np.linalg.norm(y1)
+        assert err < 2e-6, (v, err)
+    if flags == 0:
+        rows = np.sort(rng.choice(m.n, size=min(256, m.n), replace=False))
+        g = oracle.Geometry(m.verts, m.tris)
+        yref = oracle.mvm_rows(g, x[3:6], rows)
+        assert oracle.rel_l2(y[3:6, rows], yref) <= 2e-5
