@@ -37,6 +37,8 @@ def _nccl_dirs():
 
 NCCL_INC, NCCL_LIB = _nccl_dirs()
 CUFLAGS = CUFLAGS + ["-I" + NCCL_INC]
+# tuning experiments only (e.g. "-DXRL_P2P_TPT=6"): extra flags for every translation unit
+CUFLAGS = CUFLAGS + os.environ.get("XRL_EXTRA_NVCC", "").split()
 HEADERS = ["xrl_internal.h", "harmonics.h", "operators.h", "tcgen05.h"]
 
 

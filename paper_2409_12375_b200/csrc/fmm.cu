@@ -763,7 +763,14 @@ __global__ void __launch_bounds__(256, 4) k_near_seg(int64_t nseg, const int32_t
 // y += (1/W) sum_{l != k} x_l / r_kl.
 constexpr int kSrcChunk = 1024;
 constexpr int kP2PSmem = (kSrcChunk * 12 > 128 * (4 * 6 + 1) * 2 ? kSrcChunk * 12 : 128 * (4 * 6 + 1) * 2) * 4;
-constexpr int kTPT = 8;
+#ifndef XRL_P2P_TPT
+#define XRL_P2P_TPT 8
+#endif
+#ifndef XRL_P2P_UNROLL
+#define XRL_P2P_UNROLL 2
+#endif
+constexpr int kTPT = XRL_P2P_TPT;
+constexpr int kP2PUnroll = XRL_P2P_UNROLL;
 constexpr int kTP2 = kTPT / 2;  // packed target pairs per thread
 
 // Packed FP32 pairs (sm_100 FFMA2/FADD2/FMUL2): two targets per instruction.
@@ -827,7 +834,7 @@ __device__ __forceinline__ void p2p_range(int j0, int j1, int S, const float4* _
                                           const float4 (*__restrict__ Sq)[2], const f2x* tx, const f2x* ty,
                                           const f2x* tz, f2x (*acc)[6])
 {
-#pragma unroll 2
+#pragma unroll kP2PUnroll
     for (int j = j0; j < j1; j += S) {
         const float4 sp = Sp[j];
         const float4 q0 = Sq[j][0], q1 = Sq[j][1];

@@ -897,7 +897,10 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
                 for (int64_t q = hup[L]; q < hup[L + 1]; ++q) src += hpe[hus[q]] - hpb[hus[q]];
                 const int nt = hpe[L] - hpb[L];
                 for (int o = 0; o < nt;) {
-                    const int c = (nt - o > 256) ? 256 : nt - o;
+#ifndef XRL_P2P_CUT
+#define XRL_P2P_CUT 256
+#endif
+                    const int c = (nt - o > XRL_P2P_CUT) ? XRL_P2P_CUT : nt - o;
                     cost.push_back({-(int64_t)c * src, make_int4(L, hpb[L] + o, c, 0)});
                     o += c;
                 }
