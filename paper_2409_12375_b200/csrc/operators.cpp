@@ -190,6 +190,8 @@ void build_operators(HostOperators& ops)
                 ops.m2l_index[(dx + 3) * 49 + (dy + 3) * 7 + (dz + 3)] = idx;
                 ++idx;
             }
+    // the 316 offsets are independent: one per OpenMP thread (context creation; ~1 s single-threaded)
+#pragma omp parallel for schedule(dynamic) firstprivate(Rt, It, A, B)
     for (int o = 0; o < kNM2L; ++o) {
         const int* d = ops.m2l_off[o];
         cplx_harmonics(double(d[0]), double(d[1]), double(d[2]), 2 * kP, Rt, It);

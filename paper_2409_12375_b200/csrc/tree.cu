@@ -9,6 +9,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 
@@ -561,6 +562,18 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     if (hbad & 2) { set_error("xrl_tree_build: zero-area panel"); return XRL_EGEOM; }
     if (hbad & 8) { set_error("xrl_tree_build: rectangle panel is not a planar parallelogram"); return XRL_EGEOM; }
 
+    // XRL_SETUP_TIMES=1: per-section wall times of the build on stderr (the stream synchronised at each mark)
+    static const bool setup_times = getenv("XRL_SETUP_TIMES") != nullptr;
+    auto setup_t0 = std::chrono::steady_clock::now();
+    auto setup_mark = [&](const char* what) {
+        if (!setup_times) return;
+        XRL_CUDA(cudaStreamSynchronize(st));
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "xrl setup: %-45s %8.1f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - setup_t0).count());
+        setup_t0 = now;
+    };
+    setup_mark("start");
     // root cube
     const int nbb = 256;
     DBuf<double> part(6 * nbb);
@@ -578,6 +591,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     for (int d = 0; d < 3; ++d) T->lo[d] = 0.5 * (mn[d] + mx[d]) - 0.5 * T->W;
     const double invW = 1.0 / T->W;
 
+    setup_mark("root");
     // Morton keys + stable radix sort
     DBuf<uint64_t> key(n);
     DBuf<int32_t> id(n);
@@ -602,6 +616,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
                                                   T->iperm.p);
     XRL_LAUNCH_CHECK();
 
+    setup_mark("morton sort");
     // octree, level by level
     std::vector<LevelBoxes> lv;
     std::vector<DBuf<int32_t>> lv_first_child;
@@ -693,6 +708,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     if (!hparents.empty())
         XRL_CUDA(cudaMemcpyAsync(T->parents.p, hparents.data(), 4 * hparents.size(), cudaMemcpyHostToDevice, st));
 
+    setup_mark("octree");
     // panel -> leaf, local coordinates, per-box max edge
     T->panel_leaf.alloc(n);
     T->loc.alloc(n);
@@ -704,6 +720,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     k_box_dmax<<<nbox, 128, 0, st>>>(nbox, T->bpb.p, T->bpe.p, T->dmax.p, T->bdmax.p);
     XRL_LAUNCH_CHECK();
 
+    setup_mark("local coords");
     // lists
     DBuf<int32_t> coll((size_t)kMaxColl * nbox), ncoll(nbox), adjc((size_t)kMaxAdj * nbox), nadjc(nbox);
     DBuf<int32_t> nV(nbox), nX(nbox);
@@ -837,6 +854,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         XRL_CUDA(cudaStreamSynchronize(st));
         T->np2p = (int64_t)ht;
     }
+    setup_mark("lists");
     // ---- partition over ranks: contiguous Morton ranges of
     // leaves balanced by estimated work; this rank owns panels [p0, p1).
     {
@@ -1056,6 +1074,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         }
         XRL_CUDA(cudaStreamSynchronize(st));
     }
+    setup_mark("partition + P2P tasks + translation passes");
     // M2L pairs sorted by (offset, target)
     T->m2l_tgt.alloc(std::max<int64_t>(1, T->nv));
     T->m2l_srcb.alloc(std::max<int64_t>(1, T->nv));
@@ -1116,6 +1135,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
             XRL_CUDA(cudaMemcpyAsync(T->m2l_blocks.p, blocks.data(), sizeof(int4) * blocks.size(), cudaMemcpyHostToDevice, st));
         XRL_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
     }
+    setup_mark("M2L tiles");
     // X targets (boxes with kept P2L pairs)
     {
         std::vector<int64_t> hx(nbox + 1);
@@ -1128,6 +1148,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         T->x_targets.alloc(std::max<size_t>(1, xt.size()));
         if (!xt.empty()) XRL_CUDA(cudaMemcpyAsync(T->x_targets.p, xt.data(), 4 * xt.size(), cudaMemcpyHostToDevice, st));
     }
+    setup_mark("X");
     // W pairs of the owned leaves (M2P: one CTA per pair)
     {
         std::vector<int64_t> hw(nbox + 1);
@@ -1147,6 +1168,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         if (!wp.empty()) XRL_CUDA(cudaMemcpyAsync(T->w_targets.p, wp.data(), sizeof(int2) * wp.size(), cudaMemcpyHostToDevice, st));
         XRL_CUDA(cudaStreamSynchronize(st));
     }
+    setup_mark("W");
     // multi-rank exchange plan: shared boxes, LET lists, remote leaves for the halo (exchange.cu)
     if (T->part_world > 1) {
         build_let_plan(T.get(), hpb, hpe, hchild, st);
@@ -1161,6 +1183,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         if (!mz.empty()) XRL_CUDA(cudaMemcpyAsync(T->mu_zero.p, mz.data(), 4 * mz.size(), cudaMemcpyHostToDevice, st));
         XRL_CUDA(cudaStreamSynchronize(st));
     }
+    setup_mark("exchange plans");
     // MVM scratch
     T->mu.alloc((size_t)nbox * kMuStride);
     T->ell.alloc((size_t)nbox * kEllStride);
@@ -1168,6 +1191,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     XRL_CUDA(cudaMemsetAsync(T->mu.p, 0, T->mu.bytes(), st));
     XRL_CUDA(cudaMemsetAsync(T->xq.p, 0, T->xq.bytes(), st));
     XRL_CUDA(cudaStreamSynchronize(st));
+    setup_mark("scratch");
     cref.keep = true;
     *out = T.release();
     return XRL_OK;
