@@ -588,7 +588,11 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     double ext = std::max({mx[0] - mn[0], mx[1] - mn[1], mx[2] - mn[2]});
     if (!(ext > 0)) ext = 1e-6;
     T->W = ext * (1.0 + 1e-6);
-    for (int d = 0; d < 3; ++d) T->lo[d] = 0.5 * (mn[d] + mx[d]) - 0.5 * T->W;
+    // the cube starts at the bounding box's low corner on every axis (not centred): on an axis much thinner
+    // than the cube (the layers of a package) the top levels then never split the geometry in that axis, so
+    // the first Morton cuts -- the rank partition's cuts -- run across the layers, not between them
+    // (config 4 at 2 ranks: 0.78 M halo panels with a centred cube)
+    for (int d = 0; d < 3; ++d) T->lo[d] = mn[d] - 0.25e-6 * ext;
     const double invW = 1.0 / T->W;
 
     setup_mark("root");
