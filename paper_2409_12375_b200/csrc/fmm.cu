@@ -1539,7 +1539,12 @@ static Mvm mvm_make(xrl_tree t, xrl_near nr, float2* y, uint32_t flags, int sche
     // the fused P2P warps pay off when the M2L is long and L2-bound (whole meshes, 2-way shards); on a rank's
     // share of an 8-way partition the M2L is short and the warps only stretch it (projection: 5.77x fused vs
     // 5.9x unfused at 8 ranks of config 4)
-    M.fuse = sched != 0 && ctx->fuse_p2p && M.chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0 && t->part_world <= 2;
+    static const int fuse_max_world = [] {  // XRL_FUSE_MAXWORLD (tuning): largest partition that fuses
+        const char* e = std::getenv("XRL_FUSE_MAXWORLD");
+        return e ? std::atoi(e) : 2;
+    }();
+    M.fuse = sched != 0 && ctx->fuse_p2p && M.chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0 &&
+             t->part_world <= fuse_max_world;
     M.side_done = false;
     M.nl = t->p1 - t->p0;
     M.p0 = t->p0;

@@ -872,6 +872,10 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         for (int32_t b : hleaves) lf.push_back({hpb[b], b});
         std::sort(lf.begin(), lf.end());
         std::vector<double> w(lf.size());
+        // cost weights per M2L translation, per panel (P2M + L2P), per near nonzero, in P2P pairs (measured,
+        // below); XRL_PART_W="a,b,c" overrides them (tuning)
+        double cw[3] = {2.0, 0.7, 0.006};
+        if (const char* e = getenv("XRL_PART_W")) sscanf(e, "%lf,%lf,%lf", &cw[0], &cw[1], &cw[2]);
         // near-field rows differ by an order of magnitude in length (coarse ground-plane panels see many fine
         // trace panels): a partitioned tree counts them (default eta) for the SpMV's share of the cost
         std::vector<int64_t> nnz_row;
@@ -889,7 +893,7 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
             double nnz = 0;
             if (!nnz_row.empty())
                 for (int32_t p = hpb[L]; p < hpe[L]; ++p) nnz += (double)nnz_row[p];
-            w[i] = nL * src + 2.0 * m2l + 0.7 * nL + 0.006 * nnz;
+            w[i] = nL * src + cw[0] * m2l + cw[1] * nL + cw[2] * nnz;
         }
         std::vector<int64_t> cuts(T->part_world + 1);
         xrl_partition_cuts((int64_t)w.size(), w.data(), T->part_world, cuts.data());
