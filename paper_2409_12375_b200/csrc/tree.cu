@@ -525,7 +525,7 @@ std::vector<int4> balance_blocks(const std::vector<int4>& blocks, int G)
 
 // ----------------------------------------------------------------- build
 static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* vert_h, int64_t n, const int32_t* tri_h,
-                                  int stride, const xrl_fmm_opts* opts, xrl_tree* out)
+                                  int stride, const xrl_fmm_opts* opts, xrl_tree* out, int align)
 {
     cudaStream_t st = ctx->stream;
     XRL_CUDA(cudaSetDevice(ctx->device));
@@ -588,11 +588,13 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     double ext = std::max({mx[0] - mn[0], mx[1] - mn[1], mx[2] - mn[2]});
     if (!(ext > 0)) ext = 1e-6;
     T->W = ext * (1.0 + 1e-6);
-    // the cube starts at the bounding box's low corner on every axis (not centred): on an axis much thinner
-    // than the cube (the layers of a package) the top levels then never split the geometry in that axis, so
-    // the first Morton cuts -- the rank partition's cuts -- run across the layers, not between them
-    // (config 4 at 2 ranks: 0.78 M halo panels with a centred cube)
-    for (int d = 0; d < 3; ++d) T->lo[d] = mn[d] - 0.25e-6 * ext;
+    // align 0: the cube starts at the bounding box's low corner on every axis; align 1: centred on it.  They
+    // differ only on axes thinner than the cube (the layers of a package): with the corner the top levels
+    // never split the geometry in that axis, so the first Morton cuts -- the rank partition's cuts -- run
+    // across the layers, not between them (config 4 at 2 ranks: 35 k halo panels vs 0.78 M centred), and the
+    // boxes cut the layer stack at different heights (tree_build_checked keeps the cheaper tree)
+    for (int d = 0; d < 3; ++d)
+        T->lo[d] = align == 0 ? mn[d] - 0.25e-6 * ext : 0.5 * (mn[d] + mx[d]) - 0.5 * T->W;
     const double invW = 1.0 / T->W;
 
     setup_mark("root");
@@ -1270,7 +1272,25 @@ static xrl_status tree_build_checked(xrl_ctx ctx, int64_t n_vert, const double* 
         }
     }
     try {
-        return tree_build_impl(ctx, n_vert, vert, n_tri, tri, stride, opts, out);
+        // the root cube at the bounding box's corner and centred on it (see tree_build_impl): both trees are
+        // built and the one with the smaller estimated MVM cost is kept -- P2P pairs + 2180 x V-list pairs
+        // (measured on config 4: 0.50 ns per pair, 1.09 us per tensor-core translation).  Every rank of a
+        // partition builds the same two global trees, so all ranks keep the same one.  XRL_ROOT_ALIGN=corner
+        // or centre builds one.
+        static const int forced = [] {
+            const char* e = getenv("XRL_ROOT_ALIGN");
+            return !e ? -1 : (e[0] == 'c' && e[1] == 'o') ? 0 : (e[0] == 'c') ? 1 : -1;
+        }();
+        xrl_tree a = nullptr, b = nullptr;
+        xrl_status s = tree_build_impl(ctx, n_vert, vert, n_tri, tri, stride, opts, &a, forced == 1 ? 1 : 0);
+        if (s != XRL_OK || forced >= 0) { *out = a; return s; }
+        s = tree_build_impl(ctx, n_vert, vert, n_tri, tri, stride, opts, &b, 1);
+        if (s != XRL_OK) { *out = a; return XRL_OK; }
+        const double ca = (double)a->np2p + 2180.0 * (double)a->nv, cb = (double)b->np2p + 2180.0 * (double)b->nv;
+        if (cb < ca) std::swap(a, b);
+        xrl_tree_destroy(b);
+        *out = a;
+        return XRL_OK;
     } catch (const CudaError& e) {
         return e.code;
     } catch (const std::bad_alloc&) {
