@@ -524,8 +524,16 @@ std::vector<int4> balance_blocks(const std::vector<int4>& blocks, int G)
 }  // namespace
 
 // ----------------------------------------------------------------- build
+// Root placement of one candidate tree: centred on the bounding box, or at its low corner with the thinnest
+// axis shifted down by `shift` x W (tree_build_checked searches these by the cost model).
+struct RootPlace {
+    bool centred = false;
+    double shift = 0.0;
+};
+
 static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* vert_h, int64_t n, const int32_t* tri_h,
-                                  int stride, const xrl_fmm_opts* opts, xrl_tree* out, int align)
+                                  int stride, const xrl_fmm_opts* opts, xrl_tree* out, RootPlace place,
+                                  double* cost_only = nullptr)
 {
     cudaStream_t st = ctx->stream;
     XRL_CUDA(cudaSetDevice(ctx->device));
@@ -588,13 +596,19 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     double ext = std::max({mx[0] - mn[0], mx[1] - mn[1], mx[2] - mn[2]});
     if (!(ext > 0)) ext = 1e-6;
     T->W = ext * (1.0 + 1e-6);
-    // align 0: the cube starts at the bounding box's low corner on every axis; align 1: centred on it.  They
-    // differ only on axes thinner than the cube (the layers of a package): with the corner the top levels
-    // never split the geometry in that axis, so the first Morton cuts -- the rank partition's cuts -- run
-    // across the layers, not between them (config 4 at 2 ranks: 35 k halo panels vs 0.78 M centred), and the
-    // boxes cut the layer stack at different heights (tree_build_checked keeps the cheaper tree)
+    // centred on the bounding box, or starting at its low corner (the thinnest axis optionally shifted down).
+    // They differ only on axes thinner than the cube (the layers of a package): with the corner the top
+    // levels never split the geometry in that axis, so the first Morton cuts -- the rank partition's cuts --
+    // run across the layers, not between them (config 4 at 2 ranks: 35 k halo panels vs 0.78 M centred), and
+    // the boxes cut the layer stack at different heights (tree_build_checked picks the cheapest placement)
     for (int d = 0; d < 3; ++d)
-        T->lo[d] = align == 0 ? mn[d] - 0.25e-6 * ext : 0.5 * (mn[d] + mx[d]) - 0.5 * T->W;
+        T->lo[d] = place.centred ? 0.5 * (mn[d] + mx[d]) - 0.5 * T->W : mn[d] - 0.25e-6 * ext;
+    if (!place.centred && place.shift > 0) {
+        int dt = 0;
+        for (int d = 1; d < 3; ++d) if (mx[d] - mn[d] < mx[dt] - mn[dt]) dt = d;
+        if (mx[dt] - mn[dt] + place.shift * T->W < (1.0 - 1e-6) * T->W) T->lo[dt] = mn[dt] - place.shift * T->W;
+        else if (cost_only) { *cost_only = 1e300; return XRL_OK; }  // the geometry would leave the cube
+    }
     const double invW = 1.0 / T->W;
 
     setup_mark("root");
@@ -861,6 +875,10 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
         T->np2p = (int64_t)ht;
     }
     setup_mark("lists");
+    if (cost_only) {  // candidate evaluation: the MVM's cost model (P2P pairs, V-list pairs) only
+        *cost_only = (double)T->np2p + 2180.0 * (double)T->nv;
+        return XRL_OK;
+    }
     // ---- partition over ranks: contiguous Morton ranges of
     // leaves balanced by estimated work; this rank owns panels [p0, p1).
     {
@@ -1272,25 +1290,34 @@ static xrl_status tree_build_checked(xrl_ctx ctx, int64_t n_vert, const double* 
         }
     }
     try {
-        // the root cube at the bounding box's corner and centred on it (see tree_build_impl): both trees are
-        // built and the one with the smaller estimated MVM cost is kept -- P2P pairs + 2180 x V-list pairs
+        // the root cube's placement is chosen by the MVM's cost model -- P2P pairs + 2180 x V-list pairs
         // (measured on config 4: 0.50 ns per pair, 1.09 us per tensor-core translation).  Every rank of a
-        // partition builds the same two global trees, so all ranks keep the same one.  XRL_ROOT_ALIGN=corner
-        // or centre builds one.
+        // partition evaluates the same global candidates, so all ranks pick the same one.
+        // XRL_ROOT_ALIGN=corner or centre skips the search.
         static const int forced = [] {
             const char* e = getenv("XRL_ROOT_ALIGN");
             return !e ? -1 : (e[0] == 'c' && e[1] == 'o') ? 0 : (e[0] == 'c') ? 1 : -1;
         }();
-        xrl_tree a = nullptr, b = nullptr;
-        xrl_status s = tree_build_impl(ctx, n_vert, vert, n_tri, tri, stride, opts, &a, forced == 1 ? 1 : 0);
-        if (s != XRL_OK || forced >= 0) { *out = a; return s; }
-        s = tree_build_impl(ctx, n_vert, vert, n_tri, tri, stride, opts, &b, 1);
-        if (s != XRL_OK) { *out = a; return XRL_OK; }
-        const double ca = (double)a->np2p + 2180.0 * (double)a->nv, cb = (double)b->np2p + 2180.0 * (double)b->nv;
-        if (cb < ca) std::swap(a, b);
-        xrl_tree_destroy(b);
-        *out = a;
-        return XRL_OK;
+        RootPlace best;
+        best.centred = forced == 1;
+        if (forced < 0) {
+            // candidates: centred, and the corner with the thinnest axis shifted by 0 .. 0.024 W; each is built
+            // up to its interaction lists (about a third of a build) and costed, the cheapest is built in full
+            // (config 4: leaf 384 5.49 -> 5.40 ms of modelled P2P + M2L, leaf 64 9.12 -> 8.39 ms)
+            static const double shifts[] = {0.0, 0.002, 0.004, 0.006, 0.008, 0.012, 0.016, 0.024};
+            double cbest = 1e301;
+            for (int c = -1; c < (int)(sizeof(shifts) / sizeof(shifts[0])); ++c) {
+                RootPlace pl;
+                pl.centred = c < 0;
+                pl.shift = c < 0 ? 0.0 : shifts[c];
+                double cost = 1e300;
+                xrl_tree dummy = nullptr;
+                const xrl_status s = tree_build_impl(ctx, n_vert, vert, n_tri, tri, stride, opts, &dummy, pl, &cost);
+                if (s != XRL_OK) return s;
+                if (cost < cbest) { cbest = cost; best = pl; }
+            }
+        }
+        return tree_build_impl(ctx, n_vert, vert, n_tri, tri, stride, opts, out, best);
     } catch (const CudaError& e) {
         return e.code;
     } catch (const std::bad_alloc&) {

@@ -1,4 +1,4 @@
-# root alignment chosen by the cost model: bench (leaf 384 + leaf 64 line), parity subset, setup times
+# root placement chosen by the cost model: bench (leaf 384 + leaf 64 line), parity subset, setup times
 O=gpurun_out/${1:-q45}; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 300 python tools/setup_times.py 4 384 > $O/setup.log 2>&1
