@@ -322,7 +322,7 @@ static xrl_status ilu_build(xrl_precond pc, std::unique_ptr<Exact>& E, const std
         return XRL_ECUDA;
     }
     DBuf<char> buf(std::max(bytes, 16));
-    const int policy = 1;  // CUSPARSE_SOLVE_POLICY_USE_LEVEL
+    const int policy = CUSPARSE_SOLVE_POLICY_USE_LEVEL;
     if (A.iluAnalysis(E->sh, N, nnz, E->descr, E->lv.p, E->lp.p, E->lc.p, E->ilu_info, policy, buf.p) ||
         A.iluFactor(E->sh, N, nnz, E->descr, E->lv.p, E->lp.p, E->lc.p, E->ilu_info, policy, buf.p)) {
         set_error("xrl_precond_build_kind: ILU(0) factorisation failed");
@@ -330,7 +330,7 @@ static xrl_status ilu_build(xrl_precond pc, std::unique_ptr<Exact>& E, const std
     }
     int zp = -1;
     const int zs = A.iluZeroPivot(E->sh, E->ilu_info, &zp);  // synchronises
-    if (zs == 3 /* CUSPARSE_STATUS_ZERO_PIVOT */ || zp >= 0) {
+    if (zs == CUSPARSE_STATUS_ZERO_PIVOT || zp >= 0) {
         set_error("xrl_precond_build_kind: ILU(0) zero pivot at row %d", zp);
         return XRL_ESINGULAR;
     }
