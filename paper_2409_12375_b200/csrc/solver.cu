@@ -134,6 +134,7 @@ constexpr int kBS = 64;
 __global__ void __launch_bounds__(256) k_block_inverse(const int32_t* __restrict__ bptr, const int64_t* __restrict__ clp,
                                                        const int32_t* __restrict__ clc, const double* __restrict__ clv,
                                                        const int64_t* __restrict__ cpp, const int32_t* __restrict__ cpc,
+                                                       const double* __restrict__ cpv,
                                                        const double2* __restrict__ dk, const double2* __restrict__ qdense,
                                                        float2* __restrict__ inv, int* singular)
 {
@@ -162,11 +163,9 @@ __global__ void __launch_bounds__(256) k_block_inverse(const int32_t* __restrict
             for (int64_t q2 = cpp[k]; q2 < cpp[k + 1]; ++q2) {
                 const int lb = cpc[q2];
                 if (lb < l0 || lb >= l0 + m) continue;
-                // C value of (lb, k): find in lb's row (short rows)
-                double cb0 = 0, cb1 = 0, cb2 = 0;
-                for (int64_t q3 = clp[lb]; q3 < clp[lb + 1]; ++q3)
-                    if (clc[q3] == k) { cb0 = clv[3 * q3]; cb1 = clv[3 * q3 + 1]; cb2 = clv[3 * q3 + 2]; break; }
-                const double s = ca0 * cb0 + ca1 * cb1 + ca2 * cb2;
+                // C value of (lb, k) from the panel row (was a search of lb's loop row: quadratic in the length
+                // of the long fundamental loops, 1.1 s of block build on config 4)
+                const double s = ca0 * cpv[3 * q2] + ca1 * cpv[3 * q2 + 1] + ca2 * cpv[3 * q2 + 2];
                 Q[a][lb - l0].x += d.x * s;
                 Q[a][lb - l0].y += d.y * s;
             }
@@ -1055,7 +1054,7 @@ static xrl_status precond_build_blocks(xrl_op op, int32_t qkind, int32_t block_s
         const int smem = kBS * (kBS + 1) * (int)sizeof(double2);
         XRL_CUDA(cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         k_block_inverse<<<pc->nblocks, 256, smem, st>>>(pc->bptr.p, T->cl_ptr.p, T->cl_col.p, T->cl_val64.p, T->cp_ptr.p,
-                                                     T->cp_col.p, dk.p, qd.p, pc->inv.p, sing.p);
+                                                     T->cp_col.p, T->cp_val64.p, dk.p, qd.p, pc->inv.p, sing.p);
         XRL_LAUNCH_CHECK();
     }
     int hs = 0;

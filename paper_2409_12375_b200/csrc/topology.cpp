@@ -435,13 +435,17 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
     for (int64_t i = 0; i < n; ++i) cpp[i + 1] += cpp[i];
     std::vector<int32_t> cpc(clc.size());
     std::vector<float> cpv(3 * clc.size());
+    std::vector<double> cpv64(3 * clc.size());
     {
         std::vector<int64_t> fill(cpp.begin(), cpp.end() - 1);
         for (int64_t l = 0; l < T->n_loops; ++l)
             for (int64_t q = clp[l]; q < clp[l + 1]; ++q) {
                 const int64_t o = fill[clc[q]]++;
                 cpc[o] = (int32_t)l;
-                for (int d = 0; d < 3; ++d) cpv[3 * o + d] = (float)clv[3 * q + d];
+                for (int d = 0; d < 3; ++d) {
+                    cpv[3 * o + d] = (float)clv[3 * q + d];
+                    cpv64[3 * o + d] = clv[3 * q + d];
+                }
             }
     }
     std::vector<float> clvf(clv.begin(), clv.end());
@@ -452,6 +456,7 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
     T->cp_ptr.alloc(n + 1);
     T->cp_col.alloc(std::max<size_t>(1, cpc.size()));
     T->cp_val.alloc(std::max<size_t>(3, cpv.size()));
+    T->cp_val64.alloc(std::max<size_t>(3, cpv64.size()));
     XRL_CUDA(cudaMemcpyAsync(T->cl_ptr.p, clp.data(), 8 * clp.size(), cudaMemcpyHostToDevice, st));
     if (!clc.empty()) {
         XRL_CUDA(cudaMemcpyAsync(T->cl_col.p, clc.data(), 4 * clc.size(), cudaMemcpyHostToDevice, st));
@@ -459,6 +464,7 @@ static xrl_status topo_impl(xrl_tree t, int32_t n_ports, const xrl_port* ports, 
         XRL_CUDA(cudaMemcpyAsync(T->cl_val64.p, clv.data(), 8 * clv.size(), cudaMemcpyHostToDevice, st));
         XRL_CUDA(cudaMemcpyAsync(T->cp_col.p, cpc.data(), 4 * cpc.size(), cudaMemcpyHostToDevice, st));
         XRL_CUDA(cudaMemcpyAsync(T->cp_val.p, cpv.data(), 4 * cpv.size(), cudaMemcpyHostToDevice, st));
+        XRL_CUDA(cudaMemcpyAsync(T->cp_val64.p, cpv64.data(), 8 * cpv64.size(), cudaMemcpyHostToDevice, st));
     }
     XRL_CUDA(cudaMemcpyAsync(T->cp_ptr.p, cpp.data(), 8 * cpp.size(), cudaMemcpyHostToDevice, st));
     {

@@ -254,6 +254,7 @@ struct xrl_topo_s {
     xrl::DBuf<int32_t> cl_col, cp_col;
     xrl::DBuf<float> cl_val, cp_val;             // 3 floats per nonzero
     xrl::DBuf<double> cl_val64;                  // FP64 copy for the preconditioner assembly
+    xrl::DBuf<double> cp_val64;                  // the same by panel rows (c_l(k) read directly, no row search)
     xrl::DBuf<int32_t> long_rows;                // loops with > 64 panel entries (CTA per row)
     int32_t n_long = 0;
 };
