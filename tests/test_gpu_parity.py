@@ -420,3 +420,31 @@ def test_paired_triples_equal_single_triples(cfg, leaf, nvec, flags):
         g = oracle.Geometry(m.verts, m.tris)
         yref = oracle.mvm_rows(g, x[3:6], rows)
         assert oracle.rel_l2(y[3:6, rows], yref) <= 2e-5
+
+
+@pytest.mark.parametrize("align", ["corner", "centre"])
+def test_root_placements_agree(align, tmp_path):
+    """The root cube placement (the cost-model search, or XRL_ROOT_ALIGN=corner / centre) changes
+    the tree, not the product: config 2's MVM with a forced placement (fresh process, the variable is read
+    once) matches the oracle on sampled rows and the searched tree's result to FP32 accuracy."""
+    import os
+    import subprocess
+    import sys
+    m = meshes.make_config(2)
+    ctx, tree, near = cuda_setup(m, leaf_max=64)
+    x = meshes.make_x(2, m.n)
+    y = run_mvm(tree, near, x)
+    out = tmp_path / "y.npy"
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "from inputs import meshes\nfrom tests.gpu_helpers import cuda_setup, run_mvm\n"
+            "m = meshes.make_config(2); ctx, tree, near = cuda_setup(m, leaf_max=64)\n"
+            "np.save(%r, run_mvm(tree, near, meshes.make_x(2, m.n)))\n"
+            "print(tree.info()['root_lo'])\n") % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), str(out))
+    env = dict(os.environ, XRL_ROOT_ALIGN=align)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    print(align, "root_lo", r.stdout.strip(), "searched", tree.info()["root_lo"])
+    y2 = np.load(out)
+    assert oracle.rel_l2(y2, y) < 1e-5
+    rows = np.random.default_rng(3).choice(m.n, size=256, replace=False)
+    assert oracle.rel_l2(y2[:, rows], oracle_rows(m, x, rows)) <= TOL_FULL
