@@ -1217,8 +1217,18 @@ struct GPart {
     int64_t nl;
     DBuf<float2> V, w, tmp;
     DBuf<double2> dh;
+    DBuf<double2> dc;  // one Arnoldi step's coefficients on the device: CGS2 passes [2][nrhs][m+1], norms [nrhs]
     DBuf<double> ds, ones;
 };
+
+// ds[r] = 1 / sqrt(max(dn[r].x, 0)) (0 below 1e-300): the new basis vector's scale from the device norm
+__global__ void k_inv_norm(int nrhs, const double2* __restrict__ dn, double* __restrict__ ds)
+{
+    const int r = threadIdx.x;
+    if (r >= nrhs) return;
+    const double hn = sqrt(fmax(dn[r].x, 0.0));
+    ds[r] = hn > 1e-300 ? 1.0 / hn : 0.0;
+}
 
 static xrl_status gmres_parts(std::vector<GPart>& P, bool nccl, int32_t nrhs, const xrl_gmres_opts* opts,
                               int32_t* iters_out, double* rre_out, double* true_rre_out, int32_t* conv_out)
@@ -1240,6 +1250,7 @@ static xrl_status gmres_parts(std::vector<GPart>& P, bool nccl, int32_t nrhs, co
         p.w.alloc(std::max<size_t>(1, (size_t)nrhs * p.nl));
         p.tmp.alloc(std::max<size_t>(1, (size_t)nrhs * p.nl));
         p.dh.alloc((size_t)nrhs * (m + 1));
+        p.dc.alloc((size_t)nrhs * (2 * (m + 1) + 1));
         p.ds.alloc(nrhs);
         p.ones.alloc(nrhs);
         std::vector<double> one(nrhs, 1.0);
@@ -1370,7 +1381,58 @@ static xrl_status gmres_parts(std::vector<GPart>& P, bool nccl, int32_t nrhs, co
             }
             // CGS2
             std::vector<std::vector<cd>> hcol(nrhs, std::vector<cd>(j + 2, 0.0));
-            for (int pass = 0; pass < 2; ++pass) {
+            std::vector<double> hn;
+            if (k == 1 || nccl) {
+                // one host synchronisation per step: both projection passes and the norm stay on the device (the
+                // update and the scale read the coefficients there; NCCL sums them across the ranks), then one
+                // copy of [h1 | h2 | |w|^2] feeds the host's Hessenberg / Givens step
+                GPart& p = P[0];
+                const int ni = j + 1;
+                double2* h1 = p.dc.p;
+                double2* h2 = p.dc.p + (size_t)nrhs * (m + 1);
+                double2* dn = p.dc.p + (size_t)2 * nrhs * (m + 1);
+                for (int pass = 0; pass < 2; ++pass) {
+                    double2* hp = pass ? h2 : h1;
+                    XRL_CUDA(cudaMemsetAsync(hp, 0, 16 * (size_t)nrhs * ni, st));
+                    if (p.nl > 0) {
+                        k_gdots<<<dim3(ni, nrhs, (unsigned)((p.nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(
+                            p.nl, m + 1, p.V.p, p.w.p, hp, ni);
+                        XRL_LAUNCH_CHECK();
+                    }
+                    if (nccl && (s = nccl_allreduce_sum_f64(ctx, (double*)hp, (size_t)2 * nrhs * ni, st))) return s;
+                    if (p.nl > 0) {
+                        k_gupdate<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, m + 1, nrhs, p.V.p, hp, ni, -1.f, p.w.p);
+                        XRL_LAUNCH_CHECK();
+                    }
+                }
+                XRL_CUDA(cudaMemsetAsync(dn, 0, 16 * (size_t)nrhs, st));
+                if (p.nl > 0) {
+                    k_gdots<<<dim3(1, nrhs, (unsigned)((p.nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(p.nl, 1, p.w.p,
+                                                                                                          p.w.p, dn, 1);
+                    XRL_LAUNCH_CHECK();
+                }
+                if (nccl && (s = nccl_allreduce_sum_f64(ctx, (double*)dn, (size_t)2 * nrhs, st))) return s;
+                k_inv_norm<<<1, 32, 0, st>>>(nrhs, dn, p.ds.p);
+                XRL_LAUNCH_CHECK();
+                if (p.nl > 0) {
+                    k_gscale<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, nrhs, p.w.p, p.nl, p.ds.p, p.V.p + (int64_t)(j + 1) * p.nl,
+                                                              (int64_t)(m + 1) * p.nl);
+                    XRL_LAUNCH_CHECK();
+                }
+                std::vector<double2> hb((size_t)nrhs * (2 * (m + 1) + 1));
+                XRL_CUDA(cudaMemcpyAsync(hb.data(), p.dc.p, 16 * hb.size(), cudaMemcpyDeviceToHost, st));
+                XRL_CUDA(cudaStreamSynchronize(st));
+                hn.resize(nrhs);
+                for (int r = 0; r < nrhs; ++r) {
+                    for (int i = 0; i <= j; ++i) {
+                        const double2 a = hb[(size_t)r * ni + i], b2 = hb[(size_t)nrhs * (m + 1) + (size_t)r * ni + i];
+                        hcol[r][i] += cd(a.x + b2.x, a.y + b2.y);
+                    }
+                    hn[r] = std::sqrt(std::max(hb[(size_t)2 * nrhs * (m + 1) + r].x, 0.0));
+                    hcol[r][j + 1] = hn[r];
+                }
+            }
+            for (int pass = 0; pass < 2 && !(k == 1 || nccl); ++pass) {
                 std::vector<double2> hv;
                 if ((s = dots([](GPart& p) -> const float2* { return p.V.p; }, m + 1, cW, j + 1, hv))) return s;
                 for (int r = 0; r < nrhs; ++r)
@@ -1384,19 +1446,20 @@ static xrl_status gmres_parts(std::vector<GPart>& P, bool nccl, int32_t nrhs, co
                     }
                 }
             }
-            std::vector<double> hn;
-            if ((s = norms(cW, hn))) return s;
-            for (int r = 0; r < nrhs; ++r) {
-                hcol[r][j + 1] = hn[r];
-                sc[r] = hn[r] > 1e-300 ? 1.0 / hn[r] : 0.0;
-            }
-            setscale(sc);
-            for (auto& p : P)
-                if (p.nl) {
-                    k_gscale<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, nrhs, p.w.p, p.nl, p.ds.p, p.V.p + (int64_t)(j + 1) * p.nl,
-                                                              (int64_t)(m + 1) * p.nl);
-                    XRL_LAUNCH_CHECK();
+            if (!(k == 1 || nccl)) {  // virtual ranks: the coefficients are summed on the host
+                if ((s = norms(cW, hn))) return s;
+                for (int r = 0; r < nrhs; ++r) {
+                    hcol[r][j + 1] = hn[r];
+                    sc[r] = hn[r] > 1e-300 ? 1.0 / hn[r] : 0.0;
                 }
+                setscale(sc);
+                for (auto& p : P)
+                    if (p.nl) {
+                        k_gscale<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, nrhs, p.w.p, p.nl, p.ds.p,
+                                                                  p.V.p + (int64_t)(j + 1) * p.nl, (int64_t)(m + 1) * p.nl);
+                        XRL_LAUNCH_CHECK();
+                    }
+            }
             for (int r = 0; r < nrhs; ++r) {
                 if (!active[r]) continue;
                 auto& hc = hcol[r];
