@@ -224,11 +224,18 @@ def gmres_iteration_time(xrl, tree, near, args, freq=1e9):
     # a call also applies the operator twice outside the Arnoldi steps (initial and true residual): the steady
     # per-iteration time is the difference of two runs, 2k and k iterations, over k
     k2 = max(2, args.gmres_iters // 2)
+    ms_half = None
+    for _ in range(2):
+        e0.record()
+        _, rep_h = xrl.gmres(op, pc, b, max_iters=k2, restart=50, tol=1e-30)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_half = e0.elapsed_time(e1) if ms_half is None else min(ms_half, e0.elapsed_time(e1))
     e0.record()
-    _, rep_h = xrl.gmres(op, pc, b, max_iters=k2, restart=50, tol=1e-30)
+    _, rep = xrl.gmres(op, pc, b, max_iters=args.gmres_iters, restart=50, tol=1e-30)
     e1.record()
     torch.cuda.synchronize()
-    ms_half = e0.elapsed_time(e1)
+    ms = min(ms, e0.elapsed_time(e1))
     steady = (ms - ms_half) / max(int(rep["iters"][0]) - int(rep_h["iters"][0]), 1)
     solve = None
     if args.gmres_solve > 0:  # optional: the solve to the paper's tolerance (1e-4 above 1 MHz)

@@ -1221,6 +1221,16 @@ struct GPart {
     DBuf<double> ds, ones;
 };
 
+// virtual ranks: buf[q][off .. off + cnt) summed over the k parts, the sum written back to every part
+__global__ void k_sum_parts(int k, double2* const* __restrict__ buf, size_t off, int cnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    double2 a = make_double2(0, 0);
+    for (int q = 0; q < k; ++q) { const double2 v = buf[q][off + i]; a.x += v.x; a.y += v.y; }
+    for (int q = 0; q < k; ++q) buf[q][off + i] = a;
+}
+
 // ds[r] = 1 / sqrt(max(dn[r].x, 0)) (0 below 1e-300): the new basis vector's scale from the device norm
 __global__ void k_inv_norm(int nrhs, const double2* __restrict__ dn, double* __restrict__ ds)
 {
@@ -1257,6 +1267,12 @@ static xrl_status gmres_parts(std::vector<GPart>& P, bool nccl, int32_t nrhs, co
         XRL_CUDA(cudaMemcpyAsync(p.ones.p, one.data(), 8 * nrhs, cudaMemcpyHostToDevice, st));
     }
     std::vector<double2> hh((size_t)nrhs * (m + 1)), hsum((size_t)nrhs * (m + 1));
+    DBuf<double2*> dcptr(k);  // the parts' step-coefficient buffers (device sum over virtual ranks)
+    {
+        std::vector<double2*> h(k);
+        for (int q = 0; q < k; ++q) h[q] = P[q].dc.p;
+        XRL_CUDA(cudaMemcpyAsync(dcptr.p, h.data(), sizeof(double2*) * k, cudaMemcpyHostToDevice, st));
+    }
     using BufSel = DBuf<float2> GPart::*;
     auto opA = [&](std::function<const float2*(GPart&)> in, std::function<float2*(GPart&)> out) -> xrl_status {
         if (!sharded) return op_apply(P[0].op, in(P[0]), out(P[0]), nrhs);
@@ -1382,83 +1398,69 @@ static xrl_status gmres_parts(std::vector<GPart>& P, bool nccl, int32_t nrhs, co
             // CGS2
             std::vector<std::vector<cd>> hcol(nrhs, std::vector<cd>(j + 2, 0.0));
             std::vector<double> hn;
-            if (k == 1 || nccl) {
+            {
                 // one host synchronisation per step: both projection passes and the norm stay on the device (the
-                // update and the scale read the coefficients there; NCCL sums them across the ranks), then one
-                // copy of [h1 | h2 | |w|^2] feeds the host's Hessenberg / Givens step
-                GPart& p = P[0];
+                // update and the scale read the coefficients there; NCCL -- or, for virtual ranks, a device sum
+                // over the parts -- adds them up across the ranks), then one copy of [h1 | h2 | |w|^2] feeds the
+                // host's Hessenberg / Givens step
                 const int ni = j + 1;
-                double2* h1 = p.dc.p;
-                double2* h2 = p.dc.p + (size_t)nrhs * (m + 1);
-                double2* dn = p.dc.p + (size_t)2 * nrhs * (m + 1);
+                const size_t o1 = 0, o2 = (size_t)nrhs * (m + 1), on = (size_t)2 * nrhs * (m + 1);
+                auto reduce = [&](size_t off, int cnt) -> xrl_status {
+                    if (nccl) return nccl_allreduce_sum_f64(ctx, (double*)(P[0].dc.p + off), (size_t)2 * cnt, st);
+                    if (k > 1) {
+                        k_sum_parts<<<nblk(cnt, 128), 128, 0, st>>>(k, dcptr.p, off, cnt);
+                        XRL_LAUNCH_CHECK();
+                    }
+                    return XRL_OK;
+                };
                 for (int pass = 0; pass < 2; ++pass) {
-                    double2* hp = pass ? h2 : h1;
-                    XRL_CUDA(cudaMemsetAsync(hp, 0, 16 * (size_t)nrhs * ni, st));
-                    if (p.nl > 0) {
-                        k_gdots<<<dim3(ni, nrhs, (unsigned)((p.nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(
-                            p.nl, m + 1, p.V.p, p.w.p, hp, ni);
-                        XRL_LAUNCH_CHECK();
+                    const size_t off = pass ? o2 : o1;
+                    for (auto& p : P) {
+                        XRL_CUDA(cudaMemsetAsync(p.dc.p + off, 0, 16 * (size_t)nrhs * ni, st));
+                        if (p.nl > 0) {
+                            k_gdots<<<dim3(ni, nrhs, (unsigned)((p.nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(
+                                p.nl, m + 1, p.V.p, p.w.p, p.dc.p + off, ni);
+                            XRL_LAUNCH_CHECK();
+                        }
                     }
-                    if (nccl && (s = nccl_allreduce_sum_f64(ctx, (double*)hp, (size_t)2 * nrhs * ni, st))) return s;
-                    if (p.nl > 0) {
-                        k_gupdate<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, m + 1, nrhs, p.V.p, hp, ni, -1.f, p.w.p);
-                        XRL_LAUNCH_CHECK();
-                    }
+                    if ((s = reduce(off, nrhs * ni))) return s;
+                    for (auto& p : P)
+                        if (p.nl > 0) {
+                            k_gupdate<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, m + 1, nrhs, p.V.p, p.dc.p + off, ni, -1.f,
+                                                                       p.w.p);
+                            XRL_LAUNCH_CHECK();
+                        }
                 }
-                XRL_CUDA(cudaMemsetAsync(dn, 0, 16 * (size_t)nrhs, st));
-                if (p.nl > 0) {
-                    k_gdots<<<dim3(1, nrhs, (unsigned)((p.nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(p.nl, 1, p.w.p,
-                                                                                                          p.w.p, dn, 1);
-                    XRL_LAUNCH_CHECK();
-                }
-                if (nccl && (s = nccl_allreduce_sum_f64(ctx, (double*)dn, (size_t)2 * nrhs, st))) return s;
-                k_inv_norm<<<1, 32, 0, st>>>(nrhs, dn, p.ds.p);
-                XRL_LAUNCH_CHECK();
-                if (p.nl > 0) {
-                    k_gscale<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, nrhs, p.w.p, p.nl, p.ds.p, p.V.p + (int64_t)(j + 1) * p.nl,
-                                                              (int64_t)(m + 1) * p.nl);
-                    XRL_LAUNCH_CHECK();
-                }
-                std::vector<double2> hb((size_t)nrhs * (2 * (m + 1) + 1));
-                XRL_CUDA(cudaMemcpyAsync(hb.data(), p.dc.p, 16 * hb.size(), cudaMemcpyDeviceToHost, st));
-                XRL_CUDA(cudaStreamSynchronize(st));
-                hn.resize(nrhs);
-                for (int r = 0; r < nrhs; ++r) {
-                    for (int i = 0; i <= j; ++i) {
-                        const double2 a = hb[(size_t)r * ni + i], b2 = hb[(size_t)nrhs * (m + 1) + (size_t)r * ni + i];
-                        hcol[r][i] += cd(a.x + b2.x, a.y + b2.y);
-                    }
-                    hn[r] = std::sqrt(std::max(hb[(size_t)2 * nrhs * (m + 1) + r].x, 0.0));
-                    hcol[r][j + 1] = hn[r];
-                }
-            }
-            for (int pass = 0; pass < 2 && !(k == 1 || nccl); ++pass) {
-                std::vector<double2> hv;
-                if ((s = dots([](GPart& p) -> const float2* { return p.V.p; }, m + 1, cW, j + 1, hv))) return s;
-                for (int r = 0; r < nrhs; ++r)
-                    for (int i = 0; i <= j; ++i) hcol[r][i] += cd(hv[(size_t)r * (j + 1) + i].x, hv[(size_t)r * (j + 1) + i].y);
                 for (auto& p : P) {
-                    // the summed coefficients go back to every part (all ranks subtract the same projection)
-                    XRL_CUDA(cudaMemcpyAsync(p.dh.p, hv.data(), 16 * hv.size(), cudaMemcpyHostToDevice, st));
-                    if (p.nl) {
-                        k_gupdate<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, m + 1, nrhs, p.V.p, p.dh.p, j + 1, -1.f, p.w.p);
+                    XRL_CUDA(cudaMemsetAsync(p.dc.p + on, 0, 16 * (size_t)nrhs, st));
+                    if (p.nl > 0) {
+                        k_gdots<<<dim3(1, nrhs, (unsigned)((p.nl + kDotChunk - 1) / kDotChunk)), 256, 0, st>>>(
+                            p.nl, 1, p.w.p, p.w.p, p.dc.p + on, 1);
                         XRL_LAUNCH_CHECK();
                     }
                 }
-            }
-            if (!(k == 1 || nccl)) {  // virtual ranks: the coefficients are summed on the host
-                if ((s = norms(cW, hn))) return s;
-                for (int r = 0; r < nrhs; ++r) {
-                    hcol[r][j + 1] = hn[r];
-                    sc[r] = hn[r] > 1e-300 ? 1.0 / hn[r] : 0.0;
-                }
-                setscale(sc);
-                for (auto& p : P)
-                    if (p.nl) {
+                if ((s = reduce(on, nrhs))) return s;
+                for (auto& p : P) {
+                    k_inv_norm<<<1, 32, 0, st>>>(nrhs, p.dc.p + on, p.ds.p);
+                    XRL_LAUNCH_CHECK();
+                    if (p.nl > 0) {
                         k_gscale<<<nblk(p.nl, 256), 256, 0, st>>>(p.nl, nrhs, p.w.p, p.nl, p.ds.p,
                                                                   p.V.p + (int64_t)(j + 1) * p.nl, (int64_t)(m + 1) * p.nl);
                         XRL_LAUNCH_CHECK();
                     }
+                }
+                std::vector<double2> hb((size_t)nrhs * (2 * (m + 1) + 1));
+                XRL_CUDA(cudaMemcpyAsync(hb.data(), P[0].dc.p, 16 * hb.size(), cudaMemcpyDeviceToHost, st));
+                XRL_CUDA(cudaStreamSynchronize(st));
+                hn.resize(nrhs);
+                for (int r = 0; r < nrhs; ++r) {
+                    for (int i = 0; i <= j; ++i) {
+                        const double2 a = hb[o1 + (size_t)r * ni + i], b2 = hb[o2 + (size_t)r * ni + i];
+                        hcol[r][i] += cd(a.x + b2.x, a.y + b2.y);
+                    }
+                    hn[r] = std::sqrt(std::max(hb[on + r].x, 0.0));
+                    hcol[r][j + 1] = hn[r];
+                }
             }
             for (int r = 0; r < nrhs; ++r) {
                 if (!active[r]) continue;

@@ -73,19 +73,23 @@ def main():
             return e0.elapsed_time(e1), int(r["iters"][0])
         # steady per-iteration time: difference of an a.iters and an a.iters/2 call (a call also applies the
         # operator for the initial and the true residual)
-        t_full, it = run(a.iters)
-        t_half, it_h = run(max(2, a.iters // 2))
+        t_full, it = min(run(a.iters) for _ in range(3))
+        t_half, it_h = min(run(max(2, a.iters // 2)) for _ in range(3))
         ms_iter_all = (t_full - t_half) / max(it - it_h, 1)
         if k == 1:  # the single-GPU solver itself (xrl_gmres), beside the one-rank xrl_gmres_vranks
             xrl.gmres(ops[0], pcs[0], bs[0], max_iters=a.iters, tol=1e-30)
             torch.cuda.synchronize()
             tt = []
             for n in (a.iters, max(2, a.iters // 2)):
-                e0.record()
-                _, rep1 = xrl.gmres(ops[0], pcs[0], bs[0], max_iters=n, tol=1e-30)
-                e1.record()
-                torch.cuda.synchronize()
-                tt.append((e0.elapsed_time(e1), int(rep1["iters"][0])))
+                best = None
+                for _ in range(3):
+                    e0.record()
+                    _, rep1 = xrl.gmres(ops[0], pcs[0], bs[0], max_iters=n, tol=1e-30)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    v = (e0.elapsed_time(e1), int(rep1["iters"][0]))
+                    best = v if best is None or v < best else best
+                tt.append(best)
             res["xrl_gmres_ms_per_iter"] = (tt[0][0] - tt[1][0]) / max(tt[0][1] - tt[1][1], 1)
         # MVM projection inputs of this partition
         xs = []
