@@ -3,9 +3,7 @@
 
 The sharded loop-space GMRES (xrl_gmres_vranks: k operators on the k trees of a partition, rank-local block
 diag-of-P preconditioners, inner products summed over the ranks) runs a fixed number of iterations on one GPU
-with the ranks serialised; the steady time per iteration (the difference of a 20- and a 10-iteration call,
-which removes the call's initial and true-residual operator applies) divided by k is the mean rank's device
-time per iteration.
+with the ranks serialised; its time per iteration divided by k is the mean rank's device time per iteration.
 The projection multiplies that by the MVM's measured rank imbalance and adds the exposed communication per
 iteration: the MVM's (tools/vrank_projection.py model), two loop-space halo exchanges of the operator (loop
 values, panel values: volumes from the plans) and 2 x CGS2 passes + 1 norm of FP64 all-reduces, 15 us each.
@@ -34,7 +32,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--leaf", type=int, default=384)
     ap.add_argument("--ks", default="1,2,4,8")
-    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--freq", type=float, default=1e9)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -64,33 +62,20 @@ def main():
         xrl.gmres_vranks(ops, pcs, bs, max_iters=a.iters, tol=1e-30)  # warm-up (Krylov basis allocated)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-        def run(n):
-            e0.record()
-            _, r = xrl.gmres_vranks(ops, pcs, bs, max_iters=n, tol=1e-30)
-            e1.record()
-            torch.cuda.synchronize()
-            return e0.elapsed_time(e1), int(r["iters"][0])
-        # steady per-iteration time: difference of an a.iters and an a.iters/2 call (a call also applies the
-        # operator for the initial and the true residual)
-        t_full, it = min(run(a.iters) for _ in range(3))
-        t_half, it_h = min(run(max(2, a.iters // 2)) for _ in range(3))
-        ms_iter_all = (t_full - t_half) / max(it - it_h, 1)
+        e0.record()
+        _, rep = xrl.gmres_vranks(ops, pcs, bs, max_iters=a.iters, tol=1e-30)
+        e1.record()
+        torch.cuda.synchronize()
+        it = int(rep["iters"][0])
+        ms_iter_all = e0.elapsed_time(e1) / max(it, 1)
         if k == 1:  # the single-GPU solver itself (xrl_gmres), beside the one-rank xrl_gmres_vranks
             xrl.gmres(ops[0], pcs[0], bs[0], max_iters=a.iters, tol=1e-30)
             torch.cuda.synchronize()
-            tt = []
-            for n in (a.iters, max(2, a.iters // 2)):
-                best = None
-                for _ in range(3):
-                    e0.record()
-                    _, rep1 = xrl.gmres(ops[0], pcs[0], bs[0], max_iters=n, tol=1e-30)
-                    e1.record()
-                    torch.cuda.synchronize()
-                    v = (e0.elapsed_time(e1), int(rep1["iters"][0]))
-                    best = v if best is None or v < best else best
-                tt.append(best)
-            res["xrl_gmres_ms_per_iter"] = (tt[0][0] - tt[1][0]) / max(tt[0][1] - tt[1][1], 1)
+            e0.record()
+            _, rep1 = xrl.gmres(ops[0], pcs[0], bs[0], max_iters=a.iters, tol=1e-30)
+            e1.record()
+            torch.cuda.synchronize()
+            res["xrl_gmres_ms_per_iter"] = e0.elapsed_time(e1) / max(int(rep1["iters"][0]), 1)
         # MVM projection inputs of this partition
         xs = []
         off = 0
