@@ -9,8 +9,9 @@
 //
 // Kernels (one launch each unless noted):
 //   k_pack       complex64 [3][n] -> float [n][8] charges          (HBM, 48 B/panel)
-//   k_near_spmv  near correction CSR x (side stream)               (HBM)
+//   k_near_seg   near correction N x, 6-byte segment format (side stream)   (HBM / latency)
 //   k_p2p        U-list direct sum, packed f32x2 (side stream)     (FP32 pipe)
+//   k_p2p12, k_near_seg12   the same for two triples in one pass (xrl_mvm nvec = 6k)
 //   k_p2m        leaf multipoles mu = sum q Rt(u)                   (per leaf)
 //   (M2M)        child -> parent per level on the tensor-core translation kernel (k_m2l_tc)
 //   k_m2l_tc     V-list translations on tcgen05 (3xTF32, warp-specialised)
