@@ -37,7 +37,7 @@ def main():
     for cfg in [int(c) for c in a.configs.split(",")]:
         m = meshes.make_config(cfg)
         ctx = xrl.Context(0)
-        tree = xrl.Tree(ctx, m.verts, m.tris, leaf_max=64 if cfg <= 2 else 352)
+        tree = xrl.Tree(ctx, m.verts, m.tris, leaf_max=64 if cfg <= 2 else 384)
         near = xrl.Near(tree)
         topo = xrl.Topology(tree, [(p, q) for _, p, q in m.ports])
         op = xrl.Operator(tree, near, topo, a.freq, sigma=5.8e7, zeta=ZETA[cfg])

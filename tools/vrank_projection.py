@@ -13,7 +13,7 @@ the halo of x overlaps the up pass (xrl_mvm issues it on its comm stream while P
 own charges), the shared-box all-reduce and the LET exchange are on the critical path.  The single-GPU references are the
 same driver at k = 1 and xrl_mvm itself.
 
-    python tools/vrank_projection.py [--config 4] [--leaf 352] [--ks 1,2,4,8] [--reps 5] [--out file.json]
+    python tools/vrank_projection.py [--config 4] [--leaf 384] [--ks 1,2,4,8] [--reps 5] [--out file.json]
 """
 import argparse
 import json
