@@ -206,7 +206,9 @@ xrl_status xrl_near_export_rows(xrl_near near, int64_t nrows, const int64_t* row
  * x, y: device complex64 [nvec][n_local] in library order (this rank's slice
  * [offset, offset + n_local) on a multi-rank context), must not alias;
  * nvec a multiple of 3 (each triple of complex components = 6 real RHS through
- * one tree traversal).  Enqueued on the context stream.
+ * one tree traversal; on a single-rank tree consecutive triples
+ * run in pairs whose P2P and near SpMV are one pass for 12 RHS, XRL_PAIR=0
+ * turns that off).  Enqueued on the context stream.
  * Multi-rank (plans built at setup from the shared tree and near
  * pattern): each rank packs its own charges, receives the halo of
  * remote charges its P2P / P2L / near rows read (grouped ncclSend/ncclRecv),
