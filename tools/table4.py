@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--max-iters", type=int, default=1000)
     ap.add_argument("--out", default=None)
     ap.add_argument("--only-ilu", action="store_true")
+    ap.add_argument("--only-exact", action="store_true")
     a = ap.parse_args()
     out = {"tol": a.tol, "freq_hz": a.freq, "restart": 50, "rows": []}
     for cfg in [int(c) for c in a.configs.split(",")]:
@@ -55,6 +56,8 @@ def main():
                             ("diag_p", "ilu"), ("diag_l", "ilu")):
             if a.only_ilu and exact != "ilu":
                 continue
+            if a.only_exact and not (exact is True and kind == "diag_p"):
+                continue
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             pc = None if kind == "none" else xrl.Precond(op, 64, exact=exact is True, kind=kind, ilu=exact == "ilu")
@@ -64,7 +67,7 @@ def main():
             x, rep = xrl.gmres(op, pc, b, tol=a.tol, max_iters=a.max_iters)
             torch.cuda.synchronize()
             solve = time.perf_counter() - t0
-            row = {"config": cfg, "n_panels": m.n, "n_loops": nl, "rhs": rhs,
+            row = {"config": cfg, "n_panels": m.n, "n_loops": nl, "rhs": rhs, "rre": [float(v) for v in rep["rre"]],
                    "preconditioner": kind + (" (ILU(0) on the GPU)" if exact == "ilu" else " (exact Q^-1)" if exact
                                              else " (block-Jacobi 64)" if kind != "none" else ""),
                    "setup_s": round(setup, 3), "iters": rep["iters"].tolist(), "converged": rep["converged"].tolist(),
