@@ -689,22 +689,37 @@ __global__ void __launch_bounds__(256, 4) k_near_seg(int64_t nseg, const int32_t
                                                     const uint16_t* __restrict__ eoff, const float* __restrict__ xq,
                                                     int64_t nl, float2* __restrict__ y)
 {
-    const int64_t team = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
-    const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) >> 3;
+    // each CTA owns a contiguous, entry-balanced range of segments (consecutive rows share most of their
+    // columns, so the CTA's charge gathers hit L1 again on the next rows); its teams take the range's segments
+    // round-robin
+    __shared__ int64_t rng[2];
+    if (threadIdx.x < 2) {
+        const int64_t E = __ldg(seg_off + nseg);
+        const int64_t target = (E * (int64_t)(blockIdx.x + threadIdx.x)) / gridDim.x;
+        int64_t lo = 0, hi = nseg;  // first segment whose start is >= target
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(seg_off + mid) < target) lo = mid + 1; else hi = mid;
+        }
+        rng[threadIdx.x] = (blockIdx.x + threadIdx.x == gridDim.x) ? nseg : lo;
+    }
+    __syncthreads();
+    const int64_t s_end = rng[1];
+    const int64_t nteams = blockDim.x >> 3;
     const int l8 = threadIdx.x & 7;
     const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-    int64_t s = team;
+    int64_t s = rng[0] + (threadIdx.x >> 3);
     int64_t b0 = 0, b1 = 0;  // entry range of segment s
     int32_t base = 0;
-    if (s < nseg) { b0 = __ldg(seg_off + s); b1 = __ldg(seg_off + s + 1); base = __ldg(seg_base + s); }
+    if (s < s_end) { b0 = __ldg(seg_off + s); b1 = __ldg(seg_off + s + 1); base = __ldg(seg_base + s); }
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     uint2 o = make_uint2(0u, 0u);
-    if (s < nseg && b0 + 4 * l8 < b1) { v = ldg_stream4(eval + b0 + 4 * l8, pol_stream); o = ldg_stream_u64(eoff + b0 + 4 * l8, pol_stream); }
-    while (s < nseg) {
+    if (s < s_end && b0 + 4 * l8 < b1) { v = ldg_stream4(eval + b0 + 4 * l8, pol_stream); o = ldg_stream_u64(eoff + b0 + 4 * l8, pol_stream); }
+    while (s < s_end) {
         const int64_t sn = s + nteams;
         int64_t n0 = 0, n1 = 0;
         int32_t nbase = 0;
-        if (sn < nseg) { n0 = __ldg(seg_off + sn); n1 = __ldg(seg_off + sn + 1); nbase = __ldg(seg_base + sn); }
+        if (sn < s_end) { n0 = __ldg(seg_off + sn); n1 = __ldg(seg_off + sn + 1); nbase = __ldg(seg_base + sn); }
         const int32_t row = __ldg(seg_row + s);
         const float* xb = xq + 8 * (int64_t)base;
         float a[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -724,7 +739,7 @@ __global__ void __launch_bounds__(256, 4) k_near_seg(int64_t nseg, const int32_t
             // the next chunk: this segment's, else the next segment's first
             const int64_t np = it + 1 < nit ? pos + 32 : n0 + 4 * l8;
             const int64_t ne = it + 1 < nit ? b1 : n1;
-            if ((it + 1 < nit || sn < nseg) && np < ne) {
+            if ((it + 1 < nit || sn < s_end) && np < ne) {
                 v = ldg_stream4(eval + np, pol_stream);
                 o = ldg_stream_u64(eoff + np, pol_stream);
             }
