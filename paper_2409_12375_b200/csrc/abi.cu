@@ -130,6 +130,7 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_m2l, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_p2p, cudaEventDisableTiming));
         if (const char* e = getenv("XRL_FUSE"); e && e[0] == '0') c->fuse_p2p = false;
+        if (const char* e = getenv("XRL_M2L_TF32"); e && e[0] == '1') c->m2l_h16 = false;
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         if (const char* e = getenv("XRL_SCHED")) c->sched = atoi(e);
         if (const char* e = getenv("XRL_SERIAL"); e && e[0] == '1') c->sched = XRL_SCHED_SERIAL;

@@ -20,6 +20,8 @@
 //   k_ell_kmajor leaves' ell[r][k] -> ellk[k][8]
 //   k_l2p        per target panel: L2P
 //   k_m2p        W-list M2P (leaves with a W list), completes y
+#include <cuda_fp16.h>
+
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -127,7 +129,13 @@ __device__ __forceinline__ int degree_of(int i)
 // One persistent CTA per SM; blocks (runs of tiles with one (chunk, offset))
 // dealt round-robin, so all CTAs work inside one L2-resident target chunk.
 constexpr int kTcPairs = 21;                        // pairs per tile (126 of 128 TMEM lanes)
-constexpr int kTcThreads = 384;                     // 4 loader + 4 drain + 1 MMA warps + 3 fused-P2P warps
+#ifndef XRL_FUSE_WARPS
+#define XRL_FUSE_WARPS 3
+#endif
+constexpr int kTcLdW = 8;                           // loader warps (two per TMEM lane quarter, one per K-half)
+constexpr int kTcMmaW = kTcLdW + 4;                 // the MMA warp (after 4 drain warps)
+constexpr int kTcFuseW = XRL_FUSE_WARPS;            // fused-P2P warps
+constexpr int kTcThreads = 32 * (kTcMmaW + 1 + kTcFuseW);
 constexpr int kTcOpBytes = 128 * 128 * 4;           // one operator part (hi or lo): 64 KB
 constexpr int kTcStageLd = 132;                     // drain stage row stride (floats; conflict-free STS.128)
 constexpr int kTcSmem = 2 * kTcOpBytes + 128 * kTcStageLd * 4 + 1024 + 512 * 12 * 4;  // operator hi + lo, drain stage (+ align), fused-P2P staging
@@ -278,15 +286,32 @@ __device__ __forceinline__ void ldg256_coherent(const float* p, float* v)
 }
 
 // blocks[j] = {first tile, #tiles, offset, chunk}; tiles[t] = {offset, first pair, #pairs, chunk}
+// Scale exponent e of the multipoles for the 3xFP16 M2L: the largest |mu| times 2^e lies in [2^14, 2^15)
+// (clamped to [-90, 90]: the drain's 2^-(e + opexp) stays a normal float; 0 when every multipole is zero).
+__device__ __forceinline__ int mu_scale_exp(const unsigned* mumax)
+{
+    const unsigned bits = *mumax;  // written by k_mu_max before this launch (stream order)
+    if (bits == 0u) return 0;
+    return max(-90, min(90, 14 - ((int)(bits >> 23) - 127)));
+}
+
+// kH = false: 3xTF32 (kind::tf32, K = 8); the M2M / L2L passes.  kH = true: 3xFP16 (kind::f16, K = 16, twice
+// the tensor rate at the same 11-bit significand per part) on power-of-2 scaled operands: every multipole times
+// 2^e, e = 14 - exponent of the largest |mu| of the MVM (*mumax, k_mu_max), every operator times 2^opexp (host,
+// largest |T| in [2^14, 2^15)); the drain multiplies by 2^-(e + opexp).  Used for the M2L.
+template <bool kH>
 __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict__ blocks, int nblocks,
                                                           const int4* __restrict__ tiles,
                                                           const int32_t* __restrict__ tgt,
                                                           const int32_t* __restrict__ srcb,
-                                                          const float* __restrict__ opimg,
+                                                          const void* __restrict__ opimg,
                                                           const float* __restrict__ bimg, float* __restrict__ ell,
                                                           int dbg, P2PTasks p2p, const int* __restrict__ lvr,
-                                                          int* __restrict__ lv_done, int nlv)
+                                                          int* __restrict__ lv_done, int nlv,
+                                                          const unsigned* __restrict__ mumax, int opexp)
 {
+    constexpr uint32_t kOpPart = kH ? 128 * 128 * 2 : kTcOpBytes;  // bytes of one operator part (hi or lo)
+    constexpr uint32_t kColAl = kH ? 64 : kTcColAl;
     extern __shared__ uint8_t tsm_raw[];
     uint8_t* opsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
     float* stage = reinterpret_cast<float*>(opsm + 2 * kTcOpBytes);  // [128 rows][kTcStageLd]
@@ -296,7 +321,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
     __shared__ int m2l_live, p2p_task;
     __shared__ P2PWin p2p_win;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) m2l_live = 9;  // warps of the translation roles still running
+    if (tid == 0) m2l_live = kTcMmaW + 1;  // warps of the translation roles still running
     if (tid == 0) {
         for (int h = 0; h < 2; ++h) {
             tc::mbar_init(&a_full[h], 4);
@@ -306,41 +331,43 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
         }
         tc::mbar_init(&op_full, 1);
     }
-    if (warp == 8) tc::tmem_alloc<512>(&tbase);
+    if (warp == kTcMmaW) tc::tmem_alloc<512>(&tbase);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tm = tbase;
 
-    if (warp >= 9) {
+    if (warp > kTcMmaW) {
         // ---------------- fused P2P: three warps take target-leaf tasks from the shared counter while the
         // translation roles run (the M2L is bound by L2 traffic and leaves the FP32 pipes idle)
         if (p2p.tasks) {
-            const int tp = tid - 9 * 32;
+            const int tp = tid - 32 * (kTcMmaW + 1);
             for (;;) {
                 if (tp == 0) p2p_task = *(volatile int*)&m2l_live > 0 ? atomicAdd(p2p.counter, 1) : INT_MAX;
-                asm volatile("bar.sync 1, 96;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcFuseW) : "memory");
                 const int task = p2p_task;
                 if (task >= p2p.ntasks) break;
                 const int4 tk = p2p.tasks[task];
-                p2p_leaf<96, kFuseChunk, 1>(tk.x, tk.y, tk.y + tk.z, tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
+                p2p_leaf<32 * kTcFuseW, kFuseChunk, 1>(tk.x, tk.y, tk.y + tk.z, tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
                                             p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, 0, p2p.n,
                                             p2p.p0, p2p.y);
             }
         }
-    } else if (warp < 4) {
-        // ---------------- loaders: thread = TMEM lane L = (p, r).  A K-half of the multipole row
-        // (64 floats, 8 x 256-bit loads: whole 32-byte sectors per lane) is prefetched into
-        // registers half a tile ahead of its use; tile descriptors and source ids a tile ahead.
-        const int L = tid, p = L / 6, r = L % 6;
+    } else if (warp < kTcLdW) {
+        // ---------------- loaders: thread = TMEM lane L = (p, r); warps w and w + 4 share lane quarter w % 4,
+        // warps 0-3 convert K-half 0 of their rows and warps 4-7 K-half 1.  Each thread's half row (64 floats,
+        // 8 x 256-bit loads: whole 32-byte sectors) of the next tile is loaded right after the current one is
+        // handed to the MMA, so the gathers have a whole tile period to arrive.
+        const int L = tid & 127, p = L / 6, r = L % 6, h = warp >> 2;
         const bool lane_ok = L < 6 * kTcPairs;
-        const uint32_t ta = tm + ((uint32_t)(32 * warp) << 16);
+        const uint32_t ta = tm + ((uint32_t)(32 * (warp & 3)) << 16);
         auto row_of = [&](const int4& tl, bool ok) -> const float* {
             if (!ok || !lane_ok || p >= tl.z || (dbg & 2)) return nullptr;
             return bimg + (size_t)__ldg(srcb + tl.y + p) * kMuStride + r * 128;
         };
+        const float sc0 = kH ? __int_as_float((127 + mu_scale_exp(mumax)) << 23) : 1.f;  // the multipoles' 2^e
         float x[64];
-        auto load_half = [&](const float* row, int h) {
+        auto load_half = [&](const float* row) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 if (row) {
@@ -358,21 +385,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
         };
         TileSeq s0(blocks, nblocks, lvr);
         if (s0.ok) level_gate(s0.lev);
-        const float* row0 = row_of(s0.ok ? __ldg(tiles + s0.ti) : make_int4(0, 0, 0, 0), s0.ok);
-        load_half(row0, 0);
-        TileSeq s1 = s0;
-        s1.advance(blocks, nblocks, lvr);
-        int4 tl1 = s1.ok ? __ldg(tiles + s1.ti) : make_int4(0, 0, 0, 0);
+        load_half(row_of(s0.ok ? __ldg(tiles + s0.ti) : make_int4(0, 0, 0, 0), s0.ok));
         for (int j = 0; s0.ok; ++j) {
-            const float* row1 = nullptr;
-            // the next tile opens a new level: its rows are read only after the grid barrier, which needs this
-            // tile fully handed to the MMA first (no prefetch across levels)
-            const bool defer = s1.ok && s1.lev != s0.lev;
+            TileSeq s1 = s0;
+            s1.advance(blocks, nblocks, lvr);
+            const int4 tl1 = s1.ok ? __ldg(tiles + s1.ti) : make_int4(0, 0, 0, 0);
+            // the MMAs of the previous tile must be done with this K-half of A
+            tc::mbar_wait(&a_free[h], (j & 1) ^ 1);
+            tc::fence_after();
+            if constexpr (kH) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                // the MMAs of the previous tile must be done with this K-half of A
-                tc::mbar_wait(&a_free[h], (j & 1) ^ 1);
-                tc::fence_after();
+                for (int c2 = 0; c2 < 4; ++c2) {  // 16 coefficients = 8 columns of packed f16 pairs at a time
+                    uint32_t hi[8], lo[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float a = x[16 * c2 + 2 * q] * sc0, b = x[16 * c2 + 2 * q + 1] * sc0;
+                        const __half2 hh = __floats2half2_rn(a, b);  // .x (low half) = a: the lower k
+                        const float2 hf = __half22float2(hh);
+                        const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
+                        hi[q] = *reinterpret_cast<const uint32_t*>(&hh);
+                        lo[q] = *reinterpret_cast<const uint32_t*>(&ll);
+                    }
+                    tc::tmem_st8u(ta + kTcColAh + 32 * h + 8 * c2, hi);
+                    tc::tmem_st8u(ta + kColAl + 32 * h + 8 * c2, lo);
+                }
+            } else {
 #pragma unroll
                 for (int c2 = 0; c2 < 8; ++c2) {  // 8 columns at a time
                     float hi[8], lo[8];
@@ -384,34 +421,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                     tc::tmem_st8(ta + kTcColAh + 64 * h + 8 * c2, hi);
                     tc::tmem_st8(ta + kTcColAl + 64 * h + 8 * c2, lo);
                 }
-                tc::tmem_st_wait();
-                tc::fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&a_full[h]);
-                if (h == 0) {
-                    load_half(row0, 1);
-                    if (!defer) row1 = row_of(tl1, s1.ok);
-                } else if (!defer) {
-                    load_half(row1, 0);
-                }
+            }
+            tc::tmem_st_wait();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_full[h]);
+            if (s1.ok) {
+                // a tile of the next level is read only after the grid barrier (this tile is already handed over)
+                if (s1.lev != s0.lev) level_gate(s1.lev);
+                load_half(row_of(tl1, true));
             }
             s0 = s1;
-            row0 = row1;
-            if (defer) {
-                level_gate(s0.lev);
-                row0 = row_of(tl1, true);
-                load_half(row0, 0);
-            }
-            s1.advance(blocks, nblocks, lvr);
-            if (s1.ok) tl1 = __ldg(tiles + s1.ti);
         }
-    } else if (warp < 8) {
+    } else if (warp < kTcMmaW) {
         // ---------------- drain: thread = TMEM lane L = (p, r) reads its accumulator row into a
         // shared-memory stage; then each thread reduces its whole row into ell with one TMA bulk
         // reduction (asynchronous: frees the drain warps; tools/ubench_red.cu measured the variants)
-        const int L = tid - 128, p = L / 6, r = L % 6;
+        const int L = tid - 32 * kTcLdW, p = L / 6, r = L % 6;
         const bool lane_ok = L < 6 * kTcPairs;
-        const int qd = warp - 4;  // lane quarter (warp % 4)
+        const int qd = warp & 3;  // lane quarter (warp % 4)
         // multi-level launch: after its last tile of a level, every drain thread waits for its bulk reductions
         // to complete and fences them; then one thread marks the level (and any level this CTA had no tile
         // in) done for the other CTAs' loaders
@@ -426,6 +454,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                 for (int v = signaled; v < lv; ++v) atomicAdd(lv_done + v, 1);
             signaled = lv;
         };
+        const float unscale = kH ? __int_as_float((127 - mu_scale_exp(mumax) - opexp) << 23) : 1.f;
         TileSeq sq(blocks, nblocks, lvr);
         if (sq.ok) signal_upto(sq.lev);
         int4 cur = sq.ok ? __ldg(tiles + sq.ti) : make_int4(0, 0, 0, 0);
@@ -452,6 +481,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                     for (int q = 0; q < 32; ++q) v[q] = 0.f;
                 } else {
                     tc::tmem_ld32(ta + 32 * c, v);
+                    if (kH) {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) v[q] *= unscale;
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
@@ -479,8 +512,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
         // descriptors stay in uniform registers and lane 0 issues back-to-back UTCHMMAs
         // (uniform bases recomputed here so they live in uniform registers)
         const uint32_t tmu = tbase;
-        const uint32_t oph = (tc::smem_u32(tsm_raw) + 1023u) & ~1023u, opl = oph + kTcOpBytes;
-        const uint32_t idesc = tc::idesc_tf32(128, 128);
+        const uint32_t oph = (tc::smem_u32(tsm_raw) + 1023u) & ~1023u, opl = oph + kOpPart;
+        const uint32_t idesc = kH ? tc::idesc_f16(128, 128) : tc::idesc_tf32(128, 128);
         int j = 0, nb = 0;
         for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x, ++nb) {
             int4 bk = __ldg(blocks + bi);
@@ -492,10 +525,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                 tc::fence_after();
             }
             if (lane == 0) {
-                mbar_expect_tx(&op_full, 2 * kTcOpBytes);
-                const float* src = opimg + (size_t)bk.z * 2 * 128 * 128;
-                for (int c = 0; c < 4; ++c)
-                    bulk_g2s(opsm + c * (kTcOpBytes / 2), src + c * (kTcOpBytes / 8), kTcOpBytes / 2, &op_full);
+                mbar_expect_tx(&op_full, 2 * kOpPart);
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(opimg) + (size_t)bk.z * 2 * kOpPart;
+                for (uint32_t c = 0; c < 2 * kOpPart / 32768; ++c)
+                    bulk_g2s(opsm + c * 32768, src + c * 32768, 32768, &op_full);
             }
             mbar_wait_warp(&op_full, nb & 1);
             for (int ti = 0; ti < bk.y; ++ti, ++j) {
@@ -507,7 +540,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
                 for (int h = 0; h < 2; ++h) {
                     mbar_wait_warp(&a_full[h], j & 1);
                     tc::fence_after();
-                    if (tc::elect_one()) {
+                    if (kH && tc::elect_one()) {
+#pragma unroll
+                        for (int s = 4 * h; s < 4 * h + 4; ++s) {
+                            // B element (i, k) at half ((i/8)*16 + k/8)*64 + (i%8)*8 + k%8: LBO 128, SBO 2048 bytes
+                            const uint64_t bh = tc::smem_desc(oph + 256 * s, 128, 2048);
+                            const uint64_t bl = tc::smem_desc(opl + 256 * s, 128, 2048);
+                            tc::mma_f16_ts(dst, tmu + kColAl + 8 * s, bh, idesc, s > 0);
+                            tc::mma_f16_ts(dst, tmu + kTcColAh + 8 * s, bl, idesc, 1);
+                            tc::mma_f16_ts(dst, tmu + kTcColAh + 8 * s, bh, idesc, 1);
+                        }
+                        tc::commit(&a_free[h]);
+                        if (h == 1) tc::commit(&d_full[d]);
+                    } else if (!kH && tc::elect_one()) {
 #pragma unroll
                         for (int s = 8 * h; s < 8 * h + 8; ++s) {
                             // B (operator) element (i, k) at ((i/8)*32 + k/4)*128 + (i%8)*16 + (k%4)*4: LBO 128, SBO 4096
@@ -525,10 +570,34 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             }
         }
     }
-    if (warp < 9 && lane == 0) atomicSub(&m2l_live, 1);
+    if (warp <= kTcMmaW && lane == 0) atomicSub(&m2l_live, 1);
     tc::fence_before();
     __syncthreads();
-    if (warp == 8) tc::tmem_dealloc<512>(tbase);
+    if (warp == kTcMmaW) tc::tmem_dealloc<512>(tbase);
+}
+
+// Largest |mu| of the MVM for the 3xFP16 M2L scale: *mumax = max over the boxes' multipole coefficients (as the
+// bits of a non-negative float, so an unsigned atomicMax orders them); one warp per box, 6 rows of 124 floats.
+__global__ void __launch_bounds__(256) k_mu_max(int nbox, const float* __restrict__ mu, unsigned* __restrict__ mumax)
+{
+    const int b = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    float m = 0.f;
+    if (b < nbox && lane < 31) {
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(mu + (size_t)b * kMuStride + r * 128) + lane);
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
+    __shared__ float wm[8];
+    if (lane == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) m = fmaxf(m, wm[w]);
+        atomicMax(mumax, __float_as_uint(m));
+    }
 }
 
 // ------------------------------------------------------------------ P2L (X list)
@@ -1476,6 +1545,34 @@ void upload_tc_images(DBuf<float>& dst, const HostOperators& ops)
     XRL_CUDA(cudaMemcpy(dst.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
 }
 
+// M2L operator images for k_m2l_tc<true> (3xFP16): per offset o, T[i][k] * 2^opexp (one exponent for all
+// offsets: the largest |entry| in [2^14, 2^15)) split into FP16 hi = rn(a), lo = rn(a - hi), in the canonical K-major layout of a 128 x 128
+// 16-bit B operand: element (i, k) at half ((i/8)*16 + k/8)*64 + (i%8)*8 + k%8; [offset][hi|lo][16384].
+void upload_h16_images(DBuf<uint16_t>& dst, int& opexp, const HostOperators& ops)
+{
+    const size_t img = 128 * 128;
+    std::vector<uint16_t> h((size_t)kNM2L * 2 * img, 0);
+    double mx = 0;
+    for (size_t i = 0; i < (size_t)kNM2L * kNC * kNC; ++i) mx = std::max(mx, std::fabs(ops.m2l[i]));
+    int e2;
+    std::frexp(mx, &e2);  // mx in [2^(e2-1), 2^e2)
+    opexp = 15 - e2;
+    for (int m = 0; m < kNM2L; ++m) {
+        const double* T = &ops.m2l[(size_t)m * kNC * kNC];
+        for (int i = 0; i < kNC; ++i)
+            for (int k = 0; k < kNC; ++k) {
+                const double a = std::ldexp(T[(size_t)i * kNC + k], opexp);
+                const __half hi = __double2half(a);
+                const __half lo = __double2half(a - (double)__half2float(hi));
+                const size_t e = ((size_t)(i / 8) * 16 + k / 8) * 64 + (i % 8) * 8 + k % 8;
+                h[(size_t)m * 2 * img + e] = __half_as_ushort(hi);
+                h[(size_t)m * 2 * img + img + e] = __half_as_ushort(lo);
+            }
+    }
+    dst.alloc(h.size());
+    XRL_CUDA(cudaMemcpy(dst.p, h.data(), h.size() * 2, cudaMemcpyHostToDevice));
+}
+
 }  // namespace
 
 namespace xrl {
@@ -1487,7 +1584,9 @@ void upload_constants(xrl_ctx ctx)
     XRL_CUDA(cudaMemcpyToSymbol(c_tab, &tab, sizeof(tab)));
     const HostOperators& ops = host_ops();
     upload_tc_images(ctx->ops.m2l_tc, ops);
-    XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+    upload_h16_images(ctx->ops.m2l_h16, ctx->ops.m2l_hexp, ops);
+    XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+    XRL_CUDA(cudaFuncSetAttribute(k_m2l_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2p, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2PSmem));
     XRL_CUDA(cudaFuncSetAttribute(k_p2p12, cudaFuncAttributeMaxDynamicSharedMemorySize, kP2PSmem12));
     XRL_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
@@ -1506,9 +1605,9 @@ static void translate_pass(xrl_tree t, xrl::TransPass& P, const float* src, floa
     if (P.nblocks <= 0 || P.nlev <= 0) return;
     xrl_ctx ctx = t->ctx;
     XRL_CUDA(cudaMemsetAsync(P.done.p, 0, sizeof(int) * P.nlev, st));
-    k_m2l_tc<<<P.grid, kTcThreads, kTcSmem, st>>>(t->tr_blocks.p + P.first, P.nblocks, t->tr_tiles.p, t->tr_tgt.p,
-                                                  t->tr_src.p, ctx->ops.m2l_tc.p, src, dst, 0, P2PTasks{}, P.rows.p,
-                                                  P.done.p, P.nlev);
+    k_m2l_tc<false><<<P.grid, kTcThreads, kTcSmem, st>>>(t->tr_blocks.p + P.first, P.nblocks, t->tr_tiles.p,
+                                                         t->tr_tgt.p, t->tr_src.p, ctx->ops.m2l_tc.p, src, dst, 0,
+                                                         P2PTasks{}, P.rows.p, P.done.p, P.nlev, nullptr, 0);
     XRL_LAUNCH_CHECK();
     ctx->launches += 1;
 }
@@ -1766,11 +1865,25 @@ static void mvm_down(Mvm& M)
                 tasks = P2PTasks{t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
                                  t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, M.xq, M.invW, M.nl,
                                  M.p0, M.y};
-            k_m2l_tc<<<grid, kTcThreads, kTcSmem, M.st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p,
-                                                          t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l_tc.p, t->mu.p,
-                                                          t->ell.p, m2l_dbg, tasks, nullptr, nullptr, 0);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
+            if (ctx->m2l_h16) {  // 3xFP16 (default): the multipole row exponents first
+                if (t->mu_max.n < 1) t->mu_max.alloc(1);
+                XRL_CUDA(cudaMemsetAsync(t->mu_max.p, 0, sizeof(unsigned), M.st));
+                k_mu_max<<<(t->nbox + 7) / 8, 256, 0, M.st>>>(t->nbox, t->mu.p, t->mu_max.p);
+                XRL_LAUNCH_CHECK();
+                k_m2l_tc<true><<<grid, kTcThreads, kTcSmem, M.st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p,
+                                                                    t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l_h16.p,
+                                                                    t->mu.p, t->ell.p, m2l_dbg, tasks, nullptr, nullptr,
+                                                                    0, t->mu_max.p, ctx->ops.m2l_hexp);
+                XRL_LAUNCH_CHECK();
+                ctx->launches += 2;
+            } else {
+                k_m2l_tc<false><<<grid, kTcThreads, kTcSmem, M.st>>>(t->m2l_blocks.p, t->n_m2l_blocks, t->m2l_tiles.p,
+                                                                     t->m2l_tgt.p, t->m2l_srcb.p, ctx->ops.m2l_tc.p,
+                                                                     t->mu.p, t->ell.p, m2l_dbg, tasks, nullptr,
+                                                                     nullptr, 0, nullptr, 0);
+                XRL_LAUNCH_CHECK();
+                ctx->launches += 1;
+            }
         }
         phase_end(ctx, PH_M2L, ev, M.st);
         if (M.fuse) {

@@ -73,6 +73,8 @@ enum Phase { PH_PACK = 0, PH_P2M, PH_M2M, PH_M2L, PH_P2L, PH_L2L, PH_L2P, PH_P2P
 
 struct DeviceOperators {
     DBuf<float> m2l_tc;  // [332: M2L 316, M2M 8, L2L 8][2 (hi, lo)][128 x 128 tf32, tcgen05 canonical K-major]
+    DBuf<uint16_t> m2l_h16;  // [316 M2L][2 (hi, lo)][128 x 128 f16, canonical K-major], scaled by 2^m2l_hexp
+    int m2l_hexp = 0;
     int m2l_index[343];
 };
 
@@ -104,6 +106,7 @@ struct xrl_ctx_s {
     cudaStream_t comm = nullptr;      // library-owned stream of a multi-rank context's NCCL exchanges
     cudaEvent_t ev_halo = nullptr, ev_comm = nullptr, ev_p2l = nullptr;
     bool fuse_p2p = true;             // P2P warps inside the M2L kernel (XRL_FUSE=0: off)
+    bool m2l_h16 = true;              // M2L in 3xFP16 (XRL_M2L_TF32=1: 3xTF32, the round-2 kernel)
     bool own_stream = false;
     int rank = 0, world = 1;
     void* nccl_comm = nullptr;        // ncclComm_t when world > 1
@@ -199,6 +202,7 @@ struct xrl_tree_s {
     int32_t stride = 3;                      // 3: triangles; 4: hybrid panels pv[n][4] (-1: triangle)
     // MVM scratch
     xrl::DBuf<float> mu;                     // [nbox][kMuStride]  mu[r][k]
+    xrl::DBuf<unsigned> mu_max;              // largest |mu| of the MVM (float bits) for the 3xFP16 M2L scale
     xrl::DBuf<float> ell;                    // [nbox][kEllStride] ell[r][k]
     xrl::DBuf<float> ellk;                   // [nbox][kEllKStride] ellk[k][8] (leaves, per MVM)
     xrl::DBuf<float> xq;                     // [n][8] packed charges

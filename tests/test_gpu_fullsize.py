@@ -153,3 +153,51 @@ def test_leaf_above_32767_panels():
     err = oracle.rel_l2(y[:, rows], oracle.mvm_rows(g, x, rows))
     print("max_depth 1 leaves", ex["pe"][leaves] - ex["pb"][leaves], err)
     assert err <= TOL_FULL
+
+
+def _ctx_tree(cfg, leaf, env):
+    """A fresh context/tree/near with environment switches read at context creation (XRL_M2L_TF32)."""
+    import os
+    from paper_2409_12375_b200 import xrl
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        m = meshes.make_config(cfg)
+        ctx = xrl.Context(0)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    tree = xrl.Tree(ctx, m.verts, m.tris, leaf_max=leaf)
+    return m, ctx, tree, xrl.Near(tree)
+
+
+def test_m2l_fp16_matches_tf32():
+    """The default 3xFP16 M2L (scaled operands) and the 3xTF32 one agree to FP32 rounding of the far field
+    (both keep 22 significand bits per product)."""
+    m, _, t16, n16 = _ctx_tree(3, 64, {"XRL_M2L_TF32": "0"})
+    _, _, t32, n32 = _ctx_tree(3, 64, {"XRL_M2L_TF32": "1"})
+    x = meshes.make_x(3, m.n)
+    y16 = run_mvm(t16, n16, x, flags=2)  # XRL_MVM_FAR_ONLY: the FMM part alone
+    y32 = run_mvm(t32, n32, x, flags=2)
+    d = oracle.rel_l2(y16, y32)
+    print("far-only rel L2 fp16 vs tf32 M2L:", d)
+    assert d <= 1e-6
+
+
+def test_m2l_fp16_skewed_charges():
+    """Charges spanning 16 decades across the mesh (one power-of-2 scale for all multipoles of the MVM):
+    the MVM stays within the north-star bound of the oracle on sampled rows."""
+    m, ctx, tree, near, g = _setup(3, BENCH_LEAF)
+    x = meshes.make_x(3, m.n)
+    z = m.verts[m.tris].mean(axis=1)[:, 2]
+    s = 10.0 ** (-16.0 * (z - z.min()) / max(z.max() - z.min(), 1e-30))
+    x = (x * s[None, :]).astype(np.complex64)
+    y = run_mvm(tree, near, x)
+    rows = _rows(m.n)
+    yref = oracle.mvm_rows(g, x, rows)
+    err = oracle.rel_l2(y[:, rows], yref)
+    print("skewed charges rel L2", err)
+    assert err <= TOL_FULL
