@@ -1042,16 +1042,31 @@ __device__ void p2p_leaf(
             for (int s0 = 0; s0 < total; s0 += kChunk) {
                 const int sn = min(kChunk, total - s0);
                 if (s0 > 0) sync();
-                for (int j = tid; j < sn; j += kNT) {
-                    const int f = s0 + j;
-                    const int li = find_seg(Uoff, nu, f);
-                    const int i = Upb[li] + (f - Uoff[li]);
-                    const float3 d = Ud[li];
-                    const float4 p = loc[i];
-                    Sp[j] = make_float4(p.x + d.x, p.y + d.y, p.z + d.z, 0.f);
-                    const float4* q = reinterpret_cast<const float4*>(xq + 8 * (int64_t)i);
-                    Sq[j][0] = q[0];
-                    Sq[j][1] = q[1];
+                // staging: a thread's sources j, j + kNT, ... ascend, so its window leaf is searched once and then
+                // advanced; two sources per round with all six loads issued before the stores
+                int li = tid < sn ? find_seg(Uoff, nu, s0 + tid) : 0;
+                for (int j = tid; j < sn; j += 2 * kNT) {
+                    const int f0 = s0 + j, f1 = f0 + kNT;
+                    const bool two = j + kNT < sn;
+                    while (Uoff[li + 1] <= f0) ++li;
+                    const int i0 = Upb[li] + (f0 - Uoff[li]);
+                    const float3 d0 = Ud[li];
+                    if (two)
+                        while (Uoff[li + 1] <= f1) ++li;
+                    const int i1 = two ? Upb[li] + (f1 - Uoff[li]) : i0;
+                    const float3 d1 = Ud[li];
+                    const float4 p0 = loc[i0], p1 = loc[i1];
+                    const float4* q0 = reinterpret_cast<const float4*>(xq + 8 * (int64_t)i0);
+                    const float4* q1 = reinterpret_cast<const float4*>(xq + 8 * (int64_t)i1);
+                    const float4 a0 = q0[0], b0 = q0[1], a1 = q1[0], b1 = q1[1];
+                    Sp[j] = make_float4(p0.x + d0.x, p0.y + d0.y, p0.z + d0.z, 0.f);
+                    Sq[j][0] = a0;
+                    Sq[j][1] = b0;
+                    if (two) {
+                        Sp[j + kNT] = make_float4(p1.x + d1.x, p1.y + d1.y, p1.z + d1.z, 0.f);
+                        Sq[j + kNT][0] = a1;
+                        Sq[j + kNT][1] = b1;
+                    }
                 }
                 sync();
                 if (act) {
