@@ -475,26 +475,33 @@ def run_xrl(args):
 
     roofs = {}
     if phases["m2l"][1]:
-        # tcgen05 3xTF32: per 21-pair tile 48 MMAs of M128 N128 K8 (2*128*128*8 flops each)
+        # the M2L runs 3xFP16 (kind::f16: per 21-pair tile 8 K-steps x 3 MMAs of M128 N128 K16) unless
+        # XRL_M2L_TF32=1 selects 3xTF32 (kind::tf32: 16 K-steps x 3 MMAs of M128 N128 K8); both issue
+        # 2*128*128*128*3 flops per tile
+        h16 = os.environ.get("XRL_M2L_TF32", "0") != "1"
         n_sub = _tc_subtiles(tree)
-        issued = n_sub * 48 * 2.0 * 128 * 128 * 8
-        tf32_peak = float(peaks.get("bf16_tflops", 1656.1)) * 0.5  # nominal tf32/bf16 dense ratio 1.1/2.25
-        ceil3 = tf32_peak / 3.0  # 3xTF32: three tf32 MMAs per FP32-accurate product
+        issued = n_sub * 3 * 2.0 * 128 * 128 * 128
+        bf16_peak = float(peaks.get("bf16_tflops", 1656.1))
+        tc_peak = bf16_peak if h16 else bf16_peak * 0.5  # f16 dense = bf16 dense; tf32 nominal 1.1/2.25 of it
+        ceil3 = tc_peak / 3.0  # three MMAs per FP32-accurate product
         alg_w = 2.0 * nc * nc * 6 * info["n_v_pairs"]
         ai = rate("m2l", alg_w, phases_iso) / 1e12
         a = rate("m2l", alg_w) / 1e12
         issued_i = rate("m2l", issued, phases_iso) / 1e12
-        roofs["m2l"] = {"kernel": "k_m2l_tc", "bound": "tensor", "achieved": ai, "peak": tf32_peak, "unit": "TFLOP/s",
-                        "frac": ai / tf32_peak, "traffic": traffic_from_profiles("k_m2l_tc", tkey),
+        kind = "3xFP16 kind::f16, 24 MMAs M128 N128 K16" if h16 else "3xTF32 kind::tf32, 48 MMAs M128 N128 K8"
+        roofs["m2l"] = {"kernel": "k_m2l_tc", "bound": "tensor", "achieved": ai, "peak": tc_peak, "unit": "TFLOP/s",
+                        "frac": ai / tc_peak, "traffic": traffic_from_profiles("k_m2l_tc", tkey),
                         "ms": per_launch_ms("m2l", phases_iso),
-                        "frac_of_3xtf32_ceiling": ai / ceil3, "frac_of_fp32_simt_peak": ai / fp32_peak,
-                        "in_step": {"achieved": a, "frac": a / tf32_peak, "ms": per_launch_ms("m2l")},
-                        "issued": {"achieved": issued_i, "frac": issued_i / tf32_peak,
-                                   "what": f"{n_sub} tiles x 48 tcgen05 kind::tf32 MMAs (M128 N128 K8) per launch"},
+                        ("frac_of_3xf16_ceiling" if h16 else "frac_of_3xtf32_ceiling"): ai / ceil3,
+                        "frac_of_fp32_simt_peak": ai / fp32_peak,
+                        "in_step": {"achieved": a, "frac": a / tc_peak, "ms": per_launch_ms("m2l")},
+                        "issued": {"achieved": issued_i, "frac": issued_i / tc_peak,
+                                   "what": f"{n_sub} tiles x ({kind}) per launch"},
                         "algorithmic": f"{2 * nc * nc * 6} flops (121 x 121 operator x 6 RHS, dense) x "
                                        f"{info['n_v_pairs']} V-list translations per launch",
-                        "peak_source": "tf32 dense = bf16_tflops (MEASURED_PEAKS.json) x 0.5 (nominal 1.1/2.25 PF); "
-                                       "3xTF32 ceiling = that / 3"}
+                        "peak_source": ("f16 dense = bf16_tflops (MEASURED_PEAKS.json)" if h16 else
+                                        "tf32 dense = bf16_tflops (MEASURED_PEAKS.json) x 0.5 (nominal 1.1/2.25 PF)")
+                                       + "; 3x ceiling = that / 3"}
     if phases["p2p"][1]:
         w = 20.0 * info["n_p2p"]
         a, ai = rate("p2p", w) / 1e12, rate("p2p", w, phases_iso) / 1e12
@@ -513,16 +520,25 @@ def run_xrl(args):
     if phases["near"][1]:
         ni = near.info()
         nl_ = tree.n_local
-        byts = 6.0 * ni["n_entries"] + 16.0 * ni["n_segments"] + 24.0 * nl_ + 48.0 * nl_
+        # SURVEY §8(d)'s per-unit figure for the near SpMV: 8 B per nnz (FP32 value + int32 column) + 8 B per row
+        # (row pointer) + 24 B per row (x, read once) + 48 B per row (y read-modify-write).  The row-group format
+        # streams its own bytes (18 B per union-column slot + 16 B per segment), reported beside it.
+        # the CSR holds every row; on a partitioned tree the owned rows' share is taken pro rata
+        nnz_loc = ni["nnz"] if nl_ == tree.n else int(ni["nnz"] * nl_ / tree.n)
+        byts = 8.0 * nnz_loc + 80.0 * nl_
+        fmt = 18.0 * ni["n_entries"] + 16.0 * ni["n_segments"] + 72.0 * nl_
         a, ai = rate("near", byts) / 1e9, rate("near", byts, phases_iso) / 1e9
-        roofs["near"] = {"kernel": "k_near_seg", "bound": "hbm", "achieved": ai, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": ai / hbm_peak, "traffic": traffic_from_profiles("k_near_seg", tkey),
+        roofs["near"] = {"kernel": "k_near_rg", "bound": "hbm", "achieved": ai, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": ai / hbm_peak, "traffic": traffic_from_profiles("k_near_rg", tkey),
                          "ms": per_launch_ms("near", phases_iso),
                          "in_step": {"achieved": a, "frac": a / hbm_peak, "ms": per_launch_ms("near")},
-                         "algorithmic": f"6 B x {ni['n_entries']} padded entries (FP32 value + u16 column offset; "
-                                        f"{nnz} nnz) + 16 B x {ni['n_segments']} segments (row, base, offset) + "
-                                        f"24 B x {nl_} rows of x (read once) + 48 B x {nl_} rows of y "
-                                        f"(read-modify-write) per launch",
+                         "algorithmic": f"SURVEY 8(d): 8 B x {nnz_loc} nnz of the owned rows + 80 B x {nl_} rows "
+                                        f"(8 B row pointer, 24 B x read once, 48 B y read-modify-write) per launch",
+                         "format_bytes": fmt,
+                         "format_frac": rate("near", fmt, phases_iso) / 1e9 / hbm_peak,
+                         "format": f"row groups of 4 rows: 18 B x {ni['n_entries']} union-column slots (float4 of the "
+                                   f"4 rows' values + u16 column offset) + 16 B x {ni['n_segments']} segments + "
+                                   f"24 B x / 48 B y per row",
                          "peak_source": "hbm_gbs, MEASURED_PEAKS.json"}
     # dominant kernel: largest isolated time (the work that bounds the step)
     dom = max(roofs, key=lambda k: phases_iso[k][0]) if roofs else max(phases, key=lambda k: phases[k][0])
@@ -531,7 +547,8 @@ def run_xrl(args):
     roof["share_of_isolated_sum"] = phases_iso[dom][0] / sum(v[0] for v in phases_iso.values())
     roof["others"] = {k: {kk: v[kk] for kk in ("kernel", "bound", "achieved", "peak", "unit", "frac", "traffic", "ms",
                                                "in_step", "issued", "frac_of_3xtf32_ceiling",
-                                               "frac_of_fp32_simt_peak", "algorithmic") if kk in v}
+                                               "frac_of_fp32_simt_peak", "algorithmic", "format", "format_bytes",
+                                               "format_frac", "frac_of_3xf16_ceiling", "note") if kk in v}
                       for k, v in roofs.items() if k != dom}
 
     line = {

@@ -190,9 +190,10 @@ void xrl_near_destroy(xrl_near near);
 xrl_status xrl_near_export(xrl_near near, int64_t* row_ptr, int32_t* col, float* val32,
                            double* val64, int64_t* nnz);
 /* Sizes of the near field (any pointer may be NULL): nnz of the CSR (all rows), and of the
- * segment format the SpMV streams for this rank's rows: segments (runs of
- * <= 256 entries of one row whose columns share their upper 16 bits) and padded entries
- * (FP32 value + u16 lower column bits; 6 B each). */
+ * row-group format the SpMV streams for this rank's rows: segments (runs of
+ * <= 256 union columns of a group of 4 consecutive rows whose columns share their upper 16
+ * bits) and padded slots (one per union column: float4 of the 4 rows' FP32 values + u16 lower
+ * column bits; 18 B each). */
 xrl_status xrl_near_info(xrl_near near, int64_t* nnz, int64_t* n_segments, int64_t* n_entries);
 /* Selected rows of the CSR (tests on full-size meshes): rows host int64 [nrows]
  * (library order); cnt host int64 [nrows] receives each row's length; col,

@@ -9,9 +9,9 @@
 //
 // Kernels (one launch each unless noted):
 //   k_pack       complex64 [3][n] -> float [n][8] charges          (HBM, 48 B/panel)
-//   k_near_seg   near correction N x, 6-byte segment format (side stream)   (HBM / latency)
+//   k_near_rg<1> near correction N x, row-group format (side stream)      (HBM / L1 gathers)
 //   k_p2p        U-list direct sum, packed f32x2 (side stream)     (FP32 pipe)
-//   k_p2p12, k_near_seg12   the same for two triples in one pass (xrl_mvm nvec = 6k)
+//   k_p2p12, k_near_rg<2>   the same for two triples in one pass (xrl_mvm nvec = 6k)
 //   k_p2m        leaf multipoles mu = sum q Rt(u)                   (per leaf)
 //   (M2M)        child -> parent per level on the tensor-core translation kernel (k_m2l_tc)
 //   k_m2l_tc     V-list translations on tcgen05 (3xTF32, warp-specialised)
@@ -691,12 +691,12 @@ __global__ void __launch_bounds__(128) k_p2l(const int32_t* __restrict__ xt, con
 
 // ------------------------------------------------------------------ near-field SpMV
 // y += N x for the 6 real RHS (N: the near correction and the self terms) over the
-// segment format of near.cu (build_near_segments): 8 lanes per segment, 4 segments per warp.  A lane streams
-// its 4-entry chunks (chunks l8, l8 + 8, ...) as one float4 of values + one ushort4 of column offsets (6 B per
-// entry instead of 8 for int32 column + value), keeps the next chunk's loads in flight behind the current
-// chunk's 4 gathers of 32-byte charge records (L1-cached: neighbouring rows share their near columns), and
-// the 8 lanes reduce with shuffles; the segment total is added into y with vector L2 reductions (a row with
-// several segments adds several times; the L2P / M2P add concurrently).
+// row-group format of near.cu (build_near_groups): 8 lanes per segment, 4 segments per warp.  Per union column
+// of a group of 4 rows a lane gathers one 32-byte charge record (L1-cached: neighbouring groups share their
+// near columns) and applies the float4 of the 4 rows' values to it (24 FMAs).  A lane's next four column
+// offsets (one u64) are loaded one chunk ahead, so the offset -> gather chain of one chunk overlaps the
+// previous chunk; the 8 lanes reduce-scatter the 4 x 6 sums with 24 shuffles and add them into y with vector
+// L2 reductions (a group with several segments adds several times; the L2P / M2P add concurrently).
 
 // 32-byte read-only load through L1 (the charge records are re-read by neighbouring rows)
 __device__ __forceinline__ void ldg256_l1(const float* p, float* v)
@@ -748,19 +748,71 @@ __device__ __forceinline__ void ldg256_l1_keep(const float* p, float* v, uint64_
                  : "l"(p), "l"(pol));
 }
 
-// Persistent 8-lane teams: team t takes segments t, t + T, ...; a segment's header is loaded one segment
-// ahead and the first chunk of the next segment is loaded during the current segment's last chunk, so the
-// (header -> chunk -> gather) chain of one segment overlaps the previous one (segments are short: ~75
-// entries, 2-3 chunks per lane).
-__global__ void __launch_bounds__(256, 4) k_near_seg(int64_t nseg, const int32_t* __restrict__ seg_row,
-                                                    const int32_t* __restrict__ seg_base,
-                                                    const int64_t* __restrict__ seg_off, const float* __restrict__ eval,
-                                                    const uint16_t* __restrict__ eoff, const float* __restrict__ xq,
-                                                    int64_t nl, float2* __restrict__ y)
+__device__ __forceinline__ float4 ldg_stream4v(const float4* p, uint64_t pol)
 {
-    // each CTA owns a contiguous, entry-balanced range of segments (consecutive rows share most of their
-    // columns, so the CTA's charge gathers hit L1 again on the next rows); its teams take the range's segments
-    // round-robin
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+
+// a[j * 6 + r] (row j of the group, RHS r) summed over the 8 lanes of a team; lane l8 ends with the sums of row
+// 2 (l8 >> 2 & 1) + (l8 >> 1 & 1) in c[0..5] (xor 4 halves the rows, xor 2 halves them again, xor 1 all-reduces)
+__device__ __forceinline__ void rg_reduce(const float (&a)[24], int l8, float (&c)[6])
+{
+    const unsigned m = 0xffu << (threadIdx.x & 24);  // the team's lanes (teams of a warp may leave the loop apart)
+    const bool h2 = l8 & 4, h1 = l8 & 2;
+    float b[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const float send = h2 ? a[k] : a[12 + k], keep = h2 ? a[12 + k] : a[k];
+        b[k] = keep + __shfl_xor_sync(m, send, 4);
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const float send = h1 ? b[k] : b[6 + k], keep = h1 ? b[6 + k] : b[k];
+        c[k] = keep + __shfl_xor_sync(m, send, 2);
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) c[k] += __shfl_xor_sync(m, c[k], 1);
+}
+
+// NT = 1: one triple (xq -> y); NT = 2: two triples in one pass over the format (xq -> y, xq2 -> y2).
+// Each CTA owns a contiguous, slot-balanced range of segments (consecutive groups share most of their columns,
+// so the CTA's charge gathers hit L1 again); its 32 teams take the range's segments round-robin.
+#ifndef XRL_NEAR_MINB
+#define XRL_NEAR_MINB 2
+#endif
+#ifndef XRL_NEAR_PFW
+#define XRL_NEAR_PFW 0
+#endif
+constexpr bool kNearPfw = XRL_NEAR_PFW;
+#ifndef XRL_NEAR_G6
+#define XRL_NEAR_G6 0
+#endif
+// charge record gather: one 32-byte load (8 registers), or XRL_NEAR_G6 16 + 8 bytes (6 registers, 2 requests)
+constexpr int kNearQ = XRL_NEAR_G6 ? 6 : 8;
+__device__ __forceinline__ void ldg_rec_keep(const float* p, float* v, uint64_t pol)
+{
+    if (XRL_NEAR_G6) {
+        asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "l"(p), "l"(pol));
+        asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;" : "=f"(v[4]), "=f"(v[5]) : "l"(p + 4), "l"(pol));
+    } else {
+        ldg256_l1_keep(p, v, pol);
+    }
+}
+#ifndef XRL_NEAR_NT
+#define XRL_NEAR_NT 256
+#endif
+template <int NT>
+__global__ void __launch_bounds__(XRL_NEAR_NT, NT == 1 ? XRL_NEAR_MINB : 512 / XRL_NEAR_NT) k_near_rg(int64_t nseg, const int32_t* __restrict__ seg_grp,
+                                                  const int32_t* __restrict__ seg_base,
+                                                  const int64_t* __restrict__ seg_off, const float4* __restrict__ gval,
+                                                  const uint16_t* __restrict__ eoff, const float* __restrict__ xq,
+                                                  const float* __restrict__ xq2, int64_t nl, float2* __restrict__ y,
+                                                  float2* __restrict__ y2)
+{
     __shared__ int64_t rng[2];
     if (threadIdx.x < 2) {
         const int64_t E = __ldg(seg_off + nseg);
@@ -778,57 +830,85 @@ __global__ void __launch_bounds__(256, 4) k_near_seg(int64_t nseg, const int32_t
     const int l8 = threadIdx.x & 7;
     const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
     int64_t s = rng[0] + (threadIdx.x >> 3);
-    int64_t b0 = 0, b1 = 0;  // entry range of segment s
+    int64_t b0 = 0, b1 = 0;  // slot range of segment s
     int32_t base = 0;
     if (s < s_end) { b0 = __ldg(seg_off + s); b1 = __ldg(seg_off + s + 1); base = __ldg(seg_base + s); }
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     uint2 o = make_uint2(0u, 0u);
-    if (s < s_end && b0 + 4 * l8 < b1) { v = ldg_stream4(eval + b0 + 4 * l8, pol_stream); o = ldg_stream_u64(eoff + b0 + 4 * l8, pol_stream); }
+    if (s < s_end && b0 + 4 * l8 < b1) o = ldg_stream_u64(eoff + b0 + 4 * l8, pol_stream);
+    // values of the chunk at block start `bs` of a segment ending at `be` (the lane's u-th value at u nc + l8)
+    auto load_w = [&](int64_t bs, int64_t be, float4 (&w)[4]) {
+        const int nc = (int)(be - bs < 32 ? be - bs : 32) >> 2;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            w[u] = l8 < nc ? ldg_stream4v(gval + bs + u * nc + l8, pol_stream) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    float4 pw[4];  // XRL_NEAR_PFW: the next chunk's values, loaded one chunk ahead like the offsets
+    if (kNearPfw) {
+        if (s < s_end) load_w(b0, b1, pw);
+        else for (int u = 0; u < 4; ++u) pw[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     while (s < s_end) {
         const int64_t sn = s + nteams;
         int64_t n0 = 0, n1 = 0;
         int32_t nbase = 0;
         if (sn < s_end) { n0 = __ldg(seg_off + sn); n1 = __ldg(seg_off + sn + 1); nbase = __ldg(seg_base + sn); }
-        const int32_t row = __ldg(seg_row + s);
-        const float* xb = xq + 8 * (int64_t)base;
-        float a[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const int64_t grp = __ldg(seg_grp + s);
+        float a[NT][24];
+#pragma unroll
+        for (int v = 0; v < NT; ++v)
+#pragma unroll
+            for (int k = 0; k < 24; ++k) a[v][k] = 0.f;
         const int nit = (int)((b1 - b0 + 31) >> 5);  // chunk rounds of the team (uniform over its 8 lanes)
         for (int it = 0; it < nit; ++it) {
-            const int64_t pos = b0 + 32 * it + 4 * l8;
-            if (pos >= b1) {  // a lane past its segment's end gathers record `base` with weight 0 (no branches)
-                v = make_float4(0.f, 0.f, 0.f, 0.f);
-                o = make_uint2(0u, 0u);
-            }
-            float q[4][8];
-            ldg256_l1_keep(xb + 8 * (o.x & 0xffff), q[0], pol_keep);
-            ldg256_l1_keep(xb + 8 * (o.x >> 16), q[1], pol_keep);
-            ldg256_l1_keep(xb + 8 * (o.y & 0xffff), q[2], pol_keep);
-            ldg256_l1_keep(xb + 8 * (o.y >> 16), q[3], pol_keep);
-            const float w0 = v.x, w1 = v.y, w2 = v.z, w3 = v.w;
-            // the next chunk: this segment's, else the next segment's first
-            const int64_t np = it + 1 < nit ? pos + 32 : n0 + 4 * l8;
+            const int64_t blk = b0 + 32 * it;
+            const int nc = (int)(b1 - blk < 32 ? b1 - blk : 32) >> 2;  // lanes with a chunk in this block
+            const bool act = l8 < nc;
+            // a lane without a chunk gathers record `base` with weight 0 (no branches around the gathers)
+            const uint32_t c0 = act ? o.x & 0xffff : 0u, c1 = act ? o.x >> 16 : 0u;
+            const uint32_t c2 = act ? o.y & 0xffff : 0u, c3 = act ? o.y >> 16 : 0u;
+            // the next chunk's offsets: this segment's, else the next segment's first
+            const int64_t np = it + 1 < nit ? blk + 32 + 4 * l8 : n0 + 4 * l8;
             const int64_t ne = it + 1 < nit ? b1 : n1;
-            if ((it + 1 < nit || sn < s_end) && np < ne) {
-                v = ldg_stream4(eval + np, pol_stream);
-                o = ldg_stream_u64(eoff + np, pol_stream);
+            if ((it + 1 < nit || sn < s_end) && np < ne) o = ldg_stream_u64(eoff + np, pol_stream);
+            float4 w[4];
+            if (kNearPfw) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) w[u] = pw[u];
+                if (it + 1 < nit) load_w(blk + 32, b1, pw);
+                else if (sn < s_end) load_w(n0, n1, pw);
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    w[u] = act ? ldg_stream4v(gval + blk + u * nc + l8, pol_stream) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
-            for (int r = 0; r < 6; ++r) {
-                a[r] = fmaf(w0, q[0][r], a[r]);
-                a[r] = fmaf(w1, q[1][r], a[r]);
-                a[r] = fmaf(w2, q[2][r], a[r]);
-                a[r] = fmaf(w3, q[3][r], a[r]);
+            for (int v = 0; v < NT; ++v) {
+                const float* xb = (v == 0 ? xq : xq2) + 8 * (int64_t)base;
+                float q[4][kNearQ];
+                ldg_rec_keep(xb + 8 * c0, q[0], pol_keep);
+                ldg_rec_keep(xb + 8 * c1, q[1], pol_keep);
+                ldg_rec_keep(xb + 8 * c2, q[2], pol_keep);
+                ldg_rec_keep(xb + 8 * c3, q[3], pol_keep);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float wj[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int r = 0; r < 6; ++r) a[v][j * 6 + r] = fmaf(wj[j], q[u][r], a[v][j * 6 + r]);
+                }
             }
         }
 #pragma unroll
-        for (int r = 0; r < 6; ++r) {
-#pragma unroll
-            for (int d = 1; d < 8; d <<= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], d);
-        }
-        if (l8 < 3) {
-            const float re = l8 == 0 ? a[0] : (l8 == 1 ? a[2] : a[4]);  // (no dynamic register indexing)
-            const float im = l8 == 0 ? a[1] : (l8 == 1 ? a[3] : a[5]);
-            red_add2(y + l8 * nl + row, re, im);
+        for (int v = 0; v < NT; ++v) {
+            float c[6];
+            rg_reduce(a[v], l8, c);
+            const int64_t row = kNearG * grp + 2 * ((l8 >> 2) & 1) + ((l8 >> 1) & 1);
+            float2* yv = v == 0 ? y : y2;
+            if (row < nl) {
+                if (l8 & 1) red_add2(yv + 2 * nl + row, c[4], c[5]);
+                else { red_add2(yv + row, c[0], c[1]); red_add2(yv + nl + row, c[2], c[3]); }
+            }
         }
         s = sn;
         b0 = n0;
@@ -1318,94 +1398,6 @@ __global__ void __launch_bounds__(128) k_p2p12(
                invW, 0, n, p0, y, y2);
 }
 
-// the near SpMV of k_near_seg for two triples: one pass over the entries, gathers from xq and xq2
-__global__ void __launch_bounds__(256, 3) k_near_seg12(int64_t nseg, const int32_t* __restrict__ seg_row,
-                                                       const int32_t* __restrict__ seg_base,
-                                                       const int64_t* __restrict__ seg_off,
-                                                       const float* __restrict__ eval, const uint16_t* __restrict__ eoff,
-                                                       const float* __restrict__ xq, const float* __restrict__ xq2,
-                                                       int64_t nl, float2* __restrict__ y, float2* __restrict__ y2)
-{
-    const int64_t team = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
-    const int64_t nteams = ((int64_t)gridDim.x * blockDim.x) >> 3;
-    const int l8 = threadIdx.x & 7;
-    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
-    int64_t s = team;
-    int64_t b0 = 0, b1 = 0;
-    int32_t base = 0;
-    if (s < nseg) { b0 = __ldg(seg_off + s); b1 = __ldg(seg_off + s + 1); base = __ldg(seg_base + s); }
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint2 o = make_uint2(0u, 0u);
-    if (s < nseg && b0 + 4 * l8 < b1) { v = ldg_stream4(eval + b0 + 4 * l8, pol_stream); o = ldg_stream_u64(eoff + b0 + 4 * l8, pol_stream); }
-    while (s < nseg) {
-        const int64_t sn = s + nteams;
-        int64_t n0 = 0, n1 = 0;
-        int32_t nbase = 0;
-        if (sn < nseg) { n0 = __ldg(seg_off + sn); n1 = __ldg(seg_off + sn + 1); nbase = __ldg(seg_base + sn); }
-        const int32_t row = __ldg(seg_row + s);
-        const float* xb = xq + 8 * (int64_t)base;
-        const float* xb2 = xq2 + 8 * (int64_t)base;
-        float a[12];
-#pragma unroll
-        for (int r = 0; r < 12; ++r) a[r] = 0.f;
-        const int nit = (int)((b1 - b0 + 31) >> 5);
-        for (int it = 0; it < nit; ++it) {
-            const int64_t pos = b0 + 32 * it + 4 * l8;
-            if (pos >= b1) {
-                v = make_float4(0.f, 0.f, 0.f, 0.f);
-                o = make_uint2(0u, 0u);
-            }
-            const uint32_t c0 = o.x & 0xffff, c1 = o.x >> 16, c2 = o.y & 0xffff, c3 = o.y >> 16;
-            const float w0 = v.x, w1 = v.y, w2 = v.z, w3 = v.w;
-            const int64_t np = it + 1 < nit ? pos + 32 : n0 + 4 * l8;
-            const int64_t ne = it + 1 < nit ? b1 : n1;
-            if ((it + 1 < nit || sn < nseg) && np < ne) {
-                v = ldg_stream4(eval + np, pol_stream);
-                o = ldg_stream_u64(eoff + np, pol_stream);
-            }
-            float q[4][8];
-            ldg256_l1_keep(xb + 8 * c0, q[0], pol_keep);
-            ldg256_l1_keep(xb + 8 * c1, q[1], pol_keep);
-            ldg256_l1_keep(xb + 8 * c2, q[2], pol_keep);
-            ldg256_l1_keep(xb + 8 * c3, q[3], pol_keep);
-#pragma unroll
-            for (int r = 0; r < 6; ++r) {
-                a[r] = fmaf(w0, q[0][r], a[r]);
-                a[r] = fmaf(w1, q[1][r], a[r]);
-                a[r] = fmaf(w2, q[2][r], a[r]);
-                a[r] = fmaf(w3, q[3][r], a[r]);
-            }
-            ldg256_l1_keep(xb2 + 8 * c0, q[0], pol_keep);
-            ldg256_l1_keep(xb2 + 8 * c1, q[1], pol_keep);
-            ldg256_l1_keep(xb2 + 8 * c2, q[2], pol_keep);
-            ldg256_l1_keep(xb2 + 8 * c3, q[3], pol_keep);
-#pragma unroll
-            for (int r = 0; r < 6; ++r) {
-                a[6 + r] = fmaf(w0, q[0][r], a[6 + r]);
-                a[6 + r] = fmaf(w1, q[1][r], a[6 + r]);
-                a[6 + r] = fmaf(w2, q[2][r], a[6 + r]);
-                a[6 + r] = fmaf(w3, q[3][r], a[6 + r]);
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 12; ++r) {
-#pragma unroll
-            for (int d = 1; d < 8; d <<= 1) a[r] += __shfl_xor_sync(0xffffffffu, a[r], d);
-        }
-        if (l8 < 6) {
-            const int c = l8 % 3;
-            float re, im;
-            if (l8 < 3) { re = c == 0 ? a[0] : (c == 1 ? a[2] : a[4]); im = c == 0 ? a[1] : (c == 1 ? a[3] : a[5]); }
-            else { re = c == 0 ? a[6] : (c == 1 ? a[8] : a[10]); im = c == 0 ? a[7] : (c == 1 ? a[9] : a[11]); }
-            red_add2((l8 < 3 ? y : y2) + c * nl + row, re, im);
-        }
-        s = sn;
-        b0 = n0;
-        b1 = n1;
-        base = nbase;
-    }
-}
-
 // ell[r][k] (r-major, M2L/L2L layout) -> ellk[k][8] (k-major, 6 RHS + 2 pad) for the leaves: the L2P
 // then reads one 32-byte record per coefficient instead of 6 scalars.
 __global__ void k_ell_kmajor(const int32_t* __restrict__ leaves, const float* __restrict__ ell, float* __restrict__ ellk)
@@ -1729,17 +1721,16 @@ static void launch_near(Mvm& M)
         // the SpMV adds into y: in the near-only mode it starts from zero
         if (!M.do_far && M.nl > 0) XRL_CUDA(cudaMemsetAsync(M.y, 0, sizeof(float2) * 3 * (size_t)M.nl, M.side));
         if (!M.do_far && M.nl > 0 && M.y2) XRL_CUDA(cudaMemsetAsync(M.y2, 0, sizeof(float2) * 3 * (size_t)M.nl, M.side));
-        if (nr->n_segs > 0 && M.xq2) {
-            const int grid = (int)std::min<int64_t>(nblk(8 * nr->n_segs, 256), 3 * ctx->num_sms);
-            k_near_seg12<<<grid, 256, 0, M.side>>>(nr->n_segs, nr->seg_row.p, nr->seg_base.p, nr->seg_off.p,
-                                                   nr->eval.p, nr->eoff.p, M.xq, M.xq2, M.nl, M.y, M.y2);
-            XRL_LAUNCH_CHECK();
-            ctx->launches += 1;
-        } else if (nr->n_segs > 0) {
-            const int grid = (int)std::min<int64_t>(nblk(8 * nr->n_segs, 256), 4 * ctx->num_sms);
-            k_near_seg<<<grid, 256, 0, M.side>>>(nr->n_segs, nr->seg_row.p, nr->seg_base.p,
-                                                                      nr->seg_off.p, nr->eval.p, nr->eoff.p, t->xq.p,
-                                                                      M.nl, M.y);
+        if (nr->n_segs > 0) {
+            // persistent: XRL_NEAR_MINB (2) CTAs of 256 per SM, each a slot-balanced range of segments
+            const int grid = (int)std::min<int64_t>(nblk(8 * nr->n_segs, XRL_NEAR_NT),
+                                                    (M.xq2 ? 512 / XRL_NEAR_NT : XRL_NEAR_MINB) * ctx->num_sms);
+            if (M.xq2)
+                k_near_rg<2><<<grid, XRL_NEAR_NT, 0, M.side>>>(nr->n_segs, nr->seg_grp.p, nr->seg_base.p, nr->seg_off.p,
+                                                              nr->gval.p, nr->eoff.p, M.xq, M.xq2, M.nl, M.y, M.y2);
+            else
+                k_near_rg<1><<<grid, XRL_NEAR_NT, 0, M.side>>>(nr->n_segs, nr->seg_grp.p, nr->seg_base.p, nr->seg_off.p,
+                                                              nr->gval.p, nr->eoff.p, t->xq.p, nullptr, M.nl, M.y, nullptr);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
@@ -2014,7 +2005,7 @@ static xrl_status mvm_triple(xrl_tree t, xrl_near nr, const float2* x, float2* y
     return XRL_OK;
 }
 
-// Two triples of a single-rank tree: the side stream's P2P and near SpMV serve both (k_p2p12, k_near_seg12:
+// Two triples of a single-rank tree: the side stream's P2P and near SpMV serve both (k_p2p12, k_near_rg<2>:
 // one pass over the U lists and the near entries for 12 right-hand sides); the FMM expansions (mu, ell: one
 // triple's worth of tree scratch) run for the first triple, then for the second, on the work stream.
 static void mvm_pair(xrl_tree t, xrl_near nr, const float2* xa, float2* ya, const float2* xb, float2* yb,

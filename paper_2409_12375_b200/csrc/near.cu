@@ -233,88 +233,133 @@ __global__ void k_near_values(int64_t n, const int64_t* __restrict__ ptr, const 
 
 inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
-// ---------------------------------------------------------------- segment format of the near SpMV
-// (SURVEY §8(a) a12).  The owned rows' entries are cut into segments: a run of one row's (ascending) columns
-// that share their upper 16 bits, at most kNearSegLen entries long.  A segment stores its row, the column
-// base (upper bits) and per entry the FP32 value and the u16 lower column bits: 6 B per entry instead of
-// 8 B for (int32 column, FP32 value).  Near columns of a Morton-ordered row are clustered, so a row has
-// ~1.4 segments on config 4; the length cap bounds the work of the 8 lanes a segment gets.  Each segment's
-// entries are padded to a multiple of 4 (value 0, offset repeated) for float4 / ushort4 loads and stored
-// lane-interleaved within blocks of 32 (k_seg_fill), so a warp's gathers touch consecutive columns.
+// ---------------------------------------------------------------- row-group format of the near SpMV
+// (SURVEY §8(a) a12).  The owned rows are taken in groups of kNearG = 4 consecutive rows (Morton order, so the
+// rows of a group are neighbouring panels with overlapping near sets).  A group's columns are the sorted union
+// of its rows' columns; per union column the format stores one float4 of the four rows' N values (0 where a row
+// has no entry) and the u16 lower column bits.  The union is cut into segments: runs that share the upper 16
+// column bits, at most kNearSegLen union columns long.  A segment stores its group, the column base and its
+// slot offset.  One 32-byte charge gather then serves up to four rows (config 3: 2.6 entries per gather, 6.9 B
+// per entry): the per-row format was bound by its L1 gather wavefronts (ncu, r03g: L1 87 % busy, 2.2 TB/s).
+// Each segment is padded to a multiple of 4 slots (value 0, offset repeated).  Values are stored in the
+// union's column order; the u16 offsets are lane-interleaved within blocks of 32 slots: with nc = (slots of
+// the block) / 4, stored offset 4l + u is union column u nc + l, so lane l of a segment's 8 lanes reads its
+// four offsets as one u64 and its u-th value at u nc + l (the 8 lanes' u-th loads and gathers are consecutive).
 
-__global__ void k_seg_count(int64_t r0, int64_t nr, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                            int64_t* __restrict__ cnt)
+// visits the union columns of group g in ascending order: f(column, src[kNearG]) with src[i] the CSR entry of
+// row 4g + i at that column, or -1
+template <typename F>
+__device__ __forceinline__ void rg_merge(int64_t r0, int64_t nr, int64_t g, const int64_t* __restrict__ ptr,
+                                         const int32_t* __restrict__ col, F&& f)
 {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= nr) return;
-    const int64_t r = r0 + i;
-    int64_t c = 0;
-    int len = 0, hi = -1;
-    for (int64_t j = ptr[r]; j < ptr[r + 1]; ++j) {
-        const int h = col[j] >> 16;
-        if (h != hi || len == kNearSegLen) { ++c; hi = h; len = 0; }
-        ++len;
+    int64_t j[kNearG], e[kNearG];
+#pragma unroll
+    for (int i = 0; i < kNearG; ++i) {
+        const int64_t r = kNearG * g + i;
+        j[i] = r < nr ? ptr[r0 + r] : 0;
+        e[i] = r < nr ? ptr[r0 + r + 1] : 0;
     }
-    cnt[i] = c;
+    for (;;) {
+        int32_t c = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < kNearG; ++i)
+            if (j[i] < e[i]) c = min(c, col[j[i]]);
+        if (c == 0x7fffffff) break;
+        int64_t src[kNearG];
+#pragma unroll
+        for (int i = 0; i < kNearG; ++i) {
+            src[i] = -1;
+            if (j[i] < e[i] && col[j[i]] == c) src[i] = j[i]++;
+        }
+        f(c, src);
+    }
 }
 
-__global__ void k_seg_emit(int64_t r0, int64_t nr, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
-                           const int64_t* __restrict__ start, int32_t* __restrict__ seg_row, int32_t* __restrict__ seg_base,
-                           int64_t* __restrict__ seg_src, int32_t* __restrict__ seg_cnt, int64_t* __restrict__ seg_pad)
+__global__ void k_rg_count(int64_t r0, int64_t nr, int64_t ng, const int64_t* __restrict__ ptr,
+                           const int32_t* __restrict__ col, int64_t* __restrict__ cnt)
 {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= nr) return;
-    const int64_t r = r0 + i;
-    int64_t s = start[i] - 1;
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    int64_t c = 0;
+    int len = 0, hi = -1;
+    rg_merge(r0, nr, g, ptr, col, [&](int32_t cl, const int64_t*) {
+        const int h = cl >> 16;
+        if (h != hi || len == kNearSegLen) { ++c; hi = h; len = 0; }
+        ++len;
+    });
+    cnt[g] = c;
+}
+
+__global__ void k_rg_emit(int64_t r0, int64_t nr, int64_t ng, const int64_t* __restrict__ ptr,
+                          const int32_t* __restrict__ col, const int64_t* __restrict__ start,
+                          int32_t* __restrict__ seg_grp, int32_t* __restrict__ seg_base, int32_t* __restrict__ seg_cnt,
+                          int64_t* __restrict__ seg_pad)
+{
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    int64_t s = start[g] - 1;
     int len = 0, hi = -1;
     auto close = [&]() {
-        if (s >= start[i]) { seg_cnt[s] = len; seg_pad[s] = (len + 3) & ~3; }
+        if (s >= start[g]) { seg_cnt[s] = len; seg_pad[s] = (len + 3) & ~3; }
     };
-    for (int64_t j = ptr[r]; j < ptr[r + 1]; ++j) {
-        const int h = col[j] >> 16;
+    rg_merge(r0, nr, g, ptr, col, [&](int32_t cl, const int64_t*) {
+        const int h = cl >> 16;
         if (h != hi || len == kNearSegLen) {
             close();
             ++s;
-            seg_row[s] = (int32_t)i;
+            seg_grp[s] = (int32_t)g;
             seg_base[s] = h << 16;
-            seg_src[s] = j;
             hi = h;
             len = 0;
         }
         ++len;
-    }
+    });
     close();
 }
 
-// one warp per segment: FP32 values and u16 lower column bits; the padding repeats the last offset with
-// value 0 (keeps every gather inside the segment's column block)
-__global__ void k_seg_fill(int64_t nseg, const int32_t* __restrict__ seg_base, const int64_t* __restrict__ seg_src,
-                           const int32_t* __restrict__ seg_cnt, const int64_t* __restrict__ seg_off,
-                           const int32_t* __restrict__ col, const float* __restrict__ val, float* __restrict__ eval,
-                           uint16_t* __restrict__ eoff)
+// stored index of union column e of a segment with `padded` slots (offset interleave above)
+__device__ __forceinline__ int64_t rg_off_slot(int64_t e, int64_t padded)
 {
-    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (s >= nseg) return;
-    const int64_t src = seg_src[s], dst = seg_off[s], padded = seg_off[s + 1] - dst;
-    const int32_t base = seg_base[s];
-    const int cnt = seg_cnt[s];
-    for (int64_t i = lane; i < padded; i += 32) {
-        // within each block of 32 stored entries (8 chunks of 4: one per lane of the segment), chunk l holds the
-        // logical entries l, l + nc, l + 2 nc, l + 3 nc (nc = chunks in the block), so the 8 lanes' u-th
-        // gathers hit 8 consecutive columns (one or two cache lines) instead of a strided set
-        const int64_t blk = i & ~int64_t(31);
-        const int nc = (int)((padded - blk < 32 ? padded - blk : 32) >> 2);
-        const int q = (int)(i - blk), l = q >> 2, u = q & 3;
-        const int64_t e = blk + u * nc + l;
-        const int64_t j = src + (e < cnt ? e : cnt - 1);
-        eval[dst + i] = e < cnt ? val[j] : 0.f;
-        eoff[dst + i] = (uint16_t)(col[j] - base);
-    }
+    const int64_t blk = e & ~int64_t(31);
+    const int nc = (int)((padded - blk < 32 ? padded - blk : 32) >> 2);
+    const int q = (int)(e - blk);
+    return blk + 4 * (q % nc) + q / nc;
+}
+
+__global__ void k_rg_fill(int64_t r0, int64_t nr, int64_t ng, const int64_t* __restrict__ ptr,
+                          const int32_t* __restrict__ col, const float* __restrict__ val,
+                          const int64_t* __restrict__ start, const int32_t* __restrict__ seg_base,
+                          const int32_t* __restrict__ seg_cnt, const int64_t* __restrict__ seg_off,
+                          float4* __restrict__ gval, uint16_t* __restrict__ eoff)
+{
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    int64_t s = start[g];
+    int64_t e = 0;
+    uint16_t last = 0;
+    auto pad = [&]() {  // padding slots of segment s (after its seg_cnt union columns)
+        const int64_t dst = seg_off[s], padded = seg_off[s + 1] - dst;
+        for (int64_t k = seg_cnt[s]; k < padded; ++k) {
+            gval[dst + k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            eoff[dst + rg_off_slot(k, padded)] = last;
+        }
+    };
+    rg_merge(r0, nr, g, ptr, col, [&](int32_t cl, const int64_t* src) {
+        if (e == seg_cnt[s]) { pad(); ++s; e = 0; }
+        const int64_t dst = seg_off[s], padded = seg_off[s + 1] - dst;
+        float w[kNearG];
+#pragma unroll
+        for (int i = 0; i < kNearG; ++i) w[i] = src[i] >= 0 ? val[src[i]] : 0.f;
+        gval[dst + e] = make_float4(w[0], w[1], w[2], w[3]);
+        last = (uint16_t)(cl - seg_base[s]);
+        eoff[dst + rg_off_slot(e, padded)] = last;
+        ++e;
+    });
+    if (e > 0) pad();
 }
 }  // namespace
 
-// Segment format (above) for the owned rows [t->p0, t->p1) of the CSR in N.
+// Row-group format (above) for the owned rows [t->p0, t->p1) of the CSR in N.
 template <typename T>
 static void exclusive_sum(const T* in, T* out, int64_t n, cudaStream_t st)
 {
@@ -324,9 +369,10 @@ static void exclusive_sum(const T* in, T* out, int64_t n, cudaStream_t st)
     XRL_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, st));
 }
 
-static void build_near_segments(xrl_tree t, xrl_near N, cudaStream_t st)
+static void build_near_groups(xrl_tree t, xrl_near N, cudaStream_t st)
 {
-    const int64_t r0 = t->p0, nr = t->p1 - t->p0;
+    static_assert(kNearG == 4, "the SpMV kernel reads one float4 of values per union column");
+    const int64_t r0 = t->p0, nr = t->p1 - t->p0, ng = (nr + kNearG - 1) / kNearG;
     N->n_segs = 0;
     N->n_entries = 0;
     if (nr <= 0) {
@@ -335,31 +381,31 @@ static void build_near_segments(xrl_tree t, xrl_near N, cudaStream_t st)
         XRL_CUDA(cudaStreamSynchronize(st));
         return;
     }
-    DBuf<int64_t> cnt(nr + 1), start(nr + 1);
-    XRL_CUDA(cudaMemsetAsync(cnt.p + nr, 0, 8, st));
-    k_seg_count<<<nblk(nr, 256), 256, 0, st>>>(r0, nr, N->row_ptr.p, N->col.p, cnt.p);
+    DBuf<int64_t> cnt(ng + 1), start(ng + 1);
+    XRL_CUDA(cudaMemsetAsync(cnt.p + ng, 0, 8, st));
+    k_rg_count<<<nblk(ng, 128), 128, 0, st>>>(r0, nr, ng, N->row_ptr.p, N->col.p, cnt.p);
     XRL_LAUNCH_CHECK();
-    exclusive_sum(cnt.p, start.p, nr + 1, st);
+    exclusive_sum(cnt.p, start.p, ng + 1, st);
     int64_t nseg = 0;
-    XRL_CUDA(cudaMemcpyAsync(&nseg, start.p + nr, 8, cudaMemcpyDeviceToHost, st));
+    XRL_CUDA(cudaMemcpyAsync(&nseg, start.p + ng, 8, cudaMemcpyDeviceToHost, st));
     XRL_CUDA(cudaStreamSynchronize(st));
     N->n_segs = nseg;
-    N->seg_row.alloc(nseg);
+    N->seg_grp.alloc(nseg);
     N->seg_base.alloc(nseg);
     N->seg_off.alloc(nseg + 1);
-    DBuf<int64_t> src(nseg), pad(nseg + 1);
+    DBuf<int64_t> pad(nseg + 1);
     DBuf<int32_t> scnt(nseg);
     XRL_CUDA(cudaMemsetAsync(pad.p + nseg, 0, 8, st));
-    k_seg_emit<<<nblk(nr, 256), 256, 0, st>>>(r0, nr, N->row_ptr.p, N->col.p, start.p, N->seg_row.p, N->seg_base.p,
-                                              src.p, scnt.p, pad.p);
+    k_rg_emit<<<nblk(ng, 128), 128, 0, st>>>(r0, nr, ng, N->row_ptr.p, N->col.p, start.p, N->seg_grp.p,
+                                             N->seg_base.p, scnt.p, pad.p);
     XRL_LAUNCH_CHECK();
     exclusive_sum(pad.p, N->seg_off.p, nseg + 1, st);
     XRL_CUDA(cudaMemcpyAsync(&N->n_entries, N->seg_off.p + nseg, 8, cudaMemcpyDeviceToHost, st));
     XRL_CUDA(cudaStreamSynchronize(st));
-    N->eval.alloc(std::max<int64_t>(4, N->n_entries));
+    N->gval.alloc(std::max<int64_t>(4, N->n_entries));
     N->eoff.alloc(std::max<int64_t>(4, N->n_entries));
-    k_seg_fill<<<nblk(nseg * 32, 256), 256, 0, st>>>(nseg, N->seg_base.p, src.p, scnt.p, N->seg_off.p, N->col.p,
-                                                    N->val.p, N->eval.p, N->eoff.p);
+    k_rg_fill<<<nblk(ng, 128), 128, 0, st>>>(r0, nr, ng, N->row_ptr.p, N->col.p, N->val.p, start.p, N->seg_base.p,
+                                             scnt.p, N->seg_off.p, N->gval.p, N->eoff.p);
     XRL_LAUNCH_CHECK();
     XRL_CUDA(cudaStreamSynchronize(st));
 }
@@ -399,7 +445,7 @@ static xrl_status near_impl(xrl_tree t, double eta, int galerkin, xrl_near* out)
                                               t->pvid.p, galerkin, N->val.p, N->val64.p);
     XRL_LAUNCH_CHECK();
     // the segment format the SpMV streams (owned rows)
-    build_near_segments(t, N.get(), st);
+    build_near_groups(t, N.get(), st);
     // the halo of x a partitioned tree's MVM exchanges (near columns + remote P2P / P2L leaves)
     if (t->part_world > 1) build_halo_plan(t, N.get(), st);
     ++t->refs;

@@ -82,7 +82,11 @@ constexpr int kMuStride = 768;       // floats per box multipole mu[r][k] (r-maj
 constexpr int kOpM2M = 316, kOpL2L = 324, kNOpImg = 332;  // tensor-core operator images: M2L 0..315, M2M, L2L
 constexpr int kEllStride = 768;      // floats per box local expansion ell[r][k] (r-major, k padded to 128)
 constexpr int kEllKStride = 968;     // floats per leaf local expansion ellk[k][8] (k-major, for the L2P)
-constexpr int kNearSegLen = 256;     // near SpMV: max entries per segment (8 lanes each)
+#ifndef XRL_NEAR_SEGLEN
+#define XRL_NEAR_SEGLEN 96
+#endif
+constexpr int kNearSegLen = XRL_NEAR_SEGLEN;  // near SpMV: max union columns per segment (8 lanes each)
+constexpr int kNearG = 4;            // near SpMV: rows per row group
 
 }  // namespace xrl
 
@@ -221,13 +225,14 @@ struct xrl_near_s {
     xrl::DBuf<int32_t> col;
     xrl::DBuf<float> val;       // N_kl (FP32)
     xrl::DBuf<double> val64;    // P_kl (FP64, before subtraction)
-    // segment format of the owned rows for the SpMV (near.cu build_near_segments)
+    // row-group format of the owned rows for the SpMV (near.cu build_near_groups): n_entries slots, one per
+    // union column of a group of kNearG rows
     int64_t n_segs = 0, n_entries = 0;
-    xrl::DBuf<int32_t> seg_row;   // [n_segs] local row (row - p0)
+    xrl::DBuf<int32_t> seg_grp;   // [n_segs] local row group ((row - p0) / kNearG)
     xrl::DBuf<int32_t> seg_base;  // [n_segs] column base (upper 16 bits)
-    xrl::DBuf<int64_t> seg_off;   // [n_segs+1] padded entry offsets (multiples of 4)
-    xrl::DBuf<float> eval;        // [n_entries] N_kl (FP32), 0 in the padding
-    xrl::DBuf<uint16_t> eoff;     // [n_entries] column - base
+    xrl::DBuf<int64_t> seg_off;   // [n_segs+1] padded slot offsets (multiples of 4)
+    xrl::DBuf<float4> gval;       // [n_entries] the group's kNearG rows' N values (FP32), 0 where absent
+    xrl::DBuf<uint16_t> eoff;     // [n_entries] column - base, lane-interleaved per 32 slots
     // halo of x (exchange.cu; part_world > 1): panels peers read from this rank / this rank reads
     std::vector<int64_t> halo_soff, halo_roff;  // [world+1] panel offsets per peer
     xrl::DBuf<int32_t> halo_sidx, halo_ridx;

@@ -401,7 +401,7 @@ def test_schedules_agree(cfg, leaf):
 @pytest.mark.parametrize("flags", [0, 1, 2])
 def test_paired_triples_equal_single_triples(cfg, leaf, nvec, flags):
     """xrl_mvm with nvec = 6k runs the triples in pairs (one P2P / near pass for 12 right-hand sides,
-    k_p2p12 / k_near_seg12); each triple of the result equals the same triple run alone (nvec = 3) up to
+    k_p2p12 / k_near_rg<2>); each triple of the result equals the same triple run alone (nvec = 3) up to
     the FP32 summation order, for the full, near-only and far-only products, and the paired full product
     matches the oracle on sampled rows (north-star bound)."""
     import torch

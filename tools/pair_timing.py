@@ -1,4 +1,4 @@
-"""Two triples per traversal (xrl_mvm nvec = 6: k_p2p12 / k_near_seg12) against one triple (nvec = 3), and
+"""Two triples per traversal (xrl_mvm nvec = 6: k_p2p12 / k_near_rg<2>) against one triple (nvec = 3), and
 the 2-port loop-space operator apply against the 1-port one.
 
     python tools/pair_timing.py [--config 4] [--leaf 384] [--reps 20] [--out file.json]"""
