@@ -993,33 +993,47 @@ __device__ __forceinline__ float rsqrt_ftz(float x)
     return r;
 }
 
-// Per source: 3 FADD2 + FMUL2 + 2 FFMA2 + 2 MUFU + 6 FFMA2 per two targets (7 issue slots per pair).
+// one source j against the thread's kTP2 target pairs
+template <bool kSelf>
+__device__ __forceinline__ void p2p_one(int j, const float4* __restrict__ Sp, const float4 (*__restrict__ Sq)[2],
+                                        const f2x* tx, const f2x* ty, const f2x* tz, f2x (*acc)[6])
+{
+    const float4 sp = Sp[j];
+    const float4 q0 = Sq[j][0], q1 = Sq[j][1];
+    const f2x sx = pk2(sp.x, sp.x), sy = pk2(sp.y, sp.y), sz = pk2(sp.z, sp.z);
+    const f2x c0 = pk2(q0.x, q0.x), c1 = pk2(q0.y, q0.y), c2 = pk2(q0.z, q0.z);
+    const f2x c3 = pk2(q0.w, q0.w), c4 = pk2(q1.x, q1.x), c5 = pk2(q1.y, q1.y);
+#pragma unroll
+    for (int q = 0; q < kTP2; ++q) {
+        const f2x dx = sub2(tx[q], sx), dy = sub2(ty[q], sy), dz = sub2(tz[q], sz);
+        const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
+        float ra = rsqrt_ftz(r2.x), rb = rsqrt_ftz(r2.y);
+        if (kSelf) {
+            ra = r2.x > 0.f ? ra : 0.f;
+            rb = r2.y > 0.f ? rb : 0.f;
+        }
+        const f2x ri = pk2(ra, rb);
+        fma2_acc(acc[q][0], c0, ri); fma2_acc(acc[q][1], c1, ri); fma2_acc(acc[q][2], c2, ri);
+        fma2_acc(acc[q][3], c3, ri); fma2_acc(acc[q][4], c4, ri); fma2_acc(acc[q][5], c5, ri);
+    }
+}
+
+// Per source: 3 FADD2 + FMUL2 + 2 FFMA2 + 2 MUFU + 6 FFMA2 per two targets (7 issue slots per pair).  The main
+// loop takes kP2PUnroll sources per trip without guards, so ptxas interleaves one source's rsqrt chain with the
+// other's charge FMAs; the remainder follows.
 template <bool kSelf>
 __device__ __forceinline__ void p2p_range(int j0, int j1, int S, const float4* __restrict__ Sp,
                                           const float4 (*__restrict__ Sq)[2], const f2x* tx, const f2x* ty,
                                           const f2x* tz, f2x (*acc)[6])
 {
-#pragma unroll kP2PUnroll
-    for (int j = j0; j < j1; j += S) {
-        const float4 sp = Sp[j];
-        const float4 q0 = Sq[j][0], q1 = Sq[j][1];
-        const f2x sx = pk2(sp.x, sp.x), sy = pk2(sp.y, sp.y), sz = pk2(sp.z, sp.z);
-        const f2x c0 = pk2(q0.x, q0.x), c1 = pk2(q0.y, q0.y), c2 = pk2(q0.z, q0.z);
-        const f2x c3 = pk2(q0.w, q0.w), c4 = pk2(q1.x, q1.x), c5 = pk2(q1.y, q1.y);
+    int j = j0;
+#pragma unroll 1
+    for (; j + (kP2PUnroll - 1) * S < j1; j += kP2PUnroll * S) {
 #pragma unroll
-        for (int q = 0; q < kTP2; ++q) {
-            const f2x dx = sub2(tx[q], sx), dy = sub2(ty[q], sy), dz = sub2(tz[q], sz);
-            const float2 r2 = upk2(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))));
-            float ra = rsqrt_ftz(r2.x), rb = rsqrt_ftz(r2.y);
-            if (kSelf) {
-                ra = r2.x > 0.f ? ra : 0.f;
-                rb = r2.y > 0.f ? rb : 0.f;
-            }
-            const f2x ri = pk2(ra, rb);
-            fma2_acc(acc[q][0], c0, ri); fma2_acc(acc[q][1], c1, ri); fma2_acc(acc[q][2], c2, ri);
-            fma2_acc(acc[q][3], c3, ri); fma2_acc(acc[q][4], c4, ri); fma2_acc(acc[q][5], c5, ri);
-        }
+        for (int u = 0; u < kP2PUnroll; ++u) p2p_one<kSelf>(j + u * S, Sp, Sq, tx, ty, tz, acc);
     }
+#pragma unroll 1
+    for (; j < j1; j += S) p2p_one<kSelf>(j, Sp, Sq, tx, ty, tz, acc);
 }
 
 __device__ __forceinline__ int first_in_class(int lo, int sg, int S)
@@ -1125,7 +1139,10 @@ __device__ void p2p_leaf(
                 // staging: a thread's sources j, j + kNT, ... ascend, so its window leaf is searched once and then
                 // advanced; two sources per round with all six loads issued before the stores
                 int li = tid < sn ? find_seg(Uoff, nu, s0 + tid) : 0;
-                for (int j = tid; j < sn; j += 2 * kNT) {
+#ifdef XRL_P2P_DBG_NOSTAGE  // timing ablation only (WRONG RESULTS): stage the first chunk of the first window
+                if (s0 > 0 || u0 > uptr[b]) li = -1;
+#endif
+                for (int j = tid; li >= 0 && j < sn; j += 2 * kNT) {
                     const int f0 = s0 + j, f1 = f0 + kNT;
                     const bool two = j + kNT < sn;
                     while (Uoff[li + 1] <= f0) ++li;
