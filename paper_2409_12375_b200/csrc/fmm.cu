@@ -108,26 +108,26 @@ __device__ __forceinline__ int degree_of(int i)
 }
 
 // ------------------------------------------------------------------ M2L on tcgen05
-// Tensor-core M2L (V list), 3xTF32 on tcgen05.mma kind::tf32.  Pairs (target t,
-// source s) sharing one offset o are cut into tiles of <= 21 pairs; a tile is one
-// 128 x 128 x 128 product
+// Tensor-core M2L (V list) on tcgen05.mma: 3xFP16 (kind::f16, the default for the M2L) or 3xTF32
+// (kind::tf32: the M2M / L2L passes, and the M2L with XRL_M2L_TF32=1).  Pairs (target t, source s) sharing one
+// offset o are cut into tiles of <= 21 pairs; a tile is one 128 x 128 x 128 product
 //     D[(p, r)][i] = sum_k A[(p, r)][k] B[i][k],   A = mu_s(p)[r][k], B = T_o[i][k]
-// with row (p, r) = 6 p + r (126 rows used), i.e. the 6 RHS of 21 source
-// multipoles against one operator.  Roles (384 threads, warp-specialised):
-//   warps 0-3 (loaders, thread = TMEM lane (p, r)): LDG the FP32 multipole row
-//     (r-major image, 512 B), split it into TF32 hi/lo and tcgen05.st them into
-//     TMEM (A_hi, A_lo), one K-half (64 columns) at a time, one tile ahead;
-//   warp 8 (MMA issuer, one thread): per K-half 3 x 8 MMAs (A_lo B_hi, A_hi B_lo,
-//     A_hi B_hi, M128 N128 K8) into one of two TMEM accumulators; the operator
-//     hi/lo (128 KB, canonical K-major layout) stays in shared memory for a block
-//     of tiles with the same offset (cp.async.bulk);
-//   warps 4-7 (drain, thread = TMEM lane): tcgen05.ld the 121 coefficients of
-//     row (p, r) into a shared-memory stage and reduce it into ell[t(p)][r][0..123]
-//     (r-major) with one TMA bulk reduction (cp.reduce.async.bulk .add.f32) per row;
-//   warps 9-11 (fused P2P): P2P target-leaf tasks from the counter shared with k_p2p.
+// with row (p, r) = 6 p + r (126 rows used), i.e. the 6 RHS of 21 source multipoles against one operator.
+// Roles (warp-specialised, one persistent CTA per SM):
+//   warps 0-7 (loaders, kTcLdW; two per TMEM lane quarter, one per K-half; thread = TMEM lane (p, r)): LDG
+//     the FP32 multipole row (r-major image, 512 B), split it into hi/lo parts (FP16 on power-of-2 scaled
+//     values, or TF32) and tcgen05.st them into TMEM (A_hi, A_lo), one tile of prefetch lead;
+//   warps 8-11 (drain, thread = TMEM lane): tcgen05.ld the 121 coefficients of row (p, r) into a
+//     shared-memory stage and reduce it into ell[t(p)][r][0..123] (r-major) with one TMA bulk reduction
+//     (cp.reduce.async.bulk .add.f32) per row;
+//   warp kTcMmaW (MMA issuer, one elected thread): per K-half 3 MMAs per K-step (A_lo B_hi, A_hi B_lo, A_hi
+//     B_hi; f16: 4 K16 steps, tf32: 8 K8 steps) into one of two TMEM accumulators; the operator hi/lo
+//     (canonical K-major layout) stays in shared memory for a block of tiles with the same offset
+//     (cp.async.bulk);
+//   warps after it (kTcFuseW, fused P2P): P2P target-leaf tasks from the counter shared with k_p2p.
 // mbarriers: a_full/a_free per K-half (A), d_full/d_free per accumulator, op_full.
-// One persistent CTA per SM; blocks (runs of tiles with one (chunk, offset))
-// dealt round-robin, so all CTAs work inside one L2-resident target chunk.
+// Blocks (runs of tiles with one (chunk, offset)) are dealt to the CTAs by the LPT schedule of tree.cu, so all
+// CTAs work inside one L2-resident target chunk.
 constexpr int kTcPairs = 21;                        // pairs per tile (126 of 128 TMEM lanes)
 #ifndef XRL_FUSE_WARPS
 #define XRL_FUSE_WARPS 3

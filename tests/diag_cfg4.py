@@ -1,4 +1,5 @@
-"""Component-wise accuracy diagnosis on config 4 sampled rows."""
+"""Component-wise accuracy diagnosis on config 4 sampled rows (test infrastructure: GPU path vs the oracle).
+    python tests/diag_cfg4.py [cfg] [leaf]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

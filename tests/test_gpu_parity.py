@@ -338,10 +338,11 @@ def test_hybrid_mesh_errors():
     assert all(np.array_equal(u, v) for u, v in zip(a, b))
 
 
-@pytest.mark.parametrize("npanel", [1, 2, 5])
+@pytest.mark.parametrize("npanel", [1, 2, 5, 7, 11])
 def test_degenerate_tiny_meshes(npanel):
-    """Degenerate sizes: 1, 2 and 5 panels (a single leaf, no far field, the self term alone for N = 1);
-    also leaf_max = 1 (every panel its own leaf, the deepest tree) on 5 panels."""
+    """Degenerate sizes: 1, 2, 5, 7 and 11 panels (a single leaf, no far field, the self term alone for
+    N = 1; the near SpMV's last row group of 4 rows partial); also leaf_max = 1 (every panel its own leaf,
+    the deepest tree).  The near-only product is checked against the oracle's CSR as well."""
     rng = np.random.default_rng(npanel)
     V = rng.normal(size=(3 * npanel, 3)) * 1e-4
     T = np.arange(3 * npanel, dtype=np.int32).reshape(-1, 3)
@@ -352,6 +353,12 @@ def test_degenerate_tiny_meshes(npanel):
         err = oracle.rel_l2(run_mvm(tree, near, x), oracle_rows(m, x))
         print("tiny", npanel, leaf, err)
         assert err < 1e-6
+        optr, ocol, oval, oinv_r = oracle.near_rows(oracle.Geometry(m.verts, m.tris))
+        rows = np.repeat(np.arange(m.n), np.diff(optr))
+        yref = np.zeros((3, m.n), dtype=np.complex128)
+        for v in range(3):
+            np.add.at(yref[v], rows, (oval - oinv_r) * x[v, ocol].astype(np.complex128))
+        assert oracle.rel_l2(run_mvm(tree, near, x, flags=1), yref) <= TOL_NEAR
 
 
 def test_host_batch_pipelined_equals_single_calls(bar_setup):

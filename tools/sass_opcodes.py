@@ -25,7 +25,10 @@ for line in sass.splitlines():
     m = re.search(r"Function : (\S+)", line)
     if m:
         name = m.group(1)
-        cur = next((k for k in KERNELS if re.search(r"\d" + k + r"E", name) or name.endswith(k)), None)
+        cur = next((k for k in KERNELS if re.search(r"\d" + k + r"[EI]", name) or name.endswith(k)), None)
+        t = re.search(r"\d" + cur + r"IL([ib])(\d+)E", name) if cur else None
+        if t:  # template instance: k<1>, k<true>, ...
+            cur += "<%s>" % ({"0": "false", "1": "true"}[t.group(2)] if t.group(1) == "b" else t.group(2))
         counts = collections.Counter() if cur else None
         if cur:
             out["kernels"].setdefault(cur, {"mangled": name, "total": 0, "ops": {}})
