@@ -134,8 +134,41 @@ constexpr int kTcPairs = 21;                        // pairs per tile (126 of 12
 #endif
 constexpr int kTcLdW = 8;                           // loader warps (two per TMEM lane quarter, one per K-half)
 constexpr int kTcMmaW = kTcLdW + 4;                 // the MMA warp (after 4 drain warps)
-constexpr int kTcFuseW = XRL_FUSE_WARPS;            // fused-P2P warps
-constexpr int kTcThreads = 32 * (kTcMmaW + 1 + kTcFuseW);
+constexpr int kTcFuseW = XRL_FUSE_WARPS;            // fused-P2P warps (group 1, beside the MMA warp)
+// A second fused-P2P group of 4 warps (one warpgroup after the MMA warp's) runs in the 3xFP16 M2L, staging in the
+// half of the operator buffer the FP16 operator leaves free.  Registers are moved to the P2P warpgroups with
+// setmaxnreg: loaders kTcRegLd, drain kTcRegDr, MMA + P2P warpgroups kTcRegP2P (launched at 96 per thread).
+#ifndef XRL_FUSE2_WARPS
+#define XRL_FUSE2_WARPS 4
+#endif
+constexpr int kTcFuse2W = XRL_FUSE2_WARPS;
+static_assert(kTcFuse2W == 0 || (kTcFuse2W == 4 && kTcMmaW % 4 == 0 && kTcFuseW == 3), "warpgroup-aligned roles");
+#ifndef XRL_TC_REGS_LD
+#define XRL_TC_REGS_LD 104
+#endif
+#ifndef XRL_TC_REGS_DR
+#define XRL_TC_REGS_DR 48
+#endif
+#ifndef XRL_TC_REGS_WG4
+#define XRL_TC_REGS_WG4 112
+#endif
+#ifndef XRL_TC_REGS_WG3
+#define XRL_TC_REGS_WG3 112
+#endif
+constexpr int kTcDrCols = XRL_FUSE2_WARPS ? 16 : 32;  // drain: accumulator columns per tcgen05.ld
+constexpr int kTcRegLd = XRL_TC_REGS_LD, kTcRegDr = XRL_TC_REGS_DR, kTcRegP2P = XRL_TC_REGS_WG3,
+              kTcRegP2P2 = XRL_TC_REGS_WG4;
+constexpr int kTcThreads = 32 * (kTcMmaW + 1 + kTcFuseW + kTcFuse2W);
+constexpr int kTcRegLaunch = 96;  // per-thread registers at launch (__maxnreg__) when kTcFuse2W > 0
+// this warpgroup's register count: setmaxnreg.inc above the launch count, .dec below it
+template <int kRegs>
+__device__ __forceinline__ void set_max_regs()
+{
+    if constexpr (kRegs > kTcRegLaunch) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+    else if constexpr (kRegs < kTcRegLaunch) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+static_assert(kTcFuse2W == 0 || 32 * (8 * kTcRegLd + 4 * kTcRegDr + 4 * kTcRegP2P + 4 * kTcRegP2P2) <= kTcRegLaunch * kTcThreads,
+              "setmaxnreg budget: the CTA's registers at launch (96 per thread)");
 constexpr int kTcOpBytes = 128 * 128 * 4;           // one operator part (hi or lo): 64 KB
 constexpr int kTcStageLd = 132;                     // drain stage row stride (floats; conflict-free STS.128)
 constexpr int kTcSmem = 2 * kTcOpBytes + 128 * kTcStageLd * 4 + 1024 + 512 * 12 * 4;  // operator hi + lo, drain stage (+ align), fused-P2P staging
@@ -229,6 +262,7 @@ struct P2PTasks {
 };
 constexpr int kFuseChunk = 512;                          // sources staged per chunk by the fused P2P warps
 constexpr int kFuseSmem = kFuseChunk * 12 * 4;           // their staging / reduction buffer (bytes)
+constexpr int kFuse2Chunk = 1024;                        // the second group: 48 KB in the free operator half
 
 // This CTA's tile sequence: blocks blockIdx.x, blockIdx.x + gridDim.x, ...; all tiles of each block.  In a
 // multi-level launch (lvr != nullptr) `lev` is the level of the current block: level v owns the block rows
@@ -300,7 +334,12 @@ __device__ __forceinline__ int mu_scale_exp(const unsigned* mumax)
 // 2^e, e = 14 - exponent of the largest |mu| of the MVM (*mumax, k_mu_max), every operator times 2^opexp (host,
 // largest |T| in [2^14, 2^15)); the drain multiplies by 2^-(e + opexp).  Used for the M2L.
 template <bool kH>
-__global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict__ blocks, int nblocks,
+#if XRL_FUSE2_WARPS
+#define XRL_TC_REGS __maxnreg__(96)  /* kTcRegLaunch */
+#else
+#define XRL_TC_REGS __launch_bounds__(kTcThreads, 1)
+#endif
+__global__ void XRL_TC_REGS k_m2l_tc(const int4* __restrict__ blocks, int nblocks,
                                                           const int4* __restrict__ tiles,
                                                           const int32_t* __restrict__ tgt,
                                                           const int32_t* __restrict__ srcb,
@@ -318,8 +357,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
     float* p2p_sm = stage + 128 * kTcStageLd;                          // fused P2P staging (kFuseSmem)
     __shared__ uint64_t a_full[2], a_free[2], d_full[2], d_free[2], op_full;
     __shared__ uint32_t tbase;
-    __shared__ int m2l_live, p2p_task;
-    __shared__ P2PWin p2p_win;
+    __shared__ int m2l_live, p2p_task, p2p_task2;
+    __shared__ P2PWin p2p_win, p2p_win2;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) m2l_live = kTcMmaW + 1;  // warps of the translation roles still running
     if (tid == 0) {
@@ -336,24 +375,111 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
     __syncthreads();
     tc::fence_after();
     const uint32_t tm = tbase;
-
-    if (warp > kTcMmaW) {
-        // ---------------- fused P2P: three warps take target-leaf tasks from the shared counter while the
-        // translation roles run (the M2L is bound by L2 traffic and leaves the FP32 pipes idle)
-        if (p2p.tasks) {
-            const int tp = tid - 32 * (kTcMmaW + 1);
-            for (;;) {
-                if (tp == 0) p2p_task = *(volatile int*)&m2l_live > 0 ? atomicAdd(p2p.counter, 1) : INT_MAX;
-                asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcFuseW) : "memory");
-                const int task = p2p_task;
-                if (task >= p2p.ntasks) break;
-                const int4 tk = p2p.tasks[task];
-                p2p_leaf<32 * kTcFuseW, kFuseChunk, 1>(tk.x, tk.y, tk.y + tk.z, tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
-                                            p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, 0, p2p.n,
-                                            p2p.p0, p2p.y);
+    // roles by warpgroup (setmaxnreg is warpgroup-wide: each role branch starts with its own, so ptxas
+    // allocates the branch within it): 0-7 loaders, 8-11 drain, 12 MMA, 13-15 fused P2P 1, 16-19 fused P2P 2
+    if (warp >= kTcMmaW + 1 + kTcFuseW) {
+        if (kTcFuse2W > 0) set_max_regs<kTcRegP2P2>();
+        {
+            // ---------------- fused P2P, second group (3xFP16 M2L only): staging in the free operator half
+            if (kH && p2p.tasks) {
+                const int tp = tid - 32 * (kTcMmaW + 1 + kTcFuseW);
+                float* sm2 = reinterpret_cast<float*>(opsm + 2 * kOpPart);
+                for (;;) {
+                    if (tp == 0) p2p_task2 = *(volatile int*)&m2l_live > 0 ? atomicAdd(p2p.counter, 1) : INT_MAX;
+                    asm volatile("bar.sync 3, %0;" ::"n"(32 * kTcFuse2W) : "memory");
+                    const int task = p2p_task2;
+                    if (task >= p2p.ntasks) break;
+                    const int4 tk = p2p.tasks[task];
+                    p2p_leaf<32 * kTcFuse2W, kFuse2Chunk, 3>(tk.x, tk.y, tk.y + tk.z, tp, sm2, p2p_win2, p2p.level, p2p.ix,
+                                                             p2p.iy, p2p.iz, p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc,
+                                                             p2p.xq, p2p.invW, 0, p2p.n, p2p.p0, p2p.y);
+                }
+            }
+        }
+    } else if (warp >= kTcMmaW) {
+        if (kTcFuse2W > 0) set_max_regs<kTcRegP2P>();
+        if (warp > kTcMmaW) {
+            // ---------------- fused P2P: three warps take target-leaf tasks from the shared counter while the
+            // translation roles run (the M2L is bound by L2 traffic and leaves the FP32 pipes idle)
+            if (p2p.tasks) {
+                const int tp = tid - 32 * (kTcMmaW + 1);
+                for (;;) {
+                    if (tp == 0) p2p_task = *(volatile int*)&m2l_live > 0 ? atomicAdd(p2p.counter, 1) : INT_MAX;
+                    asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcFuseW) : "memory");
+                    const int task = p2p_task;
+                    if (task >= p2p.ntasks) break;
+                    const int4 tk = p2p.tasks[task];
+                    p2p_leaf<32 * kTcFuseW, kFuseChunk, 1>(tk.x, tk.y, tk.y + tk.z, tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
+                                                p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, 0, p2p.n,
+                                                p2p.p0, p2p.y);
+                }
+            }
+        } else {
+            // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform control
+            // (block descriptors through shared memory, barrier waits voted with __all_sync) so the
+            // descriptors stay in uniform registers and lane 0 issues back-to-back UTCHMMAs
+            // (uniform bases recomputed here so they live in uniform registers)
+            const uint32_t tmu = tbase;
+            const uint32_t oph = (tc::smem_u32(tsm_raw) + 1023u) & ~1023u, opl = oph + kOpPart;
+            const uint32_t idesc = kH ? tc::idesc_f16(128, 128) : tc::idesc_tf32(128, 128);
+            int j = 0, nb = 0;
+            for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x, ++nb) {
+                int4 bk = __ldg(blocks + bi);
+                bk.y = __shfl_sync(0xffffffffu, bk.y, 0);  // warp-uniform (keeps the MMA operands in uniform registers)
+                bk.z = __shfl_sync(0xffffffffu, bk.z, 0);
+                if (bk.y <= 0) { --nb; continue; }  // padding block of the balanced order: no operator load
+                if (j > 0) {  // every MMA reading the previous operator must be complete
+                    mbar_wait_warp(&d_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                    tc::fence_after();
+                }
+                if (lane == 0) {
+                    mbar_expect_tx(&op_full, 2 * kOpPart);
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(opimg) + (size_t)bk.z * 2 * kOpPart;
+                    for (uint32_t c = 0; c < 2 * kOpPart / 32768; ++c)
+                        bulk_g2s(opsm + c * 32768, src + c * 32768, 32768, &op_full);
+                }
+                mbar_wait_warp(&op_full, nb & 1);
+                for (int ti = 0; ti < bk.y; ++ti, ++j) {
+                    const int d = j & 1;
+                    mbar_wait_warp(&d_free[d], ((j >> 1) & 1) ^ 1);
+                    tc::fence_after();
+                    const uint32_t dst = tmu + kTcColD + 128 * d;
+    #pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        mbar_wait_warp(&a_full[h], j & 1);
+                        tc::fence_after();
+                        if (kH && tc::elect_one()) {
+    #pragma unroll
+                            for (int s = 4 * h; s < 4 * h + 4; ++s) {
+                                // B element (i, k) at half ((i/8)*16 + k/8)*64 + (i%8)*8 + k%8: LBO 128, SBO 2048 bytes
+                                const uint64_t bh = tc::smem_desc(oph + 256 * s, 128, 2048);
+                                const uint64_t bl = tc::smem_desc(opl + 256 * s, 128, 2048);
+                                tc::mma_f16_ts(dst, tmu + kColAl + 8 * s, bh, idesc, s > 0);
+                                tc::mma_f16_ts(dst, tmu + kTcColAh + 8 * s, bl, idesc, 1);
+                                tc::mma_f16_ts(dst, tmu + kTcColAh + 8 * s, bh, idesc, 1);
+                            }
+                            tc::commit(&a_free[h]);
+                            if (h == 1) tc::commit(&d_full[d]);
+                        } else if (!kH && tc::elect_one()) {
+    #pragma unroll
+                            for (int s = 8 * h; s < 8 * h + 8; ++s) {
+                                // B (operator) element (i, k) at ((i/8)*32 + k/4)*128 + (i%8)*16 + (k%4)*4: LBO 128, SBO 4096
+                                const uint64_t bh = tc::smem_desc(oph + 256 * s, 128, 4096);
+                                const uint64_t bl = tc::smem_desc(opl + 256 * s, 128, 4096);
+                                tc::mma_tf32_ts(dst, tmu + kTcColAl + 8 * s, bh, idesc, s > 0);
+                                tc::mma_tf32_ts(dst, tmu + kTcColAh + 8 * s, bl, idesc, 1);
+                                tc::mma_tf32_ts(dst, tmu + kTcColAh + 8 * s, bh, idesc, 1);
+                            }
+                            tc::commit(&a_free[h]);
+                            if (h == 1) tc::commit(&d_full[d]);
+                        }
+                        __syncwarp();
+                    }
+                }
             }
         }
     } else if (warp < kTcLdW) {
+        if (kTcFuse2W > 0) set_max_regs<kTcRegLd>();
         // ---------------- loaders: thread = TMEM lane L = (p, r); warps w and w + 4 share lane quarter w % 4,
         // warps 0-3 convert K-half 0 of their rows and warps 4-7 K-half 1.  Each thread's half row (64 floats,
         // 8 x 256-bit loads: whole 32-byte sectors) of the next tile is loaded right after the current one is
@@ -433,7 +559,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             }
             s0 = s1;
         }
-    } else if (warp < kTcMmaW) {
+    } else {
+        if (kTcFuse2W > 0) set_max_regs<kTcRegDr>();
         // ---------------- drain: thread = TMEM lane L = (p, r) reads its accumulator row into a
         // shared-memory stage; then each thread reduces its whole row into ell with one TMA bulk
         // reduction (asynchronous: frees the drain warps; tools/ubench_red.cu measured the variants)
@@ -475,20 +602,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
             float* srow = stage + L * kTcStageLd;
             bulk_wait_read0();  // this thread's previous bulk reduction has finished reading its stage row
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float v[32];
+            for (int c = 0; c < 128 / kTcDrCols; ++c) {  // kTcDrCols columns per tcgen05.ld (registers: see kTcRegDr)
+                float v[kTcDrCols];
                 if (dbg & 4) {
-                    for (int q = 0; q < 32; ++q) v[q] = 0.f;
+                    for (int q = 0; q < kTcDrCols; ++q) v[q] = 0.f;
                 } else {
-                    tc::tmem_ld32(ta + 32 * c, v);
+                    if (kTcDrCols == 32) tc::tmem_ld32(ta + kTcDrCols * c, v);
+                    else tc::tmem_ld16(ta + kTcDrCols * c, v);
                     if (kH) {
 #pragma unroll
-                        for (int q = 0; q < 32; ++q) v[q] *= unscale;
+                        for (int q = 0; q < kTcDrCols; ++q) v[q] *= unscale;
                     }
                 }
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<float4*>(srow + 32 * c + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                for (int q = 0; q < kTcDrCols / 4; ++q)
+                    *reinterpret_cast<float4*>(srow + kTcDrCols * c + 4 * q) =
+                        make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             }
             tc::fence_before();
             __syncwarp();
@@ -506,69 +635,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_m2l_tc(const int4* __restrict
         }
         if (lvr) signal_upto(nlv);
         bulk_wait0();
-    } else {
-        // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform control
-        // (block descriptors through shared memory, barrier waits voted with __all_sync) so the
-        // descriptors stay in uniform registers and lane 0 issues back-to-back UTCHMMAs
-        // (uniform bases recomputed here so they live in uniform registers)
-        const uint32_t tmu = tbase;
-        const uint32_t oph = (tc::smem_u32(tsm_raw) + 1023u) & ~1023u, opl = oph + kOpPart;
-        const uint32_t idesc = kH ? tc::idesc_f16(128, 128) : tc::idesc_tf32(128, 128);
-        int j = 0, nb = 0;
-        for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x, ++nb) {
-            int4 bk = __ldg(blocks + bi);
-            bk.y = __shfl_sync(0xffffffffu, bk.y, 0);  // warp-uniform (keeps the MMA operands in uniform registers)
-            bk.z = __shfl_sync(0xffffffffu, bk.z, 0);
-            if (bk.y <= 0) { --nb; continue; }  // padding block of the balanced order: no operator load
-            if (j > 0) {  // every MMA reading the previous operator must be complete
-                mbar_wait_warp(&d_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
-                tc::fence_after();
-            }
-            if (lane == 0) {
-                mbar_expect_tx(&op_full, 2 * kOpPart);
-                const uint8_t* src = reinterpret_cast<const uint8_t*>(opimg) + (size_t)bk.z * 2 * kOpPart;
-                for (uint32_t c = 0; c < 2 * kOpPart / 32768; ++c)
-                    bulk_g2s(opsm + c * 32768, src + c * 32768, 32768, &op_full);
-            }
-            mbar_wait_warp(&op_full, nb & 1);
-            for (int ti = 0; ti < bk.y; ++ti, ++j) {
-                const int d = j & 1;
-                mbar_wait_warp(&d_free[d], ((j >> 1) & 1) ^ 1);
-                tc::fence_after();
-                const uint32_t dst = tmu + kTcColD + 128 * d;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    mbar_wait_warp(&a_full[h], j & 1);
-                    tc::fence_after();
-                    if (kH && tc::elect_one()) {
-#pragma unroll
-                        for (int s = 4 * h; s < 4 * h + 4; ++s) {
-                            // B element (i, k) at half ((i/8)*16 + k/8)*64 + (i%8)*8 + k%8: LBO 128, SBO 2048 bytes
-                            const uint64_t bh = tc::smem_desc(oph + 256 * s, 128, 2048);
-                            const uint64_t bl = tc::smem_desc(opl + 256 * s, 128, 2048);
-                            tc::mma_f16_ts(dst, tmu + kColAl + 8 * s, bh, idesc, s > 0);
-                            tc::mma_f16_ts(dst, tmu + kTcColAh + 8 * s, bl, idesc, 1);
-                            tc::mma_f16_ts(dst, tmu + kTcColAh + 8 * s, bh, idesc, 1);
-                        }
-                        tc::commit(&a_free[h]);
-                        if (h == 1) tc::commit(&d_full[d]);
-                    } else if (!kH && tc::elect_one()) {
-#pragma unroll
-                        for (int s = 8 * h; s < 8 * h + 8; ++s) {
-                            // B (operator) element (i, k) at ((i/8)*32 + k/4)*128 + (i%8)*16 + (k%4)*4: LBO 128, SBO 4096
-                            const uint64_t bh = tc::smem_desc(oph + 256 * s, 128, 4096);
-                            const uint64_t bl = tc::smem_desc(opl + 256 * s, 128, 4096);
-                            tc::mma_tf32_ts(dst, tmu + kTcColAl + 8 * s, bh, idesc, s > 0);
-                            tc::mma_tf32_ts(dst, tmu + kTcColAh + 8 * s, bl, idesc, 1);
-                            tc::mma_tf32_ts(dst, tmu + kTcColAh + 8 * s, bh, idesc, 1);
-                        }
-                        tc::commit(&a_free[h]);
-                        if (h == 1) tc::commit(&d_full[d]);
-                    }
-                    __syncwarp();
-                }
-            }
-        }
     }
     if (warp <= kTcMmaW && lane == 0) atomicSub(&m2l_live, 1);
     tc::fence_before();
