@@ -129,6 +129,7 @@ xrl_status xrl_ctx_create(int device, void* cuda_stream, int rank, int world, co
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_m2l, cudaEventDisableTiming));
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_p2p, cudaEventDisableTiming));
+        XRL_CUDA(cudaEventCreateWithFlags(&c->ev_near, cudaEventDisableTiming));
         if (const char* e = getenv("XRL_FUSE"); e && e[0] == '0') c->fuse_p2p = false;
         if (const char* e = getenv("XRL_M2L_TF32"); e && e[0] == '1') c->m2l_h16 = false;
         XRL_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -185,6 +186,7 @@ void xrl::ctx_release(xrl_ctx ctx)
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_m2l) cudaEventDestroy(ctx->ev_m2l);
     if (ctx->ev_p2p) cudaEventDestroy(ctx->ev_p2p);
+    if (ctx->ev_near) cudaEventDestroy(ctx->ev_near);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->comm) { cudaStreamSynchronize(ctx->comm); cudaStreamDestroy(ctx->comm); }
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);

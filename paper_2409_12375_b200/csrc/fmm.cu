@@ -17,8 +17,7 @@
 //   k_m2l_tc     V-list translations on tcgen05 (3xTF32, warp-specialised)
 //   k_p2l        X-list particle -> local
 //   (L2L)        parent -> child per level on k_m2l_tc
-//   k_ell_kmajor leaves' ell[r][k] -> ellk[k][8]
-//   k_l2p        per target panel: L2P
+//   k_l2p_leaf   per owned leaf: ell to shared memory, L2P of its panels
 //   k_m2p        W-list M2P (leaves with a W list), completes y
 #include <cuda_fp16.h>
 
@@ -57,46 +56,92 @@ __global__ void k_pack(int64_t n, const float2* __restrict__ x, float* __restric
 }
 
 // ------------------------------------------------------------------ P2M
-constexpr int kChunk = 128;  // panels per P2M pass (one per thread)
-constexpr int kP2MSmem = kChunk * (kNC + 6) * 4;
+// One CTA (128 threads) per owned leaf, panels in chunks of 128: (1) thread t evaluates the 121 regular solid
+// harmonics of panel t of the chunk into H^T[k][t] (row stride 132: the float4 reads below are conflict-free)
+// and stages its 6 charges; (2) mu[k][r] += sum_p H^T[k][p] q[p][r] as a register-blocked product: thread
+// (lane l, warp g) owns coefficients k = l, l + 32, l + 64, l + 96 and the panels p = 32 g .. 32 g + 31, four
+// at a time (one float4 of H^T per coefficient, the 4 panels' charges broadcast: 96 FMAs per 12 shared loads);
+// (3) the 4 warps' partial sums are added through shared memory.
+constexpr int kChunk = 128;       // panels per P2M pass (one per thread)
+constexpr int kP2MLd = 132;       // H^T row stride (floats): 132 = 4 mod 32
+constexpr int kP2MSmem = (kNC * kP2MLd + kChunk * 8) * 4;
 
 __global__ void __launch_bounds__(128) k_p2m(const int32_t* __restrict__ leaves, const int32_t* __restrict__ pb,
                                              const int32_t* __restrict__ pe, const int32_t* __restrict__ level,
                                              const float4* __restrict__ loc, const float* __restrict__ xq,
                                              float* __restrict__ mu)
 {
+    static_assert(4 * 32 >= kNC && kNC * kP2MLd >= 4 * 128 * 6, "P2M shape");
     extern __shared__ __align__(16) float p2m_sm[];
-    float(*H)[kNC] = reinterpret_cast<float(*)[kNC]>(p2m_sm);          // [kChunk][121]
-    float(*Q)[6] = reinterpret_cast<float(*)[6]>(p2m_sm + kChunk * kNC);  // [kChunk][6]
+    float* HT = p2m_sm;                                                 // [kNC][kP2MLd]
+    float(*Q)[8] = reinterpret_cast<float(*)[8]>(p2m_sm + kNC * kP2MLd);  // [kChunk][8]
     const int b = leaves[blockIdx.x];
     const int s = pb[b], e = pe[b];
     const float inv_s = ldexpf(1.f, level[b]);
-    float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // thread k < 121: mu[k][0..5]
-    const int k = threadIdx.x;
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    float acc[4][6];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int r = 0; r < 6; ++r) acc[i][r] = 0.f;
     for (int c0 = s; c0 < e; c0 += kChunk) {
         const int cn = min(kChunk, e - c0);
-        if (threadIdx.x < cn) {
-            const int i = c0 + threadIdx.x;
-            float4 p = loc[i];
-            float* hrow = H[threadIdx.x];
-            regular_harmonics_visit<kP>(p.x * inv_s, p.y * inv_s, p.z * inv_s, c_tab,
-                                        [&](int kk, float v) { hrow[kk] = v; });
+        {
+            const int t = threadIdx.x;
+            if (t < cn) {
+                const int i = c0 + t;
+                const float4 p = loc[i];
+                regular_harmonics_visit<kP>(p.x * inv_s, p.y * inv_s, p.z * inv_s, c_tab,
+                                            [&](int kk, float v) { HT[kk * kP2MLd + t] = v; });
+                const float4 q0 = *reinterpret_cast<const float4*>(xq + 8 * (int64_t)i);
+                const float2 q1 = *reinterpret_cast<const float2*>(xq + 8 * (int64_t)i + 4);
+                *reinterpret_cast<float4*>(Q[t]) = q0;
+                *reinterpret_cast<float4*>(Q[t] + 4) = make_float4(q1.x, q1.y, 0.f, 0.f);
+            } else {  // padding panels: zero charge (their harmonics column is never read with weight != 0)
 #pragma unroll
-            for (int r = 0; r < 6; ++r) Q[threadIdx.x][r] = xq[8 * (int64_t)i + r];
+                for (int kk = 0; kk < kNC; ++kk) HT[kk * kP2MLd + t] = 0.f;
+                *reinterpret_cast<float4*>(Q[t]) = make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(Q[t] + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
         __syncthreads();
-        if (k < kNC) {
-            for (int p = 0; p < cn; ++p) {
-                const float hv = H[p][k];
+        const int p_end = min(32 * g + 32, cn);
+        for (int p = 32 * g; p < p_end; p += 4) {
+            float4 h[4];
 #pragma unroll
-                for (int r = 0; r < 6; ++r) acc[r] = fmaf(hv, Q[p][r], acc[r]);
+            for (int i = 0; i < 4; ++i) {
+                const int k = lane + 32 * i;
+                h[i] = k < kNC ? *reinterpret_cast<const float4*>(HT + k * kP2MLd + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float4 qa = *reinterpret_cast<const float4*>(Q[p + u]);
+                const float2 qb = *reinterpret_cast<const float2*>(Q[p + u] + 4);
+                const float q[6] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float hv = u == 0 ? h[i].x : (u == 1 ? h[i].y : (u == 2 ? h[i].z : h[i].w));
+#pragma unroll
+                    for (int r = 0; r < 6; ++r) acc[i][r] = fmaf(hv, q[r], acc[i][r]);
+                }
             }
         }
         __syncthreads();
     }
-    float* out = mu + (size_t)b * kMuStride;  // mu[r][k], k >= 121 zero
+    // partial sums of the 4 warps -> mu[r][k] (k >= 121 zero); HT is free now
+    float* red = p2m_sm;  // [4 warps][6][128]
 #pragma unroll
-    for (int r = 0; r < 6; ++r) out[r * 128 + k] = k < kNC ? acc[r] : 0.f;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int r = 0; r < 6; ++r) red[(g * 6 + r) * 128 + lane + 32 * i] = acc[i][r];
+    __syncthreads();
+    float* out = mu + (size_t)b * kMuStride;
+    for (int j = threadIdx.x; j < 6 * 128; j += blockDim.x) {
+        const int r = j >> 7, k = j & 127;
+        const float v = red[(0 * 6 + r) * 128 + k] + red[(1 * 6 + r) * 128 + k] + red[(2 * 6 + r) * 128 + k] +
+                        red[(3 * 6 + r) * 128 + k];
+        out[r * 128 + k] = k < kNC ? v : 0.f;
+    }
 }
 
 // degree n of real coefficient index i = n*n + j
@@ -259,6 +304,7 @@ struct P2PTasks {
     float invW;
     int64_t n, p0;
     float2* y;
+    int accumulate;  // 1: y already holds the near part (near-first side stream), the P2P adds to it
 };
 constexpr int kFuseChunk = 512;                          // sources staged per chunk by the fused P2P warps
 constexpr int kFuseSmem = kFuseChunk * 12 * 4;           // their staging / reduction buffer (bytes)
@@ -392,7 +438,7 @@ __global__ void XRL_TC_REGS k_m2l_tc(const int4* __restrict__ blocks, int nblock
                     const int4 tk = p2p.tasks[task];
                     p2p_leaf<32 * kTcFuse2W, kFuse2Chunk, 3>(tk.x, tk.y, tk.y + tk.z, tp, sm2, p2p_win2, p2p.level, p2p.ix,
                                                              p2p.iy, p2p.iz, p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc,
-                                                             p2p.xq, p2p.invW, 0, p2p.n, p2p.p0, p2p.y);
+                                                             p2p.xq, p2p.invW, p2p.accumulate, p2p.n, p2p.p0, p2p.y);
                 }
             }
         }
@@ -410,7 +456,7 @@ __global__ void XRL_TC_REGS k_m2l_tc(const int4* __restrict__ blocks, int nblock
                     if (task >= p2p.ntasks) break;
                     const int4 tk = p2p.tasks[task];
                     p2p_leaf<32 * kTcFuseW, kFuseChunk, 1>(tk.x, tk.y, tk.y + tk.z, tp, p2p_sm, p2p_win, p2p.level, p2p.ix, p2p.iy, p2p.iz,
-                                                p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, 0, p2p.n,
+                                                p2p.pb, p2p.pe, p2p.uptr, p2p.usrc, p2p.loc, p2p.xq, p2p.invW, p2p.accumulate, p2p.n,
                                                 p2p.p0, p2p.y);
                 }
             }
@@ -1481,47 +1527,45 @@ __global__ void __launch_bounds__(128) k_p2p12(
                invW, 0, n, p0, y, y2);
 }
 
-// ell[r][k] (r-major, M2L/L2L layout) -> ellk[k][8] (k-major, 6 RHS + 2 pad) for the leaves: the L2P
-// then reads one 32-byte record per coefficient instead of 6 scalars.
-__global__ void k_ell_kmajor(const int32_t* __restrict__ leaves, const float* __restrict__ ell, float* __restrict__ ellk)
+// ------------------------------------------------------------------ L2P (+ M2P below)
+// L2P per owned leaf (one CTA of 128 threads): the leaf's local expansion ell[r][k] (r-major) is transposed
+// into shared memory as [k][8] once, then each thread evaluates panels pb + tid, pb + tid + 128, ... with
+// broadcast shared-memory reads per coefficient (the panel-per-thread k_l2p re-read the k-major copy through
+// L1 and was latency-bound on it: 45 % L1 hits, 0.23 ms on config 4).
+__global__ void __launch_bounds__(128) k_l2p_leaf(const int32_t* __restrict__ leaves,
+                                                  const int32_t* __restrict__ pb, const int32_t* __restrict__ pe,
+                                                  const int32_t* __restrict__ level, const float4* __restrict__ loc,
+                                                  const float* __restrict__ ell, int64_t p0, int64_t n, float invW,
+                                                  float2* __restrict__ y)
 {
+    __shared__ __align__(16) float sl[kNC * 8];
     const int b = leaves[blockIdx.x];
     const float* src = ell + (size_t)b * kEllStride;
-    float* dst = ellk + (size_t)b * kEllKStride;
     for (int j = threadIdx.x; j < kNC * 8; j += blockDim.x) {
         const int k = j >> 3, r = j & 7;
-        dst[j] = r < 6 ? src[r * 128 + k] : 0.f;
+        sl[j] = r < 6 ? src[r * 128 + k] : 0.f;
     }
-}
-
-// ------------------------------------------------------------------ L2P (+ M2P below)
-// One thread per target panel: y += (1/W) (1/s_b) sum_k ellk_b[k] Rt_k(u).
-__global__ void __launch_bounds__(128) k_l2p(int64_t n, int64_t p0, const int32_t* __restrict__ panel_leaf,
-                                             const int32_t* __restrict__ level, const float4* __restrict__ loc,
-                                             const float* __restrict__ ellk, float invW, float2* __restrict__ y)
-{
-    const int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // local index, panel p0 + li
-    if (li >= n) return;
-    const int64_t i = p0 + li;
-    const int b = panel_leaf[i];
+    __syncthreads();
     const float inv_sb = ldexpf(1.f, level[b]);
-    const float4 tp = loc[i];
-    float far[6] = {0, 0, 0, 0, 0, 0};
-    {
-        // L2P: contract the k-major local expansion ellk[k][8] (one 256-bit load per coefficient) on the fly
-        const float* L = ellk + (size_t)b * kEllKStride;
+    const float sc = inv_sb * invW;
+    for (int64_t i = pb[b] + threadIdx.x; i < pe[b]; i += blockDim.x) {
+        const float4 tp = loc[i];
+        float far[6] = {0, 0, 0, 0, 0, 0};
         regular_harmonics_visit<kP>(tp.x * inv_sb, tp.y * inv_sb, tp.z * inv_sb, c_tab, [&](int k, float v) {
-            float l[8];
-            ldg256_l1(L + 8 * k, l);
-#pragma unroll
-            for (int r = 0; r < 6; ++r) far[r] = fmaf(l[r], v, far[r]);
+            const float4 a = *reinterpret_cast<const float4*>(sl + 8 * k);
+            const float2 c = *reinterpret_cast<const float2*>(sl + 8 * k + 4);
+            far[0] = fmaf(a.x, v, far[0]);
+            far[1] = fmaf(a.y, v, far[1]);
+            far[2] = fmaf(a.z, v, far[2]);
+            far[3] = fmaf(a.w, v, far[3]);
+            far[4] = fmaf(c.x, v, far[4]);
+            far[5] = fmaf(c.y, v, far[5]);
         });
-#pragma unroll
-        for (int r = 0; r < 6; ++r) far[r] *= inv_sb;
+        const int64_t li = i - p0;
+        red_add2(y + li, far[0] * sc, far[1] * sc);
+        red_add2(y + n + li, far[2] * sc, far[3] * sc);
+        red_add2(y + 2 * n + li, far[4] * sc, far[5] * sc);
     }
-    red_add2(y + li, far[0] * invW, far[1] * invW);
-    red_add2(y + n + li, far[2] * invW, far[3] * invW);
-    red_add2(y + 2 * n + li, far[4] * invW, far[5] * invW);
 }
 
 __device__ __forceinline__ void red_add_v2(float* p, float a, float b)
@@ -1718,6 +1762,7 @@ struct Mvm {
     int sched;
     cudaStream_t st, side;
     bool do_far, do_near, chain, fuse, side_done;
+    bool near_first = false;  // side stream: near SpMV (into zeroed y) before the P2P, which then accumulates
     int64_t nl, p0;
     float invW;
     cudaEvent_t halo = nullptr;  // multi-rank, overlapped halo: the P2P / P2L wait for it
@@ -1751,6 +1796,11 @@ static Mvm mvm_make(xrl_tree t, xrl_near nr, float2* y, uint32_t flags, int sche
     M.fuse = sched != 0 && ctx->fuse_p2p && M.chain && t->n_m2l_tiles > 0 && t->n_own_leaves > 0 &&
              t->part_world <= fuse_max_world;
     M.side_done = false;
+    static const bool near_first_env = [] {  // XRL_NEAR_FIRST=1 (schedule experiment)
+        const char* e = std::getenv("XRL_NEAR_FIRST");
+        return e && e[0] == '1';
+    }();
+    M.near_first = near_first_env && sched != 0 && M.do_far && M.do_near;
     M.nl = t->p1 - t->p0;
     M.p0 = t->p0;
     M.invW = (float)(1.0 / t->W);
@@ -1833,6 +1883,12 @@ static void mvm_side(Mvm& M)
     XRL_CUDA(cudaEventRecord(ctx->ev_fork, M.st));
     XRL_CUDA(cudaStreamWaitEvent(M.side, ctx->ev_fork, 0));
     if (M.halo) XRL_CUDA(cudaStreamWaitEvent(M.side, M.halo, 0));  // the P2P reads remote charges
+    const bool nf = M.near_first && !M.xq2;
+    if (nf) {  // y = 0, y += N x, then the P2P adds its part
+        if (M.nl > 0) XRL_CUDA(cudaMemsetAsync(M.y, 0, sizeof(float2) * 3 * (size_t)M.nl, M.side));
+        launch_near(M);
+        XRL_CUDA(cudaEventRecord(ctx->ev_near, M.side));
+    }
     if (M.do_far) {
         phase_begin(ctx, PH_P2P, &ev, M.side);
         if (t->n_own_leaves > 0 && M.xq2) {
@@ -1846,14 +1902,15 @@ static void mvm_side(Mvm& M)
             k_p2p<<<t->n_p2p_tasks, 128, kP2PSmem, M.side>>>(t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p,
                                                             t->blevel.p, t->bix.p, t->biy.p, t->biz.p, t->bpb.p,
                                                             t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, M.xq,
-                                                            M.invW, 0, M.nl, M.p0, M.y);
+                                                            M.invW, nf ? 1 : 0, M.nl, M.p0, M.y);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
         phase_end(ctx, PH_P2P, ev, M.side);
     }
     XRL_CUDA(cudaEventRecord(ctx->ev_p2p, M.side));  // y holds the P2P part: the L2P may add to it
-    if (!M.fuse) launch_near(M);
+    if (nf) XRL_CUDA(cudaEventRecord(ctx->ev_join, M.side));
+    else if (!M.fuse) launch_near(M);
 }
 
 static void launch_p2l(Mvm& M, cudaStream_t st)
@@ -1950,10 +2007,12 @@ static void mvm_down(Mvm& M)
         if (t->n_m2l_tiles > 0) {
             const int grid = t->m2l_grid;  // the grid the block order was balanced for (tree.cu)
             P2PTasks tasks{};
+            if (M.fuse && M.near_first && !M.xq2)  // the fused warps add to y after the near SpMV
+                XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_near, 0));
             if (M.fuse)
                 tasks = P2PTasks{t->p2p_tasks.p, t->n_p2p_tasks, t->p2p_counter.p, t->blevel.p, t->bix.p, t->biy.p,
                                  t->biz.p, t->bpb.p, t->bpe.p, t->u_ptr.p, t->u_src.p, t->loc.p, M.xq, M.invW, M.nl,
-                                 M.p0, M.y};
+                                 M.p0, M.y, M.near_first ? 1 : 0};
             if (ctx->m2l_h16) {  // 3xFP16 (default): the multipole row exponents first
                 if (t->mu_max.n < 1) t->mu_max.alloc(1);
                 XRL_CUDA(cudaMemsetAsync(t->mu_max.p, 0, sizeof(unsigned), M.st));
@@ -1975,7 +2034,7 @@ static void mvm_down(Mvm& M)
             }
         }
         phase_end(ctx, PH_M2L, ev, M.st);
-        if (M.fuse) {
+        if (M.fuse && !(M.near_first && !M.xq2)) {
             XRL_CUDA(cudaEventRecord(ctx->ev_m2l, M.st));
             XRL_CUDA(cudaStreamWaitEvent(M.side, ctx->ev_m2l, 0));  // fused P2P tasks done
             launch_near(M);
@@ -1997,16 +2056,12 @@ static void mvm_down(Mvm& M)
     if (M.sched) XRL_CUDA(cudaStreamWaitEvent(M.st, ctx->ev_p2p, 0));
     if (M.chain && M.nl > 0) {
         phase_begin(ctx, PH_L2P, &ev, M.st);
-        if (t->ellk.n < (size_t)t->nbox * kEllKStride) t->ellk.alloc((size_t)t->nbox * kEllKStride);
         if (t->n_own_leaves > 0) {
-            k_ell_kmajor<<<t->n_own_leaves, 256, 0, M.st>>>(t->own_leaves.p, t->ell.p, t->ellk.p);
+            k_l2p_leaf<<<t->n_own_leaves, 128, 0, M.st>>>(t->own_leaves.p, t->bpb.p, t->bpe.p, t->blevel.p, t->loc.p,
+                                                        t->ell.p, M.p0, M.nl, M.invW, M.y);
             XRL_LAUNCH_CHECK();
             ctx->launches += 1;
         }
-        k_l2p<<<nblk(M.nl, 128), 128, 0, M.st>>>(M.nl, M.p0, t->panel_leaf.p, t->blevel.p, t->loc.p, t->ellk.p,
-                                                 M.invW, M.y);
-        XRL_LAUNCH_CHECK();
-        ctx->launches += 1;
         if (t->n_w_targets > 0) {
             k_m2p<<<t->n_w_targets, 128, 0, M.st>>>(t->w_targets.p, M.p0, M.nl, t->bpb.p, t->bpe.p, t->blevel.p,
                                                     t->bix.p, t->biy.p, t->biz.p, t->loc.p, t->mu.p, M.invW, M.y);

@@ -81,7 +81,6 @@ struct DeviceOperators {
 constexpr int kMuStride = 768;       // floats per box multipole mu[r][k] (r-major, k padded to 128)
 constexpr int kOpM2M = 316, kOpL2L = 324, kNOpImg = 332;  // tensor-core operator images: M2L 0..315, M2M, L2L
 constexpr int kEllStride = 768;      // floats per box local expansion ell[r][k] (r-major, k padded to 128)
-constexpr int kEllKStride = 968;     // floats per leaf local expansion ellk[k][8] (k-major, for the L2P)
 #ifndef XRL_NEAR_SEGLEN
 #define XRL_NEAR_SEGLEN 96
 #endif
@@ -107,6 +106,7 @@ struct xrl_ctx_s {
     cudaStream_t work = nullptr;      // library-owned high-priority stream (FMM chain of xrl_mvm)
     cudaStream_t side = nullptr;      // library-owned low-priority side stream (near SpMV, P2P)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_work = nullptr, ev_m2l = nullptr, ev_p2p = nullptr;
+    cudaEvent_t ev_near = nullptr;    // near-first side stream: the near SpMV is done (the fused P2P adds after it)
     cudaStream_t comm = nullptr;      // library-owned stream of a multi-rank context's NCCL exchanges
     cudaEvent_t ev_halo = nullptr, ev_comm = nullptr, ev_p2l = nullptr;
     bool fuse_p2p = true;             // P2P warps inside the M2L kernel (XRL_FUSE=0: off)
@@ -208,7 +208,6 @@ struct xrl_tree_s {
     xrl::DBuf<float> mu;                     // [nbox][kMuStride]  mu[r][k]
     xrl::DBuf<unsigned> mu_max;              // largest |mu| of the MVM (float bits) for the 3xFP16 M2L scale
     xrl::DBuf<float> ell;                    // [nbox][kEllStride] ell[r][k]
-    xrl::DBuf<float> ellk;                   // [nbox][kEllKStride] ellk[k][8] (leaves, per MVM)
     xrl::DBuf<float> xq;                     // [n][8] packed charges
     xrl::DBuf<float> xq2;                    // [n][8] the second triple's charges (xrl_mvm pairs, lazily)
     xrl::DBuf<float2> xtmp, ytmp, xlib, ylib; // host-API staging

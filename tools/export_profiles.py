@@ -12,7 +12,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src, pre = sys.argv[1], sys.argv[2]
 leaf = sys.argv[3] if len(sys.argv) > 3 else "512"
-KS = ["k_m2l_tc", "k_p2p", "k_near_rg", "k_l2p", "k_p2m", "k_m2p"]
+KS = ["k_m2l_tc", "k_p2p", "k_near_rg", "k_l2p_leaf", "k_p2m", "k_m2p"]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 out = {"capture": f"ncu --set full --clock-control none, config 4 (PoP, 1,907,748 panels), leaf {leaf}, p = 10, "
                   "one launch per kernel of tools/prof_mvm.py (each captured alone)", "kernels": {}}
@@ -48,7 +48,7 @@ for r in rows[1:]:
     agg[k][0] += 1
     agg[k][1] += float(r[vi].replace(",", ""))
 nm = agg["k_pack"][0]
-mvm = [k for k in agg if k in ("k_pack", "k_p2m", "k_m2l_tc", "k_p2l", "k_ell_kmajor", "k_l2p", "k_m2p", "k_p2p",
+mvm = [k for k in agg if k in ("k_pack", "k_p2m", "k_m2l_tc", "k_p2l", "k_l2p_leaf", "k_m2p", "k_p2p",
                                "k_near_rg", "k_gather_rec", "k_scatter_rec")]
 tot = sum(agg[k][1] for k in mvm)
 print("| kernel | launches per MVM | ms per MVM (ncu, serialised, cold) | share |\n|---|---|---|---|")

@@ -15,7 +15,7 @@ timeout 1200 python bench.py > $O/bench.log 2>&1; echo "bench rc=$?" >> $O/statu
 if [ "${NCU:-1}" = "1" ]; then
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/launches.csv python bench.py --steps 3 --warmup 3 --leaf $L --no-cpu-baseline --gmres-iters 0 --no-leaf64 --project 0 > $O/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> $O/status.txt
 # k_m2l_tc also runs the M2M and L2L passes (3 launches per MVM): skip 4 to capture the second MVM's M2L; fusion off (pure M2L)
-for KS in k_m2l_tc:4 k_p2p:1 k_near_rg:1 k_l2p:1 k_m2p:1 k_p2m:1; do
+for KS in k_m2l_tc:4 k_p2p:1 k_near_rg:1 k_l2p_leaf:1 k_m2p:1 k_p2m:1; do
 K=${KS%%:*}; SK=${KS##*:}
 XRL_FUSE=0 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^${K}\$|::${K}\$|${K}\(|${K}<" -s $SK -c 1 -o $O/full_$K python tools/prof_mvm.py 4 3 $L > $O/ncu_$K.log 2>&1; echo "ncu full $K rc=$?" >> $O/status.txt
 done

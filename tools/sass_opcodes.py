@@ -11,7 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2409_12375_b200", "libxrl.so")
-KERNELS = ["k_m2l_tc", "k_p2p", "k_near_rg", "k_p2m", "k_l2p", "k_m2p", "k_p2l"]
+KERNELS = ["k_m2l_tc", "k_p2p", "k_near_rg", "k_p2m", "k_l2p_leaf", "k_m2p", "k_p2l"]
 WATCH = ["UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UBLKCP", "UBLKRED", "UTMALDG", "SYNCS", "FFMA2", "FADD2",
          "FMUL2", "FFMA", "FADD", "FMUL", "MUFU.RSQ", "LDS", "STS", "LDG", "STG", "RED", "ATOMS", "SHFL", "LDGSTS",
          "BAR", "HMMA", "DMMA"]
