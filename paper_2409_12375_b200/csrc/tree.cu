@@ -876,7 +876,11 @@ static xrl_status tree_build_impl(xrl_ctx ctx, int64_t n_vert, const double* ver
     }
     setup_mark("lists");
     if (cost_only) {  // candidate evaluation: the MVM's cost model (P2P pairs, V-list pairs) only
-        *cost_only = (double)T->np2p + 2180.0 * (double)T->nv;
+        static const double wv = [] {  // XRL_COST_V (tuning): P2P pairs per V-list translation
+            const char* e = getenv("XRL_COST_V");
+            return e ? atof(e) : 1500.0;
+        }();
+        *cost_only = (double)T->np2p + wv * (double)T->nv;
         return XRL_OK;
     }
     // ---- partition over ranks: contiguous Morton ranges of
@@ -1290,8 +1294,11 @@ static xrl_status tree_build_checked(xrl_ctx ctx, int64_t n_vert, const double* 
         }
     }
     try {
-        // the root cube's placement is chosen by the MVM's cost model -- P2P pairs + 2180 x V-list pairs
-        // (measured on config 4: 0.50 ns per pair, 1.09 us per tensor-core translation).  Every rank of a
+        // the root cube's placement is chosen by the MVM's cost model -- P2P pairs + 1500 x V-list pairs
+        // (isolated on config 4: 0.49 ns per pair, 1.0 us per 3xFP16 translation, i.e. 2050 pairs; in the step
+        // the M2L hosts 7 fused P2P warps, so a translation costs less than that: tools/cost_sweep.sh, weights
+        // 1000 / 1500 give the same trees as 2180 at leaf 384 / 416, and avoid 2180's P2P-heavy pick at leaf 352:
+        // 5.82 vs 6.79 ms).  Every rank of a
         // partition evaluates the same global candidates, so all ranks pick the same one.
         // XRL_ROOT_ALIGN=corner or centre skips the search.
         static const int forced = [] {
