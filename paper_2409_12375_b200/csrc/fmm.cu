@@ -290,7 +290,8 @@ __device__ void p2p_leaf(int b, int tb, int te, int tid, float* smraw, P2PWin& W
                          const float4* __restrict__ loc, const float* __restrict__ xq, float invW, int accumulate,
                          int64_t n, int64_t p0, float2* __restrict__ y);
 
-// P2P leaf tasks handed to the M2L kernel's three spare warps (leaves[counter++] while the M2L runs; the
+// P2P leaf tasks handed to the M2L kernel's fused P2P warps (3 warps, plus a 4-warp group in the 3xFP16 M2L;
+// tasks[counter++] while the M2L runs; the
 // standalone k_p2p takes the rest from the same counter).  leaves == nullptr: no fused P2P.
 struct P2PTasks {
     const int4* tasks;  // (leaf, first target panel, #targets, -)
