@@ -1039,7 +1039,10 @@ __global__ void __launch_bounds__(XRL_NEAR_NT, NT == 1 ? XRL_NEAR_MINB : 512 / X
 // memory re-based to the target leaf centre (W units), and split over the
 // groups.  Only the target's own leaf needs the r = 0 (self) guard.
 // y += (1/W) sum_{l != k} x_l / r_kl.
-constexpr int kSrcChunk = 1024;
+#ifndef XRL_P2P_CHUNK
+#define XRL_P2P_CHUNK 1024
+#endif
+constexpr int kSrcChunk = XRL_P2P_CHUNK;
 constexpr int kP2PSmem = (kSrcChunk * 12 > 128 * (4 * 6 + 1) * 2 ? kSrcChunk * 12 : 128 * (4 * 6 + 1) * 2) * 4;
 #ifndef XRL_P2P_TPT
 #define XRL_P2P_TPT 8
